@@ -1,0 +1,138 @@
+"""Seeded synthetic RTCUR instances with the BASELINE.json config shapes.
+
+BASELINE names no public dataset; every config is a
+seeded synthetic stand-in.  Host generation is numpy (PCG64) so the CPU oracle
+and the GPU path see byte-identical X; the reference's own generator
+(/root/reference/pkg/src/rtcur/synth.py:74-130, exact-count outliers, c=1) is
+deliberately NOT used because BASELINE specifies Bernoulli(alpha) support with
+c=10.
+
+Layout contract (tensor.py:1-10 of the reference): mode-1-fastest ("F"-order)
+flat buffer.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["BaselineConfig", "CONFIGS", "make_gaussian_tucker", "make_video_like", "make_config",
+           "baseline_sample_sizes"]
+
+
+@dataclass(frozen=True)
+class BaselineConfig:
+    index: int
+    variant: str
+    shape: tuple
+    ranks: tuple
+    alpha: float
+    c: float
+    eps: float
+    dtype: str  # "f64" | "f32"
+    kind: str = "gaussian"  # "gaussian" | "video"
+
+    @property
+    def seed_instance(self) -> int:
+        return 1000 + self.index
+
+    @property
+    def seed_solver(self) -> int:
+        return self.index
+
+
+CONFIGS = {
+    0: BaselineConfig(0, "F", (100, 100, 100), (3, 3, 3), 0.2, 10.0, 1e-5, "f64"),
+    1: BaselineConfig(1, "R", (400, 400, 400), (5, 5, 5), 0.3, 10.0, 1e-5, "f64"),
+    2: BaselineConfig(2, "F", (1200, 1200, 1200), (10, 10, 10), 0.2, 10.0, 1e-5, "f32"),
+    3: BaselineConfig(3, "F", (240, 320, 3, 600), (10, 10, 3, 2), 0.0, 1.0, 1e-4, "f32", "video"),
+    4: BaselineConfig(4, "R", (220, 220, 220, 220), (4, 4, 4, 4), 0.2, 10.0, 1e-5, "f32"),
+}
+
+
+def baseline_sample_sizes(shape, ranks):
+    """BASELINE |I_i| = ceil(3 r ln d) (clamped to d), |J_i| = ceil(3 r^2 ln^2 d).
+
+    Passed through SolverConfig.row_sample_sizes / col_sample_sizes, the
+    reference's own override (solver.py:110-118).
+    """
+    rows = tuple(min(d, max(1, math.ceil(3 * r * math.log(d)))) for d, r in zip(shape, ranks))
+    total = int(np.prod(shape, dtype=np.int64))
+    cols = tuple(min(total // d, math.ceil(3 * r * r * math.log(d) ** 2)) for d, r in zip(shape, ranks))
+    return rows, cols
+
+
+def _tucker(core: np.ndarray, factors) -> np.ndarray:
+    """core x_1 Y_1 ... x_n Y_n on F-ordered arrays, returns F-ordered array."""
+    out = core
+    for k, y in enumerate(factors):
+        shp = out.shape
+        unf = np.reshape(np.moveaxis(out, k, 0), (shp[k], -1), order="F")
+        prod = y @ unf
+        rest = tuple(d for j, d in enumerate(shp) if j != k)
+        out = np.moveaxis(prod.reshape((y.shape[0],) + rest, order="F"), 0, k)
+    return np.asfortranarray(out)
+
+
+def make_gaussian_tucker(shape, ranks, alpha, c, seed, dtype=np.float64):
+    """L* = G x_i Y_i (all iid N(0,1)); S* Bernoulli(alpha) support, values
+    iid U[-c mean|L*|, c mean|L*|]; X = L* + S*.  Returns flat F-order
+    (x, l_star, s_star) in ``dtype`` (fp32 configs round the fp64 draw)."""
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal(int(np.prod(ranks))).reshape(ranks, order="F")
+    ys = [rng.standard_normal((d, r)) for d, r in zip(shape, ranks)]
+    low = _tucker(g, ys).reshape(-1, order="F")
+    mu = float(np.mean(np.abs(low)))
+    mask = rng.random(low.size) < alpha
+    sp = np.zeros(low.size)
+    sp[mask] = rng.uniform(-c * mu, c * mu, size=int(mask.sum()))
+    x = low + sp
+    return x.astype(dtype), low.astype(dtype), sp.astype(dtype)
+
+
+def make_video_like(shape=(240, 320, 3, 600), ranks=(10, 10, 3, 2), n_blocks=40, block=16, seed=1003,
+                    dtype=np.float32):
+    """Config-3 stand-in: H x W x C x T background of multilinear rank
+    (10,10,3,2) = Gaussian core x orthonormalised Gaussian factors, scaled
+    rank-preservingly by 1/max|L| (an affine map to [0,1] would add a constant
+    and raise the rank); foreground = ``n_blocks`` axis-aligned 16x16 blocks
+    moving with constant random velocity (bouncing at the borders), iid
+    U[0,1] values on all colour channels (same support per channel)."""
+    rng = np.random.default_rng(seed)
+    h, w, ch, t = shape
+    g = rng.standard_normal(int(np.prod(ranks))).reshape(ranks, order="F")
+    qs = []
+    for d, r in zip(shape, ranks):
+        q, _ = np.linalg.qr(rng.standard_normal((d, r)))
+        qs.append(q)
+    low = _tucker(g, qs)
+    low /= float(np.max(np.abs(low)))
+    sp = np.zeros(shape, order="F")
+    pos = np.stack([rng.uniform(0, h - block, n_blocks), rng.uniform(0, w - block, n_blocks)], 1)
+    vel = rng.uniform(-3.0, 3.0, (n_blocks, 2))
+    for f in range(t):
+        for b in range(n_blocks):
+            r0, c0 = int(pos[b, 0]), int(pos[b, 1])
+            vals = rng.random((block, block, ch))
+            sp[r0:r0 + block, c0:c0 + block, :, f] = vals
+        pos += vel
+        for ax, lim in ((0, h - block), (1, w - block)):
+            lo = pos[:, ax] < 0
+            hi = pos[:, ax] > lim
+            vel[lo | hi, ax] *= -1.0
+            pos[:, ax] = np.clip(pos[:, ax], 0, lim)
+    x = (low + sp).reshape(-1, order="F")
+    return x.astype(dtype), low.reshape(-1, order="F").astype(dtype), sp.reshape(-1, order="F").astype(dtype)
+
+
+def make_config(index: int):
+    """(x_flat, l_star_flat, s_star_flat, cfg) for BASELINE config ``index``."""
+    cfg = CONFIGS[index]
+    dt = np.float64 if cfg.dtype == "f64" else np.float32
+    if cfg.kind == "video":
+        x, low, sp = make_video_like(cfg.shape, cfg.ranks, seed=cfg.seed_instance, dtype=dt)
+    else:
+        x, low, sp = make_gaussian_tucker(cfg.shape, cfg.ranks, cfg.alpha, cfg.c, cfg.seed_instance, dt)
+    return x, low, sp, cfg
