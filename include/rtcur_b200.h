@@ -1,0 +1,117 @@
+/*
+ * rtcur_b200.h -- C ABI of the B200-native RTCUR hot path (librtcur_b200.so).
+ *
+ * Plain pointers, sizes and a cudaStream_t passed as void*; no torch types.
+ * Every entry returns an int status (RTCUR_OK = 0); rtcur_last_error() gives
+ * the message.  Status -> reference exception mapping used by the Python
+ * layer: RTCUR_E_VALUE -> ValueError, RTCUR_E_INDEX -> IndexError,
+ * RTCUR_E_ARITH -> ArithmeticError, others -> RuntimeError.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/rtcur):
+ *
+ *   rtcur_gather_columns   _backend/_core.pyx:265-288  gather_columns(flat, bases, stride, length)
+ *   rtcur_hard_threshold   _backend/_core.pyx:252-262  hard_threshold(a, zeta)
+ *   rtcur_truncated_svd    linalg.py:59-74 (+ _core.pyx:24-58 dense_svd) truncated_svd(m, r)
+ *   rtcur_engine_*         solver.py:260-389 rtcur() loop body:
+ *       _absmax            solver.py:184-192  DenseTensorAccessor.inf_norm
+ *       _set_sample        fiber_cur.py:148-174 (indices drawn by the host; uploaded here)
+ *       _gather            solver.py:234-239 / 172-182  _gather_blocks (core_block, fiber_block)
+ *       _iterate           solver.py:324-357  HT on the blocks, assemble_fiber_cur
+ *                          (fiber_cur.py:229-274), _eval_blocks (solver.py:242-249),
+ *                          sampled_relative_error sums (solver.py:209-231)
+ *       _export_*          solver.py:378-389 SolveResult pieces (sparse blocks, FiberCur)
+ *   rtcur_full_output      cli.py:237-243 cur_reconstruct_full + hard_threshold(x - L, zeta)
+ *
+ * Layout: tensors are mode-1-fastest ("F" order, tensor.py:1-10).  Index
+ * arrays handed to rtcur_engine_set_sample are the reference's 1-based sorted
+ * sets.  Compact blocks are [core (|I_1| x ... x |I_n|, F-order) | fibers
+ * C_1 (d_1 x |J_1|, column-major) | ... | C_n].
+ */
+#ifndef RTCUR_B200_H
+#define RTCUR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RTCUR_OK 0
+#define RTCUR_E_VALUE 1
+#define RTCUR_E_INDEX 2
+#define RTCUR_E_ARITH 3
+#define RTCUR_E_CUDA 4
+#define RTCUR_E_UNSUPPORTED 5
+
+#define RTCUR_F64 0
+#define RTCUR_F32 1
+
+typedef struct rtcur_engine rtcur_engine;
+
+const char* rtcur_last_error(void);
+const char* rtcur_version(void);
+/* number of kernel launches issued by this library since load */
+unsigned long long rtcur_launch_count(void);
+
+/* ---- kernel-level plug (reference _backend triple), device pointers, stream-ordered ---- */
+
+/* out (length x ncols, column-major fp64) [i, c] = flat[bases[c] + i * stride] */
+int rtcur_gather_columns(const void* flat, int dtype, int64_t flat_len, const int64_t* bases_dev, int64_t ncols,
+                         int64_t stride, int64_t length, double* out, void* stream);
+/* out[i] = |a[i]| > zeta ? a[i] : 0 */
+int rtcur_hard_threshold(const double* a, int64_t n, double zeta, double* out, void* stream);
+/* rank-r truncated SVD of an m x p column-major fp64 matrix (min(m, p) <= 235, r <= 32):
+ * u (m x r, column-major), s (r, non-increasing), v (p x r, column-major).  Synchronous. */
+int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, int r, double* u_dev, double* s_dev,
+                        double* v_dev, void* stream);
+
+/* ---- solver engine ---- */
+
+/* Size the device workspace for a problem (bytes); also returns the byte offset
+ * and element count of the compact x-block buffer inside it (so a caller can
+ * all-reduce it across ranks). */
+int rtcur_engine_plan(int n, const int64_t* dims, const int32_t* ranks, const int64_t* row_sizes,
+                      const int64_t* col_sizes, int dtype, int64_t* workspace_bytes, int64_t* xblocks_offset,
+                      int64_t* xblocks_elems);
+
+/* workspace: device memory of rtcur_engine_plan's size (caller-owned, 256-B aligned).
+ * [slab_lo, slab_hi) is this rank's mode-1 slab of X (0, d_1 on one GPU). */
+int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dims, const int32_t* ranks,
+                        const int64_t* row_sizes, const int64_t* col_sizes, int dtype, void* workspace,
+                        int64_t workspace_bytes, int64_t slab_lo, int64_t slab_hi, void* stream);
+int rtcur_engine_destroy(rtcur_engine* e);
+
+/* X (device): this rank's slab, (slab_hi - slab_lo) x d_2 x ... x d_n, mode-1 fastest */
+int rtcur_engine_bind(rtcur_engine* e, const void* x_dev);
+/* max|X| over the bound slab (K0); synchronous, result on the host */
+int rtcur_engine_absmax(rtcur_engine* e, double* out);
+/* rows[k]: |I_k| sorted 1-based indices, cols[k]: |J_k| sorted 1-based unfolding columns (host) */
+int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols);
+/* gather this rank's owned sampled entries into the compact x blocks (others 0) */
+int rtcur_engine_gather(rtcur_engine* e);
+/* one RTCUR iteration at threshold zeta (already decayed).  first != 0: L = 0.
+ * sums (host, 2*(n+1)): per block sum((x-L-S)^2), sum(x^2) of the NEW iterate;
+ * flags (host, n): rank-deficiency flags of the new intersections. */
+int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, double* sums, int* flags);
+
+/* Export (device outputs, caller-allocated, fp64), for the iterate of the last
+ * rtcur_engine_iterate call:
+ *   s_blocks, clean_blocks: N_blk compact sparse values and X - S (either may be NULL)
+ *   l_blocks: low-rank values of the new iterate on the blocks (NULL to skip) */
+int rtcur_engine_export_blocks(rtcur_engine* e, double* s_blocks, double* clean_blocks, double* l_blocks);
+/* per mode k: U_k (|I_k| x r_k), sigma_k (r_k), V_k (|J_k| x r_k), A_k (d_k x r_k), all row-major fp64
+ * except A_k (column-major); G (prod r, F-order).  Host pointers; synchronous. */
+int rtcur_engine_export_cur(rtcur_engine* e, double* const* U, double* const* sigma, double* const* V,
+                            double* const* A, double* G);
+/* K3 on the bound slab with the current iterate: optional L/S outputs (dtype of X, slab layout),
+ * sums (host, 2): sum((x-L-S)^2), sum(x^2).  Uses a device scratch of prod_{m>=2} d_m * r_1 doubles
+ * supplied by the caller (tf_dev). */
+int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_dev, void* S_dev, double* tf_dev,
+                             double* sums);
+/* bytes of the tf_dev scratch rtcur_engine_full_output needs */
+int64_t rtcur_engine_full_scratch_bytes(rtcur_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

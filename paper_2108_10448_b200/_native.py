@@ -1,0 +1,104 @@
+"""ctypes binding of librtcur_b200.so (include/rtcur_b200.h).
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is visible, every entry point raises.  Status codes map to the
+reference's exception types (solver.py / fiber_cur.py / linalg.py raise
+ValueError, IndexError, ArithmeticError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "librtcur_b200.so")
+
+RTCUR_OK, RTCUR_E_VALUE, RTCUR_E_INDEX, RTCUR_E_ARITH, RTCUR_E_CUDA, RTCUR_E_UNSUPPORTED = range(6)
+RTCUR_F64, RTCUR_F32 = 0, 1
+
+# every symbol include/rtcur_b200.h declares
+EXPORTED = (
+    "rtcur_last_error", "rtcur_version", "rtcur_launch_count", "rtcur_gather_columns", "rtcur_hard_threshold",
+    "rtcur_truncated_svd", "rtcur_engine_plan", "rtcur_engine_create", "rtcur_engine_destroy", "rtcur_engine_bind",
+    "rtcur_engine_absmax", "rtcur_engine_set_sample", "rtcur_engine_gather", "rtcur_engine_iterate",
+    "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
+    "rtcur_engine_full_scratch_bytes",
+)
+
+_lib = None
+
+c_i64 = ctypes.c_int64
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+c_dp = ctypes.POINTER(ctypes.c_double)
+c_vp = ctypes.c_void_p
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load the sm_100a library (no fallback: raises if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeUnavailable(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the B200 path has no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    lib.rtcur_last_error.restype = ctypes.c_char_p
+    lib.rtcur_version.restype = ctypes.c_char_p
+    lib.rtcur_launch_count.restype = ctypes.c_ulonglong
+    lib.rtcur_gather_columns.argtypes = [c_vp, ctypes.c_int, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp]
+    lib.rtcur_hard_threshold.argtypes = [c_vp, c_i64, ctypes.c_double, c_vp, c_vp]
+    lib.rtcur_truncated_svd.argtypes = [c_vp, c_i64, c_i64, ctypes.c_int, c_vp, c_vp, c_vp, c_vp]
+    lib.rtcur_engine_plan.argtypes = [ctypes.c_int, c_i64p, c_i32p, c_i64p, c_i64p, ctypes.c_int, c_i64p, c_i64p,
+                                      c_i64p]
+    lib.rtcur_engine_create.argtypes = [ctypes.POINTER(c_vp), ctypes.c_int, c_i64p, c_i32p, c_i64p, c_i64p,
+                                        ctypes.c_int, c_vp, c_i64, c_i64, c_i64, c_vp]
+    lib.rtcur_engine_destroy.argtypes = [c_vp]
+    lib.rtcur_engine_bind.argtypes = [c_vp, c_vp]
+    lib.rtcur_engine_absmax.argtypes = [c_vp, c_dp]
+    lib.rtcur_engine_set_sample.argtypes = [c_vp, ctypes.POINTER(c_i64p), ctypes.POINTER(c_i64p)]
+    lib.rtcur_engine_gather.argtypes = [c_vp]
+    lib.rtcur_engine_iterate.argtypes = [c_vp, ctypes.c_double, ctypes.c_int, c_dp, c_i32p]
+    lib.rtcur_engine_export_blocks.argtypes = [c_vp, c_vp, c_vp, c_vp]
+    lib.rtcur_engine_export_cur.argtypes = [c_vp, ctypes.POINTER(c_dp), ctypes.POINTER(c_dp), ctypes.POINTER(c_dp),
+                                            ctypes.POINTER(c_dp), c_dp]
+    lib.rtcur_engine_full_output.argtypes = [c_vp, ctypes.c_double, c_vp, c_vp, c_vp, c_dp]
+    lib.rtcur_engine_full_scratch_bytes.argtypes = [c_vp]
+    lib.rtcur_engine_full_scratch_bytes.restype = c_i64
+    for name in EXPORTED:
+        if not hasattr(lib, name):
+            raise NativeUnavailable(f"{path} does not export {name}")
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status == RTCUR_OK:
+        return
+    msg = (_lib.rtcur_last_error() or b"").decode()
+    if status == RTCUR_E_VALUE:
+        raise ValueError(msg)
+    if status == RTCUR_E_INDEX:
+        raise IndexError(msg)
+    if status == RTCUR_E_ARITH:
+        raise ArithmeticError(msg)
+    raise RuntimeError(f"rtcur_b200 status {status}: {msg}")
+
+
+def launch_count() -> int:
+    return int(load().rtcur_launch_count())
+
+
+def i64_array(values):
+    arr = (ctypes.c_int64 * len(values))(*[int(v) for v in values])
+    return arr
+
+
+def i32_array(values):
+    return (ctypes.c_int32 * len(values))(*[int(v) for v in values])

@@ -1,0 +1,918 @@
+// engine.cu -- C-ABI entry points (include/rtcur_b200.h) and the per-iteration
+// launch schedule of the B200 RTCUR hot path.  One translation unit: the
+// kernel files are included so their parameter structs are shared.
+//
+// Iteration k (reference solver.py:314-375) on the compact sampled blocks:
+//   1. k_block_pass  S = HT(X - L_{k-1}, zeta_k), clean intersections -> M_i
+//   2. k_gram_*      K_i = B_i B_i^T  (short side of each intersection)
+//   3. k_eig         top-r_i eigenbasis of K_i
+//   4. k_zproj .. k_complete   rank-r_i truncated SVD (U, sigma, V), pinv cutoff
+//   5. k_apass/k_areduce       A_i = C_i V_i S_i^+
+//   6. k_gpass/k_modeprod      G = core x_i U_i^T
+//   7. k_wcols                 W_b per block column (Tucker evaluation weights)
+//   8. k_block_pass  e-sums of X - L_k - S_k and X sums (sampled error)
+// States (G, A, W) live in a 3-slot ring so the previous iterate stays
+// available for the threshold recomputation and the export.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <atomic>
+#include <algorithm>
+
+#include "k_block.cu"
+#include "k_gram.cu"
+#include "k_eig.cu"
+#include "k_svdpost.cu"
+#include "k_factors.cu"
+#include "k_full.cu"
+#include "../../include/rtcur_b200.h"
+
+static std::atomic<unsigned long long> g_launches{0};
+extern "C" unsigned long long rtcur_launch_counter_add(unsigned long long k) { return g_launches.fetch_add(k) + k; }
+extern "C" unsigned long long rtcur_launch_count(void) { return g_launches.load(); }
+
+static thread_local std::string g_err;
+extern "C" const char* rtcur_last_error(void) { return g_err.c_str(); }
+extern "C" const char* rtcur_version(void) { return "rtcur_b200 0.1 sm_100a"; }
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess) return fail(RT_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define LAUNCH_CHECK()                                                                 \
+  do {                                                                                 \
+    RT_COUNT_LAUNCH();                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(_e) + " @" + std::to_string(__LINE__)); \
+  } while (0)
+
+static inline i64 cdiv(i64 a, i64 b) { return (a + b - 1) / b; }
+static inline i64 align256(i64 x) { return (x + 255) & ~(i64)255; }
+
+static int rbucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32; }
+
+#define DISPATCH_R(RB, KERNEL, GRID, BLOCK, SMEM, STREAM, ...)                     \
+  do {                                                                               \
+    switch (RB) {                                                                    \
+      case 4: KERNEL<4><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__); break;           \
+      case 8: KERNEL<8><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__); break;           \
+      case 16: KERNEL<16><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__); break;         \
+      default: KERNEL<32><<<GRID, BLOCK, SMEM, STREAM>>>(__VA_ARGS__); break;         \
+    }                                                                                \
+  } while (0)
+
+struct Plan {
+  Geom g;
+  TileMap tm;
+  int dtype;
+  int esize;
+  int rmax, rb;
+  i64 s[RT_MAX_MODES], l[RT_MAX_MODES];
+  int tall[RT_MAX_MODES];
+  int nb[RT_MAX_MODES];
+  i64 col_off[RT_MAX_BLOCKS + 1];
+  int gram_maxchunks, gram_maxpairs;
+  int a_chunk, a_maxchunks;
+  i64 dmax, lmax, smax, qmax;
+  i64 g_tmp;         // doubles per G temp buffer
+  int hchunk, h_maxchunks;
+  // workspace offsets (bytes)
+  i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
+  i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES],
+      o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
+      o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
+      o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_apart, o_gt0, o_gt1, o_bpart, o_sums,
+      o_fpart;
+  i64 total;
+};
+
+static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, const int64_t* row_sizes,
+                     const int64_t* col_sizes, int dtype) {
+  memset(&P, 0, sizeof(P));
+  if (n < 1 || n > RT_MAX_MODES) return fail(RT_ERR_UNSUPPORTED, "number of modes must be in [1, 8]");
+  if (dtype != 0 && dtype != 1) return fail(RT_ERR_VALUE, "dtype must be RTCUR_F64 or RTCUR_F32");
+  Geom& g = P.g;
+  g.n = n;
+  g.nblk = n + 1;
+  P.dtype = dtype;
+  P.esize = dtype == 0 ? 8 : 4;
+  i64 total = 1;
+  for (int m = 0; m < n; ++m) {
+    if (dims[m] < 1) return fail(RT_ERR_VALUE, "nonpositive extent");
+    g.dim[m] = dims[m];
+    g.stride[m] = total;
+    total *= dims[m];
+  }
+  i64 rs = 0;
+  for (int m = 0; m < n; ++m) {
+    g.rstride[m] = (m == 0) ? 0 : (m == 1 ? 1 : rs);
+    if (m >= 1) rs = (m == 1 ? dims[1] : rs * dims[m]);
+  }
+  g.gsize = 1;
+  P.rmax = 1;
+  for (int m = 0; m < n; ++m) {
+    const i64 rest = total / dims[m];
+    if (ranks[m] < 1 || ranks[m] > dims[m]) return fail(RT_ERR_VALUE, "rank outside [1, d_k]");
+    if (row_sizes[m] < 1 || row_sizes[m] > dims[m]) return fail(RT_ERR_VALUE, "row sample size outside [1, d_k]");
+    if (col_sizes[m] < 1 || col_sizes[m] > rest) return fail(RT_ERR_VALUE, "column sample size outside range");
+    if (ranks[m] > row_sizes[m] || ranks[m] > col_sizes[m])
+      return fail(RT_ERR_VALUE, "mode " + std::to_string(m + 1) + ": rank exceeds sample sizes");
+    if (ranks[m] > RT_MAX_RANK) return fail(RT_ERR_UNSUPPORTED, "rank > 32 not supported");
+    g.rank[m] = ranks[m];
+    g.nrows[m] = row_sizes[m];
+    g.ncols[m] = col_sizes[m];
+    g.gstride[m] = g.gsize;
+    g.gsize *= ranks[m];
+    P.rmax = std::max(P.rmax, (int)ranks[m]);
+    P.s[m] = std::min(row_sizes[m], col_sizes[m]);
+    P.l[m] = std::max(row_sizes[m], col_sizes[m]);
+    P.tall[m] = row_sizes[m] > col_sizes[m];
+    if (P.s[m] > 235) return fail(RT_ERR_UNSUPPORTED, "intersection short side > 235 not supported");
+  }
+  if (g.gsize > 8192) return fail(RT_ERR_UNSUPPORTED, "prod(ranks) > 8192 not supported");
+  P.rb = rbucket(P.rmax);
+  // blocks
+  i64 off = 0;
+  {
+    BlockDesc& b = g.blk[0];
+    b.P = row_sizes[0];
+    b.Q = 1;
+    for (int m = 1; m < n; ++m) b.Q *= row_sizes[m];
+    b.off = off;
+    b.mode = 0;
+    b.is_core = 1;
+    b.r = ranks[0];
+    off += b.P * b.Q;
+  }
+  for (int k = 0; k < n; ++k) {
+    BlockDesc& b = g.blk[k + 1];
+    b.P = dims[k];
+    b.Q = col_sizes[k];
+    b.off = off;
+    b.mode = k;
+    b.is_core = 0;
+    b.r = ranks[k];
+    off += b.P * b.Q;
+  }
+  g.nblk_total = off;
+  // state layout: G | A_0..A_{n-1} | W_0..W_n
+  i64 so = align256(g.gsize * 8) / 8;
+  for (int m = 0; m < n; ++m) {
+    g.a_off[m] = so;
+    so += align256(dims[m] * ranks[m] * 8) / 8;
+  }
+  for (int b = 0; b < g.nblk; ++b) {
+    g.blk[b].w_off = so;
+    so += align256(g.blk[b].Q * g.blk[b].r * 8) / 8;
+  }
+  g.state_doubles = so;
+  // tiles
+  TileMap& tm = P.tm;
+  tm.nblk = g.nblk;
+  tm.tile = 4096;
+  i64 t = 0;
+  for (int b = 0; b < g.nblk; ++b) {
+    tm.first[b] = t;
+    t += cdiv(g.blk[b].P * g.blk[b].Q, tm.tile);
+  }
+  tm.first[g.nblk] = t;
+  P.col_off[0] = 0;
+  for (int b = 0; b < g.nblk; ++b) P.col_off[b + 1] = P.col_off[b] + g.blk[b].Q;
+  // gram / svd sizing
+  P.gram_maxchunks = 1;
+  P.gram_maxpairs = 1;
+  P.dmax = 1;
+  P.lmax = 1;
+  P.smax = 1;
+  P.qmax = 1;
+  for (int m = 0; m < n; ++m) {
+    const int nt = (int)cdiv(P.s[m], GRAM_T);
+    P.gram_maxpairs = std::max(P.gram_maxpairs, nt * (nt + 1) / 2);
+    P.gram_maxchunks = std::max(P.gram_maxchunks, (int)cdiv(P.l[m], GRAM_CL));
+    P.dmax = std::max(P.dmax, (i64)dims[m]);
+    P.lmax = std::max(P.lmax, P.l[m]);
+    P.smax = std::max(P.smax, P.s[m]);
+    // inverse-iteration batch: vectors whose LU fits next to the packed matrix
+    const i64 npk = P.s[m] * (P.s[m] + 1) / 2;
+    int nb = (int)std::max<i64>(1, std::min<i64>(ranks[m], std::max<i64>(npk, 5 * P.s[m] * 4) / (5 * P.s[m])));
+    P.nb[m] = nb;
+  }
+  for (int b = 0; b < g.nblk; ++b) P.qmax = std::max(P.qmax, g.blk[b].Q);
+  P.a_chunk = 128;
+  P.a_maxchunks = 1;
+  for (int m = 0; m < n; ++m) P.a_maxchunks = std::max(P.a_maxchunks, (int)cdiv(col_sizes[m], P.a_chunk));
+  P.hchunk = 256;
+  P.h_maxchunks = (int)cdiv(P.lmax, P.hchunk);
+  // G temporaries: largest partially contracted core
+  {
+    i64 mx = 1, cur = ranks[0];
+    for (int m = 1; m < n; ++m) cur *= row_sizes[m];
+    mx = cur;
+    for (int m = 1; m < n; ++m) {
+      cur = cur / row_sizes[m] * ranks[m];
+      mx = std::max(mx, cur);
+    }
+    P.g_tmp = std::max<i64>(mx, g.gsize);
+  }
+  // workspace carve
+  i64 o = 0;
+  auto take = [&](i64 bytes) { i64 r = o; o += align256(std::max<i64>(bytes, 8)); return r; };
+  for (int m = 0; m < n; ++m) P.o_rows[m] = take(row_sizes[m] * 4);
+  for (int m = 0; m < n; ++m) P.o_cols[m] = take(col_sizes[m] * 8);
+  {
+    i64 sd = 0;
+    for (int m = 0; m < n; ++m) sd += dims[m];
+    P.o_rowpos = take(sd * 4);
+  }
+  P.o_colR = take(P.col_off[g.nblk] * 8);
+  P.o_coli1 = take(P.col_off[g.nblk] * 4);
+  P.o_coloff = take((RT_MAX_BLOCKS + 1) * 8);
+  P.o_xb = take(g.nblk_total * P.esize);
+  P.o_state = take(3 * g.state_doubles * 8);
+  for (int m = 0; m < n; ++m) P.o_M[m] = take(row_sizes[m] * col_sizes[m] * 8);
+  P.o_gpart = take((i64)n * P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
+  for (int m = 0; m < n; ++m) {
+    const i64 s = P.s[m];
+    P.o_K[m] = take(s * (s + 1) / 2 * 8);
+    P.o_hv[m] = take((s * (s - 1) / 2 + s) * 8);
+    P.o_E[m] = take(s * ranks[m] * 8);
+    P.o_lam[m] = take(ranks[m] * 8);
+    P.o_Z[m] = take(P.l[m] * ranks[m] * 8);
+    P.o_hpart[m] = take((i64)cdiv(P.l[m], P.hchunk) * ranks[m] * (ranks[m] + 1) / 2 * 8);
+    P.o_H[m] = take(ranks[m] * ranks[m] * 8);
+    P.o_Q[m] = take(ranks[m] * ranks[m] * 8);
+    P.o_U[m] = take(row_sizes[m] * ranks[m] * 8);
+    P.o_V[m] = take(col_sizes[m] * ranks[m] * 8);
+    P.o_sig[m] = take(ranks[m] * 8);
+    P.o_siginv[m] = take(ranks[m] * 8);
+    P.o_perm[m] = take(ranks[m] * 4);
+    P.o_degen[m] = take((ranks[m] + 1) * 4);
+  }
+  P.o_flags = take(n * 4);
+  P.o_nonfinite = take(4);
+  P.o_counters = take(64 * 4);
+  P.o_absmax = take(8);
+  P.o_apart = take((i64)n * P.a_maxchunks * P.dmax * RT_MAX_RANK * 8);
+  P.o_gt0 = take(P.g_tmp * 8);
+  P.o_gt1 = take(P.g_tmp * 8);
+  P.o_bpart = take(tm.first[g.nblk] * 2 * 8);
+  P.o_sums = take(2 * g.nblk * 8);
+  P.o_fpart = take(148 * 8 * 2 * 8);
+  P.total = o;
+  return RT_OK;
+}
+
+struct rtcur_engine {
+  Plan P;
+  char* ws;
+  cudaStream_t st;
+  i64 lo, hi;
+  const void* X;
+  int cur;          // ring slot of the latest iterate (-1: none)
+  int prev;         // ring slot of the one before (-1: none, i.e. latest is iteration 1)
+  double zeta_last;
+  bool sampled;
+  double* h_pinned;  // host staging: sums, flags
+  int* h_flags;
+  i64* h_idx;        // pinned staging for index upload
+  i64 h_idx_len;
+  template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
+  double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
+};
+
+static IndexPtrs make_ip(const rtcur_engine* e) {
+  const Plan& P = e->P;
+  IndexPtrs ip;
+  memset(&ip, 0, sizeof(ip));
+  i64 roff = 0;
+  for (int m = 0; m < P.g.n; ++m) {
+    ip.rows[m] = e->at<int>(P.o_rows[m]);
+    ip.cols[m] = e->at<i64>(P.o_cols[m]);
+    ip.rowpos[m] = e->at<int>(P.o_rowpos) + roff;
+    roff += P.g.dim[m];
+  }
+  for (int b = 0; b < P.g.nblk; ++b) {
+    ip.colR[b] = e->at<i64>(P.o_colR) + P.col_off[b];
+    ip.coli1[b] = e->at<int>(P.o_coli1) + P.col_off[b];
+  }
+  return ip;
+}
+
+static int eig_smem_bytes(const Plan& P, int m) {
+  const i64 s = P.s[m];
+  const i64 region0 = std::max<i64>(s * (s + 1) / 2, 5 * s * P.nb[m]);
+  return (int)((region0 + 5 * s + 32) * 8);
+}
+
+extern "C" int rtcur_engine_plan(int n, const int64_t* dims, const int32_t* ranks, const int64_t* row_sizes,
+                                 const int64_t* col_sizes, int dtype, int64_t* workspace_bytes,
+                                 int64_t* xblocks_offset, int64_t* xblocks_elems) {
+  Plan* P = new Plan;
+  int st = make_plan(*P, n, dims, ranks, row_sizes, col_sizes, dtype);
+  if (st == RT_OK) {
+    if (workspace_bytes) *workspace_bytes = P->total;
+    if (xblocks_offset) *xblocks_offset = P->o_xb;
+    if (xblocks_elems) *xblocks_elems = P->g.nblk_total;
+  }
+  delete P;
+  return st;
+}
+
+extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dims, const int32_t* ranks,
+                                   const int64_t* row_sizes, const int64_t* col_sizes, int dtype, void* workspace,
+                                   int64_t workspace_bytes, int64_t slab_lo, int64_t slab_hi, void* stream) {
+  rtcur_engine* e = new rtcur_engine;
+  memset((void*)e, 0, sizeof(*e));
+  int st = make_plan(e->P, n, dims, ranks, row_sizes, col_sizes, dtype);
+  if (st != RT_OK) { delete e; return st; }
+  if (workspace_bytes < e->P.total || workspace == nullptr) { delete e; return fail(RT_ERR_VALUE, "workspace too small"); }
+  if (((uintptr_t)workspace & 255) != 0) { delete e; return fail(RT_ERR_VALUE, "workspace must be 256-byte aligned"); }
+  if (slab_lo < 0 || slab_hi > dims[0] || slab_lo >= slab_hi) { delete e; return fail(RT_ERR_VALUE, "bad mode-1 slab"); }
+  e->ws = (char*)workspace;
+  e->st = (cudaStream_t)stream;
+  e->lo = slab_lo;
+  e->hi = slab_hi;
+  e->cur = e->prev = -1;
+  cudaError_t ce = cudaMallocHost(&e->h_pinned, 4096);
+  if (ce != cudaSuccess) { delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
+  e->h_flags = reinterpret_cast<int*>(e->h_pinned + 256);
+  i64 idx_len = 0;
+  for (int m = 0; m < n; ++m) idx_len += row_sizes[m] + col_sizes[m];
+  e->h_idx_len = idx_len;
+  ce = cudaMallocHost(&e->h_idx, idx_len * 8 + 64);
+  if (ce != cudaSuccess) { cudaFreeHost(e->h_pinned); delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
+  // counters + col offsets
+  CK(cudaMemsetAsync(e->ws + e->P.o_counters, 0, 64 * 4, e->st));
+  CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  // opt-in shared memory sizes
+  int maxe = 0;
+  for (int m = 0; m < n; ++m) maxe = std::max(maxe, eig_smem_bytes(e->P, m));
+  CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(maxe, 48 * 1024)));
+  const int gs = (int)(e->P.g.gsize * 8);
+  CK(cudaFuncSetAttribute(k_wcols<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_wcols<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_wcols<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_wcols<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
+  const int zs = (int)(e->P.smax * e->P.rmax * 8);
+  CK(cudaFuncSetAttribute(k_zproj<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_zproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_zproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_zproj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  *out = e;
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
+  if (!e) return RT_OK;
+  cudaStreamSynchronize(e->st);
+  if (e->h_pinned) cudaFreeHost(e->h_pinned);
+  if (e->h_idx) cudaFreeHost(e->h_idx);
+  delete e;
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_bind(rtcur_engine* e, const void* x_dev) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  e->X = x_dev;   // NULL unbinds (K3 then reconstructs L only)
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_absmax(rtcur_engine* e, double* out) {
+  if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
+  const Plan& P = e->P;
+  i64 nloc = e->hi - e->lo;
+  for (int m = 1; m < P.g.n; ++m) nloc *= P.g.dim[m];
+  unsigned long long* d = e->at<unsigned long long>(P.o_absmax);
+  CK(cudaMemsetAsync(d, 0, 8, e->st));
+  int nsm = 148;
+  const int grid = nsm * 8;
+  if (P.dtype == 0) k_absmax<double><<<grid, 256, 0, e->st>>>((const double*)e->X, nloc, d);
+  else k_absmax<float><<<grid, 256, 0, e->st>>>((const float*)e->X, nloc, d);
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(e->h_pinned, d, 8, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  unsigned long long bits;
+  memcpy(&bits, e->h_pinned, 8);
+  double v;
+  memcpy(&v, &bits, 8);
+  *out = v;
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  const Plan& P = e->P;
+  const Geom& g = P.g;
+  const i64 total = [&] { i64 t = 1; for (int m = 0; m < g.n; ++m) t *= g.dim[m]; return t; }();
+  // validate (fiber_cur.py:67-83) and stage 0-based copies in pinned memory
+  CK(cudaStreamSynchronize(e->st));   // staging buffer reuse
+  i64 o = 0;
+  std::vector<i64> offs(2 * g.n);
+  for (int m = 0; m < g.n; ++m) {
+    offs[m] = o;
+    int* dst = reinterpret_cast<int*>(e->h_idx + o);
+    for (i64 i = 0; i < g.nrows[m]; ++i) {
+      const int64_t v = rows[m][i];
+      if (v < 1 || v > g.dim[m]) return fail(RT_ERR_INDEX, "mode " + std::to_string(m + 1) + ": row index outside [1, d]");
+      if (i > 0 && v <= rows[m][i - 1]) return fail(RT_ERR_VALUE, "row sets must be sorted and unique");
+      dst[i] = (int)(v - 1);
+    }
+    o += cdiv(g.nrows[m], 2);
+  }
+  for (int m = 0; m < g.n; ++m) {
+    offs[g.n + m] = o;
+    const i64 rest = total / g.dim[m];
+    for (i64 i = 0; i < g.ncols[m]; ++i) {
+      const int64_t v = cols[m][i];
+      if (v < 1 || v > rest) return fail(RT_ERR_INDEX, "mode " + std::to_string(m + 1) + ": fiber column outside range");
+      if (i > 0 && v <= cols[m][i - 1]) return fail(RT_ERR_VALUE, "column sets must be sorted and unique");
+      e->h_idx[o + i] = v - 1;
+    }
+    o += g.ncols[m];
+  }
+  for (int m = 0; m < g.n; ++m) {
+    CK(cudaMemcpyAsync(e->ws + P.o_rows[m], e->h_idx + offs[m], g.nrows[m] * 4, cudaMemcpyHostToDevice, e->st));
+    CK(cudaMemcpyAsync(e->ws + P.o_cols[m], e->h_idx + offs[g.n + m], g.ncols[m] * 8, cudaMemcpyHostToDevice, e->st));
+  }
+  IndexPtrs ip = make_ip(e);
+  dim3 gr((unsigned)std::min<i64>(cdiv(P.dmax, 256), 1024), g.n);
+  k_rowpos<<<gr, 256, 0, e->st>>>(g, ip, e->at<int>(P.o_rowpos));
+  LAUNCH_CHECK();
+  dim3 gc((unsigned)std::min<i64>(cdiv(P.qmax, 256), 4096), g.nblk);
+  k_colprep<<<gc, 256, 0, e->st>>>(g, ip, e->at<i64>(P.o_colR), e->at<int>(P.o_coli1), e->at<i64>(P.o_coloff));
+  LAUNCH_CHECK();
+  e->sampled = true;
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_gather(rtcur_engine* e) {
+  if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
+  if (!e->sampled) return fail(RT_ERR_VALUE, "no sample set");
+  const Plan& P = e->P;
+  IndexPtrs ip = make_ip(e);
+  k_gather<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, e->X, P.dtype, e->lo, e->hi,
+                                                              e->ws + P.o_xb);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
+static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_e, double zeta, bool with_M,
+                          double* s_out, double* c_out, double* l_out, bool sums) {
+  const Plan& P = e->P;
+  IndexPtrs ip = make_ip(e);
+  PassArgs a;
+  memset(&a, 0, sizeof(a));
+  a.xb = e->ws + P.o_xb;
+  a.dtype = P.dtype;
+  a.st_s = st_s;
+  a.st_e = st_e;
+  a.zeta = zeta;
+  if (with_M)
+    for (int m = 0; m < P.g.n; ++m) a.M[m] = e->at<double>(P.o_M[m]);
+  a.s_out = s_out;
+  a.c_out = c_out;
+  a.l_out = l_out;
+  if (sums) {
+    a.partial = e->at<double>(P.o_bpart);
+    a.sums = e->at<double>(P.o_sums);
+    a.counter = e->at<unsigned int>(P.o_counters);
+  }
+  a.nonfinite = e->at<int>(P.o_nonfinite);
+  k_block_pass<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, a);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
+static SvdArgs make_svd_args(rtcur_engine* e) {
+  const Plan& P = e->P;
+  SvdArgs sa;
+  memset(&sa, 0, sizeof(sa));
+  sa.n = P.g.n;
+  for (int m = 0; m < P.g.n; ++m) {
+    sa.s[m] = (int)P.s[m];
+    sa.l[m] = P.l[m];
+    sa.r[m] = P.g.rank[m];
+    sa.tall[m] = P.tall[m];
+    sa.mrows[m] = P.g.nrows[m];
+    sa.pcols[m] = P.g.ncols[m];
+    sa.M[m] = e->at<double>(P.o_M[m]);
+    sa.E[m] = e->at<double>(P.o_E[m]);
+    sa.Z[m] = e->at<double>(P.o_Z[m]);
+    sa.hpart[m] = e->at<double>(P.o_hpart[m]);
+    sa.H[m] = e->at<double>(P.o_H[m]);
+    sa.Q[m] = e->at<double>(P.o_Q[m]);
+    sa.U[m] = e->at<double>(P.o_U[m]);
+    sa.V[m] = e->at<double>(P.o_V[m]);
+    sa.sig[m] = e->at<double>(P.o_sig[m]);
+    sa.siginv[m] = e->at<double>(P.o_siginv[m]);
+    sa.perm[m] = e->at<int>(P.o_perm[m]);
+    sa.degen[m] = e->at<int>(P.o_degen[m]);
+  }
+  sa.flags = e->at<int>(P.o_flags);
+  sa.hchunk = P.hchunk;
+  return sa;
+}
+
+// rank-r truncated SVD of every mode's intersection M_k (already in the workspace)
+static int run_svd(rtcur_engine* e) {
+  const Plan& P = e->P;
+  const int n = P.g.n;
+  GramArgs ga;
+  memset(&ga, 0, sizeof(ga));
+  ga.n = n;
+  for (int m = 0; m < n; ++m) {
+    ga.s[m] = (int)P.s[m];
+    ga.l[m] = P.l[m];
+    ga.tall[m] = P.tall[m];
+    ga.mrows[m] = P.g.nrows[m];
+    ga.M[m] = e->at<double>(P.o_M[m]);
+    ga.K[m] = e->at<double>(P.o_K[m]);
+  }
+  ga.part = e->at<double>(P.o_gpart);
+  ga.maxchunks = P.gram_maxchunks;
+  ga.maxpairs = P.gram_maxpairs;
+  k_gram_tiles<<<dim3(P.gram_maxpairs, P.gram_maxchunks, n), 256, 0, e->st>>>(ga);
+  LAUNCH_CHECK();
+  {
+    const i64 npk = P.smax * (P.smax + 1) / 2;
+    k_gram_reduce<<<dim3((unsigned)std::min<i64>(cdiv(npk, 256), 512), n), 256, 0, e->st>>>(ga);
+    LAUNCH_CHECK();
+  }
+  EigArgs ea;
+  memset(&ea, 0, sizeof(ea));
+  ea.n = n;
+  int esm = 0;
+  for (int m = 0; m < n; ++m) {
+    ea.s[m] = (int)P.s[m];
+    ea.r[m] = P.g.rank[m];
+    ea.K[m] = e->at<double>(P.o_K[m]);
+    ea.hv[m] = e->at<double>(P.o_hv[m]);
+    ea.E[m] = e->at<double>(P.o_E[m]);
+    ea.lam[m] = e->at<double>(P.o_lam[m]);
+    ea.nb[m] = P.nb[m];
+    esm = std::max(esm, eig_smem_bytes(P, m));
+  }
+  k_eig<<<n, 1024, esm, e->st>>>(ea);
+  LAUNCH_CHECK();
+  SvdArgs sa = make_svd_args(e);
+  unsigned int* hcnt = e->at<unsigned int>(P.o_counters) + 16;
+  const unsigned gz = (unsigned)cdiv(P.lmax, 256);
+  const int zsm = (int)(P.smax * P.rmax * 8);
+  DISPATCH_R(P.rb, k_zproj, dim3(gz, n), 256, zsm, e->st, sa);
+  LAUNCH_CHECK();
+  k_hgram<<<dim3(P.h_maxchunks, n), 576, 0, e->st>>>(sa, hcnt);
+  LAUNCH_CHECK();
+  k_svd_fin1<<<n, 32, 0, e->st>>>(sa);
+  LAUNCH_CHECK();
+  k_short_vecs<<<dim3((unsigned)cdiv(P.smax * P.rmax, 256), n), 256, 0, e->st>>>(sa);
+  LAUNCH_CHECK();
+  DISPATCH_R(P.rb, k_zrot, dim3(gz, n), 256, 0, e->st, sa);
+  LAUNCH_CHECK();
+  k_hgram<<<dim3(P.h_maxchunks, n), 576, 0, e->st>>>(sa, hcnt);
+  LAUNCH_CHECK();
+  k_svd_fin2<<<n, 32, 0, e->st>>>(sa);
+  LAUNCH_CHECK();
+  DISPATCH_R(P.rb, k_long, dim3(gz, n), 256, 0, e->st, sa);
+  LAUNCH_CHECK();
+  k_complete<<<n, 256, 0, e->st>>>(sa);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
+// A_k, G, W of the new iterate into state slot `dst` (threshold from st_s)
+static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst) {
+  const Plan& P = e->P;
+  const Geom& g = P.g;
+  const int n = g.n;
+  IndexPtrs ip = make_ip(e);
+  double* sto = e->state(dst);
+  APassArgs aa;
+  memset(&aa, 0, sizeof(aa));
+  aa.xb = e->ws + P.o_xb;
+  aa.dtype = P.dtype;
+  aa.st_s = st_s;
+  aa.zeta = zeta;
+  for (int m = 0; m < n; ++m) {
+    aa.V[m] = e->at<double>(P.o_V[m]);
+    aa.siginv[m] = e->at<double>(P.o_siginv[m]);
+  }
+  aa.part = e->at<double>(P.o_apart);
+  aa.chunk = P.a_chunk;
+  aa.maxchunks = P.a_maxchunks;
+  aa.dmax = P.dmax;
+  aa.st_out = sto;
+  DISPATCH_R(P.rb, k_apass, dim3((unsigned)cdiv(P.dmax, 256), P.a_maxchunks, n), 256, 0, e->st, g, ip, aa);
+  LAUNCH_CHECK();
+  k_areduce<<<dim3((unsigned)std::min<i64>(cdiv(P.dmax * P.rmax, 256), 1024), n), 256, 0, e->st>>>(g, aa);
+  LAUNCH_CHECK();
+  // G = clean_core x_1 U_1^T x_2 ... x_n U_n^T
+  GPassArgs gp;
+  memset(&gp, 0, sizeof(gp));
+  gp.xb = e->ws + P.o_xb;
+  gp.dtype = P.dtype;
+  gp.st_s = st_s;
+  gp.zeta = zeta;
+  for (int m = 0; m < n; ++m) gp.U[m] = e->at<double>(P.o_U[m]);
+  double* t0 = e->at<double>(P.o_gt0);
+  double* t1 = e->at<double>(P.o_gt1);
+  gp.t1 = (n == 1) ? sto : t0;
+  {
+    const i64 Q = g.blk[0].Q;
+    DISPATCH_R(rbucket(g.rank[0]), k_gpass, (unsigned)cdiv(Q * 32, 256), 256, 0, e->st, g, ip, gp);
+    LAUNCH_CHECK();
+  }
+  {
+    i64 rho = g.rank[0];
+    const double* in = t0;
+    for (int m = 1; m < n; ++m) {
+      i64 beta = 1;
+      for (int l = m + 1; l < n; ++l) beta *= g.nrows[l];
+      double* out = (m == n - 1) ? sto : (in == t0 ? t1 : t0);
+      const i64 total = rho * g.rank[m] * beta;
+      k_modeprod<<<(unsigned)std::min<i64>(cdiv(total, 256), 2048), 256, 0, e->st>>>(
+          in, out, e->at<double>(P.o_U[m]), rho, (int)g.nrows[m], g.rank[m], beta);
+      LAUNCH_CHECK();
+      rho *= g.rank[m];
+      in = out;
+    }
+  }
+  // W for every block column
+  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(P.qmax, 128), g.nblk), 128, (int)(g.gsize * 8), e->st, g, ip, sto, 0,
+             (double*)nullptr);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, double* sums, int* flags) {
+  if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
+  if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
+  const Plan& P = e->P;
+  const int n = P.g.n;
+  if (first) e->cur = e->prev = -1;
+  const double* st_s = (e->cur >= 0) ? e->state(e->cur) : nullptr;
+  int newslot = 0;
+  while (newslot == e->cur || newslot == e->prev) ++newslot;
+  CK(cudaMemsetAsync(e->ws + P.o_nonfinite, 0, 4, e->st));
+  int st;
+  if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false))) return st;
+  if ((st = run_svd(e))) return st;
+  if ((st = run_factors(e, st_s, zeta, newslot))) return st;
+  if ((st = run_block_pass(e, st_s, e->state(newslot), zeta, false, nullptr, nullptr, nullptr, true))) return st;
+  CK(cudaMemcpyAsync(e->h_pinned, e->ws + P.o_sums, 2 * P.g.nblk * 8, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaMemcpyAsync(e->h_flags, e->ws + P.o_flags, n * 4, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaMemcpyAsync(e->h_flags + 16, e->ws + P.o_nonfinite, 4, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  if (e->h_flags[16]) return fail(RT_ERR_VALUE, "truncated_svd input contains non-finite entries");
+  if (sums) memcpy(sums, e->h_pinned, 2 * P.g.nblk * 8);
+  if (flags) memcpy(flags, e->h_flags, n * 4);
+  e->prev = e->cur;
+  e->cur = newslot;
+  e->zeta_last = zeta;
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_export_blocks(rtcur_engine* e, double* s_blocks, double* clean_blocks, double* l_blocks) {
+  if (!e || e->cur < 0) return fail(RT_ERR_VALUE, "no iterate to export");
+  const double* st_s = e->prev >= 0 ? e->state(e->prev) : nullptr;
+  int st = run_block_pass(e, st_s, l_blocks ? e->state(e->cur) : nullptr, e->zeta_last, false, s_blocks,
+                          clean_blocks, l_blocks, false);
+  if (st) return st;
+  CK(cudaStreamSynchronize(e->st));
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_export_cur(rtcur_engine* e, double* const* U, double* const* sigma, double* const* V,
+                                       double* const* A, double* G) {
+  if (!e || e->cur < 0) return fail(RT_ERR_VALUE, "no iterate to export");
+  const Plan& P = e->P;
+  const Geom& g = P.g;
+  const double* sto = e->state(e->cur);
+  for (int m = 0; m < g.n; ++m) {
+    if (U && U[m]) CK(cudaMemcpyAsync(U[m], e->ws + P.o_U[m], g.nrows[m] * g.rank[m] * 8, cudaMemcpyDeviceToHost, e->st));
+    if (sigma && sigma[m]) CK(cudaMemcpyAsync(sigma[m], e->ws + P.o_sig[m], g.rank[m] * 8, cudaMemcpyDeviceToHost, e->st));
+    if (V && V[m]) CK(cudaMemcpyAsync(V[m], e->ws + P.o_V[m], g.ncols[m] * g.rank[m] * 8, cudaMemcpyDeviceToHost, e->st));
+    if (A && A[m]) CK(cudaMemcpyAsync(A[m], sto + g.a_off[m], g.dim[m] * g.rank[m] * 8, cudaMemcpyDeviceToHost, e->st));
+  }
+  if (G) CK(cudaMemcpyAsync(G, sto, g.gsize * 8, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  return RT_OK;
+}
+
+extern "C" int64_t rtcur_engine_full_scratch_bytes(rtcur_engine* e) {
+  if (!e) return 0;
+  i64 q = 1;
+  for (int m = 1; m < e->P.g.n; ++m) q *= e->P.g.dim[m];
+  return q * e->P.g.rank[0] * 8;
+}
+
+extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_dev, void* S_dev, double* tf_dev,
+                                        double* sums) {
+  if (!e || e->cur < 0) return fail(RT_ERR_VALUE, "no iterate");
+  if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
+  const Plan& P = e->P;
+  const Geom& g = P.g;
+  IndexPtrs ip = make_ip(e);
+  double* sto = e->state(e->cur);
+  i64 ncols = 1;
+  for (int m = 1; m < g.n; ++m) ncols *= g.dim[m];
+  DISPATCH_R(rbucket(g.rank[0]), k_wcols, dim3((unsigned)cdiv(ncols, 128), 1), 128, (int)(g.gsize * 8), e->st, g, ip,
+             sto, 1, tf_dev);
+  LAUNCH_CHECK();
+  FullArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.X = e->X;   // may be null: reconstruction only (x = 0)
+  fa.dtype = P.dtype;
+  fa.lo = e->lo;
+  fa.hi = e->hi;
+  fa.ncols = ncols;
+  fa.A1 = sto + g.a_off[0];
+  fa.d1 = g.dim[0];
+  fa.r1 = g.rank[0];
+  fa.Tf = tf_dev;
+  fa.zeta = zeta;
+  fa.L = L_dev;
+  fa.S = S_dev;
+  fa.partial = e->at<double>(P.o_fpart);
+  fa.sums = e->at<double>(P.o_sums);
+  fa.counter = e->at<unsigned int>(P.o_counters) + 32;
+  const int grid = 148 * 8;
+  if (P.dtype == 0) k_full<double><<<grid, 256, 0, e->st>>>(fa);
+  else k_full<float><<<grid, 256, 0, e->st>>>(fa);
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(e->h_pinned, fa.sums, 16, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  if (sums) memcpy(sums, e->h_pinned, 16);
+  return RT_OK;
+}
+
+// ------------------------------------------------------------------ kernel-level plug
+
+extern "C" int rtcur_gather_columns(const void* flat, int dtype, int64_t flat_len, const int64_t* bases_dev,
+                                    int64_t ncols, int64_t stride, int64_t length, double* out, void* stream) {
+  if (stride < 1 || length < 1) return fail(RT_ERR_VALUE, "stride and length must be >= 1");
+  if (ncols == 0) return RT_OK;
+  // bounds (py_kernels.py:242-251): check on the device copy via a host round trip of min/max
+  std::vector<int64_t> b(ncols);
+  CK(cudaMemcpyAsync(b.data(), bases_dev, ncols * 8, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  for (int64_t c = 0; c < ncols; ++c)
+    if (b[c] < 0 || b[c] + (length - 1) * stride >= flat_len)
+      return fail(RT_ERR_VALUE, "gather out of range: base " + std::to_string(b[c]));
+  const i64 n = ncols * length;
+  k_gather_columns<<<(unsigned)std::min<i64>(cdiv(n, 256), 4096), 256, 0, (cudaStream_t)stream>>>(
+      flat, dtype, bases_dev, ncols, stride, length, out);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
+extern "C" int rtcur_hard_threshold(const double* a, int64_t n, double zeta, double* out, void* stream) {
+  if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
+  if (n == 0) return RT_OK;
+  k_hard_threshold<<<(unsigned)std::min<i64>(cdiv(n, 256), 4096), 256, 0, (cudaStream_t)stream>>>(a, n, zeta, out);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
+extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, int r, double* u_dev, double* s_dev,
+                                   double* v_dev, void* stream) {
+  if (m < 1 || p < 1) return fail(RT_ERR_VALUE, "truncated_svd needs a nonempty matrix");
+  if (r < 1 || r > std::min(m, p)) return fail(RT_ERR_VALUE, "rank outside [1, min(m, p)]");
+  cudaStream_t st = (cudaStream_t)stream;
+  // Reuse the engine machinery on a one-mode "problem": the intersection is the
+  // whole matrix, so plan a 1-mode geometry with |I| = m, |J| = p.
+  Plan P;
+  memset(&P, 0, sizeof(P));
+  P.g.n = 1;
+  P.s[0] = std::min(m, p);
+  P.l[0] = std::max(m, p);
+  P.tall[0] = m > p;
+  if (P.s[0] > 235) return fail(RT_ERR_UNSUPPORTED, "min(m, p) > 235 not supported");
+  if (r > RT_MAX_RANK) return fail(RT_ERR_UNSUPPORTED, "rank > 32 not supported");
+  const i64 s = P.s[0], l = P.l[0];
+  P.g.rank[0] = r;
+  P.g.nrows[0] = m;
+  P.g.ncols[0] = p;
+  P.rmax = r;
+  P.rb = rbucket(r);
+  P.smax = s;
+  P.lmax = l;
+  P.hchunk = 256;
+  P.h_maxchunks = (int)cdiv(l, 256);
+  const int nt = (int)cdiv(s, GRAM_T);
+  P.gram_maxpairs = nt * (nt + 1) / 2;
+  P.gram_maxchunks = (int)cdiv(l, GRAM_CL);
+  P.nb[0] = (int)std::max<i64>(1, std::min<i64>(r, std::max<i64>(s * (s + 1) / 2, 5 * s * 4) / (5 * s)));
+  i64 o = 0;
+  auto take = [&](i64 bytes) { i64 rr = o; o += align256(std::max<i64>(bytes, 8)); return rr; };
+  P.o_M[0] = take(8);
+  P.o_gpart = take((i64)P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
+  P.o_K[0] = take(s * (s + 1) / 2 * 8);
+  P.o_hv[0] = take((s * (s - 1) / 2 + s) * 8);
+  P.o_E[0] = take(s * r * 8);
+  P.o_lam[0] = take(r * 8);
+  P.o_Z[0] = take(l * r * 8);
+  P.o_hpart[0] = take(cdiv(l, 256) * r * (r + 1) / 2 * 8);
+  P.o_H[0] = take(r * r * 8);
+  P.o_Q[0] = take(r * r * 8);
+  P.o_U[0] = take(m * r * 8);
+  P.o_V[0] = take(p * r * 8);
+  P.o_sig[0] = take(r * 8);
+  P.o_siginv[0] = take(r * 8);
+  P.o_perm[0] = take(r * 4);
+  P.o_degen[0] = take((r + 1) * 4);
+  P.o_flags = take(4);
+  P.o_counters = take(64 * 4);
+  char* ws = nullptr;
+  CK(cudaMallocAsync((void**)&ws, o, st));
+  rtcur_engine tmp;
+  memset((void*)&tmp, 0, sizeof(tmp));
+  tmp.P = P;
+  tmp.ws = ws;
+  tmp.st = st;
+  CK(cudaMemsetAsync(ws + P.o_counters, 0, 64 * 4, st));
+  // the SVD kernels take raw pointers: M points straight at the caller's matrix
+  int esm = eig_smem_bytes(P, 0);
+  CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(esm, 48 * 1024)));
+  const int zs = (int)(s * r * 8);
+  CK(cudaFuncSetAttribute(k_zproj<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_zproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_zproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  CK(cudaFuncSetAttribute(k_zproj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
+  GramArgs ga;
+  memset(&ga, 0, sizeof(ga));
+  ga.n = 1;
+  ga.s[0] = (int)s;
+  ga.l[0] = l;
+  ga.tall[0] = P.tall[0];
+  ga.mrows[0] = m;
+  ga.M[0] = m_dev;
+  ga.K[0] = tmp.at<double>(P.o_K[0]);
+  ga.part = tmp.at<double>(P.o_gpart);
+  ga.maxchunks = P.gram_maxchunks;
+  ga.maxpairs = P.gram_maxpairs;
+  k_gram_tiles<<<dim3(P.gram_maxpairs, P.gram_maxchunks, 1), 256, 0, st>>>(ga);
+  LAUNCH_CHECK();
+  k_gram_reduce<<<dim3((unsigned)std::min<i64>(cdiv(s * (s + 1) / 2, 256), 512), 1), 256, 0, st>>>(ga);
+  LAUNCH_CHECK();
+  EigArgs ea;
+  memset(&ea, 0, sizeof(ea));
+  ea.n = 1;
+  ea.s[0] = (int)s;
+  ea.r[0] = r;
+  ea.K[0] = ga.K[0];
+  ea.hv[0] = tmp.at<double>(P.o_hv[0]);
+  ea.E[0] = tmp.at<double>(P.o_E[0]);
+  ea.lam[0] = tmp.at<double>(P.o_lam[0]);
+  ea.nb[0] = P.nb[0];
+  k_eig<<<1, 1024, esm, st>>>(ea);
+  LAUNCH_CHECK();
+  SvdArgs sa = make_svd_args(&tmp);
+  sa.M[0] = m_dev;
+  unsigned int* hcnt = tmp.at<unsigned int>(P.o_counters) + 16;
+  const unsigned gz = (unsigned)cdiv(l, 256);
+  DISPATCH_R(P.rb, k_zproj, dim3(gz, 1), 256, zs, st, sa);
+  LAUNCH_CHECK();
+  k_hgram<<<dim3(P.h_maxchunks, 1), 576, 0, st>>>(sa, hcnt);
+  LAUNCH_CHECK();
+  k_svd_fin1<<<1, 32, 0, st>>>(sa);
+  LAUNCH_CHECK();
+  k_short_vecs<<<dim3((unsigned)cdiv(s * r, 256), 1), 256, 0, st>>>(sa);
+  LAUNCH_CHECK();
+  DISPATCH_R(P.rb, k_zrot, dim3(gz, 1), 256, 0, st, sa);
+  LAUNCH_CHECK();
+  k_hgram<<<dim3(P.h_maxchunks, 1), 576, 0, st>>>(sa, hcnt);
+  LAUNCH_CHECK();
+  k_svd_fin2<<<1, 32, 0, st>>>(sa);
+  LAUNCH_CHECK();
+  DISPATCH_R(P.rb, k_long, dim3(gz, 1), 256, 0, st, sa);
+  LAUNCH_CHECK();
+  k_complete<<<1, 256, 0, st>>>(sa);
+  LAUNCH_CHECK();
+  // row-major (m x r), (p x r) -> column-major outputs
+  std::vector<double> U(m * r), V(p * r), S(r);
+  CK(cudaMemcpyAsync(U.data(), sa.U[0], m * r * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(V.data(), sa.V[0], p * r * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(S.data(), sa.sig[0], r * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<double> Uc(m * r), Vc(p * r);
+  for (i64 i = 0; i < m; ++i)
+    for (int a = 0; a < r; ++a) Uc[i + a * m] = U[i * r + a];
+  for (i64 i = 0; i < p; ++i)
+    for (int a = 0; a < r; ++a) Vc[i + a * p] = V[i * r + a];
+  CK(cudaMemcpyAsync(u_dev, Uc.data(), m * r * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(v_dev, Vc.data(), p * r * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s_dev, S.data(), r * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaFreeAsync(ws, st));
+  CK(cudaStreamSynchronize(st));
+  return RT_OK;
+}

@@ -1,0 +1,289 @@
+// k_block.cu -- index preparation, fused gather, the fused residual/threshold
+// block pass (K1) and the streaming abs-max scan (K0).
+//
+// K1 replaces, per sampled entry, the reference's
+//   _eval_blocks (solver.py:242-249 -> fiber_cur.py:288-326, the einsum hot spot)
+//   hard_threshold(x_b - l_b, zeta) (solver.py:336-341 -> _core.pyx:252-262)
+//   clean = x_b - s_b and the intersection extraction fib[rows-1, :] (fiber_cur.py:265)
+//   sampled_relative_error sums (solver.py:209-231)
+// in one pass over the compact sampled blocks: the low-rank value is evaluated
+// on the fly from the rank-(r_1..r_n) Tucker state (G, A_k, W_b), so the
+// reference's |J_k| * prod|I_m| einsum becomes r FMAs per entry.
+#include "common.cuh"
+
+// ------------------------------------------------------------------ index prep
+
+// rowpos_k[p] = position of p in the sorted row set I_k, or -1.
+__global__ void k_rowpos(Geom g, IndexPtrs ip, int* __restrict__ rowpos_base) {
+  const int k = blockIdx.y;
+  if (k >= g.n) return;
+  i64 base = 0;
+  for (int m = 0; m < k; ++m) base += g.dim[m];
+  int* out = rowpos_base + base;
+  const int* rows = ip.rows[k];
+  const int nr = (int)g.nrows[k];
+  for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < g.dim[k]; p += (i64)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nr - 1, pos = -1;
+    while (lo <= hi) {
+      int mid = (lo + hi) >> 1;
+      int v = rows[mid];
+      if (v == (int)p) { pos = mid; break; }
+      if (v < (int)p) lo = mid + 1; else hi = mid - 1;
+    }
+    out[p] = pos;
+  }
+}
+
+// Per block column: the "rest" offset R over modes >= 2 and, for fiber blocks
+// of modes >= 2, the fixed mode-1 index.  Mirrors tensor.py:250-283
+// (decode_fiber_columns / fiber_base_offsets: other modes ascending, first
+// other mode fastest) and, for the core, the np.ix_ ordering of tensor.py:239.
+__global__ void k_colprep(Geom g, IndexPtrs ip, i64* __restrict__ colR_base, int* __restrict__ coli1_base,
+                          const i64* __restrict__ col_off) {
+  const int b = blockIdx.y;
+  if (b >= g.nblk) return;
+  const BlockDesc bd = g.blk[b];
+  i64* colR = colR_base + col_off[b];
+  int* coli1 = coli1_base + col_off[b];
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < bd.Q; q += (i64)gridDim.x * blockDim.x) {
+    i64 R = 0;
+    int i1 = -1;
+    if (bd.is_core) {
+      i64 t = q;
+      for (int m = 1; m < g.n; ++m) {
+        i64 pos = t % g.nrows[m];
+        t /= g.nrows[m];
+        R += (i64)ip.rows[m][pos] * g.rstride[m];
+      }
+    } else {
+      const int k = bd.mode;
+      i64 j = ip.cols[k][q];
+      for (int m = 0; m < g.n; ++m) {
+        if (m == k) continue;
+        i64 im = j % g.dim[m];
+        j /= g.dim[m];
+        if (m == 0) i1 = (int)im; else R += im * g.rstride[m];
+      }
+    }
+    colR[q] = R;
+    coli1[q] = i1;
+  }
+}
+
+// ------------------------------------------------------------------ tile map
+
+struct TileMap {
+  int nblk;
+  int tile;                        // elements per CTA tile
+  i64 first[RT_MAX_BLOCKS + 1];    // first tile of each block, first[nblk] = total tiles
+};
+
+__device__ __forceinline__ int tile_block(const TileMap& tm, i64 t) {
+  int b = 0;
+  while (b + 1 < tm.nblk && t >= tm.first[b + 1]) ++b;
+  return b;
+}
+
+// ------------------------------------------------------------------ gather (sharded)
+
+// x_b[e] = X_local[(i1 - lo) + (hi - lo) * R] when lo <= i1 < hi, else 0.
+// With one rank (lo = 0, hi = d_1) this is the plain gather of solver.py:172-182.
+// Multi-rank: every sampled entry has exactly one owner, so a sum all-reduce of
+// the per-rank x_b reproduces the full gather bit-exactly.
+__global__ void __launch_bounds__(256) k_gather(Geom g, TileMap tm, IndexPtrs ip, const void* __restrict__ X, int dtype,
+                                               i64 lo, i64 hi, void* __restrict__ xb) {
+  const i64 t = blockIdx.x;
+  const int b = tile_block(tm, t);
+  const BlockDesc bd = g.blk[b];
+  const i64 nel = bd.P * bd.Q;
+  const i64 e0 = (t - tm.first[b]) * tm.tile;
+  const i64 e1 = min(nel, e0 + tm.tile);
+  const i64 ld = hi - lo;
+  const i64* colR = ip.colR[b];
+  const int* coli1 = ip.coli1[b];
+  const int* rows0 = ip.rows[0];
+  const i64 rstr = bd.mode >= 1 ? g.rstride[bd.mode] : 0;
+  i64 e = e0 + threadIdx.x;
+  if (e >= e1) return;
+  i64 q = e / bd.P, p = e - q * bd.P;
+  for (; e < e1; e += blockDim.x) {
+    int ci = coli1[q];
+    i64 i1 = ci >= 0 ? (i64)ci : (bd.is_core ? (i64)rows0[p] : p);
+    i64 R = colR[q] + p * rstr;
+    double v = 0.0;
+    if (i1 >= lo && i1 < hi) v = ld_elem(X, (i1 - lo) + ld * R, dtype);
+    if (dtype == 0) reinterpret_cast<double*>(xb)[bd.off + e] = v;
+    else reinterpret_cast<float*>(xb)[bd.off + e] = (float)v;
+    p += blockDim.x;
+    while (p >= bd.P) { p -= bd.P; ++q; }
+  }
+}
+
+// ------------------------------------------------------------------ K1 block pass
+
+struct PassArgs {
+  const void* xb;
+  int dtype;
+  const double* st_s;      // state giving L for the threshold (null: L = 0, first iteration)
+  const double* st_e;      // state giving L for the error / trace (null: no error)
+  double zeta;
+  double* M[RT_MAX_MODES]; // intersection outputs, m_k x p_k column-major (null: skip)
+  double* s_out;           // optional sparse values on the blocks
+  double* c_out;           // optional clean values
+  double* l_out;           // optional low-rank values (state st_e)
+  double* partial;         // [tiles][2] per-CTA (e2, x2)
+  double* sums;            // [nblk][2]  final (e2, x2)
+  unsigned int* counter;   // last-CTA ticket
+  int* nonfinite;          // set if a clean intersection entry is not finite
+  int want_x2;
+};
+
+__global__ void __launch_bounds__(256) k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a) {
+  __shared__ double red[8];
+  __shared__ bool am_last;
+  const i64 t = blockIdx.x;
+  const int b = tile_block(tm, t);
+  const BlockDesc bd = g.blk[b];
+  const i64 nel = bd.P * bd.Q;
+  const i64 e0 = (t - tm.first[b]) * tm.tile;
+  const i64 e1 = min(nel, e0 + tm.tile);
+  const int* rows0 = ip.rows[0];
+  double* Mk = bd.is_core ? nullptr : a.M[bd.mode];
+  const int* rowpos = bd.is_core ? nullptr : ip.rowpos[bd.mode];
+  const i64 mrows = bd.is_core ? 0 : g.nrows[bd.mode];
+  double e2 = 0.0, x2 = 0.0;
+  bool bad = false;
+  i64 e = e0 + threadIdx.x;
+  if (e < e1) {
+    i64 q = e / bd.P, p = e - q * bd.P;
+    for (; e < e1; e += blockDim.x) {
+      const double x = ld_elem(a.xb, bd.off + e, a.dtype);
+      const double ls = a.st_s ? eval_low(a.st_s, g, bd, rows0, p, q) : 0.0;
+      const double s = hard_thr(x - ls, a.zeta);
+      const double c = x - s;
+      if (Mk) {
+        const int pos = rowpos[p];
+        if (pos >= 0) {
+          Mk[pos + q * mrows] = c;
+          bad |= !isfinite(c);
+        }
+      }
+      if (a.s_out) a.s_out[bd.off + e] = s;
+      if (a.c_out) a.c_out[bd.off + e] = c;
+      if (a.st_e) {
+        const double le = eval_low(a.st_e, g, bd, rows0, p, q);
+        const double r = x - le - s;
+        e2 = fma(r, r, e2);
+        if (a.l_out) a.l_out[bd.off + e] = le;
+      }
+      x2 = fma(x, x, x2);
+      p += blockDim.x;
+      while (p >= bd.P) { p -= bd.P; ++q; }
+    }
+  }
+  if (bad) atomicExch(a.nonfinite, 1);
+  if (a.partial == nullptr) return;
+  e2 = block_sum(e2, red);
+  x2 = block_sum(x2, red);
+  if (threadIdx.x == 0) {
+    a.partial[2 * t] = e2;
+    a.partial[2 * t + 1] = x2;
+    __threadfence();
+    unsigned int ticket = atomicAdd(a.counter, 1u);
+    am_last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // last CTA: per-block sums over the block's tiles in tile order (deterministic)
+  for (int bb = 0; bb < tm.nblk; ++bb) {
+    double se = 0.0, sx = 0.0;
+    for (i64 tt = tm.first[bb] + threadIdx.x; tt < tm.first[bb + 1]; tt += blockDim.x) {
+      se += ((volatile double*)a.partial)[2 * tt];
+      sx += ((volatile double*)a.partial)[2 * tt + 1];
+    }
+    se = block_sum(se, red);
+    sx = block_sum(sx, red);
+    if (threadIdx.x == 0) {
+      a.sums[2 * bb] = se;
+      a.sums[2 * bb + 1] = sx;
+    }
+  }
+  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
+// ------------------------------------------------------------------ K0 abs-max
+
+// zeta_0 = max|X| (solver.py:184-192, used when cfg.zeta0 is None, solver.py:304).
+// NaN propagates like numpy's max.  Result is written as the IEEE bit pattern
+// of a nonnegative double (monotone as an unsigned integer) via atomicMax.
+template <typename T>
+__global__ void __launch_bounds__(256) k_absmax(const T* __restrict__ x, i64 n, unsigned long long* __restrict__ out) {
+  __shared__ double red[8];
+  double m = 0.0;
+  bool nan = false;
+  constexpr int VEC = 16 / sizeof(T);
+  const i64 nv = n / VEC;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  // 4 independent 16-byte loads in flight per thread
+  for (; i + 3 * stride < nv; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcs(xv + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const T* e = reinterpret_cast<const T*>(&v[u]);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        double a = fabs((double)e[j]);
+        nan |= (a != a);
+        m = fmax(m, a);
+      }
+    }
+  }
+  for (; i < nv; i += stride) {
+    uint4 v = __ldcs(xv + i);
+    const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      double a = fabs((double)e[j]);
+      nan |= (a != a);
+      m = fmax(m, a);
+    }
+  }
+  for (i64 j = nv * VEC + blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += stride) {
+    double a = fabs((double)x[j]);
+    nan |= (a != a);
+    m = fmax(m, a);
+  }
+  m = block_max(m, red);
+  int anynan = __syncthreads_or(nan);
+  if (threadIdx.x == 0) {
+    unsigned long long bits = anynan ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(m);
+    atomicMax(out, bits);
+  }
+}
+
+template __global__ void k_absmax<float>(const float*, i64, unsigned long long*);
+template __global__ void k_absmax<double>(const double*, i64, unsigned long long*);
+
+// ------------------------------------------------------------------ kernel-level plug
+
+// gather_columns (reference _core.pyx:265-288): out[i, c] = flat[bases[c] + i*stride],
+// out is length x ncols column-major (the Cython backend's F-order result).
+__global__ void k_gather_columns(const void* __restrict__ flat, int dtype, const i64* __restrict__ bases, i64 ncols,
+                                 i64 stride, i64 length, double* __restrict__ out) {
+  const i64 n = ncols * length;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x) {
+    i64 c = e / length, i = e - c * length;
+    out[e] = ld_elem(flat, bases[c] + i * stride, dtype);
+  }
+}
+
+// hard_threshold (reference _core.pyx:252-262): strict keep |x| > zeta.
+__global__ void k_hard_threshold(const double* __restrict__ a, i64 n, double zeta, double* __restrict__ out) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x)
+    out[e] = hard_thr(a[e], zeta);
+}

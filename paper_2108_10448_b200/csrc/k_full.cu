@@ -1,0 +1,87 @@
+// k_full.cu -- K3: streaming full-tensor reconstruction + threshold + residual
+// sums, the device form of the reference's full-output step
+//   L = cur_reconstruct_full(cur)              (cli.py:238 -> fiber_cur.py:277-285)
+//   S = hard_threshold(x - L, zeta_final)       (cli.py:240-242)
+// evaluated in Tucker form L(i_1, R) = sum_a A_1[i_1, a] Tf[R, a] with
+// Tf = G x_{m>=2} A_m (one fp64 row of r_1 values per mode-1 fiber), so each
+// element costs r_1 FMAs and the kernel streams X once and writes L and S once
+// (3 E bytes per element).  Works on a mode-1 slab [lo, hi) of a sharded X.
+#include "common.cuh"
+
+struct FullArgs {
+  const void* X;        // local slab, (hi-lo) x d_2 x ... mode-1 fastest
+  int dtype;
+  i64 lo, hi;           // mode-1 slab
+  i64 ncols;            // prod_{m>=2} d_m
+  const double* A1;     // d_1 x r_1 col-major (state)
+  i64 d1;
+  int r1;
+  const double* Tf;     // ncols x r_1 row-major
+  double zeta;
+  void* L;              // optional outputs (dtype), same layout as X
+  void* S;
+  double* partial;      // [grid][2]
+  double* sums;         // [2]: sum (x-L-S)^2, sum x^2
+  unsigned int* counter;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_full(FullArgs a) {
+  __shared__ double red[8];
+  __shared__ bool am_last;
+  const i64 ld = a.hi - a.lo;
+  const i64 n = ld * a.ncols;
+  const T* X = reinterpret_cast<const T*>(a.X);
+  T* L = reinterpret_cast<T*>(a.L);
+  T* S = reinterpret_cast<T*>(a.S);
+  double e2 = 0.0, x2 = 0.0;
+  const i64 stride = (i64)gridDim.x * blockDim.x;
+  const double* A1 = a.A1 + a.lo;
+  // each thread walks elements e = start + k*stride; (i1, col) tracked incrementally
+  i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (e < n) {
+    i64 col = e / ld, i1 = e - col * ld;
+    const i64 dcol = stride / ld, di = stride - dcol * ld;
+    for (; e < n; e += stride) {
+      const double x = X ? (double)X[e] : 0.0;
+      const double* tf = a.Tf + col * a.r1;
+      double l = 0.0;
+      for (int k = 0; k < a.r1; ++k) l = fma(A1[i1 + k * a.d1], tf[k], l);
+      const double s = hard_thr(x - l, a.zeta);
+      const double res = x - l - s;
+      e2 = fma(res, res, e2);
+      x2 = fma(x, x, x2);
+      if (L) L[e] = (T)l;
+      if (S) S[e] = (T)s;
+      i1 += di;
+      col += dcol;
+      if (i1 >= ld) { i1 -= ld; ++col; }
+    }
+  }
+  e2 = block_sum(e2, red);
+  x2 = block_sum(x2, red);
+  if (threadIdx.x == 0) {
+    a.partial[2 * blockIdx.x] = e2;
+    a.partial[2 * blockIdx.x + 1] = x2;
+    __threadfence();
+    am_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double se = 0.0, sx = 0.0;
+  for (i64 t = threadIdx.x; t < gridDim.x; t += blockDim.x) {
+    se += ((volatile double*)a.partial)[2 * t];
+    sx += ((volatile double*)a.partial)[2 * t + 1];
+  }
+  se = block_sum(se, red);
+  sx = block_sum(sx, red);
+  if (threadIdx.x == 0) {
+    a.sums[0] = se;
+    a.sums[1] = sx;
+    *a.counter = 0u;
+  }
+}
+
+template __global__ void k_full<float>(FullArgs);
+template __global__ void k_full<double>(FullArgs);

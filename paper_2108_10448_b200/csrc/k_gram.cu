@@ -1,0 +1,114 @@
+// k_gram.cu -- fp64 Gram matrix of each mode's intersection on its short side.
+//
+// The reference factorises every intersection C_i(I_i, :) (|I_i| x |J_i|) with
+// a full Householder + implicit-QR SVD (linalg.py:59-74 -> _core.pyx:24-58).
+// On the device we only need its rank-r_i truncation, so each intersection B
+// (viewed as s x l, s = min(|I|, |J|)) is reduced to the s x s Gram K = B B^T
+// (this kernel), whose top-r eigenvectors give the short-side singular
+// subspace (k_eig.cu); the long-side vectors, the singular values and the
+// orthonormality repair are then recomputed directly from B (k_svdpost.cu), so
+// singular values keep absolute accuracy ~eps*sigma_1 as in the reference.
+#include "common.cuh"
+
+#define GRAM_T 64      // output tile edge
+#define GRAM_KS 16     // k-step
+#define GRAM_CL 256    // long-side chunk per CTA (split-K)
+
+struct GramArgs {
+  int n;
+  int s[RT_MAX_MODES];
+  i64 l[RT_MAX_MODES];
+  int tall[RT_MAX_MODES];           // 1: B = M^T (|I| > |J|), else B = M
+  i64 mrows[RT_MAX_MODES];          // rows of M (= |I_k|)
+  const double* M[RT_MAX_MODES];
+  double* part;                     // [n][maxchunks][maxpairs][T*T]
+  double* K[RT_MAX_MODES];          // packed lower s(s+1)/2
+  int maxchunks, maxpairs;
+};
+
+__device__ __forceinline__ double gram_B(const GramArgs& ga, int k, i64 a, i64 t) {
+  const double* M = ga.M[k];
+  return ga.tall[k] ? M[t + a * ga.mrows[k]] : M[a + t * ga.mrows[k]];
+}
+
+__device__ __forceinline__ void pair_decode(int pair, int& I, int& J) {
+  int i = (int)((sqrt(8.0 * pair + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) / 2 <= pair) ++i;
+  while (i * (i + 1) / 2 > pair) --i;
+  I = i;
+  J = pair - i * (i + 1) / 2;
+}
+
+__global__ void __launch_bounds__(256) k_gram_tiles(GramArgs ga) {
+  const int k = blockIdx.z;
+  if (k >= ga.n) return;
+  const int s = ga.s[k];
+  const i64 l = ga.l[k];
+  const int nt = (s + GRAM_T - 1) / GRAM_T;
+  const int npairs = nt * (nt + 1) / 2;
+  const int pair = blockIdx.x;
+  if (pair >= npairs) return;
+  const i64 t0 = (i64)blockIdx.y * GRAM_CL;
+  if (t0 >= l) return;
+  const i64 t1 = min(l, t0 + GRAM_CL);
+  int I, J;
+  pair_decode(pair, I, J);
+  __shared__ double As[GRAM_KS][GRAM_T + 1];
+  __shared__ double Bs[GRAM_KS][GRAM_T + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (i64 tt = t0; tt < t1; tt += GRAM_KS) {
+    for (int idx = threadIdx.x; idx < GRAM_T * GRAM_KS; idx += blockDim.x) {
+      const int r = idx % GRAM_T, kk = idx / GRAM_T;
+      const i64 t = tt + kk;
+      const int a = I * GRAM_T + r, b = J * GRAM_T + r;
+      As[kk][r] = (a < s && t < t1) ? gram_B(ga, k, a, t) : 0.0;
+      Bs[kk][r] = (b < s && t < t1) ? gram_B(ga, k, b, t) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GRAM_KS; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  double* out = ga.part + (((i64)k * ga.maxchunks + blockIdx.y) * ga.maxpairs + pair) * (GRAM_T * GRAM_T);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) out[(ty * 4 + i) * GRAM_T + tx + 16 * j] = acc[i][j];
+}
+
+// Sum the split-K partials in chunk order (deterministic) into packed lower K.
+__global__ void k_gram_reduce(GramArgs ga) {
+  const int k = blockIdx.y;
+  if (k >= ga.n) return;
+  const int s = ga.s[k];
+  const i64 npk = (i64)s * (s + 1) / 2;
+  const int nchunks = (int)((ga.l[k] + GRAM_CL - 1) / GRAM_CL);
+  for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < npk; idx += (i64)gridDim.x * blockDim.x) {
+    int i = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+    while ((i64)(i + 1) * (i + 2) / 2 <= idx) ++i;
+    while ((i64)i * (i + 1) / 2 > idx) --i;
+    const int j = (int)(idx - (i64)i * (i + 1) / 2);
+    const int I = i / GRAM_T, J = j / GRAM_T;
+    const int pair = I * (I + 1) / 2 + J;
+    const int li = i % GRAM_T, lj = j % GRAM_T;
+    const double* p = ga.part + ((i64)k * ga.maxchunks * ga.maxpairs + pair) * (GRAM_T * GRAM_T) + li * GRAM_T + lj;
+    double acc = 0.0;
+    for (int c = 0; c < nchunks; ++c) acc += p[(i64)c * ga.maxpairs * (GRAM_T * GRAM_T)];
+    ga.K[k][idx] = acc;
+  }
+}

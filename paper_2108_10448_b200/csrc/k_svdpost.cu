@@ -1,0 +1,388 @@
+// k_svdpost.cu -- finish the rank-r truncated SVD of each intersection from
+// the short-side eigenbasis E (k_eig.cu):
+//
+//   Z  = B^T E            long-side projections (l x r)         k_zproj
+//   H  = Z^T Z            r x r (split over l, deterministic)    k_hgram
+//   H = Q diag(mu) Q^T    Rayleigh-Ritz rotation (warp Jacobi)   k_svd_fin1
+//   S_short = E Q,  Z <- Z Q                                     k_zrot
+//   H' = Z^T Z; sigma_a = sqrt(H'_aa) = ||z_a||, stable sort,
+//   Cholesky of the normalised H' -> T with Z T orthonormal      k_svd_fin2
+//   S_long = Z T (+ orthonormal completion for sigma <= tau)     k_long, k_complete
+//
+// Output per mode (matching linalg.py:26-56 TruncatedSvd): U (|I| x r),
+// singular values (non-increasing), V (|J| x r), the truncated-pinv
+// reciprocals 1/sigma for sigma > tau = max(m, p) * sigma_1 * 1e-12 (else 0,
+// linalg.py:54-55) and the rank-deficiency flag of solver.py:252-257.
+// U/V are stored row-major (row index major, r contiguous values per row).
+#include "common.cuh"
+#include <cfloat>
+
+struct SvdArgs {
+  int n;
+  int s[RT_MAX_MODES];
+  i64 l[RT_MAX_MODES];
+  int r[RT_MAX_MODES];
+  int tall[RT_MAX_MODES];
+  i64 mrows[RT_MAX_MODES];           // |I_k| (rows of M)
+  i64 pcols[RT_MAX_MODES];           // |J_k|
+  const double* M[RT_MAX_MODES];     // m x p column-major intersection
+  const double* E[RT_MAX_MODES];     // s x r column-major eigenbasis
+  double* Z[RT_MAX_MODES];           // l x r row-major
+  double* hpart[RT_MAX_MODES];       // [chunks][r*r]
+  double* H[RT_MAX_MODES];           // r x r
+  double* Q[RT_MAX_MODES];           // r x r (col-major) Ritz rotation, then T
+  double* U[RT_MAX_MODES];           // m x r row-major (output)
+  double* V[RT_MAX_MODES];           // p x r row-major (output)
+  double* sig[RT_MAX_MODES];         // r (output)
+  double* siginv[RT_MAX_MODES];      // r (output)
+  int* perm[RT_MAX_MODES];           // r
+  int* degen[RT_MAX_MODES];          // r flags + [r] = any
+  int* flags;                        // n rank-deficiency flags (output)
+  int hchunk;                        // long-side rows per CTA for k_hgram
+};
+
+__device__ __forceinline__ double svd_B(const SvdArgs& sa, int k, i64 c, i64 t) {
+  // B is s x l: B = M (wide) or M^T (tall)
+  const double* M = sa.M[k];
+  return sa.tall[k] ? M[t + c * sa.mrows[k]] : M[c + t * sa.mrows[k]];
+}
+
+// Z[t, a] = sum_c B[c, t] E[c, a]
+template <int R>
+__global__ void __launch_bounds__(256) k_zproj(SvdArgs sa) {
+  extern __shared__ double es[];
+  const int k = blockIdx.y;
+  if (k >= sa.n) return;
+  const int s = sa.s[k], r = sa.r[k];
+  const i64 l = sa.l[k];
+  if ((i64)blockIdx.x * blockDim.x >= l) return;
+  for (int i = threadIdx.x; i < s * r; i += blockDim.x) es[i] = sa.E[k][i];
+  __syncthreads();
+  const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= l) return;
+  double z[R];
+#pragma unroll
+  for (int a = 0; a < R; ++a) z[a] = 0.0;
+  for (int c = 0; c < s; ++c) {
+    const double b = svd_B(sa, k, c, t);
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+      if (a < r) z[a] = fma(es[c + a * s], b, z[a]);
+  }
+  double* Z = sa.Z[k] + t * r;
+#pragma unroll
+  for (int a = 0; a < R; ++a)
+    if (a < r) Z[a] = z[a];
+}
+
+// Z <- Z Q (in place, per long-side row)
+template <int R>
+__global__ void __launch_bounds__(256) k_zrot(SvdArgs sa) {
+  __shared__ double qs[RT_MAX_RANK * RT_MAX_RANK];
+  const int k = blockIdx.y;
+  if (k >= sa.n) return;
+  const int r = sa.r[k];
+  const i64 l = sa.l[k];
+  if ((i64)blockIdx.x * blockDim.x >= l) return;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) qs[i] = sa.Q[k][i];
+  __syncthreads();
+  const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= l) return;
+  double* Z = sa.Z[k] + t * r;
+  double z[R], o[R];
+#pragma unroll
+  for (int a = 0; a < R; ++a) { z[a] = a < r ? Z[a] : 0.0; o[a] = 0.0; }
+#pragma unroll
+  for (int b = 0; b < R; ++b)
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+      if (a < r && b < r) o[a] = fma(z[b], qs[b + a * r], o[a]);
+#pragma unroll
+  for (int a = 0; a < R; ++a)
+    if (a < r) Z[a] = o[a];
+}
+
+// H = Z^T Z: CTA = (chunk of long rows, mode); thread = (a, b) pair with a <= b.
+// Partials per chunk, the last CTA of each mode sums them in chunk order.
+__global__ void __launch_bounds__(576) k_hgram(SvdArgs sa, unsigned int* counters) {
+  __shared__ bool am_last;
+  const int k = blockIdx.y;
+  if (k >= sa.n) return;
+  const int r = sa.r[k];
+  const i64 l = sa.l[k];
+  const int nch = (int)((l + sa.hchunk - 1) / sa.hchunk);
+  if ((int)blockIdx.x >= nch) return;
+  const int npair = r * (r + 1) / 2;
+  const int tid = threadIdx.x;
+  int a = 0, b = 0;
+  if (tid < npair) {
+    int rem = tid;
+    while (rem >= r - a) { rem -= r - a; ++a; }
+    b = a + rem;
+  }
+  const i64 t0 = (i64)blockIdx.x * sa.hchunk, t1 = min(l, t0 + sa.hchunk);
+  if (tid < npair) {
+    double acc = 0.0;
+    const double* Z = sa.Z[k];
+    for (i64 t = t0; t < t1; ++t) acc = fma(Z[t * r + a], Z[t * r + b], acc);
+    sa.hpart[k][(i64)blockIdx.x * npair + tid] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = (atomicAdd(&counters[k], 1u) == (unsigned)nch - 1);
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  if (tid < npair) {
+    double acc = 0.0;
+    for (int c = 0; c < nch; ++c) acc += ((volatile double*)sa.hpart[k])[(i64)c * npair + tid];
+    sa.H[k][a + b * r] = acc;
+    sa.H[k][b + a * r] = acc;
+  }
+  if (tid == 0) counters[k] = 0u;
+}
+
+// Rayleigh-Ritz: cyclic Jacobi on H (one warp per mode, lane = row), sort the
+// Ritz values descending, write Q (col-major) and the short-side vectors E Q.
+__global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
+  __shared__ double h[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ double q[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ int ord[RT_MAX_RANK];
+  const int k = blockIdx.x;
+  if (k >= sa.n) return;
+  const int r = sa.r[k], lane = threadIdx.x;
+  for (int i = lane; i < r * r; i += 32) {
+    h[i] = sa.H[k][i];
+    q[i] = (i % r == i / r) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0, dia = 0.0;
+    for (int i = lane; i < r * r; i += 32) {
+      const double v = h[i] * h[i];
+      if (i % r == i / r) dia += v; else off += v;
+    }
+    off = warp_sum(off);
+    dia = warp_sum(dia);
+    if (off <= DBL_EPSILON * DBL_EPSILON * dia * 1e-4 || off == 0.0) break;
+    for (int p = 0; p < r - 1; ++p) {
+      for (int qq = p + 1; qq < r; ++qq) {
+        const double apq = h[p + qq * r];
+        if (apq == 0.0) continue;
+        const double app = h[p + p * r], aqq = h[qq + qq * r];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        __syncwarp();
+        // columns p, q of h
+        if (lane < r) {
+          const double hp = h[lane + p * r], hq = h[lane + qq * r];
+          h[lane + p * r] = c * hp - sn * hq;
+          h[lane + qq * r] = sn * hp + c * hq;
+        }
+        __syncwarp();
+        if (lane < r) {
+          const double hp = h[p + lane * r], hq = h[qq + lane * r];
+          h[p + lane * r] = c * hp - sn * hq;
+          h[qq + lane * r] = sn * hp + c * hq;
+          const double qp = q[lane + p * r], qv = q[lane + qq * r];
+          q[lane + p * r] = c * qp - sn * qv;
+          q[lane + qq * r] = sn * qp + c * qv;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (lane == 0) {
+    for (int i = 0; i < r; ++i) ord[i] = i;
+    for (int i = 1; i < r; ++i) {
+      const int t = ord[i];
+      int j = i - 1;
+      while (j >= 0 && h[ord[j] + ord[j] * r] < h[t + t * r]) { ord[j + 1] = ord[j]; --j; }
+      ord[j + 1] = t;
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < r * r; i += 32) {
+    const int row = i % r, col = i / r;
+    sa.Q[k][i] = q[row + ord[col] * r];
+  }
+}
+
+// short-side vectors S = E Q written row-major into U (wide) or V (tall)
+__global__ void k_short_vecs(SvdArgs sa) {
+  const int k = blockIdx.y;
+  if (k >= sa.n) return;
+  const int s = sa.s[k], r = sa.r[k];
+  double* out = sa.tall[k] ? sa.V[k] : sa.U[k];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < s * r; e += gridDim.x * blockDim.x) {
+    const int i = e / r, a = e % r;
+    double acc = 0.0;
+    for (int b = 0; b < r; ++b) acc = fma(sa.E[k][i + b * s], sa.Q[k][b + a * r], acc);
+    out[(i64)i * r + a] = acc;
+  }
+}
+
+// sigma from ||z_a||, stable descending order, truncated-pinv reciprocals,
+// Cholesky orthonormalisation T (Z T orthonormal) over non-degenerate columns.
+__global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
+  __shared__ double h[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ double R[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ double sg[RT_MAX_RANK];
+  __shared__ int ord[RT_MAX_RANK], dg[RT_MAX_RANK];
+  const int k = blockIdx.x;
+  if (k >= sa.n) return;
+  const int r = sa.r[k], lane = threadIdx.x;
+  for (int i = lane; i < r * r; i += 32) h[i] = sa.H[k][i];
+  __syncwarp();
+  if (lane == 0) {
+    for (int a = 0; a < r; ++a) sg[a] = sqrt(fmax(h[a + a * r], 0.0));
+    for (int i = 0; i < r; ++i) ord[i] = i;
+    for (int i = 1; i < r; ++i) {
+      const int t = ord[i];
+      int j = i - 1;
+      while (j >= 0 && sg[ord[j]] < sg[t]) { ord[j + 1] = ord[j]; --j; }
+      ord[j + 1] = t;
+    }
+    const double s1 = sg[ord[0]];
+    const double mx = (double)(sa.mrows[k] > sa.pcols[k] ? sa.mrows[k] : sa.pcols[k]);
+    const double tau = mx * s1 * 1e-12;   // linalg.py:54
+    int anyd = 0;
+    for (int a = 0; a < r; ++a) {
+      const double sv = sg[ord[a]];
+      sa.sig[k][a] = sv;
+      sa.siginv[k][a] = sv > tau ? 1.0 / sv : 0.0;
+      sa.perm[k][a] = ord[a];
+      dg[a] = !(sv > tau);
+    }
+    // flags: solver.py:252-257 (sigma_1 <= 0 or sigma_r <= 1e-8 sigma_1)
+    sa.flags[k] = (s1 <= 0.0 || sg[ord[r - 1]] <= 1e-8 * s1) ? 1 : 0;
+    // Cholesky of C = D^-1 P^T H P D^-1 on non-degenerate columns (sorted order)
+    for (int i = 0; i < r * r; ++i) R[i] = 0.0;
+    for (int j = 0; j < r; ++j) {
+      if (dg[j]) continue;
+      const int oj = ord[j];
+      for (int i = 0; i <= j; ++i) {
+        if (dg[i]) continue;
+        const int oi = ord[i];
+        double c = h[oi + oj * r] / (sg[oi] * sg[oj]);
+        for (int p = 0; p < i; ++p) c -= R[p + i * r] * R[p + j * r];
+        if (i == j) {
+          if (c <= 1e-6) { dg[j] = 1; break; }   // numerically dependent: complete instead
+          R[j + j * r] = sqrt(c);
+        } else {
+          R[i + j * r] = c / R[i + i * r];
+        }
+      }
+    }
+    // T = P D^-1 R^-1 (upper triangular inverse by back substitution), stored in Q
+    double* T = sa.Q[k];
+    for (int i = 0; i < r * r; ++i) T[i] = 0.0;
+    for (int j = 0; j < r; ++j) {
+      if (dg[j]) continue;
+      // column j of R^-1: solve R x = e_j over non-degenerate indices <= j
+      double x[RT_MAX_RANK];
+      for (int i = j; i >= 0; --i) {
+        if (dg[i]) { x[i] = 0.0; continue; }
+        double v = (i == j) ? 1.0 : 0.0;
+        for (int p = i + 1; p <= j; ++p) if (!dg[p]) v -= R[i + p * r] * x[p];
+        x[i] = v / R[i + i * r];
+      }
+      for (int i = 0; i <= j; ++i)
+        if (!dg[i]) T[ord[i] + j * r] = x[i] / sg[ord[i]];
+    }
+    for (int a = 0; a < r; ++a) {
+      sa.degen[k][a] = dg[a];
+      anyd |= dg[a];
+    }
+    sa.degen[k][r] = anyd;
+  }
+}
+
+// long-side vectors: out[t, a] = sum_b Z[t, b] T[b, a]; short side permuted in place later
+template <int R>
+__global__ void __launch_bounds__(256) k_long(SvdArgs sa) {
+  __shared__ double ts[RT_MAX_RANK * RT_MAX_RANK];
+  const int k = blockIdx.y;
+  if (k >= sa.n) return;
+  const int r = sa.r[k];
+  const i64 l = sa.l[k];
+  if ((i64)blockIdx.x * blockDim.x >= l) return;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) ts[i] = sa.Q[k][i];
+  __syncthreads();
+  const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= l) return;
+  const double* Z = sa.Z[k] + t * r;
+  double z[R], o[R];
+#pragma unroll
+  for (int a = 0; a < R; ++a) { z[a] = a < r ? Z[a] : 0.0; o[a] = 0.0; }
+#pragma unroll
+  for (int b = 0; b < R; ++b)
+#pragma unroll
+    for (int a = 0; a < R; ++a)
+      if (a < r && b < r) o[a] = fma(z[b], ts[b + a * r], o[a]);
+  double* out = (sa.tall[k] ? sa.U[k] : sa.V[k]) + t * r;
+#pragma unroll
+  for (int a = 0; a < R; ++a)
+    if (a < r) out[a] = o[a];
+}
+
+// permute the short-side columns to the sigma order; complete degenerate
+// columns of both sides with orthonormal vectors (only when sigma <= tau, where
+// 1/sigma is dropped, so this never changes the low-rank iterate).
+__global__ void __launch_bounds__(256) k_complete(SvdArgs sa) {
+  __shared__ double tmp[RT_MAX_RANK];
+  __shared__ double red[8];
+  __shared__ double coef[RT_MAX_RANK];
+  const int k = blockIdx.x;
+  if (k >= sa.n) return;
+  const int r = sa.r[k];
+  const int s = sa.s[k];
+  const i64 l = sa.l[k];
+  double* S = sa.tall[k] ? sa.V[k] : sa.U[k];   // short side, s x r row-major
+  double* Lg = sa.tall[k] ? sa.U[k] : sa.V[k];  // long side, l x r row-major
+  // permute short side rows in place
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    double row[RT_MAX_RANK];
+    for (int a = 0; a < r; ++a) row[a] = S[(i64)i * r + a];
+    for (int a = 0; a < r; ++a) S[(i64)i * r + a] = row[sa.perm[k][a]];
+  }
+  __syncthreads();
+  if (!sa.degen[k][r]) return;
+  for (int side = 0; side < 2; ++side) {
+    double* X = side == 0 ? Lg : S;
+    const i64 len = side == 0 ? l : s;
+    const bool short_side = side == 1;
+    for (int a = 0; a < r; ++a) {
+      // the short side from the eigensolver is orthonormal already
+      if (short_side) break;
+      if (!sa.degen[k][a]) continue;
+      for (i64 c = 0; c < len; ++c) {
+        // candidate e_c: residual norm^2 = 1 - sum_b X[c, b]^2 over valid columns b
+        if (threadIdx.x == 0) {
+          double nn = 1.0;
+          for (int b = 0; b < r; ++b) {
+            const bool valid = (b < a) || !sa.degen[k][b];
+            coef[b] = (valid && b != a) ? X[c * r + b] : 0.0;
+            nn -= coef[b] * coef[b];
+          }
+          tmp[0] = nn;
+        }
+        __syncthreads();
+        const double nn = tmp[0];
+        if (nn > 0.5) {
+          const double inv = 1.0 / sqrt(nn);
+          for (i64 t = threadIdx.x; t < len; t += blockDim.x) {
+            double v = (t == c) ? 1.0 : 0.0;
+            for (int b = 0; b < r; ++b) v -= coef[b] * X[t * r + b];
+            X[t * r + a] = v * inv;
+          }
+          __syncthreads();
+          break;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  (void)red;
+}

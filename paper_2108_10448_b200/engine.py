@@ -1,0 +1,169 @@
+"""Python handle on the native RTCUR engine (rtcur_engine_* in include/rtcur_b200.h).
+
+The device workspace is one torch uint8 allocation (torch's caching allocator
+owns all HBM); the engine carves it.  Work is issued on the current torch
+CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as nat
+
+__all__ = ["Engine"]
+
+
+class Engine:
+    def __init__(self, shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=None):
+        import torch
+
+        self.lib = nat.load()
+        if not torch.cuda.is_available():
+            raise RuntimeError("rtcur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+        self.shape = tuple(int(d) for d in shape)
+        self.n = len(self.shape)
+        self.ranks = tuple(int(r) for r in ranks)
+        self.row_sizes = tuple(int(s) for s in row_sizes)
+        self.col_sizes = tuple(int(s) for s in col_sizes)
+        self.torch_dtype = dtype
+        self.dtype_code = nat.RTCUR_F64 if dtype == torch.float64 else nat.RTCUR_F32
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.slab = slab or (0, self.shape[0])
+        dims = nat.i64_array(self.shape)
+        rk = nat.i32_array(self.ranks)
+        rs = nat.i64_array(self.row_sizes)
+        cs = nat.i64_array(self.col_sizes)
+        self._args = (dims, rk, rs, cs)
+        ws = ctypes.c_int64()
+        xo = ctypes.c_int64()
+        xn = ctypes.c_int64()
+        nat.check(self.lib.rtcur_engine_plan(self.n, dims, rk, rs, cs, self.dtype_code, ctypes.byref(ws),
+                                             ctypes.byref(xo), ctypes.byref(xn)))
+        self.workspace = torch.empty(int(ws.value) + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        pad = (-base) % 256
+        self._ws_ptr = base + pad
+        self._ws_off = pad
+        self.xblocks_offset = int(xo.value) + pad
+        self.nblk_total = int(xn.value)
+        self.stream = torch.cuda.current_stream(self.device)
+        h = ctypes.c_void_p()
+        nat.check(self.lib.rtcur_engine_create(ctypes.byref(h), self.n, dims, rk, rs, cs, self.dtype_code,
+                                               ctypes.c_void_p(self._ws_ptr), int(ws.value), int(self.slab[0]),
+                                               int(self.slab[1]), ctypes.c_void_p(self.stream.cuda_stream)))
+        self.handle = h
+        self._x = None
+        # compact block geometry (host): core, then fiber blocks
+        n = self.n
+        self.block_shapes = [(self.row_sizes[0], int(np.prod(self.row_sizes[1:], dtype=np.int64)))]
+        self.block_shapes += [(self.shape[k], self.col_sizes[k]) for k in range(n)]
+        offs = [0]
+        for p, q in self.block_shapes:
+            offs.append(offs[-1] + p * q)
+        self.block_offsets = offs
+
+    # ------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.lib.rtcur_engine_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ steps
+    def xblocks(self):
+        """torch view of the compact sampled X blocks (dtype of X) inside the workspace."""
+        import torch
+
+        esz = 8 if self.dtype_code == nat.RTCUR_F64 else 4
+        raw = self.workspace[self.xblocks_offset:self.xblocks_offset + self.nblk_total * esz]
+        return raw.view(torch.float64 if esz == 8 else torch.float32)
+
+    def bind(self, flat):
+        """flat: contiguous CUDA tensor holding this rank's mode-1 slab."""
+        self._x = flat
+        nat.check(self.lib.rtcur_engine_bind(self.handle, ctypes.c_void_p(flat.data_ptr())))
+
+    def unbind(self):
+        self._x = None
+        nat.check(self.lib.rtcur_engine_bind(self.handle, ctypes.c_void_p(0)))
+
+    def absmax(self) -> float:
+        out = ctypes.c_double()
+        nat.check(self.lib.rtcur_engine_absmax(self.handle, ctypes.byref(out)))
+        return float(out.value)
+
+    def set_sample(self, idx):
+        rows = [np.ascontiguousarray(r, dtype=np.int64) for r in idx.rows]
+        cols = [np.ascontiguousarray(c, dtype=np.int64) for c in idx.cols]
+        rp = (nat.c_i64p * self.n)(*[r.ctypes.data_as(nat.c_i64p) for r in rows])
+        cp = (nat.c_i64p * self.n)(*[c.ctypes.data_as(nat.c_i64p) for c in cols])
+        nat.check(self.lib.rtcur_engine_set_sample(self.handle, rp, cp))
+        self._keep = (rows, cols)
+
+    def gather(self):
+        nat.check(self.lib.rtcur_engine_gather(self.handle))
+
+    def iterate(self, zeta: float, first: bool):
+        sums = (ctypes.c_double * (2 * (self.n + 1)))()
+        flags = (ctypes.c_int32 * self.n)()
+        nat.check(self.lib.rtcur_engine_iterate(self.handle, float(zeta), int(bool(first)), sums, flags))
+        s = np.frombuffer(sums, dtype=np.float64).copy()
+        return s[0::2], s[1::2], tuple(bool(f) for f in flags)
+
+    def export_blocks(self, want_s=True, want_clean=True, want_l=False):
+        """Device fp64 tensors (N_blk) of S, X - S and L_new on the compact blocks."""
+        import torch
+
+        outs = [torch.empty(self.nblk_total, dtype=torch.float64, device=self.device) if w else None
+                for w in (want_s, want_clean, want_l)]
+        ptr = [ctypes.c_void_p(o.data_ptr()) if o is not None else ctypes.c_void_p() for o in outs]
+        nat.check(self.lib.rtcur_engine_export_blocks(self.handle, *ptr))
+        return outs
+
+    def export_cur(self):
+        """Host arrays: U_k (|I|xr), sigma_k, V_k (|J|xr), A_k (d x r), G (F-order)."""
+        n = self.n
+        U = [np.zeros((self.row_sizes[k], self.ranks[k])) for k in range(n)]
+        S = [np.zeros(self.ranks[k]) for k in range(n)]
+        V = [np.zeros((self.col_sizes[k], self.ranks[k])) for k in range(n)]
+        A = [np.zeros((self.ranks[k], self.shape[k])) for k in range(n)]   # col-major d x r == row-major r x d
+        G = np.zeros(int(np.prod(self.ranks)))
+
+        def arr(lst):
+            return (nat.c_dp * n)(*[x.ctypes.data_as(nat.c_dp) for x in lst])
+
+        nat.check(self.lib.rtcur_engine_export_cur(self.handle, arr(U), arr(S), arr(V), arr(A),
+                                                    G.ctypes.data_as(nat.c_dp)))
+        return U, S, V, [a.T.copy() for a in A], G.reshape(self.ranks, order="F")
+
+    def full_output(self, zeta: float, want_L=True, want_S=True):
+        """K3 on the bound slab: (L, S, sum (x-L-S)^2, sum x^2)."""
+        import torch
+
+        nloc = (self.slab[1] - self.slab[0]) * int(np.prod(self.shape[1:], dtype=np.int64))
+        L = torch.empty(nloc, dtype=self.torch_dtype, device=self.device) if want_L else None
+        S = torch.empty(nloc, dtype=self.torch_dtype, device=self.device) if (want_S and self._x is not None) else None
+        nbytes = int(self.lib.rtcur_engine_full_scratch_bytes(self.handle))
+        tf = torch.empty(max(nbytes // 8, 1), dtype=torch.float64, device=self.device)
+        sums = (ctypes.c_double * 2)()
+        nat.check(self.lib.rtcur_engine_full_output(
+            self.handle, float(zeta), ctypes.c_void_p(L.data_ptr() if L is not None else 0),
+            ctypes.c_void_p(S.data_ptr() if S is not None else 0), ctypes.c_void_p(tf.data_ptr()), sums))
+        return L, S, float(sums[0]), float(sums[1])
+
+    # ------------------------------------------------------------ helpers
+    def split_blocks(self, flat_np):
+        """Split a compact N_blk host array into (core n-d F-order, [fiber d_k x |J_k|])."""
+        o = self.block_offsets
+        core = flat_np[o[0]:o[1]].reshape(self.row_sizes, order="F")
+        fibers = tuple(flat_np[o[k + 1]:o[k + 2]].reshape(self.block_shapes[k + 1], order="F")
+                       for k in range(self.n))
+        return core, fibers

@@ -1,0 +1,191 @@
+"""GPU parity: the sm_100a path (through librtcur_b200.so) against the
+reference's golden vectors and the CPU oracle on identical inputs and
+identical sampled index sets.
+
+Bars (north_star + reference tests): index sets bit-exact; recovered sparse
+support bit-exact; S/L blocks and errors within 1e-10 absolute in fp64
+(test_reference.py:177-214); iteration counts and convergence identical;
+singular values 1e-10 relative; full-output L/S 1e-8 (test_reference.py:217).
+fp32 inputs: compared against the fp64 oracle run on the exactly-upcast X,
+tolerance 1e-4 relative Frobenius (BASELINE north_star), support bit-exact.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cfg_kwargs, load_golden, solve_cases
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, run on the B200
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import rtcur_oracle as orc  # noqa: E402
+from paper_2108_10448_b200 import (DenseTensor, DeviceTensor, SolverConfig, cur_reconstruct_full,  # noqa: E402
+                                   full_output, hard_threshold, rtcur)
+from paper_2108_10448_b200 import _native  # noqa: E402
+from paper_2108_10448_b200.synth import baseline_sample_sizes, make_config, make_gaussian_tucker  # noqa: E402
+
+
+def _flat(a):
+    return np.asarray(a).reshape(-1, order="F")
+
+
+@pytest.mark.parametrize("case", solve_cases())
+def test_solve_matches_reference_golden(case):
+    g = load_golden(f"solve_{case}.npz")
+    shape = tuple(int(d) for d in g["shape"])
+    n = len(shape)
+    cfg = SolverConfig(**golden_cfg_kwargs(g))
+    res = rtcur(DenseTensor(g["x"], shape), cfg, record_trace=True)
+    assert res.iterations == int(g["iterations"])
+    assert res.converged == bool(g["converged"])
+    np.testing.assert_allclose(res.error_history, g["error_history"], atol=1e-10, rtol=0)
+    assert np.array_equal(np.array(res.diagnostics, dtype=bool).reshape(g["diagnostics"].shape), g["diagnostics"])
+    assert res.zeta_final == pytest.approx(float(g["zeta_final"]), rel=1e-15)
+    for t in g["trace_iters"]:
+        tr = res.trace[int(t)]
+        for m in range(n):
+            assert np.array_equal(tr["indices"].rows[m], g[f"t{t}_rows{m}"])
+            assert np.array_equal(tr["indices"].cols[m], g[f"t{t}_cols{m}"])
+        for key in ("s_core", "l_core"):
+            got, want = _flat(tr[key]), g[f"t{t}_{key}"]
+            np.testing.assert_allclose(got, want, atol=1e-10, rtol=0, err_msg=f"iter {t} {key}")
+        assert np.array_equal(_flat(tr["s_core"]) != 0, g[f"t{t}_s_core"] != 0)
+        for m in range(n):
+            np.testing.assert_allclose(tr["s_fibers"][m], g[f"t{t}_s_fib{m}"], atol=1e-10, rtol=0)
+            np.testing.assert_allclose(tr["l_fibers"][m], g[f"t{t}_l_fib{m}"], atol=1e-10, rtol=0)
+            assert np.array_equal(tr["s_fibers"][m] != 0, g[f"t{t}_s_fib{m}"] != 0)
+    # final SolveResult pieces
+    np.testing.assert_allclose(_flat(res.sparse.core), g["s_core"], atol=1e-10, rtol=0)
+    assert np.array_equal(_flat(res.sparse.core) != 0, g["s_core"] != 0)
+    np.testing.assert_allclose(res.cur.core.data, g["cur_core"], atol=1e-10, rtol=0)
+    for m in range(n):
+        assert np.array_equal(res.sparse.indices.cols[m], g[f"cols{m}"])
+        np.testing.assert_allclose(res.sparse.fibers[m], g[f"s_fib{m}"], atol=1e-10, rtol=0)
+        np.testing.assert_allclose(res.cur.fibers[m], g[f"cur_fib{m}"], atol=1e-10, rtol=0)
+        sv = res.cur.intersections[m].singular_values
+        scale = max(1.0, float(g[f"cur_sv{m}"][0]))
+        np.testing.assert_allclose(sv, g[f"cur_sv{m}"], atol=1e-10 * scale, rtol=0)
+        np.testing.assert_allclose(res.cur.intersections[m].reconstruct(), g[f"cur_rec{m}"], atol=1e-9 * scale)
+        np.testing.assert_allclose(res.cur.factors[m], g[f"cur_factor{m}"], atol=1e-8)
+    # full-output step (cli.py:237-243)
+    L, S, _ = full_output(res)
+    np.testing.assert_allclose(L.flat.cpu().numpy(), g["full_L"], atol=1e-8)
+    np.testing.assert_allclose(S.flat.cpu().numpy(), g["full_S"], atol=1e-8)
+    np.testing.assert_allclose(cur_reconstruct_full(res.cur).data, g["full_L"], atol=1e-8)
+
+
+def test_cfg0_matches_reference_summary():
+    g = load_golden("cfg0_summary.npz")
+    xf, _, _, bc = make_config(0)
+    rows, cols = baseline_sample_sizes(bc.shape, bc.ranks)
+    cfg = SolverConfig(ranks=bc.ranks, eps=bc.eps, variant=bc.variant, max_iters=100, seed=bc.seed_solver,
+                       row_sample_sizes=rows, col_sample_sizes=cols)
+    res = rtcur(DeviceTensor.from_host(xf.reshape(bc.shape, order="F")), cfg)
+    assert res.iterations == int(g["iterations"])
+    np.testing.assert_allclose(res.error_history, g["error_history"], atol=1e-10, rtol=0)
+    s_core = _flat(res.sparse.core)
+    assert np.array_equal(np.packbits(s_core != 0), g["s_core_bits"])
+    np.testing.assert_allclose(s_core[g["s_core_pos"]], g["s_core_val"], atol=1e-10)
+    for m in range(3):
+        s = _flat(res.sparse.fibers[m])
+        assert np.array_equal(np.packbits(s != 0), g[f"s_fib{m}_bits"])
+        np.testing.assert_allclose(s[g[f"s_fib{m}_pos"]], g[f"s_fib{m}_val"], atol=1e-10)
+        np.testing.assert_allclose(res.cur.intersections[m].singular_values, g[f"sv{m}"], rtol=1e-10)
+        assert np.array_equal(res.sparse.indices.cols[m], g[f"cols{m}"])
+    L, _, _ = full_output(res, want_S=False)
+    np.testing.assert_allclose(L.flat.cpu().numpy()[g["L_pos"]], g["L_val"], atol=1e-9)
+
+
+@pytest.mark.parametrize("variant", ["F", "R"])
+def test_fp32_storage_matches_fp64_oracle(variant):
+    """fp32-stored X (configs 2-4 precision): GPU computes in fp64 on the exact
+    upcast, so it must track the fp64 oracle run on the same values."""
+    shape, ranks = (40, 36, 30), (3, 3, 3)
+    xf, _, _ = make_gaussian_tucker(shape, ranks, 0.2, 10.0, seed=21, dtype=np.float32)
+    rows, cols = baseline_sample_sizes(shape, ranks)
+    kw = dict(eps=1e-5, variant=variant, max_iters=100, seed=4, row_sample_sizes=rows, col_sample_sizes=cols)
+    dev = DeviceTensor(torch.from_numpy(xf).cuda(), shape)
+    res = rtcur(dev, SolverConfig(ranks=ranks, **kw))
+    ref = orc.solve(xf.astype(np.float64), shape, ranks, **kw)
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    np.testing.assert_allclose(res.error_history, ref.error_history, atol=1e-10, rtol=0)
+    s_core = _flat(res.sparse.core)
+    r_core = _flat(ref.s_core)
+    assert np.array_equal(s_core != 0, r_core != 0)
+    assert np.linalg.norm(s_core - r_core) <= 1e-4 * max(np.linalg.norm(r_core), 1e-300)
+    for m in range(3):
+        assert np.array_equal(res.sparse.fibers[m] != 0, ref.s_fibers[m] != 0)
+        rel = np.linalg.norm(res.sparse.fibers[m] - ref.s_fibers[m]) / max(np.linalg.norm(ref.s_fibers[m]), 1e-300)
+        assert rel <= 1e-4
+    low, sp, e2, x2 = orc.full_output(xf.astype(np.float64), shape, ref.cur, ref.zeta_final)
+    L, S, rel = full_output(res)
+    Lh = L.flat.double().cpu().numpy()
+    assert np.linalg.norm(Lh - low) <= 1e-4 * np.linalg.norm(low)
+    assert rel == pytest.approx(np.sqrt(e2 / x2), rel=1e-3, abs=1e-7)
+
+
+def test_kernel_plug_hard_threshold_and_gather(kernels_golden):
+    g = kernels_golden
+    for i in range(6):
+        y = hard_threshold(g[f"ht{i}_x"], float(g[f"ht{i}_z"]))
+        assert np.array_equal(y, g[f"ht{i}_y"])
+    assert np.array_equal(hard_threshold(g["ht_edge_x"], 1.0), g["ht_edge_y"])
+    with pytest.raises(ValueError):
+        hard_threshold(np.ones(3), -0.1)
+    lib = _native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    for i in range(5):
+        flat = torch.from_numpy(g[f"gather{i}_flat"]).cuda()
+        bases = torch.from_numpy(g[f"gather{i}_bases"]).cuda()
+        stride, length = int(g[f"gather{i}_stride"]), int(g[f"gather{i}_length"])
+        out = torch.empty(length * bases.numel(), dtype=torch.float64, device="cuda")
+        _native.check(lib.rtcur_gather_columns(flat.data_ptr(), 0, flat.numel(), bases.data_ptr(), bases.numel(),
+                                               stride, length, out.data_ptr(), st))
+        got = out.cpu().numpy().reshape((length, bases.numel()), order="F")
+        assert np.array_equal(got, g[f"gather{i}_out"])
+    bad = torch.tensor([5], dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):
+        _native.check(lib.rtcur_gather_columns(flat.data_ptr(), 0, 6, bad.data_ptr(), 1, 1, 3, out.data_ptr(), st))
+
+
+def test_kernel_plug_truncated_svd_battery(kernels_golden):
+    g = kernels_golden
+    lib = _native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    i = 0
+    while f"svd{i}_m" in g:
+        m, r = g[f"svd{i}_m"], int(g[f"svd{i}_r"])
+        a = torch.from_numpy(np.asfortranarray(m).reshape(-1, order="F").copy()).cuda()
+        u = torch.empty(m.shape[0] * r, dtype=torch.float64, device="cuda")
+        v = torch.empty(m.shape[1] * r, dtype=torch.float64, device="cuda")
+        s = torch.empty(r, dtype=torch.float64, device="cuda")
+        _native.check(lib.rtcur_truncated_svd(a.data_ptr(), m.shape[0], m.shape[1], r, u.data_ptr(), s.data_ptr(),
+                                              v.data_ptr(), st))
+        U = u.cpu().numpy().reshape((m.shape[0], r), order="F")
+        V = v.cpu().numpy().reshape((m.shape[1], r), order="F")
+        S = s.cpu().numpy()
+        scale = max(float(g[f"svd{i}_s"][0]), 1.0)
+        np.testing.assert_allclose(S, g[f"svd{i}_s"], atol=1e-10 * scale, err_msg=f"case {i}")
+        np.testing.assert_allclose((U * S) @ V.T, g[f"svd{i}_rec"], atol=1e-9 * scale, err_msg=f"case {i}")
+        np.testing.assert_allclose(U.T @ U, np.eye(r), atol=1e-10, err_msg=f"case {i}")
+        np.testing.assert_allclose(V.T @ V, np.eye(r), atol=1e-10, err_msg=f"case {i}")
+        i += 1
+
+
+def test_errors_mirror_reference():
+    t = DenseTensor.zeros((5, 5, 5))
+    with pytest.raises(ValueError):
+        rtcur(t, SolverConfig(ranks=(6, 2, 2)))
+    with pytest.raises(ValueError):
+        rtcur(t, SolverConfig(ranks=(2, 2)))
+    x = np.zeros((6, 6, 6))
+    x[0, 0, 0] = np.nan
+    with pytest.raises(ValueError):
+        rtcur(DenseTensor.from_array(x), SolverConfig(ranks=(2, 2, 2), seed=1, zeta0=1.0, upsilon=10.0))
+
+
+def test_native_code_ran():
+    assert _native.launch_count() > 0
