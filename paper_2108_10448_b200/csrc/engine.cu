@@ -278,6 +278,8 @@ struct rtcur_engine {
   i64 lo, hi;
   const void* X;
   int cur;          // ring slot of the latest iterate (-1: none)
+  int sample_epoch; // bumped by every rtcur_engine_set_sample
+  int w_epoch[3];   // sample epoch each slot's W (column weights) was built for
   int prev;         // ring slot of the one before (-1: none, i.e. latest is iteration 1)
   double zeta_last;
   bool sampled;
@@ -452,6 +454,7 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
   k_colprep<<<gc, 256, 0, e->st>>>(g, ip, e->at<i64>(P.o_colR), e->at<int>(P.o_coli1), e->at<i64>(P.o_coloff));
   LAUNCH_CHECK();
   e->sampled = true;
+  e->sample_epoch++;
   return RT_OK;
 }
 
@@ -589,6 +592,16 @@ static int run_svd(rtcur_engine* e) {
   return RT_OK;
 }
 
+static int run_wcols(rtcur_engine* e, double* sto) {
+  const Plan& P = e->P;
+  const Geom& g = P.g;
+  IndexPtrs ip = make_ip(e);
+  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(P.qmax, 128), g.nblk), 128, (int)(g.gsize * 8), e->st, g, ip, sto, 0,
+             (double*)nullptr);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
 // A_k, G, W of the new iterate into state slot `dst` (threshold from st_s)
 static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst) {
   const Plan& P = e->P;
@@ -647,9 +660,9 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     }
   }
   // W for every block column
-  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(P.qmax, 128), g.nblk), 128, (int)(g.gsize * 8), e->st, g, ip, sto, 0,
-             (double*)nullptr);
-  LAUNCH_CHECK();
+  int st = run_wcols(e, sto);
+  if (st) return st;
+  e->w_epoch[dst] = e->sample_epoch;
   return RT_OK;
 }
 
@@ -664,6 +677,12 @@ extern "C" int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, dou
   while (newslot == e->cur || newslot == e->prev) ++newslot;
   CK(cudaMemsetAsync(e->ws + P.o_nonfinite, 0, 4, e->st));
   int st;
+  // RTCUR-R: the sample moved, re-evaluate the previous iterate on it
+  // (reference solver.py:330-331, _eval_blocks(lcur, idx) on the new draw)
+  if (e->cur >= 0 && e->w_epoch[e->cur] != e->sample_epoch) {
+    if ((st = run_wcols(e, e->state(e->cur)))) return st;
+    e->w_epoch[e->cur] = e->sample_epoch;
+  }
   if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false))) return st;
   if ((st = run_svd(e))) return st;
   if ((st = run_factors(e, st_s, zeta, newslot))) return st;

@@ -144,7 +144,7 @@ class DeviceTensor:
         else:
             arr = np.asarray(x)
             flat, shape = arr.reshape(-1, order="F"), arr.shape
-        t = torch.from_numpy(np.ascontiguousarray(flat))
+        t = torch.from_numpy(np.array(flat, copy=True))
         dt = dtype or (torch.float64 if t.dtype == torch.float64 else torch.float32)
         dev = device or torch.device("cuda", torch.cuda.current_device())
         return cls(t.to(device=dev, dtype=dt), shape)
