@@ -1,0 +1,341 @@
+"""bench.py -- RTCUR on B200 (BASELINE.json metric: RTCUR iters/sec & sec-to-tol).
+
+Default workload (N=1): BASELINE config 1 -- RTCUR-R, 400^3 float64, ranks
+(5,5,5), Bernoulli(0.3) outliers c=10, eps=1e-5, max_iters=100, BASELINE
+sample sizes |I|=90, |J|=2693 (seeded synthetic instance, paper_2108_10448_b200.synth).
+
+A *step* is one complete solve to tolerance (``rtcur(x, cfg)``) with X
+resident in HBM; ``value`` = iterations/sec over the K timed solves (sum of
+iterations / device time), ``ms_per_step`` = seconds-to-tolerance.  X is
+512 MB > the 126 MB L2, so no explicit flush is needed between steps.
+
+``e2e``: the same metric through the public API with HOST buffers: each step
+copies X from pinned host memory to HBM, solves, and materialises the full
+SolveResult on the host (sparse blocks, FiberCur pieces).
+
+``--impl reference`` times the CPU port of the reference loop (oracle/, the
+reference itself is Python and cannot be installed as a GPU-box baseline) on
+the host cores: one step = one steady-state RTCUR-R iteration of the same
+config.
+
+Multi-GPU (torchrun, N>1): config 1 does not shard (BASELINE runs it on one
+GPU), so N ranks run N independent replicas ("scaling": "weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RTCUR iters/sec & sec-to-tol (eps=1e-5) per config; achieved HBM GB/s vs B200 peak"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy test)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _make_problem(config: int):
+    from paper_2108_10448_b200.synth import baseline_sample_sizes, make_config
+
+    xf, low, _, bc = make_config(config)
+    rows, cols = baseline_sample_sizes(bc.shape, bc.ranks)
+    return xf, low, bc, rows, cols
+
+
+def _algorithmic_bytes(bc, rows, cols):
+    """Per-launch algorithmic bytes of each HBM-bound phase."""
+    E = 8 if bc.dtype == "f64" else 4
+    n_core = int(np.prod(rows))
+    n_fib = sum(d * c for d, c in zip(bc.shape, cols))
+    n_blk = n_core + n_fib
+    inter = sum(r * c for r, c in zip(rows, cols))
+    return {
+        "gather": 2 * E * n_blk,            # read the sampled X entries, write the compact blocks
+        "threshold": E * n_blk + 8 * inter,  # read blocks, write the fp64 intersections
+        "error": E * n_blk,                  # read blocks
+        "apass": E * n_fib,                  # read fiber blocks
+        "gpass": E * n_core,                 # read core block
+    }, n_blk
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    from oracle import rtcur_oracle as orc
+
+    orc.build_oracle_lib()
+    xf, _, bc, rows, cols = _make_problem(args.config)
+    x64 = xf.astype(np.float64)
+    n_iters = args.warmup + args.steps
+    t0 = time.perf_counter()
+    res = orc.solve(x64, bc.shape, bc.ranks, eps=bc.eps, variant=bc.variant, max_iters=n_iters, seed=bc.seed_solver,
+                    row_sample_sizes=rows, col_sample_sizes=cols)
+    wall = time.perf_counter() - t0
+    its = res.iter_times
+    timed = its[args.warmup:args.warmup + args.steps]
+    if len(timed) < args.steps:   # converged early: time the trailing iterations available
+        timed = its[-args.steps:]
+    value = len(timed) / sum(timed)
+    cores = os.cpu_count()
+    line = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "impl": "reference", "n_gpus": world,
+        "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * sum(timed) / len(timed),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": bc.dtype,
+        "data": "synthetic (seeded, paper_2108_10448_b200.synth)",
+        "config": _config_dict(bc, rows, cols, world),
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
+                         "sample": f"RTCUR-{bc.variant} iterations {args.warmup + 1}..{args.warmup + len(timed)} of "
+                                   f"config {bc.index} on the host (numpy/OpenBLAS all cores; einsum and SVD "
+                                   f"single-threaded as in the reference)"},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_dict(bc, rows, cols, world):
+    return {"workload": f"config{bc.index}: RTCUR-{bc.variant} {'x'.join(map(str, bc.shape))} {bc.dtype} ranks "
+                        f"{tuple(bc.ranks)} alpha={bc.alpha} c={bc.c} eps={bc.eps} max_iters=100",
+            "shape": list(bc.shape), "ranks": list(bc.ranks), "variant": bc.variant, "row_samples": list(rows),
+            "col_samples": list(cols), "l2": "inputs larger than L2 (X = %.0f MB > 126 MB)" % (
+                np.prod(bc.shape) * (8 if bc.dtype == "f64" else 4) / 1e6),
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
+def _cpu_baseline(bc, rows, cols, xf, budget_iters=2):
+    from oracle import rtcur_oracle as orc
+
+    orc.build_oracle_lib()
+    res = orc.solve(xf.astype(np.float64), bc.shape, bc.ranks, eps=bc.eps, variant=bc.variant,
+                    max_iters=budget_iters, seed=bc.seed_solver, row_sample_sizes=rows, col_sample_sizes=cols)
+    t = res.iter_times[-1]
+    return {"value": 1.0 / t, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"iteration {len(res.iter_times)} (steady state, both _eval_blocks) of a config-{bc.index} "
+                      f"RTCUR-{bc.variant} solve by the oracle port on the host; setup (sample+gather) "
+                      f"{res.timings['gather'] + res.timings['sample']:.2f}s excluded"}
+
+
+def run_b200(args):
+    import torch
+
+    world, rank, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_2108_10448_b200 import DeviceTensor, SolverConfig, rtcur
+    from paper_2108_10448_b200 import _native
+    from paper_2108_10448_b200 import solver as solver_mod
+
+    xf, _, bc, rows, cols = _make_problem(args.config)
+    dt = torch.float64 if bc.dtype == "f64" else torch.float32
+    host = torch.from_numpy(xf).to(dt)
+    x_dev = DeviceTensor(host.cuda(), bc.shape)
+    cfg = SolverConfig(ranks=bc.ranks, eps=bc.eps, gamma=0.7, variant=bc.variant, max_iters=100,
+                       seed=bc.seed_solver + 1000 * rank, row_sample_sizes=rows, col_sample_sizes=cols)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        rtcur(x_dev, cfg)
+    torch.cuda.synchronize()
+
+    # ---------------- device-resident timed region
+    solver_mod.PROFILE = True
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = _native.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    iters, conv, phase_ms, phase_n = 0, True, {}, {}
+    for _ in range(args.steps):
+        res = rtcur(x_dev, cfg)
+        iters += res.iterations
+        conv &= res.converged
+        for k, v in res.timings["device_ms"].items():
+            phase_ms[k] = phase_ms.get(k, 0.0) + v
+            phase_n[k] = phase_n.get(k, 0) + res.timings["device_launches"][k]
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _native.launch_count() - l0
+    clk = clocks.stop()
+    solver_mod.PROFILE = False
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    it = torch.tensor([iters], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(it, op=torch.distributed.ReduceOp.SUM)
+    ms_max = float(t.item())
+    value = float(it.item()) / (ms_max / 1e3)
+
+    # ---------------- e2e through the public API with host buffers
+    pinned = host.pin_memory()
+    x_buf = torch.empty_like(x_dev.flat)
+    e2e_iters, d2h = 0, 0
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x_buf.copy_(pinned, non_blocking=True)
+        res = rtcur(DeviceTensor(x_buf, bc.shape), cfg)
+        e2e_iters += res.iterations
+        sc = res.sparse.core
+        sf = res.sparse.fibers
+        core = res.cur.core
+        fib = res.cur.fibers
+        inters = res.cur.intersections
+        facs = res.cur.factors
+        d2h = (sc.nbytes + sum(f.nbytes for f in sf) + core.data.nbytes + sum(f.nbytes for f in fib)
+               + sum(i.u.nbytes + i.v.nbytes + i.singular_values.nbytes for i in inters)
+               + sum(f.nbytes for f in facs) + 8 * res.iterations)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    ie = torch.tensor([e2e_iters], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(ie, op=torch.distributed.ReduceOp.SUM)
+    e2e_value = float(ie.item()) / float(te.item())
+
+    # ---------------- roofline of the dominant HBM-bound kernel
+    peak, peak_src = _peaks()
+    alg, n_blk = _algorithmic_bytes(bc, rows, cols)
+    total_dev = sum(phase_ms.values())
+    hbm_phases = {k: v for k, v in phase_ms.items() if k in alg and phase_n.get(k)}
+    dom = max(hbm_phases, key=hbm_phases.get)
+    per_launch_ms = phase_ms[dom] / phase_n[dom]
+    achieved = alg[dom] / (per_launch_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": {"threshold": "k_block_pass (threshold)", "error": "k_block_pass (error)",
+                                        "gather": "k_gather", "apass": "k_apass", "gpass": "k_gpass"}[dom],
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "alg_bytes_per_launch": alg[dom], "launch_us": 1e3 * per_launch_ms, "peak_source": peak_src,
+            "share_of_device_time": phase_ms[dom] / total_dev if total_dev else None}
+    phases = {k: {"ms_per_step": v / args.steps, "launches_per_step": phase_n[k] / args.steps,
+                  "share": v / total_dev if total_dev else None}
+              for k, v in sorted(phase_ms.items(), key=lambda kv: -kv[1]) if phase_n.get(k)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = _cpu_baseline(bc, rows, cols, xf)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": bc.dtype,
+            "data": "synthetic (seeded, paper_2108_10448_b200.synth)",
+            "config": _config_dict(bc, rows, cols, world),
+            "sec_to_tol": ms_max / args.steps / 1e3, "iterations_per_solve": iters / args.steps,
+            "converged": bool(conv), "gpu_launches": int(launches),
+            "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(host.numel() * host.element_size()),
+                    "d2h_bytes_per_step": int(d2h), "sec_per_solve": e2e_s / args.steps},
+            "roofline": roof, "phases": phases, "clocks": clk, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -111,6 +111,14 @@ int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_dev, void* S_
 /* bytes of the tf_dev scratch rtcur_engine_full_output needs */
 int64_t rtcur_engine_full_scratch_bytes(rtcur_engine* e);
 
+/* Per-phase device timing with CUDA events on the engine's stream (for the
+ * bench roofline).  Phases: 0 absmax (K0), 1 index prep, 2 gather, 3 threshold
+ * pass (K1), 4 Gram, 5 eigensolver, 6 SVD post, 7 A pass, 8 G pass, 9 W
+ * columns, 10 error pass, 11 export, 12 full output (K3).  nphase >= 13. */
+#define RTCUR_NPHASE 13
+int rtcur_engine_profile(rtcur_engine* e, int on);
+int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* counts, int nphase, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -358,6 +358,7 @@ class OracleResult:
     zeta_final: float
     timings: dict
     trace: list = field(default_factory=list)
+    iter_times: list = field(default_factory=list)
 
 
 def inf_norm(flat: np.ndarray) -> float:
@@ -407,11 +408,12 @@ def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, 
 
     lcur = None
     lblocks = None
-    history, flags, trace = [], [], []
+    history, flags, trace, iter_times = [], [], [], []
     converged = False
     s_core = np.zeros_like(x_core)
     s_fibers = [np.zeros_like(f) for f in x_fibers]
     for k in range(1, max_iters + 1):
+        t_iter = time.perf_counter()
         if variant == "R" and k >= 2:
             t0 = time.perf_counter()
             idx = draw_sample_indices(shape, rows, cols, rng)
@@ -448,6 +450,7 @@ def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, 
         err = sampled_relative_error(e_core, e_fibers, x_core, x_fibers)
         timings["error"] += time.perf_counter() - t0
         history.append(err)
+        iter_times.append(time.perf_counter() - t_iter)
         if record_trace:
             trace.append({"iteration": k, "zeta": zeta, "indices": idx, "s_core": s_core,
                           "s_fibers": tuple(s_fibers), "l_core": l_core,
@@ -461,7 +464,8 @@ def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, 
     timings["loop"] = time.perf_counter() - t_loop
     return OracleResult(cur=lcur, s_core=s_core, s_fibers=tuple(s_fibers), indices=idx,
                         error_history=tuple(history), iterations=len(history), converged=converged,
-                        diagnostics=tuple(flags), zeta_final=zeta, timings=timings, trace=trace)
+                        diagnostics=tuple(flags), zeta_final=zeta, timings=timings, trace=trace,
+                        iter_times=iter_times)
 
 
 def full_output(x_flat: np.ndarray, shape, cur: OracleCur, zeta_final: float):

@@ -23,8 +23,10 @@ EXPORTED = (
     "rtcur_truncated_svd", "rtcur_engine_plan", "rtcur_engine_create", "rtcur_engine_destroy", "rtcur_engine_bind",
     "rtcur_engine_absmax", "rtcur_engine_set_sample", "rtcur_engine_gather", "rtcur_engine_iterate",
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
-    "rtcur_engine_full_scratch_bytes",
+    "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_read",
 )
+PHASES = ("absmax", "prep", "gather", "threshold", "gram", "eig", "svdpost", "apass", "gpass", "wcols", "error",
+          "export", "full")
 
 _lib = None
 
@@ -71,6 +73,8 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_full_output.argtypes = [c_vp, ctypes.c_double, c_vp, c_vp, c_vp, c_dp]
     lib.rtcur_engine_full_scratch_bytes.argtypes = [c_vp]
     lib.rtcur_engine_full_scratch_bytes.restype = c_i64
+    lib.rtcur_engine_profile.argtypes = [c_vp, ctypes.c_int]
+    lib.rtcur_engine_profile_read.argtypes = [c_vp, c_dp, c_i64p, ctypes.c_int, ctypes.c_int]
     for name in EXPORTED:
         if not hasattr(lib, name):
             raise NativeUnavailable(f"{path} does not export {name}")

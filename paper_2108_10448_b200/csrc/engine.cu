@@ -271,6 +271,10 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   return RT_OK;
 }
 
+// profiled phases (index into rtcur_engine_profile_read outputs)
+enum { PH_ABSMAX = 0, PH_PREP, PH_GATHER, PH_THRESH, PH_GRAM, PH_EIG, PH_SVDPOST, PH_APASS, PH_GPASS, PH_WCOLS,
+       PH_ERROR, PH_EXPORT, PH_FULL, RT_NPHASE };
+
 struct rtcur_engine {
   Plan P;
   char* ws;
@@ -287,9 +291,53 @@ struct rtcur_engine {
   int* h_flags;
   i64* h_idx;        // pinned staging for index upload
   i64 h_idx_len;
+  // optional per-phase CUDA-event timing (rtcur_engine_profile)
+  bool prof_on;
+  double prof_ms[RT_NPHASE];
+  long long prof_cnt[RT_NPHASE];
+  std::vector<cudaEvent_t>* prof_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* prof_pending;
+  cudaEvent_t prof_open[RT_NPHASE];
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
 };
+
+static cudaEvent_t prof_event(rtcur_engine* e) {
+  if (!e->prof_pool->empty()) {
+    cudaEvent_t ev = e->prof_pool->back();
+    e->prof_pool->pop_back();
+    return ev;
+  }
+  cudaEvent_t ev;
+  cudaEventCreate(&ev);
+  return ev;
+}
+static void prof_begin(rtcur_engine* e, int ph) {
+  if (!e->prof_on) return;
+  cudaEvent_t ev = prof_event(e);
+  cudaEventRecord(ev, e->st);
+  e->prof_open[ph] = ev;
+}
+static void prof_end(rtcur_engine* e, int ph) {
+  if (!e->prof_on || !e->prof_open[ph]) return;
+  cudaEvent_t ev = prof_event(e);
+  cudaEventRecord(ev, e->st);
+  e->prof_pending->push_back({ph, {e->prof_open[ph], ev}});
+  e->prof_open[ph] = nullptr;
+}
+// after a stream synchronisation: fold the recorded intervals into the totals
+static void prof_flush(rtcur_engine* e) {
+  for (auto& p : *e->prof_pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
+      e->prof_ms[p.first] += ms;
+      e->prof_cnt[p.first] += 1;
+    }
+    e->prof_pool->push_back(p.second.first);
+    e->prof_pool->push_back(p.second.second);
+  }
+  e->prof_pending->clear();
+}
 
 static IndexPtrs make_ip(const rtcur_engine* e) {
   const Plan& P = e->P;
@@ -344,6 +392,8 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->lo = slab_lo;
   e->hi = slab_hi;
   e->cur = e->prev = -1;
+  e->prof_pool = new std::vector<cudaEvent_t>();
+  e->prof_pending = new std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>();
   cudaError_t ce = cudaMallocHost(&e->h_pinned, 4096);
   if (ce != cudaSuccess) { delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   e->h_flags = reinterpret_cast<int*>(e->h_pinned + 256);
@@ -379,6 +429,17 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   cudaStreamSynchronize(e->st);
   if (e->h_pinned) cudaFreeHost(e->h_pinned);
   if (e->h_idx) cudaFreeHost(e->h_idx);
+  if (e->prof_pending) {
+    for (auto& p : *e->prof_pending) {
+      cudaEventDestroy(p.second.first);
+      cudaEventDestroy(p.second.second);
+    }
+    delete e->prof_pending;
+  }
+  if (e->prof_pool) {
+    for (auto ev : *e->prof_pool) cudaEventDestroy(ev);
+    delete e->prof_pool;
+  }
   delete e;
   return RT_OK;
 }
@@ -396,13 +457,16 @@ extern "C" int rtcur_engine_absmax(rtcur_engine* e, double* out) {
   for (int m = 1; m < P.g.n; ++m) nloc *= P.g.dim[m];
   unsigned long long* d = e->at<unsigned long long>(P.o_absmax);
   CK(cudaMemsetAsync(d, 0, 8, e->st));
+  prof_begin(e, PH_ABSMAX);
   int nsm = 148;
   const int grid = nsm * 8;
   if (P.dtype == 0) k_absmax<double><<<grid, 256, 0, e->st>>>((const double*)e->X, nloc, d);
   else k_absmax<float><<<grid, 256, 0, e->st>>>((const float*)e->X, nloc, d);
   LAUNCH_CHECK();
+  prof_end(e, PH_ABSMAX);
   CK(cudaMemcpyAsync(e->h_pinned, d, 8, cudaMemcpyDeviceToHost, e->st));
   CK(cudaStreamSynchronize(e->st));
+  prof_flush(e);
   unsigned long long bits;
   memcpy(&bits, e->h_pinned, 8);
   double v;
@@ -447,12 +511,14 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
     CK(cudaMemcpyAsync(e->ws + P.o_cols[m], e->h_idx + offs[g.n + m], g.ncols[m] * 8, cudaMemcpyHostToDevice, e->st));
   }
   IndexPtrs ip = make_ip(e);
+  prof_begin(e, PH_PREP);
   dim3 gr((unsigned)std::min<i64>(cdiv(P.dmax, 256), 1024), g.n);
   k_rowpos<<<gr, 256, 0, e->st>>>(g, ip, e->at<int>(P.o_rowpos));
   LAUNCH_CHECK();
   dim3 gc((unsigned)std::min<i64>(cdiv(P.qmax, 256), 4096), g.nblk);
   k_colprep<<<gc, 256, 0, e->st>>>(g, ip, e->at<i64>(P.o_colR), e->at<int>(P.o_coli1), e->at<i64>(P.o_coloff));
   LAUNCH_CHECK();
+  prof_end(e, PH_PREP);
   e->sampled = true;
   e->sample_epoch++;
   return RT_OK;
@@ -463,14 +529,16 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   if (!e->sampled) return fail(RT_ERR_VALUE, "no sample set");
   const Plan& P = e->P;
   IndexPtrs ip = make_ip(e);
+  prof_begin(e, PH_GATHER);
   k_gather<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, e->X, P.dtype, e->lo, e->hi,
                                                               e->ws + P.o_xb);
   LAUNCH_CHECK();
+  prof_end(e, PH_GATHER);
   return RT_OK;
 }
 
 static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_e, double zeta, bool with_M,
-                          double* s_out, double* c_out, double* l_out, bool sums) {
+                          double* s_out, double* c_out, double* l_out, bool sums, int phase) {
   const Plan& P = e->P;
   IndexPtrs ip = make_ip(e);
   PassArgs a;
@@ -491,8 +559,10 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
     a.counter = e->at<unsigned int>(P.o_counters);
   }
   a.nonfinite = e->at<int>(P.o_nonfinite);
+  prof_begin(e, phase);
   k_block_pass<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, a);
   LAUNCH_CHECK();
+  prof_end(e, phase);
   return RT_OK;
 }
 
@@ -544,6 +614,7 @@ static int run_svd(rtcur_engine* e) {
   ga.part = e->at<double>(P.o_gpart);
   ga.maxchunks = P.gram_maxchunks;
   ga.maxpairs = P.gram_maxpairs;
+  prof_begin(e, PH_GRAM);
   k_gram_tiles<<<dim3(P.gram_maxpairs, P.gram_maxchunks, n), 256, 0, e->st>>>(ga);
   LAUNCH_CHECK();
   {
@@ -551,6 +622,7 @@ static int run_svd(rtcur_engine* e) {
     k_gram_reduce<<<dim3((unsigned)std::min<i64>(cdiv(npk, 256), 512), n), 256, 0, e->st>>>(ga);
     LAUNCH_CHECK();
   }
+  prof_end(e, PH_GRAM);
   EigArgs ea;
   memset(&ea, 0, sizeof(ea));
   ea.n = n;
@@ -565,8 +637,11 @@ static int run_svd(rtcur_engine* e) {
     ea.nb[m] = P.nb[m];
     esm = std::max(esm, eig_smem_bytes(P, m));
   }
+  prof_begin(e, PH_EIG);
   k_eig<<<n, 1024, esm, e->st>>>(ea);
   LAUNCH_CHECK();
+  prof_end(e, PH_EIG);
+  prof_begin(e, PH_SVDPOST);
   SvdArgs sa = make_svd_args(e);
   unsigned int* hcnt = e->at<unsigned int>(P.o_counters) + 16;
   const unsigned gz = (unsigned)cdiv(P.lmax, 256);
@@ -589,6 +664,7 @@ static int run_svd(rtcur_engine* e) {
   LAUNCH_CHECK();
   k_complete<<<n, 256, 0, e->st>>>(sa);
   LAUNCH_CHECK();
+  prof_end(e, PH_SVDPOST);
   return RT_OK;
 }
 
@@ -596,9 +672,11 @@ static int run_wcols(rtcur_engine* e, double* sto) {
   const Plan& P = e->P;
   const Geom& g = P.g;
   IndexPtrs ip = make_ip(e);
+  prof_begin(e, PH_WCOLS);
   DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(P.qmax, 128), g.nblk), 128, (int)(g.gsize * 8), e->st, g, ip, sto, 0,
              (double*)nullptr);
   LAUNCH_CHECK();
+  prof_end(e, PH_WCOLS);
   return RT_OK;
 }
 
@@ -624,10 +702,13 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   aa.maxchunks = P.a_maxchunks;
   aa.dmax = P.dmax;
   aa.st_out = sto;
+  prof_begin(e, PH_APASS);
   DISPATCH_R(P.rb, k_apass, dim3((unsigned)cdiv(P.dmax, 256), P.a_maxchunks, n), 256, 0, e->st, g, ip, aa);
   LAUNCH_CHECK();
   k_areduce<<<dim3((unsigned)std::min<i64>(cdiv(P.dmax * P.rmax, 256), 1024), n), 256, 0, e->st>>>(g, aa);
   LAUNCH_CHECK();
+  prof_end(e, PH_APASS);
+  prof_begin(e, PH_GPASS);
   // G = clean_core x_1 U_1^T x_2 ... x_n U_n^T
   GPassArgs gp;
   memset(&gp, 0, sizeof(gp));
@@ -659,6 +740,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
       in = out;
     }
   }
+  prof_end(e, PH_GPASS);
   // W for every block column
   int st = run_wcols(e, sto);
   if (st) return st;
@@ -683,14 +765,16 @@ extern "C" int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, dou
     if ((st = run_wcols(e, e->state(e->cur)))) return st;
     e->w_epoch[e->cur] = e->sample_epoch;
   }
-  if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false))) return st;
+  if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false, PH_THRESH))) return st;
   if ((st = run_svd(e))) return st;
   if ((st = run_factors(e, st_s, zeta, newslot))) return st;
-  if ((st = run_block_pass(e, st_s, e->state(newslot), zeta, false, nullptr, nullptr, nullptr, true))) return st;
+  if ((st = run_block_pass(e, st_s, e->state(newslot), zeta, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
+    return st;
   CK(cudaMemcpyAsync(e->h_pinned, e->ws + P.o_sums, 2 * P.g.nblk * 8, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(e->h_flags, e->ws + P.o_flags, n * 4, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(e->h_flags + 16, e->ws + P.o_nonfinite, 4, cudaMemcpyDeviceToHost, e->st));
   CK(cudaStreamSynchronize(e->st));
+  prof_flush(e);
   if (e->h_flags[16]) return fail(RT_ERR_VALUE, "truncated_svd input contains non-finite entries");
   if (sums) memcpy(sums, e->h_pinned, 2 * P.g.nblk * 8);
   if (flags) memcpy(flags, e->h_flags, n * 4);
@@ -704,9 +788,10 @@ extern "C" int rtcur_engine_export_blocks(rtcur_engine* e, double* s_blocks, dou
   if (!e || e->cur < 0) return fail(RT_ERR_VALUE, "no iterate to export");
   const double* st_s = e->prev >= 0 ? e->state(e->prev) : nullptr;
   int st = run_block_pass(e, st_s, l_blocks ? e->state(e->cur) : nullptr, e->zeta_last, false, s_blocks,
-                          clean_blocks, l_blocks, false);
+                          clean_blocks, l_blocks, false, PH_EXPORT);
   if (st) return st;
   CK(cudaStreamSynchronize(e->st));
+  prof_flush(e);
   return RT_OK;
 }
 
@@ -744,9 +829,11 @@ extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_de
   double* sto = e->state(e->cur);
   i64 ncols = 1;
   for (int m = 1; m < g.n; ++m) ncols *= g.dim[m];
+  prof_begin(e, PH_WCOLS);
   DISPATCH_R(rbucket(g.rank[0]), k_wcols, dim3((unsigned)cdiv(ncols, 128), 1), 128, (int)(g.gsize * 8), e->st, g, ip,
              sto, 1, tf_dev);
   LAUNCH_CHECK();
+  prof_end(e, PH_WCOLS);
   FullArgs fa;
   memset(&fa, 0, sizeof(fa));
   fa.X = e->X;   // may be null: reconstruction only (x = 0)
@@ -765,12 +852,36 @@ extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_de
   fa.sums = e->at<double>(P.o_sums);
   fa.counter = e->at<unsigned int>(P.o_counters) + 32;
   const int grid = 148 * 8;
+  prof_begin(e, PH_FULL);
   if (P.dtype == 0) k_full<double><<<grid, 256, 0, e->st>>>(fa);
   else k_full<float><<<grid, 256, 0, e->st>>>(fa);
   LAUNCH_CHECK();
+  prof_end(e, PH_FULL);
   CK(cudaMemcpyAsync(e->h_pinned, fa.sums, 16, cudaMemcpyDeviceToHost, e->st));
   CK(cudaStreamSynchronize(e->st));
+  prof_flush(e);
   if (sums) memcpy(sums, e->h_pinned, 16);
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_profile(rtcur_engine* e, int on) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  CK(cudaStreamSynchronize(e->st));
+  prof_flush(e);
+  e->prof_on = on != 0;
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* counts, int nphase, int reset) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  CK(cudaStreamSynchronize(e->st));
+  prof_flush(e);
+  for (int i = 0; i < nphase && i < RT_NPHASE; ++i) {
+    if (ms) ms[i] = e->prof_ms[i];
+    if (counts) counts[i] = e->prof_cnt[i];
+  }
+  if (reset)
+    for (int i = 0; i < RT_NPHASE; ++i) { e->prof_ms[i] = 0.0; e->prof_cnt[i] = 0; }
   return RT_OK;
 }
 

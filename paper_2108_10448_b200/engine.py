@@ -159,6 +159,17 @@ class Engine:
             ctypes.c_void_p(S.data_ptr() if S is not None else 0), ctypes.c_void_p(tf.data_ptr()), sums))
         return L, S, float(sums[0]), float(sums[1])
 
+    def profile(self, on: bool = True):
+        nat.check(self.lib.rtcur_engine_profile(self.handle, int(bool(on))))
+
+    def profile_read(self, reset: bool = False):
+        """{phase: (total_ms, launches)} of the CUDA-event phase timers."""
+        k = len(nat.PHASES)
+        ms = (ctypes.c_double * k)()
+        cnt = (ctypes.c_int64 * k)()
+        nat.check(self.lib.rtcur_engine_profile_read(self.handle, ms, cnt, k, int(bool(reset))))
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(nat.PHASES)}
+
     # ------------------------------------------------------------ helpers
     def split_blocks(self, flat_np):
         """Split a compact N_blk host array into (core n-d F-order, [fiber d_k x |J_k|])."""

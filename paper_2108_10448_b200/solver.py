@@ -37,6 +37,10 @@ __all__ = ["SolverConfig", "SparseEstimate", "SolveResult", "TensorAccessor", "D
 
 RANK_DEFICIENCY_RTOL = 1e-8  # solver.py:64 (applied on device, k_svd_fin2)
 
+# When True, rtcur() records per-phase device times (CUDA events on the solve's
+# stream) into timings["device_ms"] / timings["device_launches"] (bench.py).
+PROFILE = False
+
 
 @dataclass(frozen=True)
 class SolverConfig:
@@ -342,6 +346,8 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
             raise ValueError(f"mode {m}: rank {r} exceeds sample sizes (|rows|={rs}, |cols|={cs})")
 
     eng = Engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype)
+    if PROFILE:
+        eng.profile(True)
     src.attach(eng)
     t0 = time.perf_counter()
     eng.set_sample(idx)
@@ -380,4 +386,8 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
             break
     timings["loop"] = time.perf_counter() - t_loop
     timings["total"] = time.perf_counter() - t_start
+    if PROFILE:
+        ph = eng.profile_read(reset=True)
+        timings["device_ms"] = {k: v[0] for k, v in ph.items()}
+        timings["device_launches"] = {k: v[1] for k, v in ph.items()}
     return _make_result(eng, src, idx, cfg, history, flags, timings, zeta, converged, trace)
