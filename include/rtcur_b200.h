@@ -93,6 +93,10 @@ int rtcur_engine_gather(rtcur_engine* e);
  * sums (host, 2*(n+1)): per block sum((x-L-S)^2), sum(x^2) of the NEW iterate;
  * flags (host, n): rank-deficiency flags of the new intersections. */
 int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, double* sums, int* flags);
+/* the same split in two: enqueue the iteration on the engine's stream and return at once,
+ * then wait for it (lets the host draw the next RTCUR-R sample while the GPU works) */
+int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first);
+int rtcur_engine_iterate_wait(rtcur_engine* e, double* sums, int* flags);
 
 /* Export (device outputs, caller-allocated, fp64), for the iterate of the last
  * rtcur_engine_iterate call:

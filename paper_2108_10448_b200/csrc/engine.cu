@@ -58,6 +58,26 @@ static int fail(int code, const std::string& msg) {
 static inline i64 cdiv(i64 a, i64 b) { return (a + b - 1) / b; }
 static inline i64 align256(i64 x) { return (x + 255) & ~(i64)255; }
 
+// full-storage tridiagonalisation when it fits (faster), else packed
+static int eig_pick_full(int s, int r) { return eig_smem_doubles(s, r, 1, 1) <= EIG_SMEM_DOUBLES ? 1 : 0; }
+static int eig_pick_nb(int s, int r) {
+  const int full = eig_pick_full(s, r);
+  int nb = 0;
+  for (int b = 1; b <= r; ++b)
+    if (eig_smem_doubles(s, r, b, full) <= EIG_SMEM_DOUBLES) nb = b;
+  return nb;
+}
+
+// k_wcols scratch: the other modes' A rows per thread (max over target modes)
+static int wcols_rows_per_thread(const Geom& g) {
+  int tot = 0;
+  for (int m = 0; m < g.n; ++m) tot += g.rank[m];
+  int mn = g.rank[0];
+  for (int m = 0; m < g.n; ++m) mn = std::min(mn, g.rank[m]);
+  return std::max(1, tot - mn);
+}
+static int wcols_smem(const Geom& g) { return (int)((g.gsize + 128 * wcols_rows_per_thread(g)) * 8); }
+
 static int rbucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32; }
 
 #define DISPATCH_R(RB, KERNEL, GRID, BLOCK, SMEM, STREAM, ...)                     \
@@ -80,7 +100,7 @@ struct Plan {
   int tall[RT_MAX_MODES];
   int nb[RT_MAX_MODES];
   i64 col_off[RT_MAX_BLOCKS + 1];
-  int gram_maxchunks, gram_maxpairs;
+  int gram_maxchunks, gram_maxpairs, gram_cl;
   int a_chunk, a_maxchunks;
   i64 dmax, lmax, smax, qmax;
   i64 g_tmp;         // doubles per G temp buffer
@@ -91,7 +111,7 @@ struct Plan {
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
       o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_apart, o_gt0, o_gt1, o_bpart, o_sums,
-      o_fpart;
+      o_fpart, o_dbg;
   i64 total;
 };
 
@@ -182,7 +202,8 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   i64 t = 0;
   for (int b = 0; b < g.nblk; ++b) {
     tm.first[b] = t;
-    t += cdiv(g.blk[b].P * g.blk[b].Q, tm.tile);
+    tm.cpt[b] = std::max<i64>(1, tm.tile / g.blk[b].P);
+    t += cdiv(g.blk[b].Q, tm.cpt[b]);
   }
   tm.first[g.nblk] = t;
   P.col_off[0] = 0;
@@ -194,23 +215,35 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.lmax = 1;
   P.smax = 1;
   P.qmax = 1;
+  // split-K so that the Gram tiles fill ~4 waves of 148 SMs
+  {
+    int pairs_tot = 0;
+    i64 lm = 1;
+    for (int m = 0; m < n; ++m) {
+      const int nt = (int)cdiv(P.s[m], GRAM_T);
+      pairs_tot += nt * (nt + 1) / 2;
+      lm = std::max(lm, P.l[m]);
+    }
+    const i64 want = std::max<i64>(1, cdiv(4 * 148, pairs_tot));
+    P.gram_cl = (int)std::max<i64>(GRAM_KS, cdiv(cdiv(lm, want), GRAM_KS) * GRAM_KS);
+  }
   for (int m = 0; m < n; ++m) {
     const int nt = (int)cdiv(P.s[m], GRAM_T);
     P.gram_maxpairs = std::max(P.gram_maxpairs, nt * (nt + 1) / 2);
-    P.gram_maxchunks = std::max(P.gram_maxchunks, (int)cdiv(P.l[m], GRAM_CL));
+    P.gram_maxchunks = std::max(P.gram_maxchunks, (int)cdiv(P.l[m], P.gram_cl));
     P.dmax = std::max(P.dmax, (i64)dims[m]);
     P.lmax = std::max(P.lmax, P.l[m]);
     P.smax = std::max(P.smax, P.s[m]);
-    // inverse-iteration batch: vectors whose LU fits next to the packed matrix
-    const i64 npk = P.s[m] * (P.s[m] + 1) / 2;
-    int nb = (int)std::max<i64>(1, std::min<i64>(ranks[m], std::max<i64>(npk, 5 * P.s[m] * 4) / (5 * P.s[m])));
+    // inverse-iteration batch: as many LU factorisations as fit in 227 KB next to K and E
+    int nb = eig_pick_nb((int)P.s[m], ranks[m]);
+    if (nb < 1) return fail(RT_ERR_UNSUPPORTED, "intersection too large for the shared-memory eigensolver");
     P.nb[m] = nb;
   }
   for (int b = 0; b < g.nblk; ++b) P.qmax = std::max(P.qmax, g.blk[b].Q);
-  P.a_chunk = 128;
+  P.a_chunk = APASS_CH;
   P.a_maxchunks = 1;
   for (int m = 0; m < n; ++m) P.a_maxchunks = std::max(P.a_maxchunks, (int)cdiv(col_sizes[m], P.a_chunk));
-  P.hchunk = 256;
+  P.hchunk = HG_CH;
   P.h_maxchunks = (int)cdiv(P.lmax, P.hchunk);
   // G temporaries: largest partially contracted core
   {
@@ -243,11 +276,10 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   for (int m = 0; m < n; ++m) {
     const i64 s = P.s[m];
     P.o_K[m] = take(s * (s + 1) / 2 * 8);
-    P.o_hv[m] = take((s * (s - 1) / 2 + s) * 8);
     P.o_E[m] = take(s * ranks[m] * 8);
     P.o_lam[m] = take(ranks[m] * 8);
     P.o_Z[m] = take(P.l[m] * ranks[m] * 8);
-    P.o_hpart[m] = take((i64)cdiv(P.l[m], P.hchunk) * ranks[m] * (ranks[m] + 1) / 2 * 8);
+    P.o_hpart[m] = take((i64)cdiv(P.l[m], HG_CH) * ranks[m] * (ranks[m] + 1) / 2 * 8);
     P.o_H[m] = take(ranks[m] * ranks[m] * 8);
     P.o_Q[m] = take(ranks[m] * ranks[m] * 8);
     P.o_U[m] = take(row_sizes[m] * ranks[m] * 8);
@@ -267,6 +299,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_bpart = take(tm.first[g.nblk] * 2 * 8);
   P.o_sums = take(2 * g.nblk * 8);
   P.o_fpart = take(148 * 8 * 2 * 8);
+  P.o_dbg = take(8 * RT_MAX_MODES * 8);
   P.total = o;
   return RT_OK;
 }
@@ -284,6 +317,8 @@ struct rtcur_engine {
   int cur;          // ring slot of the latest iterate (-1: none)
   int sample_epoch; // bumped by every rtcur_engine_set_sample
   int w_epoch[3];   // sample epoch each slot's W (column weights) was built for
+  bool pending;     // an iterate_async awaits its iterate_wait
+  cudaEvent_t done; // recorded after the iteration's result copies
   int prev;         // ring slot of the one before (-1: none, i.e. latest is iteration 1)
   double zeta_last;
   bool sampled;
@@ -358,9 +393,7 @@ static IndexPtrs make_ip(const rtcur_engine* e) {
 }
 
 static int eig_smem_bytes(const Plan& P, int m) {
-  const i64 s = P.s[m];
-  const i64 region0 = std::max<i64>(s * (s + 1) / 2, 5 * s * P.nb[m]);
-  return (int)((region0 + 5 * s + 32) * 8);
+  return (int)(eig_smem_doubles((int)P.s[m], P.g.rank[m], P.nb[m], eig_pick_full((int)P.s[m], P.g.rank[m])) * 8);
 }
 
 extern "C" int rtcur_engine_plan(int n, const int64_t* dims, const int32_t* ranks, const int64_t* row_sizes,
@@ -393,6 +426,10 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->hi = slab_hi;
   e->cur = e->prev = -1;
   e->prof_pool = new std::vector<cudaEvent_t>();
+  if (cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming) != cudaSuccess) {
+    delete e;
+    return fail(RT_ERR_CUDA, "cudaEventCreate");
+  }
   e->prof_pending = new std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>();
   cudaError_t ce = cudaMallocHost(&e->h_pinned, 4096);
   if (ce != cudaSuccess) { delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
@@ -410,12 +447,12 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   int maxe = 0;
   for (int m = 0; m < n; ++m) maxe = std::max(maxe, eig_smem_bytes(e->P, m));
   CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(maxe, 48 * 1024)));
-  const int gs = (int)(e->P.g.gsize * 8);
+  const int gs = wcols_smem(e->P.g);
   CK(cudaFuncSetAttribute(k_wcols<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_wcols<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_wcols<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_wcols<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
-  const int zs = (int)(e->P.smax * e->P.rmax * 8);
+  const int zs = (int)(e->P.smax * (e->P.rmax + ZP_T) * 8);
   CK(cudaFuncSetAttribute(k_zproj<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_zproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_zproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
@@ -429,6 +466,7 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   cudaStreamSynchronize(e->st);
   if (e->h_pinned) cudaFreeHost(e->h_pinned);
   if (e->h_idx) cudaFreeHost(e->h_idx);
+  if (e->done) cudaEventDestroy(e->done);
   if (e->prof_pending) {
     for (auto& p : *e->prof_pending) {
       cudaEventDestroy(p.second.first);
@@ -614,12 +652,13 @@ static int run_svd(rtcur_engine* e) {
   ga.part = e->at<double>(P.o_gpart);
   ga.maxchunks = P.gram_maxchunks;
   ga.maxpairs = P.gram_maxpairs;
+  ga.cl = P.gram_cl;
   prof_begin(e, PH_GRAM);
   k_gram_tiles<<<dim3(P.gram_maxpairs, P.gram_maxchunks, n), 256, 0, e->st>>>(ga);
   LAUNCH_CHECK();
   {
     const i64 npk = P.smax * (P.smax + 1) / 2;
-    k_gram_reduce<<<dim3((unsigned)std::min<i64>(cdiv(npk, 256), 512), n), 256, 0, e->st>>>(ga);
+    k_gram_reduce<<<dim3((unsigned)std::min<i64>(cdiv(npk * 32, 256), 2048), n), 256, 0, e->st>>>(ga);
     LAUNCH_CHECK();
   }
   prof_end(e, PH_GRAM);
@@ -631,24 +670,26 @@ static int run_svd(rtcur_engine* e) {
     ea.s[m] = (int)P.s[m];
     ea.r[m] = P.g.rank[m];
     ea.K[m] = e->at<double>(P.o_K[m]);
-    ea.hv[m] = e->at<double>(P.o_hv[m]);
     ea.E[m] = e->at<double>(P.o_E[m]);
     ea.lam[m] = e->at<double>(P.o_lam[m]);
     ea.nb[m] = P.nb[m];
+    ea.full[m] = eig_pick_full((int)P.s[m], P.g.rank[m]);
     esm = std::max(esm, eig_smem_bytes(P, m));
   }
+  ea.tmark = e->at<long long>(P.o_dbg);
   prof_begin(e, PH_EIG);
-  k_eig<<<n, 1024, esm, e->st>>>(ea);
+  k_eig<<<n, EIG_THREADS, esm, e->st>>>(ea);
   LAUNCH_CHECK();
   prof_end(e, PH_EIG);
   prof_begin(e, PH_SVDPOST);
   SvdArgs sa = make_svd_args(e);
   unsigned int* hcnt = e->at<unsigned int>(P.o_counters) + 16;
   const unsigned gz = (unsigned)cdiv(P.lmax, 256);
-  const int zsm = (int)(P.smax * P.rmax * 8);
-  DISPATCH_R(P.rb, k_zproj, dim3(gz, n), 256, zsm, e->st, sa);
+  const int zsm = (int)(P.smax * (P.rmax + ZP_T) * 8);
+  DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(P.lmax, ZP_T), n), 32 * P.rb, zsm, e->st, sa);
   LAUNCH_CHECK();
-  k_hgram<<<dim3(P.h_maxchunks, n), 576, 0, e->st>>>(sa, hcnt);
+  const int hsm = (int)((HG_CH * P.rmax + 512) * 8);
+  k_hgram<<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
   LAUNCH_CHECK();
   k_svd_fin1<<<n, 32, 0, e->st>>>(sa);
   LAUNCH_CHECK();
@@ -656,7 +697,7 @@ static int run_svd(rtcur_engine* e) {
   LAUNCH_CHECK();
   DISPATCH_R(P.rb, k_zrot, dim3(gz, n), 256, 0, e->st, sa);
   LAUNCH_CHECK();
-  k_hgram<<<dim3(P.h_maxchunks, n), 576, 0, e->st>>>(sa, hcnt);
+  k_hgram<<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
   LAUNCH_CHECK();
   k_svd_fin2<<<n, 32, 0, e->st>>>(sa);
   LAUNCH_CHECK();
@@ -673,8 +714,9 @@ static int run_wcols(rtcur_engine* e, double* sto) {
   const Geom& g = P.g;
   IndexPtrs ip = make_ip(e);
   prof_begin(e, PH_WCOLS);
-  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(P.qmax, 128), g.nblk), 128, (int)(g.gsize * 8), e->st, g, ip, sto, 0,
-             (double*)nullptr);
+  const int rpt = wcols_rows_per_thread(g);
+  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(P.qmax, 128), g.nblk), 128, wcols_smem(g), e->st, g, ip, sto, 0,
+             (double*)nullptr, rpt);
   LAUNCH_CHECK();
   prof_end(e, PH_WCOLS);
   return RT_OK;
@@ -705,7 +747,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   prof_begin(e, PH_APASS);
   DISPATCH_R(P.rb, k_apass, dim3((unsigned)cdiv(P.dmax, 256), P.a_maxchunks, n), 256, 0, e->st, g, ip, aa);
   LAUNCH_CHECK();
-  k_areduce<<<dim3((unsigned)std::min<i64>(cdiv(P.dmax * P.rmax, 256), 1024), n), 256, 0, e->st>>>(g, aa);
+  k_areduce<<<dim3((unsigned)std::min<i64>(cdiv(P.dmax * P.rmax * 32, 256), 2048), n), 256, 0, e->st>>>(g, aa);
   LAUNCH_CHECK();
   prof_end(e, PH_APASS);
   prof_begin(e, PH_GPASS);
@@ -733,7 +775,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
       for (int l = m + 1; l < n; ++l) beta *= g.nrows[l];
       double* out = (m == n - 1) ? sto : (in == t0 ? t1 : t0);
       const i64 total = rho * g.rank[m] * beta;
-      k_modeprod<<<(unsigned)std::min<i64>(cdiv(total, 256), 2048), 256, 0, e->st>>>(
+      k_modeprod<<<(unsigned)std::min<i64>(cdiv(total * 32, 256), 4096), 256, 0, e->st>>>(
           in, out, e->at<double>(P.o_U[m]), rho, (int)g.nrows[m], g.rank[m], beta);
       LAUNCH_CHECK();
       rho *= g.rank[m];
@@ -748,9 +790,10 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   return RT_OK;
 }
 
-extern "C" int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, double* sums, int* flags) {
+extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first) {
   if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
   if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
+  if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
   const Plan& P = e->P;
   const int n = P.g.n;
   if (first) e->cur = e->prev = -1;
@@ -773,15 +816,29 @@ extern "C" int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, dou
   CK(cudaMemcpyAsync(e->h_pinned, e->ws + P.o_sums, 2 * P.g.nblk * 8, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(e->h_flags, e->ws + P.o_flags, n * 4, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(e->h_flags + 16, e->ws + P.o_nonfinite, 4, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaStreamSynchronize(e->st));
-  prof_flush(e);
-  if (e->h_flags[16]) return fail(RT_ERR_VALUE, "truncated_svd input contains non-finite entries");
-  if (sums) memcpy(sums, e->h_pinned, 2 * P.g.nblk * 8);
-  if (flags) memcpy(flags, e->h_flags, n * 4);
+  CK(cudaEventRecord(e->done, e->st));
   e->prev = e->cur;
   e->cur = newslot;
   e->zeta_last = zeta;
+  e->pending = true;
   return RT_OK;
+}
+
+extern "C" int rtcur_engine_iterate_wait(rtcur_engine* e, double* sums, int* flags) {
+  if (!e || !e->pending) return fail(RT_ERR_VALUE, "no iteration in flight");
+  e->pending = false;
+  CK(cudaEventSynchronize(e->done));
+  prof_flush(e);
+  if (e->h_flags[16]) return fail(RT_ERR_VALUE, "truncated_svd input contains non-finite entries");
+  if (sums) memcpy(sums, e->h_pinned, 2 * e->P.g.nblk * 8);
+  if (flags) memcpy(flags, e->h_flags, e->P.g.n * 4);
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, double* sums, int* flags) {
+  int st = rtcur_engine_iterate_async(e, zeta, first);
+  if (st) return st;
+  return rtcur_engine_iterate_wait(e, sums, flags);
 }
 
 extern "C" int rtcur_engine_export_blocks(rtcur_engine* e, double* s_blocks, double* clean_blocks, double* l_blocks) {
@@ -830,8 +887,8 @@ extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_de
   i64 ncols = 1;
   for (int m = 1; m < g.n; ++m) ncols *= g.dim[m];
   prof_begin(e, PH_WCOLS);
-  DISPATCH_R(rbucket(g.rank[0]), k_wcols, dim3((unsigned)cdiv(ncols, 128), 1), 128, (int)(g.gsize * 8), e->st, g, ip,
-             sto, 1, tf_dev);
+  DISPATCH_R(rbucket(g.rank[0]), k_wcols, dim3((unsigned)cdiv(ncols, 128), 1), 128, wcols_smem(g), e->st, g, ip,
+             sto, 1, tf_dev, wcols_rows_per_thread(g));
   LAUNCH_CHECK();
   prof_end(e, PH_WCOLS);
   FullArgs fa;
@@ -861,6 +918,14 @@ extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_de
   CK(cudaStreamSynchronize(e->st));
   prof_flush(e);
   if (sums) memcpy(sums, e->h_pinned, 16);
+  return RT_OK;
+}
+
+// internal diagnostics: clock64 phase marks of the last eigensolver launch (8 per mode)
+extern "C" int rtcur_engine_debug_marks(rtcur_engine* e, int64_t* out, int n) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  CK(cudaStreamSynchronize(e->st));
+  CK(cudaMemcpy(out, e->ws + e->P.o_dbg, sizeof(int64_t) * std::min(n, 8 * RT_MAX_MODES), cudaMemcpyDeviceToHost));
   return RT_OK;
 }
 
@@ -936,22 +1001,23 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   P.rb = rbucket(r);
   P.smax = s;
   P.lmax = l;
-  P.hchunk = 256;
-  P.h_maxchunks = (int)cdiv(l, 256);
+  P.hchunk = HG_CH;
+  P.h_maxchunks = (int)cdiv(l, HG_CH);
   const int nt = (int)cdiv(s, GRAM_T);
   P.gram_maxpairs = nt * (nt + 1) / 2;
-  P.gram_maxchunks = (int)cdiv(l, GRAM_CL);
-  P.nb[0] = (int)std::max<i64>(1, std::min<i64>(r, std::max<i64>(s * (s + 1) / 2, 5 * s * 4) / (5 * s)));
+  P.gram_cl = (int)std::max<i64>(GRAM_KS, cdiv(cdiv(l, std::max<i64>(1, cdiv(4 * 148, P.gram_maxpairs))), GRAM_KS) * GRAM_KS);
+  P.gram_maxchunks = (int)cdiv(l, P.gram_cl);
+  P.nb[0] = eig_pick_nb((int)s, r);
+  if (P.nb[0] < 1) return fail(RT_ERR_UNSUPPORTED, "matrix too large for the shared-memory eigensolver");
   i64 o = 0;
   auto take = [&](i64 bytes) { i64 rr = o; o += align256(std::max<i64>(bytes, 8)); return rr; };
   P.o_M[0] = take(8);
   P.o_gpart = take((i64)P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
   P.o_K[0] = take(s * (s + 1) / 2 * 8);
-  P.o_hv[0] = take((s * (s - 1) / 2 + s) * 8);
   P.o_E[0] = take(s * r * 8);
   P.o_lam[0] = take(r * 8);
   P.o_Z[0] = take(l * r * 8);
-  P.o_hpart[0] = take(cdiv(l, 256) * r * (r + 1) / 2 * 8);
+  P.o_hpart[0] = take(cdiv(l, HG_CH) * r * (r + 1) / 2 * 8);
   P.o_H[0] = take(r * r * 8);
   P.o_Q[0] = take(r * r * 8);
   P.o_U[0] = take(m * r * 8);
@@ -973,7 +1039,7 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   // the SVD kernels take raw pointers: M points straight at the caller's matrix
   int esm = eig_smem_bytes(P, 0);
   CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(esm, 48 * 1024)));
-  const int zs = (int)(s * r * 8);
+  const int zs = (int)(s * (r + ZP_T) * 8);
   CK(cudaFuncSetAttribute(k_zproj<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_zproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_zproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
@@ -990,9 +1056,10 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   ga.part = tmp.at<double>(P.o_gpart);
   ga.maxchunks = P.gram_maxchunks;
   ga.maxpairs = P.gram_maxpairs;
+  ga.cl = P.gram_cl;
   k_gram_tiles<<<dim3(P.gram_maxpairs, P.gram_maxchunks, 1), 256, 0, st>>>(ga);
   LAUNCH_CHECK();
-  k_gram_reduce<<<dim3((unsigned)std::min<i64>(cdiv(s * (s + 1) / 2, 256), 512), 1), 256, 0, st>>>(ga);
+  k_gram_reduce<<<dim3((unsigned)std::min<i64>(cdiv(s * (s + 1) / 2 * 32, 256), 2048), 1), 256, 0, st>>>(ga);
   LAUNCH_CHECK();
   EigArgs ea;
   memset(&ea, 0, sizeof(ea));
@@ -1000,19 +1067,20 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   ea.s[0] = (int)s;
   ea.r[0] = r;
   ea.K[0] = ga.K[0];
-  ea.hv[0] = tmp.at<double>(P.o_hv[0]);
   ea.E[0] = tmp.at<double>(P.o_E[0]);
   ea.lam[0] = tmp.at<double>(P.o_lam[0]);
   ea.nb[0] = P.nb[0];
-  k_eig<<<1, 1024, esm, st>>>(ea);
+  ea.full[0] = eig_pick_full((int)s, r);
+  k_eig<<<1, EIG_THREADS, esm, st>>>(ea);
   LAUNCH_CHECK();
   SvdArgs sa = make_svd_args(&tmp);
   sa.M[0] = m_dev;
   unsigned int* hcnt = tmp.at<unsigned int>(P.o_counters) + 16;
   const unsigned gz = (unsigned)cdiv(l, 256);
-  DISPATCH_R(P.rb, k_zproj, dim3(gz, 1), 256, zs, st, sa);
+  DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(l, ZP_T), 1), 32 * P.rb, zs, st, sa);
   LAUNCH_CHECK();
-  k_hgram<<<dim3(P.h_maxchunks, 1), 576, 0, st>>>(sa, hcnt);
+  const int hsm = (int)((HG_CH * r + 512) * 8);
+  k_hgram<<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
   LAUNCH_CHECK();
   k_svd_fin1<<<1, 32, 0, st>>>(sa);
   LAUNCH_CHECK();
@@ -1020,7 +1088,7 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   LAUNCH_CHECK();
   DISPATCH_R(P.rb, k_zrot, dim3(gz, 1), 256, 0, st, sa);
   LAUNCH_CHECK();
-  k_hgram<<<dim3(P.h_maxchunks, 1), 576, 0, st>>>(sa, hcnt);
+  k_hgram<<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
   LAUNCH_CHECK();
   k_svd_fin2<<<1, 32, 0, st>>>(sa);
   LAUNCH_CHECK();

@@ -72,11 +72,27 @@ __global__ void k_colprep(Geom g, IndexPtrs ip, i64* __restrict__ colR_base, int
 
 // ------------------------------------------------------------------ tile map
 
+#define GATHER_U 4
+#define PASS_U 4
+
 struct TileMap {
   int nblk;
-  int tile;                        // elements per CTA tile
+  int tile;                        // target elements per CTA tile
   i64 first[RT_MAX_BLOCKS + 1];    // first tile of each block, first[nblk] = total tiles
+  i64 cpt[RT_MAX_BLOCKS];          // block columns per tile (column-oriented kernels)
 };
+
+// (q, p) = divmod(e, P) -- 32-bit when the block fits (always for the BASELINE shapes)
+__device__ __forceinline__ void split_pq(i64 e, i64 P, bool small, i64& q, i64& p) {
+  if (small) {
+    const unsigned int qq = (unsigned int)e / (unsigned int)P;
+    q = qq;
+    p = (i64)((unsigned int)e - qq * (unsigned int)P);
+  } else {
+    q = e / P;
+    p = e - q * P;
+  }
+}
 
 __device__ __forceinline__ int tile_block(const TileMap& tm, i64 t) {
   int b = 0;
@@ -90,32 +106,44 @@ __device__ __forceinline__ int tile_block(const TileMap& tm, i64 t) {
 // With one rank (lo = 0, hi = d_1) this is the plain gather of solver.py:172-182.
 // Multi-rank: every sampled entry has exactly one owner, so a sum all-reduce of
 // the per-rank x_b reproduces the full gather bit-exactly.
+// Column-oriented: tile = cpt consecutive columns of one block, warp per column,
+// lanes over rows (2 rows per lane per step for ILP).
 __global__ void __launch_bounds__(256) k_gather(Geom g, TileMap tm, IndexPtrs ip, const void* __restrict__ X, int dtype,
                                                i64 lo, i64 hi, void* __restrict__ xb) {
   const i64 t = blockIdx.x;
   const int b = tile_block(tm, t);
-  const BlockDesc bd = g.blk[b];
-  const i64 nel = bd.P * bd.Q;
-  const i64 e0 = (t - tm.first[b]) * tm.tile;
-  const i64 e1 = min(nel, e0 + tm.tile);
+  const BlockDesc& bd = g.blk[b];
+  const i64 P = bd.P;
+  const i64 q0 = (t - tm.first[b]) * tm.cpt[b];
+  const i64 q1 = min(bd.Q, q0 + tm.cpt[b]);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const i64 ld = hi - lo;
-  const i64* colR = ip.colR[b];
-  const int* coli1 = ip.coli1[b];
-  const int* rows0 = ip.rows[0];
+  const int* __restrict__ rows0 = ip.rows[0];
+  const bool core = bd.is_core;
   const i64 rstr = bd.mode >= 1 ? g.rstride[bd.mode] : 0;
-  i64 e = e0 + threadIdx.x;
-  if (e >= e1) return;
-  i64 q = e / bd.P, p = e - q * bd.P;
-  for (; e < e1; e += blockDim.x) {
-    int ci = coli1[q];
-    i64 i1 = ci >= 0 ? (i64)ci : (bd.is_core ? (i64)rows0[p] : p);
-    i64 R = colR[q] + p * rstr;
-    double v = 0.0;
-    if (i1 >= lo && i1 < hi) v = ld_elem(X, (i1 - lo) + ld * R, dtype);
-    if (dtype == 0) reinterpret_cast<double*>(xb)[bd.off + e] = v;
-    else reinterpret_cast<float*>(xb)[bd.off + e] = (float)v;
-    p += blockDim.x;
-    while (p >= bd.P) { p -= bd.P; ++q; }
+  for (i64 q = q0 + wid; q < q1; q += nw) {
+    const int ci = ip.coli1[b][q];
+    const i64 R0 = ip.colR[b][q];
+    const i64 cbase = bd.off + q * P;
+    for (i64 p = lane; p < P; p += 64) {
+      double v0 = 0.0, v1 = 0.0;
+      {
+        const i64 i1 = ci >= 0 ? (i64)ci : (core ? (i64)rows0[p] : p);
+        if (i1 >= lo && i1 < hi) v0 = ld_elem(X, (i1 - lo) + ld * (R0 + p * rstr), dtype);
+      }
+      const i64 p1 = p + 32;
+      if (p1 < P) {
+        const i64 i1 = ci >= 0 ? (i64)ci : (core ? (i64)rows0[p1] : p1);
+        if (i1 >= lo && i1 < hi) v1 = ld_elem(X, (i1 - lo) + ld * (R0 + p1 * rstr), dtype);
+      }
+      if (dtype == 0) {
+        reinterpret_cast<double*>(xb)[cbase + p] = v0;
+        if (p1 < P) reinterpret_cast<double*>(xb)[cbase + p1] = v1;
+      } else {
+        reinterpret_cast<float*>(xb)[cbase + p] = (float)v0;
+        if (p1 < P) reinterpret_cast<float*>(xb)[cbase + p1] = (float)v1;
+      }
+    }
   }
 }
 

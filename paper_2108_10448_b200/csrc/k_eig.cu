@@ -1,35 +1,55 @@
 // k_eig.cu -- top-r eigenvectors of a small symmetric PSD matrix (the
-// intersection Gram, s <= 235), one CTA per matrix, fp64 throughout:
+// intersection Gram, s <= 235), one CTA per matrix, fp64 throughout, all
+// working data in shared memory:
 //
-//   1. Householder tridiagonalisation K = Q T Q^T, packed lower K in shared
-//      memory (warp-per-row symv and rank-2 update; reflectors go to global).
-//   2. The r largest eigenvalues of T by multisection on Sturm counts (each
-//      warp owns one eigenvalue; 32 lanes test 32 shifts per round,
-//      division-free three-term recurrence with exact power-of-2 rescaling).
-//   3. Block inverse iteration on T (thread-per-vector pivoted tridiagonal LU,
-//      3 solves) with block classical Gram-Schmidt (twice) after each solve,
-//      so clusters converge to their invariant subspace.
-//   4. Back-transform by the stored reflectors (warp-per-vector, no barriers).
+//   1. Householder tridiagonalisation K = Q T Q^T.  Small s: full symmetric
+//      storage (odd leading dimension, conflict-free rows), row groups of 8
+//      threads for the symv and the rank-2 update, reflectors copied to a
+//      contiguous array.  Large s (full storage does not fit 227 KB): packed
+//      lower triangle, warp per row, reflectors kept in place.  3 barriers per
+//      Householder step in both layouts.
+//   2. The r largest eigenvalues of T by multisection on Sturm counts of the
+//      tn-normalised T (one warp per eigenvalue, 32 shifts per round; the
+//      three-term recurrence runs branch-free in groups of 4 with exact
+//      power-of-two rescaling in between).
+//   3. Block inverse iteration on T: thread-per-vector pivoted tridiagonal LU
+//      (factored once, 3 solves); vectors whose eigenvalues cluster (gap below
+//      1e-3 * ||T||, LAPACK dstein's ORTOL) are re-orthogonalised after every
+//      solve, everything once more (CGS2) at the end.
+//   4. Back-transform by the stored reflectors, warp per vector (no barriers).
 //
 // Only the span of the r vectors must be accurate: the Rayleigh-Ritz step in
 // k_svdpost.cu fixes the basis inside it and recomputes the singular values
-// from the intersection itself.  Replaces the dense_svd call of
-// linalg.py:73 (_core.pyx:24-249) for the rank-r part the solver uses.
+// from the intersection itself.  Replaces the dense_svd call of linalg.py:73
+// (_core.pyx:24-249) for the rank-r part the solver uses.
 #include "common.cuh"
 #include <cfloat>
+
+#define EIG_SMEM_DOUBLES 29056   // 227 KB opt-in shared memory per CTA
+#define EIG_TPR 4                // threads per row group (full-storage path)
+#define EIG_THREADS 512
 
 struct EigArgs {
   int n;
   int s[RT_MAX_MODES];
   int r[RT_MAX_MODES];
   const double* K[RT_MAX_MODES];   // packed lower, s(s+1)/2
-  double* hv[RT_MAX_MODES];        // reflectors: s*(s-1)/2 + s doubles
   double* E[RT_MAX_MODES];         // s x r, column-major (output)
   double* lam[RT_MAX_MODES];       // r, descending (output)
   int nb[RT_MAX_MODES];            // inverse-iteration batch (vectors factored at once)
+  int full[RT_MAX_MODES];          // 1: full-storage tridiagonalisation
+  long long* tmark;                // optional: per-matrix clock64 marks at phase boundaries (8 each)
 };
 
-__device__ __forceinline__ i64 pk(int i, int j) { return (i64)i * (i + 1) / 2 + j; }  // i >= j
+__host__ __device__ inline int eig_ld(int s) { return s | 1; }
+
+// doubles of shared memory k_eig needs for (s, r, nb, layout)
+__host__ __device__ inline long long eig_smem_doubles(int s, int r, int nb, int full) {
+  const long long amat = full ? (long long)s * eig_ld(s) + (long long)s * (s - 1) / 2 : (long long)s * (s + 1) / 2;
+  return amat + (long long)s * r + 8LL * s + 8 + 2LL * r + 96 + (long long)nb * 4 * s + ((long long)nb * s + 7) / 8;
+}
+
+__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // i >= j
 
 __device__ __forceinline__ double hash_unit(unsigned long long a) {
   a += 0x9E3779B97F4A7C15ull;
@@ -39,121 +59,295 @@ __device__ __forceinline__ double hash_unit(unsigned long long a) {
   return (double)(a >> 11) * (2.0 / 9007199254740992.0) - 1.0;   // (-1, 1)
 }
 
-// number of eigenvalues of T (dd, ed) strictly less than x
-__device__ int sturm_count(const double* dd, const double* ed, int s, double x, double pivmin) {
-  double pm2 = 1.0, pm1 = dd[0] - x;
-  int cnt = 0;
-  double sp = 1.0;
-  if (pm1 == 0.0) pm1 = -pivmin;
-  if ((pm1 < 0.0) != (sp < 0.0)) ++cnt;
-  sp = pm1;
-  for (int i = 1; i < s; ++i) {
-    const double e = ed[i - 1];
-    double p = (dd[i] - x) * pm1 - (e * e) * pm2;
-    if (p == 0.0) p = -pivmin * pm1;
-    if ((p < 0.0) != (sp < 0.0)) ++cnt;
-    sp = p;
-    const double ap = fabs(p);
-    if (ap > 0x1p+400 || ap < 0x1p-400) {
-      const int ex = ilogb(p);
-      pm1 = ldexp(pm1, -ex);
-      p = ldexp(p, -ex);
+// Number of eigenvalues of the normalised tridiagonal (d, e2 = offdiag^2, all
+// entries O(1); arrays padded to a multiple of 4 with d = +1e30, e2 = 0, which
+// adds no sign change) strictly less than x0 and x1 (two independent Sturm
+// sequences interleaved for ILP): sign changes of the leading principal minors,
+// a zero minor replaced by -tiny * previous (the q-form's -pivmin), rescaled by
+// an exact power of two every 4 steps.
+__device__ __forceinline__ void sturm_count2(const double* __restrict__ d, const double* __restrict__ e2, int s4,
+                                             double x0, double x1, int& c0, int& c1) {
+  const double tiny = 1e-300;
+  double pa1 = d[0] - x0, pb1 = d[0] - x1, pa2 = 1.0, pb2 = 1.0;
+  pa1 = (pa1 == 0.0) ? -tiny : pa1;
+  pb1 = (pb1 == 0.0) ? -tiny : pb1;
+  int ca = pa1 < 0.0, cb = pb1 < 0.0;
+  bool na = pa1 < 0.0, nb = pb1 < 0.0;
+  for (int i = 1; i < s4; i += 4) {
+    double dv[4], ev[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { dv[u] = d[i + u]; ev[u] = e2[i + u - 1]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double pa = fma(dv[u] - x0, pa1, -ev[u] * pa2);
+      double pb = fma(dv[u] - x1, pb1, -ev[u] * pb2);
+      pa = (pa == 0.0) ? -tiny * pa1 : pa;
+      pb = (pb == 0.0) ? -tiny * pb1 : pb;
+      const bool qa = pa < 0.0, qb = pb < 0.0;
+      ca += (qa != na);
+      cb += (qb != nb);
+      na = qa;
+      nb = qb;
+      pa2 = pa1; pa1 = pa;
+      pb2 = pb1; pb1 = pb;
     }
-    pm2 = pm1;
-    pm1 = p;
+    const int ea = (int)((__double_as_longlong(pa1) >> 52) & 0x7ff);
+    const int eb = (int)((__double_as_longlong(pb1) >> 52) & 0x7ff);
+    if (ea > 1023 + 300 || ea < 1023 - 300) {
+      const double sc = __longlong_as_double((long long)(2046 - ea) << 52);   // 2^(1023-ea), exact
+      pa1 *= sc;
+      pa2 *= sc;
+    }
+    if (eb > 1023 + 300 || eb < 1023 - 300) {
+      const double sc = __longlong_as_double((long long)(2046 - eb) << 52);
+      pb1 *= sc;
+      pb2 *= sc;
+    }
   }
-  return cnt;
+  c0 = ca;
+  c1 = cb;
+}
+
+// sum over the warp of red[0..nw) (every lane gets the total; deterministic order)
+__device__ __forceinline__ double warp_sum_of(const double* red, int nw) {
+  const int lane = threadIdx.x & 31;
+  double t = lane < nw ? red[lane] : 0.0;
+  return warp_sum(t);
+}
+
+__device__ __forceinline__ double group_sum8(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
 }
 
 extern __shared__ double eig_smem[];
 
-__global__ void __launch_bounds__(1024) k_eig(EigArgs ea) {
+__global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
   const int mi = blockIdx.x;
   if (mi >= ea.n) return;
-  const int s = ea.s[mi], r = ea.r[mi];
+  const int s = ea.s[mi], r = ea.r[mi], nb = ea.nb[mi];
+  const bool full = ea.full[mi] != 0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  const i64 npk = (i64)s * (s + 1) / 2;
-  const int nb = ea.nb[mi];
-  const i64 region0 = max(npk, (i64)5 * s * nb);
-  double* A = eig_smem;
-  double* dd = eig_smem + region0;
-  double* ed = dd + s;
-  double* vv = ed + s;
-  double* yy = vv + s;
-  double* ww = yy + s;
-  double* red = ww + s;     // 32
-  __shared__ double sh_beta, sh_tn, sh_lo, sh_hi;
-  double* hv = ea.hv[mi];
-  double* hb = hv + (i64)s * (s - 1) / 2;   // betas
-  double* E = ea.E[mi];
+  const int ld = eig_ld(s);
+  const int npk = s * (s + 1) / 2;
+  double* A = eig_smem;                                            // matrix
+  double* HV = full ? A + s * ld : A;                              // reflectors (full: contiguous)
+  double* E = full ? HV + s * (s - 1) / 2 : A + npk;               // s x r eigenvector block
+  double* dd = E + s * r;                                          // diagonal of T
+  double* ed = dd + s;                                             // off-diagonal of T
+  double* dn = ed + s;                                             // normalised diagonal
+  double* e2n = dn + (s + 4);                                      // normalised off-diagonal^2
+  double* bet = e2n + (s + 4);                                     // reflector scalars
+  double* vv = bet + s;                                            // current reflector
+  double* yy = vv + s;                                             // symv result
+  double* ww = yy + s;                                             // (spare)
+  double* lam = ww + s;                                            // r eigenvalues
+  int* clus = reinterpret_cast<int*>(lam + r);                     // r cluster starts (as doubles)
+  double* red = lam + 2 * r;                                       // 32
+  double* red2 = red + 32;                                         // 32
+  double* scal = red2 + 32;                                        // 32
+  double* lu = scal + 32;                                          // nb * 4s
+  unsigned char* piv = reinterpret_cast<unsigned char*>(lu + (size_t)nb * 4 * s);
+  (void)ww;
 
-  for (i64 i = tid; i < npk; i += blockDim.x) A[i] = ea.K[mi][i];
+  long long* tm = ea.tmark ? ea.tmark + 8 * mi : nullptr;
+  if (tm && tid == 0) tm[0] = clock64();
+  const double* Kg = ea.K[mi];
+  if (full) {
+    for (int idx = tid; idx < npk; idx += blockDim.x) {
+      int i = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+      while ((i + 1) * (i + 2) / 2 <= idx) ++i;
+      while (i * (i + 1) / 2 > idx) --i;
+      const int j = idx - i * (i + 1) / 2;
+      const double v = Kg[idx];
+      A[i * ld + j] = v;
+      A[j * ld + i] = v;
+    }
+  } else {
+    for (int i = tid; i < npk; i += blockDim.x) A[i] = Kg[i];
+  }
   __syncthreads();
+  if (tm && tid == 0) tm[1] = clock64();
 
   // ---------------------------------------------------------------- 1. tridiagonalise
-  i64 hoff = 0;
-  for (int k = 0; k + 2 < s; ++k) {
-    const int L = s - k - 1;
-    double sq = 0.0;
-    for (int i = tid; i < L; i += blockDim.x) {
-      const double x = A[pk(k + 1 + i, k)];
-      vv[i] = x;
-      sq = fma(x, x, sq);
-    }
-    sq = block_sum(sq, red);
-    if (tid == 0) {
-      const double x0 = vv[0];
-      const double nrm = sqrt(sq);
-      dd[k] = A[pk(k, k)];
-      if (nrm == 0.0) {
-        sh_beta = 0.0;
-        ed[k] = 0.0;
-      } else {
-        const double alpha = -copysign(nrm, x0);
-        vv[0] = x0 - alpha;
-        sh_beta = 1.0 / (nrm * (nrm + fabs(x0)));
-        ed[k] = alpha;
+  int hoff = 0;
+  if (full) {
+    // Full symmetric storage.  The column k+1 that step k+1 reflects is produced
+    // by step k's rank-2 update (row groups own it), so its squared norm is
+    // reduced there: 2 barriers per Householder step.
+    double* vbuf0 = vv;
+    double* vbuf1 = ww;
+    {
+      const int L = s - 1;
+      double sq = 0.0;
+      for (int i = tid; i < L; i += blockDim.x) {
+        const double x = A[(1 + i) * ld];
+        vbuf0[i] = x;
+        sq = fma(x, x, sq);
       }
-      hb[k] = sh_beta;
+      sq = warp_sum(sq);
+      if (lane == 0) red[wid] = sq;
     }
     __syncthreads();
-    const double beta = sh_beta;
-    for (int i = tid; i < L; i += blockDim.x) hv[hoff + i] = vv[i];
-    if (beta != 0.0) {
-      // y = beta * A22 v   (warp per row; A22[i][j] = A[k+1+max, k+1+min])
-      for (int i = wid; i < L; i += nw) {
-        const int gi = k + 1 + i;
-        double acc = 0.0;
-        const i64 rowbase = pk(gi, k + 1);
-        for (int j = lane; j < L; j += 32) {
-          const double a = (j <= i) ? A[rowbase + j] : A[pk(k + 1 + j, gi)];
-          acc = fma(a, vv[j], acc);
+    const int sub = tid & (EIG_TPR - 1);
+    const int gpw = 32 / EIG_TPR;          // row groups per warp
+    for (int k = 0; k + 2 < s; ++k) {
+      const int L = s - k - 1, b0 = k + 1;
+      double* vc = (k & 1) ? vbuf1 : vbuf0;   // this step's column / reflector
+      double* vn = (k & 1) ? vbuf0 : vbuf1;   // next step's column
+      double* rc = (k & 1) ? red + 16 : red;  // this step's column norm partials (<= 16 warps)
+      double* rn = (k & 1) ? red : red + 16;
+      const double nrm = sqrt(warp_sum_of(rc, nw));
+      const double x0 = vc[0];
+      double alpha = 0.0, beta = 0.0;
+      if (nrm > 0.0) {
+        alpha = -copysign(nrm, x0);
+        beta = 1.0 / (nrm * (nrm + fabs(x0)));
+      }
+      const double v0 = x0 - alpha;
+      // y = beta * A22 v: row groups of EIG_TPR threads (warp-uniform trip count)
+      double dotp = 0.0;
+      for (int ib = wid * gpw; ib < L; ib += nw * gpw) {
+        const int i = ib + lane / EIG_TPR;
+        double a0 = 0.0, a1 = 0.0;
+        if (i < L) {
+          const double* __restrict__ row = A + (b0 + i) * ld + b0;
+          int j = sub;
+          if (sub == 0) { a0 = row[0] * v0; j = EIG_TPR; }
+          for (; j + 3 * EIG_TPR < L; j += 4 * EIG_TPR) {
+            double rv[4], vv4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { rv[u] = row[j + u * EIG_TPR]; vv4[u] = vc[j + u * EIG_TPR]; }
+            a0 = fma(rv[0], vv4[0], a0);
+            a1 = fma(rv[1], vv4[1], a1);
+            a0 = fma(rv[2], vv4[2], a0);
+            a1 = fma(rv[3], vv4[3], a1);
+          }
+          for (; j < L; j += EIG_TPR) a0 = fma(row[j], vc[j], a0);
         }
-        acc = warp_sum(acc);
-        if (lane == 0) yy[i] = beta * acc;
+        double acc = a0 + a1;
+#pragma unroll
+        for (int o = EIG_TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        acc *= beta;
+        if (i < L && sub == 0) {
+          yy[i] = acc;
+          dotp = fma(acc, i == 0 ? v0 : vc[i], dotp);
+        }
       }
-      __syncthreads();
-      double dot = 0.0;
-      for (int i = tid; i < L; i += blockDim.x) dot = fma(yy[i], vv[i], dot);
-      dot = block_sum(dot, red);
-      const double kk = 0.5 * beta * dot;
-      for (int i = tid; i < L; i += blockDim.x) ww[i] = yy[i] - kk * vv[i];
-      __syncthreads();
-      for (int i = wid; i < L; i += nw) {
-        const double vi = vv[i], wi = ww[i];
-        const i64 rowbase = pk(k + 1 + i, k + 1);
-        for (int j = lane; j <= i; j += 32) A[rowbase + j] -= vi * ww[j] + wi * vv[j];
+      dotp = warp_sum(dotp);
+      if (lane == 0) red2[wid] = dotp;
+      __syncthreads();                                             // B1
+      const double kk = 0.5 * beta * warp_sum_of(red2, nw);
+      // A22 -= v w^T + w v^T (w = y - kk v); the new column k+1 (local column 0,
+      // rows >= 1) goes to vn with its squared norm
+      double sq = 0.0;
+      for (int ib = wid * gpw; ib < L; ib += nw * gpw) {
+        const int i = ib + lane / EIG_TPR;
+        if (i < L) {
+          const double vi = i == 0 ? v0 : vc[i];
+          const double wi = yy[i] - kk * vi;
+          double* __restrict__ row = A + (b0 + i) * ld + b0;
+          if (sub == 0) {
+            // column 0 (next step's reflector input) first
+            const double nv = row[0] - (vi * (yy[0] - kk * v0) + wi * v0);
+            row[0] = nv;
+            if (i >= 1) {
+              vn[i - 1] = nv;
+              sq = fma(nv, nv, sq);
+            }
+          }
+          int j = (sub == 0) ? EIG_TPR : sub;
+          for (; j + 3 * EIG_TPR < L; j += 4 * EIG_TPR) {
+            double rv[4], vv4[4], yv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              rv[u] = row[j + u * EIG_TPR];
+              vv4[u] = vc[j + u * EIG_TPR];
+              yv[u] = yy[j + u * EIG_TPR];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) row[j + u * EIG_TPR] = rv[u] - (vi * (yv[u] - kk * vv4[u]) + wi * vv4[u]);
+          }
+          for (; j < L; j += EIG_TPR) {
+            const double vj = vc[j];
+            row[j] -= vi * (yy[j] - kk * vj) + wi * vj;
+          }
+        }
       }
+      sq = warp_sum(sq);
+      if (lane == 0) rn[wid] = sq;
+      for (int i = tid; i < L; i += blockDim.x) HV[hoff + i] = i == 0 ? v0 : vc[i];
+      if (tid == 0) {
+        dd[k] = A[k * ld + k];
+        ed[k] = alpha;
+        bet[k] = beta;
+      }
+      hoff += L;
+      __syncthreads();                                             // B2
     }
-    __syncthreads();
-    hoff += L;
+  } else {
+    for (int k = 0; k + 2 < s; ++k) {
+      const int L = s - k - 1, b0 = k + 1;
+      double sq = 0.0;
+      for (int i = tid; i < L; i += blockDim.x) {
+        const double x = A[pk(b0 + i, k)];
+        vv[i] = x;
+        sq = fma(x, x, sq);
+      }
+      sq = warp_sum(sq);
+      if (lane == 0) red[wid] = sq;
+      __syncthreads();                                             // B1
+      const double nrm = sqrt(warp_sum_of(red, nw));
+      const double x0 = vv[0];
+      double alpha = 0.0, beta = 0.0;
+      if (nrm > 0.0) {
+        alpha = -copysign(nrm, x0);
+        beta = 1.0 / (nrm * (nrm + fabs(x0)));
+      }
+      const double v0 = x0 - alpha;
+      double dotp = 0.0;
+      for (int i = wid; i < L; i += nw) {
+        const int gi = b0 + i;
+        const int rowbase = pk(gi, b0);
+        double acc = 0.0;
+        for (int j = lane; j < L; j += 32) {
+          const double a = (j <= i) ? A[rowbase + j] : A[pk(b0 + j, gi)];
+          acc = fma(a, j == 0 ? v0 : vv[j], acc);
+        }
+        acc = warp_sum(acc) * beta;
+        if (lane == 0) yy[i] = acc;
+        dotp = fma(acc, i == 0 ? v0 : vv[i], dotp);
+      }
+      if (lane == 0) red2[wid] = dotp;
+      __syncthreads();                                             // B2
+      const double kk = 0.5 * beta * warp_sum_of(red2, nw);
+      for (int i = wid; i < L; i += nw) {
+        const double vi = i == 0 ? v0 : vv[i];
+        const double wi = yy[i] - kk * vi;
+        const int rowbase = pk(b0 + i, b0);
+        for (int j = lane; j <= i; j += 32) {
+          const double vj = j == 0 ? v0 : vv[j];
+          A[rowbase + j] -= vi * (yy[j] - kk * vj) + wi * vj;
+        }
+        if (lane == 0) A[pk(b0 + i, k)] = vi;   // reflector in place (column k left the active block)
+      }
+      if (tid == 0) {
+        dd[k] = A[pk(k, k)];
+        ed[k] = alpha;
+        bet[k] = beta;
+      }
+      hoff += L;
+      __syncthreads();                                             // B3
+    }
   }
   if (tid == 0) {
     if (s >= 2) {
-      dd[s - 2] = A[pk(s - 2, s - 2)];
-      ed[s - 2] = A[pk(s - 1, s - 2)];
+      dd[s - 2] = full ? A[(s - 2) * ld + s - 2] : A[pk(s - 2, s - 2)];
+      ed[s - 2] = full ? A[(s - 1) * ld + s - 2] : A[pk(s - 1, s - 2)];
     }
-    dd[s - 1] = A[pk(s - 1, s - 1)];
+    dd[s - 1] = full ? A[(s - 1) * ld + s - 1] : A[pk(s - 1, s - 1)];
     double tn = 0.0, lo = DBL_MAX, hi = -DBL_MAX;
     for (int i = 0; i < s; ++i) {
       const double rad = (i > 0 ? fabs(ed[i - 1]) : 0.0) + (i + 1 < s ? fabs(ed[i]) : 0.0);
@@ -161,60 +355,100 @@ __global__ void __launch_bounds__(1024) k_eig(EigArgs ea) {
       lo = fmin(lo, dd[i] - rad);
       hi = fmax(hi, dd[i] + rad);
     }
-    sh_tn = tn;
-    sh_lo = lo;
-    sh_hi = hi;
+    scal[0] = tn;
+    scal[1] = lo;
+    scal[2] = hi;
   }
   __syncthreads();
-  const double tn = sh_tn;
+  if (tm && tid == 0) tm[2] = clock64();
+  const double tn = scal[0];
+  double* Eout = ea.E[mi];
 
   if (tn == 0.0) {
     // zero matrix: every eigenvalue is 0, any orthonormal basis is exact
-    for (int j = 0; j < r; ++j) {
-      for (int i = tid; i < s; i += blockDim.x) E[i + (i64)j * s] = (i == j) ? 1.0 : 0.0;
-      if (tid == 0) ea.lam[mi][j] = 0.0;
-    }
+    for (int e = tid; e < s * r; e += blockDim.x) Eout[e] = (e % s == e / s) ? 1.0 : 0.0;
+    for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = 0.0;
     return;
   }
 
-  // ---------------------------------------------------------------- 2. multisection
-  const double pivmin = DBL_MIN * fmax(1.0, tn * tn);
-  const double pad = 2.0 * DBL_EPSILON * tn * s + pivmin;
-  double* lam = yy;   // reuse (s >= r)
-  for (int j = wid; j < r; j += nw) {
-    const int target = s - 1 - j;   // ascending index of the j-th largest
-    double lo = sh_lo - pad, hi = sh_hi + pad;
-    for (int round = 0; round < 24; ++round) {
-      const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-      const int c = sturm_count(dd, ed, s, x, pivmin);
-      double nlo = (c <= target) ? x : -DBL_MAX;
-      double nhi = (c >= target + 1) ? x : DBL_MAX;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        nlo = fmax(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
-        nhi = fmin(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
-      }
-      if (nlo != -DBL_MAX) lo = nlo;
-      if (nhi != DBL_MAX) hi = nhi;
-      if (lo >= hi) { const double mid = 0.5 * (lo + hi); lo = hi = mid; break; }
-      if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin || hi - lo <= 0.25 * DBL_EPSILON * tn) break;
-    }
-    if (lane == 0) lam[j] = 0.5 * (lo + hi);
+  // ---------------------------------------------------------------- 2. multisection (normalised T)
+  const double itn = 1.0 / tn;
+  const int s4 = 1 + ((s - 1 + 3) / 4) * 4;   // padded length of the Sturm arrays
+  for (int i = tid; i < s4; i += blockDim.x) {
+    dn[i] = i < s ? dd[i] * itn : 1e30;
+    const double en = (i + 1 < s) ? ed[i] * itn : 0.0;
+    e2n[i] = en * en;
   }
   __syncthreads();
+  {
+    // ng warps per eigenvalue test ng*32 shifts per round; brackets combined in
+    // shared memory (double-buffered by round parity: one barrier per round)
+    const double pad = 4.0 * DBL_EPSILON * s;
+    double* blo = red;                  // 2 x 16 warp brackets (lo); red/red2 are free here
+    double* bhi = red2;                 // 2 x 16 warp brackets (hi)
+    for (int j0 = 0; j0 < r; j0 += nw) {
+      const int rr = min(nw, r - j0);
+      const int ng = nw / rr;
+      const int j = j0 + wid / ng, g = wid % ng;
+      const bool act = wid < rr * ng;
+      const double nsh = (double)(ng * 64 + 1);
+      const int rounds = (int)ceil(log(16.0 / DBL_EPSILON) / log(nsh)) + 1;
+      double lo = scal[1] * itn - pad, hi = scal[2] * itn + pad;
+      for (int round = 0; round < rounds; ++round) {
+        double nlo = -DBL_MAX, nhi = DBL_MAX;
+        if (act && hi > lo) {
+          const int target = s - 1 - j;   // ascending index of the j-th largest
+          const double xa = lo + (hi - lo) * (double)(g * 64 + 2 * lane + 1) / nsh;
+          const double xb = lo + (hi - lo) * (double)(g * 64 + 2 * lane + 2) / nsh;
+          int ca, cb;
+          sturm_count2(dn, e2n, s4, xa, xb, ca, cb);
+          if (ca <= target) nlo = xa;
+          if (cb <= target) nlo = xb;
+          if (cb >= target + 1) nhi = xb;
+          if (ca >= target + 1) nhi = xa;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          nlo = fmax(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
+          nhi = fmin(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+        }
+        double* bl = blo + (round & 1) * 16;
+        double* bh = bhi + (round & 1) * 16;
+        if (lane == 0) { bl[wid] = nlo; bh[wid] = nhi; }
+        __syncthreads();
+        if (act) {
+          for (int q = 0; q < ng; ++q) {
+            const int w2 = (wid / ng) * ng + q;
+            if (bl[w2] != -DBL_MAX) lo = fmax(lo, bl[w2]);
+            if (bh[w2] != DBL_MAX) hi = fmin(hi, bh[w2]);
+          }
+          if (lo > hi) lo = hi = 0.5 * (lo + hi);
+        }
+      }
+      if (act && g == 0 && lane == 0) lam[j] = 0.5 * (lo + hi) * tn;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // clusters (descending order): j joins j-1 when the gap is below ORTOL * ||T||
+    clus[0] = 0;
+    for (int j = 1; j < r; ++j) clus[j] = (lam[j - 1] - lam[j] < 1e-3 * tn) ? clus[j - 1] : j;
+  }
   for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = lam[j];
+  __syncthreads();
+  if (tm && tid == 0) tm[3] = clock64();
 
   // ---------------------------------------------------------------- 3. block inverse iteration
   const double tiny = DBL_EPSILON * tn;
   const double pertol = 10.0 * DBL_EPSILON * tn;
   for (int j0 = 0; j0 < r; j0 += nb) {
     const int jn = min(nb, r - j0);
-    // thread t < jn owns vector j0+t: factor T - mu I with partial pivoting
-    double* u0 = A + (i64)5 * s * tid;
+    double* u0 = lu + (size_t)4 * s * tid;
     double* u1 = u0 + s;
     double* u2 = u1 + s;
     double* lm = u2 + s;
-    double* pv = lm + s;
+    unsigned char* pv = piv + (size_t)s * tid;
     if (tid < jn) {
       const int j = j0 + tid;
       double mu = lam[j];
@@ -226,115 +460,169 @@ __global__ void __launch_bounds__(1024) k_eig(EigArgs ea) {
         const double na = dd[i + 1] - mu;
         const double nbv = (i + 2 < s) ? ed[i + 1] : 0.0;
         const double c = ed[i];
-        double l;
         if (fabs(ca) >= fabs(c)) {
           if (fabs(ca) < tiny) ca = copysign(tiny, ca);
-          l = c / ca;
-          u0[i] = 1.0 / ca;
+          const double inv = 1.0 / ca;
+          const double l = c * inv;
+          u0[i] = inv;
           u1[i] = cb;
           u2[i] = 0.0;
-          pv[i] = 0.0;
+          pv[i] = 0;
+          lm[i] = l;
           ca = na - l * cb;
           cb = nbv;
         } else {
-          l = ca / c;
-          u0[i] = 1.0 / c;
+          const double inv = 1.0 / c;
+          const double l = ca * inv;
+          u0[i] = inv;
           u1[i] = na;
           u2[i] = nbv;
-          pv[i] = 1.0;
+          pv[i] = 1;
+          lm[i] = l;
           ca = cb - l * na;
           cb = -l * nbv;
         }
-        lm[i] = l;
       }
       if (fabs(ca) < tiny) ca = copysign(tiny, ca);
       u0[s - 1] = 1.0 / ca;
-      double* x = E + (i64)j * s;
+      u1[s - 1] = 0.0;
+      u2[s - 1] = 0.0;
+      if (s >= 2) u2[s - 2] = 0.0;
+      double* x = E + j * s;
       for (int i = 0; i < s; ++i) x[i] = hash_unit(((unsigned long long)j << 32) ^ (unsigned long long)i);
     }
     __syncthreads();
+    bool any_cluster = false;
+    for (int j = j0; j < j0 + jn; ++j) any_cluster |= (clus[j] != j);
     for (int it = 0; it < 3; ++it) {
       if (tid < jn) {
-        double* x = E + (i64)(j0 + tid) * s;
-        // forward: apply P and L^-1
+        double* __restrict__ x = E + (j0 + tid) * s;
+        double bi = x[0];
+        double bn = s > 1 ? x[1] : 0.0;
+        double l_i = lm[0];
+        bool p_i = s > 1 ? pv[0] : 0;
         for (int i = 0; i + 1 < s; ++i) {
-          double bi = x[i], bn = x[i + 1];
-          if (pv[i] != 0.0) { const double t = bi; bi = bn; bn = t; x[i] = bi; }
-          x[i + 1] = bn - lm[i] * bi;
+          // prefetch the next step's operands before the dependent update
+          const double bnn = (i + 2 < s) ? x[i + 2] : 0.0;
+          const double lnx = (i + 2 < s) ? lm[i + 1] : 0.0;
+          const bool pnx = (i + 2 < s) ? pv[i + 1] : 0;
+          double b_lo = bi, b_hi = bn;
+          if (p_i) { b_lo = bn; b_hi = bi; }
+          x[i] = b_lo;
+          bi = fma(-l_i, b_lo, b_hi);
+          bn = bnn;
+          l_i = lnx;
+          p_i = pnx;
         }
-        // back substitution with U (diag reciprocal u0, supers u1, u2)
-        double xn1 = 0.0, xn2 = 0.0;
+        x[s - 1] = bi;
+        double xn1 = 0.0, xn2 = 0.0, mx = 0.0;
+        double xi = x[s - 1], a1 = u1[s - 1], a2 = u2[s - 1], a0 = u0[s - 1];
         for (int i = s - 1; i >= 0; --i) {
-          double v = x[i];
-          if (i + 1 < s) v -= u1[i] * xn1;
-          if (i + 2 < s) v -= u2[i] * xn2;
-          v *= u0[i];
-          if (!isfinite(v)) v = 0.0;
+          const double xp = i > 0 ? x[i - 1] : 0.0;
+          const double b1 = i > 0 ? u1[i - 1] : 0.0, b2 = i > 0 ? u2[i - 1] : 0.0, b0 = i > 0 ? u0[i - 1] : 0.0;
+          double v = (xi - a1 * xn1 - a2 * xn2) * a0;
+          v = isfinite(v) ? v : 0.0;
           x[i] = v;
+          mx = fmax(mx, fabs(v));
           xn2 = xn1;
           xn1 = v;
+          xi = xp; a1 = b1; a2 = b2; a0 = b0;
         }
-        // scale to unit max so the next solve cannot overflow
-        double mx = 0.0;
-        for (int i = 0; i < s; ++i) mx = fmax(mx, fabs(x[i]));
-        if (mx > 0.0) {
-          const double inv = 1.0 / mx;
-          for (int i = 0; i < s; ++i) x[i] *= inv;
-        }
+        const double inv = mx > 0.0 ? 1.0 / mx : 0.0;
+        for (int i = 0; i < s; ++i) x[i] *= inv;
       }
       __syncthreads();
-      __threadfence_block();
-      // block CGS2 over vectors 0..j0+jn-1 (earlier batches are final)
+      if (!any_cluster) continue;
+      // orthogonalise each clustered vector against the earlier members of its cluster
       for (int j = j0; j < j0 + jn; ++j) {
-        double* xj = E + (i64)j * s;
+        const int c0 = clus[j];
+        if (c0 == j) continue;
+        double* xj = E + j * s;
         for (int pass = 0; pass < 2; ++pass) {
-          // dots with all previous vectors: warp w handles vector i = w, w+nw, ...
-          for (int i = wid; i < j; i += nw) {
-            const double* xi = E + (i64)i * s;
+          for (int i = c0 + wid; i < j; i += nw) {
+            const double* xi = E + i * s;
             double d = 0.0;
             for (int t = lane; t < s; t += 32) d = fma(xi[t], xj[t], d);
             d = warp_sum(d);
-            if (lane == 0) red[i % 32] = d;   // j <= 32 guaranteed by RT_MAX_RANK
+            if (lane == 0) red[i - c0] = d;
           }
           __syncthreads();
           for (int t = tid; t < s; t += blockDim.x) {
             double v = xj[t];
-            for (int i = 0; i < j; ++i) v = fma(-red[i], E[t + (i64)i * s], v);
+            for (int i = c0; i < j; ++i) v = fma(-red[i - c0], E[t + i * s], v);
             xj[t] = v;
           }
           __syncthreads();
         }
         double nn = 0.0;
         for (int t = tid; t < s; t += blockDim.x) nn = fma(xj[t], xj[t], nn);
-        nn = block_sum(nn, red);
-        if (nn > 0.0) {
-          const double inv = 1.0 / sqrt(nn);
-          for (int t = tid; t < s; t += blockDim.x) xj[t] *= inv;
-        } else {
-          // degenerate: replace with a unit vector, orthogonalised on the next pass
-          for (int t = tid; t < s; t += blockDim.x) xj[t] = (t == j % s) ? 1.0 : 0.0;
-        }
+        nn = warp_sum(nn);
+        if (lane == 0) red2[wid] = nn;
+        __syncthreads();
+        nn = warp_sum_of(red2, nw);
+        const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+        for (int t = tid; t < s; t += blockDim.x) xj[t] = nn > 0.0 ? xj[t] * inv : (t == j % s ? 1.0 : 0.0);
         __syncthreads();
       }
     }
   }
-  __syncthreads();
+  // final CGS2 over all r vectors (warp w owns vector j; dots against the finished ones)
+  for (int j = 0; j < r; ++j) {
+    double* xj = E + j * s;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (j > 0) {
+        for (int i = wid; i < j; i += nw) {
+          const double* xi = E + i * s;
+          double d = 0.0;
+          for (int t = lane; t < s; t += 32) d = fma(xi[t], xj[t], d);
+          d = warp_sum(d);
+          if (lane == 0) red[i] = d;
+        }
+        __syncthreads();
+        for (int t = tid; t < s; t += blockDim.x) {
+          double v = xj[t];
+          for (int i = 0; i < j; ++i) v = fma(-red[i], E[t + i * s], v);
+          xj[t] = v;
+        }
+      }
+      double nn = 0.0;
+      for (int t = tid; t < s; t += blockDim.x) nn = fma(xj[t], xj[t], nn);
+      nn = warp_sum(nn);
+      __syncthreads();
+      if (lane == 0) red2[wid] = nn;
+      __syncthreads();
+      nn = warp_sum_of(red2, nw);
+      const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+      for (int t = tid; t < s; t += blockDim.x) xj[t] = nn > 0.0 ? xj[t] * inv : (t == j % s ? 1.0 : 0.0);
+      __syncthreads();
+    }
+  }
+  if (tm && tid == 0) tm[4] = clock64();
 
   // ---------------------------------------------------------------- 4. back-transform
   for (int j = wid; j < r; j += nw) {
-    double* x = E + (i64)j * s;
-    i64 off = hoff;
+    double* x = E + j * s;
+    int off = hoff;
     for (int k = s - 3; k >= 0; --k) {
       const int L = s - k - 1;
       off -= L;
-      const double beta = hb[k];
+      const double beta = bet[k];
       if (beta == 0.0) continue;
-      const double* v = hv + off;
       double d = 0.0;
-      for (int i = lane; i < L; i += 32) d = fma(v[i], x[k + 1 + i], d);
-      d = warp_sum(d) * beta;
-      for (int i = lane; i < L; i += 32) x[k + 1 + i] -= d * v[i];
+      if (full) {
+        const double* v = HV + off;
+        for (int i = lane; i < L; i += 32) d = fma(v[i], x[k + 1 + i], d);
+        d = warp_sum(d) * beta;
+        for (int i = lane; i < L; i += 32) x[k + 1 + i] = fma(-d, v[i], x[k + 1 + i]);
+      } else {
+        for (int i = lane; i < L; i += 32) d = fma(A[pk(k + 1 + i, k)], x[k + 1 + i], d);
+        d = warp_sum(d) * beta;
+        for (int i = lane; i < L; i += 32) x[k + 1 + i] = fma(-d, A[pk(k + 1 + i, k)], x[k + 1 + i]);
+      }
       __syncwarp();
     }
   }
+  __syncthreads();
+  if (tm && tid == 0) tm[5] = clock64();
+  for (int e = tid; e < s * r; e += blockDim.x) Eout[e] = E[e];
 }

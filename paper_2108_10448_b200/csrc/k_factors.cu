@@ -27,62 +27,80 @@ struct APassArgs {
   double* st_out;                   // new state (A_k written at g.a_off[k])
 };
 
+#define APASS_CH 32   // fiber columns per CTA (V and W rows staged in shared memory)
+
 template <int R>
 __global__ void __launch_bounds__(256) k_apass(Geom g, IndexPtrs ip, APassArgs a) {
-  __shared__ double vs[64 * RT_MAX_RANK];
+  __shared__ double vs[APASS_CH * RT_MAX_RANK];
+  __shared__ double wsh[APASS_CH * RT_MAX_RANK];
   const int k = blockIdx.z;
   if (k >= g.n) return;
-  const BlockDesc bd = g.blk[k + 1];
+  const BlockDesc& bd = g.blk[k + 1];
   const int r = bd.r;
+  const i64 P = bd.P;
   const i64 q0 = (i64)blockIdx.y * a.chunk;
   if (q0 >= bd.Q) return;
-  const i64 q1 = min(bd.Q, q0 + a.chunk);
+  if ((i64)blockIdx.x * blockDim.x >= P) return;
+  const int nq = (int)min((i64)a.chunk, bd.Q - q0);
+  const double* V = a.V[k];
+  for (int i = threadIdx.x; i < nq * r; i += blockDim.x) {
+    vs[i] = V[q0 * r + i];
+    wsh[i] = a.st_s ? a.st_s[bd.w_off + q0 * r + i] : 0.0;
+  }
+  __syncthreads();
   const i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  if ((i64)blockIdx.x * blockDim.x >= bd.P) return;
+  if (p >= P) return;
+  // this row's A_prev entries are shared by every column of the chunk
+  double arow[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) arow[i] = (a.st_s && i < r) ? a.st_s[g.a_off[k] + p + (i64)i * P] : 0.0;
   double acc[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) acc[i] = 0.0;
-  const double* V = a.V[k];
-  for (i64 qs = q0; qs < q1; qs += 64) {
-    const i64 qe = min(q1, qs + 64);
-    __syncthreads();
-    for (int i = threadIdx.x; i < (qe - qs) * r; i += blockDim.x) vs[i] = V[qs * r + i];
-    __syncthreads();
-    if (p < bd.P) {
-      for (i64 q = qs; q < qe; ++q) {
-        const double x = ld_elem(a.xb, bd.off + q * bd.P + p, a.dtype);
-        const double ls = a.st_s ? eval_low(a.st_s, g, bd, ip.rows[0], p, q) : 0.0;
-        const double c = x - hard_thr(x - ls, a.zeta);
-        const double* vq = vs + (q - qs) * r;
+  const i64 base = bd.off + q0 * P + p;
+  for (int q = 0; q < nq; q += 4) {
+    double xv[4];
 #pragma unroll
-        for (int i = 0; i < R; ++i)
-          if (i < r) acc[i] = fma(c, vq[i], acc[i]);
-      }
+    for (int u = 0; u < 4; ++u) xv[u] = (q + u < nq) ? ld_elem(a.xb, base + (i64)(q + u) * P, a.dtype) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (q + u >= nq) break;
+      const double* wq = wsh + (q + u) * r;
+      const double* vq = vs + (q + u) * r;
+      double ls = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (i < r) ls = fma(arow[i], wq[i], ls);
+      const double c = xv[u] - hard_thr(xv[u] - ls, a.zeta);
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (i < r) acc[i] = fma(c, vq[i], acc[i]);
     }
   }
-  if (p < bd.P) {
-    double* out = a.part + (((i64)k * a.maxchunks + blockIdx.y) * a.dmax + p) * RT_MAX_RANK;
+  double* out = a.part + (((i64)k * a.maxchunks + blockIdx.y) * a.dmax + p) * RT_MAX_RANK;
 #pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (i < r) out[i] = acc[i];
-  }
+  for (int i = 0; i < R; ++i)
+    if (i < r) out[i] = acc[i];
 }
 
-// A_k[p, a] = siginv_a * sum over chunks (chunk order) of the partials
-__global__ void k_areduce(Geom g, APassArgs a) {
+// A_k[p, a] = siginv_a * sum over chunks (fixed warp-butterfly order) of the partials
+__global__ void __launch_bounds__(256) k_areduce(Geom g, APassArgs a) {
   const int k = blockIdx.y;
   if (k >= g.n) return;
-  const BlockDesc bd = g.blk[k + 1];
+  const BlockDesc& bd = g.blk[k + 1];
   const int r = bd.r;
   const int nch = (int)((bd.Q + a.chunk - 1) / a.chunk);
   double* A = a.st_out + g.a_off[k];
-  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < bd.P * r; e += (i64)gridDim.x * blockDim.x) {
-    const i64 p = e % bd.P;
-    const int i = (int)(e / bd.P);
-    double acc = 0.0;
+  const int lane = threadIdx.x & 31;
+  const i64 nout = bd.P * r;
+  for (i64 o = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < nout; o += ((i64)gridDim.x * blockDim.x) >> 5) {
+    const i64 p = o % bd.P;
+    const int i = (int)(o / bd.P);
     const double* src = a.part + ((i64)k * a.maxchunks * a.dmax + p) * RT_MAX_RANK + i;
-    for (int c = 0; c < nch; ++c) acc += src[(i64)c * a.dmax * RT_MAX_RANK];
-    A[p + (i64)i * bd.P] = acc * a.siginv[k][i];
+    double acc = 0.0;
+    for (int c = lane; c < nch; c += 32) acc += src[(i64)c * a.dmax * RT_MAX_RANK];
+    acc = warp_sum(acc);
+    if (lane == 0) A[p + (i64)i * bd.P] = acc * a.siginv[k][i];
   }
 }
 
@@ -128,18 +146,20 @@ __global__ void __launch_bounds__(256) k_gpass(Geom g, IndexPtrs ip, GPassArgs a
 
 // out = in x_m U_m^T on the small partially-contracted core:
 // in dims (r_1..r_{m-1}, |I_m|, |I_{m+1}|..), out dims (r_1..r_m, |I_{m+1}|..)
-__global__ void k_modeprod(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ U,
-                           i64 rho, int Im, int rm, i64 beta_n) {
+__global__ void __launch_bounds__(256) k_modeprod(const double* __restrict__ in, double* __restrict__ out,
+                                                   const double* __restrict__ U, i64 rho, int Im, int rm, i64 beta_n) {
   const i64 total = rho * rm * beta_n;
-  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (i64 e = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += ((i64)gridDim.x * blockDim.x) >> 5) {
     const i64 alpha = e % rho;
     const i64 rest = e / rho;
     const int aa = (int)(rest % rm);
     const i64 beta = rest / rm;
-    double acc = 0.0;
     const double* src = in + alpha + rho * (i64)Im * beta;
-    for (int i = 0; i < Im; ++i) acc = fma(U[(i64)i * rm + aa], src[rho * i], acc);
-    out[e] = acc;
+    double acc = 0.0;
+    for (int i = lane; i < Im; i += 32) acc = fma(U[(i64)i * rm + aa], src[rho * i], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) out[e] = acc;
   }
 }
 
@@ -148,71 +168,83 @@ __global__ void k_modeprod(const double* __restrict__ in, double* __restrict__ o
 // Per block column q: w[a] = sum over the other modes' rank indices of
 //   G[a, beta] * prod_{m != mode} A_m[i_m(q), beta_m]
 // full = 1: columns run over every (i_2..i_n) of the full tensor (K3 weights).
+// dynamic shared memory: G (gsize doubles) + per thread the other modes' A rows
 template <int R>
 __global__ void __launch_bounds__(128) k_wcols(Geom g, IndexPtrs ip, double* __restrict__ st, int full,
-                                              double* __restrict__ wfull) {
+                                              double* __restrict__ wfull, int rows_per_thread) {
   extern __shared__ double gs[];
   const int b = blockIdx.y;
-  BlockDesc bd;
   i64 Q;
+  int tgt, is_core;
+  i64 w_off;
   if (full) {
-    bd = g.blk[0];
     Q = 1;
     for (int m = 1; m < g.n; ++m) Q *= g.dim[m];
+    tgt = 0;
+    is_core = 1;
+    w_off = 0;
   } else {
     if (b >= g.nblk) return;
-    bd = g.blk[b];
-    Q = bd.Q;
+    Q = g.blk[b].Q;
+    tgt = g.blk[b].mode;
+    is_core = g.blk[b].is_core;
+    w_off = g.blk[b].w_off;
   }
   if ((i64)blockIdx.x * blockDim.x >= Q) return;
   for (i64 i = threadIdx.x; i < g.gsize; i += blockDim.x) gs[i] = st[i];
+  double* rowbuf = gs + g.gsize + (i64)threadIdx.x * rows_per_thread;
   __syncthreads();
   const i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
-  const int tgt = bd.mode;
-  i64 idx[RT_MAX_MODES];
-  if (full) {
-    i64 t = q;
-    for (int m = 1; m < g.n; ++m) { idx[m] = t % g.dim[m]; t /= g.dim[m]; }
-  } else if (bd.is_core) {
-    i64 t = q;
-    for (int m = 1; m < g.n; ++m) {
-      const i64 pos = t % g.nrows[m];
-      t /= g.nrows[m];
-      idx[m] = ip.rows[m][pos];
-    }
-  } else {
-    i64 j = ip.cols[tgt][q];
+  // gather the A_m rows of the other modes (independent loads, all in flight)
+  {
+    i64 t = q, j = 0;
+    if (!full && !is_core) j = ip.cols[tgt][q];
+    int o = 0;
     for (int m = 0; m < g.n; ++m) {
       if (m == tgt) continue;
-      idx[m] = j % g.dim[m];
-      j /= g.dim[m];
+      i64 im;
+      if (full) {
+        im = t % g.dim[m];
+        t /= g.dim[m];
+      } else if (is_core) {
+        const i64 pos = t % g.nrows[m];
+        t /= g.nrows[m];
+        im = ip.rows[m][pos];
+      } else {
+        im = j % g.dim[m];
+        j /= g.dim[m];
+      }
+      const double* Am = st + g.a_off[m] + im;
+      for (int bm = 0; bm < g.rank[m]; ++bm) rowbuf[o + bm] = Am[(i64)bm * g.dim[m]];
+      o += g.rank[m];
     }
   }
-  const double* Abase[RT_MAX_MODES];
-  for (int m = 0; m < g.n; ++m) Abase[m] = st + g.a_off[m] + (m == tgt ? 0 : idx[m]);
   double w[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) w[i] = 0.0;
   i64 combos = 1;
   for (int m = 0; m < g.n; ++m) if (m != tgt) combos *= g.rank[m];
   const int rt = g.rank[tgt];
+  const i64 gst = g.gstride[tgt];
   for (i64 c = 0; c < combos; ++c) {
     i64 t = c, goff = 0;
     double coef = 1.0;
+    int o = 0;
     for (int m = 0; m < g.n; ++m) {
       if (m == tgt) continue;
       const int bm = (int)(t % g.rank[m]);
       t /= g.rank[m];
       goff += bm * g.gstride[m];
-      coef *= Abase[m][(i64)bm * g.dim[m]];
+      coef *= rowbuf[o + bm];
+      o += g.rank[m];
     }
     const double* gp = gs + goff;
 #pragma unroll
     for (int i = 0; i < R; ++i)
-      if (i < rt) w[i] = fma(gp[i * g.gstride[tgt]], coef, w[i]);
+      if (i < rt) w[i] = fma(gp[i * gst], coef, w[i]);
   }
-  double* out = full ? wfull + q * rt : st + bd.w_off + q * rt;
+  double* out = full ? wfull + q * rt : st + w_off + q * rt;
 #pragma unroll
   for (int i = 0; i < R; ++i)
     if (i < rt) out[i] = w[i];
@@ -226,7 +258,7 @@ template __global__ void k_gpass<4>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<8>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<16>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<32>(Geom, IndexPtrs, GPassArgs);
-template __global__ void k_wcols<4>(Geom, IndexPtrs, double*, int, double*);
-template __global__ void k_wcols<8>(Geom, IndexPtrs, double*, int, double*);
-template __global__ void k_wcols<16>(Geom, IndexPtrs, double*, int, double*);
-template __global__ void k_wcols<32>(Geom, IndexPtrs, double*, int, double*);
+template __global__ void k_wcols<4>(Geom, IndexPtrs, double*, int, double*, int);
+template __global__ void k_wcols<8>(Geom, IndexPtrs, double*, int, double*, int);
+template __global__ void k_wcols<16>(Geom, IndexPtrs, double*, int, double*, int);
+template __global__ void k_wcols<32>(Geom, IndexPtrs, double*, int, double*, int);

@@ -12,7 +12,7 @@
 
 #define GRAM_T 64      // output tile edge
 #define GRAM_KS 16     // k-step
-#define GRAM_CL 256    // long-side chunk per CTA (split-K)
+
 
 struct GramArgs {
   int n;
@@ -24,6 +24,7 @@ struct GramArgs {
   double* part;                     // [n][maxchunks][maxpairs][T*T]
   double* K[RT_MAX_MODES];          // packed lower s(s+1)/2
   int maxchunks, maxpairs;
+  int cl;                           // long-side chunk per CTA (split-K), multiple of GRAM_KS
 };
 
 __device__ __forceinline__ double gram_B(const GramArgs& ga, int k, i64 a, i64 t) {
@@ -48,9 +49,9 @@ __global__ void __launch_bounds__(256) k_gram_tiles(GramArgs ga) {
   const int npairs = nt * (nt + 1) / 2;
   const int pair = blockIdx.x;
   if (pair >= npairs) return;
-  const i64 t0 = (i64)blockIdx.y * GRAM_CL;
+  const i64 t0 = (i64)blockIdx.y * ga.cl;
   if (t0 >= l) return;
-  const i64 t1 = min(l, t0 + GRAM_CL);
+  const i64 t1 = min(l, t0 + ga.cl);
   int I, J;
   pair_decode(pair, I, J);
   __shared__ double As[GRAM_KS][GRAM_T + 1];
@@ -91,14 +92,16 @@ __global__ void __launch_bounds__(256) k_gram_tiles(GramArgs ga) {
     for (int j = 0; j < 4; ++j) out[(ty * 4 + i) * GRAM_T + tx + 16 * j] = acc[i][j];
 }
 
-// Sum the split-K partials in chunk order (deterministic) into packed lower K.
-__global__ void k_gram_reduce(GramArgs ga) {
+// Sum the split-K partials (warp per output, fixed butterfly order) into packed lower K.
+__global__ void __launch_bounds__(256) k_gram_reduce(GramArgs ga) {
   const int k = blockIdx.y;
   if (k >= ga.n) return;
   const int s = ga.s[k];
   const i64 npk = (i64)s * (s + 1) / 2;
-  const int nchunks = (int)((ga.l[k] + GRAM_CL - 1) / GRAM_CL);
-  for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < npk; idx += (i64)gridDim.x * blockDim.x) {
+  const int nchunks = (int)((ga.l[k] + ga.cl - 1) / ga.cl);
+  const int lane = threadIdx.x & 31;
+  for (i64 idx = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; idx < npk;
+       idx += ((i64)gridDim.x * blockDim.x) >> 5) {
     int i = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
     while ((i64)(i + 1) * (i + 2) / 2 <= idx) ++i;
     while ((i64)i * (i + 1) / 2 > idx) --i;
@@ -108,7 +111,8 @@ __global__ void k_gram_reduce(GramArgs ga) {
     const int li = i % GRAM_T, lj = j % GRAM_T;
     const double* p = ga.part + ((i64)k * ga.maxchunks * ga.maxpairs + pair) * (GRAM_T * GRAM_T) + li * GRAM_T + lj;
     double acc = 0.0;
-    for (int c = 0; c < nchunks; ++c) acc += p[(i64)c * ga.maxpairs * (GRAM_T * GRAM_T)];
-    ga.K[k][idx] = acc;
+    for (int c = lane; c < nchunks; c += 32) acc += p[(i64)c * ga.maxpairs * (GRAM_T * GRAM_T)];
+    acc = warp_sum(acc);
+    if (lane == 0) ga.K[k][idx] = acc;
   }
 }

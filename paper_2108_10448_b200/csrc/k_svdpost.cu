@@ -47,32 +47,49 @@ __device__ __forceinline__ double svd_B(const SvdArgs& sa, int k, i64 c, i64 t) 
   return sa.tall[k] ? M[t + c * sa.mrows[k]] : M[c + t * sa.mrows[k]];
 }
 
-// Z[t, a] = sum_c B[c, t] E[c, a]
+// Z[t, a] = sum_c B[c, t] E[c, a]: a CTA owns ZP_T long-side columns t; the
+// s x ZP_T slab of B and E (s x r) are staged in shared memory; thread
+// (tl, a) = (tid % ZP_T, tid / ZP_T) reduces over c.
+#define ZP_T 32
 template <int R>
-__global__ void __launch_bounds__(256) k_zproj(SvdArgs sa) {
+__global__ void __launch_bounds__(32 * R) k_zproj(SvdArgs sa) {
   extern __shared__ double es[];
   const int k = blockIdx.y;
   if (k >= sa.n) return;
   const int s = sa.s[k], r = sa.r[k];
   const i64 l = sa.l[k];
-  if ((i64)blockIdx.x * blockDim.x >= l) return;
+  const i64 t0 = (i64)blockIdx.x * ZP_T;
+  if (t0 >= l) return;
+  const int nt = (int)min((i64)ZP_T, l - t0);
+  double* bs = es + s * r;   // s x ZP_T
   for (int i = threadIdx.x; i < s * r; i += blockDim.x) es[i] = sa.E[k][i];
-  __syncthreads();
-  const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= l) return;
-  double z[R];
-#pragma unroll
-  for (int a = 0; a < R; ++a) z[a] = 0.0;
-  for (int c = 0; c < s; ++c) {
-    const double b = svd_B(sa, k, c, t);
-#pragma unroll
-    for (int a = 0; a < R; ++a)
-      if (a < r) z[a] = fma(es[c + a * s], b, z[a]);
+  const double* M = sa.M[k];
+  const i64 mr = sa.mrows[k];
+  if (sa.tall[k]) {
+    // B[c, t] = M[t + c*m]: t contiguous
+    for (int i = threadIdx.x; i < s * ZP_T; i += blockDim.x) {
+      const int tl = i % ZP_T, c = i / ZP_T;
+      bs[c * ZP_T + tl] = tl < nt ? M[t0 + tl + (i64)c * mr] : 0.0;
+    }
+  } else {
+    // B[c, t] = M[c + t*m]: c contiguous
+    for (int i = threadIdx.x; i < s * ZP_T; i += blockDim.x) {
+      const int c = i % s, tl = i / s;
+      bs[c * ZP_T + tl] = tl < nt ? M[c + (t0 + tl) * mr] : 0.0;
+    }
   }
-  double* Z = sa.Z[k] + t * r;
-#pragma unroll
-  for (int a = 0; a < R; ++a)
-    if (a < r) Z[a] = z[a];
+  __syncthreads();
+  const int tl = threadIdx.x % ZP_T, a = threadIdx.x / ZP_T;
+  if (a >= r || tl >= nt) return;
+  const double* ea = es + a * s;
+  double z0 = 0.0, z1 = 0.0;
+  int c = 0;
+  for (; c + 1 < s; c += 2) {
+    z0 = fma(ea[c], bs[c * ZP_T + tl], z0);
+    z1 = fma(ea[c + 1], bs[(c + 1) * ZP_T + tl], z1);
+  }
+  if (c < s) z0 = fma(ea[c], bs[c * ZP_T + tl], z0);
+  sa.Z[k][(t0 + tl) * r + a] = z0 + z1;
 }
 
 // Z <- Z Q (in place, per long-side row)
@@ -102,30 +119,45 @@ __global__ void __launch_bounds__(256) k_zrot(SvdArgs sa) {
     if (a < r) Z[a] = o[a];
 }
 
-// H = Z^T Z: CTA = (chunk of long rows, mode); thread = (a, b) pair with a <= b.
-// Partials per chunk, the last CTA of each mode sums them in chunk order.
-__global__ void __launch_bounds__(576) k_hgram(SvdArgs sa, unsigned int* counters) {
+// H = Z^T Z: CTA = (chunk of HG_CH long rows, mode).  The chunk of Z is staged
+// in shared memory; thread (pair, slice) sums a strided slice of rows; slices
+// are combined in fixed order; the last CTA of each mode combines the chunk
+// partials the same way (deterministic).
+#define HG_CH 128
+__global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counters) {
+  extern __shared__ double hz[];   // HG_CH * r + blockDim
   __shared__ bool am_last;
   const int k = blockIdx.y;
   if (k >= sa.n) return;
   const int r = sa.r[k];
   const i64 l = sa.l[k];
-  const int nch = (int)((l + sa.hchunk - 1) / sa.hchunk);
+  const int nch = (int)((l + HG_CH - 1) / HG_CH);
   if ((int)blockIdx.x >= nch) return;
   const int npair = r * (r + 1) / 2;
+  const int nsl = max(1, (int)blockDim.x / npair);
   const int tid = threadIdx.x;
+  const int pair = tid % npair, sl = tid / npair;
   int a = 0, b = 0;
-  if (tid < npair) {
-    int rem = tid;
+  {
+    int rem = pair;
     while (rem >= r - a) { rem -= r - a; ++a; }
     b = a + rem;
   }
-  const i64 t0 = (i64)blockIdx.x * sa.hchunk, t1 = min(l, t0 + sa.hchunk);
+  double* red = hz + HG_CH * r;
+  const i64 t0 = (i64)blockIdx.x * HG_CH;
+  const int nt = (int)min((i64)HG_CH, l - t0);
+  const double* Z = sa.Z[k] + t0 * r;
+  for (int i = tid; i < nt * r; i += blockDim.x) hz[i] = Z[i];
+  __syncthreads();
+  double acc = 0.0;
+  if (sl < nsl)
+    for (int t = sl; t < nt; t += nsl) acc = fma(hz[t * r + a], hz[t * r + b], acc);
+  red[tid] = acc;
+  __syncthreads();
   if (tid < npair) {
-    double acc = 0.0;
-    const double* Z = sa.Z[k];
-    for (i64 t = t0; t < t1; ++t) acc = fma(Z[t * r + a], Z[t * r + b], acc);
-    sa.hpart[k][(i64)blockIdx.x * npair + tid] = acc;
+    double v = 0.0;
+    for (int q = 0; q < nsl; ++q) v += red[q * npair + tid];
+    sa.hpart[k][(i64)blockIdx.x * npair + tid] = v;
   }
   __threadfence();
   __syncthreads();
@@ -133,11 +165,16 @@ __global__ void __launch_bounds__(576) k_hgram(SvdArgs sa, unsigned int* counter
   __syncthreads();
   if (!am_last) return;
   __threadfence();
+  acc = 0.0;
+  if (sl < nsl)
+    for (int c = sl; c < nch; c += nsl) acc += ((volatile double*)sa.hpart[k])[(i64)c * npair + pair];
+  red[tid] = acc;
+  __syncthreads();
   if (tid < npair) {
-    double acc = 0.0;
-    for (int c = 0; c < nch; ++c) acc += ((volatile double*)sa.hpart[k])[(i64)c * npair + tid];
-    sa.H[k][a + b * r] = acc;
-    sa.H[k][b + a * r] = acc;
+    double v = 0.0;
+    for (int q = 0; q < nsl; ++q) v += red[q * npair + tid];
+    sa.H[k][a + b * r] = v;
+    sa.H[k][b + a * r] = v;
   }
   if (tid == 0) counters[k] = 0u;
 }
@@ -228,15 +265,22 @@ __global__ void k_short_vecs(SvdArgs sa) {
 __global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
   __shared__ double h[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ double R[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ double T[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ double X[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ double sg[RT_MAX_RANK];
   __shared__ int ord[RT_MAX_RANK], dg[RT_MAX_RANK];
   const int k = blockIdx.x;
   if (k >= sa.n) return;
   const int r = sa.r[k], lane = threadIdx.x;
-  for (int i = lane; i < r * r; i += 32) h[i] = sa.H[k][i];
+  for (int i = lane; i < r * r; i += 32) {
+    h[i] = sa.H[k][i];
+    R[i] = 0.0;
+    T[i] = 0.0;
+  }
+  __syncwarp();
+  if (lane < r) sg[lane] = sqrt(fmax(h[lane + lane * r], 0.0));
   __syncwarp();
   if (lane == 0) {
-    for (int a = 0; a < r; ++a) sg[a] = sqrt(fmax(h[a + a * r], 0.0));
     for (int i = 0; i < r; ++i) ord[i] = i;
     for (int i = 1; i < r; ++i) {
       const int t = ord[i];
@@ -244,59 +288,66 @@ __global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
       while (j >= 0 && sg[ord[j]] < sg[t]) { ord[j + 1] = ord[j]; --j; }
       ord[j + 1] = t;
     }
-    const double s1 = sg[ord[0]];
-    const double mx = (double)(sa.mrows[k] > sa.pcols[k] ? sa.mrows[k] : sa.pcols[k]);
-    const double tau = mx * s1 * 1e-12;   // linalg.py:54
-    int anyd = 0;
-    for (int a = 0; a < r; ++a) {
-      const double sv = sg[ord[a]];
-      sa.sig[k][a] = sv;
-      sa.siginv[k][a] = sv > tau ? 1.0 / sv : 0.0;
-      sa.perm[k][a] = ord[a];
-      dg[a] = !(sv > tau);
-    }
+  }
+  __syncwarp();
+  const double s1 = sg[ord[0]];
+  const double mx = (double)(sa.mrows[k] > sa.pcols[k] ? sa.mrows[k] : sa.pcols[k]);
+  const double tau = mx * s1 * 1e-12;   // linalg.py:54
+  if (lane < r) {
+    const double sv = sg[ord[lane]];
+    sa.sig[k][lane] = sv;
+    sa.siginv[k][lane] = sv > tau ? 1.0 / sv : 0.0;
+    sa.perm[k][lane] = ord[lane];
+    dg[lane] = !(sv > tau);
+  }
+  if (lane == 0) {
     // flags: solver.py:252-257 (sigma_1 <= 0 or sigma_r <= 1e-8 sigma_1)
     sa.flags[k] = (s1 <= 0.0 || sg[ord[r - 1]] <= 1e-8 * s1) ? 1 : 0;
-    // Cholesky of C = D^-1 P^T H P D^-1 on non-degenerate columns (sorted order)
-    for (int i = 0; i < r * r; ++i) R[i] = 0.0;
-    for (int j = 0; j < r; ++j) {
-      if (dg[j]) continue;
-      const int oj = ord[j];
-      for (int i = 0; i <= j; ++i) {
-        if (dg[i]) continue;
+  }
+  __syncwarp();
+  // Cholesky of C = D^-1 P^T H P D^-1 on non-degenerate columns (column by column;
+  // lanes own rows i of column j)
+  for (int j = 0; j < r; ++j) {
+    if (dg[j]) continue;
+    const int oj = ord[j];
+    for (int i = 0; i <= j; ++i) {
+      if (dg[i]) continue;
+      if (lane == 0) {
         const int oi = ord[i];
         double c = h[oi + oj * r] / (sg[oi] * sg[oj]);
         for (int p = 0; p < i; ++p) c -= R[p + i * r] * R[p + j * r];
         if (i == j) {
-          if (c <= 1e-6) { dg[j] = 1; break; }   // numerically dependent: complete instead
-          R[j + j * r] = sqrt(c);
+          if (c <= 1e-6) dg[j] = 1;   // numerically dependent: complete instead
+          else R[j + j * r] = sqrt(c);
         } else {
           R[i + j * r] = c / R[i + i * r];
         }
       }
+      __syncwarp();
+      if (dg[j]) break;
     }
-    // T = P D^-1 R^-1 (upper triangular inverse by back substitution), stored in Q
-    double* T = sa.Q[k];
-    for (int i = 0; i < r * r; ++i) T[i] = 0.0;
-    for (int j = 0; j < r; ++j) {
-      if (dg[j]) continue;
-      // column j of R^-1: solve R x = e_j over non-degenerate indices <= j
-      double x[RT_MAX_RANK];
-      for (int i = j; i >= 0; --i) {
-        if (dg[i]) { x[i] = 0.0; continue; }
-        double v = (i == j) ? 1.0 : 0.0;
-        for (int p = i + 1; p <= j; ++p) if (!dg[p]) v -= R[i + p * r] * x[p];
-        x[i] = v / R[i + i * r];
-      }
-      for (int i = 0; i <= j; ++i)
-        if (!dg[i]) T[ord[i] + j * r] = x[i] / sg[ord[i]];
-    }
-    for (int a = 0; a < r; ++a) {
-      sa.degen[k][a] = dg[a];
-      anyd |= dg[a];
-    }
-    sa.degen[k][r] = anyd;
   }
+  __syncwarp();
+  // T = P D^-1 R^-1: lane j solves R x = e_j (upper triangular) for column j
+  if (lane < r && !dg[lane]) {
+    const int j = lane;
+    double* x = X + j * r;
+    for (int i = j; i >= 0; --i) {
+      if (dg[i]) { x[i] = 0.0; continue; }
+      double v = (i == j) ? 1.0 : 0.0;
+      for (int p = i + 1; p <= j; ++p)
+        if (!dg[p]) v -= R[i + p * r] * x[p];
+      x[i] = v / R[i + i * r];
+    }
+    for (int i = 0; i <= j; ++i)
+      if (!dg[i]) T[ord[i] + j * r] = x[i] / sg[ord[i]];
+  }
+  __syncwarp();
+  for (int i = lane; i < r * r; i += 32) sa.Q[k][i] = T[i];
+  int anyd = 0;
+  for (int a = 0; a < r; ++a) anyd |= dg[a];
+  if (lane < r) sa.degen[k][lane] = dg[lane];
+  if (lane == 0) sa.degen[k][r] = anyd;
 }
 
 // long-side vectors: out[t, a] = sum_b Z[t, b] T[b, a]; short side permuted in place later

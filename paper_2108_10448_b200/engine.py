@@ -118,6 +118,16 @@ class Engine:
         s = np.frombuffer(sums, dtype=np.float64).copy()
         return s[0::2], s[1::2], tuple(bool(f) for f in flags)
 
+    def iterate_async(self, zeta: float, first: bool):
+        nat.check(self.lib.rtcur_engine_iterate_async(self.handle, float(zeta), int(bool(first))))
+
+    def iterate_wait(self):
+        sums = (ctypes.c_double * (2 * (self.n + 1)))()
+        flags = (ctypes.c_int32 * self.n)()
+        nat.check(self.lib.rtcur_engine_iterate_wait(self.handle, sums, flags))
+        s = np.frombuffer(sums, dtype=np.float64).copy()
+        return s[0::2], s[1::2], tuple(bool(f) for f in flags)
+
     def export_blocks(self, want_s=True, want_clean=True, want_l=False):
         """Device fp64 tensors (N_blk) of S, X - S and L_new on the compact blocks."""
         import torch

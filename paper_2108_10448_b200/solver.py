@@ -359,10 +359,15 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
     history, flags = [], []
     trace = [] if record_trace else None
     converged = False
+    # RTCUR-R draws the next sample while the GPU runs the current iteration:
+    # the generator is consumed by sampling only, so drawing ahead leaves every
+    # index set identical to the reference's (solver.py:315-317).
+    next_idx = None
     for k in range(1, cfg.max_iters + 1):
         if cfg.variant == "R" and k >= 2:
             t0 = time.perf_counter()
-            idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+            idx = next_idx if next_idx is not None else draw_sample_indices(shape, row_sizes, col_sizes, rng)
+            next_idx = None
             timings["sample"] += time.perf_counter() - t0
             t0 = time.perf_counter()
             eng.set_sample(idx)
@@ -370,7 +375,12 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
             timings["gather"] += time.perf_counter() - t0
         zeta *= cfg.gamma
         t0 = time.perf_counter()
-        e2, x2, fl = eng.iterate(zeta, first=(k == 1))
+        eng.iterate_async(zeta, first=(k == 1))
+        if cfg.variant == "R" and k < cfg.max_iters:
+            t1 = time.perf_counter()
+            next_idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+            timings["sample"] += time.perf_counter() - t1
+        e2, x2, fl = eng.iterate_wait()
         timings["build"] += time.perf_counter() - t0
         err = _error_from_sums(e2, x2)
         history.append(err)
