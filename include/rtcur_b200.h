@@ -123,6 +123,12 @@ int64_t rtcur_engine_full_scratch_bytes(rtcur_engine* e);
 int rtcur_engine_profile(rtcur_engine* e, int on);
 int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* counts, int nphase, int reset);
 
+/* Host helper of the index sampler (fiber_cur.py:202-208): append the values of
+ * batch not yet marked in seen (population bytes) to out, in first-occurrence
+ * order; returns the new length (-1 if a value is out of range). */
+int64_t rtcur_append_distinct(int64_t* out, int64_t nout, const int64_t* batch, int64_t nb, unsigned char* seen,
+                              int64_t population);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,8 @@ static int wcols_rows_per_thread(const Geom& g) {
 }
 static int wcols_smem(const Geom& g) { return (int)((g.gsize + 128 * wcols_rows_per_thread(g)) * 8); }
 
+#define BP_GRID (148 * 2)   // persistent block-pass CTAs (2 per SM)
+
 static int rbucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32; }
 
 #define DISPATCH_R(RB, KERNEL, GRID, BLOCK, SMEM, STREAM, ...)                     \
@@ -105,13 +107,14 @@ struct Plan {
   i64 dmax, lmax, smax, qmax;
   i64 g_tmp;         // doubles per G temp buffer
   int hchunk, h_maxchunks;
+  BPGeom bp;
   // workspace offsets (bytes)
   i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
   i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES],
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
       o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_apart, o_gt0, o_gt1, o_bpart, o_sums,
-      o_fpart, o_dbg;
+      o_fpart, o_dbg, o_fast;
   i64 total;
 };
 
@@ -177,6 +180,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     BlockDesc& b = g.blk[k + 1];
     b.P = dims[k];
     b.Q = col_sizes[k];
+    off = (off + 3) & ~(i64)3;   // 16-byte aligned block start (TMA bulk copies)
     b.off = off;
     b.mode = k;
     b.is_core = 0;
@@ -198,12 +202,46 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   // tiles
   TileMap& tm = P.tm;
   tm.nblk = g.nblk;
-  tm.tile = 4096;
+  // Block-pass shared memory: A rows of both states for the largest block,
+  // the intersection row map, and a ring of x/W tile stages in what is left.
+  {
+    i64 maxP = 1, maxArows = 1;
+    for (int b = 0; b < g.nblk; ++b) {
+      maxP = std::max(maxP, g.blk[b].P);
+      maxArows = std::max(maxArows, g.blk[b].P * (i64)bp_rp(g.blk[b].r));
+    }
+    if (maxP > TILE_MAX_ELEMS) return fail(RT_ERR_UNSUPPORTED, "mode extent above 4096 not supported");
+    BPGeom& G = P.bp;
+    G.rowmap_ints = (int)maxP;
+    // two CTAs per SM when the staged A rows leave room for 3 stages of >= 16 KB
+    const i64 rowmap_b = (G.rowmap_ints * 4 + 15) & ~15;
+    const i64 a_b = 2 * maxArows * 8;
+    i64 cta_budget = 100 * 1024;
+    G.a_doubles = (int)maxArows;
+    if (cta_budget - a_b - rowmap_b - 512 < 3 * 16 * 1024) cta_budget = 227 * 1024;   // one CTA per SM
+    if (cta_budget - a_b - rowmap_b - 512 < 3 * 16 * 1024) {
+      G.a_doubles = 0;                                                               // A from global (L1)
+      cta_budget = 100 * 1024;
+    }
+    const i64 budget = cta_budget - 2 * (i64)G.a_doubles * 8 - rowmap_b - 512;
+    G.stages = 3;
+    const i64 stage = budget / G.stages;
+    // x bytes per stage: whole columns of the largest P, at most TILE_MAX_ELEMS elements
+    G.x_bytes = (int)std::min<i64>((i64)TILE_MAX_ELEMS * P.esize + 32, (stage * 3 / 4) & ~15LL);
+    G.w_doubles = (int)(((stage - G.x_bytes) / 2 / 8) & ~1LL);
+    G.rp_max = bp_rp(P.rmax);
+  }
+  tm.tile = TILE_MAX_ELEMS;
   i64 t = 0;
   for (int b = 0; b < g.nblk; ++b) {
     tm.first[b] = t;
-    tm.cpt[b] = std::max<i64>(1, tm.tile / g.blk[b].P);
-    t += cdiv(g.blk[b].Q, tm.cpt[b]);
+    const i64 Pb = g.blk[b].P, nel = Pb * g.blk[b].Q;
+    // whole columns; bounded by the stage's x bytes and W rows
+    i64 cpt = std::max<i64>(1, (P.bp.x_bytes - 32) / (Pb * P.esize));
+    cpt = std::min<i64>(cpt, std::max<i64>(1, (P.bp.w_doubles - 4) / g.blk[b].r));
+    cpt = std::min<i64>(cpt, std::max<i64>(1, TILE_MAX_ELEMS / Pb));
+    tm.te[b] = cpt * Pb;
+    t += cdiv(nel, tm.te[b]);
   }
   tm.first[g.nblk] = t;
   P.col_off[0] = 0;
@@ -269,7 +307,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_colR = take(P.col_off[g.nblk] * 8);
   P.o_coli1 = take(P.col_off[g.nblk] * 4);
   P.o_coloff = take((RT_MAX_BLOCKS + 1) * 8);
-  P.o_xb = take(g.nblk_total * P.esize);
+  P.o_xb = take(g.nblk_total * P.esize + 64);   // +64: aligned bulk-copy supersets may read past the end
   P.o_state = take(3 * g.state_doubles * 8);
   for (int m = 0; m < n; ++m) P.o_M[m] = take(row_sizes[m] * col_sizes[m] * 8);
   P.o_gpart = take((i64)n * P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
@@ -296,10 +334,11 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_apart = take((i64)n * P.a_maxchunks * P.dmax * RT_MAX_RANK * 8);
   P.o_gt0 = take(P.g_tmp * 8);
   P.o_gt1 = take(P.g_tmp * 8);
-  P.o_bpart = take(tm.first[g.nblk] * 2 * 8);
+  P.o_bpart = take((i64)BP_GRID * g.nblk * 2 * 8 + 64);
   P.o_sums = take(2 * g.nblk * 8);
   P.o_fpart = take(148 * 8 * 2 * 8);
   P.o_dbg = take(8 * RT_MAX_MODES * 8);
+  P.o_fast = take(RT_MAX_MODES * 4);
   P.total = o;
   return RT_OK;
 }
@@ -318,6 +357,7 @@ struct rtcur_engine {
   int sample_epoch; // bumped by every rtcur_engine_set_sample
   int w_epoch[3];   // sample epoch each slot's W (column weights) was built for
   bool pending;     // an iterate_async awaits its iterate_wait
+  bool use_fast;    // allow the warm-started subspace-iteration eigensolver
   cudaEvent_t done; // recorded after the iteration's result copies
   int prev;         // ring slot of the one before (-1: none, i.e. latest is iteration 1)
   double zeta_last;
@@ -392,8 +432,14 @@ static IndexPtrs make_ip(const rtcur_engine* e) {
   return ip;
 }
 
+// the warm-started fast path needs extra scratch; used only when it fits
+static int eig_fast_ok(const Plan& P, int m) {
+  const int s = (int)P.s[m], r = P.g.rank[m];
+  return !P.tall[m] && eig_smem_doubles(s, r, P.nb[m], eig_pick_full(s, r), 1) <= EIG_SMEM_DOUBLES;
+}
 static int eig_smem_bytes(const Plan& P, int m) {
-  return (int)(eig_smem_doubles((int)P.s[m], P.g.rank[m], P.nb[m], eig_pick_full((int)P.s[m], P.g.rank[m])) * 8);
+  const int s = (int)P.s[m], r = P.g.rank[m];
+  return (int)(eig_smem_doubles(s, r, P.nb[m], eig_pick_full(s, r), eig_fast_ok(P, m)) * 8);
 }
 
 extern "C" int rtcur_engine_plan(int n, const int64_t* dims, const int32_t* ranks, const int64_t* row_sizes,
@@ -425,6 +471,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->lo = slab_lo;
   e->hi = slab_hi;
   e->cur = e->prev = -1;
+  e->use_fast = getenv("RTCUR_NO_FAST_EIG") == nullptr;
   e->prof_pool = new std::vector<cudaEvent_t>();
   if (cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming) != cudaSuccess) {
     delete e;
@@ -447,6 +494,17 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   int maxe = 0;
   for (int m = 0; m < n; ++m) maxe = std::max(maxe, eig_smem_bytes(e->P, m));
   CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(maxe, 48 * 1024)));
+  {
+    const int smb = (int)bp_smem_bytes(e->P.bp);
+    CK(cudaFuncSetAttribute(k_block_pass<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    CK(cudaFuncSetAttribute(k_block_pass<true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    CK(cudaFuncSetAttribute(k_block_pass<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    CK(cudaFuncSetAttribute(k_block_pass<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    CK(cudaFuncSetAttribute(k_block_pass<true, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    CK(cudaFuncSetAttribute(k_block_pass<false, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    CK(cudaFuncSetAttribute(k_block_pass<true, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    CK(cudaFuncSetAttribute(k_block_pass<false, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+  }
   const int gs = wcols_smem(e->P.g);
   CK(cudaFuncSetAttribute(k_wcols<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
   CK(cudaFuncSetAttribute(k_wcols<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
@@ -598,7 +656,22 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   }
   a.nonfinite = e->at<int>(P.o_nonfinite);
   prof_begin(e, phase);
-  k_block_pass<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, a);
+  const i64 smb = bp_smem_bytes(P.bp);
+  const unsigned per_sm = smb <= 110 * 1024 ? 2 : 1;
+  const unsigned grid = (unsigned)std::min<i64>(148 * per_sm, P.tm.first[P.g.nblk]);
+  const bool hs = st_s != nullptr, he = st_e != nullptr;
+  if (s_out || c_out || l_out) {
+    if (hs && he) k_block_pass<true, true, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    else if (hs) k_block_pass<true, false, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    else if (he) k_block_pass<false, true, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    else k_block_pass<false, false, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+  } else if (with_M) {
+    if (hs) k_block_pass<true, false, true, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    else k_block_pass<false, false, true, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+  } else {
+    if (hs) k_block_pass<true, true, false, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    else k_block_pass<false, true, false, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+  }
   LAUNCH_CHECK();
   prof_end(e, phase);
   return RT_OK;
@@ -635,7 +708,7 @@ static SvdArgs make_svd_args(rtcur_engine* e) {
 }
 
 // rank-r truncated SVD of every mode's intersection M_k (already in the workspace)
-static int run_svd(rtcur_engine* e) {
+static int run_svd(rtcur_engine* e, const double* warm_state) {
   const Plan& P = e->P;
   const int n = P.g.n;
   GramArgs ga;
@@ -677,6 +750,15 @@ static int run_svd(rtcur_engine* e) {
     esm = std::max(esm, eig_smem_bytes(P, m));
   }
   ea.tmark = e->at<long long>(P.o_dbg);
+  ea.max_sub_steps = 24;
+  ea.fast_used = e->at<int>(P.o_fast);
+  IndexPtrs ipw = make_ip(e);
+  for (int m = 0; m < n; ++m) {
+    // fast path only for wide intersections (short side = rows I_k) with a previous iterate
+    ea.warmA[m] = (warm_state && eig_fast_ok(P, m) && e->use_fast) ? warm_state + P.g.a_off[m] : nullptr;
+    ea.warm_rows[m] = ipw.rows[m];
+    ea.warm_d[m] = P.g.dim[m];
+  }
   prof_begin(e, PH_EIG);
   k_eig<<<n, EIG_THREADS, esm, e->st>>>(ea);
   LAUNCH_CHECK();
@@ -809,7 +891,7 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
     e->w_epoch[e->cur] = e->sample_epoch;
   }
   if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false, PH_THRESH))) return st;
-  if ((st = run_svd(e))) return st;
+  if ((st = run_svd(e, st_s))) return st;
   if ((st = run_factors(e, st_s, zeta, newslot))) return st;
   if ((st = run_block_pass(e, st_s, e->state(newslot), zeta, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
     return st;
@@ -926,6 +1008,11 @@ extern "C" int rtcur_engine_debug_marks(rtcur_engine* e, int64_t* out, int n) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
   CK(cudaStreamSynchronize(e->st));
   CK(cudaMemcpy(out, e->ws + e->P.o_dbg, sizeof(int64_t) * std::min(n, 8 * RT_MAX_MODES), cudaMemcpyDeviceToHost));
+  if (n >= 8 * RT_MAX_MODES + RT_MAX_MODES) {
+    int f[RT_MAX_MODES];
+    CK(cudaMemcpy(f, e->ws + e->P.o_fast, sizeof(int) * RT_MAX_MODES, cudaMemcpyDeviceToHost));
+    for (int m = 0; m < RT_MAX_MODES; ++m) out[8 * RT_MAX_MODES + m] = f[m];
+  }
   return RT_OK;
 }
 
@@ -948,6 +1035,26 @@ extern "C" int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* c
   if (reset)
     for (int i = 0; i < RT_NPHASE; ++i) { e->prof_ms[i] = 0.0; e->prof_cnt[i] = 0; }
   return RT_OK;
+}
+
+// ------------------------------------------------------------------ host helpers
+
+// Append to out[0..nout) the values of batch[0..nb) not seen before, in order of
+// first occurrence (seen: population-byte bitmap kept by the caller).  This is
+// the deduplication of the reference's iid draw (fiber_cur.py:202-208:
+// np.unique(..., return_index=True) then merged[np.sort(first)]) in O(n); the
+// random stream itself stays numpy's Generator.integers.
+extern "C" int64_t rtcur_append_distinct(int64_t* out, int64_t nout, const int64_t* batch, int64_t nb,
+                                         unsigned char* seen, int64_t population) {
+  for (int64_t i = 0; i < nb; ++i) {
+    const int64_t v = batch[i];
+    if (v < 0 || v >= population) return -1;
+    if (!seen[v]) {
+      seen[v] = 1;
+      out[nout++] = v;
+    }
+  }
+  return nout;
 }
 
 // ------------------------------------------------------------------ kernel-level plug

@@ -39,14 +39,22 @@ struct EigArgs {
   int nb[RT_MAX_MODES];            // inverse-iteration batch (vectors factored at once)
   int full[RT_MAX_MODES];          // 1: full-storage tridiagonalisation
   long long* tmark;                // optional: per-matrix clock64 marks at phase boundaries (8 each)
+  // warm start for the subspace-iteration fast path (null: full solver only)
+  const double* warmA[RT_MAX_MODES];   // previous iterate's A_k (d_k x r_k, column-major)
+  const int* warm_rows[RT_MAX_MODES];  // current row set I_k (0-based)
+  i64 warm_d[RT_MAX_MODES];
+  int max_sub_steps;
+  int* fast_used;                      // per mode: 1 if the fast path certified the subspace
 };
 
 __host__ __device__ inline int eig_ld(int s) { return s | 1; }
 
 // doubles of shared memory k_eig needs for (s, r, nb, layout)
-__host__ __device__ inline long long eig_smem_doubles(int s, int r, int nb, int full) {
+// sub: reserve the subspace-iteration scratch (Y: s x r, three r x r) after the LU area
+__host__ __device__ inline long long eig_smem_doubles(int s, int r, int nb, int full, int sub = 0) {
   const long long amat = full ? (long long)s * eig_ld(s) + (long long)s * (s - 1) / 2 : (long long)s * (s + 1) / 2;
-  return amat + (long long)s * r + 8LL * s + 8 + 2LL * r + 96 + (long long)nb * 4 * s + ((long long)nb * s + 7) / 8;
+  return amat + (long long)s * r + 8LL * s + 8 + 2LL * r + 96 + (long long)nb * 4 * s + ((long long)nb * s + 7) / 8 +
+         8 + (sub ? (long long)s * r + 3LL * r * r : 0);
 }
 
 __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // i >= j
@@ -122,6 +130,192 @@ __device__ __forceinline__ double group_sum8(double v) {
   return v;
 }
 
+// ---------------------------------------------------------------- subspace iteration
+// Top-r invariant subspace of the PSD Gram K (resident in shared memory, full or
+// packed) by block power iteration from a warm start X0 = A_prev(I, :), with
+// Cholesky-QR (twice) orthonormalisation.  Certified when
+//     ||K X - X H||_F <= 1e-12 * delta,   delta = lambda_min(H) - (tr K - tr H)
+// where H = X^T K X: for PSD K every eigenvalue outside the top r is at most
+// tr K - tr(top-r) <= tr K - tr H, so delta lower-bounds the spectral gap and
+// the subspace angle is <= 1e-12 (Davis-Kahan sin-theta).  Returns false
+// (caller falls back to the full solver) otherwise.  Block-uniform result.
+__device__ __forceinline__ double eig_kval(const double* A, bool full, int ld, int i, int j) {
+  return full ? A[i * ld + j] : (i >= j ? A[pk(i, j)] : A[pk(j, i)]);
+}
+
+// Cholesky-QR of X (s x r, column-major): X <- X R^-1.  false if not SPD.
+__device__ bool eig_cholqr(double* X, int s, int r, double* C, double* red, double* scal) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int np = r * (r + 1) / 2;
+  for (int q = wid; q < np; q += nw) {
+    int a = 0, rem = q;
+    while (rem >= r - a) { rem -= r - a; ++a; }
+    const int b = a + rem;
+    double d = 0.0;
+    for (int i = lane; i < s; i += 32) d = fma(X[a * s + i], X[b * s + i], d);
+    d = warp_sum(d);
+    if (lane == 0) { C[a + b * r] = d; C[b + a * r] = d; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // in-place upper Cholesky C = R^T R (R stored in the upper triangle of C)
+    bool ok = true;
+    const double c00 = C[0];
+    for (int j = 0; j < r && ok; ++j) {
+      for (int i = 0; i <= j; ++i) {
+        double v = C[i + j * r];
+        for (int k = 0; k < i; ++k) v -= C[k + i * r] * C[k + j * r];
+        if (i == j) {
+          if (!(v > 1e-28 * c00)) { ok = false; break; }
+          C[j + j * r] = sqrt(v);
+        } else {
+          C[i + j * r] = v / C[i + i * r];
+        }
+      }
+    }
+    scal[8] = ok ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (scal[8] == 0.0) return false;
+  // rows: x R = x_old  (forward substitution over columns)
+  for (int i = tid; i < s; i += blockDim.x) {
+    double xr[RT_MAX_RANK];
+    for (int j = 0; j < r; ++j) {
+      double v = X[j * s + i];
+      for (int k = 0; k < j; ++k) v -= xr[k] * C[k + j * r];
+      xr[j] = v / C[j + j * r];
+    }
+    for (int j = 0; j < r; ++j) X[j * s + i] = xr[j];
+  }
+  __syncthreads();
+  (void)red;
+  return true;
+}
+
+__device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, double* X, double* Y, double* H,
+                             double* C, double* Rm, double* red, double* red2, double* scal, const double* warmA,
+                             const int* rows, i64 d, int max_steps) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  // trace of K and the warm start
+  double t = 0.0;
+  for (int i = tid; i < s; i += blockDim.x) t += eig_kval(A, full, ld, i, i);
+  t = warp_sum(t);
+  if (lane == 0) red[wid] = t;
+  for (int e = tid; e < s * r; e += blockDim.x) {
+    const int i = e % s, c = e / s;
+    X[e] = warmA[rows[i] + (i64)c * d];
+  }
+  __syncthreads();
+  const double trK = warp_sum_of(red, nw);
+  if (!(trK > 0.0)) return false;
+  for (int rep = 0; rep < 2; ++rep)
+    if (!eig_cholqr(X, s, r, C, red, scal)) return false;
+  for (int step = 0; step < max_steps; ++step) {
+    // Y = K X
+    for (int e = tid; e < s * r; e += blockDim.x) {
+      const int i = e % s, c = e / s;
+      const double* x = X + c * s;
+      double a0 = 0.0, a1 = 0.0;
+      int j = 0;
+      if (full) {
+        const double* row = A + i * ld;
+        for (; j + 1 < s; j += 2) {
+          a0 = fma(row[j], x[j], a0);
+          a1 = fma(row[j + 1], x[j + 1], a1);
+        }
+        if (j < s) a0 = fma(row[j], x[j], a0);
+      } else {
+        for (; j < s; ++j) a0 = fma(eig_kval(A, false, ld, i, j), x[j], a0);
+      }
+      Y[e] = a0 + a1;
+    }
+    __syncthreads();
+    // H = X^T Y (symmetrised)
+    const int np = r * (r + 1) / 2;
+    for (int q = wid; q < np; q += nw) {
+      int a = 0, rem = q;
+      while (rem >= r - a) { rem -= r - a; ++a; }
+      const int b = a + rem;
+      double d1 = 0.0, d2 = 0.0;
+      for (int i = lane; i < s; i += 32) {
+        d1 = fma(X[a * s + i], Y[b * s + i], d1);
+        d2 = fma(X[b * s + i], Y[a * s + i], d2);
+      }
+      const double hv = 0.5 * (warp_sum(d1) + warp_sum(d2));
+      if (lane == 0) { H[a + b * r] = hv; H[b + a * r] = hv; }
+    }
+    __syncthreads();
+    // residual ||Y - X H||_F^2 and tr H
+    double rn = 0.0;
+    for (int e = tid; e < s * r; e += blockDim.x) {
+      const int i = e % s, c = e / s;
+      double v = Y[e];
+      for (int k = 0; k < r; ++k) v -= X[k * s + i] * H[k + c * r];
+      rn = fma(v, v, rn);
+    }
+    rn = warp_sum(rn);
+    if (lane == 0) red2[wid] = rn;
+    __syncthreads();
+    const double res = sqrt(warp_sum_of(red2, nw));
+    double trH = 0.0;
+    for (int c = 0; c < r; ++c) trH += H[c + c * r];
+    // lambda_min(H) <= tr H / r: if even that cannot exceed the energy outside the
+    // subspace, the gap bound can never certify -> give up at once (full solver)
+    if (!(trH / r - (trK - trH) > 0.0)) return false;
+    // certify (one warp runs Jacobi for lambda_min(H) only when the residual is small)
+    if (res <= 1e-9 * trK) {
+      if (wid == 0) {
+        for (int e = lane; e < r * r; e += 32) Rm[e] = H[e];
+        __syncwarp();
+        for (int sweep = 0; sweep < 30; ++sweep) {
+          double off = 0.0;
+          for (int e = lane; e < r * r; e += 32)
+            if (e % r != e / r) off += Rm[e] * Rm[e];
+          off = warp_sum(off);
+          if (off <= 1e-32 * trH * trH) break;
+          for (int p = 0; p < r - 1; ++p)
+            for (int qq = p + 1; qq < r; ++qq) {
+              const double apq = Rm[p + qq * r];
+              if (apq == 0.0) continue;
+              const double app = Rm[p + p * r], aqq = Rm[qq + qq * r];
+              const double th = (aqq - app) / (2.0 * apq);
+              const double tt = copysign(1.0, th) / (fabs(th) + sqrt(th * th + 1.0));
+              const double cs = 1.0 / sqrt(tt * tt + 1.0), sn = tt * cs;
+              __syncwarp();
+              if (lane < r) {
+                const double hp = Rm[lane + p * r], hq = Rm[lane + qq * r];
+                Rm[lane + p * r] = cs * hp - sn * hq;
+                Rm[lane + qq * r] = sn * hp + cs * hq;
+              }
+              __syncwarp();
+              if (lane < r) {
+                const double hp = Rm[p + lane * r], hq = Rm[qq + lane * r];
+                Rm[p + lane * r] = cs * hp - sn * hq;
+                Rm[qq + lane * r] = sn * hp + cs * hq;
+              }
+              __syncwarp();
+            }
+        }
+        if (lane == 0) {
+          double lmin = Rm[0];
+          for (int c = 1; c < r; ++c) lmin = fmin(lmin, Rm[c + c * r]);
+          const double delta = lmin - (trK - trH);
+          scal[9] = (delta > 0.0 && res <= 1e-12 * delta) ? 1.0 : (delta > 0.0 ? 0.0 : -1.0);
+        }
+      }
+      __syncthreads();
+      if (scal[9] > 0.0) return true;
+    }
+    if (step + 1 == max_steps) break;
+    // X <- orth(Y)
+    for (int e = tid; e < s * r; e += blockDim.x) X[e] = Y[e];
+    __syncthreads();
+    for (int rep = 0; rep < 2; ++rep)
+      if (!eig_cholqr(X, s, r, C, red, scal)) return false;
+  }
+  return false;
+}
+
 extern __shared__ double eig_smem[];
 
 __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
@@ -150,6 +344,10 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
   double* scal = red2 + 32;                                        // 32
   double* lu = scal + 32;                                          // nb * 4s
   unsigned char* piv = reinterpret_cast<unsigned char*>(lu + (size_t)nb * 4 * s);
+  double* Ysub = lu + (size_t)nb * 4 * s + ((size_t)nb * s + 7) / 8 + 8;   // s x r (subspace iteration)
+  double* Hs = Ysub + s * r;                                       // r x r
+  double* Cs = Hs + r * r;                                         // r x r
+  double* Rs = Cs + r * r;                                         // r x r
   (void)ww;
 
   long long* tm = ea.tmark ? ea.tmark + 8 * mi : nullptr;
@@ -170,6 +368,20 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
   }
   __syncthreads();
   if (tm && tid == 0) tm[1] = clock64();
+
+  // ---------------------------------------------------------------- 0. warm-started subspace iteration
+  if (ea.warmA[mi] != nullptr) {
+    const bool ok = eig_subspace(A, full, ld, s, r, E, Ysub, Hs, Cs, Rs, red, red2, scal, ea.warmA[mi],
+                                 ea.warm_rows[mi], ea.warm_d[mi], ea.max_sub_steps);
+    if (ok) {
+      if (tid == 0 && ea.fast_used) ea.fast_used[mi] = 1;
+      for (int e = tid; e < s * r; e += blockDim.x) ea.E[mi][e] = E[e];
+      for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = 0.0;
+      if (tm && tid == 0) tm[2] = tm[3] = tm[4] = tm[5] = clock64();
+      return;
+    }
+  }
+  if (tid == 0 && ea.fast_used) ea.fast_used[mi] = 0;
 
   // ---------------------------------------------------------------- 1. tridiagonalise
   int hoff = 0;

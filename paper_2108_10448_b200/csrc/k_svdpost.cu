@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
     }
     off = warp_sum(off);
     dia = warp_sum(dia);
-    if (off <= DBL_EPSILON * DBL_EPSILON * dia * 1e-4 || off == 0.0) break;
+    if (off <= 1e-30 * dia || off == 0.0) break;
     for (int p = 0; p < r - 1; ++p) {
       for (int qq = p + 1; qq < r; ++qq) {
         const double apq = h[p + qq * r];

@@ -60,9 +60,15 @@ class Engine:
         n = self.n
         self.block_shapes = [(self.row_sizes[0], int(np.prod(self.row_sizes[1:], dtype=np.int64)))]
         self.block_shapes += [(self.shape[k], self.col_sizes[k]) for k in range(n)]
-        offs = [0]
-        for p, q in self.block_shapes:
-            offs.append(offs[-1] + p * q)
+        # element offsets of the blocks in the compact buffer; fiber blocks start
+        # 16-byte aligned (TMA bulk copies), as laid out by make_plan in engine.cu
+        offs, o = [], 0
+        for b, (p, q) in enumerate(self.block_shapes):
+            if b >= 1:
+                o = (o + 3) & ~3
+            offs.append(o)
+            o += p * q
+        offs.append(o)
         self.block_offsets = offs
 
     # ------------------------------------------------------------ lifecycle
@@ -184,7 +190,8 @@ class Engine:
     def split_blocks(self, flat_np):
         """Split a compact N_blk host array into (core n-d F-order, [fiber d_k x |J_k|])."""
         o = self.block_offsets
-        core = flat_np[o[0]:o[1]].reshape(self.row_sizes, order="F")
-        fibers = tuple(flat_np[o[k + 1]:o[k + 2]].reshape(self.block_shapes[k + 1], order="F")
+        sz = [p * q for p, q in self.block_shapes]
+        core = flat_np[o[0]:o[0] + sz[0]].reshape(self.row_sizes, order="F")
+        fibers = tuple(flat_np[o[k + 1]:o[k + 1] + sz[k + 1]].reshape(self.block_shapes[k + 1], order="F")
                        for k in range(self.n))
         return core, fibers

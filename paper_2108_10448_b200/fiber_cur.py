@@ -157,13 +157,23 @@ def _draw_without_replacement(rng: np.random.Generator, population: int, k: int)
     if 3 * k >= population:
         picked = rng.permutation(population)[:k]
         return np.sort(picked.astype(np.int64)) + 1
-    out = np.empty(0, dtype=np.int64)
-    while out.size < k:
-        need = k - out.size
+    # Same generator calls as the reference (so the same stream); the
+    # first-occurrence dedup of np.unique(..., return_index=True) is done in
+    # O(n) by the native helper.
+    from . import _native
+
+    lib = _native.load()
+    seen = np.zeros(population, dtype=np.uint8)
+    cap = 2 * k + 64
+    out = np.empty(cap, dtype=np.int64)
+    nout = 0
+    while nout < k:
+        need = k - nout
         batch = rng.integers(0, population, size=need + need // 2 + 16, dtype=np.int64)
-        merged = np.concatenate([out, batch])
-        _, first = np.unique(merged, return_index=True)
-        out = merged[np.sort(first)]
+        if nout + batch.size > out.size:
+            out = np.concatenate([out, np.empty(nout + batch.size, dtype=np.int64)])
+        nout = int(lib.rtcur_append_distinct(out.ctypes.data, nout, batch.ctypes.data, batch.size, seen.ctypes.data,
+                                             population))
     return np.sort(out[:k]) + 1
 
 

@@ -263,12 +263,14 @@ class _Source:
             return
         import torch
 
-        core = np.asarray(self.accessor.core_block(idx.rows), dtype=np.float64)
-        parts = [core.reshape(-1, order="F")]
+        host = np.zeros(eng.nblk_total, dtype=np.float64)
+        o = eng.block_offsets
+        core = np.asarray(self.accessor.core_block(idx.rows), dtype=np.float64).reshape(-1, order="F")
+        host[o[0]:o[0] + core.size] = core
         for k, cols in enumerate(idx.cols, start=1):
-            parts.append(np.asarray(self.accessor.fiber_block(k, cols), dtype=np.float64).reshape(-1, order="F"))
-        host = torch.from_numpy(np.concatenate(parts))
-        eng.xblocks().copy_(host, non_blocking=False)
+            f = np.asarray(self.accessor.fiber_block(k, cols), dtype=np.float64).reshape(-1, order="F")
+            host[o[k]:o[k] + f.size] = f
+        eng.xblocks().copy_(torch.from_numpy(host), non_blocking=False)
 
 
 def _make_result(eng: Engine, src: _Source, idx, cfg, history, flags, timings, zeta, converged, trace):

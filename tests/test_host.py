@@ -64,7 +64,7 @@ def test_engine_plan_sizes_and_errors():
                                    ctypes.byref(xo), ctypes.byref(xn))
         assert st == 0, _native.load().rtcur_last_error()
         nblk = int(np.prod(rows)) + sum(d * c for d, c in zip(cfg.shape, cols))
-        assert xn.value == nblk
+        assert nblk <= xn.value <= nblk + 3 * len(cfg.shape)   # fiber blocks start 16-byte aligned
         assert ws.value < 8 * 2 ** 30
     # rank above the sample sizes -> ValueError (fiber_cur.py:257-261)
     st = lib.rtcur_engine_plan(3, _native.i64_array((10, 10, 10)), _native.i32_array((3, 3, 3)),
