@@ -414,6 +414,33 @@ static void prof_flush(rtcur_engine* e) {
   e->prof_pending->clear();
 }
 
+static int set_smem_limits_once() {
+  static std::atomic<int> done{0};
+  if (done.load()) return RT_OK;
+  int dev = 0, optin = 227 * 1024;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // per kernel: opt-in maximum minus its static shared memory
+#define SMEM_ATTR(F)                                                                          \
+  do {                                                                                        \
+    cudaFuncAttributes fa;                                                                    \
+    CK(cudaFuncGetAttributes(&fa, F));                                                        \
+    CK(cudaFuncSetAttribute(F, cudaFuncAttributeMaxDynamicSharedMemorySize,                   \
+                            optin - (int)fa.sharedSizeBytes));                                \
+  } while (0)
+  SMEM_ATTR(k_eig);
+  SMEM_ATTR(k_wcols<4>); SMEM_ATTR(k_wcols<8>); SMEM_ATTR(k_wcols<16>); SMEM_ATTR(k_wcols<32>);
+  SMEM_ATTR(k_zproj<4>); SMEM_ATTR(k_zproj<8>); SMEM_ATTR(k_zproj<16>); SMEM_ATTR(k_zproj<32>);
+  SMEM_ATTR((k_block_pass<true, true, false, true>)); SMEM_ATTR((k_block_pass<true, false, false, true>));
+  SMEM_ATTR((k_block_pass<false, true, false, true>)); SMEM_ATTR((k_block_pass<false, false, false, true>));
+  SMEM_ATTR((k_block_pass<true, false, true, false>)); SMEM_ATTR((k_block_pass<false, false, true, false>));
+  SMEM_ATTR((k_block_pass<true, true, false, false>)); SMEM_ATTR((k_block_pass<false, true, false, false>));
+  SMEM_ATTR(k_hgram);
+#undef SMEM_ATTR
+  done.store(1);
+  return RT_OK;
+}
+
 static IndexPtrs make_ip(const rtcur_engine* e) {
   const Plan& P = e->P;
   IndexPtrs ip;
@@ -490,31 +517,13 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   CK(cudaMemsetAsync(e->ws + e->P.o_counters, 0, 64 * 4, e->st));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
-  // opt-in shared memory sizes
-  int maxe = 0;
-  for (int m = 0; m < n; ++m) maxe = std::max(maxe, eig_smem_bytes(e->P, m));
-  CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(maxe, 48 * 1024)));
+  // opt-in shared memory: kernel attributes are process-global, so raise every
+  // dynamic-smem kernel to the device maximum once (pooled engines of different
+  // geometries share them; occupancy follows the bytes of each launch)
   {
-    const int smb = (int)bp_smem_bytes(e->P.bp);
-    CK(cudaFuncSetAttribute(k_block_pass<true, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    CK(cudaFuncSetAttribute(k_block_pass<true, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    CK(cudaFuncSetAttribute(k_block_pass<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    CK(cudaFuncSetAttribute(k_block_pass<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    CK(cudaFuncSetAttribute(k_block_pass<true, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    CK(cudaFuncSetAttribute(k_block_pass<false, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    CK(cudaFuncSetAttribute(k_block_pass<true, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    CK(cudaFuncSetAttribute(k_block_pass<false, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    int st = set_smem_limits_once();
+    if (st) { delete e; return st; }
   }
-  const int gs = wcols_smem(e->P.g);
-  CK(cudaFuncSetAttribute(k_wcols<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_wcols<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_wcols<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_wcols<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(gs, 48 * 1024)));
-  const int zs = (int)(e->P.smax * (e->P.rmax + ZP_T) * 8);
-  CK(cudaFuncSetAttribute(k_zproj<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_zproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_zproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_zproj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
   *out = e;
   return RT_OK;
 }
@@ -1145,12 +1154,11 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   CK(cudaMemsetAsync(ws + P.o_counters, 0, 64 * 4, st));
   // the SVD kernels take raw pointers: M points straight at the caller's matrix
   int esm = eig_smem_bytes(P, 0);
-  CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(esm, 48 * 1024)));
+  {
+    int st2 = set_smem_limits_once();
+    if (st2) return st2;
+  }
   const int zs = (int)(s * (r + ZP_T) * 8);
-  CK(cudaFuncSetAttribute(k_zproj<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_zproj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_zproj<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
-  CK(cudaFuncSetAttribute(k_zproj<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(zs, 48 * 1024)));
   GramArgs ga;
   memset(&ga, 0, sizeof(ga));
   ga.n = 1;

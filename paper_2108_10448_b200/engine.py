@@ -13,7 +13,42 @@ import numpy as np
 
 from . import _native as nat
 
-__all__ = ["Engine"]
+__all__ = ["Engine", "acquire_engine"]
+
+# Engines (device workspace + pinned staging + native handle) are pooled per
+# problem geometry: creating one costs pinned host allocations and kernel
+# attribute setup that would otherwise dominate a short solve.  A pooled engine
+# is handed out only when no live SolveResult still references it.
+_POOL: dict = {}
+
+
+def acquire_engine(shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=None):
+    import torch
+    import weakref
+
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    key = (tuple(shape), tuple(ranks), tuple(row_sizes), tuple(col_sizes), str(dtype), tuple(slab or (0, shape[0])),
+           str(dev))
+    free = _POOL.setdefault(key, [])
+    eng = None
+    while free:
+        ref = free.pop()
+        eng = ref() if isinstance(ref, weakref.ref) else ref
+        if eng is not None and eng.handle.value:
+            break
+        eng = None
+    if eng is None:
+        eng = Engine(shape, ranks, row_sizes, col_sizes, dtype, slab=slab, device=dev)
+    eng._pool_key = key
+    return eng
+
+
+def release_engine(eng):
+    """Return an engine to the pool (called when the result holding it dies)."""
+    key = getattr(eng, "_pool_key", None)
+    if key is not None and eng.handle.value:
+        eng.unbind_quiet()
+        _POOL.setdefault(key, []).append(eng)
 
 
 class Engine:
@@ -96,6 +131,10 @@ class Engine:
         """flat: contiguous CUDA tensor holding this rank's mode-1 slab."""
         self._x = flat
         nat.check(self.lib.rtcur_engine_bind(self.handle, ctypes.c_void_p(flat.data_ptr())))
+
+    def unbind_quiet(self):
+        self._x = None
+        self.lib.rtcur_engine_bind(self.handle, ctypes.c_void_p(0))
 
     def unbind(self):
         self._x = None

@@ -28,7 +28,7 @@ from typing import Protocol, Sequence
 import numpy as np
 
 from . import _native as nat
-from .engine import Engine
+from .engine import Engine, acquire_engine, release_engine
 from .fiber_cur import FiberCur, SampleIndices, TruncatedSvd, draw_sample_indices, sample_sizes
 from .tensor import DenseTensor, DeviceTensor, as_shape
 
@@ -313,6 +313,9 @@ def _make_result(eng: Engine, src: _Source, idx, cfg, history, flags, timings, z
 
     cur = FiberCur(load_cur, idx)
     cur._engine = eng        # keep the device state alive with the result
+    import weakref
+
+    weakref.finalize(cur, release_engine, eng)   # back to the pool once the result is gone
     sparse = SparseEstimate(load_sparse, idx)
     return SolveResult(cur=cur, sparse=sparse, error_history=tuple(history), iterations=len(history),
                        converged=converged, diagnostics=tuple(flags), timings=timings, zeta_final=zeta,
@@ -347,7 +350,7 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
         if r > rs or r > cs:   # fiber_cur.py:257-261
             raise ValueError(f"mode {m}: rank {r} exceeds sample sizes (|rows|={rs}, |cols|={cs})")
 
-    eng = Engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype)
+    eng = acquire_engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype)
     if PROFILE:
         eng.profile(True)
     src.attach(eng)
@@ -402,4 +405,5 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
         ph = eng.profile_read(reset=True)
         timings["device_ms"] = {k: v[0] for k, v in ph.items()}
         timings["device_launches"] = {k: v[1] for k, v in ph.items()}
+        eng.profile(False)
     return _make_result(eng, src, idx, cfg, history, flags, timings, zeta, converged, trace)
