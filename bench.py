@@ -170,13 +170,14 @@ def run_reference(args):
     return 0
 
 
-def _config_dict(bc, rows, cols, world):
+def _config_dict(bc, rows, cols, world, shard=False):
     return {"workload": f"config{bc.index}: RTCUR-{bc.variant} {'x'.join(map(str, bc.shape))} {bc.dtype} ranks "
                         f"{tuple(bc.ranks)} alpha={bc.alpha} c={bc.c} eps={bc.eps} max_iters=100",
             "shape": list(bc.shape), "ranks": list(bc.ranks), "variant": bc.variant, "row_samples": list(rows),
             "col_samples": list(cols), "l2": "inputs larger than L2 (X = %.0f MB > 126 MB)" % (
                 np.prod(bc.shape) * (8 if bc.dtype == "f64" else 4) / 1e6),
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+            "parallelism": (f"mode-1 slabs x{world} (NCCL all-reduce of the sampled blocks)" if shard else
+                            f"replicas x{world}" if world > 1 else "single GPU")}
 
 
 def _cpu_baseline(bc, rows, cols, xf, budget_iters=2):
@@ -192,32 +193,56 @@ def _cpu_baseline(bc, rows, cols, xf, budget_iters=2):
                       f"{res.timings['gather'] + res.timings['sample']:.2f}s excluded"}
 
 
+def _sharded(config: int) -> bool:
+    """BASELINE shards configs 2 and 4 in mode-1 slabs; the others run replicas."""
+    return config in (2, 4)
+
+
 def run_b200(args):
     import torch
 
     world, rank, local = _dist()
+    group = None
     if world > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
     torch.cuda.set_device(local)
     from paper_2108_10448_b200 import DeviceTensor, SolverConfig, rtcur
     from paper_2108_10448_b200 import _native
     from paper_2108_10448_b200 import solver as solver_mod
+    from paper_2108_10448_b200.dist import rtcur_sharded
+    from paper_2108_10448_b200.synth import CONFIGS, baseline_sample_sizes, make_config_device, slab_bounds
 
-    xf, _, bc, rows, cols = _make_problem(args.config)
+    bc = CONFIGS[args.config]
+    rows, cols = baseline_sample_sizes(bc.shape, bc.ranks)
     dt = torch.float64 if bc.dtype == "f64" else torch.float32
-    host = torch.from_numpy(xf).to(dt)
-    x_dev = DeviceTensor(host.cuda(), bc.shape)
+    shard = _sharded(args.config) and world > 1
+    slab = slab_bounds(bc.shape[0], world, rank) if shard else None
+    xf = None
+    if args.config <= 1:
+        xf, _, bc, rows, cols = _make_problem(args.config)
+        host = torch.from_numpy(xf).to(dt)
+        x_dev = DeviceTensor(host.cuda(), bc.shape)
+    else:
+        x_dev, _ = make_config_device(args.config, slab=slab, group=group if shard else None)
+        host = None
     cfg = SolverConfig(ranks=bc.ranks, eps=bc.eps, gamma=0.7, variant=bc.variant, max_iters=100,
-                       seed=bc.seed_solver + 1000 * rank, row_sample_sizes=rows, col_sample_sizes=cols)
+                       seed=bc.seed_solver + (0 if shard else 1000 * rank), row_sample_sizes=rows,
+                       col_sample_sizes=cols)
+
+    def solve(x):
+        if shard:
+            return rtcur_sharded(x, bc.shape, slab, cfg, group=group)
+        return rtcur(x, cfg)
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
-        rtcur(x_dev, cfg)
+        solve(x_dev)
     torch.cuda.synchronize()
 
     # ---------------- device-resident timed region
@@ -231,7 +256,7 @@ def run_b200(args):
     ev0.record()
     iters, conv, phase_ms, phase_n = 0, True, {}, {}
     for _ in range(args.steps):
-        res = rtcur(x_dev, cfg)
+        res = solve(x_dev)
         iters += res.iterations
         conv &= res.converged
         for k, v in res.timings["device_ms"].items():
@@ -248,20 +273,24 @@ def run_b200(args):
     it = torch.tensor([iters], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(it, op=torch.distributed.ReduceOp.SUM)
+        if not shard:   # replicas: every rank's iterations count; sharded: one solve spans all ranks
+            torch.distributed.all_reduce(it, op=torch.distributed.ReduceOp.SUM)
     ms_max = float(t.item())
     value = float(it.item()) / (ms_max / 1e3)
 
     # ---------------- e2e through the public API with host buffers
+    if host is None:
+        host = x_dev.flat.cpu()
     pinned = host.pin_memory()
     x_buf = torch.empty_like(x_dev.flat)
     e2e_iters, d2h = 0, 0
+    e2e_steps = max(1, args.steps if args.config <= 1 else min(args.steps, 2))
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         x_buf.copy_(pinned, non_blocking=True)
-        res = rtcur(DeviceTensor(x_buf, bc.shape), cfg)
+        res = solve(DeviceTensor(x_buf, x_dev.shape))
         e2e_iters += res.iterations
         sc = res.sparse.core
         sf = res.sparse.fibers
@@ -278,12 +307,15 @@ def run_b200(args):
     ie = torch.tensor([e2e_iters], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(ie, op=torch.distributed.ReduceOp.SUM)
+        if not shard:
+            torch.distributed.all_reduce(ie, op=torch.distributed.ReduceOp.SUM)
     e2e_value = float(ie.item()) / float(te.item())
 
     # ---------------- roofline of the dominant HBM-bound kernel
     peak, peak_src = _peaks()
     alg, n_blk = _algorithmic_bytes(bc, rows, cols)
+    if shard:   # the slab gather reads only this rank's entries; the other passes work on the full blocks
+        alg["gather"] = alg["gather"] // 2 + alg["gather"] // 2 // world
     total_dev = sum(phase_ms.values())
     hbm_phases = {k: v for k, v in phase_ms.items() if k in alg and phase_n.get(k)}
     dom = max(hbm_phases, key=hbm_phases.get)
@@ -300,19 +332,24 @@ def run_b200(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = _cpu_baseline(bc, rows, cols, xf)
+        if xf is not None:
+            cpu = _cpu_baseline(bc, rows, cols, xf)
+        else:
+            cpu = {"value": None, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"not run for config {bc.index}: one CPU iteration of the port takes minutes "
+                             "(SURVEY §6: ~12 min/iter config 2, ~91 s config 3, ~6.5 s config 4)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": bc.dtype,
+            "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": bc.dtype,
             "data": "synthetic (seeded, paper_2108_10448_b200.synth)",
-            "config": _config_dict(bc, rows, cols, world),
+            "config": _config_dict(bc, rows, cols, world, shard),
             "sec_to_tol": ms_max / args.steps / 1e3, "iterations_per_solve": iters / args.steps,
             "converged": bool(conv), "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(host.numel() * host.element_size()),
-                    "d2h_bytes_per_step": int(d2h), "sec_per_solve": e2e_s / args.steps},
+                    "d2h_bytes_per_step": int(d2h), "sec_per_solve": e2e_s / e2e_steps},
             "roofline": roof, "phases": phases, "clocks": clk, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

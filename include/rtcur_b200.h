@@ -123,6 +123,16 @@ int64_t rtcur_engine_full_scratch_bytes(rtcur_engine* e);
 int rtcur_engine_profile(rtcur_engine* e, int on);
 int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* counts, int nphase, int reset);
 
+/* Synthetic instance support (bench/tests).  On a mode-1 slab [lo, hi) of a d1 x ... tensor:
+ * L(i1, R) = sum_a Y1[i1, a] Tf[R, a] (Y1: d1 x r1 column-major, Tf: ncols x r1 row-major,
+ * ncols = prod_{m>=2} d_m, both device pointers shared by every slab).  mode 0 returns
+ * sum |L| over the slab in *sum_abs (host, synchronous); mode 1 writes X = L + S (dtype),
+ * S Bernoulli(alpha) with values U[-cmu, cmu] keyed by (seed, global element index), so any
+ * slab decomposition generates the same tensor bit for bit.  scratch: device, >= 1200 doubles. */
+int rtcur_generate_tucker(const double* Y1, const double* Tf, int64_t d1, int r1, int64_t lo, int64_t hi,
+                          int64_t ncols, int mode, uint64_t seed, double alpha, double cmu, int dtype, void* X,
+                          double* scratch, double* sum_abs, void* stream);
+
 /* Host helper of the index sampler (fiber_cur.py:202-208): append the values of
  * batch not yet marked in seen (population bytes) to out, in first-occurrence
  * order; returns the new length (-1 if a value is out of range). */

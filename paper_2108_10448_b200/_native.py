@@ -25,7 +25,7 @@ EXPORTED = (
     "rtcur_engine_iterate_async", "rtcur_engine_iterate_wait",
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
     "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_read",
-    "rtcur_append_distinct",
+    "rtcur_append_distinct", "rtcur_generate_tucker",
 )
 PHASES = ("absmax", "prep", "gather", "threshold", "gram", "eig", "svdpost", "apass", "gpass", "wcols", "error",
           "export", "full")
@@ -81,6 +81,9 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_profile_read.argtypes = [c_vp, c_dp, c_i64p, ctypes.c_int, ctypes.c_int]
     lib.rtcur_append_distinct.argtypes = [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]
     lib.rtcur_append_distinct.restype = c_i64
+    lib.rtcur_generate_tucker.argtypes = [c_vp, c_vp, c_i64, ctypes.c_int, c_i64, c_i64, c_i64, ctypes.c_int,
+                                          ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_int, c_vp, c_vp,
+                                          c_dp, c_vp]
     for name in EXPORTED:
         if not hasattr(lib, name):
             raise NativeUnavailable(f"{path} does not export {name}")

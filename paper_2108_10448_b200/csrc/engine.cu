@@ -1066,6 +1066,32 @@ extern "C" int64_t rtcur_append_distinct(int64_t* out, int64_t nout, const int64
   return nout;
 }
 
+// Synthetic instance on a mode-1 slab (see rtcur_b200.h).  mode 0: *sum_abs = sum |L|
+// over the slab; mode 1: X = L + S.  scratch: >= 2 * 148 * 8 doubles + 64 bytes.
+extern "C" int rtcur_generate_tucker(const double* Y1, const double* Tf, int64_t d1, int r1, int64_t lo, int64_t hi,
+                                     int64_t ncols, int mode, uint64_t seed, double alpha, double cmu, int dtype,
+                                     void* X, double* scratch, double* sum_abs, void* stream) {
+  if (lo < 0 || hi <= lo || hi > d1 || r1 < 1 || ncols < 1) return fail(RT_ERR_VALUE, "bad generator arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = 148 * 8;
+  double* partial = scratch;
+  double* outs = scratch + grid;
+  unsigned int* counter = reinterpret_cast<unsigned int*>(scratch + grid + 1);
+  if (mode == 0) CK(cudaMemsetAsync(counter, 0, 4, st));
+  if (dtype == 0)
+    k_gen_tucker<double><<<grid, 256, 0, st>>>(Y1, Tf, d1, r1, lo, hi, ncols, mode, seed, alpha, cmu, (double*)X,
+                                              partial, outs, counter);
+  else
+    k_gen_tucker<float><<<grid, 256, 0, st>>>(Y1, Tf, d1, r1, lo, hi, ncols, mode, seed, alpha, cmu, (float*)X,
+                                             partial, outs, counter);
+  LAUNCH_CHECK();
+  if (mode == 0) {
+    CK(cudaMemcpyAsync(sum_abs, outs, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return RT_OK;
+}
+
 // ------------------------------------------------------------------ kernel-level plug
 
 extern "C" int rtcur_gather_columns(const void* flat, int dtype, int64_t flat_len, const int64_t* bases_dev,

@@ -85,3 +85,90 @@ __global__ void __launch_bounds__(256) k_full(FullArgs a) {
 
 template __global__ void k_full<float>(FullArgs);
 template __global__ void k_full<double>(FullArgs);
+
+// ------------------------------------------------------------------ synthetic instances
+
+// Counter-based uniform in [0, 1) keyed by (seed, global element index, stream).
+__device__ __forceinline__ double gen_u01(unsigned long long seed, unsigned long long idx, unsigned long long stream) {
+  unsigned long long z = seed * 0x9E3779B97F4A7C15ull + idx * 0xD1B54A32D192ED03ull + stream * 0x8CB92BA72F3D8DD7ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// X = L + S on a mode-1 slab [lo, hi): S is Bernoulli(alpha) supported with
+// values U[-cmu, cmu], both drawn from the GLOBAL element index, so any slab
+// decomposition of the tensor reproduces the same instance (BASELINE configs,
+// SURVEY §8(d.1)).  L (fp64) may alias nothing; X is written in dtype.
+template <typename T>
+__global__ void __launch_bounds__(256) k_gen_outliers(const double* __restrict__ L, T* __restrict__ X, i64 nloc, i64 lo,
+                                                      i64 hi, i64 d1, unsigned long long seed, double alpha,
+                                                      double cmu) {
+  const i64 ld = hi - lo;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < nloc; e += (i64)gridDim.x * blockDim.x) {
+    const i64 R = e / ld, i1 = e - R * ld;
+    const unsigned long long gidx = (unsigned long long)(lo + i1 + d1 * R);
+    double v = L[e];
+    if (gen_u01(seed, gidx, 1) < alpha) v += (2.0 * gen_u01(seed, gidx, 2) - 1.0) * cmu;
+    X[e] = (T)v;
+  }
+}
+template __global__ void k_gen_outliers<float>(const double*, float*, i64, i64, i64, i64, unsigned long long, double,
+                                               double);
+template __global__ void k_gen_outliers<double>(const double*, double*, i64, i64, i64, i64, unsigned long long,
+                                                double, double);
+
+// Generator pass over a mode-1 slab [lo, hi): L(i1, R) = sum_a Y1[i1, a] Tf[R, a]
+// (Y1: d1 x r1 column-major, Tf: ncols x r1 row-major, both shared by every slab,
+// so each entry is bitwise independent of the slab decomposition).
+//   mode 0: sums |L| over the slab (per-CTA partials, last CTA sums in order)
+//   mode 1: writes X = L + S (hashed outliers, values U[-cmu, cmu]) in T
+template <typename T>
+__global__ void __launch_bounds__(256) k_gen_tucker(const double* __restrict__ Y1, const double* __restrict__ Tf,
+                                                    i64 d1, int r1, i64 lo, i64 hi, i64 ncols, int mode,
+                                                    unsigned long long seed, double alpha, double cmu,
+                                                    T* __restrict__ X, double* partial, double* out_sum,
+                                                    unsigned int* counter) {
+  __shared__ double red[8];
+  __shared__ bool am_last;
+  const i64 ld = hi - lo;
+  const i64 n = ld * ncols;
+  double acc = 0.0;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x) {
+    const i64 R = e / ld, i1 = e - R * ld;
+    const double* tf = Tf + R * r1;
+    double l = 0.0;
+    for (int a = 0; a < r1; ++a) l = fma(Y1[lo + i1 + (i64)a * d1], tf[a], l);
+    if (mode == 0) {
+      acc += fabs(l);
+    } else {
+      const unsigned long long gidx = (unsigned long long)(lo + i1 + d1 * R);
+      if (gen_u01(seed, gidx, 1) < alpha) l += (2.0 * gen_u01(seed, gidx, 2) - 1.0) * cmu;
+      X[e] = (T)l;
+    }
+  }
+  if (mode != 0) return;
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = acc;
+    __threadfence();
+    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  double t = 0.0;
+  for (i64 c = threadIdx.x; c < gridDim.x; c += blockDim.x) t += ((volatile double*)partial)[c];
+  t = block_sum(t, red);
+  if (threadIdx.x == 0) {
+    *out_sum = t;
+    *counter = 0u;
+  }
+}
+template __global__ void k_gen_tucker<float>(const double*, const double*, i64, int, i64, i64, i64, int,
+                                             unsigned long long, double, double, float*, double*, double*,
+                                             unsigned int*);
+template __global__ void k_gen_tucker<double>(const double*, const double*, i64, int, i64, i64, i64, int,
+                                              unsigned long long, double, double, double*, double*, double*,
+                                              unsigned int*);

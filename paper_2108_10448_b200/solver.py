@@ -221,11 +221,19 @@ def _error_from_sums(e2, x2) -> float:
 
 class _Source:
     """Where the sampled blocks come from: a resident device tensor (gathered
-    by the fused K1 gather) or a generic host TensorAccessor (blocks uploaded)."""
+    by the fused K1 gather) or a generic host TensorAccessor (blocks uploaded).
 
-    def __init__(self, x):
+    Sharded (``slab``/``group`` given): the device tensor is this rank's mode-1
+    slab of a ``global_shape`` tensor; the gather fills only the entries the
+    rank owns and a sum all-reduce of the compact blocks completes them (each
+    sampled entry has exactly one owner, so the sum is exact); zeta_0 is a max
+    all-reduce of the slab abs-maxima."""
+
+    def __init__(self, x, slab=None, group=None, global_shape=None):
         import torch
 
+        self.slab = slab
+        self.group = group
         self.accessor = None
         self.dev = None
         if isinstance(x, DenseTensor):
@@ -240,7 +248,14 @@ class _Source:
             self.accessor = x
         else:
             raise TypeError(f"unsupported tensor source {type(x).__name__}")
-        self.shape = as_shape(self.dev.shape if self.dev is not None else x.shape)
+        self.shape = as_shape(global_shape if global_shape is not None else
+                              (self.dev.shape if self.dev is not None else x.shape))
+        if slab is not None:
+            lo, hi = slab
+            if self.dev is None or not (0 <= lo < hi <= self.shape[0]):
+                raise ValueError("a sharded solve needs a device slab [lo, hi) of mode 1")
+            if tuple(self.dev.shape) != (hi - lo,) + tuple(self.shape[1:]):
+                raise ValueError(f"slab tensor shape {self.dev.shape} does not match [{lo}, {hi}) of {self.shape}")
 
     @property
     def torch_dtype(self):
@@ -254,12 +269,24 @@ class _Source:
 
     def inf_norm(self, eng: Engine) -> float:
         if self.dev is not None:
-            return eng.absmax()
+            v = eng.absmax()
+            if self.group is not None:
+                import torch
+                import torch.distributed as dist
+
+                t = torch.tensor([v], dtype=torch.float64, device=eng.device)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+                v = float(t.item())
+            return v
         return float(self.accessor.inf_norm())
 
     def load_blocks(self, eng: Engine, idx: SampleIndices):
         if self.dev is not None:
             eng.gather()
+            if self.group is not None:
+                import torch.distributed as dist
+
+                dist.all_reduce(eng.xblocks(), op=dist.ReduceOp.SUM, group=self.group)
             return
         import torch
 
@@ -329,9 +356,12 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
     x: DenseTensor (uploaded once), DeviceTensor / F-contiguous torch CUDA
     tensor (used in place, fp64 or fp32), or any TensorAccessor.
     """
+    return _solve(_Source(x), cfg, record_trace)
+
+
+def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
     import torch
 
-    src = _Source(x)
     shape = src.shape
     if len(cfg.ranks) != len(shape):
         raise ValueError(f"{len(cfg.ranks)} ranks for a {len(shape)}-mode tensor")
@@ -350,7 +380,7 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
         if r > rs or r > cs:   # fiber_cur.py:257-261
             raise ValueError(f"mode {m}: rank {r} exceeds sample sizes (|rows|={rs}, |cols|={cs})")
 
-    eng = acquire_engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype)
+    eng = acquire_engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype, slab=src.slab)
     if PROFILE:
         eng.profile(True)
     src.attach(eng)

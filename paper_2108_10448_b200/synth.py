@@ -136,3 +136,85 @@ def make_config(index: int):
     else:
         x, low, sp = make_gaussian_tucker(cfg.shape, cfg.ranks, cfg.alpha, cfg.c, cfg.seed_instance, dt)
     return x, low, sp, cfg
+
+
+# ----------------------------------------------------------------- device generation (configs 2-4)
+
+
+def slab_bounds(d1: int, world: int, rank: int):
+    """Mode-1 slab of `rank` among `world` (contiguous, sizes differ by at most 1;
+    220/8 -> 28/27 rows)."""
+    return (d1 * rank) // world, (d1 * (rank + 1)) // world
+
+
+def make_gaussian_tucker_device(shape, ranks, alpha, c, seed, dtype=None, slab=None, group=None, mu=None):
+    """Device-side instance with the same law as ``make_gaussian_tucker``:
+    L* = G x_i Y_i (iid N(0,1) core and factors, drawn on the host from
+    ``seed``), S* Bernoulli(alpha) with values U[-c mean|L*|, c mean|L*|] keyed
+    by (seed, global element index).  Every entry is bitwise independent of the
+    slab decomposition (the mode>=2 contraction Tf is shared; the mode-1 step is
+    a fixed-order per-entry dot product in ``rtcur_generate_tucker``).  Returns
+    this rank's mode-1 slab as a DeviceTensor (shape (hi-lo, d_2, ..)) and
+    mean|L*| (all-reduced over ``group``, or taken from ``mu``)."""
+    import torch
+
+    from . import _native as nat
+    from .tensor import DeviceTensor
+
+    dtype = dtype or torch.float32
+    n = len(shape)
+    lo, hi = slab or (0, shape[0])
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal(int(np.prod(ranks))).reshape(ranks, order="F")
+    ys = [rng.standard_normal((d, r)) for d, r in zip(shape, ranks)]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    r1 = ranks[0]
+    # Tf[R, a] = (G x_{m>=2} Y_m)[a, i_2, .., i_n], R = i_2 + d_2 i_3 + ... (host, exact same bits on every rank)
+    tf = g
+    for m in range(1, n):
+        tf = np.tensordot(tf, ys[m], axes=([1], [1]))   # contract the next rank axis, append the mode axis
+    tf = np.moveaxis(tf, 0, -1)                          # (i_2, .., i_n, a)
+    tf = np.ascontiguousarray(np.transpose(tf, tuple(range(n - 2, -1, -1)) + (n - 1,)) if n > 1 else tf)
+    Tf = torch.from_numpy(tf.reshape(-1, r1)).to(dev)
+    Y1 = torch.from_numpy(np.asfortranarray(ys[0]).reshape(-1, order="F")).to(dev)
+    ncols = int(np.prod(shape[1:], dtype=np.int64)) if n > 1 else 1
+    lib = nat.load()
+    scratch = torch.empty(1300, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    dt_code = 0 if dtype == torch.float64 else 1
+    if mu is None:
+        import ctypes
+
+        s_abs = ctypes.c_double()
+        nat.check(lib.rtcur_generate_tucker(Y1.data_ptr(), Tf.data_ptr(), shape[0], r1, lo, hi, ncols, 0, int(seed),
+                                            float(alpha), 0.0, dt_code, None, scratch.data_ptr(),
+                                            ctypes.byref(s_abs), stream))
+        tot = torch.tensor([s_abs.value], dtype=torch.float64, device=dev)
+        if group is not None:
+            import torch.distributed as dist
+
+            dist.all_reduce(tot, group=group)
+        mu = float(tot.item()) / float(np.prod(shape, dtype=np.float64))
+    X = torch.empty((hi - lo) * ncols, dtype=dtype, device=dev)
+    nat.check(lib.rtcur_generate_tucker(Y1.data_ptr(), Tf.data_ptr(), shape[0], r1, lo, hi, ncols, 1, int(seed),
+                                        float(alpha), float(c * mu), dt_code, X.data_ptr(), scratch.data_ptr(), None,
+                                        stream))
+    return DeviceTensor(X, (hi - lo,) + tuple(shape[1:])), mu
+
+
+def make_config_device(index: int, slab=None, group=None):
+    """BASELINE config ``index`` generated on the GPU (slab of mode 1 when sharded)."""
+    import torch
+
+    cfg = CONFIGS[index]
+    dt = torch.float64 if cfg.dtype == "f64" else torch.float32
+    if cfg.kind == "video":
+        from .tensor import DeviceTensor
+
+        x, _, _ = make_video_like(cfg.shape, cfg.ranks, seed=cfg.seed_instance, dtype=np.float32)
+        lo, hi = slab or (0, cfg.shape[0])
+        full = torch.from_numpy(x).cuda().reshape(tuple(reversed(cfg.shape)))
+        part = full[..., lo:hi].contiguous() if slab else full
+        return DeviceTensor(part.reshape(-1), (hi - lo,) + tuple(cfg.shape[1:])), cfg
+    X, _ = make_gaussian_tucker_device(cfg.shape, cfg.ranks, cfg.alpha, cfg.c, cfg.seed_instance, dt, slab, group)
+    return X, cfg
