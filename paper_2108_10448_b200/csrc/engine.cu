@@ -106,6 +106,7 @@ struct Plan {
   int a_chunk, a_maxchunks;
   i64 dmax, lmax, smax, qmax;
   i64 g_tmp;         // doubles per G temp buffer
+  i64 w_tmp;         // doubles per W-chain temp buffer
   int hchunk, h_maxchunks;
   BPGeom bp;
   // workspace offsets (bytes)
@@ -114,7 +115,7 @@ struct Plan {
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
       o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_apart, o_gt0, o_gt1, o_bpart, o_sums,
-      o_fpart, o_dbg, o_fast;
+      o_fpart, o_dbg, o_fast, o_wt0, o_wt1;
   i64 total;
 };
 
@@ -293,6 +294,22 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
       mx = std::max(mx, cur);
     }
     P.g_tmp = std::max<i64>(mx, g.gsize);
+    // W_core chain G x_2 A_2(I_2) .. x_n A_n(I_n): intermediates (r1, I2..Im, r_{m+1}..rn), m < n
+    i64 wmx = 1;
+    for (int m = 1; m + 1 < n; ++m) {
+      i64 sz = ranks[0];
+      for (int l = 1; l <= m; ++l) sz *= row_sizes[l];
+      for (int l = m + 1; l < n; ++l) sz *= ranks[l];
+      wmx = std::max(wmx, sz);
+    }
+    // same for the full-tensor chain (K3 weights): (r1, d2..dm, r_{m+1}..rn)
+    for (int m = 1; m + 1 < n; ++m) {
+      i64 sz = ranks[0];
+      for (int l = 1; l <= m; ++l) sz *= dims[l];
+      for (int l = m + 1; l < n; ++l) sz *= ranks[l];
+      wmx = std::max(wmx, sz);
+    }
+    P.w_tmp = wmx;
   }
   // workspace carve
   i64 o = 0;
@@ -334,6 +351,8 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_apart = take((i64)n * P.a_maxchunks * P.dmax * RT_MAX_RANK * 8);
   P.o_gt0 = take(P.g_tmp * 8);
   P.o_gt1 = take(P.g_tmp * 8);
+  P.o_wt0 = take(P.w_tmp * 8);
+  P.o_wt1 = take(P.w_tmp * 8);
   P.o_bpart = take((i64)BP_GRID * g.nblk * 2 * 8 + 64);
   P.o_sums = take(2 * g.nblk * 8);
   P.o_fpart = take(148 * 8 * 2 * 8);
@@ -515,6 +534,9 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   if (ce != cudaSuccess) { cudaFreeHost(e->h_pinned); delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   // counters + col offsets
   CK(cudaMemsetAsync(e->ws + e->P.o_counters, 0, 64 * 4, e->st));
+  // zero the compact blocks once: the alignment pads between blocks are never
+  // written by the gather and must not carry garbage into rank all-reduces
+  CK(cudaMemsetAsync(e->ws + e->P.o_xb, 0, e->P.g.nblk_total * e->P.esize + 64, e->st));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -800,14 +822,56 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   return RT_OK;
 }
 
+// Expanding chain out = G x_2 B_2 x_3 .. x_n B_n with B_m = A_m(rows_m, :) (rows_m null:
+// all d_m rows), written to `dst` in (r1, P_2, .., P_n) F-order.
+static int run_wchain(rtcur_engine* e, const double* sto, const int* const* rows, const i64* Pm, double* dst) {
+  const Plan& P = e->P;
+  const Geom& g = P.g;
+  const int n = g.n;
+  if (n == 1) {
+    CK(cudaMemcpyAsync(dst, sto, g.gsize * 8, cudaMemcpyDeviceToDevice, e->st));
+    return RT_OK;
+  }
+  double* t0 = e->at<double>(P.o_wt0);
+  double* t1 = e->at<double>(P.o_wt1);
+  const double* in = sto;   // G
+  i64 rho = g.rank[0];
+  for (int m = 1; m < n; ++m) {
+    i64 beta = 1;
+    for (int l = m + 1; l < n; ++l) beta *= g.rank[l];
+    double* out = (m == n - 1) ? dst : (in == t0 ? t1 : t0);
+    const i64 total = rho * Pm[m] * beta;
+    k_modeprod_fwd<<<(unsigned)std::min<i64>(cdiv(total, 256), 148 * 16), 256, 0, e->st>>>(
+        in, out, sto + g.a_off[m], rows ? rows[m] : nullptr, g.dim[m], rho, Pm[m], g.rank[m], beta);
+    LAUNCH_CHECK();
+    rho *= Pm[m];
+    in = out;
+  }
+  return RT_OK;
+}
+
+// W_b of every block column for state `sto`: the core by the separable chain,
+// the fiber blocks (arbitrary multi-indices) by k_wcols
 static int run_wcols(rtcur_engine* e, double* sto) {
   const Plan& P = e->P;
   const Geom& g = P.g;
   IndexPtrs ip = make_ip(e);
   prof_begin(e, PH_WCOLS);
+  // large cores: separable chain (r_m FMAs per output); small ones stay in the
+  // single k_wcols launch (launch overhead dominates there)
+  const bool chain = g.n >= 2 && g.blk[0].Q * (g.gsize / g.rank[0]) > (i64)2000000;
+  if (chain) {
+    const int* rows[RT_MAX_MODES];
+    i64 Pm[RT_MAX_MODES];
+    for (int m = 0; m < g.n; ++m) { rows[m] = ip.rows[m]; Pm[m] = g.nrows[m]; }
+    int st = run_wchain(e, sto, rows, Pm, sto + g.blk[0].w_off);
+    if (st) return st;
+  }
   const int rpt = wcols_rows_per_thread(g);
-  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(P.qmax, 128), g.nblk), 128, wcols_smem(g), e->st, g, ip, sto, 0,
-             (double*)nullptr, rpt);
+  i64 qf = 1;
+  for (int b = chain ? 1 : 0; b < g.nblk; ++b) qf = std::max(qf, g.blk[b].Q);
+  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(qf, 128), g.nblk), 128, wcols_smem(g), e->st, g, ip, sto, 0,
+             (double*)nullptr, rpt, chain ? 1 : 0);
   LAUNCH_CHECK();
   prof_end(e, PH_WCOLS);
   return RT_OK;
@@ -978,9 +1042,13 @@ extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_de
   i64 ncols = 1;
   for (int m = 1; m < g.n; ++m) ncols *= g.dim[m];
   prof_begin(e, PH_WCOLS);
-  DISPATCH_R(rbucket(g.rank[0]), k_wcols, dim3((unsigned)cdiv(ncols, 128), 1), 128, wcols_smem(g), e->st, g, ip,
-             sto, 1, tf_dev, wcols_rows_per_thread(g));
-  LAUNCH_CHECK();
+  {
+    i64 Pm[RT_MAX_MODES];
+    for (int m = 0; m < g.n; ++m) Pm[m] = g.dim[m];
+    int st = run_wchain(e, sto, nullptr, Pm, tf_dev);   // Tf = G x_{m>=2} A_m over the full tensor
+    if (st) return st;
+  }
+  (void)ip;
   prof_end(e, PH_WCOLS);
   FullArgs fa;
   memset(&fa, 0, sizeof(fa));

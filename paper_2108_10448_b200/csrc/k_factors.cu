@@ -163,6 +163,28 @@ __global__ void __launch_bounds__(256) k_modeprod(const double* __restrict__ in,
   }
 }
 
+// out = in x_m B with B[p, b] = A[row(p) + b * d] (row(p) = rows[p] or p):
+// in dims (rho, r_m, beta_n), out dims (rho, Pm, beta_n) -- the expanding mode
+// product used to build W_core = G x_{m>=2} A_m(I_m, :) and the full-tensor
+// weights Tf = G x_{m>=2} A_m as a chain (cost r_m per output instead of
+// prod r per column).
+__global__ void __launch_bounds__(256) k_modeprod_fwd(const double* __restrict__ in, double* __restrict__ out,
+                                                       const double* __restrict__ A, const int* __restrict__ rows,
+                                                       i64 d, i64 rho, i64 Pm, int rm, i64 beta_n) {
+  const i64 total = rho * Pm * beta_n;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
+    const i64 alpha = e % rho;
+    const i64 rest = e / rho;
+    const i64 p = rest % Pm;
+    const i64 beta = rest / Pm;
+    const double* src = in + alpha + rho * (i64)rm * beta;
+    const double* arow = A + (rows ? (i64)rows[p] : p);
+    double acc = 0.0;
+    for (int b = 0; b < rm; ++b) acc = fma(arow[(i64)b * d], src[rho * b], acc);
+    out[e] = acc;
+  }
+}
+
 // ------------------------------------------------------------------ W
 
 // Per block column q: w[a] = sum over the other modes' rank indices of
@@ -171,8 +193,8 @@ __global__ void __launch_bounds__(256) k_modeprod(const double* __restrict__ in,
 // dynamic shared memory: G (gsize doubles) + per thread the other modes' A rows
 template <int R>
 __global__ void __launch_bounds__(128) k_wcols(Geom g, IndexPtrs ip, double* __restrict__ st, int full,
-                                              double* __restrict__ wfull, int rows_per_thread) {
-  extern __shared__ double gs[];
+                                              double* __restrict__ wfull, int rows_per_thread, int skip_core) {
+  extern __shared__ double gsm[];
   const int b = blockIdx.y;
   i64 Q;
   int tgt, is_core;
@@ -184,15 +206,15 @@ __global__ void __launch_bounds__(128) k_wcols(Geom g, IndexPtrs ip, double* __r
     is_core = 1;
     w_off = 0;
   } else {
-    if (b >= g.nblk) return;
+    if (b >= g.nblk || (skip_core && g.blk[b].is_core)) return;
     Q = g.blk[b].Q;
     tgt = g.blk[b].mode;
     is_core = g.blk[b].is_core;
     w_off = g.blk[b].w_off;
   }
   if ((i64)blockIdx.x * blockDim.x >= Q) return;
-  for (i64 i = threadIdx.x; i < g.gsize; i += blockDim.x) gs[i] = st[i];
-  double* rowbuf = gs + g.gsize + (i64)threadIdx.x * rows_per_thread;
+  for (i64 i = threadIdx.x; i < g.gsize; i += blockDim.x) gsm[i] = st[i];
+  double* rowbuf = gsm + g.gsize + (i64)threadIdx.x * rows_per_thread;
   __syncthreads();
   const i64 q = (i64)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= Q) return;
@@ -223,27 +245,52 @@ __global__ void __launch_bounds__(128) k_wcols(Geom g, IndexPtrs ip, double* __r
   double w[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) w[i] = 0.0;
-  i64 combos = 1;
-  for (int m = 0; m < g.n; ++m) if (m != tgt) combos *= g.rank[m];
-  const int rt = g.rank[tgt];
-  const i64 gst = g.gstride[tgt];
-  for (i64 c = 0; c < combos; ++c) {
-    i64 t = c, goff = 0;
-    double coef = 1.0;
+  // odometer over the other modes' rank indices (first other mode fastest):
+  // suffix products pp[j] = prod_{l >= j} rows_l[idx_l] and the G offset are
+  // updated incrementally, so a combination costs r_t FMAs + O(1)
+  int om[RT_MAX_MODES], rk[RT_MAX_MODES], ro[RT_MAX_MODES], ix[RT_MAX_MODES];
+  i64 gs[RT_MAX_MODES];
+  int no = 0;
+  {
     int o = 0;
     for (int m = 0; m < g.n; ++m) {
       if (m == tgt) continue;
-      const int bm = (int)(t % g.rank[m]);
-      t /= g.rank[m];
-      goff += bm * g.gstride[m];
-      coef *= rowbuf[o + bm];
+      om[no] = m;
+      rk[no] = g.rank[m];
+      ro[no] = o;
+      gs[no] = g.gstride[m];
+      ix[no] = 0;
       o += g.rank[m];
+      ++no;
     }
-    const double* gp = gs + goff;
+  }
+  double pp[RT_MAX_MODES + 1];
+  pp[no] = 1.0;
+  for (int j = no - 1; j >= 0; --j) pp[j] = pp[j + 1] * rowbuf[ro[j]];
+  i64 goff = 0;
+  const int rt = g.rank[tgt];
+  const i64 gst = g.gstride[tgt];
+  while (true) {
+    const double coef = pp[0];
+    const double* gq = gsm + goff;
 #pragma unroll
     for (int i = 0; i < R; ++i)
-      if (i < rt) w[i] = fma(gp[i * gst], coef, w[i]);
+      if (i < rt) w[i] = fma(gq[i * gst], coef, w[i]);
+    // increment the odometer
+    int j = 0;
+    while (j < no) {
+      ++ix[j];
+      goff += gs[j];
+      if (ix[j] < rk[j]) break;
+      goff -= gs[j] * rk[j];
+      ix[j] = 0;
+      ++j;
+    }
+    if (j == no) break;
+    // refresh the suffix products of positions <= j
+    for (int l = j; l >= 0; --l) pp[l] = pp[l + 1] * rowbuf[ro[l] + ix[l]];
   }
+  (void)om;
   double* out = full ? wfull + q * rt : st + w_off + q * rt;
 #pragma unroll
   for (int i = 0; i < R; ++i)
@@ -258,7 +305,7 @@ template __global__ void k_gpass<4>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<8>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<16>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<32>(Geom, IndexPtrs, GPassArgs);
-template __global__ void k_wcols<4>(Geom, IndexPtrs, double*, int, double*, int);
-template __global__ void k_wcols<8>(Geom, IndexPtrs, double*, int, double*, int);
-template __global__ void k_wcols<16>(Geom, IndexPtrs, double*, int, double*, int);
-template __global__ void k_wcols<32>(Geom, IndexPtrs, double*, int, double*, int);
+template __global__ void k_wcols<4>(Geom, IndexPtrs, double*, int, double*, int, int);
+template __global__ void k_wcols<8>(Geom, IndexPtrs, double*, int, double*, int, int);
+template __global__ void k_wcols<16>(Geom, IndexPtrs, double*, int, double*, int, int);
+template __global__ void k_wcols<32>(Geom, IndexPtrs, double*, int, double*, int, int);
