@@ -121,6 +121,10 @@ int64_t rtcur_engine_full_scratch_bytes(rtcur_engine* e);
  * columns, 10 error pass, 11 export, 12 full output (K3).  nphase >= 13. */
 #define RTCUR_NPHASE 13
 int rtcur_engine_profile(rtcur_engine* e, int on);
+/* Restrict the timers to the phases whose bit (1 << phase) is set in `mask`
+ * (default: all).  Timing only the phase a measurement needs keeps the event
+ * overhead (two event records per timed phase launch) out of the other phases. */
+int rtcur_engine_profile_phases(rtcur_engine* e, uint32_t mask);
 int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* counts, int nphase, int reset);
 
 /* Synthetic instance support (bench/tests).  On a mode-1 slab [lo, hi) of a d1 x ... tensor:

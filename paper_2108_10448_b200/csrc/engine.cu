@@ -387,6 +387,7 @@ struct rtcur_engine {
   i64 h_idx_len;
   // optional per-phase CUDA-event timing (rtcur_engine_profile)
   bool prof_on;
+  unsigned prof_mask;  // phases timed while prof_on
   double prof_ms[RT_NPHASE];
   long long prof_cnt[RT_NPHASE];
   std::vector<cudaEvent_t>* prof_pool;
@@ -407,7 +408,7 @@ static cudaEvent_t prof_event(rtcur_engine* e) {
   return ev;
 }
 static void prof_begin(rtcur_engine* e, int ph) {
-  if (!e->prof_on) return;
+  if (!e->prof_on || !((e->prof_mask >> ph) & 1u)) return;
   cudaEvent_t ev = prof_event(e);
   cudaEventRecord(ev, e->st);
   e->prof_open[ph] = ev;
@@ -456,6 +457,12 @@ static int set_smem_limits_once() {
   SMEM_ATTR((k_block_pass<true, true, false, false>)); SMEM_ATTR((k_block_pass<false, true, false, false>));
   SMEM_ATTR(k_hgram);
 #undef SMEM_ATTR
+  // L2 fetch granularity for the sampled gathers (element-sized loads scattered
+  // over X): RTCUR_L2_FETCH=<32|64|128> bytes; unset leaves the device default
+  if (const char* gf = getenv("RTCUR_L2_FETCH")) {
+    const int b = atoi(gf);
+    if (b == 32 || b == 64 || b == 128) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)b));
+  }
   done.store(1);
   return RT_OK;
 }
@@ -517,6 +524,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->lo = slab_lo;
   e->hi = slab_hi;
   e->cur = e->prev = -1;
+  e->prof_mask = ~0u;
   e->use_fast = getenv("RTCUR_NO_FAST_EIG") == nullptr;
   e->prof_pool = new std::vector<cudaEvent_t>();
   if (cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming) != cudaSuccess) {
@@ -1093,11 +1101,20 @@ extern "C" int rtcur_engine_debug_marks(rtcur_engine* e, int64_t* out, int n) {
   return RT_OK;
 }
 
+extern "C" int rtcur_engine_profile_phases(rtcur_engine* e, uint32_t mask) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  CK(cudaStreamSynchronize(e->st));
+  prof_flush(e);
+  e->prof_mask = mask ? mask : ~0u;
+  return RT_OK;
+}
+
 extern "C" int rtcur_engine_profile(rtcur_engine* e, int on) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
   CK(cudaStreamSynchronize(e->st));
   prof_flush(e);
   e->prof_on = on != 0;
+  if (on) e->prof_mask = e->prof_mask ? e->prof_mask : ~0u;
   return RT_OK;
 }
 

@@ -214,7 +214,12 @@ class Engine:
             ctypes.c_void_p(S.data_ptr() if S is not None else 0), ctypes.c_void_p(tf.data_ptr()), sums))
         return L, S, float(sums[0]), float(sums[1])
 
-    def profile(self, on: bool = True):
+    def profile(self, on: bool = True, phases=None):
+        """Enable the CUDA-event phase timers; ``phases``: names to time (default all)."""
+        mask = 0
+        for name in phases or ():
+            mask |= 1 << nat.PHASES.index(name)
+        nat.check(self.lib.rtcur_engine_profile_phases(self.handle, mask))
         nat.check(self.lib.rtcur_engine_profile(self.handle, int(bool(on))))
 
     def profile_read(self, reset: bool = False):

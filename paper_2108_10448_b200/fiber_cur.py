@@ -10,6 +10,7 @@ bit-identical to the reference's for equal seeds (same numpy build).
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -150,6 +151,22 @@ def sample_sizes(shape: Sequence[int], ranks: Sequence[int], upsilon: float):
     return tuple(rows), tuple(cols)
 
 
+_SEEN = threading.local()
+
+
+def _seen_mask(population: int) -> np.ndarray:
+    """Per-thread zeroed membership mask, reused across draws (the draw clears
+    exactly the entries it set, so a 10^7-entry population is not re-zeroed on
+    every RTCUR-R iteration)."""
+    cache = getattr(_SEEN, "masks", None)
+    if cache is None:
+        cache = _SEEN.masks = {}
+    m = cache.get(population)
+    if m is None:
+        m = cache[population] = np.zeros(population, dtype=np.uint8)
+    return m
+
+
 def _draw_without_replacement(rng: np.random.Generator, population: int, k: int) -> np.ndarray:
     """fiber_cur.py:189-209 (permutation for 3k >= pop, else iid stream + first-unique)."""
     if k >= population:
@@ -163,7 +180,7 @@ def _draw_without_replacement(rng: np.random.Generator, population: int, k: int)
     from . import _native
 
     lib = _native.load()
-    seen = np.zeros(population, dtype=np.uint8)
+    seen = _seen_mask(population)
     cap = 2 * k + 64
     out = np.empty(cap, dtype=np.int64)
     nout = 0
@@ -172,8 +189,13 @@ def _draw_without_replacement(rng: np.random.Generator, population: int, k: int)
         batch = rng.integers(0, population, size=need + need // 2 + 16, dtype=np.int64)
         if nout + batch.size > out.size:
             out = np.concatenate([out, np.empty(nout + batch.size, dtype=np.int64)])
-        nout = int(lib.rtcur_append_distinct(out.ctypes.data, nout, batch.ctypes.data, batch.size, seen.ctypes.data,
-                                             population))
+        got = int(lib.rtcur_append_distinct(out.ctypes.data, nout, batch.ctypes.data, batch.size, seen.ctypes.data,
+                                            population))
+        if got < 0:
+            seen[:] = 0
+            raise RuntimeError("rtcur_append_distinct: index outside the population")
+        nout = got
+    seen[out[:nout]] = 0
     return np.sort(out[:k]) + 1
 
 

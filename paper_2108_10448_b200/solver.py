@@ -40,6 +40,7 @@ RANK_DEFICIENCY_RTOL = 1e-8  # solver.py:64 (applied on device, k_svd_fin2)
 # When True, rtcur() records per-phase device times (CUDA events on the solve's
 # stream) into timings["device_ms"] / timings["device_launches"] (bench.py).
 PROFILE = False
+PROFILE_PHASES = None  # phase names timed while PROFILE (None: all)
 
 
 @dataclass(frozen=True)
@@ -382,7 +383,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> Sol
 
     eng = acquire_engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype, slab=src.slab)
     if PROFILE:
-        eng.profile(True)
+        eng.profile(True, PROFILE_PHASES)
     src.attach(eng)
     t0 = time.perf_counter()
     eng.set_sample(idx)
