@@ -1,0 +1,408 @@
+// bp_pass.cuh -- the persistent K1 block pass (template definition).  Explicitly
+// instantiated per rank bucket in bp_rb{4,8,16,32}.cu so the variants compile in
+// parallel; engine.cu/k_block.cu see only the declaration in k_block.cu.
+#pragma once
+#include "bp_types.cuh"
+
+// Per-tile operands of the block pass.  A tile is `ncols` whole columns of one
+// block (P rows each) staged in shared memory: x (column-major, tile-local)
+// and the columns' W rows of both states (row-major, r per column).  A rows
+// are read through L1 from the state (column-major, stride d; core rows via I_1).
+struct BPTile {
+  const unsigned char* x;  // staged x (dtype), already offset by the 16-byte skip
+  int dtype;
+  int P, ncols, r;
+  const double* As;        // A_mode of the threshold state (global) or null
+  const double* Ae;        // A_mode of the error state (global) or null
+  i64 d;                   // A column stride
+  const int* rows0;        // core: I_1 (0-based); fibers: null
+  const double* Wss;       // smem W rows, threshold state
+  const double* Wes;       // smem W rows, error state
+  const int* rmap;         // smem rowpos of the fiber mode (-1: row not in I_k)
+  const double* Asm;       // lanes over columns: the block's A rows (threshold state), smem, row pitch apitch
+  const double* Aem;       // same for the error state
+  int apitch;
+  double* Mk;              // intersection output at the tile's first column (column-major, mrows)
+  int mrows;
+  double zeta;
+  double *s_out, *c_out, *l_out;   // exports at the tile's first element
+  const double* U;         // G pass: U~_1 (|I_1| x r row-major)
+  double* t1;              // G pass: output rows at the tile's first column
+  double* gp;              // G pass: smem partials
+};
+
+__device__ __forceinline__ double bp_x(const BPTile& T, int i) {
+  return T.dtype == 0 ? reinterpret_cast<const double*>(T.x)[i] : (double)reinterpret_cast<const float*>(T.x)[i];
+}
+
+// One entry: threshold against state s, clean value, intersection scatter, error
+// against state e, exports, and the sums.  Returns the clean value.
+template <bool HS, bool HE, bool WM, bool EXP>
+__device__ __forceinline__ double bp_entry(const BPTile& T, double x, double ls, double le, int pos, int ql, int p,
+                                           double& e2, double& x2, bool& bad) {
+  const double sv = fabs(x - ls) <= T.zeta ? 0.0 : x - ls;
+  const double c = x - sv;
+  if (WM && pos >= 0) {
+    T.Mk[pos + (i64)ql * T.mrows] = c;
+    bad |= !isfinite(c);
+  }
+  if (HE) {
+    const double rr = x - le - sv;
+    e2 = fma(rr, rr, e2);
+  }
+  if (EXP) {
+    const int k = ql * T.P + p;
+    if (T.s_out) T.s_out[k] = sv;
+    if (T.c_out) T.c_out[k] = c;
+    if (T.l_out) T.l_out[k] = le;
+  }
+  x2 = fma(x, x, x2);
+  return c;
+}
+
+template <int DT>
+__device__ __forceinline__ double bp_xt(const unsigned char* x, int i) {
+  return DT == 0 ? reinterpret_cast<const double*>(x)[i] : (double)reinterpret_cast<const float*>(x)[i];
+}
+
+// A row dot W row with R terms; A row from shared memory (even pitch, 16-byte aligned)
+template <int R, bool EX>
+__device__ __forceinline__ double bp_dot_sm(const double* __restrict__ arow, const double* w, int r) {
+  double acc = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < R; kk += 2) {
+    const double2 a2 = *reinterpret_cast<const double2*>(arow + kk);
+    if (EX || kk < r) acc = fma(a2.x, w[kk], acc);
+    if (kk + 1 < R && (EX || kk + 1 < r)) acc = fma(a2.y, w[kk + 1], acc);
+  }
+  return acc;
+}
+
+// Lanes over columns (tiles of 32 * 2^k columns, small P): each lane keeps its
+// column's W rows in registers; the warps split the tile into (32-column group,
+// row range) items (the planner makes the group count divide the 8 warps) and
+// the block's A rows come from shared memory as warp-broadcast loads.
+// GP: the G pass -- t1[q, :] = sum_p U~_1[p, :] clean(p, q) on the core,
+// with the row-range partials combined in fixed order through shared memory.
+template <int R, bool EX, int DT, bool HS, bool HE, bool WM, bool EXP, bool GP>
+__device__ __forceinline__ void bp_cols(const BPTile& T, double& e2, double& x2, bool& bad) {
+  const int r = EX ? R : T.r;   // EX: the block rank is exactly R, else r <= R
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int P = T.P, ncols = T.ncols, ap = T.apitch;
+  const int ncg = (ncols + 31) >> 5;
+  const int nrr = max(1, nw / ncg);
+  const int rlen = (P + nrr - 1) / nrr;
+  const int items = ncg * nrr;
+#pragma unroll 1
+  for (int it = w; it < items; it += nw) {
+    const int cg = it % ncg, rr = it / ncg;
+    const int ql = cg * 32 + lane;
+    const bool valid = ql < ncols;
+    double ws[R], we[R], acc[R];
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk) {
+      const bool on = valid && (EX || kk < r);
+      ws[kk] = (HS && on) ? T.Wss[ql * r + kk] : 0.0;
+      we[kk] = (HE && on) ? T.Wes[ql * r + kk] : 0.0;
+      acc[kk] = 0.0;
+    }
+    const int pb = rr * rlen, pe = min(P, pb + rlen);
+    const int qoff = (valid ? ql : 0) * P;
+#pragma unroll 1
+    for (int p = pb; p < pe; ++p) {
+      const double x = bp_xt<DT>(T.x, qoff + p);
+      const double ls = HS ? bp_dot_sm<R, EX>(T.Asm + p * ap, ws, r) : 0.0;
+      const double le = HE ? bp_dot_sm<R, EX>(T.Aem + p * ap, we, r) : 0.0;
+      const int pos = WM ? T.rmap[p] : -1;
+      double c = 0.0;
+      if (valid) c = bp_entry<HS, HE, WM, EXP>(T, x, ls, le, pos, ql, p, e2, x2, bad);
+      if (GP) {
+        const double* u = T.Aem + p * ap;   // U~_1 row p (staged, even pitch)
+#pragma unroll
+        for (int kk = 0; kk < R; kk += 2) {
+          const double2 u2 = *reinterpret_cast<const double2*>(u + kk);
+          if (EX || kk < r) acc[kk] = fma(u2.x, c, acc[kk]);
+          if (kk + 1 < R && (EX || kk + 1 < r)) acc[kk + 1] = fma(u2.y, c, acc[kk + 1]);
+        }
+      }
+    }
+    if (GP) {
+      if (nrr == 1) {
+        if (valid)
+#pragma unroll
+          for (int kk = 0; kk < R; ++kk)
+            if (EX || kk < r) T.t1[(i64)ql * r + kk] = acc[kk];
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk)
+          if (EX || kk < r) T.gp[((i64)rr * ncg * 32 + ql) * r + kk] = acc[kk];
+      }
+    }
+  }
+  if (GP && nrr > 1) {
+    __syncthreads();
+    for (int o = threadIdx.x; o < ncols * r; o += blockDim.x) {
+      double s = 0.0;
+      for (int rr = 0; rr < nrr; ++rr) s += T.gp[(i64)rr * ncg * 32 * r + o];   // fixed order
+      T.t1[o] = s;
+    }
+  }
+}
+
+// Lanes over rows (tall tiles): items are (32-row chunk, column) pairs in
+// chunk-major order and each warp takes a contiguous run of them, so a lane
+// keeps the A rows of its row p in registers across the run (reloaded only at
+// a chunk change) and each column's W row is a warp-broadcast shared load.
+template <int R, bool EX, int DT, bool HS, bool HE, bool WM, bool EXP>
+__device__ __forceinline__ void bp_rows(const BPTile& T, double& e2, double& x2, bool& bad) {
+  const int r = EX ? R : T.r;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int P = T.P, ncols = T.ncols;
+  const int nrc = (P + 31) >> 5;
+  const int items = nrc * ncols;
+  const int i0 = items * w / nw, i1 = items * (w + 1) / nw;
+  // the warp's run [i0, i1) as segments of one row chunk each
+#pragma unroll 1
+  for (int it = i0; it < i1;) {
+    const int rc = it / ncols, qb = it - rc * ncols;
+    const int qe = min(ncols, qb + (i1 - it));
+    it += qe - qb;
+    const int p = rc * 32 + lane;
+    if (p >= P) continue;
+    const i64 grow = T.rows0 ? (i64)T.rows0[p] : (i64)p;
+    double as[R], ae[R];
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk) {
+      const bool on = EX || kk < r;
+      as[kk] = (HS && on) ? __ldg(T.As + grow + (i64)kk * T.d) : 0.0;
+      ae[kk] = (HE && on) ? __ldg(T.Ae + grow + (i64)kk * T.d) : 0.0;
+    }
+    const int pos = WM ? T.rmap[p] : -1;
+#pragma unroll 1
+    for (int q = qb; q < qe; ++q) {
+      const double x = bp_xt<DT>(T.x, q * P + p);
+      const double* wsr = T.Wss + q * r;
+      const double* wer = T.Wes + q * r;
+      double ls = 0.0, le = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < R; ++kk) {
+        if (EX || kk < r) {
+          if (HS) ls = fma(as[kk], wsr[kk], ls);
+          if (HE) le = fma(ae[kk], wer[kk], le);
+        }
+      }
+      bp_entry<HS, HE, WM, EXP>(T, x, ls, le, pos, q, p, e2, x2, bad);
+    }
+  }
+}
+
+template <int RR, int RB, bool HS, bool HE, bool WM, bool EXP, bool GP>
+__device__ __forceinline__ bool bp_try(const BPTile& T, bool cols, double& e2, double& x2, bool& bad) {
+  if (RR > RB || 2 * RR <= RB || T.r != RR) return false;   // exact ranks in (RB/2, RB]
+  constexpr int R = RR <= RB ? RR : RB;
+  if (cols) {
+    if (T.dtype == 0) bp_cols<R, true, 0, HS, HE, WM, EXP, GP>(T, e2, x2, bad);
+    else bp_cols<R, true, 1, HS, HE, WM, EXP, GP>(T, e2, x2, bad);
+  } else if (!GP) {
+    if (T.dtype == 0) bp_rows<R, true, 0, HS, HE, WM, EXP>(T, e2, x2, bad);
+    else bp_rows<R, true, 1, HS, HE, WM, EXP>(T, e2, x2, bad);
+  }
+  return true;
+}
+
+// exact-rank specialisations in the kernel's rank bucket (RB/2, RB], else r <= RB at run time
+template <int RB, bool HS, bool HE, bool WM, bool EXP, bool GP>
+__device__ __forceinline__ void bp_tile_r(const BPTile& T, bool cols, double& e2, double& x2, bool& bad) {
+  if (bp_try<1, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<2, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<3, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<4, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<5, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<6, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<8, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<10, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (bp_try<16, RB, HS, HE, WM, EXP, GP>(T, cols, e2, x2, bad)) return;
+  if (cols) {
+    if (T.dtype == 0) bp_cols<RB, false, 0, HS, HE, WM, EXP, GP>(T, e2, x2, bad);
+    else bp_cols<RB, false, 1, HS, HE, WM, EXP, GP>(T, e2, x2, bad);
+  } else if (!GP) {
+    if (T.dtype == 0) bp_rows<RB, false, 0, HS, HE, WM, EXP>(T, e2, x2, bad);
+    else bp_rows<RB, false, 1, HS, HE, WM, EXP>(T, e2, x2, bad);
+  }
+}
+
+// Persistent K1 block pass.  CTA c processes a contiguous range of tiles of
+// the compact blocks (tiles are whole columns of one block, so x and the
+// columns' W rows are contiguous).  Each tile's x, W_s, W_e ranges are
+// streamed into a shared-memory ring by cp.async.bulk (one mbarrier per
+// stage).  Per entry -- L = A[row] . W[col] (r FMAs per state), hard
+// threshold, clean value, intersection scatter, error sums -- with the lane
+// mapping chosen per block (TileMap::cols): lanes over columns for short
+// blocks, lanes over rows for tall ones.  Per-(CTA, block) partial sums are
+// combined by the last CTA in CTA order (deterministic: the tile -> CTA
+// assignment is static).  GP: the G pass over the core block's tiles only.
+template <bool HS, bool HE, bool WM, bool EXP, bool GP, int RB>
+__global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeom G) {
+  extern __shared__ __align__(128) unsigned char bp_smem[];
+  __shared__ unsigned long long bars[4];
+  __shared__ double red[8];
+  __shared__ bool am_last;
+  const int tid = threadIdx.x;
+  const i64 ntiles = GP ? tm.first[1] : tm.first[tm.nblk];
+  const int esz = a.dtype == 0 ? 8 : 4;
+  int* rmap = reinterpret_cast<int*>(bp_smem);
+  double* gp = reinterpret_cast<double*>(bp_smem + (((size_t)G.rowmap_ints * 4 + 15) & ~(size_t)15));
+  double* Asm = gp + G.gp_doubles;
+  double* Aem = Asm + G.a_doubles;
+  unsigned char* stage0 = reinterpret_cast<unsigned char*>(Aem + G.a_doubles);
+  const size_t stage_bytes = (size_t)G.x_bytes + 2 * (size_t)G.w_doubles * 8;
+  const char* xbase = reinterpret_cast<const char*>(a.xb);
+  if (tid == 0) {
+    for (int st = 0; st < G.stages; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // tile t -> block b, first column q0 and column count (no divisions: tiles are cpt[b] whole columns)
+  auto tile_cols = [&](i64 t, int& b, i64& q0, int& nc) {
+    b = tile_block(tm, t);
+    q0 = (t - tm.first[b]) * tm.cpt[b];
+    nc = (int)min((i64)tm.cpt[b], g.blk[b].Q - q0);
+  };
+  // bulk-copy tile t (x range and, when used, the columns' W rows of both states)
+  auto issue = [&](i64 t, int st) {
+    int b, nc;
+    i64 q0;
+    tile_cols(t, b, q0, nc);
+    const BlockDesc& bd = g.blk[b];
+    unsigned char* sb = stage0 + (size_t)st * stage_bytes;
+    const i64 e0 = q0 * bd.P, e1 = e0 + (i64)nc * bd.P;
+    const i64 x0 = ((bd.off + e0) * esz) & ~(i64)15, x1 = ((bd.off + e1) * esz + 15) & ~(i64)15;
+    const i64 q1 = q0 + nc;
+    const i64 w0 = ((bd.w_off + q0 * bd.r) * 8) & ~(i64)15, w1 = ((bd.w_off + q1 * bd.r) * 8 + 15) & ~(i64)15;
+    unsigned total = (unsigned)(x1 - x0);
+    if (HS) total += (unsigned)(w1 - w0);
+    if (HE) total += (unsigned)(w1 - w0);
+    mbar_expect_tx(&bars[st], total);
+    tma_load_1d(sb, xbase + x0, (unsigned)(x1 - x0), &bars[st]);
+    if (HS) tma_load_1d(sb + G.x_bytes, reinterpret_cast<const char*>(a.st_s) + w0, (unsigned)(w1 - w0), &bars[st]);
+    if (HE)
+      tma_load_1d(sb + G.x_bytes + (size_t)G.w_doubles * 8, reinterpret_cast<const char*>(a.st_e) + w0,
+                  (unsigned)(w1 - w0), &bars[st]);
+  };
+  // contiguous tile range per CTA: at most a couple of block switches
+  const i64 t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const i64 my_n = t_end - t_begin;
+  if (tid == 0)
+    for (int st = 0; st < G.stages && st < my_n; ++st) issue(t_begin + st, st);
+
+  int cur_b = -1;
+  double e2 = 0.0, x2 = 0.0;
+  bool bad = false;
+  auto flush = [&](int b) {
+    const double se = block_sum(e2, red);
+    const double sx = block_sum(x2, red);
+    if (tid == 0 && a.partial) {
+      a.partial[((i64)blockIdx.x * tm.nblk + b) * 2] = se;
+      a.partial[((i64)blockIdx.x * tm.nblk + b) * 2 + 1] = sx;
+    }
+    e2 = 0.0;
+    x2 = 0.0;
+  };
+  if (a.partial && tid < tm.nblk * 2) a.partial[(i64)blockIdx.x * tm.nblk * 2 + tid] = 0.0;
+  int st = 0;
+  unsigned phase = 0;
+  for (i64 i = 0; i < my_n; ++i) {
+    const i64 t = t_begin + i;
+    int b, nc;
+    i64 q0;
+    tile_cols(t, b, q0, nc);
+    const BlockDesc& bd = g.blk[b];
+    const int P = (int)bd.P;
+    const bool core = bd.is_core;
+    const int r = bd.r;
+    if (b != cur_b) {
+      if (cur_b >= 0) flush(cur_b);   // (block_sum has barriers: everyone is done with the old row map)
+      cur_b = b;
+      if (WM && !core)
+        for (int pp = tid; pp < P; pp += blockDim.x) rmap[pp] = ip.rowpos[bd.mode][pp];
+      if (tm.cols[b]) {   // lanes over columns: the block's A rows, row-major with an even pitch
+        const int ap = (r + 1) & ~1;
+        const i64 d = g.dim[bd.mode];
+        for (int e = tid; e < P * ap; e += blockDim.x) {
+          const int pp = e / ap, kk = e - pp * ap;
+          const i64 row = core ? (i64)ip.rows[0][pp] : (i64)pp;
+          if (HS) Asm[e] = kk < r ? a.st_s[g.a_off[bd.mode] + row + kk * d] : 0.0;
+          if (HE) Aem[e] = kk < r ? a.st_e[g.a_off[bd.mode] + row + kk * d] : 0.0;
+          if (GP) Aem[e] = kk < r ? a.U[(i64)pp * r + kk] : 0.0;   // U~_1 rows (the error state is unused)
+        }
+      }
+      __syncthreads();
+    }
+    const unsigned char* sb = stage0 + (size_t)st * stage_bytes;
+    const i64 e0 = q0 * P;
+    const int xskip = (int)((((bd.off + e0) * esz) & 15) / esz);
+    const int wskip = (int)((((bd.w_off + q0 * r) * 8) & 15) / 8);
+    BPTile T;
+    T.x = sb + (size_t)xskip * esz;
+    T.dtype = a.dtype;
+    T.P = P;
+    T.ncols = nc;
+    T.r = r;
+    T.As = HS ? a.st_s + g.a_off[bd.mode] : nullptr;
+    T.Ae = HE ? a.st_e + g.a_off[bd.mode] : nullptr;
+    T.d = g.dim[bd.mode];
+    T.rows0 = core ? ip.rows[0] : nullptr;
+    T.Wss = reinterpret_cast<const double*>(sb + G.x_bytes) + wskip;
+    T.Wes = reinterpret_cast<const double*>(sb + G.x_bytes + (size_t)G.w_doubles * 8) + wskip;
+    T.rmap = rmap;
+    T.Asm = Asm;
+    T.Aem = Aem;
+    T.apitch = (r + 1) & ~1;
+    T.Mk = (WM && !core) ? a.M[bd.mode] + q0 * g.nrows[bd.mode] : nullptr;
+    T.mrows = (int)g.nrows[bd.mode];
+    T.zeta = a.zeta;
+    const i64 gofs = bd.off + e0;
+    T.s_out = EXP && a.s_out ? a.s_out + gofs : nullptr;
+    T.c_out = EXP && a.c_out ? a.c_out + gofs : nullptr;
+    T.l_out = EXP && a.l_out ? a.l_out + gofs : nullptr;
+    T.U = GP ? a.U : nullptr;
+    T.t1 = GP ? a.t1 + q0 * r : nullptr;
+    T.gp = gp;
+    mbar_wait(&bars[st], phase);
+    if (core) bp_tile_r<RB, HS, HE, false, EXP, GP>(T, tm.cols[b] != 0, e2, x2, bad);
+    else bp_tile_r<RB, HS, HE, WM, EXP, false>(T, tm.cols[b] != 0, e2, x2, bad);
+    __syncthreads();   // stage st fully consumed
+    if (tid == 0 && i + G.stages < my_n) issue(t_begin + i + G.stages, st);
+    if (++st == G.stages) {
+      st = 0;
+      phase ^= 1u;
+    }
+  }
+  if (cur_b >= 0) flush(cur_b);
+  if (bad) atomicExch(a.nonfinite, 1);
+  if (a.partial == nullptr) return;
+  if (tid == 0) {
+    __threadfence();
+    unsigned int ticket = atomicAdd(a.counter, 1u);
+    am_last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // last CTA: per-block sums over CTAs in CTA order (deterministic)
+  for (int bb = 0; bb < tm.nblk; ++bb) {
+    double se = 0.0, sx = 0.0;
+    for (i64 c = tid; c < gridDim.x; c += blockDim.x) {
+      se += ((volatile double*)a.partial)[(c * tm.nblk + bb) * 2];
+      sx += ((volatile double*)a.partial)[(c * tm.nblk + bb) * 2 + 1];
+    }
+    se = block_sum(se, red);
+    sx = block_sum(sx, red);
+    if (tid == 0) {
+      a.sums[2 * bb] = se;
+      a.sums[2 * bb + 1] = sx;
+    }
+  }
+  if (tid == 0) *a.counter = 0u;
+}
+

@@ -203,48 +203,57 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   // tiles
   TileMap& tm = P.tm;
   tm.nblk = g.nblk;
-  // Block-pass shared memory: A rows of both states for the largest block,
-  // the intersection row map, and a ring of x/W tile stages in what is left.
+  // Block-pass tiles: whole columns, at most BP_X_BYTES of x per stage.  Lanes
+  // over columns when >= 32 columns fit (32 * 2^k columns, <= 8 column groups),
+  // else lanes over rows with the column-range count that balances the 8 warps.
   {
-    i64 maxP = 1, maxArows = 1;
-    for (int b = 0; b < g.nblk; ++b) {
-      maxP = std::max(maxP, g.blk[b].P);
-      maxArows = std::max(maxArows, g.blk[b].P * (i64)bp_rp(g.blk[b].r));
-    }
+    i64 maxP = 1;
+    for (int b = 0; b < g.nblk; ++b) maxP = std::max(maxP, g.blk[b].P);
     if (maxP > TILE_MAX_ELEMS) return fail(RT_ERR_UNSUPPORTED, "mode extent above 4096 not supported");
     BPGeom& G = P.bp;
     G.rowmap_ints = (int)maxP;
-    // two CTAs per SM when the staged A rows leave room for 3 stages of >= 16 KB
-    const i64 rowmap_b = (G.rowmap_ints * 4 + 15) & ~15;
-    const i64 a_b = 2 * maxArows * 8;
-    i64 cta_budget = 100 * 1024;
-    G.a_doubles = (int)maxArows;
-    if (cta_budget - a_b - rowmap_b - 512 < 3 * 16 * 1024) cta_budget = 227 * 1024;   // one CTA per SM
-    if (cta_budget - a_b - rowmap_b - 512 < 3 * 16 * 1024) {
-      G.a_doubles = 0;                                                               // A from global (L1)
-      cta_budget = 100 * 1024;
-    }
-    const i64 budget = cta_budget - 2 * (i64)G.a_doubles * 8 - rowmap_b - 512;
+    G.gp_doubles = 0;
     G.stages = 3;
-    const i64 stage = budget / G.stages;
-    // x bytes per stage: whole columns of the largest P, at most TILE_MAX_ELEMS elements
-    G.x_bytes = (int)std::min<i64>((i64)TILE_MAX_ELEMS * P.esize + 32, (stage * 3 / 4) & ~15LL);
-    G.w_doubles = (int)(((stage - G.x_bytes) / 2 / 8) & ~1LL);
-    G.rp_max = bp_rp(P.rmax);
+    G.x_bytes = BP_X_BYTES + 32;
+    int wmax = 2;
+    i64 amax = 0;
+    tm.tile = TILE_MAX_ELEMS;
+    i64 t = 0;
+    for (int b = 0; b < g.nblk; ++b) {
+      tm.first[b] = t;
+      const i64 Pb = g.blk[b].P, nel = Pb * g.blk[b].Q;
+      const int rb = g.blk[b].r;
+      const i64 xcap = std::max<i64>(1, BP_X_BYTES / (Pb * P.esize));
+      const i64 wcap = std::max<i64>(1, (BP_W_DOUBLES - 4) / rb);
+      i64 cpt;
+      if (std::min(xcap, wcap) >= 32) {
+        cpt = 32;
+        while (cpt * 2 <= std::min<i64>(std::min(xcap, wcap), 256)) cpt *= 2;
+        tm.cols[b] = 1;
+        tm.ncr[b] = 1;
+      } else {
+        cpt = std::min(xcap, wcap);
+        tm.cols[b] = 0;
+        const i64 nrc = cdiv(Pb, 32);
+        double best = -1.0;
+        int bn = 1;
+        for (int ncr = 1; ncr <= std::min<i64>(cpt, 16); ++ncr) {
+          const double eff = (double)(nrc * cpt) / (double)(cdiv(nrc * ncr, 8) * 8 * cdiv(cpt, ncr));
+          if (eff > best + 1e-9) { best = eff; bn = ncr; }
+        }
+        tm.ncr[b] = bn;
+      }
+      tm.te[b] = cpt * Pb;
+      tm.cpt[b] = (int)cpt;
+      if (tm.cols[b]) amax = std::max<i64>(amax, Pb * ((rb + 1) & ~1));
+      wmax = std::max(wmax, (int)(cpt * rb + 4));
+      t += cdiv(nel, tm.te[b]);
+    }
+    G.w_doubles = (wmax + 1) & ~1;
+    G.a_doubles = (int)((amax + 1) & ~1);
+    tm.first[g.nblk] = t;
   }
-  tm.tile = TILE_MAX_ELEMS;
-  i64 t = 0;
-  for (int b = 0; b < g.nblk; ++b) {
-    tm.first[b] = t;
-    const i64 Pb = g.blk[b].P, nel = Pb * g.blk[b].Q;
-    // whole columns; bounded by the stage's x bytes and W rows
-    i64 cpt = std::max<i64>(1, (P.bp.x_bytes - 32) / (Pb * P.esize));
-    cpt = std::min<i64>(cpt, std::max<i64>(1, (P.bp.w_doubles - 4) / g.blk[b].r));
-    cpt = std::min<i64>(cpt, std::max<i64>(1, TILE_MAX_ELEMS / Pb));
-    tm.te[b] = cpt * Pb;
-    t += cdiv(nel, tm.te[b]);
-  }
-  tm.first[g.nblk] = t;
+
   P.col_off[0] = 0;
   for (int b = 0; b < g.nblk; ++b) P.col_off[b + 1] = P.col_off[b] + g.blk[b].Q;
   // gram / svd sizing
@@ -451,10 +460,19 @@ static int set_smem_limits_once() {
   SMEM_ATTR(k_eig);
   SMEM_ATTR(k_wcols<4>); SMEM_ATTR(k_wcols<8>); SMEM_ATTR(k_wcols<16>); SMEM_ATTR(k_wcols<32>);
   SMEM_ATTR(k_zproj<4>); SMEM_ATTR(k_zproj<8>); SMEM_ATTR(k_zproj<16>); SMEM_ATTR(k_zproj<32>);
-  SMEM_ATTR((k_block_pass<true, true, false, true>)); SMEM_ATTR((k_block_pass<true, false, false, true>));
-  SMEM_ATTR((k_block_pass<false, true, false, true>)); SMEM_ATTR((k_block_pass<false, false, false, true>));
-  SMEM_ATTR((k_block_pass<true, false, true, false>)); SMEM_ATTR((k_block_pass<false, false, true, false>));
-  SMEM_ATTR((k_block_pass<true, true, false, false>)); SMEM_ATTR((k_block_pass<false, true, false, false>));
+#define BP_ATTRS(RB)                                                                                     \
+  SMEM_ATTR((k_block_pass<true, true, false, true, false, RB>));                                         \
+  SMEM_ATTR((k_block_pass<true, false, false, true, false, RB>));                                        \
+  SMEM_ATTR((k_block_pass<false, true, false, true, false, RB>));                                        \
+  SMEM_ATTR((k_block_pass<false, false, false, true, false, RB>));                                       \
+  SMEM_ATTR((k_block_pass<true, false, true, false, false, RB>));                                        \
+  SMEM_ATTR((k_block_pass<false, false, true, false, false, RB>));                                       \
+  SMEM_ATTR((k_block_pass<true, true, false, false, false, RB>));                                        \
+  SMEM_ATTR((k_block_pass<false, true, false, false, false, RB>));                                       \
+  SMEM_ATTR((k_block_pass<true, false, false, false, true, RB>));                                        \
+  SMEM_ATTR((k_block_pass<false, false, false, false, true, RB>))
+  BP_ATTRS(4); BP_ATTRS(8); BP_ATTRS(16); BP_ATTRS(32);
+#undef BP_ATTRS
   SMEM_ATTR(k_hgram);
 #undef SMEM_ATTR
   // L2 fetch granularity for the sampled gathers (element-sized loads scattered
@@ -672,6 +690,19 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   return RT_OK;
 }
 
+// persistent grid: as many CTAs per SM as the kernel's registers and shared memory allow (<= 4)
+template <typename K>
+static int launch_bp(K kern, i64 ntiles, i64 smb, cudaStream_t st, const Geom& g, const TileMap& tm,
+                     const IndexPtrs& ip, const PassArgs& a, const BPGeom& G) {
+  int per_sm = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, (size_t)smb));
+  per_sm = std::max(1, std::min(per_sm, 4));
+  const unsigned grid = (unsigned)std::max<i64>(1, std::min<i64>(148 * per_sm, ntiles));
+  kern<<<grid, 256, smb, st>>>(g, tm, ip, a, G);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
 static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_e, double zeta, bool with_M,
                           double* s_out, double* c_out, double* l_out, bool sums, int phase) {
   const Plan& P = e->P;
@@ -696,21 +727,31 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   a.nonfinite = e->at<int>(P.o_nonfinite);
   prof_begin(e, phase);
   const i64 smb = bp_smem_bytes(P.bp);
-  const unsigned per_sm = smb <= 110 * 1024 ? 2 : 1;
-  const unsigned grid = (unsigned)std::min<i64>(148 * per_sm, P.tm.first[P.g.nblk]);
   const bool hs = st_s != nullptr, he = st_e != nullptr;
+#define BP_LAUNCH(HS, HE, WM, EXP)                                                                        \
+  (P.rb == 4    ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 4>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
+                            ip, a, P.bp)                                                                          \
+   : P.rb == 8  ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 8>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
+                            ip, a, P.bp)                                                                          \
+   : P.rb == 16 ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 16>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
+                            P.tm, ip, a, P.bp)                                                                    \
+                : launch_bp(k_block_pass<HS, HE, WM, EXP, false, 32>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
+                            P.tm, ip, a, P.bp))
+  int lst;
   if (s_out || c_out || l_out) {
-    if (hs && he) k_block_pass<true, true, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
-    else if (hs) k_block_pass<true, false, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
-    else if (he) k_block_pass<false, true, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
-    else k_block_pass<false, false, false, true><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    if (hs && he) lst = BP_LAUNCH(true, true, false, true);
+    else if (hs) lst = BP_LAUNCH(true, false, false, true);
+    else if (he) lst = BP_LAUNCH(false, true, false, true);
+    else lst = BP_LAUNCH(false, false, false, true);
   } else if (with_M) {
-    if (hs) k_block_pass<true, false, true, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
-    else k_block_pass<false, false, true, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    if (hs) lst = BP_LAUNCH(true, false, true, false);
+    else lst = BP_LAUNCH(false, false, true, false);
   } else {
-    if (hs) k_block_pass<true, true, false, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
-    else k_block_pass<false, true, false, false><<<grid, 256, smb, e->st>>>(P.g, P.tm, ip, a, P.bp);
+    if (hs) lst = BP_LAUNCH(true, true, false, false);
+    else lst = BP_LAUNCH(false, true, false, false);
   }
+#undef BP_LAUNCH
+  if (lst) return lst;
   LAUNCH_CHECK();
   prof_end(e, phase);
   return RT_OK;
@@ -926,9 +967,40 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   double* t1 = e->at<double>(P.o_gt1);
   gp.t1 = (n == 1) ? sto : t0;
   {
-    const i64 Q = g.blk[0].Q;
-    DISPATCH_R(rbucket(g.rank[0]), k_gpass, (unsigned)cdiv(Q * 32, 256), 256, 0, e->st, g, ip, gp);
-    LAUNCH_CHECK();
+    // first contraction t1 = clean_core x_1 U~_1^T on the block-pass tiles (lanes over columns)
+    IndexPtrs ipg = make_ip(e);
+    PassArgs pa;
+    memset(&pa, 0, sizeof(pa));
+    pa.xb = e->ws + P.o_xb;
+    pa.dtype = P.dtype;
+    pa.st_s = st_s;
+    pa.zeta = zeta;
+    pa.U = gp.U[0];
+    pa.t1 = gp.t1;
+    pa.nonfinite = e->at<int>(P.o_nonfinite);
+    BPGeom G = P.bp;
+    G.gp_doubles = 256 * g.rank[0];
+    const i64 smb = bp_smem_bytes(G);
+    if (P.tm.cols[0]) {
+      int lst;
+#define GP_LAUNCH(RB)                                                                                      \
+  (st_s ? launch_bp(k_block_pass<true, false, false, false, true, RB>, P.tm.first[1], smb, e->st, g, P.tm, ipg, \
+                    pa, G)                                                                                   \
+        : launch_bp(k_block_pass<false, false, false, false, true, RB>, P.tm.first[1], smb, e->st, g, P.tm, ipg, \
+                    pa, G))
+      switch (rbucket(g.rank[0])) {
+        case 4: lst = GP_LAUNCH(4); break;
+        case 8: lst = GP_LAUNCH(8); break;
+        case 16: lst = GP_LAUNCH(16); break;
+        default: lst = GP_LAUNCH(32); break;
+      }
+#undef GP_LAUNCH
+      if (lst) return lst;
+    } else {   // tall core tiles (fewer than 32 columns fit a stage): warp per column
+      const i64 Q = g.blk[0].Q;
+      DISPATCH_R(rbucket(g.rank[0]), k_gpass, (unsigned)cdiv(Q * 32, 256), 256, 0, e->st, g, ipg, gp);
+      LAUNCH_CHECK();
+    }
   }
   {
     i64 rho = g.rank[0];

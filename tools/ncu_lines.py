@@ -1,12 +1,13 @@
 """Summarise an ncu report's source page: top CUDA source lines by warp-state samples.
 
-usage: python tools/ncu_lines.py report.ncu-rep [N]
+usage: python tools/ncu_lines.py report.ncu-rep [N] [launch index]
 """
 import csv, io, os, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+extra = ["--launch-skip", sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + extra,
                      capture_output=True, text=True).stdout
 data, fname, hdr = [], "", None
 for r in csv.reader(io.StringIO(out)):
