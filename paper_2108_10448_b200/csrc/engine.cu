@@ -251,6 +251,12 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     }
     G.w_doubles = (wmax + 1) & ~1;
     G.a_doubles = (int)((amax + 1) & ~1);
+    // three stages when two CTAs per SM still fit (with the G pass's partials), else two
+    {
+      BPGeom g3 = G;
+      g3.gp_doubles = 256 * P.rmax;
+      if (bp_smem_bytes(g3) + 1024 > 113 * 1024) G.stages = 2;
+    }
     tm.first[g.nblk] = t;
   }
 
