@@ -143,8 +143,39 @@ __device__ __forceinline__ double eig_kval(const double* A, bool full, int ld, i
   return full ? A[i * ld + j] : (i >= j ? A[pk(i, j)] : A[pk(j, i)]);
 }
 
-// Cholesky-QR of X (s x r, column-major): X <- X R^-1.  false if not SPD.
-__device__ bool eig_cholqr(double* X, int s, int r, double* C, double* red, double* scal) {
+// In-place lower Cholesky of the r x r symmetric C (column-major, r <= 32) by
+// warp 0, lane i owning row i: C = L L^T with L in the lower triangle and the
+// reciprocal diagonal in rinv[0..r).  Every pivot must exceed `floor` (else
+// false).  Call with the whole block; returns a block-uniform result.
+__device__ bool eig_chol_warp(double* C, int r, double* rinv, double floor, double* scal) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {
+    bool ok = true;
+    for (int k = 0; k < r; ++k) {
+      // pivot (row k, already updated by the previous columns)
+      const double piv = C[k + k * r];
+      if (!(piv > floor)) { ok = false; break; }
+      const double d = sqrt(piv), di = 1.0 / d;
+      if (lane == k) { C[k + k * r] = d; rinv[k] = di; }
+      double lik = 0.0;
+      if (lane > k && lane < r) {
+        lik = C[lane + k * r] * di;
+        C[lane + k * r] = lik;
+      }
+      __syncwarp();
+      // trailing update of row `lane`: C[lane, j] -= L[lane, k] L[j, k], k < j <= lane
+      if (lane > k && lane < r)
+        for (int j = k + 1; j <= lane; ++j) C[lane + j * r] = fma(-lik, C[j + k * r], C[lane + j * r]);
+      __syncwarp();
+    }
+    if (lane == 0) scal[8] = ok ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  return scal[8] != 0.0;
+}
+
+// Cholesky-QR of X (s x r, column-major): X <- X L^-T.  false if not SPD.
+__device__ bool eig_cholqr(double* X, int s, int r, double* C, double* rinv, double* scal) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   const int np = r * (r + 1) / 2;
   for (int q = wid; q < np; q += nw) {
@@ -157,38 +188,18 @@ __device__ bool eig_cholqr(double* X, int s, int r, double* C, double* red, doub
     if (lane == 0) { C[a + b * r] = d; C[b + a * r] = d; }
   }
   __syncthreads();
-  if (tid == 0) {
-    // in-place upper Cholesky C = R^T R (R stored in the upper triangle of C)
-    bool ok = true;
-    const double c00 = C[0];
-    for (int j = 0; j < r && ok; ++j) {
-      for (int i = 0; i <= j; ++i) {
-        double v = C[i + j * r];
-        for (int k = 0; k < i; ++k) v -= C[k + i * r] * C[k + j * r];
-        if (i == j) {
-          if (!(v > 1e-28 * c00)) { ok = false; break; }
-          C[j + j * r] = sqrt(v);
-        } else {
-          C[i + j * r] = v / C[i + i * r];
-        }
-      }
-    }
-    scal[8] = ok ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  if (scal[8] == 0.0) return false;
-  // rows: x R = x_old  (forward substitution over columns)
+  if (!eig_chol_warp(C, r, rinv, 1e-28 * C[0], scal)) return false;
+  // rows: y L^T = x  (forward substitution, reciprocal pivots)
   for (int i = tid; i < s; i += blockDim.x) {
     double xr[RT_MAX_RANK];
     for (int j = 0; j < r; ++j) {
       double v = X[j * s + i];
-      for (int k = 0; k < j; ++k) v -= xr[k] * C[k + j * r];
-      xr[j] = v / C[j + j * r];
+      for (int k = 0; k < j; ++k) v = fma(-xr[k], C[j + k * r], v);
+      xr[j] = v * rinv[j];
     }
     for (int j = 0; j < r; ++j) X[j * s + i] = xr[j];
   }
   __syncthreads();
-  (void)red;
   return true;
 }
 
@@ -196,6 +207,7 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
                              double* C, double* Rm, double* red, double* red2, double* scal, const double* warmA,
                              const int* rows, i64 d, int max_steps) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  double* rinv = Rm;   // r reciprocal pivots
   // trace of K and the warm start
   double t = 0.0;
   for (int i = tid; i < s; i += blockDim.x) t += eig_kval(A, full, ld, i, i);
@@ -209,25 +221,50 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
   const double trK = warp_sum_of(red, nw);
   if (!(trK > 0.0)) return false;
   for (int rep = 0; rep < 2; ++rep)
-    if (!eig_cholqr(X, s, r, C, red, scal)) return false;
+    if (!eig_cholqr(X, s, r, C, rinv, scal)) return false;
+  const int nch = (r + 3) >> 2;   // 4-column chunks
   for (int step = 0; step < max_steps; ++step) {
-    // Y = K X
-    for (int e = tid; e < s * r; e += blockDim.x) {
-      const int i = e % s, c = e / s;
-      const double* x = X + c * s;
-      double a0 = 0.0, a1 = 0.0;
-      int j = 0;
+    // Y = K X: item (row i, 4-column chunk), each K element read once per chunk
+    for (int it = tid; it < s * nch; it += blockDim.x) {
+      const int ch = it / s, i = it - ch * s;
+      const int c0 = ch * 4;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* x0 = X + c0 * s;
+      const bool h1 = c0 + 1 < r, h2 = c0 + 2 < r, h3 = c0 + 3 < r;
       if (full) {
         const double* row = A + i * ld;
-        for (; j + 1 < s; j += 2) {
-          a0 = fma(row[j], x[j], a0);
-          a1 = fma(row[j + 1], x[j + 1], a1);
+        for (int j = 0; j < s; ++j) {
+          const double k = row[j];
+          a0 = fma(k, x0[j], a0);
+          if (h1) a1 = fma(k, x0[s + j], a1);
+          if (h2) a2 = fma(k, x0[2 * s + j], a2);
+          if (h3) a3 = fma(k, x0[3 * s + j], a3);
         }
-        if (j < s) a0 = fma(row[j], x[j], a0);
       } else {
-        for (; j < s; ++j) a0 = fma(eig_kval(A, false, ld, i, j), x[j], a0);
+        // row part j <= i (contiguous packed row), column part j > i (column i of rows j)
+        const double* row = A + pk(i, 0);
+        for (int j = 0; j <= i; ++j) {
+          const double k = row[j];
+          a0 = fma(k, x0[j], a0);
+          if (h1) a1 = fma(k, x0[s + j], a1);
+          if (h2) a2 = fma(k, x0[2 * s + j], a2);
+          if (h3) a3 = fma(k, x0[3 * s + j], a3);
+        }
+        int cb = pk(i + 1, i);
+        for (int j = i + 1; j < s; ++j) {
+          const double k = A[cb];
+          cb += j + 1;
+          a0 = fma(k, x0[j], a0);
+          if (h1) a1 = fma(k, x0[s + j], a1);
+          if (h2) a2 = fma(k, x0[2 * s + j], a2);
+          if (h3) a3 = fma(k, x0[3 * s + j], a3);
+        }
       }
-      Y[e] = a0 + a1;
+      double* y0 = Y + c0 * s + i;
+      y0[0] = a0;
+      if (h1) y0[s] = a1;
+      if (h2) y0[2 * s] = a2;
+      if (h3) y0[3 * s] = a3;
     }
     __syncthreads();
     // H = X^T Y (symmetrised)
@@ -257,61 +294,32 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
     if (lane == 0) red2[wid] = rn;
     __syncthreads();
     const double res = sqrt(warp_sum_of(red2, nw));
+    // stagnation: the residual must at least halve every two steps, else the
+    // gap is too small for this path (the full solver is cheaper than waiting)
+    if (step >= 4 && !(res <= 0.5 * scal[12 + (step & 1)])) return false;
+    __syncthreads();
+    if (tid == 0) scal[12 + (step & 1)] = res;
+    if (tid == 0) scal[14] = (double)(step + 1);
     double trH = 0.0;
     for (int c = 0; c < r; ++c) trH += H[c + c * r];
     // lambda_min(H) <= tr H / r: if even that cannot exceed the energy outside the
     // subspace, the gap bound can never certify -> give up at once (full solver)
     if (!(trH / r - (trK - trH) > 0.0)) return false;
-    // certify (one warp runs Jacobi for lambda_min(H) only when the residual is small)
+    // certify: lambda_min(H) > mu = (tr K - tr H) + 1e12 res  <=>  H - mu I is positive
+    // definite (one warp Cholesky of the shifted copy; no eigen-solve needed)
     if (res <= 1e-9 * trK) {
-      if (wid == 0) {
-        for (int e = lane; e < r * r; e += 32) Rm[e] = H[e];
-        __syncwarp();
-        for (int sweep = 0; sweep < 30; ++sweep) {
-          double off = 0.0;
-          for (int e = lane; e < r * r; e += 32)
-            if (e % r != e / r) off += Rm[e] * Rm[e];
-          off = warp_sum(off);
-          if (off <= 1e-32 * trH * trH) break;
-          for (int p = 0; p < r - 1; ++p)
-            for (int qq = p + 1; qq < r; ++qq) {
-              const double apq = Rm[p + qq * r];
-              if (apq == 0.0) continue;
-              const double app = Rm[p + p * r], aqq = Rm[qq + qq * r];
-              const double th = (aqq - app) / (2.0 * apq);
-              const double tt = copysign(1.0, th) / (fabs(th) + sqrt(th * th + 1.0));
-              const double cs = 1.0 / sqrt(tt * tt + 1.0), sn = tt * cs;
-              __syncwarp();
-              if (lane < r) {
-                const double hp = Rm[lane + p * r], hq = Rm[lane + qq * r];
-                Rm[lane + p * r] = cs * hp - sn * hq;
-                Rm[lane + qq * r] = sn * hp + cs * hq;
-              }
-              __syncwarp();
-              if (lane < r) {
-                const double hp = Rm[p + lane * r], hq = Rm[qq + lane * r];
-                Rm[p + lane * r] = cs * hp - sn * hq;
-                Rm[qq + lane * r] = sn * hp + cs * hq;
-              }
-              __syncwarp();
-            }
-        }
-        if (lane == 0) {
-          double lmin = Rm[0];
-          for (int c = 1; c < r; ++c) lmin = fmin(lmin, Rm[c + c * r]);
-          const double delta = lmin - (trK - trH);
-          scal[9] = (delta > 0.0 && res <= 1e-12 * delta) ? 1.0 : (delta > 0.0 ? 0.0 : -1.0);
-        }
-      }
+      const double mu = (trK - trH) + 1e12 * res;
+      double* Hs = C;   // scratch (C is re-formed by the next Cholesky-QR)
+      for (int e = tid; e < r * r; e += blockDim.x) Hs[e] = H[e] - ((e % r == e / r) ? mu : 0.0);
       __syncthreads();
-      if (scal[9] > 0.0) return true;
+      if (eig_chol_warp(Hs, r, rinv, 0.0, scal)) return true;
     }
     if (step + 1 == max_steps) break;
     // X <- orth(Y)
     for (int e = tid; e < s * r; e += blockDim.x) X[e] = Y[e];
     __syncthreads();
     for (int rep = 0; rep < 2; ++rep)
-      if (!eig_cholqr(X, s, r, C, red, scal)) return false;
+      if (!eig_cholqr(X, s, r, C, rinv, scal)) return false;
   }
   return false;
 }
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
     const bool ok = eig_subspace(A, full, ld, s, r, E, Ysub, Hs, Cs, Rs, red, red2, scal, ea.warmA[mi],
                                  ea.warm_rows[mi], ea.warm_d[mi], ea.max_sub_steps);
     if (ok) {
-      if (tid == 0 && ea.fast_used) ea.fast_used[mi] = 1;
+      if (tid == 0 && ea.fast_used) ea.fast_used[mi] = (int)scal[14];   // subspace steps taken (>= 1)
       for (int e = tid; e < s * r; e += blockDim.x) ea.E[mi][e] = E[e];
       for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = 0.0;
       if (tm && tid == 0) tm[2] = tm[3] = tm[4] = tm[5] = clock64();
@@ -500,58 +508,111 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
       __syncthreads();                                             // B2
     }
   } else {
-    for (int k = 0; k + 2 < s; ++k) {
-      const int L = s - k - 1, b0 = k + 1;
+    // Packed lower storage.  Matvec by row groups of EIG_TPR threads: row part
+    // j <= i contiguous in the packed row, column part j > i read as column i of
+    // rows j (consecutive rows of a warp hit consecutive words).  The rank-2
+    // update touches the lower triangle only, each row group taking the row pair
+    // (g, L-1-g) for balance, and produces the next column (+ its norm): 2 barriers
+    // per Householder step.
+    double* vbuf0 = vv;
+    double* vbuf1 = ww;
+    {
       double sq = 0.0;
-      for (int i = tid; i < L; i += blockDim.x) {
-        const double x = A[pk(b0 + i, k)];
-        vv[i] = x;
+      for (int i = tid; i < s - 1; i += blockDim.x) {
+        const double x = A[pk(1 + i, 0)];
+        vbuf0[i] = x;
         sq = fma(x, x, sq);
       }
       sq = warp_sum(sq);
       if (lane == 0) red[wid] = sq;
-      __syncthreads();                                             // B1
-      const double nrm = sqrt(warp_sum_of(red, nw));
-      const double x0 = vv[0];
+    }
+    __syncthreads();
+    const int sub = tid & (EIG_TPR - 1);
+    const int grp = tid / EIG_TPR, ngrp = blockDim.x / EIG_TPR;
+    const int gpw = 32 / EIG_TPR;
+    for (int k = 0; k + 2 < s; ++k) {
+      const int L = s - k - 1, b0 = k + 1;
+      double* vc = (k & 1) ? vbuf1 : vbuf0;
+      double* vn = (k & 1) ? vbuf0 : vbuf1;
+      double* rc = (k & 1) ? red + 16 : red;
+      double* rn = (k & 1) ? red : red + 16;
+      const double nrm = sqrt(warp_sum_of(rc, nw));
+      const double x0 = vc[0];
       double alpha = 0.0, beta = 0.0;
       if (nrm > 0.0) {
         alpha = -copysign(nrm, x0);
         beta = 1.0 / (nrm * (nrm + fabs(x0)));
       }
       const double v0 = x0 - alpha;
+      // y = beta * A22 v
       double dotp = 0.0;
-      for (int i = wid; i < L; i += nw) {
-        const int gi = b0 + i;
-        const int rowbase = pk(gi, b0);
-        double acc = 0.0;
-        for (int j = lane; j < L; j += 32) {
-          const double a = (j <= i) ? A[rowbase + j] : A[pk(b0 + j, gi)];
-          acc = fma(a, j == 0 ? v0 : vv[j], acc);
+      for (int ib = wid * gpw; ib < L; ib += nw * gpw) {
+        const int i = ib + lane / EIG_TPR;
+        double a0 = 0.0, a1 = 0.0;
+        if (i < L) {
+          const int gi = b0 + i;
+          const double* __restrict__ row = A + pk(gi, b0);
+          int j = sub;
+          if (sub == 0) { a0 = row[0] * v0; j = EIG_TPR; }
+          for (; j <= i; j += EIG_TPR) a0 = fma(row[j], vc[j], a0);
+          // first column-part index >= i+1 with j = sub (mod EIG_TPR)
+          j = i + 1 + ((sub - (i + 1)) & (EIG_TPR - 1));
+          int cb = pk(b0 + j, gi);
+          for (; j < L; j += EIG_TPR) {
+            a1 = fma(A[cb], vc[j], a1);
+            cb += EIG_TPR * (b0 + j) + (EIG_TPR * (EIG_TPR + 1)) / 2;
+          }
         }
-        acc = warp_sum(acc) * beta;
-        if (lane == 0) yy[i] = acc;
-        dotp = fma(acc, i == 0 ? v0 : vv[i], dotp);
+        double acc = a0 + a1;
+#pragma unroll
+        for (int o = EIG_TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        acc *= beta;
+        if (i < L && sub == 0) {
+          yy[i] = acc;
+          dotp = fma(acc, i == 0 ? v0 : vc[i], dotp);
+        }
       }
+      dotp = warp_sum(dotp);
       if (lane == 0) red2[wid] = dotp;
-      __syncthreads();                                             // B2
+      __syncthreads();                                             // B1
       const double kk = 0.5 * beta * warp_sum_of(red2, nw);
-      for (int i = wid; i < L; i += nw) {
-        const double vi = i == 0 ? v0 : vv[i];
-        const double wi = yy[i] - kk * vi;
-        const int rowbase = pk(b0 + i, b0);
-        for (int j = lane; j <= i; j += 32) {
-          const double vj = j == 0 ? v0 : vv[j];
-          A[rowbase + j] -= vi * (yy[j] - kk * vj) + wi * vj;
+      const double w0 = yy[0] - kk * v0;
+      double sq = 0.0;
+      for (int g = grp; g < (L + 1) / 2; g += ngrp) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const int i = pass == 0 ? g : L - 1 - g;
+          if (pass == 1 && i == g) break;
+          const int gi = b0 + i;
+          const double vi = i == 0 ? v0 : vc[i];
+          const double wi = yy[i] - kk * vi;
+          double* __restrict__ row = A + pk(gi, b0);
+          int j = sub;
+          if (sub == 0) {
+            // column b0 (the next step's reflector input) first
+            const double nv = row[0] - (vi * w0 + wi * v0);
+            row[0] = nv;
+            if (i >= 1) {
+              vn[i - 1] = nv;
+              sq = fma(nv, nv, sq);
+            }
+            A[pk(gi, k)] = vi;   // reflector in place (column k left the active block)
+            j = EIG_TPR;
+          }
+          for (; j <= i; j += EIG_TPR) {
+            const double vj = vc[j];
+            row[j] -= vi * (yy[j] - kk * vj) + wi * vj;
+          }
         }
-        if (lane == 0) A[pk(b0 + i, k)] = vi;   // reflector in place (column k left the active block)
       }
+      sq = warp_sum(sq);
+      if (lane == 0) rn[wid] = sq;
       if (tid == 0) {
         dd[k] = A[pk(k, k)];
         ed[k] = alpha;
         bet[k] = beta;
       }
       hoff += L;
-      __syncthreads();                                             // B3
+      __syncthreads();                                             // B2
     }
   }
   if (tid == 0) {
