@@ -95,6 +95,7 @@ static int rbucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32; 
 struct Plan {
   Geom g;
   TileMap tm;
+  TileMap tm_gp;   // G pass: the core block's tiles (lanes over columns when possible)
   int dtype;
   int esize;
   int rmax, rb;
@@ -109,6 +110,7 @@ struct Plan {
   i64 w_tmp;         // doubles per W-chain temp buffer
   int hchunk, h_maxchunks;
   BPGeom bp;
+  BPGeom bp_gp;
   // workspace offsets (bytes)
   i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
   i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES],
@@ -203,61 +205,89 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   // tiles
   TileMap& tm = P.tm;
   tm.nblk = g.nblk;
-  // Block-pass tiles: whole columns, at most BP_X_BYTES of x per stage.  Lanes
+  // Block-pass tiles: whole columns, at most xb bytes of x per stage.  Lanes
   // over columns when >= 32 columns fit (32 * 2^k columns, <= 8 column groups),
-  // else lanes over rows with the column-range count that balances the 8 warps.
+  // else lanes over rows.  xb starts at BP_X_BYTES and shrinks until two stages
+  // (plus the staged A rows and the G pass's partials) leave two CTAs per SM.
   {
     i64 maxP = 1;
     for (int b = 0; b < g.nblk; ++b) maxP = std::max(maxP, g.blk[b].P);
     if (maxP > TILE_MAX_ELEMS) return fail(RT_ERR_UNSUPPORTED, "mode extent above 4096 not supported");
     BPGeom& G = P.bp;
-    G.rowmap_ints = (int)maxP;
-    G.gp_doubles = 0;
-    G.stages = 3;
-    G.x_bytes = BP_X_BYTES + 32;
-    int wmax = 2;
-    i64 amax = 0;
     tm.tile = TILE_MAX_ELEMS;
-    i64 t = 0;
-    for (int b = 0; b < g.nblk; ++b) {
-      tm.first[b] = t;
-      const i64 Pb = g.blk[b].P, nel = Pb * g.blk[b].Q;
-      const int rb = g.blk[b].r;
-      const i64 xcap = std::max<i64>(1, BP_X_BYTES / (Pb * P.esize));
-      const i64 wcap = std::max<i64>(1, (BP_W_DOUBLES - 4) / rb);
-      i64 cpt;
-      if (std::min(xcap, wcap) >= 32) {
-        cpt = 32;
-        while (cpt * 2 <= std::min<i64>(std::min(xcap, wcap), 256)) cpt *= 2;
-        tm.cols[b] = 1;
-        tm.ncr[b] = 1;
-      } else {
-        cpt = std::min(xcap, wcap);
-        tm.cols[b] = 0;
-        const i64 nrc = cdiv(Pb, 32);
-        double best = -1.0;
-        int bn = 1;
-        for (int ncr = 1; ncr <= std::min<i64>(cpt, 16); ++ncr) {
-          const double eff = (double)(nrc * cpt) / (double)(cdiv(nrc * ncr, 8) * 8 * cdiv(cpt, ncr));
-          if (eff > best + 1e-9) { best = eff; bn = ncr; }
+    for (i64 xb = BP_X_BYTES;; xb = std::max<i64>(maxP * P.esize, xb * 3 / 4)) {
+      G.rowmap_ints = (int)maxP;
+      G.gp_doubles = 0;
+      G.stages = 3;
+      i64 xmax = 16;   // largest tile's x bytes (the stage's x region)
+      int wmax = 2;
+      i64 amax = 0;
+      i64 t = 0;
+      for (int b = 0; b < g.nblk; ++b) {
+        tm.first[b] = t;
+        const i64 Pb = g.blk[b].P, nel = Pb * g.blk[b].Q;
+        const int rb = g.blk[b].r;
+        const i64 xcap = std::max<i64>(1, xb / (Pb * P.esize));
+        const i64 wcap = std::max<i64>(1, (BP_W_DOUBLES - 4) / rb);
+        i64 cpt;
+        if (std::min(xcap, wcap) >= 32) {
+          cpt = 32;
+          while (cpt * 2 <= std::min<i64>(std::min(xcap, wcap), 256)) cpt *= 2;
+          tm.cols[b] = 1;
+        } else {
+          cpt = std::min(xcap, wcap);
+          tm.cols[b] = 0;
         }
-        tm.ncr[b] = bn;
+        tm.ncr[b] = 1;
+        tm.te[b] = cpt * Pb;
+        tm.cpt[b] = (int)cpt;
+        xmax = std::max<i64>(xmax, cpt * Pb * P.esize);
+        if (tm.cols[b]) amax = std::max<i64>(amax, Pb * ((rb + 1) & ~1));
+        wmax = std::max(wmax, (int)(cpt * rb + 4));
+        t += cdiv(nel, tm.te[b]);
       }
-      tm.te[b] = cpt * Pb;
-      tm.cpt[b] = (int)cpt;
-      if (tm.cols[b]) amax = std::max<i64>(amax, Pb * ((rb + 1) & ~1));
-      wmax = std::max(wmax, (int)(cpt * rb + 4));
-      t += cdiv(nel, tm.te[b]);
+      tm.first[g.nblk] = t;
+      G.x_bytes = (int)(((xmax + 15) & ~15LL) + 32);
+      G.w_doubles = (wmax + 1) & ~1;
+      G.a_doubles = (int)((amax + 1) & ~1);
+      // three stages when two CTAs per SM still fit (with the G pass's partials), else two
+      BPGeom gg = G;
+      gg.gp_doubles = 256 * P.rmax;
+      if (bp_smem_bytes(gg) + 1024 > 113 * 1024) G.stages = 2;
+      gg.stages = G.stages;
+      if (bp_smem_bytes(gg) + 1024 <= 113 * 1024 || xb <= std::max<i64>(4096, maxP * P.esize)) break;
     }
-    G.w_doubles = (wmax + 1) & ~1;
-    G.a_doubles = (int)((amax + 1) & ~1);
-    // three stages when two CTAs per SM still fit (with the G pass's partials), else two
+    // G pass: its own map over the core block only, lanes over columns (32 * 2^k
+    // columns within BP_X_BYTES) with the staged A/U rows and partials; cols = 0
+    // when not even 32 columns fit (the warp-per-column k_gpass runs instead)
     {
-      BPGeom g3 = G;
-      g3.gp_doubles = 256 * P.rmax;
-      if (bp_smem_bytes(g3) + 1024 > 113 * 1024) G.stages = 2;
+      TileMap& tg = P.tm_gp;
+      tg = tm;
+      BPGeom& Gg = P.bp_gp;
+      const i64 Pc = g.blk[0].P;
+      const int rc = g.blk[0].r;
+      const i64 xcap = std::max<i64>(1, (i64)BP_X_BYTES / (Pc * P.esize));
+      const i64 wcap = std::max<i64>(1, (BP_W_DOUBLES - 4) / rc);
+      i64 cpt = std::min(xcap, wcap);
+      tg.cols[0] = cpt >= 32 ? 1 : 0;
+      if (tg.cols[0]) {
+        i64 c2 = 32;
+        while (c2 * 2 <= std::min<i64>(cpt, 256)) c2 *= 2;
+        cpt = c2;
+      }
+      tg.cpt[0] = (int)cpt;
+      tg.te[0] = cpt * Pc;
+      tg.first[0] = 0;
+      tg.first[1] = cdiv(Pc * g.blk[0].Q, tg.te[0]);
+      Gg.rowmap_ints = 16;
+      Gg.x_bytes = (int)(((cpt * Pc * P.esize + 15) & ~15LL) + 32);
+      Gg.w_doubles = (int)((cpt * rc + 4 + 1) & ~1);
+      Gg.a_doubles = (int)((Pc * ((rc + 1) & ~1) + 1) & ~1);
+      Gg.gp_doubles = 256 * rc;
+      Gg.stages = bp_smem_bytes(BPGeom{3, Gg.x_bytes, Gg.w_doubles, 16, Gg.gp_doubles, Gg.a_doubles}) + 1024 <= 113 * 1024
+                      ? 3
+                      : 2;
     }
-    tm.first[g.nblk] = t;
   }
 
   P.col_off[0] = 0;
@@ -294,7 +324,23 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     P.nb[m] = nb;
   }
   for (int b = 0; b < g.nblk; ++b) P.qmax = std::max(P.qmax, g.blk[b].Q);
-  P.a_chunk = APASS_CH;
+  // A pass: columns per CTA so that (row blocks x chunks x modes) fills ~4 waves of
+  // 148 SMs, in multiples of the 32-column shared-memory sub-chunk
+  {
+    i64 qmax = 1, rowblk = 0;
+    for (int m = 0; m < n; ++m) {
+      qmax = std::max<i64>(qmax, col_sizes[m]);
+      rowblk += cdiv(dims[m], 256);
+    }
+    // 32-column chunks unless the partial A rows would exceed 64 MB (then ~4 waves of CTAs)
+    i64 dsum = 0;
+    for (int m = 0; m < n; ++m) dsum += dims[m];
+    P.a_chunk = APASS_CH;
+    if (cdiv(qmax, APASS_CH) * dsum * rbucket(P.rmax) * 8 > ((i64)64 << 20)) {
+      const i64 target_chunks = std::max<i64>(1, cdiv(4 * 148, std::max<i64>(1, rowblk)));
+      P.a_chunk = (int)std::max<i64>(APASS_CH, cdiv(cdiv(qmax, target_chunks), APASS_CH) * APASS_CH);
+    }
+  }
   P.a_maxchunks = 1;
   for (int m = 0; m < n; ++m) P.a_maxchunks = std::max(P.a_maxchunks, (int)cdiv(col_sizes[m], P.a_chunk));
   P.hchunk = HG_CH;
@@ -363,7 +409,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_nonfinite = take(4);
   P.o_counters = take(64 * 4);
   P.o_absmax = take(8);
-  P.o_apart = take((i64)n * P.a_maxchunks * P.dmax * RT_MAX_RANK * 8);
+  P.o_apart = take((i64)n * P.a_maxchunks * P.dmax * P.rb * 8);   // partial A rows, pitch = rank bucket
   P.o_gt0 = take(P.g_tmp * 8);
   P.o_gt1 = take(P.g_tmp * 8);
   P.o_wt0 = take(P.w_tmp * 8);
@@ -952,10 +998,34 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   aa.part = e->at<double>(P.o_apart);
   aa.chunk = P.a_chunk;
   aa.maxchunks = P.a_maxchunks;
+  aa.pitch = P.rb;
   aa.dmax = P.dmax;
   aa.st_out = sto;
   prof_begin(e, PH_APASS);
-  DISPATCH_R(P.rb, k_apass, dim3((unsigned)cdiv(P.dmax, 256), P.a_maxchunks, n), 256, 0, e->st, g, ip, aa);
+  {
+    // exact-rank instance when every fiber mode shares the rank, else the rank bucket
+    {
+      int rm = g.rank[0];
+      for (int m = 1; m < n; ++m)
+        if (g.rank[m] != rm) rm = -1;
+      aa.mode_mask = ~0u;
+      const dim3 ag((unsigned)cdiv(P.dmax, 256), P.a_maxchunks, n);
+      switch (rm) {
+        case 1: k_apass<1><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 2: k_apass<2><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 3: k_apass<3><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 4: k_apass<4><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 5: k_apass<5><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 6: k_apass<6><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 8: k_apass<8><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 10: k_apass<10><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 12: k_apass<12><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        case 16: k_apass<16><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
+        default: DISPATCH_R(P.rb, k_apass, ag, 256, 0, e->st, g, ip, aa); break;
+      }
+      LAUNCH_CHECK();
+    }
+  }
   LAUNCH_CHECK();
   k_areduce<<<dim3((unsigned)std::min<i64>(cdiv(P.dmax * P.rmax * 32, 256), 2048), n), 256, 0, e->st>>>(g, aa);
   LAUNCH_CHECK();
@@ -984,16 +1054,15 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     pa.U = gp.U[0];
     pa.t1 = gp.t1;
     pa.nonfinite = e->at<int>(P.o_nonfinite);
-    BPGeom G = P.bp;
-    G.gp_doubles = 256 * g.rank[0];
+    const BPGeom& G = P.bp_gp;
     const i64 smb = bp_smem_bytes(G);
-    if (P.tm.cols[0]) {
+    if (P.tm_gp.cols[0]) {
       int lst;
 #define GP_LAUNCH(RB)                                                                                      \
-  (st_s ? launch_bp(k_block_pass<true, false, false, false, true, RB>, P.tm.first[1], smb, e->st, g, P.tm, ipg, \
-                    pa, G)                                                                                   \
-        : launch_bp(k_block_pass<false, false, false, false, true, RB>, P.tm.first[1], smb, e->st, g, P.tm, ipg, \
-                    pa, G))
+  (st_s ? launch_bp(k_block_pass<true, false, false, false, true, RB>, P.tm_gp.first[1], smb, e->st, g, P.tm_gp, \
+                    ipg, pa, G)                                                                              \
+        : launch_bp(k_block_pass<false, false, false, false, true, RB>, P.tm_gp.first[1], smb, e->st, g,       \
+                    P.tm_gp, ipg, pa, G))
       switch (rbucket(g.rank[0])) {
         case 4: lst = GP_LAUNCH(4); break;
         case 8: lst = GP_LAUNCH(8); break;
