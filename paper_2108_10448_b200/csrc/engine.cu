@@ -59,12 +59,17 @@ static inline i64 cdiv(i64 a, i64 b) { return (a + b - 1) / b; }
 static inline i64 align256(i64 x) { return (x + 255) & ~(i64)255; }
 
 // full-storage tridiagonalisation when it fits (faster), else packed
-static int eig_pick_full(int s, int r) { return eig_smem_doubles(s, r, 1, 1) <= EIG_SMEM_DOUBLES ? 1 : 0; }
+static int eig_pick_full(int s, int r) { return eig_smem_doubles(s, r, 1, 1, 1) <= EIG_SMEM_DOUBLES ? 1 : 0; }
 static int eig_pick_nb(int s, int r) {
+  // inverse-iteration block: the largest that still leaves room for the warm
+  // subspace-iteration scratch (fast path); without it only if nothing fits
   const int full = eig_pick_full(s, r);
   int nb = 0;
   for (int b = 1; b <= r; ++b)
-    if (eig_smem_doubles(s, r, b, full) <= EIG_SMEM_DOUBLES) nb = b;
+    if (eig_smem_doubles(s, r, b, full, 1) <= EIG_SMEM_DOUBLES) nb = b;
+  if (nb == 0)
+    for (int b = 1; b <= r; ++b)
+      if (eig_smem_doubles(s, r, b, full) <= EIG_SMEM_DOUBLES) nb = b;
   return nb;
 }
 

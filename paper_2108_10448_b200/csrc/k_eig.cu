@@ -49,12 +49,17 @@ struct EigArgs {
 
 __host__ __device__ inline int eig_ld(int s) { return s | 1; }
 
-// doubles of shared memory k_eig needs for (s, r, nb, layout)
-// sub: reserve the subspace-iteration scratch (Y: s x r, three r x r) after the LU area
+// doubles of shared memory k_eig needs for (s, r, nb, layout).  The full solver's
+// tail arrays (T's diagonals, reflector scratch, inverse-iteration LU) are idle
+// during the warm subspace iteration, so its scratch (Y: s x r, three r x r)
+// aliases them and only the excess (sub) is extra.
+__host__ __device__ inline long long eig_tail_doubles(int s, int nb) {
+  return 8LL * s + 8 + (long long)nb * 4 * s + ((long long)nb * s + 7) / 8 + 8;
+}
 __host__ __device__ inline long long eig_smem_doubles(int s, int r, int nb, int full, int sub = 0) {
   const long long amat = full ? (long long)s * eig_ld(s) + (long long)s * (s - 1) / 2 : (long long)s * (s + 1) / 2;
-  return amat + (long long)s * r + 8LL * s + 8 + 2LL * r + 96 + (long long)nb * 4 * s + ((long long)nb * s + 7) / 8 +
-         8 + (sub ? (long long)s * r + 3LL * r * r : 0);
+  const long long need = (long long)s * r + 3LL * r * r, tail = eig_tail_doubles(s, nb);
+  return amat + (long long)s * r + 2LL * r + 96 + tail + (sub && need > tail ? need - tail : 0);
 }
 
 __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // i >= j
@@ -337,7 +342,12 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
   double* A = eig_smem;                                            // matrix
   double* HV = full ? A + s * ld : A;                              // reflectors (full: contiguous)
   double* E = full ? HV + s * (s - 1) / 2 : A + npk;               // s x r eigenvector block
-  double* dd = E + s * r;                                          // diagonal of T
+  double* lam = E + s * r;                                         // r eigenvalues
+  int* clus = reinterpret_cast<int*>(lam + r);                     // r cluster starts (as doubles)
+  double* red = lam + 2 * r;                                       // 32
+  double* red2 = red + 32;                                         // 32
+  double* scal = red2 + 32;                                        // 32
+  double* dd = scal + 32;                                          // diagonal of T (tail starts here)
   double* ed = dd + s;                                             // off-diagonal of T
   double* dn = ed + s;                                             // normalised diagonal
   double* e2n = dn + (s + 4);                                      // normalised off-diagonal^2
@@ -345,14 +355,9 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
   double* vv = bet + s;                                            // current reflector
   double* yy = vv + s;                                             // symv result
   double* ww = yy + s;                                             // (spare)
-  double* lam = ww + s;                                            // r eigenvalues
-  int* clus = reinterpret_cast<int*>(lam + r);                     // r cluster starts (as doubles)
-  double* red = lam + 2 * r;                                       // 32
-  double* red2 = red + 32;                                         // 32
-  double* scal = red2 + 32;                                        // 32
-  double* lu = scal + 32;                                          // nb * 4s
+  double* lu = ww + s;                                             // nb * 4s
   unsigned char* piv = reinterpret_cast<unsigned char*>(lu + (size_t)nb * 4 * s);
-  double* Ysub = lu + (size_t)nb * 4 * s + ((size_t)nb * s + 7) / 8 + 8;   // s x r (subspace iteration)
+  double* Ysub = dd;                                               // s x r (subspace iteration, aliases the tail)
   double* Hs = Ysub + s * r;                                       // r x r
   double* Cs = Hs + r * r;                                         // r x r
   double* Rs = Cs + r * r;                                         // r x r
