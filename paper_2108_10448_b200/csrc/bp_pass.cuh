@@ -196,6 +196,93 @@ __device__ __forceinline__ void bp_rows(const BPTile& T, double& e2, double& x2,
   }
 }
 
+// A pass: A_new[p, :] += sum_q clean(p, q) V[q, :] over the tile's columns.
+// Warp w owns the 32-row chunks rc = w (mod warps), the same rows in every tile,
+// so the per-block shared accumulator acc[p * r + a] has a single writer per row.
+template <int R, bool EX, int DT, bool HS>
+__device__ __forceinline__ void bp_apass(const BPTile& T, double* __restrict__ acc) {
+  const int r = EX ? R : T.r;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int P = T.P, ncols = T.ncols;
+  const int nrc = (P + 31) >> 5;
+#pragma unroll 1
+  for (int rc = w; rc < nrc; rc += nw) {
+    const int p = rc * 32 + lane;
+    if (p >= P) continue;
+    double as[R], ar[R];
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk) {
+      as[kk] = (HS && (EX || kk < r)) ? __ldg(T.As + p + (i64)kk * T.d) : 0.0;
+      ar[kk] = 0.0;
+    }
+    // two columns per step: independent threshold chains (each in the threshold
+    // pass's kk order, so the clean values are bit-identical to it)
+    int q = 0;
+#pragma unroll 1
+    for (; q + 1 < ncols; q += 2) {
+      const double x0 = bp_xt<DT>(T.x, q * P + p), x1 = bp_xt<DT>(T.x, (q + 1) * P + p);
+      const double* w0 = T.Wss + q * r;
+      const double* v0 = T.Wes + q * r;   // V rows are staged in the second W slot
+      double l0 = 0.0, l1 = 0.0;
+      if (HS) {
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk)
+          if (EX || kk < r) {
+            l0 = fma(as[kk], w0[kk], l0);
+            l1 = fma(as[kk], w0[r + kk], l1);
+          }
+      }
+      const double c0 = x0 - hard_thr(x0 - l0, T.zeta), c1 = x1 - hard_thr(x1 - l1, T.zeta);
+#pragma unroll
+      for (int kk = 0; kk < R; ++kk)
+        if (EX || kk < r) ar[kk] = fma(c1, v0[r + kk], fma(c0, v0[kk], ar[kk]));
+    }
+    if (q < ncols) {
+      const double x = bp_xt<DT>(T.x, q * P + p);
+      const double* wsr = T.Wss + q * r;
+      const double* vr = T.Wes + q * r;
+      double ls = 0.0;
+      if (HS) {
+#pragma unroll
+        for (int kk = 0; kk < R; ++kk)
+          if (EX || kk < r) ls = fma(as[kk], wsr[kk], ls);
+      }
+      const double c = x - hard_thr(x - ls, T.zeta);
+#pragma unroll
+      for (int kk = 0; kk < R; ++kk)
+        if (EX || kk < r) ar[kk] = fma(c, vr[kk], ar[kk]);
+    }
+    double* ap = acc + (i64)p * r;
+#pragma unroll
+    for (int kk = 0; kk < R; ++kk)
+      if (EX || kk < r) ap[kk] += ar[kk];
+  }
+}
+
+template <int RR, int RB, bool HS>
+__device__ __forceinline__ bool bp_try_ap(const BPTile& T, double* acc) {
+  if (RR > RB || 2 * RR <= RB || T.r != RR) return false;
+  constexpr int R = RR <= RB ? RR : RB;
+  if (T.dtype == 0) bp_apass<R, true, 0, HS>(T, acc);
+  else bp_apass<R, true, 1, HS>(T, acc);
+  return true;
+}
+
+template <int RB, bool HS>
+__device__ __forceinline__ void bp_tile_ap(const BPTile& T, double* acc) {
+  if (bp_try_ap<1, RB, HS>(T, acc)) return;
+  if (bp_try_ap<2, RB, HS>(T, acc)) return;
+  if (bp_try_ap<3, RB, HS>(T, acc)) return;
+  if (bp_try_ap<4, RB, HS>(T, acc)) return;
+  if (bp_try_ap<5, RB, HS>(T, acc)) return;
+  if (bp_try_ap<6, RB, HS>(T, acc)) return;
+  if (bp_try_ap<8, RB, HS>(T, acc)) return;
+  if (bp_try_ap<10, RB, HS>(T, acc)) return;
+  if (bp_try_ap<16, RB, HS>(T, acc)) return;
+  if (T.dtype == 0) bp_apass<RB, false, 0, HS>(T, acc);
+  else bp_apass<RB, false, 1, HS>(T, acc);
+}
+
 template <int RR, int RB, bool HS, bool HE, bool WM, bool EXP, bool GP>
 __device__ __forceinline__ bool bp_try(const BPTile& T, bool cols, double& e2, double& x2, bool& bad) {
   if (RR > RB || 2 * RR <= RB || T.r != RR) return false;   // exact ranks in (RB/2, RB]
@@ -241,14 +328,16 @@ __device__ __forceinline__ void bp_tile_r(const BPTile& T, bool cols, double& e2
 // blocks, lanes over rows for tall ones.  Per-(CTA, block) partial sums are
 // combined by the last CTA in CTA order (deterministic: the tile -> CTA
 // assignment is static).  GP: the G pass over the core block's tiles only.
-template <bool HS, bool HE, bool WM, bool EXP, bool GP, int RB>
-__global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeom G) {
+template <bool HS, bool HE, bool WM, bool EXP, bool GP, int RB, bool AP>
+__global__ void __launch_bounds__(512, 1) k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeom G) {
   extern __shared__ __align__(128) unsigned char bp_smem[];
   __shared__ unsigned long long bars[4];
-  __shared__ double red[8];
+  __shared__ double red[16];
   __shared__ bool am_last;
   const int tid = threadIdx.x;
-  const i64 ntiles = GP ? tm.first[1] : tm.first[tm.nblk];
+  // GP: the core's tiles; AP: the fiber blocks' tiles; else every tile
+  const i64 tfirst = AP ? tm.first[1] : 0;
+  const i64 ntiles = (GP ? tm.first[1] : tm.first[tm.nblk]) - tfirst;
   const int esz = a.dtype == 0 ? 8 : 4;
   int* rmap = reinterpret_cast<int*>(bp_smem);
   double* gp = reinterpret_cast<double*>(bp_smem + (((size_t)G.rowmap_ints * 4 + 15) & ~(size_t)15));
@@ -282,15 +371,21 @@ __global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, Index
     unsigned total = (unsigned)(x1 - x0);
     if (HS) total += (unsigned)(w1 - w0);
     if (HE) total += (unsigned)(w1 - w0);
+    if (AP) total += (unsigned)((((q1 * bd.r) * 8 + 15) & ~(i64)15) - (((q0 * bd.r) * 8) & ~(i64)15));
     mbar_expect_tx(&bars[st], total);
     tma_load_1d(sb, xbase + x0, (unsigned)(x1 - x0), &bars[st]);
     if (HS) tma_load_1d(sb + G.x_bytes, reinterpret_cast<const char*>(a.st_s) + w0, (unsigned)(w1 - w0), &bars[st]);
     if (HE)
       tma_load_1d(sb + G.x_bytes + (size_t)G.w_doubles * 8, reinterpret_cast<const char*>(a.st_e) + w0,
                   (unsigned)(w1 - w0), &bars[st]);
+    if (AP) {   // the columns' V rows in the second W slot (same 16-byte phase as W: w_off is 32-aligned)
+      const i64 v0 = ((q0 * bd.r) * 8) & ~(i64)15, v1 = ((q1 * bd.r) * 8 + 15) & ~(i64)15;
+      tma_load_1d(sb + G.x_bytes + (size_t)G.w_doubles * 8, reinterpret_cast<const char*>(a.V[bd.mode]) + v0,
+                  (unsigned)(v1 - v0), &bars[st]);
+    }
   };
   // contiguous tile range per CTA: at most a couple of block switches
-  const i64 t_begin = ntiles * blockIdx.x / gridDim.x, t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const i64 t_begin = tfirst + ntiles * blockIdx.x / gridDim.x, t_end = tfirst + ntiles * (blockIdx.x + 1) / gridDim.x;
   const i64 my_n = t_end - t_begin;
   if (tid == 0)
     for (int st = 0; st < G.stages && st < my_n; ++st) issue(t_begin + st, st);
@@ -298,7 +393,18 @@ __global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, Index
   int cur_b = -1;
   double e2 = 0.0, x2 = 0.0;
   bool bad = false;
+  double* acc = gp;   // AP: the block's partial A rows (P x r), zeroed at every block switch
+  auto ap_flush = [&](int b) {
+    __syncthreads();
+    const i64 nout = g.blk[b].P * g.blk[b].r;
+    double* dst = a.apart + ap_slot(g, tm, (int)gridDim.x, b, blockIdx.x);
+    for (i64 o = tid; o < nout; o += blockDim.x) dst[o] = acc[o];
+  };
   auto flush = [&](int b) {
+    if (AP) {
+      ap_flush(b);
+      return;
+    }
     const double se = block_sum(e2, red);
     const double sx = block_sum(x2, red);
     if (tid == 0 && a.partial) {
@@ -325,7 +431,11 @@ __global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, Index
       cur_b = b;
       if (WM && !core)
         for (int pp = tid; pp < P; pp += blockDim.x) rmap[pp] = ip.rowpos[bd.mode][pp];
-      if (tm.cols[b]) {   // lanes over columns: the block's A rows, row-major with an even pitch
+      if (AP) {
+        __syncthreads();   // the previous block's flush has read acc
+        for (i64 o = tid; o < (i64)P * r; o += blockDim.x) acc[o] = 0.0;
+      }
+      if (tm.cols[b] && !AP) {   // lanes over columns: the block's A rows, row-major with an even pitch
         const int ap = (r + 1) & ~1;
         const i64 d = g.dim[bd.mode];
         for (int e = tid; e < P * ap; e += blockDim.x) {
@@ -369,7 +479,8 @@ __global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, Index
     T.t1 = GP ? a.t1 + q0 * r : nullptr;
     T.gp = gp;
     mbar_wait(&bars[st], phase);
-    if (core) bp_tile_r<RB, HS, HE, false, EXP, GP>(T, tm.cols[b] != 0, e2, x2, bad);
+    if (AP) bp_tile_ap<RB, HS>(T, acc);
+    else if (core) bp_tile_r<RB, HS, HE, false, EXP, GP>(T, tm.cols[b] != 0, e2, x2, bad);
     else bp_tile_r<RB, HS, HE, WM, EXP, false>(T, tm.cols[b] != 0, e2, x2, bad);
     __syncthreads();   // stage st fully consumed
     if (tid == 0 && i + G.stages < my_n) issue(t_begin + i + G.stages, st);
@@ -379,6 +490,7 @@ __global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, Index
     }
   }
   if (cur_b >= 0) flush(cur_b);
+  if (AP) return;
   if (bad) atomicExch(a.nonfinite, 1);
   if (a.partial == nullptr) return;
   if (tid == 0) {
@@ -405,4 +517,5 @@ __global__ void __launch_bounds__(256, 2) k_block_pass(Geom g, TileMap tm, Index
   }
   if (tid == 0) *a.counter = 0u;
 }
+
 

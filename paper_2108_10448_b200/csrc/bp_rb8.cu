@@ -1,13 +1,15 @@
 // Block-pass instantiations for rank bucket 8 (see bp_pass.cuh).
 #include "bp_pass.cuh"
 
-template __global__ void k_block_pass<true, true, false, true, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<true, false, false, true, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<false, true, false, true, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<false, false, false, true, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<true, false, true, false, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<false, false, true, false, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<true, true, false, false, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<false, true, false, false, false, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<true, false, false, false, true, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
-template __global__ void k_block_pass<false, false, false, false, true, 8>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<true, true, false, true, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<true, false, false, true, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<false, true, false, true, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<false, false, false, true, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<true, false, true, false, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<false, false, true, false, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<true, true, false, false, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<false, true, false, false, false, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<true, false, false, false, true, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<false, false, false, false, true, 8, false>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<true, false, false, false, false, 8, true>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);
+template __global__ void k_block_pass<false, false, false, false, false, 8, true>(Geom, TileMap, IndexPtrs, PassArgs, BPGeom);

@@ -59,7 +59,31 @@ struct PassArgs {
   unsigned int* counter;   // last-CTA ticket
   int* nonfinite;          // set if a clean intersection entry is not finite
   int want_x2;
+  // A pass (AP): per fiber mode k the V_k rows (|J_k| x r row-major) and the
+  // per-(block, CTA) partial A rows, reduced by k_areduce_bp
+  const double* V[RT_MAX_MODES];
+  const double* siginv[RT_MAX_MODES];
+  double* apart;
+  int ap_grid;             // CTAs of the A-pass launch (partial slot layout)
 };
+
+// A pass: CTA owning tile t (relative to the fiber tiles) in a persistent launch of
+// G CTAs over N tiles, where CTA c covers [N c / G, N (c + 1) / G)
+__host__ __device__ inline long long ap_cta_of(long long t, long long N, long long G) {
+  return ((t + 1) * G + N - 1) / N - 1;
+}
+// partial slot of (block b, CTA c): base_b + (c - first CTA of b) * P_b * r_b doubles
+__host__ __device__ inline long long ap_slot(const Geom& g, const TileMap& tm, int G, int b, long long c) {
+  const long long N = tm.first[tm.nblk] - tm.first[1];
+  long long base = 0;
+  for (int bb = 1; bb < b; ++bb) {
+    const long long c0 = ap_cta_of(tm.first[bb] - tm.first[1], N, G);
+    const long long c1 = ap_cta_of(tm.first[bb + 1] - 1 - tm.first[1], N, G);
+    base += (c1 - c0 + 1) * g.blk[bb].P * g.blk[bb].r;
+  }
+  const long long cb = ap_cta_of(tm.first[b] - tm.first[1], N, G);
+  return base + (c - cb) * g.blk[b].P * g.blk[b].r;
+}
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }

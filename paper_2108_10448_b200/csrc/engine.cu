@@ -7,7 +7,7 @@
 //   2. k_gram_*      K_i = B_i B_i^T  (short side of each intersection)
 //   3. k_eig         top-r_i eigenbasis of K_i
 //   4. k_zproj .. k_complete   rank-r_i truncated SVD (U, sigma, V), pinv cutoff
-//   5. k_apass/k_areduce       A_i = C_i V_i S_i^+
+//   5. A pass (k_block_pass AP) + k_areduce_bp   A_i = C_i V_i S_i^+
 //   6. k_gpass/k_modeprod      G = core x_i U_i^T
 //   7. k_wcols                 W_b per block column (Tucker evaluation weights)
 //   8. k_block_pass  e-sums of X - L_k - S_k and X sums (sampled error)
@@ -109,19 +109,21 @@ struct Plan {
   int nb[RT_MAX_MODES];
   i64 col_off[RT_MAX_BLOCKS + 1];
   int gram_maxchunks, gram_maxpairs, gram_cl;
-  int a_chunk, a_maxchunks;
   i64 dmax, lmax, smax, qmax;
   i64 g_tmp;         // doubles per G temp buffer
   i64 w_tmp;         // doubles per W-chain temp buffer
   int hchunk, h_maxchunks;
   BPGeom bp;
   BPGeom bp_gp;
+  BPGeom bp_ap;    // A pass: the pass tiles' stages + a per-block P x r accumulator
+  int ap_grid, ap_threads;
+  i64 o_apart2;
   // workspace offsets (bytes)
   i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
   i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES],
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
-      o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_apart, o_gt0, o_gt1, o_bpart, o_sums,
+      o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_gt0, o_gt1, o_bpart, o_sums,
       o_fpart, o_dbg, o_fast, o_wt0, o_wt1;
   i64 total;
 };
@@ -293,6 +295,21 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
                       ? 3
                       : 2;
     }
+    // A pass over the fiber tiles of the pass map
+    {
+      BPGeom& Ga = P.bp_ap;
+      Ga = G;
+      Ga.a_doubles = 0;
+      Ga.gp_doubles = 2;
+      for (int b = 1; b < g.nblk; ++b) Ga.gp_doubles = (int)std::max<i64>(Ga.gp_doubles, g.blk[b].P * g.blk[b].r);
+      Ga.gp_doubles = (Ga.gp_doubles + 1) & ~1;
+      Ga.stages = 3;
+      if (bp_smem_bytes(Ga) + 1024 > 113 * 1024) Ga.stages = 2;
+      const i64 nt = tm.first[g.nblk] - tm.first[1];
+      // two 256-thread CTAs per SM when they fit, else one 512-thread CTA (16 warps either way)
+      P.ap_threads = bp_smem_bytes(Ga) + 1024 <= 113 * 1024 ? 256 : 512;
+      P.ap_grid = (int)std::max<i64>(1, std::min<i64>(P.ap_threads == 256 ? 296 : 148, nt));
+    }
   }
 
   P.col_off[0] = 0;
@@ -329,25 +346,6 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     P.nb[m] = nb;
   }
   for (int b = 0; b < g.nblk; ++b) P.qmax = std::max(P.qmax, g.blk[b].Q);
-  // A pass: columns per CTA so that (row blocks x chunks x modes) fills ~4 waves of
-  // 148 SMs, in multiples of the 32-column shared-memory sub-chunk
-  {
-    i64 qmax = 1, rowblk = 0;
-    for (int m = 0; m < n; ++m) {
-      qmax = std::max<i64>(qmax, col_sizes[m]);
-      rowblk += cdiv(dims[m], 256);
-    }
-    // 32-column chunks unless the partial A rows would exceed 64 MB (then ~4 waves of CTAs)
-    i64 dsum = 0;
-    for (int m = 0; m < n; ++m) dsum += dims[m];
-    P.a_chunk = APASS_CH;
-    if (cdiv(qmax, APASS_CH) * dsum * rbucket(P.rmax) * 8 > ((i64)64 << 20)) {
-      const i64 target_chunks = std::max<i64>(1, cdiv(4 * 148, std::max<i64>(1, rowblk)));
-      P.a_chunk = (int)std::max<i64>(APASS_CH, cdiv(cdiv(qmax, target_chunks), APASS_CH) * APASS_CH);
-    }
-  }
-  P.a_maxchunks = 1;
-  for (int m = 0; m < n; ++m) P.a_maxchunks = std::max(P.a_maxchunks, (int)cdiv(col_sizes[m], P.a_chunk));
   P.hchunk = HG_CH;
   P.h_maxchunks = (int)cdiv(P.lmax, P.hchunk);
   // G temporaries: largest partially contracted core
@@ -414,7 +412,13 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_nonfinite = take(4);
   P.o_counters = take(64 * 4);
   P.o_absmax = take(8);
-  P.o_apart = take((i64)n * P.a_maxchunks * P.dmax * P.rb * 8);   // partial A rows, pitch = rank bucket
+  {
+    // A-pass partials: one P_b x r_b slot per (fiber block, CTA that touches it)
+    const i64 last = ap_slot(P.g, P.tm, P.ap_grid, P.g.nblk - 1,
+                             ap_cta_of(P.tm.first[P.g.nblk] - 1 - P.tm.first[1], P.tm.first[P.g.nblk] - P.tm.first[1],
+                                       P.ap_grid));
+    P.o_apart2 = take((last + P.g.blk[P.g.nblk - 1].P * P.g.blk[P.g.nblk - 1].r) * 8);
+  }
   P.o_gt0 = take(P.g_tmp * 8);
   P.o_gt1 = take(P.g_tmp * 8);
   P.o_wt0 = take(P.w_tmp * 8);
@@ -518,16 +522,18 @@ static int set_smem_limits_once() {
   SMEM_ATTR(k_wcols<4>); SMEM_ATTR(k_wcols<8>); SMEM_ATTR(k_wcols<16>); SMEM_ATTR(k_wcols<32>);
   SMEM_ATTR(k_zproj<4>); SMEM_ATTR(k_zproj<8>); SMEM_ATTR(k_zproj<16>); SMEM_ATTR(k_zproj<32>);
 #define BP_ATTRS(RB)                                                                                     \
-  SMEM_ATTR((k_block_pass<true, true, false, true, false, RB>));                                         \
-  SMEM_ATTR((k_block_pass<true, false, false, true, false, RB>));                                        \
-  SMEM_ATTR((k_block_pass<false, true, false, true, false, RB>));                                        \
-  SMEM_ATTR((k_block_pass<false, false, false, true, false, RB>));                                       \
-  SMEM_ATTR((k_block_pass<true, false, true, false, false, RB>));                                        \
-  SMEM_ATTR((k_block_pass<false, false, true, false, false, RB>));                                       \
-  SMEM_ATTR((k_block_pass<true, true, false, false, false, RB>));                                        \
-  SMEM_ATTR((k_block_pass<false, true, false, false, false, RB>));                                       \
-  SMEM_ATTR((k_block_pass<true, false, false, false, true, RB>));                                        \
-  SMEM_ATTR((k_block_pass<false, false, false, false, true, RB>))
+  SMEM_ATTR((k_block_pass<true, true, false, true, false, RB, false>));                                  \
+  SMEM_ATTR((k_block_pass<true, false, false, true, false, RB, false>));                                 \
+  SMEM_ATTR((k_block_pass<false, true, false, true, false, RB, false>));                                 \
+  SMEM_ATTR((k_block_pass<false, false, false, true, false, RB, false>));                                \
+  SMEM_ATTR((k_block_pass<true, false, true, false, false, RB, false>));                                 \
+  SMEM_ATTR((k_block_pass<false, false, true, false, false, RB, false>));                                \
+  SMEM_ATTR((k_block_pass<true, true, false, false, false, RB, false>));                                 \
+  SMEM_ATTR((k_block_pass<false, true, false, false, false, RB, false>));                                \
+  SMEM_ATTR((k_block_pass<true, false, false, false, true, RB, false>));                                 \
+  SMEM_ATTR((k_block_pass<false, false, false, false, true, RB, false>));                                \
+  SMEM_ATTR((k_block_pass<true, false, false, false, false, RB, true>));                                 \
+  SMEM_ATTR((k_block_pass<false, false, false, false, false, RB, true>))
   BP_ATTRS(4); BP_ATTRS(8); BP_ATTRS(16); BP_ATTRS(32);
 #undef BP_ATTRS
   SMEM_ATTR(k_hgram);
@@ -760,6 +766,15 @@ static int launch_bp(K kern, i64 ntiles, i64 smb, cudaStream_t st, const Geom& g
   return RT_OK;
 }
 
+// A pass: fixed grid (the partial-slot layout depends on it)
+template <typename K>
+static int launch_ap(K kern, int grid, int threads, i64 smb, cudaStream_t st, const Geom& g, const TileMap& tm,
+                     const IndexPtrs& ip, const PassArgs& a, const BPGeom& G) {
+  kern<<<grid, threads, smb, st>>>(g, tm, ip, a, G);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
 static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_e, double zeta, bool with_M,
                           double* s_out, double* c_out, double* l_out, bool sums, int phase) {
   const Plan& P = e->P;
@@ -786,13 +801,13 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   const i64 smb = bp_smem_bytes(P.bp);
   const bool hs = st_s != nullptr, he = st_e != nullptr;
 #define BP_LAUNCH(HS, HE, WM, EXP)                                                                        \
-  (P.rb == 4    ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 4>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
+  (P.rb == 4    ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 4, false>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
                             ip, a, P.bp)                                                                          \
-   : P.rb == 8  ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 8>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
+   : P.rb == 8  ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 8, false>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
                             ip, a, P.bp)                                                                          \
-   : P.rb == 16 ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 16>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
+   : P.rb == 16 ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 16, false>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
                             P.tm, ip, a, P.bp)                                                                    \
-                : launch_bp(k_block_pass<HS, HE, WM, EXP, false, 32>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
+                : launch_bp(k_block_pass<HS, HE, WM, EXP, false, 32, false>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
                             P.tm, ip, a, P.bp))
   int lst;
   if (s_out || c_out || l_out) {
@@ -990,50 +1005,42 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   const int n = g.n;
   IndexPtrs ip = make_ip(e);
   double* sto = e->state(dst);
-  APassArgs aa;
-  memset(&aa, 0, sizeof(aa));
-  aa.xb = e->ws + P.o_xb;
-  aa.dtype = P.dtype;
-  aa.st_s = st_s;
-  aa.zeta = zeta;
-  for (int m = 0; m < n; ++m) {
-    aa.V[m] = e->at<double>(P.o_V[m]);
-    aa.siginv[m] = e->at<double>(P.o_siginv[m]);
-  }
-  aa.part = e->at<double>(P.o_apart);
-  aa.chunk = P.a_chunk;
-  aa.maxchunks = P.a_maxchunks;
-  aa.pitch = P.rb;
-  aa.dmax = P.dmax;
-  aa.st_out = sto;
   prof_begin(e, PH_APASS);
   {
-    // exact-rank instance when every fiber mode shares the rank, else the rank bucket
-    {
-      int rm = g.rank[0];
-      for (int m = 1; m < n; ++m)
-        if (g.rank[m] != rm) rm = -1;
-      aa.mode_mask = ~0u;
-      const dim3 ag((unsigned)cdiv(P.dmax, 256), P.a_maxchunks, n);
-      switch (rm) {
-        case 1: k_apass<1><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 2: k_apass<2><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 3: k_apass<3><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 4: k_apass<4><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 5: k_apass<5><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 6: k_apass<6><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 8: k_apass<8><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 10: k_apass<10><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 12: k_apass<12><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        case 16: k_apass<16><<<ag, 256, 0, e->st>>>(g, ip, aa); break;
-        default: DISPATCH_R(P.rb, k_apass, ag, 256, 0, e->st, g, ip, aa); break;
-      }
-      LAUNCH_CHECK();
+    // A_k = C_k V_k S_k^+ on the block-pass tiles (fiber blocks), then the fixed-order reduction
+    PassArgs pa;
+    memset(&pa, 0, sizeof(pa));
+    pa.xb = e->ws + P.o_xb;
+    pa.dtype = P.dtype;
+    pa.st_s = st_s;
+    pa.zeta = zeta;
+    for (int m = 0; m < n; ++m) {
+      pa.V[m] = e->at<double>(P.o_V[m]);
+      pa.siginv[m] = e->at<double>(P.o_siginv[m]);
     }
+    pa.apart = e->at<double>(P.o_apart2);
+    pa.ap_grid = P.ap_grid;
+    pa.nonfinite = e->at<int>(P.o_nonfinite);
+    const i64 smb = bp_smem_bytes(P.bp_ap);
+#define AP_LAUNCH(RB)                                                                                  \
+  (st_s ? launch_ap(k_block_pass<true, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, P.tm, ip, pa, \
+                    P.bp_ap)                                                                             \
+        : launch_ap(k_block_pass<false, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, P.tm, ip, pa, \
+                    P.bp_ap))
+    int lst;
+    switch (P.rb) {
+      case 4: lst = AP_LAUNCH(4); break;
+      case 8: lst = AP_LAUNCH(8); break;
+      case 16: lst = AP_LAUNCH(16); break;
+      default: lst = AP_LAUNCH(32); break;
+    }
+#undef AP_LAUNCH
+    if (lst) return lst;
+    i64 maxpr = 1;
+    for (int b = 1; b < g.nblk; ++b) maxpr = std::max<i64>(maxpr, g.blk[b].P * g.blk[b].r);
+    k_areduce_bp<<<dim3((unsigned)std::min<i64>(cdiv(maxpr, 256), 1024), g.nblk - 1), 256, 0, e->st>>>(g, P.tm, pa, sto);
+    LAUNCH_CHECK();
   }
-  LAUNCH_CHECK();
-  k_areduce<<<dim3((unsigned)std::min<i64>(cdiv(P.dmax * P.rmax * 32, 256), 2048), n), 256, 0, e->st>>>(g, aa);
-  LAUNCH_CHECK();
   prof_end(e, PH_APASS);
   prof_begin(e, PH_GPASS);
   // G = clean_core x_1 U_1^T x_2 ... x_n U_n^T
@@ -1064,9 +1071,9 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     if (P.tm_gp.cols[0]) {
       int lst;
 #define GP_LAUNCH(RB)                                                                                      \
-  (st_s ? launch_bp(k_block_pass<true, false, false, false, true, RB>, P.tm_gp.first[1], smb, e->st, g, P.tm_gp, \
+  (st_s ? launch_bp(k_block_pass<true, false, false, false, true, RB, false>, P.tm_gp.first[1], smb, e->st, g, P.tm_gp, \
                     ipg, pa, G)                                                                              \
-        : launch_bp(k_block_pass<false, false, false, false, true, RB>, P.tm_gp.first[1], smb, e->st, g,       \
+        : launch_bp(k_block_pass<false, false, false, false, true, RB, false>, P.tm_gp.first[1], smb, e->st, g,       \
                     P.tm_gp, ipg, pa, G))
       switch (rbucket(g.rank[0])) {
         case 4: lst = GP_LAUNCH(4); break;

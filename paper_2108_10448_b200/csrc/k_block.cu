@@ -119,8 +119,30 @@ __global__ void __launch_bounds__(256) k_gather(Geom g, TileMap tm, IndexPtrs ip
 }
 
 // K1 block pass (definition: bp_pass.cuh, instantiated in bp_rb*.cu)
-template <bool HS, bool HE, bool WM, bool EXP, bool GP, int RB>
+template <bool HS, bool HE, bool WM, bool EXP, bool GP, int RB, bool AP>
 __global__ void k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeom G);
+
+// A_k[p, a] = siginv_a * sum over the CTAs that touched block k+1 (CTA order) of the
+// A-pass partials.  One thread per output (consecutive outputs, consecutive partials).
+__global__ void __launch_bounds__(256) k_areduce_bp(Geom g, TileMap tm, PassArgs a, double* __restrict__ st_out) {
+  const int b = blockIdx.y + 1;
+  if (b >= g.nblk) return;
+  const BlockDesc& bd = g.blk[b];
+  const i64 N = tm.first[tm.nblk] - tm.first[1];
+  const i64 G = a.ap_grid;
+  const i64 c0 = ap_cta_of(tm.first[b] - tm.first[1], N, G), c1 = ap_cta_of(tm.first[b + 1] - 1 - tm.first[1], N, G);
+  const i64 base = ap_slot(g, tm, (int)G, b, c0);
+  const i64 nout = bd.P * bd.r, stride = nout;
+  double* A = st_out + g.a_off[bd.mode];
+  for (i64 o = blockIdx.x * (i64)blockDim.x + threadIdx.x; o < nout; o += (i64)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (i64 c = c0; c <= c1; ++c) s += a.apart[base + (c - c0) * stride + o];
+    const i64 p = o / bd.r;
+    const int aa = (int)(o - p * bd.r);
+    A[p + (i64)aa * bd.P] = s * a.siginv[bd.mode][aa];
+  }
+}
+
 
 // ------------------------------------------------------------------ K0 abs-max
 

@@ -5,7 +5,7 @@
 //                                      G   = core x_k U~_k^T     (r_1 x ... x r_n)
 //   so core x_k F_k == G x_k A_k exactly (mode product with a product matrix).
 //
-// k_apass/k_areduce build A_k from the clean fibers (recomputed on the fly as
+// The A pass (k_block_pass<..AP>, bp_pass.cuh) builds A_k from the clean fibers (recomputed on the fly as
 // x - HT(x - L_prev, zeta), bit-identical to the values the threshold pass
 // produced); k_gpass/k_modeprod build G from the clean core; k_wcols builds
 // the per-column weights W_b used by every block evaluation
@@ -13,104 +13,6 @@
 // (fiber_cur.py:288-326 evaluated in Tucker form, |J| r^n instead of |J| prod|I|).
 #include "common.cuh"
 
-struct APassArgs {
-  const void* xb;
-  int dtype;
-  const double* st_s;               // state that produced the threshold (null: L = 0)
-  double zeta;
-  const double* V[RT_MAX_MODES];    // |J_k| x r row-major
-  const double* siginv[RT_MAX_MODES];
-  double* part;                     // [mode][chunks][d_max][r_max]
-  int chunk;                        // columns per CTA (multiple of APASS_CH)
-  int maxchunks;
-  int pitch;                        // partial row pitch (the rank bucket)
-  unsigned mode_mask;               // modes this launch handles (bit k)
-  i64 dmax;
-  double* st_out;                   // new state (A_k written at g.a_off[k])
-};
-
-#define APASS_CH 32   // fiber columns per CTA (V and W rows staged in shared memory)
-
-template <int R>
-__global__ void __launch_bounds__(256) k_apass(Geom g, IndexPtrs ip, APassArgs a) {
-  __shared__ double vs[APASS_CH * R];
-  __shared__ double wsh[APASS_CH * R];
-  const int k = blockIdx.z;
-  if (k >= g.n || !((a.mode_mask >> k) & 1u)) return;
-  const BlockDesc& bd = g.blk[k + 1];
-  const int r = bd.r;   // == R for the exact-rank launches (no dead unrolled terms)
-  const i64 P = bd.P;
-  const i64 q0 = (i64)blockIdx.y * a.chunk;
-  if (q0 >= bd.Q) return;
-  if ((i64)blockIdx.x * blockDim.x >= P) return;
-  const int nq = (int)min((i64)a.chunk, bd.Q - q0);
-  const double* V = a.V[k];
-  const i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = p < P;
-  // this row's A_prev entries are shared by every column of the chunk
-  double arow[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) arow[i] = (live && a.st_s && i < r) ? a.st_s[g.a_off[k] + p + (i64)i * P] : 0.0;
-  double acc[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) acc[i] = 0.0;
-  for (int s0 = 0; s0 < nq; s0 += APASS_CH) {
-    const int ns = min(APASS_CH, nq - s0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < ns * r; i += blockDim.x) {
-      vs[i] = V[(q0 + s0) * r + i];
-      wsh[i] = a.st_s ? a.st_s[bd.w_off + (q0 + s0) * r + i] : 0.0;
-    }
-    __syncthreads();
-    if (!live) continue;
-    const i64 base = bd.off + (q0 + s0) * P + p;
-    for (int q = 0; q < ns; q += 4) {
-      double xv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = (q + u < ns) ? ld_elem(a.xb, base + (i64)(q + u) * P, a.dtype) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (q + u >= ns) break;
-        const double* wq = wsh + (q + u) * r;
-        const double* vq = vs + (q + u) * r;
-        double ls = 0.0;
-#pragma unroll
-        for (int i = 0; i < R; ++i)
-          if (i < r) ls = fma(arow[i], wq[i], ls);
-        const double c = xv[u] - hard_thr(xv[u] - ls, a.zeta);
-#pragma unroll
-        for (int i = 0; i < R; ++i)
-          if (i < r) acc[i] = fma(c, vq[i], acc[i]);
-      }
-    }
-  }
-  if (!live) return;
-  double* out = a.part + (((i64)k * a.maxchunks + blockIdx.y) * a.dmax + p) * a.pitch;
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (i < r) out[i] = acc[i];
-}
-
-// A_k[p, a] = siginv_a * sum over chunks (fixed warp-butterfly order) of the partials
-__global__ void __launch_bounds__(256) k_areduce(Geom g, APassArgs a) {
-  const int k = blockIdx.y;
-  if (k >= g.n) return;
-  const BlockDesc& bd = g.blk[k + 1];
-  const int r = bd.r;
-  const int nch = (int)((bd.Q + a.chunk - 1) / a.chunk);
-  double* A = a.st_out + g.a_off[k];
-  const int lane = threadIdx.x & 31;
-  const i64 nout = bd.P * r;
-  for (i64 o = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < nout; o += ((i64)gridDim.x * blockDim.x) >> 5) {
-    const i64 p = o % bd.P;
-    const int i = (int)(o / bd.P);
-    const double* src = a.part + ((i64)k * a.maxchunks * a.dmax + p) * a.pitch + i;
-    double acc = 0.0;
-    for (int c = lane; c < nch; c += 32) acc += src[(i64)c * a.dmax * a.pitch];
-    acc = warp_sum(acc);
-    if (lane == 0) A[p + (i64)i * bd.P] = acc * a.siginv[k][i];
-  }
-}
 
 // ------------------------------------------------------------------ G
 
@@ -305,10 +207,6 @@ __global__ void __launch_bounds__(128) k_wcols(Geom g, IndexPtrs ip, double* __r
     if (i < rt) out[i] = w[i];
 }
 
-template __global__ void k_apass<4>(Geom, IndexPtrs, APassArgs);
-template __global__ void k_apass<8>(Geom, IndexPtrs, APassArgs);
-template __global__ void k_apass<16>(Geom, IndexPtrs, APassArgs);
-template __global__ void k_apass<32>(Geom, IndexPtrs, APassArgs);
 template __global__ void k_gpass<4>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<8>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<16>(Geom, IndexPtrs, GPassArgs);
