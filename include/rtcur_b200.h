@@ -42,6 +42,9 @@ extern "C" {
 #define RTCUR_E_ARITH 3
 #define RTCUR_E_CUDA 4
 #define RTCUR_E_UNSUPPORTED 5
+#define RTCUR_E_FORMAT 6      /* malformed TNSR file (TensorFormatError) */
+#define RTCUR_E_NOTFOUND 7    /* missing file (FileNotFoundError) */
+#define RTCUR_E_IO 8          /* other file-system failure (OSError) */
 
 #define RTCUR_F64 0
 #define RTCUR_F32 1
@@ -126,6 +129,20 @@ int rtcur_engine_profile(rtcur_engine* e, int on);
  * overhead (two event records per timed phase launch) out of the other phases. */
 int rtcur_engine_profile_phases(rtcur_engine* e, uint32_t mask);
 int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* counts, int nphase, int reset);
+
+/* ---- TNSR v1 tensor files (reference tensorfile.py:1-115), streamed disk <-> HBM ----
+ * Layout: "TNSR" | u16 version 1 | u16 n | n x u64 extents | prod(extents) f8, mode-1 fastest.
+ * rtcur_tnsr_read_header: tensorfile._parse_header (:50-84), plus read_tensor's payload size
+ * check (:94-107) when check_payload; messages name the offending byte offset like the
+ * reference's TensorFormatError.  dims_cap >= n entries of dims are written.
+ * rtcur_tnsr_load: read_tensor (:94-115) into device memory: dtype 0 f64 / 1 f32 (rounded),
+ * only mode-1 rows [slab_lo, slab_hi) (slab_hi < 0: all) as a mode-1-fastest slab; the
+ * payload streams through pinned double buffers (pread threads || async H2D).  Synchronous.
+ * rtcur_tnsr_store: write_tensor (:42-48) from device memory (f64, or f32 widened exactly). */
+int rtcur_tnsr_read_header(const char* path, int check_payload, int32_t* version, int32_t* n, int64_t* dims,
+                           int dims_cap, int64_t* payload_offset);
+int rtcur_tnsr_load(const char* path, int64_t slab_lo, int64_t slab_hi, int dtype, void* dst, void* stream);
+int rtcur_tnsr_store(const char* path, int n, const int64_t* dims, int dtype, const void* src, void* stream);
 
 /* Synthetic instance support (bench/tests).  On a mode-1 slab [lo, hi) of a d1 x ... tensor:
  * L(i1, R) = sum_a Y1[i1, a] Tf[R, a] (Y1: d1 x r1 column-major, Tf: ncols x r1 row-major,

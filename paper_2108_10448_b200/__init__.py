@@ -13,10 +13,13 @@ from .full import cur_reconstruct_full, full_output
 from .solver import (DenseTensorAccessor, SolveResult, SolverConfig, SparseEstimate, TensorAccessor,
                      hard_threshold, rtcur, sampled_relative_error, zeta_schedule)
 from .tensor import DenseTensor, DeviceTensor
+from .tensorfile import (TensorFormatError, read_header, read_tensor, read_tensor_device, write_tensor,
+                         write_tensor_device)
 
 __all__ = [
     "rtcur", "SolverConfig", "SolveResult", "SparseEstimate", "TensorAccessor", "DenseTensorAccessor",
     "hard_threshold", "zeta_schedule", "sampled_relative_error", "FiberCur", "SampleIndices", "TruncatedSvd",
     "sample_sizes", "sample_indices", "draw_sample_indices", "DenseTensor", "DeviceTensor", "full_output",
-    "cur_reconstruct_full",
+    "cur_reconstruct_full", "TensorFormatError", "read_header", "read_tensor", "write_tensor", "read_tensor_device",
+    "write_tensor_device",
 ]

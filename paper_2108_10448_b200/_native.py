@@ -14,7 +14,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "librtcur_b200.so")
 
-RTCUR_OK, RTCUR_E_VALUE, RTCUR_E_INDEX, RTCUR_E_ARITH, RTCUR_E_CUDA, RTCUR_E_UNSUPPORTED = range(6)
+(RTCUR_OK, RTCUR_E_VALUE, RTCUR_E_INDEX, RTCUR_E_ARITH, RTCUR_E_CUDA, RTCUR_E_UNSUPPORTED, RTCUR_E_FORMAT,
+ RTCUR_E_NOTFOUND, RTCUR_E_IO) = range(9)
 RTCUR_F64, RTCUR_F32 = 0, 1
 
 # every symbol include/rtcur_b200.h declares
@@ -25,7 +26,7 @@ EXPORTED = (
     "rtcur_engine_iterate_async", "rtcur_engine_iterate_wait",
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
     "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_profile_read",
-    "rtcur_append_distinct", "rtcur_generate_tucker",
+    "rtcur_append_distinct", "rtcur_generate_tucker", "rtcur_tnsr_read_header", "rtcur_tnsr_load", "rtcur_tnsr_store",
 )
 PHASES = ("absmax", "prep", "gather", "threshold", "gram", "eig", "svdpost", "apass", "gpass", "wcols", "error",
           "export", "full")
@@ -85,6 +86,9 @@ def load(path: str = LIB_PATH):
     lib.rtcur_generate_tucker.argtypes = [c_vp, c_vp, c_i64, ctypes.c_int, c_i64, c_i64, c_i64, ctypes.c_int,
                                           ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_int, c_vp, c_vp,
                                           c_dp, c_vp]
+    lib.rtcur_tnsr_read_header.argtypes = [ctypes.c_char_p, ctypes.c_int, c_i32p, c_i32p, c_i64p, ctypes.c_int, c_i64p]
+    lib.rtcur_tnsr_load.argtypes = [ctypes.c_char_p, c_i64, c_i64, ctypes.c_int, c_vp, c_vp]
+    lib.rtcur_tnsr_store.argtypes = [ctypes.c_char_p, ctypes.c_int, c_i64p, ctypes.c_int, c_vp, c_vp]
     for name in EXPORTED:
         if not hasattr(lib, name):
             raise NativeUnavailable(f"{path} does not export {name}")
@@ -102,6 +106,14 @@ def check(status: int) -> None:
         raise IndexError(msg)
     if status == RTCUR_E_ARITH:
         raise ArithmeticError(msg)
+    if status == RTCUR_E_FORMAT:
+        from .tensorfile import TensorFormatError
+
+        raise TensorFormatError(msg)
+    if status == RTCUR_E_NOTFOUND:
+        raise FileNotFoundError(msg)
+    if status == RTCUR_E_IO:
+        raise OSError(msg)
     raise RuntimeError(f"rtcur_b200 status {status}: {msg}")
 
 

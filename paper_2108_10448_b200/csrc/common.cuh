@@ -22,6 +22,9 @@
 #define RT_ERR_ARITH 3      // ArithmeticError
 #define RT_ERR_CUDA 4       // RuntimeError (CUDA failure)
 #define RT_ERR_UNSUPPORTED 5
+#define RT_ERR_FORMAT 6     // TensorFormatError (ValueError subclass)
+#define RT_ERR_NOTFOUND 7   // FileNotFoundError
+#define RT_ERR_IO 8         // OSError
 
 typedef int64_t i64;
 

@@ -55,6 +55,8 @@ static int fail(int code, const std::string& msg) {
     if (_e != cudaSuccess) return fail(RT_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(_e) + " @" + std::to_string(__LINE__)); \
   } while (0)
 
+#include "tnsr_io.cu"   // after fail()/CK/LAUNCH_CHECK
+
 static inline i64 cdiv(i64 a, i64 b) { return (a + b - 1) / b; }
 static inline i64 align256(i64 x) { return (x + 255) & ~(i64)255; }
 
