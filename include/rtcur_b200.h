@@ -154,6 +154,16 @@ int rtcur_generate_tucker(const double* Y1, const double* Tf, int64_t d1, int r1
                           int64_t ncols, int mode, uint64_t seed, double alpha, double cmu, int dtype, void* X,
                           double* scratch, double* sum_abs, void* stream);
 
+/* Reference-generator outliers (synth.py:101-121, gen_outliers): for k < count,
+ * v_k = -mu + (2 mu) * u[k] (numpy Generator.uniform rounding), S[pos[k]] = v_k (S optional),
+ * X[pos[k]] += v_k.  X, S fp64 device arrays; pos (0-based, distinct), u device arrays drawn
+ * on the host from the reference's exact generator stream. */
+int rtcur_scatter_outliers(double* X, const int64_t* pos, const double* u, int64_t count, double mu, double* S,
+                           void* stream);
+/* sum |x| over n fp64 device values in a fixed order (host result in *out, synchronous);
+ * scratch: device, >= 600 doubles.  mu = mean |low| of gen_outliers (synth.py:91-98). */
+int rtcur_abs_sum(const double* x, int64_t n, double* scratch, double* out, void* stream);
+
 /* Host helper of the index sampler (fiber_cur.py:202-208): append the values of
  * batch not yet marked in seen (population bytes) to out, in first-occurrence
  * order; returns the new length (-1 if a value is out of range). */

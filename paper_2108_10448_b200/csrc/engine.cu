@@ -1338,6 +1338,60 @@ extern "C" int rtcur_generate_tucker(const double* Y1, const double* Tf, int64_t
   return RT_OK;
 }
 
+// sum |x| in a fixed order: per-CTA grid-stride partial sums, then one CTA adds the
+// partials in CTA order (deterministic run to run).
+__global__ void k_abs_sum_part(const double* __restrict__ x, i64 n, double* __restrict__ part) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < n; k += (i64)gridDim.x * blockDim.x) s += fabs(x[k]);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_abs_sum_final(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) s += part[k];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+extern "C" int rtcur_abs_sum(const double* x, int64_t n, double* scratch, double* out, void* stream) {
+  if (!x || !scratch || !out || n < 0) return fail(RT_ERR_VALUE, "bad abs-sum arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int np = 148 * 4;
+  k_abs_sum_part<<<np, 256, 0, st>>>(x, n, scratch);
+  LAUNCH_CHECK();
+  k_abs_sum_final<<<1, 256, 0, st>>>(scratch, np, scratch + np);
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(out, scratch + np, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RT_OK;
+}
+
+// Outliers of the reference generator (synth.py:101-121): value_k = low + (high - low) * u_k
+// with low = -mu, high = mu, rounded step by step like numpy's Generator.uniform (no FMA);
+// S[pos_k] = value_k and X[pos_k] += value_k (fp64, X holding L: x = low + sparse).
+__global__ void k_scatter_outliers(double* __restrict__ X, const int64_t* __restrict__ pos,
+                                   const double* __restrict__ u, i64 count, double mu, double* __restrict__ S) {
+  const double lo = -mu, span = __dadd_rn(mu, mu);
+  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < count; k += (i64)gridDim.x * blockDim.x) {
+    const double v = __dadd_rn(lo, __dmul_rn(span, u[k]));
+    const i64 p = pos[k];
+    X[p] = __dadd_rn(X[p], v);
+    if (S) S[p] = v;
+  }
+}
+
+extern "C" int rtcur_scatter_outliers(double* X, const int64_t* pos, const double* u, int64_t count, double mu,
+                                      double* S, void* stream) {
+  if (!X || count < 0 || (count > 0 && (!pos || !u))) return fail(RT_ERR_VALUE, "bad outlier arguments");
+  if (count == 0) return RT_OK;
+  k_scatter_outliers<<<(unsigned)std::min<i64>(cdiv(count, 256), 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+      X, pos, u, count, mu, S);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
 // ------------------------------------------------------------------ kernel-level plug
 
 extern "C" int rtcur_gather_columns(const void* flat, int dtype, int64_t flat_len, const int64_t* bases_dev,

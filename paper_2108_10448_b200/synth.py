@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import numpy as np
 
 __all__ = ["BaselineConfig", "CONFIGS", "make_gaussian_tucker", "make_video_like", "make_config",
-           "baseline_sample_sizes"]
+           "baseline_sample_sizes", "InstanceSpec", "gen_lowrank_device", "gen_outliers_device",
+           "make_instance_device", "make_gaussian_tucker_device", "make_config_device", "slab_bounds"]
 
 
 @dataclass(frozen=True)
@@ -218,3 +219,139 @@ def make_config_device(index: int, slab=None, group=None):
         return DeviceTensor(part.reshape(-1), (hi - lo,) + tuple(cfg.shape[1:])), cfg
     X, _ = make_gaussian_tucker_device(cfg.shape, cfg.ranks, cfg.alpha, cfg.c, cfg.seed_instance, dt, slab, group)
     return X, cfg
+
+
+# ----------------------------------------------------------------- reference generator semantics on the device
+
+
+@dataclass(frozen=True)
+class InstanceSpec:
+    """Mirror of the reference's InstanceSpec (synth.py:41-72): a d x ... x d tensor
+    of order n, multilinear rank (r, ..., r), outlier fraction alpha."""
+
+    n: int
+    d: int
+    r: int
+    alpha: float
+    seed: int
+
+    def __post_init__(self):
+        if int(self.n) < 1:
+            raise ValueError(f"order must be >= 1, got {self.n}")
+        if int(self.d) < 1:
+            raise ValueError(f"extent must be >= 1, got {self.d}")
+        if not 1 <= int(self.r) <= int(self.d):
+            raise ValueError(f"rank {self.r} outside [1, {self.d}]")
+        if not 0.0 <= float(self.alpha) < 1.0:
+            raise ValueError(f"outlier fraction must lie in [0, 1), got {self.alpha}")
+        object.__setattr__(self, "n", int(self.n))
+        object.__setattr__(self, "d", int(self.d))
+        object.__setattr__(self, "r", int(self.r))
+        object.__setattr__(self, "alpha", float(self.alpha))
+
+    @property
+    def shape(self) -> tuple:
+        return (self.d,) * self.n
+
+    @property
+    def ranks(self) -> tuple:
+        return (self.r,) * self.n
+
+
+def _tucker_device(core: np.ndarray, ys, dtype=None):
+    """L = core x_1 Y_1 ... x_n Y_n on the device (rtcur_generate_tucker with no
+    outliers): Tf = core x_{m>=2} Y_m on the host (small), the mode-1 step and
+    the |L| sum on the device.  Returns (flat torch tensor, sum |L|)."""
+    import ctypes
+
+    import torch
+
+    from . import _native as nat
+
+    dtype = dtype or torch.float64
+    n = len(ys)
+    shape = tuple(int(y.shape[0]) for y in ys)
+    r1 = int(ys[0].shape[1])
+    tf = core
+    for m in range(1, n):
+        tf = np.tensordot(tf, ys[m], axes=([1], [1]))
+    tf = np.moveaxis(tf, 0, -1)
+    tf = np.ascontiguousarray(np.transpose(tf, tuple(range(n - 2, -1, -1)) + (n - 1,)) if n > 1 else tf)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Tf = torch.from_numpy(tf.reshape(-1, r1)).to(dev)
+    Y1 = torch.from_numpy(np.asfortranarray(ys[0]).reshape(-1, order="F")).to(dev)
+    ncols = int(np.prod(shape[1:], dtype=np.int64)) if n > 1 else 1
+    lib = nat.load()
+    scratch = torch.empty(1300, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    dt = 0 if dtype == torch.float64 else 1
+    s_abs = ctypes.c_double()
+    nat.check(lib.rtcur_generate_tucker(Y1.data_ptr(), Tf.data_ptr(), shape[0], r1, 0, shape[0], ncols, 0, 0, 0.0, 0.0,
+                                        dt, None, scratch.data_ptr(), ctypes.byref(s_abs), stream))
+    L = torch.empty(shape[0] * ncols, dtype=dtype, device=dev)
+    nat.check(lib.rtcur_generate_tucker(Y1.data_ptr(), Tf.data_ptr(), shape[0], r1, 0, shape[0], ncols, 1, 0, 0.0, 0.0,
+                                        dt, L.data_ptr(), scratch.data_ptr(), None, stream))
+    return L, float(s_abs.value)
+
+
+def gen_lowrank_device(spec: InstanceSpec):
+    """synth.py:74-88 on the device: the same core/factor draws (host PCG64,
+    core first, then the factors mode by mode), the expansion in HBM.
+    Returns an fp64 DeviceTensor."""
+    from .tensor import DeviceTensor
+
+    rng = np.random.default_rng(spec.seed)
+    core = rng.standard_normal(spec.r ** spec.n).reshape((spec.r,) * spec.n, order="F")
+    ys = [rng.standard_normal((spec.d, spec.r)) for _ in range(spec.n)]
+    L, _ = _tucker_device(core, ys)
+    return DeviceTensor(L, spec.shape)
+
+
+def gen_outliers_device(low, alpha: float, seed, x=None):
+    """synth.py:101-121 on the device: floor(alpha * size) positions drawn
+    without replacement by the reference's sampler (same generator stream),
+    values uniform on [-mu, mu] with mu = mean|low| (fixed-order device sum).
+    Returns the sparse DeviceTensor; when ``x`` (a copy of low) is given it is
+    updated in place to low + sparse."""
+    import ctypes
+
+    import torch
+
+    from . import _native as nat
+    from .fiber_cur import _draw_without_replacement
+    from .tensor import DeviceTensor
+
+    if not 0.0 <= alpha < 1.0:
+        raise ValueError(f"outlier fraction must lie in [0, 1), got {alpha}")
+    size = int(low.flat.numel())
+    count = int(math.floor(alpha * size + 1e-9))
+    S = torch.zeros(size, dtype=torch.float64, device=low.flat.device)
+    if count > 0:
+        rng = np.random.default_rng(seed)
+        pos = _draw_without_replacement(rng, size, count) - 1
+        lf = low.flat if low.flat.dtype == torch.float64 else low.flat.double()
+        scratch = torch.empty(600, dtype=torch.float64, device=lf.device)
+        tot = ctypes.c_double()
+        nat.check(nat.load().rtcur_abs_sum(lf.data_ptr(), size, scratch.data_ptr(), ctypes.byref(tot),
+                                           torch.cuda.current_stream().cuda_stream))
+        mu = tot.value / size
+        u = rng.random(count)
+        dev = low.flat.device
+        pos_d = torch.from_numpy(np.ascontiguousarray(pos, dtype=np.int64)).to(dev)
+        u_d = torch.from_numpy(u).to(dev)
+        target = x.flat if x is not None else torch.zeros(size, dtype=torch.float64, device=dev)
+        nat.check(nat.load().rtcur_scatter_outliers(target.data_ptr(), pos_d.data_ptr(), u_d.data_ptr(), count,
+                                                    ctypes.c_double(mu), S.data_ptr(),
+                                                    torch.cuda.current_stream().cuda_stream))
+    return DeviceTensor(S, low.shape)
+
+
+def make_instance_device(spec: InstanceSpec):
+    """synth.py:124-135 on the device: (x, low, sparse) fp64 DeviceTensors; the
+    outlier stream is seeded by SeedSequence([seed, 1]) as in the reference."""
+    from .tensor import DeviceTensor
+
+    low = gen_lowrank_device(spec)
+    x = DeviceTensor(low.flat.clone(), low.shape)
+    sparse = gen_outliers_device(low, spec.alpha, np.random.SeedSequence([spec.seed, 1]), x=x)
+    return x, low, sparse
