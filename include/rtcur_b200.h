@@ -92,6 +92,11 @@ int rtcur_engine_absmax(rtcur_engine* e, double* out);
 int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols);
 /* gather this rank's owned sampled entries into the compact x blocks (others 0) */
 int rtcur_engine_gather(rtcur_engine* e);
+/* Sample slots: set_sample + gather fill the inactive slot (so they may be enqueued
+ * while the previous iteration still runs on the stream); the next iterate_async
+ * makes it active.  Workspace byte offset of the compact blocks the next gather
+ * writes / the next iteration reads (dtype of X, xblocks_elems entries). */
+int rtcur_engine_xblocks_offset(rtcur_engine* e, int64_t* offset);
 /* one RTCUR iteration at threshold zeta (already decayed).  first != 0: L = 0.
  * sums (host, 2*(n+1)): per block sum((x-L-S)^2), sum(x^2) of the NEW iterate;
  * flags (host, n): rank-deficiency flags of the new intersections. */

@@ -22,7 +22,7 @@ RTCUR_F64, RTCUR_F32 = 0, 1
 EXPORTED = (
     "rtcur_last_error", "rtcur_version", "rtcur_launch_count", "rtcur_gather_columns", "rtcur_hard_threshold",
     "rtcur_truncated_svd", "rtcur_engine_plan", "rtcur_engine_create", "rtcur_engine_destroy", "rtcur_engine_bind",
-    "rtcur_engine_absmax", "rtcur_engine_set_sample", "rtcur_engine_gather", "rtcur_engine_iterate",
+    "rtcur_engine_absmax", "rtcur_engine_set_sample", "rtcur_engine_gather", "rtcur_engine_xblocks_offset", "rtcur_engine_iterate",
     "rtcur_engine_iterate_async", "rtcur_engine_iterate_wait",
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
     "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_profile_read",
@@ -70,6 +70,7 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_absmax.argtypes = [c_vp, c_dp]
     lib.rtcur_engine_set_sample.argtypes = [c_vp, ctypes.POINTER(c_i64p), ctypes.POINTER(c_i64p)]
     lib.rtcur_engine_gather.argtypes = [c_vp]
+    lib.rtcur_engine_xblocks_offset.argtypes = [c_vp, c_i64p]
     lib.rtcur_engine_iterate.argtypes = [c_vp, ctypes.c_double, ctypes.c_int, c_dp, c_i32p]
     lib.rtcur_engine_iterate_async.argtypes = [c_vp, ctypes.c_double, ctypes.c_int]
     lib.rtcur_engine_iterate_wait.argtypes = [c_vp, c_dp, c_i32p]

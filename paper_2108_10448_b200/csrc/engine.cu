@@ -122,6 +122,7 @@ struct Plan {
   i64 o_apart2;
   // workspace offsets (bytes)
   i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
+  i64 samp_delta;   // bytes from sample slot 0 (index sets, maps, compact blocks) to slot 1
   i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES],
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
@@ -380,6 +381,8 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   // workspace carve
   i64 o = 0;
   auto take = [&](i64 bytes) { i64 r = o; o += align256(std::max<i64>(bytes, 8)); return r; };
+  // sample slot 0 (index sets, row/column maps, compact blocks); slot 1 follows at samp_delta
+  const i64 samp0 = o;
   for (int m = 0; m < n; ++m) P.o_rows[m] = take(row_sizes[m] * 4);
   for (int m = 0; m < n; ++m) P.o_cols[m] = take(col_sizes[m] * 8);
   {
@@ -391,6 +394,8 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_coli1 = take(P.col_off[g.nblk] * 4);
   P.o_coloff = take((RT_MAX_BLOCKS + 1) * 8);
   P.o_xb = take(g.nblk_total * P.esize + 64);   // +64: aligned bulk-copy supersets may read past the end
+  P.samp_delta = o - samp0;
+  take(P.samp_delta - 8);   // slot 1 (aligned like slot 0)
   P.o_state = take(3 * g.state_doubles * 8);
   for (int m = 0; m < n; ++m) P.o_M[m] = take(row_sizes[m] * col_sizes[m] * 8);
   P.o_gpart = take((i64)n * P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
@@ -445,7 +450,8 @@ struct rtcur_engine {
   i64 lo, hi;
   const void* X;
   int cur;          // ring slot of the latest iterate (-1: none)
-  int sample_epoch; // bumped by every rtcur_engine_set_sample
+  int act, stg;     // sample slots: active (iterations, exports) and staged (next set_sample/gather), -1: none
+  int sample_epoch; // bumped whenever a staged sample becomes active
   int w_epoch[3];   // sample epoch each slot's W (column weights) was built for
   bool pending;     // an iterate_async awaits its iterate_wait
   bool use_fast;    // allow the warm-started subspace-iteration eigensolver
@@ -455,8 +461,9 @@ struct rtcur_engine {
   bool sampled;
   double* h_pinned;  // host staging: sums, flags
   int* h_flags;
-  i64* h_idx;        // pinned staging for index upload
+  i64* h_idx;        // pinned staging for index upload (one half per sample slot)
   i64 h_idx_len;
+  cudaEvent_t idx_ev[2];   // H2D of each slot's index staging done
   // optional per-phase CUDA-event timing (rtcur_engine_profile)
   bool prof_on;
   unsigned prof_mask;  // phases timed while prof_on
@@ -467,6 +474,9 @@ struct rtcur_engine {
   cudaEvent_t prof_open[RT_NPHASE];
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
+  i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
+  int act_slot() const { return act >= 0 ? act : 0; }
+  char* xb(int slot) const { return ws + P.o_xb + sd(slot); }
 };
 
 static cudaEvent_t prof_event(rtcur_engine* e) {
@@ -494,7 +504,14 @@ static void prof_end(rtcur_engine* e, int ph) {
 }
 // after a stream synchronisation: fold the recorded intervals into the totals
 static void prof_flush(rtcur_engine* e) {
+  // fold the completed intervals; intervals still in flight (work enqueued behind
+  // the synchronisation point, e.g. a prefetched gather) stay pending
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> keep;
   for (auto& p : *e->prof_pending) {
+    if (cudaEventQuery(p.second.second) != cudaSuccess) {
+      keep.push_back(p);
+      continue;
+    }
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
       e->prof_ms[p.first] += ms;
@@ -503,7 +520,7 @@ static void prof_flush(rtcur_engine* e) {
     e->prof_pool->push_back(p.second.first);
     e->prof_pool->push_back(p.second.second);
   }
-  e->prof_pending->clear();
+  e->prof_pending->swap(keep);
 }
 
 static int set_smem_limits_once() {
@@ -550,23 +567,26 @@ static int set_smem_limits_once() {
   return RT_OK;
 }
 
-static IndexPtrs make_ip(const rtcur_engine* e) {
+static IndexPtrs make_ip_slot(const rtcur_engine* e, int slot) {
   const Plan& P = e->P;
+  const i64 d = e->sd(slot);
   IndexPtrs ip;
   memset(&ip, 0, sizeof(ip));
   i64 roff = 0;
   for (int m = 0; m < P.g.n; ++m) {
-    ip.rows[m] = e->at<int>(P.o_rows[m]);
-    ip.cols[m] = e->at<i64>(P.o_cols[m]);
-    ip.rowpos[m] = e->at<int>(P.o_rowpos) + roff;
+    ip.rows[m] = e->at<int>(P.o_rows[m] + d);
+    ip.cols[m] = e->at<i64>(P.o_cols[m] + d);
+    ip.rowpos[m] = e->at<int>(P.o_rowpos + d) + roff;
     roff += P.g.dim[m];
   }
   for (int b = 0; b < P.g.nblk; ++b) {
-    ip.colR[b] = e->at<i64>(P.o_colR) + P.col_off[b];
-    ip.coli1[b] = e->at<int>(P.o_coli1) + P.col_off[b];
+    ip.colR[b] = e->at<i64>(P.o_colR + d) + P.col_off[b];
+    ip.coli1[b] = e->at<int>(P.o_coli1 + d) + P.col_off[b];
   }
   return ip;
 }
+// the active sample (iterations, exports, K3)
+static IndexPtrs make_ip(const rtcur_engine* e) { return make_ip_slot(e, e->act_slot()); }
 
 // the warm-started fast path needs extra scratch; used only when it fits
 static int eig_fast_ok(const Plan& P, int m) {
@@ -607,6 +627,8 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->lo = slab_lo;
   e->hi = slab_hi;
   e->cur = e->prev = -1;
+  e->act = e->stg = -1;
+  e->idx_ev[0] = e->idx_ev[1] = nullptr;
   e->prof_mask = ~0u;
   e->use_fast = getenv("RTCUR_NO_FAST_EIG") == nullptr;
   e->prof_pool = new std::vector<cudaEvent_t>();
@@ -621,13 +643,14 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   i64 idx_len = 0;
   for (int m = 0; m < n; ++m) idx_len += row_sizes[m] + col_sizes[m];
   e->h_idx_len = idx_len;
-  ce = cudaMallocHost(&e->h_idx, idx_len * 8 + 64);
+  ce = cudaMallocHost(&e->h_idx, 2 * (idx_len * 8 + 64));
   if (ce != cudaSuccess) { cudaFreeHost(e->h_pinned); delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   // counters + col offsets
   CK(cudaMemsetAsync(e->ws + e->P.o_counters, 0, 64 * 4, e->st));
   // zero the compact blocks once: the alignment pads between blocks are never
   // written by the gather and must not carry garbage into rank all-reduces
-  CK(cudaMemsetAsync(e->ws + e->P.o_xb, 0, e->P.g.nblk_total * e->P.esize + 64, e->st));
+  for (int s = 0; s < 2; ++s) CK(cudaMemsetAsync(e->xb(s), 0, e->P.g.nblk_total * e->P.esize + 64, e->st));
+  for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&e->idx_ev[s], cudaEventDisableTiming));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -647,6 +670,8 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   if (e->h_pinned) cudaFreeHost(e->h_pinned);
   if (e->h_idx) cudaFreeHost(e->h_idx);
   if (e->done) cudaEventDestroy(e->done);
+  for (int s = 0; s < 2; ++s)
+    if (e->idx_ev[s]) cudaEventDestroy(e->idx_ev[s]);
   if (e->prof_pending) {
     for (auto& p : *e->prof_pending) {
       cudaEventDestroy(p.second.first);
@@ -698,13 +723,19 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
   const Plan& P = e->P;
   const Geom& g = P.g;
   const i64 total = [&] { i64 t = 1; for (int m = 0; m < g.n; ++m) t *= g.dim[m]; return t; }();
+  // the next sample goes to the inactive slot (stream-ordered after the running
+  // iteration, which keeps reading the active one); its pinned index staging is
+  // free once that slot's previous upload has completed
+  const int slot = e->stg >= 0 ? e->stg : (e->act < 0 ? 0 : (e->act ^ 1));
+  CK(cudaEventSynchronize(e->idx_ev[slot]));
+  i64* h_idx = e->h_idx + (size_t)slot * (e->h_idx_len + 8);
+  const i64 sdl = e->sd(slot);
   // validate (fiber_cur.py:67-83) and stage 0-based copies in pinned memory
-  CK(cudaStreamSynchronize(e->st));   // staging buffer reuse
   i64 o = 0;
   std::vector<i64> offs(2 * g.n);
   for (int m = 0; m < g.n; ++m) {
     offs[m] = o;
-    int* dst = reinterpret_cast<int*>(e->h_idx + o);
+    int* dst = reinterpret_cast<int*>(h_idx + o);
     for (i64 i = 0; i < g.nrows[m]; ++i) {
       const int64_t v = rows[m][i];
       if (v < 1 || v > g.dim[m]) return fail(RT_ERR_INDEX, "mode " + std::to_string(m + 1) + ": row index outside [1, d]");
@@ -720,25 +751,37 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
       const int64_t v = cols[m][i];
       if (v < 1 || v > rest) return fail(RT_ERR_INDEX, "mode " + std::to_string(m + 1) + ": fiber column outside range");
       if (i > 0 && v <= cols[m][i - 1]) return fail(RT_ERR_VALUE, "column sets must be sorted and unique");
-      e->h_idx[o + i] = v - 1;
+      h_idx[o + i] = v - 1;
     }
     o += g.ncols[m];
   }
   for (int m = 0; m < g.n; ++m) {
-    CK(cudaMemcpyAsync(e->ws + P.o_rows[m], e->h_idx + offs[m], g.nrows[m] * 4, cudaMemcpyHostToDevice, e->st));
-    CK(cudaMemcpyAsync(e->ws + P.o_cols[m], e->h_idx + offs[g.n + m], g.ncols[m] * 8, cudaMemcpyHostToDevice, e->st));
+    CK(cudaMemcpyAsync(e->ws + P.o_rows[m] + sdl, h_idx + offs[m], g.nrows[m] * 4, cudaMemcpyHostToDevice, e->st));
+    CK(cudaMemcpyAsync(e->ws + P.o_cols[m] + sdl, h_idx + offs[g.n + m], g.ncols[m] * 8, cudaMemcpyHostToDevice,
+                       e->st));
   }
-  IndexPtrs ip = make_ip(e);
+  CK(cudaEventRecord(e->idx_ev[slot], e->st));
+  IndexPtrs ip = make_ip_slot(e, slot);
   prof_begin(e, PH_PREP);
   dim3 gr((unsigned)std::min<i64>(cdiv(P.dmax, 256), 1024), g.n);
-  k_rowpos<<<gr, 256, 0, e->st>>>(g, ip, e->at<int>(P.o_rowpos));
+  k_rowpos<<<gr, 256, 0, e->st>>>(g, ip, e->at<int>(P.o_rowpos + sdl));
   LAUNCH_CHECK();
   dim3 gc((unsigned)std::min<i64>(cdiv(P.qmax, 256), 4096), g.nblk);
-  k_colprep<<<gc, 256, 0, e->st>>>(g, ip, e->at<i64>(P.o_colR), e->at<int>(P.o_coli1), e->at<i64>(P.o_coloff));
+  k_colprep<<<gc, 256, 0, e->st>>>(g, ip, e->at<i64>(P.o_colR + sdl), e->at<int>(P.o_coli1 + sdl),
+                                   e->at<i64>(P.o_coloff));
   LAUNCH_CHECK();
   prof_end(e, PH_PREP);
   e->sampled = true;
-  e->sample_epoch++;
+  e->stg = slot;
+  return RT_OK;
+}
+
+// byte offset (in the workspace) of the compact blocks the next gather writes / the
+// next iteration reads: the staged sample slot if any, else the active one
+extern "C" int rtcur_engine_xblocks_offset(rtcur_engine* e, int64_t* offset) {
+  if (!e || !offset) return fail(RT_ERR_VALUE, "null argument");
+  const int slot = e->stg >= 0 ? e->stg : e->act_slot();
+  *offset = e->P.o_xb + e->sd(slot);
   return RT_OK;
 }
 
@@ -746,10 +789,11 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
   if (!e->sampled) return fail(RT_ERR_VALUE, "no sample set");
   const Plan& P = e->P;
-  IndexPtrs ip = make_ip(e);
+  const int slot = e->stg >= 0 ? e->stg : e->act_slot();
+  IndexPtrs ip = make_ip_slot(e, slot);
   prof_begin(e, PH_GATHER);
   k_gather<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, e->X, P.dtype, e->lo, e->hi,
-                                                              e->ws + P.o_xb);
+                                                              e->xb(slot));
   LAUNCH_CHECK();
   prof_end(e, PH_GATHER);
   return RT_OK;
@@ -783,7 +827,7 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   IndexPtrs ip = make_ip(e);
   PassArgs a;
   memset(&a, 0, sizeof(a));
-  a.xb = e->ws + P.o_xb;
+  a.xb = e->xb(e->act_slot());
   a.dtype = P.dtype;
   a.st_s = st_s;
   a.st_e = st_e;
@@ -1012,7 +1056,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     // A_k = C_k V_k S_k^+ on the block-pass tiles (fiber blocks), then the fixed-order reduction
     PassArgs pa;
     memset(&pa, 0, sizeof(pa));
-    pa.xb = e->ws + P.o_xb;
+    pa.xb = e->xb(e->act_slot());
     pa.dtype = P.dtype;
     pa.st_s = st_s;
     pa.zeta = zeta;
@@ -1048,7 +1092,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   // G = clean_core x_1 U_1^T x_2 ... x_n U_n^T
   GPassArgs gp;
   memset(&gp, 0, sizeof(gp));
-  gp.xb = e->ws + P.o_xb;
+  gp.xb = e->xb(e->act_slot());
   gp.dtype = P.dtype;
   gp.st_s = st_s;
   gp.zeta = zeta;
@@ -1061,7 +1105,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     IndexPtrs ipg = make_ip(e);
     PassArgs pa;
     memset(&pa, 0, sizeof(pa));
-    pa.xb = e->ws + P.o_xb;
+    pa.xb = e->xb(e->act_slot());
     pa.dtype = P.dtype;
     pa.st_s = st_s;
     pa.zeta = zeta;
@@ -1116,6 +1160,12 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
 
 extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first) {
   if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
+  if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
+  if (e->stg >= 0) {   // the staged sample (set_sample + gather) becomes the active one
+    e->act = e->stg;
+    e->stg = -1;
+    e->sample_epoch++;
+  }
   if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
   if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
   const Plan& P = e->P;

@@ -124,7 +124,10 @@ class Engine:
         import torch
 
         esz = 8 if self.dtype_code == nat.RTCUR_F64 else 4
-        raw = self.workspace[self.xblocks_offset:self.xblocks_offset + self.nblk_total * esz]
+        off = ctypes.c_int64()
+        nat.check(self.lib.rtcur_engine_xblocks_offset(self.handle, ctypes.byref(off)))
+        o = int(off.value) + self._ws_off   # offsets are relative to the 256-aligned workspace base
+        raw = self.workspace[o:o + self.nblk_total * esz]
         return raw.view(torch.float64 if esz == 8 else torch.float32)
 
     def bind(self, flat):
