@@ -169,6 +169,17 @@ int rtcur_scatter_outliers(double* X, const int64_t* pos, const double* u, int64
  * scratch: device, >= 600 doubles.  mu = mean |low| of gen_outliers (synth.py:91-98). */
 int rtcur_abs_sum(const double* x, int64_t n, double* scratch, double* out, void* stream);
 
+/* Dense HOSVD alternating projections (reference.py:132-193, the paper's comparison
+ * baseline): full-tensor passes of its loop.  rtcur_ap_threshold: S = HT(X - L, zeta)
+ * (L may be NULL: L = 0) and C = X - S in one pass.  rtcur_ap_residual: host sums[0] =
+ * sum (X - L - S)^2, sums[1] = sum X^2 in a fixed order (synchronous); scratch >= 1200
+ * doubles.  All fp64 device arrays of n entries. */
+int rtcur_ap_threshold(const double* X, const double* L, int64_t n, double zeta, double* S, double* C, void* stream);
+/* max |x| over n device values (dtype 0 f64 / 1 f32; NaN propagates), host result; scratch >= 1 double */
+int rtcur_abs_max(const void* x, int dtype, int64_t n, double* scratch, double* out, void* stream);
+int rtcur_ap_residual(const double* X, const double* L, const double* S, int64_t n, double* scratch, double* sums,
+                      void* stream);
+
 /* Host helper of the index sampler (fiber_cur.py:202-208): append the values of
  * batch not yet marked in seen (population bytes) to out, in first-occurrence
  * order; returns the new length (-1 if a value is out of range). */

@@ -1442,6 +1442,91 @@ extern "C" int rtcur_scatter_outliers(double* X, const int64_t* pos, const doubl
   return RT_OK;
 }
 
+// ---- dense HOSVD alternating projections (reference.py:132-193), full-tensor passes
+// S = HT(X - L, zeta) (strict |.| > zeta keep, solver.py:195-199) and C = X - S, one pass.
+__global__ void k_ap_threshold(const double* __restrict__ X, const double* __restrict__ L, i64 n, double zeta,
+                               double* __restrict__ S, double* __restrict__ C) {
+  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < n; k += (i64)gridDim.x * blockDim.x) {
+    const double x = X[k];
+    const double s = hard_thr(x - (L ? L[k] : 0.0), zeta);
+    S[k] = s;
+    C[k] = x - s;
+  }
+}
+// fixed-order sum of (X - L - S)^2 (and X^2): per-CTA partials, one CTA adds them in order
+__global__ void k_ap_resid_part(const double* __restrict__ X, const double* __restrict__ L,
+                                const double* __restrict__ S, i64 n, double* __restrict__ part) {
+  __shared__ double red[8];
+  double e2 = 0.0, x2 = 0.0;
+  for (i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x; k < n; k += (i64)gridDim.x * blockDim.x) {
+    const double x = X[k];
+    const double rr = x - L[k] - S[k];
+    e2 = fma(rr, rr, e2);
+    x2 = fma(x, x, x2);
+  }
+  e2 = block_sum(e2, red);
+  x2 = block_sum(x2, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = e2;
+    part[2 * blockIdx.x + 1] = x2;
+  }
+}
+__global__ void k_ap_resid_final(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double red[8];
+  double e2 = 0.0, x2 = 0.0;
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    e2 += part[2 * k];
+    x2 += part[2 * k + 1];
+  }
+  e2 = block_sum(e2, red);
+  x2 = block_sum(x2, red);
+  if (threadIdx.x == 0) {
+    out[0] = e2;
+    out[1] = x2;
+  }
+}
+
+extern "C" int rtcur_abs_max(const void* x, int dtype, int64_t n, double* scratch, double* out, void* stream) {
+  if (!x || !scratch || !out || n < 0 || (dtype != 0 && dtype != 1)) return fail(RT_ERR_VALUE, "bad abs-max arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(scratch);
+  CK(cudaMemsetAsync(d, 0, 8, st));
+  if (n > 0) {
+    if (dtype == 0) k_absmax<double><<<148 * 8, 256, 0, st>>>((const double*)x, n, d);
+    else k_absmax<float><<<148 * 8, 256, 0, st>>>((const float*)x, n, d);
+    LAUNCH_CHECK();
+  }
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, d, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(out, &bits, 8);
+  return RT_OK;
+}
+
+extern "C" int rtcur_ap_threshold(const double* X, const double* L, int64_t n, double zeta, double* S, double* C,
+                                  void* stream) {
+  if (!X || !S || !C || n < 0 || !(zeta >= 0.0)) return fail(RT_ERR_VALUE, "bad threshold arguments");
+  if (n == 0) return RT_OK;
+  k_ap_threshold<<<(unsigned)std::min<i64>(cdiv(n, 256), 148 * 16), 256, 0, (cudaStream_t)stream>>>(X, L, n, zeta, S,
+                                                                                                    C);
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
+extern "C" int rtcur_ap_residual(const double* X, const double* L, const double* S, int64_t n, double* scratch,
+                                 double* sums, void* stream) {
+  if (!X || !L || !S || !scratch || !sums || n < 0) return fail(RT_ERR_VALUE, "bad residual arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int np = 148 * 4;
+  k_ap_resid_part<<<np, 256, 0, st>>>(X, L, S, n, scratch);
+  LAUNCH_CHECK();
+  k_ap_resid_final<<<1, 256, 0, st>>>(scratch, np, scratch + 2 * np);
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(sums, scratch + 2 * np, 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RT_OK;
+}
+
 // ------------------------------------------------------------------ kernel-level plug
 
 extern "C" int rtcur_gather_columns(const void* flat, int dtype, int64_t flat_len, const int64_t* bases_dev,

@@ -8,6 +8,7 @@ CUDA stream.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -20,6 +21,7 @@ __all__ = ["Engine", "acquire_engine"]
 # attribute setup that would otherwise dominate a short solve.  A pooled engine
 # is handed out only when no live SolveResult still references it.
 _POOL: dict = {}
+_POOL_LOCK = threading.Lock()   # solves may run concurrently on several streams (sweeps)
 
 
 def acquire_engine(shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=None):
@@ -27,16 +29,18 @@ def acquire_engine(shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=
     import weakref
 
     dev = device or torch.device("cuda", torch.cuda.current_device())
+    # an engine is bound to the stream it was created on: key the pool by the caller's stream
     key = (tuple(shape), tuple(ranks), tuple(row_sizes), tuple(col_sizes), str(dtype), tuple(slab or (0, shape[0])),
-           str(dev))
-    free = _POOL.setdefault(key, [])
+           str(dev), int(torch.cuda.current_stream(dev).cuda_stream))
     eng = None
-    while free:
-        ref = free.pop()
-        eng = ref() if isinstance(ref, weakref.ref) else ref
-        if eng is not None and eng.handle.value:
-            break
-        eng = None
+    with _POOL_LOCK:
+        free = _POOL.setdefault(key, [])
+        while free:
+            ref = free.pop()
+            eng = ref() if isinstance(ref, weakref.ref) else ref
+            if eng is not None and eng.handle.value:
+                break
+            eng = None
     if eng is None:
         eng = Engine(shape, ranks, row_sizes, col_sizes, dtype, slab=slab, device=dev)
     eng._pool_key = key
@@ -48,7 +52,8 @@ def release_engine(eng):
     key = getattr(eng, "_pool_key", None)
     if key is not None and eng.handle.value:
         eng.unbind_quiet()
-        _POOL.setdefault(key, []).append(eng)
+        with _POOL_LOCK:
+            _POOL.setdefault(key, []).append(eng)
 
 
 class Engine:
