@@ -539,6 +539,7 @@ static int set_smem_limits_once() {
   } while (0)
   SMEM_ATTR(k_eig);
   SMEM_ATTR(k_wcols<4>); SMEM_ATTR(k_wcols<8>); SMEM_ATTR(k_wcols<16>); SMEM_ATTR(k_wcols<32>);
+  SMEM_ATTR(k_wcols_warp<4>); SMEM_ATTR(k_wcols_warp<8>); SMEM_ATTR(k_wcols_warp<16>); SMEM_ATTR(k_wcols_warp<32>);
   SMEM_ATTR(k_zproj<4>); SMEM_ATTR(k_zproj<8>); SMEM_ATTR(k_zproj<16>); SMEM_ATTR(k_zproj<32>);
 #define BP_ATTRS(RB)                                                                                     \
   SMEM_ATTR((k_block_pass<true, true, false, true, false, RB, false>));                                  \
@@ -1034,11 +1035,27 @@ static int run_wcols(rtcur_engine* e, double* sto) {
     int st = run_wchain(e, sto, rows, Pm, sto + g.blk[0].w_off);
     if (st) return st;
   }
-  const int rpt = wcols_rows_per_thread(g);
   i64 qf = 1;
   for (int b = chain ? 1 : 0; b < g.nblk; ++b) qf = std::max(qf, g.blk[b].Q);
-  DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(qf, 128), g.nblk), 128, wcols_smem(g), e->st, g, ip, sto, 0,
-             (double*)nullptr, rpt, chain ? 1 : 0);
+  // warp per column with the rank combinations over the lanes when its tables fit
+  i64 ncmax = 1, rsmax = 1;
+  for (int t = 0; t < g.n; ++t) {
+    i64 nc = 1, rs = 0;
+    for (int m = 0; m < g.n; ++m)
+      if (m != t) { nc *= g.rank[m]; rs += g.rank[m]; }
+    ncmax = std::max(ncmax, nc);
+    rsmax = std::max(rsmax, rs);
+  }
+  const int rows_cap = (int)(cdiv(rsmax, 32) * 32);
+  const i64 wsm = (g.gsize + (ncmax * 4 + ncmax * std::max(1, g.n - 1) + 7) / 8 + 1 + (i64)WC_WARPS * rows_cap) * 8;
+  if (wsm <= 200 * 1024 && ncmax >= 48) {   // few combinations: a thread per column is cheaper
+    const dim3 grid((unsigned)std::min<i64>(cdiv(qf, WC_WARPS * 2), 148 * 4), g.nblk);
+    DISPATCH_R(P.rb, k_wcols_warp, grid, 32 * WC_WARPS, (int)wsm, e->st, g, ip, sto, chain ? 1 : 0, rows_cap);
+  } else {
+    const int rpt = wcols_rows_per_thread(g);
+    DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(qf, 128), g.nblk), 128, wcols_smem(g), e->st, g, ip, sto, 0,
+               (double*)nullptr, rpt, chain ? 1 : 0);
+  }
   LAUNCH_CHECK();
   prof_end(e, PH_WCOLS);
   return RT_OK;

@@ -95,6 +95,97 @@ __global__ void __launch_bounds__(256) k_modeprod_fwd(const double* __restrict__
   }
 }
 
+// Warp per block column: w[a] = sum over the other modes' rank combinations c of
+//   G[a, c] * prod_{m != t} A_m[i_m(q), c_m]
+// with the combinations split over the lanes (a per-block table of G offsets and
+// per-mode indices, built once per CTA in shared memory), the other modes' A rows
+// of the column staged per warp, and a fixed-order butterfly sum of the r_t
+// partials.  Dynamic shared memory: G | goff[ncombo] (int) | cidx[ncombo][n-1]
+// (uchar) | per warp 32 * ceil(sum r_other / 32) row values.
+#define WC_WARPS 8
+template <int R>
+__global__ void __launch_bounds__(32 * WC_WARPS) k_wcols_warp(Geom g, IndexPtrs ip, double* __restrict__ st,
+                                                             int skip_core, int rows_cap) {
+  extern __shared__ double wsm[];
+  const int b = blockIdx.y;
+  if (b >= g.nblk || (skip_core && g.blk[b].is_core)) return;
+  const BlockDesc& bd = g.blk[b];
+  const i64 Q = bd.Q;
+  if ((i64)blockIdx.x * WC_WARPS >= Q) return;
+  const int tgt = bd.mode, rt = g.rank[tgt];
+  const i64 gst = g.gstride[tgt];
+  int no = 0, ncombo = 1, rsum = 0;
+  int om[RT_MAX_MODES], ro[RT_MAX_MODES];
+  for (int m = 0; m < g.n; ++m) {
+    if (m == tgt) continue;
+    om[no] = m;
+    ro[no] = rsum;
+    rsum += g.rank[m];
+    ncombo *= g.rank[m];
+    ++no;
+  }
+  double* G = wsm;
+  int* goff = reinterpret_cast<int*>(G + g.gsize);
+  unsigned char* cidx = reinterpret_cast<unsigned char*>(goff + ncombo);
+  double* rows = G + g.gsize + ((size_t)ncombo * 4 + (size_t)ncombo * (no > 0 ? no : 1) + 7) / 8 + 1;
+  for (i64 i = threadIdx.x; i < g.gsize; i += blockDim.x) G[i] = st[i];
+  for (int c = threadIdx.x; c < ncombo; c += blockDim.x) {
+    int t = c, off = 0;
+    for (int j = 0; j < no; ++j) {   // first other mode fastest
+      const int rk = g.rank[om[j]];
+      const int ij = t % rk;
+      t /= rk;
+      off += ij * (int)g.gstride[om[j]];
+      cidx[(size_t)c * no + j] = (unsigned char)ij;
+    }
+    goff[c] = off;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* rb = rows + (size_t)w * rows_cap;
+  for (i64 q = (i64)blockIdx.x * WC_WARPS + w; q < Q; q += (i64)gridDim.x * WC_WARPS) {
+    // the other modes' A rows of this column
+    {
+      i64 t = q, j = bd.is_core ? 0 : ip.cols[tgt][q];
+      for (int k = 0; k < no; ++k) {
+        const int m = om[k];
+        i64 im;
+        if (bd.is_core) {
+          const i64 pos = t % g.nrows[m];
+          t /= g.nrows[m];
+          im = ip.rows[m][pos];
+        } else {
+          // fiber columns enumerate the other modes ascending, first fastest (tensor.py:250-283)
+          im = j % g.dim[m];
+          j /= g.dim[m];
+        }
+        for (int bm = lane; bm < g.rank[m]; bm += 32) rb[ro[k] + bm] = st[g.a_off[m] + im + (i64)bm * g.dim[m]];
+      }
+    }
+    __syncwarp();
+    double acc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] = 0.0;
+    for (int c = lane; c < ncombo; c += 32) {
+      double coef = 1.0;
+      for (int k = no - 1; k >= 0; --k) coef *= rb[ro[k] + cidx[(size_t)c * no + k]];
+      const double* gq = G + goff[c];
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (i < rt) acc[i] = fma(gq[i * gst], coef, acc[i]);
+    }
+    double* out = st + bd.w_off + q * rt;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (i < rt) {
+        const double v = warp_sum(acc[i]);
+        if (lane == 0) out[i] = v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------------ W
 
 // Per block column q: w[a] = sum over the other modes' rank indices of
@@ -212,6 +303,10 @@ template __global__ void k_gpass<8>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<16>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<32>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_wcols<4>(Geom, IndexPtrs, double*, int, double*, int, int);
+template __global__ void k_wcols_warp<4>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<8>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<16>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<32>(Geom, IndexPtrs, double*, int, int);
 template __global__ void k_wcols<8>(Geom, IndexPtrs, double*, int, double*, int, int);
 template __global__ void k_wcols<16>(Geom, IndexPtrs, double*, int, double*, int, int);
 template __global__ void k_wcols<32>(Geom, IndexPtrs, double*, int, double*, int, int);
