@@ -182,18 +182,24 @@ __global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counter
 // Rayleigh-Ritz: cyclic Jacobi on H (one warp per mode, lane = row), sort the
 // Ritz values descending, write Q (col-major) and the short-side vectors E Q.
 __global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
+  // Parallel (round-robin) Jacobi on the r x r symmetric H: each round rotates
+  // the m/2 disjoint pairs of a tournament schedule at once (m = r rounded up
+  // to even, index r is a bye), columns then rows, accumulating Q.
   __shared__ double h[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ double q[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ double rc[RT_MAX_RANK / 2 + 1], rs[RT_MAX_RANK / 2 + 1];
+  __shared__ int pp[RT_MAX_RANK / 2 + 1], pq[RT_MAX_RANK / 2 + 1];
   __shared__ int ord[RT_MAX_RANK];
   const int k = blockIdx.x;
   if (k >= sa.n) return;
   const int r = sa.r[k], lane = threadIdx.x;
+  const int m = r + (r & 1), half = m / 2;
   for (int i = lane; i < r * r; i += 32) {
     h[i] = sa.H[k][i];
     q[i] = (i % r == i / r) ? 1.0 : 0.0;
   }
   __syncwarp();
-  for (int sweep = 0; sweep < 40; ++sweep) {
+  for (int sweep = 0; sweep < 40 && r > 1; ++sweep) {
     double off = 0.0, dia = 0.0;
     for (int i = lane; i < r * r; i += 32) {
       const double v = h[i] * h[i];
@@ -202,32 +208,54 @@ __global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
     off = warp_sum(off);
     dia = warp_sum(dia);
     if (off <= 1e-30 * dia || off == 0.0) break;
-    for (int p = 0; p < r - 1; ++p) {
-      for (int qq = p + 1; qq < r; ++qq) {
-        const double apq = h[p + qq * r];
-        if (apq == 0.0) continue;
-        const double app = h[p + p * r], aqq = h[qq + qq * r];
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
-        __syncwarp();
-        // columns p, q of h
-        if (lane < r) {
-          const double hp = h[lane + p * r], hq = h[lane + qq * r];
-          h[lane + p * r] = c * hp - sn * hq;
-          h[lane + qq * r] = sn * hp + c * hq;
+    for (int round = 0; round < m - 1; ++round) {
+      // tournament pairing: player 0 fixed, players 1..m-1 rotate by `round`
+      if (lane < half) {
+        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + round) % (m - 1); };
+        int a = player(lane), b = player(m - 1 - lane);
+        if (a > b) { const int t = a; a = b; b = t; }
+        double c = 1.0, sn = 0.0;
+        if (b < r) {
+          const double apq = h[a + b * r];
+          if (apq != 0.0) {
+            const double app = h[a + a * r], aqq = h[b + b * r];
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            sn = t * c;
+          }
         }
-        __syncwarp();
-        if (lane < r) {
-          const double hp = h[p + lane * r], hq = h[qq + lane * r];
-          h[p + lane * r] = c * hp - sn * hq;
-          h[qq + lane * r] = sn * hp + c * hq;
-          const double qp = q[lane + p * r], qv = q[lane + qq * r];
-          q[lane + p * r] = c * qp - sn * qv;
-          q[lane + qq * r] = sn * qp + c * qv;
-        }
-        __syncwarp();
+        pp[lane] = a;
+        pq[lane] = b;
+        rc[lane] = c;
+        rs[lane] = sn;
       }
+      __syncwarp();
+      // columns p, q of h and of q (every pair at once; lanes over (row, pair))
+      for (int e = lane; e < r * half; e += 32) {
+        const int row = e % r, pr = e / r;
+        const int p = pp[pr], qq = pq[pr];
+        if (qq >= r) continue;
+        const double c = rc[pr], sn = rs[pr];
+        const double hp = h[row + p * r], hq = h[row + qq * r];
+        h[row + p * r] = c * hp - sn * hq;
+        h[row + qq * r] = sn * hp + c * hq;
+        const double qp = q[row + p * r], qv = q[row + qq * r];
+        q[row + p * r] = c * qp - sn * qv;
+        q[row + qq * r] = sn * qp + c * qv;
+      }
+      __syncwarp();
+      // rows p, q of h
+      for (int e = lane; e < r * half; e += 32) {
+        const int col = e % r, pr = e / r;
+        const int p = pp[pr], qq = pq[pr];
+        if (qq >= r) continue;
+        const double c = rc[pr], sn = rs[pr];
+        const double hp = h[p + col * r], hq = h[qq + col * r];
+        h[p + col * r] = c * hp - sn * hq;
+        h[qq + col * r] = sn * hp + c * hq;
+      }
+      __syncwarp();
     }
   }
   if (lane == 0) {
