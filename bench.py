@@ -280,6 +280,8 @@ def run_b200(args):
 
     # ---------------- device-resident timed region (only the dominant HBM phase carries CUDA events)
     solver_mod.PROFILE_PHASES = (dom,)
+    solve(x_dev)   # untimed: the engines' per-iteration CUDA graphs for this profiling setting exist now
+    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     barrier()

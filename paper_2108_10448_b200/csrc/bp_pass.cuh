@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(512, 1) k_block_pass(Geom g, TileMap tm, Index
   __shared__ double red[16];
   __shared__ bool am_last;
   const int tid = threadIdx.x;
+  const double zeta_v = a.zetap ? __ldg(a.zetap) : a.zeta;
   // GP: the core's tiles; AP: the fiber blocks' tiles; else every tile
   const i64 tfirst = AP ? tm.first[1] : 0;
   const i64 ntiles = (GP ? tm.first[1] : tm.first[tm.nblk]) - tfirst;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(512, 1) k_block_pass(Geom g, TileMap tm, Index
     T.apitch = (r + 1) & ~1;
     T.Mk = (WM && !core) ? a.M[bd.mode] + q0 * g.nrows[bd.mode] : nullptr;
     T.mrows = (int)g.nrows[bd.mode];
-    T.zeta = a.zeta;
+    T.zeta = zeta_v;
     const i64 gofs = bd.off + e0;
     T.s_out = EXP && a.s_out ? a.s_out + gofs : nullptr;
     T.c_out = EXP && a.c_out ? a.c_out + gofs : nullptr;

@@ -50,6 +50,7 @@ struct PassArgs {
   const double* st_s;      // state giving L for the threshold (null: L = 0, first iteration)
   const double* st_e;      // state giving L for the error / trace (null: no error)
   double zeta;
+  const double* zetap;     // if set: zeta is read from device memory (graph-captured iterations)
   double* M[RT_MAX_MODES]; // intersection outputs, m_k x p_k column-major (null: skip)
   double* s_out;           // optional sparse values on the blocks
   double* c_out;           // optional clean values

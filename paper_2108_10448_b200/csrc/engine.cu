@@ -20,6 +20,8 @@
 #include <vector>
 #include <atomic>
 #include <algorithm>
+#include <map>
+#include <tuple>
 
 #include "k_block.cu"
 #include "k_gram.cu"
@@ -122,6 +124,7 @@ struct Plan {
   i64 o_apart2;
   // workspace offsets (bytes)
   i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
+  i64 o_zeta;       // device copy of the iteration's threshold (graph-captured iterations read it)
   i64 samp_delta;   // bytes from sample slot 0 (index sets, maps, compact blocks) to slot 1
   i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES],
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
@@ -397,6 +400,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.samp_delta = o - samp0;
   take(P.samp_delta - 8);   // slot 1 (aligned like slot 0)
   P.o_state = take(3 * g.state_doubles * 8);
+  P.o_zeta = take(8);
   for (int m = 0; m < n; ++m) P.o_M[m] = take(row_sizes[m] * col_sizes[m] * 8);
   P.o_gpart = take((i64)n * P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
   for (int m = 0; m < n; ++m) {
@@ -443,6 +447,17 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
 enum { PH_ABSMAX = 0, PH_PREP, PH_GATHER, PH_THRESH, PH_GRAM, PH_EIG, PH_SVDPOST, PH_APASS, PH_GPASS, PH_WCOLS,
        PH_ERROR, PH_EXPORT, PH_FULL, RT_NPHASE };
 
+struct ProfPair {
+  int ph;
+  cudaEvent_t b, e;
+  bool owned;   // from the engine's event pool (returned at flush); graph-owned events are reused
+};
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long nkernels = 0;   // kernel launches captured (counted at every replay)
+  std::vector<ProfPair> prof;      // event-record nodes of the profiled phases
+};
+
 struct rtcur_engine {
   Plan P;
   char* ws;
@@ -470,8 +485,15 @@ struct rtcur_engine {
   double prof_ms[RT_NPHASE];
   long long prof_cnt[RT_NPHASE];
   std::vector<cudaEvent_t>* prof_pool;
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>* prof_pending;
+  std::vector<ProfPair>* prof_pending;
   cudaEvent_t prof_open[RT_NPHASE];
+  // per-iteration CUDA graphs (rtcur_engine_iterate_async): one per launch-shape key
+  bool use_graphs;
+  bool capturing;
+  cudaStream_t cap_st;             // private stream the iteration is captured on
+  std::map<unsigned long long, GraphEntry>* graphs;
+  GraphEntry* cap_entry;
+  const double* zetap_cur;         // device zeta while an iteration body is enqueued/captured
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
   i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
@@ -492,33 +514,41 @@ static cudaEvent_t prof_event(rtcur_engine* e) {
 static void prof_begin(rtcur_engine* e, int ph) {
   if (!e->prof_on || !((e->prof_mask >> ph) & 1u)) return;
   cudaEvent_t ev = prof_event(e);
-  cudaEventRecord(ev, e->st);
+  if (e->capturing) cudaEventRecordWithFlags(ev, e->st, cudaEventRecordExternal);
+  else cudaEventRecord(ev, e->st);
   e->prof_open[ph] = ev;
 }
 static void prof_end(rtcur_engine* e, int ph) {
   if (!e->prof_on || !e->prof_open[ph]) return;
   cudaEvent_t ev = prof_event(e);
-  cudaEventRecord(ev, e->st);
-  e->prof_pending->push_back({ph, {e->prof_open[ph], ev}});
+  if (e->capturing) {
+    cudaEventRecordWithFlags(ev, e->st, cudaEventRecordExternal);
+    e->cap_entry->prof.push_back({ph, e->prof_open[ph], ev, false});
+  } else {
+    cudaEventRecord(ev, e->st);
+    e->prof_pending->push_back({ph, e->prof_open[ph], ev, true});
+  }
   e->prof_open[ph] = nullptr;
 }
-// after a stream synchronisation: fold the recorded intervals into the totals
+// after a stream synchronisation: fold the completed intervals into the totals;
+// intervals still in flight (work enqueued behind the synchronisation point, e.g.
+// a prefetched gather) stay pending
 static void prof_flush(rtcur_engine* e) {
-  // fold the completed intervals; intervals still in flight (work enqueued behind
-  // the synchronisation point, e.g. a prefetched gather) stay pending
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> keep;
+  std::vector<ProfPair> keep;
   for (auto& p : *e->prof_pending) {
-    if (cudaEventQuery(p.second.second) != cudaSuccess) {
+    if (cudaEventQuery(p.e) != cudaSuccess) {
       keep.push_back(p);
       continue;
     }
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
-      e->prof_ms[p.first] += ms;
-      e->prof_cnt[p.first] += 1;
+    if (cudaEventElapsedTime(&ms, p.b, p.e) == cudaSuccess) {
+      e->prof_ms[p.ph] += ms;
+      e->prof_cnt[p.ph] += 1;
     }
-    e->prof_pool->push_back(p.second.first);
-    e->prof_pool->push_back(p.second.second);
+    if (p.owned) {
+      e->prof_pool->push_back(p.b);
+      e->prof_pool->push_back(p.e);
+    }
   }
   e->prof_pending->swap(keep);
 }
@@ -637,7 +667,17 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
     delete e;
     return fail(RT_ERR_CUDA, "cudaEventCreate");
   }
-  e->prof_pending = new std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>();
+  e->prof_pending = new std::vector<ProfPair>();
+  e->graphs = new std::map<unsigned long long, GraphEntry>();
+  // opt-in: measured no gain on B200 (the host runs far ahead of the stream)
+  e->use_graphs = getenv("RTCUR_GRAPHS") != nullptr;
+  e->capturing = false;
+  e->cap_entry = nullptr;
+  e->zetap_cur = nullptr;
+  if (cudaStreamCreateWithFlags(&e->cap_st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete e;
+    return fail(RT_ERR_CUDA, "cudaStreamCreate");
+  }
   cudaError_t ce = cudaMallocHost(&e->h_pinned, 4096);
   if (ce != cudaSuccess) { delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   e->h_flags = reinterpret_cast<int*>(e->h_pinned + 256);
@@ -674,12 +714,24 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   for (int s = 0; s < 2; ++s)
     if (e->idx_ev[s]) cudaEventDestroy(e->idx_ev[s]);
   if (e->prof_pending) {
-    for (auto& p : *e->prof_pending) {
-      cudaEventDestroy(p.second.first);
-      cudaEventDestroy(p.second.second);
-    }
+    for (auto& p : *e->prof_pending)
+      if (p.owned) {
+        cudaEventDestroy(p.b);
+        cudaEventDestroy(p.e);
+      }
     delete e->prof_pending;
   }
+  if (e->graphs) {
+    for (auto& kv : *e->graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      for (auto& p : kv.second.prof) {
+        cudaEventDestroy(p.b);
+        cudaEventDestroy(p.e);
+      }
+    }
+    delete e->graphs;
+  }
+  if (e->cap_st) cudaStreamDestroy(e->cap_st);
   if (e->prof_pool) {
     for (auto ev : *e->prof_pool) cudaEventDestroy(ev);
     delete e->prof_pool;
@@ -833,6 +885,7 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   a.st_s = st_s;
   a.st_e = st_e;
   a.zeta = zeta;
+  a.zetap = e->zetap_cur;
   if (with_M)
     for (int m = 0; m < P.g.n; ++m) a.M[m] = e->at<double>(P.o_M[m]);
   a.s_out = s_out;
@@ -1077,6 +1130,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     pa.dtype = P.dtype;
     pa.st_s = st_s;
     pa.zeta = zeta;
+    pa.zetap = e->zetap_cur;
     for (int m = 0; m < n; ++m) {
       pa.V[m] = e->at<double>(P.o_V[m]);
       pa.siginv[m] = e->at<double>(P.o_siginv[m]);
@@ -1113,6 +1167,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   gp.dtype = P.dtype;
   gp.st_s = st_s;
   gp.zeta = zeta;
+  gp.zetap = e->zetap_cur;
   for (int m = 0; m < n; ++m) gp.U[m] = e->at<double>(P.o_U[m]);
   double* t0 = e->at<double>(P.o_gt0);
   double* t1 = e->at<double>(P.o_gt1);
@@ -1126,6 +1181,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     pa.dtype = P.dtype;
     pa.st_s = st_s;
     pa.zeta = zeta;
+    pa.zetap = e->zetap_cur;
     pa.U = gp.U[0];
     pa.t1 = gp.t1;
     pa.nonfinite = e->at<int>(P.o_nonfinite);
@@ -1169,36 +1225,21 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   }
   prof_end(e, PH_GPASS);
   // W for every block column
-  int st = run_wcols(e, sto);
-  if (st) return st;
-  e->w_epoch[dst] = e->sample_epoch;
-  return RT_OK;
+  return run_wcols(e, sto);   // (w_epoch of the new slot is set by the caller)
 }
 
-extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first) {
-  if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
-  if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
-  if (e->stg >= 0) {   // the staged sample (set_sample + gather) becomes the active one
-    e->act = e->stg;
-    e->stg = -1;
-    e->sample_epoch++;
-  }
-  if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
-  if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
+// The launch sequence of one iteration (captured into a CUDA graph per launch
+// shape).  Pure stream work: host-side bookkeeping stays in the caller.
+static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool reeval) {
   const Plan& P = e->P;
   const int n = P.g.n;
-  if (first) e->cur = e->prev = -1;
-  const double* st_s = (e->cur >= 0) ? e->state(e->cur) : nullptr;
-  int newslot = 0;
-  while (newslot == e->cur || newslot == e->prev) ++newslot;
+  const double zeta = e->zeta_last;   // (kernels read the device copy when zetap_cur is set)
+  CK(cudaMemcpyAsync(e->ws + P.o_zeta, e->h_pinned + 200, 8, cudaMemcpyHostToDevice, e->st));
   CK(cudaMemsetAsync(e->ws + P.o_nonfinite, 0, 4, e->st));
   int st;
   // RTCUR-R: the sample moved, re-evaluate the previous iterate on it
   // (reference solver.py:330-331, _eval_blocks(lcur, idx) on the new draw)
-  if (e->cur >= 0 && e->w_epoch[e->cur] != e->sample_epoch) {
-    if ((st = run_wcols(e, e->state(e->cur)))) return st;
-    e->w_epoch[e->cur] = e->sample_epoch;
-  }
+  if (reeval && (st = run_wcols(e, e->state(e->cur)))) return st;
   if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false, PH_THRESH))) return st;
   if ((st = run_svd(e, st_s))) return st;
   if ((st = run_factors(e, st_s, zeta, newslot))) return st;
@@ -1207,10 +1248,82 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   CK(cudaMemcpyAsync(e->h_pinned, e->ws + P.o_sums, 2 * P.g.nblk * 8, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(e->h_flags, e->ws + P.o_flags, n * 4, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(e->h_flags + 16, e->ws + P.o_nonfinite, 4, cudaMemcpyDeviceToHost, e->st));
+  return RT_OK;
+}
+
+// phases timed inside the iteration body (a graph's event nodes depend only on these)
+static const unsigned kIterPhases = (1u << PH_THRESH) | (1u << PH_GRAM) | (1u << PH_EIG) | (1u << PH_SVDPOST) |
+                                    (1u << PH_APASS) | (1u << PH_GPASS) | (1u << PH_WCOLS) | (1u << PH_ERROR);
+
+extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first) {
+  if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
+  if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
+  if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
+  if (e->stg >= 0) {   // the staged sample (set_sample + gather) becomes the active one
+    e->act = e->stg;
+    e->stg = -1;
+    e->sample_epoch++;
+  }
+  if (first) e->cur = e->prev = -1;
+  const double* st_s = (e->cur >= 0) ? e->state(e->cur) : nullptr;
+  int newslot = 0;
+  while (newslot == e->cur || newslot == e->prev) ++newslot;
+  const bool reeval = e->cur >= 0 && e->w_epoch[e->cur] != e->sample_epoch;
+  e->zeta_last = zeta;
+  e->h_pinned[200] = zeta;   // read by the iteration's first (memcpy) node
+  e->zetap_cur = e->at<double>(e->P.o_zeta);
+  int st = RT_OK;
+  if (e->use_graphs) {
+    const unsigned long long key = (unsigned long long)(e->cur + 1) | ((unsigned long long)newslot << 2) |
+                                   ((unsigned long long)e->act_slot() << 4) | ((unsigned long long)reeval << 5) |
+                                   ((unsigned long long)(e->prof_on ? (e->prof_mask & kIterPhases) : 0u) << 8);
+    auto it = e->graphs->find(key);
+    if (it == e->graphs->end()) {
+      GraphEntry ge;
+      e->cap_entry = &ge;
+      cudaStream_t saved = e->st;
+      e->st = e->cap_st;
+      e->capturing = true;
+      const unsigned long long l0 = rtcur_launch_counter_add(0);
+      cudaError_t ce = cudaStreamBeginCapture(e->cap_st, cudaStreamCaptureModeThreadLocal);
+      if (ce == cudaSuccess) st = iterate_body(e, st_s, newslot, reeval);
+      ge.nkernels = rtcur_launch_counter_add(0) - l0;
+      g_launches.fetch_sub(ge.nkernels);   // capturing executes nothing
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce2 = cudaStreamEndCapture(e->cap_st, &graph);
+      e->capturing = false;
+      e->st = saved;
+      e->cap_entry = nullptr;
+      if (ce != cudaSuccess || ce2 != cudaSuccess || st != RT_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        e->zetap_cur = nullptr;
+        if (st) return st;
+        return fail(RT_ERR_CUDA, std::string("iteration capture: ") + cudaGetErrorString(ce != cudaSuccess ? ce : ce2));
+      }
+      ce = cudaGraphInstantiate(&ge.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) {
+        e->zetap_cur = nullptr;
+        return fail(RT_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ce));
+      }
+      it = e->graphs->emplace(key, std::move(ge)).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, e->st));
+    rtcur_launch_counter_add(it->second.nkernels);   // the graph's kernels run now
+    for (auto& p : it->second.prof) e->prof_pending->push_back(p);
+  } else {
+    st = iterate_body(e, st_s, newslot, reeval);
+    if (st) {
+      e->zetap_cur = nullptr;
+      return st;
+    }
+  }
+  e->zetap_cur = nullptr;
   CK(cudaEventRecord(e->done, e->st));
+  if (reeval) e->w_epoch[e->cur] = e->sample_epoch;
+  e->w_epoch[newslot] = e->sample_epoch;
   e->prev = e->cur;
   e->cur = newslot;
-  e->zeta_last = zeta;
   e->pending = true;
   return RT_OK;
 }

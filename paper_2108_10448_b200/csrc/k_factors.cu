@@ -21,6 +21,7 @@ struct GPassArgs {
   int dtype;
   const double* st_s;
   double zeta;
+  const double* zetap;             // if set: zeta from device memory
   const double* U[RT_MAX_MODES];   // |I_k| x r row-major
   double* t1;                       // r_1 x prod_{m>=2}|I_m| (F-order)
 };
@@ -37,10 +38,11 @@ __global__ void __launch_bounds__(256) k_gpass(Geom g, IndexPtrs ip, GPassArgs a
 #pragma unroll
   for (int i = 0; i < R; ++i) acc[i] = 0.0;
   const double* U = a.U[0];
+  const double zeta = a.zetap ? __ldg(a.zetap) : a.zeta;
   for (i64 p = lane; p < bd.P; p += 32) {
     const double x = ld_elem(a.xb, bd.off + q * bd.P + p, a.dtype);
     const double ls = a.st_s ? eval_low(a.st_s, g, bd, ip.rows[0], p, q) : 0.0;
-    const double c = x - hard_thr(x - ls, a.zeta);
+    const double c = x - hard_thr(x - ls, zeta);
 #pragma unroll
     for (int i = 0; i < R; ++i)
       if (i < r) acc[i] = fma(U[p * r + i], c, acc[i]);

@@ -189,3 +189,34 @@ def test_errors_mirror_reference():
 
 def test_native_code_ran():
     assert _native.launch_count() > 0
+
+
+@pytest.mark.gpu
+def test_graph_captured_iterations_match():
+    """RTCUR_GRAPHS=1 (per-iteration CUDA graphs, zeta from device memory) gives the
+    same iterates as the stream-launched path (R and F, several slot rotations)."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import sys
+sys.path.insert(0, ".")
+from conftest import load_golden, golden_cfg_kwargs
+from paper_2108_10448_b200 import SolverConfig, rtcur
+from paper_2108_10448_b200.tensor import DenseTensor
+for case in ("bern_R", "d20_F", "n4_R"):
+    g = load_golden(f"solve_{case}.npz")
+    shape = tuple(int(v) for v in g["shape"])
+    res = rtcur(DenseTensor(g["x"], shape), SolverConfig(**golden_cfg_kwargs(g)))
+    print(case, res.iterations, repr(list(res.error_history)))
+'''
+    outs = []
+    here = os.path.dirname(os.path.abspath(__file__))
+    for env in ({}, {"RTCUR_GRAPHS": "1"}):
+        e = dict(os.environ, **env)
+        e["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, e.get("PYTHONPATH", "")])
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, cwd=here)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout)
+    assert outs[0] == outs[1] and outs[0].count("\n") == 3
