@@ -88,6 +88,13 @@ int rtcur_engine_destroy(rtcur_engine* e);
 int rtcur_engine_bind(rtcur_engine* e, const void* x_dev);
 /* max|X| over the bound slab (K0); synchronous, result on the host */
 int rtcur_engine_absmax(rtcur_engine* e, double* out);
+/* Optional copies of X with mode k fastest (rtcur_transpose_mode layout; copies[0]
+ * and NULL entries unused): the gather then reads mode-k fibers as contiguous runs
+ * instead of stride-prod_{m<k} d_m elements.  Ignored on sharded (slab) engines. */
+int rtcur_engine_bind_mode_copies(rtcur_engine* e, const void* const* copies);
+/* out = X with mode k moved to the front (then the other modes in order), i.e. for X
+ * viewed as (A, d_k, B), out[i + d_k (a + A b)] = X[a + A (i + d_k b)]; dtype 0/1. */
+int rtcur_transpose_mode(const void* x, int dtype, int n, const int64_t* dims, int k, void* out, void* stream);
 /* rows[k]: |I_k| sorted 1-based indices, cols[k]: |J_k| sorted 1-based unfolding columns (host) */
 int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols);
 /* gather this rank's owned sampled entries into the compact x blocks (others 0) */

@@ -27,7 +27,8 @@ EXPORTED = (
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
     "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_profile_read",
     "rtcur_append_distinct", "rtcur_generate_tucker", "rtcur_tnsr_read_header", "rtcur_tnsr_load", "rtcur_tnsr_store",
-    "rtcur_scatter_outliers", "rtcur_abs_sum", "rtcur_ap_threshold", "rtcur_ap_residual", "rtcur_abs_max",
+    "rtcur_scatter_outliers", "rtcur_abs_sum", "rtcur_ap_threshold", "rtcur_ap_residual", "rtcur_abs_max", "rtcur_engine_bind_mode_copies",
+    "rtcur_transpose_mode",
 )
 PHASES = ("absmax", "prep", "gather", "threshold", "gram", "eig", "svdpost", "apass", "gpass", "wcols", "error",
           "export", "full")
@@ -93,6 +94,8 @@ def load(path: str = LIB_PATH):
     lib.rtcur_ap_threshold.argtypes = [c_vp, c_vp, c_i64, ctypes.c_double, c_vp, c_vp, c_vp]
     lib.rtcur_ap_residual.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_dp, c_vp]
     lib.rtcur_abs_max.argtypes = [c_vp, ctypes.c_int, c_i64, c_vp, c_dp, c_vp]
+    lib.rtcur_engine_bind_mode_copies.argtypes = [c_vp, ctypes.POINTER(c_vp)]
+    lib.rtcur_transpose_mode.argtypes = [c_vp, ctypes.c_int, ctypes.c_int, c_i64p, ctypes.c_int, c_vp, c_vp]
     lib.rtcur_tnsr_read_header.argtypes = [ctypes.c_char_p, ctypes.c_int, c_i32p, c_i32p, c_i64p, ctypes.c_int, c_i64p]
     lib.rtcur_tnsr_load.argtypes = [ctypes.c_char_p, c_i64, c_i64, ctypes.c_int, c_vp, c_vp]
     lib.rtcur_tnsr_store.argtypes = [ctypes.c_char_p, ctypes.c_int, c_i64p, ctypes.c_int, c_vp, c_vp]

@@ -464,6 +464,7 @@ struct rtcur_engine {
   cudaStream_t st;
   i64 lo, hi;
   const void* X;
+  const void* mcopy[RT_MAX_MODES];   // optional mode-k-fastest copies of X (rtcur_engine_bind_mode_copies)
   int cur;          // ring slot of the latest iterate (-1: none)
   int act, stg;     // sample slots: active (iterations, exports) and staged (next set_sample/gather), -1: none
   int sample_epoch; // bumped whenever a staged sample becomes active
@@ -659,6 +660,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->hi = slab_hi;
   e->cur = e->prev = -1;
   e->act = e->stg = -1;
+  for (int m = 0; m < RT_MAX_MODES; ++m) e->mcopy[m] = nullptr;
   e->idx_ev[0] = e->idx_ev[1] = nullptr;
   e->prof_mask = ~0u;
   e->use_fast = getenv("RTCUR_NO_FAST_EIG") == nullptr;
@@ -743,6 +745,30 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
 extern "C" int rtcur_engine_bind(rtcur_engine* e, const void* x_dev) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
   e->X = x_dev;   // NULL unbinds (K3 then reconstructs L only)
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_bind_mode_copies(rtcur_engine* e, const void* const* copies) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  for (int m = 0; m < RT_MAX_MODES; ++m) e->mcopy[m] = (copies && m < e->P.g.n && m > 0) ? copies[m] : nullptr;
+  return RT_OK;
+}
+
+extern "C" int rtcur_transpose_mode(const void* x, int dtype, int n, const int64_t* dims, int k, void* out,
+                                    void* stream) {
+  if (!x || !out || !dims || n < 1 || k < 0 || k >= n || (dtype != 0 && dtype != 1))
+    return fail(RT_ERR_VALUE, "bad transpose arguments");
+  i64 A = 1, B = 1;
+  for (int m = 0; m < k; ++m) A *= dims[m];
+  for (int m = k + 1; m < n; ++m) B *= dims[m];
+  const i64 dk = dims[k];
+  const dim3 grid((unsigned)cdiv(A, 32), (unsigned)cdiv(dk, 32), (unsigned)std::min<i64>(B, 65535));
+  if (grid.x > 0x7fffffff || grid.y > 65535) return fail(RT_ERR_UNSUPPORTED, "transpose grid too large");
+  if (dtype == 0)
+    k_transpose_mode<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)x, A, dk, B, (double*)out);
+  else
+    k_transpose_mode<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)x, A, dk, B, (float*)out);
+  LAUNCH_CHECK();
   return RT_OK;
 }
 
@@ -845,8 +871,10 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   const int slot = e->stg >= 0 ? e->stg : e->act_slot();
   IndexPtrs ip = make_ip_slot(e, slot);
   prof_begin(e, PH_GATHER);
+  ModeCopies mc;
+  for (int m = 0; m < RT_MAX_MODES; ++m) mc.p[m] = (e->lo == 0 && e->hi == P.g.dim[0]) ? e->mcopy[m] : nullptr;
   k_gather<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, e->X, P.dtype, e->lo, e->hi,
-                                                              e->xb(slot));
+                                                              e->xb(slot), mc);
   LAUNCH_CHECK();
   prof_end(e, PH_GATHER);
   return RT_OK;

@@ -76,8 +76,14 @@ __global__ void k_colprep(Geom g, IndexPtrs ip, i64* __restrict__ colR_base, int
 // With one rank (lo = 0, hi = d_1) this is the plain gather of solver.py:172-182.
 // Multi-rank: every sampled entry has exactly one owner, so a sum all-reduce of
 // the per-rank x_b reproduces the full gather bit-exactly.
+// Optional copies of X with mode k fastest (mode k, then the other modes in order):
+// fiber column j of mode k is then the contiguous run [d_k j, d_k (j + 1)).
+struct ModeCopies {
+  const void* p[RT_MAX_MODES];
+};
+
 __global__ void __launch_bounds__(256) k_gather(Geom g, TileMap tm, IndexPtrs ip, const void* __restrict__ X, int dtype,
-                                               i64 lo, i64 hi, void* __restrict__ xb) {
+                                               i64 lo, i64 hi, void* __restrict__ xb, ModeCopies mc) {
   const i64 t = blockIdx.x;
   const int b = tile_block(tm, t);
   const BlockDesc& bd = g.blk[b];
@@ -93,6 +99,32 @@ __global__ void __launch_bounds__(256) k_gather(Geom g, TileMap tm, IndexPtrs ip
   const i64 rstr = bd.mode >= 1 ? g.rstride[bd.mode] : 0;
   const i64 off = bd.off;
   const bool small = nel < 0xFFFFFFFFll;
+  const void* cp = (!core && bd.mode >= 1) ? mc.p[bd.mode] : nullptr;
+  if (cp) {   // contiguous fibers from the mode-k-fastest copy (unsharded runs only)
+    const i64* __restrict__ cols = ip.cols[bd.mode];
+    for (i64 base = e0 + threadIdx.x; base < e1; base += (i64)GATHER_U * blockDim.x) {
+      double v[GATHER_U];
+#pragma unroll
+      for (int u = 0; u < GATHER_U; ++u) {
+        const i64 e = base + (i64)u * blockDim.x;
+        v[u] = 0.0;
+        if (e < e1) {
+          i64 q, p;
+          split_pq(e, P, small, q, p);
+          v[u] = ld_elem(cp, p + P * cols[q], dtype);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GATHER_U; ++u) {
+        const i64 e = base + (i64)u * blockDim.x;
+        if (e < e1) {
+          if (dtype == 0) reinterpret_cast<double*>(xb)[off + e] = v[u];
+          else reinterpret_cast<float*>(xb)[off + e] = (float)v[u];
+        }
+      }
+    }
+    return;
+  }
   for (i64 base = e0 + threadIdx.x; base < e1; base += (i64)GATHER_U * blockDim.x) {
     double v[GATHER_U];
 #pragma unroll
@@ -115,6 +147,33 @@ __global__ void __launch_bounds__(256) k_gather(Geom g, TileMap tm, IndexPtrs ip
         else reinterpret_cast<float*>(xb)[off + e] = (float)v[u];
       }
     }
+  }
+}
+
+// out = X with mode k moved first: view X as (A, d_k, B) (A = prod_{m<k} d_m),
+// out[i + d_k (a + A b)] = X[a + A (i + d_k b)] -- 32 x 32 shared-memory tiles,
+// both sides coalesced.
+template <typename T>
+__global__ void __launch_bounds__(256) k_transpose_mode(const T* __restrict__ X, i64 A, i64 dk, i64 B,
+                                                        T* __restrict__ out) {
+  __shared__ T tile[32][33];
+  const i64 a0 = (i64)blockIdx.x * 32, i0 = (i64)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  for (i64 b = blockIdx.z; b < B; b += gridDim.z) {
+    const T* src = X + A * dk * b;
+    T* dst = out + dk * A * b;
+#pragma unroll
+    for (int r = 0; r < 32; r += 8) {
+      const i64 a = a0 + tx, i = i0 + ty + r;
+      if (a < A && i < dk) tile[ty + r][tx] = src[a + A * i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 32; r += 8) {
+      const i64 i = i0 + tx, a = a0 + ty + r;
+      if (a < A && i < dk) dst[i + dk * a] = tile[tx][ty + r];
+    }
+    __syncthreads();
   }
 }
 

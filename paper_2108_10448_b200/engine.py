@@ -135,6 +135,25 @@ class Engine:
         raw = self.workspace[o:o + self.nblk_total * esz]
         return raw.view(torch.float64 if esz == 8 else torch.float32)
 
+    def bind_mode_copies(self, flat, modes):
+        """Build mode-k-fastest copies of the bound tensor for ``modes`` (k >= 1) and
+        let the gather read their fibers contiguously; ``modes`` empty: drop them."""
+        import torch
+
+        self._mode_copies = {}
+        if modes:
+            dims = nat.i64_array(self.shape)
+            dt = 0 if flat.dtype == torch.float64 else 1
+            for k in modes:
+                out = torch.empty_like(flat)
+                nat.check(self.lib.rtcur_transpose_mode(ctypes.c_void_p(flat.data_ptr()), dt, self.n, dims, int(k),
+                                                        ctypes.c_void_p(out.data_ptr()),
+                                                        ctypes.c_void_p(self.stream.cuda_stream)))
+                self._mode_copies[int(k)] = out
+        ptrs = (ctypes.c_void_p * self.n)(*[ctypes.c_void_p(self._mode_copies[k].data_ptr())
+                                            if k in self._mode_copies else None for k in range(self.n)])
+        nat.check(self.lib.rtcur_engine_bind_mode_copies(self.handle, ptrs))
+
     def bind(self, flat):
         """flat: contiguous CUDA tensor holding this rank's mode-1 slab."""
         self._x = flat

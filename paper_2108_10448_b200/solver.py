@@ -360,6 +360,24 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
     return _solve(_Source(x), cfg, record_trace)
 
 
+# DRAM bytes a strided fiber element costs the gather (8-byte reads one per
+# 32-byte sector, >= 64-byte DRAM fetches; ~120 B measured by ncu on config 1)
+_STRIDED_BYTES = 100
+
+
+def _mode_copy_plan(shape, col_sizes, cfg, src):
+    """Modes k >= 1 whose fibers the RTCUR-R gathers should read from a per-solve
+    mode-k-fastest copy of X: when ~max_iters gathers of d_k |J_k| strided entries
+    cost clearly more DRAM traffic than writing and reading the copy once."""
+    if cfg.variant != "R" or src.dev is None or src.group is not None or len(shape) < 2:
+        return ()
+    E = src.dev.flat.element_size()
+    N = int(np.prod(shape, dtype=np.int64))
+    gathers = min(int(cfg.max_iters), 25) + 1
+    return tuple(k for k in range(1, len(shape))
+                 if gathers * shape[k] * col_sizes[k] * (_STRIDED_BYTES - E) > 1.5 * 2 * N * E)
+
+
 def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
     import torch
 
@@ -385,6 +403,9 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> Sol
     if PROFILE:
         eng.profile(True, PROFILE_PHASES)
     src.attach(eng)
+    copies = _mode_copy_plan(shape, col_sizes, cfg, src)
+    if copies:
+        eng.bind_mode_copies(src.dev.flat, copies)
     t0 = time.perf_counter()
     eng.set_sample(idx)
     src.load_blocks(eng, idx)
@@ -442,6 +463,8 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> Sol
         if err <= cfg.eps:
             converged = True
             break
+    if copies:
+        eng.bind_mode_copies(None, ())   # the loop is done; exports do not gather
     timings["loop"] = time.perf_counter() - t_loop
     timings["total"] = time.perf_counter() - t_start
     if PROFILE:
