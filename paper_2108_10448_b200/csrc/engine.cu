@@ -336,8 +336,15 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
       pairs_tot += nt * (nt + 1) / 2;
       lm = std::max(lm, P.l[m]);
     }
-    const i64 want = std::max<i64>(1, cdiv(4 * 148, pairs_tot));
-    P.gram_cl = (int)std::max<i64>(GRAM_KS, cdiv(cdiv(lm, want), GRAM_KS) * GRAM_KS);
+    // split-K over ~6 waves of CTAs (measured: the tile loop is latency-bound, so more
+    // CTAs in flight beat fewer split-K partials)
+    const char* gw = getenv("RTCUR_GRAM_WAVES");
+    const char* gm = getenv("RTCUR_GRAM_MIN_CL");
+    const i64 waves = gw ? std::max(1, atoi(gw)) : 6;
+    const i64 mincl = gm ? std::max(GRAM_KS, atoi(gm)) : GRAM_KS;
+    const i64 want = std::max<i64>(1, cdiv(waves * 148, pairs_tot));
+    P.gram_cl = (int)std::max<i64>(std::min<i64>(mincl, cdiv(lm, GRAM_KS) * GRAM_KS),
+                                   cdiv(cdiv(lm, want), GRAM_KS) * GRAM_KS);
   }
   for (int m = 0; m < n; ++m) {
     const int nt = (int)cdiv(P.s[m], GRAM_T);

@@ -54,36 +54,60 @@ __global__ void __launch_bounds__(256) k_gram_tiles(GramArgs ga) {
   const i64 t1 = min(l, t0 + ga.cl);
   int I, J;
   pair_decode(pair, I, J);
-  __shared__ double As[GRAM_KS][GRAM_T + 1];
-  __shared__ double Bs[GRAM_KS][GRAM_T + 1];
+  __shared__ double As[2][GRAM_KS][GRAM_T + 1];
+  __shared__ double Bs[2][GRAM_KS][GRAM_T + 1];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  for (i64 tt = t0; tt < t1; tt += GRAM_KS) {
-    for (int idx = threadIdx.x; idx < GRAM_T * GRAM_KS; idx += blockDim.x) {
+  // register-prefetched double buffer: the next k-step's loads are in flight
+  // while the current one is multiplied
+  constexpr int PER = GRAM_T * GRAM_KS / 256;   // elements per thread per operand
+  double pa[PER], pb[PER];
+  auto fetch = [&](i64 tt) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * 256;
       const int r = idx % GRAM_T, kk = idx / GRAM_T;
       const i64 t = tt + kk;
       const int a = I * GRAM_T + r, b = J * GRAM_T + r;
-      As[kk][r] = (a < s && t < t1) ? gram_B(ga, k, a, t) : 0.0;
-      Bs[kk][r] = (b < s && t < t1) ? gram_B(ga, k, b, t) : 0.0;
+      pa[u] = (a < s && t < t1) ? gram_B(ga, k, a, t) : 0.0;
+      pb[u] = (b < s && t < t1) ? gram_B(ga, k, b, t) : 0.0;
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * 256;
+      const int r = idx % GRAM_T, kk = idx / GRAM_T;
+      As[buf][kk][r] = pa[u];
+      Bs[buf][kk][r] = pb[u];
+    }
+  };
+  fetch(t0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (i64 tt = t0; tt < t1; tt += GRAM_KS) {
+    const bool more = tt + GRAM_KS < t1;
+    if (more) fetch(tt + GRAM_KS);
 #pragma unroll
     for (int kk = 0; kk < GRAM_KS; ++kk) {
       double av[4], bv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+      for (int i = 0; i < 4; ++i) av[i] = As[buf][kk][ty * 4 + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][kk][tx + 16 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
+    if (more) stash(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
   }
   double* out = ga.part + (((i64)k * ga.maxchunks + blockIdx.y) * ga.maxpairs + pair) * (GRAM_T * GRAM_T);
 #pragma unroll
