@@ -594,7 +594,7 @@ static int set_smem_limits_once() {
   SMEM_ATTR((k_block_pass<false, false, false, false, false, RB, true>))
   BP_ATTRS(4); BP_ATTRS(8); BP_ATTRS(16); BP_ATTRS(32);
 #undef BP_ATTRS
-  SMEM_ATTR(k_hgram);
+  SMEM_ATTR(k_hgram<1>); SMEM_ATTR(k_hgram<2>);
 #undef SMEM_ATTR
   // L2 fetch granularity for the sampled gathers (element-sized loads scattered
   // over X): RTCUR_L2_FETCH=<32|64|128> bytes; unset leaves the device default
@@ -1058,21 +1058,14 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(P.lmax, ZP_T), n), 32 * P.rb, zsm, e->st, sa);
   LAUNCH_CHECK();
   const int hsm = (int)((HG_CH * P.rmax + 512) * 8);
-  k_hgram<<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
+  // H = Z^T Z -> (last CTA) Rayleigh-Ritz rotation + short-side vectors
+  k_hgram<1><<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
   LAUNCH_CHECK();
-  k_svd_fin1<<<n, 32, 0, e->st>>>(sa);
+  // Z <- Z Q, H' = Z^T Z -> (last CTA) sigma, order, cutoff, flags, T
+  k_hgram<2><<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
   LAUNCH_CHECK();
-  k_short_vecs<<<dim3((unsigned)cdiv(P.smax * P.rmax, 256), n), 256, 0, e->st>>>(sa);
-  LAUNCH_CHECK();
-  DISPATCH_R(P.rb, k_zrot, dim3(gz, n), 256, 0, e->st, sa);
-  LAUNCH_CHECK();
-  k_hgram<<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
-  LAUNCH_CHECK();
-  k_svd_fin2<<<n, 32, 0, e->st>>>(sa);
-  LAUNCH_CHECK();
-  DISPATCH_R(P.rb, k_long, dim3(gz, n), 256, 0, e->st, sa);
-  LAUNCH_CHECK();
-  k_complete<<<n, 256, 0, e->st>>>(sa);
+  // long side Z T -> (last CTA) short-side permutation + completion
+  DISPATCH_R(P.rb, k_long, dim3(gz, n), 256, 0, e->st, sa, hcnt + 8);
   LAUNCH_CHECK();
   prof_end(e, PH_SVDPOST);
   return RT_OK;
@@ -1821,21 +1814,11 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(l, ZP_T), 1), 32 * P.rb, zs, st, sa);
   LAUNCH_CHECK();
   const int hsm = (int)((HG_CH * r + 512) * 8);
-  k_hgram<<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
+  k_hgram<1><<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
   LAUNCH_CHECK();
-  k_svd_fin1<<<1, 32, 0, st>>>(sa);
+  k_hgram<2><<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
   LAUNCH_CHECK();
-  k_short_vecs<<<dim3((unsigned)cdiv(s * r, 256), 1), 256, 0, st>>>(sa);
-  LAUNCH_CHECK();
-  DISPATCH_R(P.rb, k_zrot, dim3(gz, 1), 256, 0, st, sa);
-  LAUNCH_CHECK();
-  k_hgram<<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
-  LAUNCH_CHECK();
-  k_svd_fin2<<<1, 32, 0, st>>>(sa);
-  LAUNCH_CHECK();
-  DISPATCH_R(P.rb, k_long, dim3(gz, 1), 256, 0, st, sa);
-  LAUNCH_CHECK();
-  k_complete<<<1, 256, 0, st>>>(sa);
+  DISPATCH_R(P.rb, k_long, dim3(gz, 1), 256, 0, st, sa, hcnt + 8);
   LAUNCH_CHECK();
   // row-major (m x r), (p x r) -> column-major outputs
   std::vector<double> U(m * r), V(p * r), S(r);

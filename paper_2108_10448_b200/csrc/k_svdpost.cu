@@ -124,9 +124,18 @@ __global__ void __launch_bounds__(256) k_zrot(SvdArgs sa) {
 // are combined in fixed order; the last CTA of each mode combines the chunk
 // partials the same way (deterministic).
 #define HG_CH 128
+// PH 1: H = Z^T Z of the projections; the last CTA of each mode then runs the
+//       Rayleigh-Ritz rotation (svd_fin1_warp) and writes the short-side vectors.
+// PH 2: each CTA first rotates its Z rows by Q (Z <- Z Q, written back), H' = Z^T Z;
+//       the last CTA runs svd_fin2_warp (sigma, order, cutoff, flags, T).
+__device__ void svd_fin1_warp(const SvdArgs& sa, int k);
+__device__ void svd_fin2_warp(const SvdArgs& sa, int k);
+__device__ void svd_short_vecs_cta(const SvdArgs& sa, int k, int t0, int stride);
+template <int PH>
 __global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counters) {
   extern __shared__ double hz[];   // HG_CH * r + blockDim
   __shared__ bool am_last;
+  __shared__ double qs[RT_MAX_RANK * RT_MAX_RANK];
   const int k = blockIdx.y;
   if (k >= sa.n) return;
   const int r = sa.r[k];
@@ -146,8 +155,23 @@ __global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counter
   double* red = hz + HG_CH * r;
   const i64 t0 = (i64)blockIdx.x * HG_CH;
   const int nt = (int)min((i64)HG_CH, l - t0);
-  const double* Z = sa.Z[k] + t0 * r;
-  for (int i = tid; i < nt * r; i += blockDim.x) hz[i] = Z[i];
+  double* Z = sa.Z[k] + t0 * r;
+  if (PH == 2) {
+    for (int i = tid; i < r * r; i += blockDim.x) qs[i] = sa.Q[k][i];
+    __syncthreads();
+    for (int t = tid; t < nt; t += blockDim.x) {   // Z <- Z Q, row t
+      double z[RT_MAX_RANK];
+      for (int b = 0; b < r; ++b) z[b] = Z[(i64)t * r + b];
+      for (int a2 = 0; a2 < r; ++a2) {
+        double o = 0.0;
+        for (int b = 0; b < r; ++b) o = fma(z[b], qs[b + a2 * r], o);
+        hz[t * r + a2] = o;
+        Z[(i64)t * r + a2] = o;
+      }
+    }
+  } else {
+    for (int i = tid; i < nt * r; i += blockDim.x) hz[i] = Z[i];
+  }
   __syncthreads();
   double acc = 0.0;
   if (sl < nsl)
@@ -177,11 +201,22 @@ __global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counter
     sa.H[k][b + a * r] = v;
   }
   if (tid == 0) counters[k] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (PH == 1) {
+    if (tid < 32) svd_fin1_warp(sa, k);
+    __threadfence();
+    __syncthreads();
+    svd_short_vecs_cta(sa, k, tid, blockDim.x);
+  } else {
+    if (tid < 32) svd_fin2_warp(sa, k);
+  }
 }
 
 // Rayleigh-Ritz: cyclic Jacobi on H (one warp per mode, lane = row), sort the
 // Ritz values descending, write Q (col-major) and the short-side vectors E Q.
-__global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
+// Rayleigh-Ritz rotation Q of mode k by one warp (lane = threadIdx.x & 31).
+__device__ void svd_fin1_warp(const SvdArgs& sa, int k) {
   // Parallel (round-robin) Jacobi on the r x r symmetric H: each round rotates
   // the m/2 disjoint pairs of a tournament schedule at once (m = r rounded up
   // to even, index r is a bye), columns then rows, accumulating Q.
@@ -190,9 +225,7 @@ __global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
   __shared__ double rc[RT_MAX_RANK / 2 + 1], rs[RT_MAX_RANK / 2 + 1];
   __shared__ int pp[RT_MAX_RANK / 2 + 1], pq[RT_MAX_RANK / 2 + 1];
   __shared__ int ord[RT_MAX_RANK];
-  const int k = blockIdx.x;
-  if (k >= sa.n) return;
-  const int r = sa.r[k], lane = threadIdx.x;
+  const int r = sa.r[k], lane = threadIdx.x & 31;
   const int m = r + (r & 1), half = m / 2;
   for (int i = lane; i < r * r; i += 32) {
     h[i] = sa.H[k][i];
@@ -274,32 +307,37 @@ __global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
   }
 }
 
+__global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
+  if ((int)blockIdx.x < sa.n) svd_fin1_warp(sa, blockIdx.x);
+}
+
 // short-side vectors S = E Q written row-major into U (wide) or V (tall)
-__global__ void k_short_vecs(SvdArgs sa) {
-  const int k = blockIdx.y;
-  if (k >= sa.n) return;
+__device__ void svd_short_vecs_cta(const SvdArgs& sa, int k, int t0, int stride) {
   const int s = sa.s[k], r = sa.r[k];
   double* out = sa.tall[k] ? sa.V[k] : sa.U[k];
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < s * r; e += gridDim.x * blockDim.x) {
+  for (int e = t0; e < s * r; e += stride) {
     const int i = e / r, a = e % r;
     double acc = 0.0;
     for (int b = 0; b < r; ++b) acc = fma(sa.E[k][i + b * s], sa.Q[k][b + a * r], acc);
     out[(i64)i * r + a] = acc;
   }
 }
+__global__ void k_short_vecs(SvdArgs sa) {
+  const int k = blockIdx.y;
+  if (k >= sa.n) return;
+  svd_short_vecs_cta(sa, k, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
 
 // sigma from ||z_a||, stable descending order, truncated-pinv reciprocals,
 // Cholesky orthonormalisation T (Z T orthonormal) over non-degenerate columns.
-__global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
+__device__ void svd_fin2_warp(const SvdArgs& sa, int k) {
   __shared__ double h[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ double R[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ double T[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ double X[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ double sg[RT_MAX_RANK];
   __shared__ int ord[RT_MAX_RANK], dg[RT_MAX_RANK];
-  const int k = blockIdx.x;
-  if (k >= sa.n) return;
-  const int r = sa.r[k], lane = threadIdx.x;
+  const int r = sa.r[k], lane = threadIdx.x & 31;
   for (int i = lane; i < r * r; i += 32) {
     h[i] = sa.H[k][i];
     R[i] = 0.0;
@@ -378,43 +416,59 @@ __global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
   if (lane == 0) sa.degen[k][r] = anyd;
 }
 
+__global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
+  if ((int)blockIdx.x < sa.n) svd_fin2_warp(sa, blockIdx.x);
+}
+
 // long-side vectors: out[t, a] = sum_b Z[t, b] T[b, a]; short side permuted in place later
+__device__ void svd_complete_cta(const SvdArgs& sa, int k);
+// the last CTA of each mode (ticket) then permutes the short side and completes
+// degenerate columns (svd_complete_cta)
 template <int R>
-__global__ void __launch_bounds__(256) k_long(SvdArgs sa) {
+__global__ void __launch_bounds__(256) k_long(SvdArgs sa, unsigned int* counters) {
   __shared__ double ts[RT_MAX_RANK * RT_MAX_RANK];
+  __shared__ bool am_last;
   const int k = blockIdx.y;
   if (k >= sa.n) return;
   const int r = sa.r[k];
   const i64 l = sa.l[k];
+  const unsigned nch = (unsigned)((l + blockDim.x - 1) / blockDim.x);
   if ((i64)blockIdx.x * blockDim.x >= l) return;
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) ts[i] = sa.Q[k][i];
   __syncthreads();
   const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= l) return;
-  const double* Z = sa.Z[k] + t * r;
-  double z[R], o[R];
+  if (t < l) {
+    const double* Z = sa.Z[k] + t * r;
+    double z[R], o[R];
 #pragma unroll
-  for (int a = 0; a < R; ++a) { z[a] = a < r ? Z[a] : 0.0; o[a] = 0.0; }
+    for (int a = 0; a < R; ++a) { z[a] = a < r ? Z[a] : 0.0; o[a] = 0.0; }
 #pragma unroll
-  for (int b = 0; b < R; ++b)
+    for (int b = 0; b < R; ++b)
+#pragma unroll
+      for (int a = 0; a < R; ++a)
+        if (a < r && b < r) o[a] = fma(z[b], ts[b + a * r], o[a]);
+    double* out = (sa.tall[k] ? sa.U[k] : sa.V[k]) + t * r;
 #pragma unroll
     for (int a = 0; a < R; ++a)
-      if (a < r && b < r) o[a] = fma(z[b], ts[b + a * r], o[a]);
-  double* out = (sa.tall[k] ? sa.U[k] : sa.V[k]) + t * r;
-#pragma unroll
-  for (int a = 0; a < R; ++a)
-    if (a < r) out[a] = o[a];
+      if (a < r) out[a] = o[a];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) am_last = (atomicAdd(&counters[k], 1u) == nch - 1);
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) counters[k] = 0u;
+  svd_complete_cta(sa, k);
 }
 
 // permute the short-side columns to the sigma order; complete degenerate
 // columns of both sides with orthonormal vectors (only when sigma <= tau, where
 // 1/sigma is dropped, so this never changes the low-rank iterate).
-__global__ void __launch_bounds__(256) k_complete(SvdArgs sa) {
+__device__ void svd_complete_cta(const SvdArgs& sa, int k) {
   __shared__ double tmp[RT_MAX_RANK];
   __shared__ double red[8];
   __shared__ double coef[RT_MAX_RANK];
-  const int k = blockIdx.x;
-  if (k >= sa.n) return;
   const int r = sa.r[k];
   const int s = sa.s[k];
   const i64 l = sa.l[k];
@@ -464,4 +518,8 @@ __global__ void __launch_bounds__(256) k_complete(SvdArgs sa) {
     }
   }
   (void)red;
+}
+
+__global__ void __launch_bounds__(256) k_complete(SvdArgs sa) {
+  if ((int)blockIdx.x < sa.n) svd_complete_cta(sa, blockIdx.x);
 }
