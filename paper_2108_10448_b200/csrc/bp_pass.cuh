@@ -178,8 +178,32 @@ __device__ __forceinline__ void bp_rows(const BPTile& T, double& e2, double& x2,
       ae[kk] = (HE && on) ? __ldg(T.Ae + grow + (i64)kk * T.d) : 0.0;
     }
     const int pos = WM ? T.rmap[p] : -1;
+    // two columns per step: independent FMA chains (each in kk order, so every
+    // entry's value is bit-identical to the one-column loop)
+    int q = qb;
 #pragma unroll 1
-    for (int q = qb; q < qe; ++q) {
+    for (; q + 1 < qe; q += 2) {
+      const double x0 = bp_xt<DT>(T.x, q * P + p), x1 = bp_xt<DT>(T.x, (q + 1) * P + p);
+      const double* ws0 = T.Wss + q * r;
+      const double* we0 = T.Wes + q * r;
+      double ls0 = 0.0, le0 = 0.0, ls1 = 0.0, le1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < R; ++kk) {
+        if (EX || kk < r) {
+          if (HS) {
+            ls0 = fma(as[kk], ws0[kk], ls0);
+            ls1 = fma(as[kk], ws0[r + kk], ls1);
+          }
+          if (HE) {
+            le0 = fma(ae[kk], we0[kk], le0);
+            le1 = fma(ae[kk], we0[r + kk], le1);
+          }
+        }
+      }
+      bp_entry<HS, HE, WM, EXP>(T, x0, ls0, le0, pos, q, p, e2, x2, bad);
+      bp_entry<HS, HE, WM, EXP>(T, x1, ls1, le1, pos, q + 1, p, e2, x2, bad);
+    }
+    if (q < qe) {
       const double x = bp_xt<DT>(T.x, q * P + p);
       const double* wsr = T.Wss + q * r;
       const double* wer = T.Wes + q * r;
@@ -451,8 +475,8 @@ __global__ void __launch_bounds__(512, 1) k_block_pass(Geom g, TileMap tm, Index
     }
     const unsigned char* sb = stage0 + (size_t)st * stage_bytes;
     const i64 e0 = q0 * P;
-    const int xskip = (int)((((bd.off + e0) * esz) & 15) / esz);
-    const int wskip = (int)((((bd.w_off + q0 * r) * 8) & 15) / 8);
+    const int xskip = (int)((((bd.off + e0) * esz) & 15) >> (esz == 8 ? 3 : 2));
+    const int wskip = (int)((bd.w_off + q0 * r) & 1);
     BPTile T;
     T.x = sb + (size_t)xskip * esz;
     T.dtype = a.dtype;
