@@ -353,7 +353,7 @@ __device__ __forceinline__ void bp_tile_r(const BPTile& T, bool cols, double& e2
 // combined by the last CTA in CTA order (deterministic: the tile -> CTA
 // assignment is static).  GP: the G pass over the core block's tiles only.
 template <bool HS, bool HE, bool WM, bool EXP, bool GP, int RB, bool AP>
-__global__ void __launch_bounds__(512, 1) k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeom G) {
+__global__ void __launch_bounds__(AP ? 512 : 256, AP ? 1 : BP_MIN_CTAS) k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeom G) {
   extern __shared__ __align__(128) unsigned char bp_smem[];
   __shared__ unsigned long long bars[4];
   __shared__ double red[16];

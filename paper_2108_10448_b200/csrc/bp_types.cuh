@@ -11,6 +11,10 @@
 #define TILE_MAX_ELEMS 4096
 #define BP_X_BYTES 34816     // x bytes per block-pass stage (whole columns)
 #define BP_W_DOUBLES 2048    // W doubles per stage and state
+#ifndef BP_MIN_CTAS
+#define BP_MIN_CTAS 2        // block-pass CTAs per SM (256 threads); 3 measured slower (smaller tiles)
+#endif
+#define BP_CTA_SMEM (113 * 1024)   // shared-memory budget per CTA (two per SM)
 
 struct TileMap {
   int nblk;

@@ -266,9 +266,9 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
       // three stages when two CTAs per SM still fit (with the G pass's partials), else two
       BPGeom gg = G;
       gg.gp_doubles = 256 * P.rmax;
-      if (bp_smem_bytes(gg) + 1024 > 113 * 1024) G.stages = 2;
+      if (bp_smem_bytes(gg) + 1024 > BP_CTA_SMEM) G.stages = 2;
       gg.stages = G.stages;
-      if (bp_smem_bytes(gg) + 1024 <= 113 * 1024 || xb <= std::max<i64>(4096, maxP * P.esize)) break;
+      if (bp_smem_bytes(gg) + 1024 <= BP_CTA_SMEM || xb <= std::max<i64>(4096, maxP * P.esize)) break;
     }
     // G pass: its own map over the core block only, lanes over columns (32 * 2^k
     // columns within BP_X_BYTES) with the staged A/U rows and partials; cols = 0
@@ -297,7 +297,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
       Gg.w_doubles = (int)((cpt * rc + 4 + 1) & ~1);
       Gg.a_doubles = (int)((Pc * ((rc + 1) & ~1) + 1) & ~1);
       Gg.gp_doubles = 256 * rc;
-      Gg.stages = bp_smem_bytes(BPGeom{3, Gg.x_bytes, Gg.w_doubles, 16, Gg.gp_doubles, Gg.a_doubles}) + 1024 <= 113 * 1024
+      Gg.stages = bp_smem_bytes(BPGeom{3, Gg.x_bytes, Gg.w_doubles, 16, Gg.gp_doubles, Gg.a_doubles}) + 1024 <= BP_CTA_SMEM
                       ? 3
                       : 2;
     }
@@ -310,10 +310,10 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
       for (int b = 1; b < g.nblk; ++b) Ga.gp_doubles = (int)std::max<i64>(Ga.gp_doubles, g.blk[b].P * g.blk[b].r);
       Ga.gp_doubles = (Ga.gp_doubles + 1) & ~1;
       Ga.stages = 3;
-      if (bp_smem_bytes(Ga) + 1024 > 113 * 1024) Ga.stages = 2;
+      if (bp_smem_bytes(Ga) + 1024 > BP_CTA_SMEM) Ga.stages = 2;
       const i64 nt = tm.first[g.nblk] - tm.first[1];
       // two 256-thread CTAs per SM when they fit, else one 512-thread CTA (16 warps either way)
-      P.ap_threads = bp_smem_bytes(Ga) + 1024 <= 113 * 1024 ? 256 : 512;
+      P.ap_threads = bp_smem_bytes(Ga) + 1024 <= BP_CTA_SMEM ? 256 : 512;
       P.ap_grid = (int)std::max<i64>(1, std::min<i64>(P.ap_threads == 256 ? 296 : 148, nt));
     }
   }
