@@ -56,6 +56,25 @@ def release_engine(eng):
             _POOL.setdefault(key, []).append(eng)
 
 
+def _parallel_copy(dst, src, parts=8):
+    """dst[:] = src with a few threads (numpy releases the GIL for large copies)."""
+    n = dst.size
+    if n < (1 << 20):
+        dst[:] = src
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    bounds = [n * i // parts for i in range(parts + 1)]
+    global _COPY_POOL
+    if _COPY_POOL is None:
+        _COPY_POOL = ThreadPoolExecutor(max_workers=parts)
+    list(_COPY_POOL.map(lambda i: np.copyto(dst[bounds[i]:bounds[i + 1]], src[bounds[i]:bounds[i + 1]]),
+                        range(parts)))
+
+
+_COPY_POOL = None
+
+
 class Engine:
     def __init__(self, shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=None):
         import torch
@@ -208,6 +227,30 @@ class Engine:
                 for w in (want_s, want_clean, want_l)]
         ptr = [ctypes.c_void_p(o.data_ptr()) if o is not None else ctypes.c_void_p() for o in outs]
         nat.check(self.lib.rtcur_engine_export_blocks(self.handle, *ptr))
+        return outs
+
+    def to_host(self, dev_tensors):
+        """Copy fp64 device vectors into fresh host numpy arrays: D2H through a
+        pinned staging buffer kept by the engine (full PCIe rate), then a
+        multi-threaded host copy into memory the caller owns."""
+        import torch
+
+        total = sum(int(t.numel()) for t in dev_tensors)
+        st = getattr(self, "_pin_stage", None)
+        if st is None or st.numel() < total:
+            st = self._pin_stage = torch.empty(total, dtype=torch.float64, pin_memory=True)
+        o = 0
+        for t in dev_tensors:
+            st[o:o + t.numel()].copy_(t, non_blocking=True)
+            o += t.numel()
+        torch.cuda.current_stream(self.device).synchronize()
+        stage = st.numpy()
+        outs, o = [], 0
+        for t in dev_tensors:
+            a = np.empty(int(t.numel()), dtype=np.float64)
+            _parallel_copy(a, stage[o:o + a.size])
+            outs.append(a)
+            o += a.size
         return outs
 
     def export_cur(self):

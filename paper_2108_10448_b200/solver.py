@@ -309,7 +309,7 @@ def _make_result(eng: Engine, src: _Source, idx, cfg, history, flags, timings, z
     def blocks():
         if "blocks" not in holder:
             s_dev, c_dev, _ = eng.export_blocks(True, True, False)
-            holder["blocks"] = (s_dev.cpu().numpy(), c_dev.cpu().numpy())
+            holder["blocks"] = tuple(eng.to_host([s_dev, c_dev]))
         return holder["blocks"]
 
     def cur_parts():
