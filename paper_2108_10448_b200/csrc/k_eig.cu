@@ -213,18 +213,38 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
                              const int* rows, i64 d, int max_steps) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   double* rinv = Rm;   // r reciprocal pivots
-  // trace of K and the warm start
-  double t = 0.0;
+  // trace and squared Frobenius norm of K, and the warm start
+  double t = 0.0, f2 = 0.0;
   for (int i = tid; i < s; i += blockDim.x) t += eig_kval(A, full, ld, i, i);
+  if (full) {
+    for (int e = tid; e < s * s; e += blockDim.x) {
+      const double v = A[(e / s) * ld + (e % s)];
+      f2 = fma(v, v, f2);
+    }
+  } else {
+    for (int e = tid; e < s * (s + 1) / 2; e += blockDim.x) {
+      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      while (i * (i + 1) / 2 > e) --i;
+      const double v = A[e];
+      f2 = fma(v, v * (e - i * (i + 1) / 2 == i ? 1.0 : 2.0), f2);
+    }
+  }
   t = warp_sum(t);
-  if (lane == 0) red[wid] = t;
+  f2 = warp_sum(f2);
+  if (lane == 0) {
+    red[wid] = t;
+    red2[wid] = f2;
+  }
   for (int e = tid; e < s * r; e += blockDim.x) {
     const int i = e % s, c = e / s;
     X[e] = warmA[rows[i] + (i64)c * d];
   }
   __syncthreads();
   const double trK = warp_sum_of(red, nw);
+  const double kf2 = warp_sum_of(red2, nw);
   if (!(trK > 0.0)) return false;
+  __syncthreads();
   for (int rep = 0; rep < 2; ++rep)
     if (!eig_cholqr(X, s, r, C, rinv, scal)) return false;
   const int nch = (r + 3) >> 2;   // 4-column chunks
@@ -287,33 +307,59 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
       if (lane == 0) { H[a + b * r] = hv; H[b + a * r] = hv; }
     }
     __syncthreads();
-    // residual ||Y - X H||_F^2 and tr H
-    double rn = 0.0;
+    // residual ||Y - X H||_F^2 and ||Y||_F^2
+    double rn = 0.0, yn = 0.0;
     for (int e = tid; e < s * r; e += blockDim.x) {
       const int i = e % s, c = e / s;
-      double v = Y[e];
+      const double y = Y[e];
+      double v = y;
       for (int k = 0; k < r; ++k) v -= X[k * s + i] * H[k + c * r];
       rn = fma(v, v, rn);
+      yn = fma(y, y, yn);
     }
     rn = warp_sum(rn);
-    if (lane == 0) red2[wid] = rn;
+    yn = warp_sum(yn);
+    if (lane == 0) {
+      red2[wid] = rn;
+      red[wid] = yn;
+    }
     __syncthreads();
     const double res = sqrt(warp_sum_of(red2, nw));
-    // stagnation: the residual must at least halve every two steps, else the
-    // gap is too small for this path (the full solver is cheaper than waiting)
-    if (step >= 4 && !(res <= 0.5 * scal[12 + (step & 1)])) return false;
+    const double yf2 = warp_sum_of(red, nw);
+    // forecast: from the two-step decay rate of the residual, give up (full solver)
+    // when more than ~10 further steps would be needed to reach the certification
+    // level (the full path costs about that much)
+    if (step >= 3) {
+      const double prev2 = scal[12 + (step & 1)];
+      const double rho2 = res / prev2;   // per two steps
+      bool hopeless = !(rho2 < 0.5);
+      if (!hopeless) {
+        const double target = 1e-13 * trK;   // certification needs res ~ 1e-12 * gap
+        if (res > target) hopeless = 0.5 * log(target / res) / log(rho2) > 10.0;
+      }
+      if (hopeless) return false;
+    }
     __syncthreads();
     if (tid == 0) scal[12 + (step & 1)] = res;
     if (tid == 0) scal[14] = (double)(step + 1);
-    double trH = 0.0;
+    double trH = 0.0, hf2 = 0.0;
     for (int c = 0; c < r; ++c) trH += H[c + c * r];
-    // lambda_min(H) <= tr H / r: if even that cannot exceed the energy outside the
-    // subspace, the gap bound can never certify -> give up at once (full solver)
-    if (!(trH / r - (trK - trH) > 0.0)) return false;
-    // certify: lambda_min(H) > mu = (tr K - tr H) + 1e12 res  <=>  H - mu I is positive
-    // definite (one warp Cholesky of the shifted copy; no eigen-solve needed)
+    for (int e = 0; e < r * r; ++e) hf2 = fma(H[e], H[e], hf2);
+    // Rigorous upper bound u >= lambda_{r+1}(K): Courant-Fischer with V = span X gives
+    // lambda_{r+1} <= lambda_max((I-P)K(I-P)) <= ||(I-P)K(I-P)||_F, and
+    // ||(I-P)K(I-P)||_F^2 = ||K||_F^2 - 2||KX||_F^2 + ||X^T K X||_F^2 (X orthonormal),
+    // plus a rounding margin for the three fixed-order sums; for PSD K also
+    // lambda_{r+1} <= tr K - tr H.  Take the smaller.
+    const double fro = sqrt(fmax(kf2 - 2.0 * yf2 + hf2, 0.0) + 4.0 * (double)s * s * DBL_EPSILON * kf2);
+    const double ub = fmin(trK - trH, fro);
+    // lambda_min(H) <= tr H / r: if even that cannot exceed the bound, certification
+    // is impossible from this subspace -> give up at once (full solver)
+    if (!(trH / r - ub > 0.0)) return false;
+    // certify: lambda_min(H) > mu = ub + 1e12 res  <=>  H - mu I is positive definite
+    // (one warp Cholesky of the shifted copy; no eigen-solve needed); then the
+    // subspace angle is <= res / (lambda_min(H) - ub) <= 1e-12 (Davis-Kahan)
     if (res <= 1e-9 * trK) {
-      const double mu = (trK - trH) + 1e12 * res;
+      const double mu = ub + 1e12 * res;
       double* Hs = C;   // scratch (C is re-formed by the next Cholesky-QR)
       for (int e = tid; e < r * r; e += blockDim.x) Hs[e] = H[e] - ((e % r == e / r) ? mu : 0.0);
       __syncthreads();
