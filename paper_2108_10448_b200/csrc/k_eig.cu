@@ -327,15 +327,17 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
     const double res = sqrt(warp_sum_of(red2, nw));
     const double yf2 = warp_sum_of(red, nw);
     // forecast: from the two-step decay rate of the residual, give up (full solver)
-    // when more than ~10 further steps would be needed to reach the certification
-    // level (the full path costs about that much)
+    // when more further steps would be needed to reach the certification level than
+    // the full path costs
     if (step >= 3) {
       const double prev2 = scal[12 + (step & 1)];
       const double rho2 = res / prev2;   // per two steps
       bool hopeless = !(rho2 < 0.5);
       if (!hopeless) {
         const double target = 1e-13 * trK;   // certification needs res ~ 1e-12 * gap
-        if (res > target) hopeless = 0.5 * log(target / res) / log(rho2) > 10.0;
+        // the full path's cost grows with s: allow ~s/8 more steps (4..10)
+        const double budget = fmin(10.0, fmax(4.0, s / 8.0));
+        if (res > target) hopeless = 0.5 * log(target / res) / log(rho2) > budget;
       }
       if (hopeless) return false;
     }
