@@ -205,6 +205,42 @@ def _ncu_traffic(config: int, phase: str):
     return d.get(f"config{config}", {}).get(phase)
 
 
+def _full_tensor_rooflines(res, x_dev, bc, phases, peak, steps):
+    """K3 (k_full: full L, S = HT(X - L, zeta_final) and the residual sums,
+    cli.py:237-243) and K0 (k_absmax, solver.py:184-192) against the HBM peak.
+    K3 runs `steps` times on the solved iterate with CUDA events on the engine's
+    stream around the kernel (the Tf contraction it needs is a separate ~us
+    launch); algorithmic bytes 3*E*N_local (read X, write L and S), K0 E*N_local."""
+    import torch
+    from paper_2108_10448_b200.full import full_output
+
+    eng = res.cur._engine
+    E = 8 if bc.dtype == "f64" else 4
+    n_loc = int(x_dev.flat.numel())
+    full_output(res, x_dev)   # warm (allocator, Tf scratch)
+    torch.cuda.synchronize()
+    eng.profile(True, ["full"])
+    eng.profile_read(reset=True)
+    rel = None
+    for _ in range(max(1, steps)):
+        _, _, rel = full_output(res, x_dev)
+    ph = eng.profile_read(reset=True)
+    eng.profile(False)
+    ms, n = ph["full"]
+    k3_us = 1e3 * ms / max(n, 1)
+    k3_bytes = 3 * E * n_loc
+    out = {"k3_full": {"bound": "hbm", "kernel": "k_full", "alg_bytes_per_launch": k3_bytes,
+                       "launch_us": k3_us, "launches_timed": int(n),
+                       "achieved": k3_bytes / (k3_us * 1e-6) / 1e9, "peak": peak, "unit": "GB/s",
+                       "frac": k3_bytes / (k3_us * 1e-6) / 1e9 / peak, "full_relative_residual": rel}}
+    if "absmax" in phases:
+        k0_us = 1e3 * phases["absmax"]["ms_per_step"] / max(phases["absmax"]["launches_per_step"], 1)
+        out["k0_absmax"] = {"bound": "hbm", "kernel": "k_absmax", "alg_bytes_per_launch": E * n_loc,
+                            "launch_us": k0_us, "achieved": E * n_loc / (k0_us * 1e-6) / 1e9, "peak": peak,
+                            "unit": "GB/s", "frac": E * n_loc / (k0_us * 1e-6) / 1e9 / peak}
+    return out
+
+
 def _sharded(config: int) -> bool:
     """BASELINE shards configs 2 and 4 in mode-1 slabs; the others run replicas."""
     return config in (2, 4)
@@ -297,6 +333,7 @@ def run_b200(args):
         dom_ms += res.timings["device_ms"][dom]
         dom_n += res.timings["device_launches"][dom]
     ev1.record()
+    res_dev = res
     torch.cuda.synchronize()
     barrier()
     launches = _native.launch_count() - l0
@@ -358,6 +395,8 @@ def run_b200(args):
             "peak_source": peak_src,
             "share_of_device_time": phases[dom]["share"] if dom in phases else None}
 
+    full_roof = _full_tensor_rooflines(res_dev, x_dev, bc, phases, peak, args.steps)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if xf is not None:
@@ -378,7 +417,7 @@ def run_b200(args):
             "converged": bool(conv), "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": int(host.numel() * host.element_size()),
                     "d2h_bytes_per_step": int(d2h), "sec_per_solve": e2e_s / e2e_steps},
-            "roofline": roof, "phases": phases,
+            "roofline": roof, "full_tensor_rooflines": full_roof, "phases": phases,
             "phases_note": f"per-phase CUDA-event times from a separate profiled pass of {bd_steps} solve(s); "
                            "the timed region carries events on the dominant phase only",
             "clocks": clk, "cpu_baseline": cpu,
