@@ -1405,7 +1405,7 @@ extern "C" int64_t rtcur_engine_full_scratch_bytes(rtcur_engine* e) {
   if (!e) return 0;
   i64 q = 1;
   for (int m = 1; m < e->P.g.n; ++m) q *= e->P.g.dim[m];
-  return q * e->P.g.rank[0] * 8;
+  return q * e->P.g.rank[0] * 8 + 16;   // +16: k_full_tma reads Tf rows in 16-byte units
 }
 
 extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_dev, void* S_dev, double* tf_dev,
@@ -1446,8 +1446,12 @@ extern "C" int rtcur_engine_full_output(rtcur_engine* e, double zeta, void* L_de
   fa.counter = e->at<unsigned int>(P.o_counters) + 32;
   const int grid = 148 * 8;
   prof_begin(e, PH_FULL);
-  if (P.dtype == 0) k_full<double><<<grid, 256, 0, e->st>>>(fa);
-  else k_full<float><<<grid, 256, 0, e->st>>>(fa);
+  const int tma = full_tma_launch(fa, grid, e->st);
+  if (tma < 0) return fail(RT_ERR_CUDA, std::string("k_full_tma: ") + cudaGetErrorString((cudaError_t)(-tma)));
+  if (tma == 0) {
+    if (P.dtype == 0) k_full<double><<<grid, 256, 0, e->st>>>(fa);
+    else k_full<float><<<grid, 256, 0, e->st>>>(fa);
+  }
   LAUNCH_CHECK();
   prof_end(e, PH_FULL);
   CK(cudaMemcpyAsync(e->h_pinned, fa.sums, 16, cudaMemcpyDeviceToHost, e->st));

@@ -6,24 +6,8 @@
 // Tf = G x_{m>=2} A_m (one fp64 row of r_1 values per mode-1 fiber), so each
 // element costs r_1 FMAs and the kernel streams X once and writes L and S once
 // (3 E bytes per element).  Works on a mode-1 slab [lo, hi) of a sharded X.
-#include "common.cuh"
+#include "full_types.cuh"
 
-struct FullArgs {
-  const void* X;        // local slab, (hi-lo) x d_2 x ... mode-1 fastest
-  int dtype;
-  i64 lo, hi;           // mode-1 slab
-  i64 ncols;            // prod_{m>=2} d_m
-  const double* A1;     // d_1 x r_1 col-major (state)
-  i64 d1;
-  int r1;
-  const double* Tf;     // ncols x r_1 row-major
-  double zeta;
-  void* L;              // optional outputs (dtype), same layout as X
-  void* S;
-  double* partial;      // [grid][2]
-  double* sums;         // [2]: sum (x-L-S)^2, sum x^2
-  unsigned int* counter;
-};
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_full(FullArgs a) {
