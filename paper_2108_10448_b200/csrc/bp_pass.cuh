@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(AP ? 512 : 256, AP ? 1 : BP_MIN_CTAS) k_block_
   __threadfence();
   // last CTA: per-block sums over CTAs in CTA order (deterministic)
   for (int bb = 0; bb < tm.nblk; ++bb) {
+    if (tm.first[bb + 1] == tm.first[bb]) continue;   // block handled by the fiber pass (k_fiber.cuh)
     double se = 0.0, sx = 0.0;
     for (i64 c = tid; c < gridDim.x; c += blockDim.x) {
       se += ((volatile double*)a.partial)[(c * tm.nblk + bb) * 2];

@@ -29,6 +29,7 @@
 #include "k_svdpost.cu"
 #include "k_factors.cu"
 #include "k_full.cu"
+#include "fiber_types.cuh"
 #include "../../include/rtcur_b200.h"
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -105,6 +106,10 @@ struct Plan {
   Geom g;
   TileMap tm;
   TileMap tm_gp;   // G pass: the core block's tiles (lanes over columns when possible)
+  TileMap tm_core; // threshold/error passes on k_block_pass: the blocks the fiber pass does not take
+  unsigned fiber_mask;   // blocks handled by the TMA fiber pass (k_fiber.cuh)
+  i64 xi_off[RT_MAX_MODES], xi_ld[RT_MAX_MODES];   // intersection copies (elements) inside o_xi
+  i64 o_xi;
   int dtype;
   int esize;
   int rmax, rb;
@@ -318,6 +323,20 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     }
   }
 
+  // fiber blocks on the TMA fiber pass; k_block_pass keeps the core (and any block outside its envelope)
+  P.fiber_mask = fiber_pass_blocks(g, dtype);
+  {
+    TileMap& tc = P.tm_core;
+    tc = P.tm;
+    i64 t = 0;
+    for (int b = 0; b < g.nblk; ++b) {
+      const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
+      tc.first[b] = t;
+      if (!(P.fiber_mask >> b & 1)) t += nt;
+    }
+    tc.first[g.nblk] = t;
+  }
+
   P.col_off[0] = 0;
   for (int b = 0; b < g.nblk; ++b) P.col_off[b + 1] = P.col_off[b] + g.blk[b].Q;
   // gram / svd sizing
@@ -404,6 +423,17 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_coli1 = take(P.col_off[g.nblk] * 4);
   P.o_coloff = take((RT_MAX_BLOCKS + 1) * 8);
   P.o_xb = take(g.nblk_total * P.esize + 64);   // +64: aligned bulk-copy supersets may read past the end
+  {
+    // intersection copies X(I_k, J_k) of the fiber blocks for the fiber pass's threshold
+    const i64 va = 16 / P.esize;
+    i64 xo = 0;
+    for (int m = 0; m < n; ++m) {
+      P.xi_ld[m] = (row_sizes[m] + va - 1) / va * va;
+      P.xi_off[m] = xo;
+      xo += (P.xi_ld[m] * col_sizes[m] + va - 1) / va * va;
+    }
+    P.o_xi = take(P.fiber_mask ? xo * P.esize + 64 : 8);
+  }
   P.samp_delta = o - samp0;
   take(P.samp_delta - 8);   // slot 1 (aligned like slot 0)
   P.o_state = take(3 * g.state_doubles * 8);
@@ -502,6 +532,7 @@ struct rtcur_engine {
   std::map<unsigned long long, GraphEntry>* graphs;
   GraphEntry* cap_entry;
   const double* zetap_cur;         // device zeta while an iteration body is enqueued/captured
+  bool xi_valid[2];                // the sample slot's intersection copies match its blocks
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
   i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
@@ -859,6 +890,7 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
   prof_end(e, PH_PREP);
   e->sampled = true;
   e->stg = slot;
+  e->xi_valid[slot] = false;
   return RT_OK;
 }
 
@@ -868,8 +900,11 @@ extern "C" int rtcur_engine_xblocks_offset(rtcur_engine* e, int64_t* offset) {
   if (!e || !offset) return fail(RT_ERR_VALUE, "null argument");
   const int slot = e->stg >= 0 ? e->stg : e->act_slot();
   *offset = e->P.o_xb + e->sd(slot);
+  e->xi_valid[slot] = false;   // the caller writes the blocks: the intersection copies are refreshed before use
   return RT_OK;
 }
+
+static int refresh_xi(rtcur_engine* e, int slot);
 
 extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
@@ -883,6 +918,8 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   k_gather<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, e->X, P.dtype, e->lo, e->hi,
                                                               e->xb(slot), mc);
   LAUNCH_CHECK();
+  e->xi_valid[slot] = false;
+  if (int st = refresh_xi(e, slot)) return st;
   prof_end(e, PH_GATHER);
   return RT_OK;
 }
@@ -906,6 +943,35 @@ static int launch_ap(K kern, int grid, int threads, i64 smb, cudaStream_t st, co
                      const IndexPtrs& ip, const PassArgs& a, const BPGeom& G) {
   kern<<<grid, threads, smb, st>>>(g, tm, ip, a, G);
   LAUNCH_CHECK();
+  return RT_OK;
+}
+
+// fiber-pass launch description for a sample slot (k_fiber.cuh)
+static FiberLaunch make_fl(const rtcur_engine* e, int slot) {
+  const Plan& P = e->P;
+  FiberLaunch fl;
+  memset(&fl, 0, sizeof(fl));
+  fl.g = P.g;
+  fl.xb = e->xb(slot);
+  fl.dtype = P.dtype;
+  fl.xi = e->ws + P.o_xi + e->sd(slot);
+  const IndexPtrs ip = make_ip_slot(e, slot);
+  for (int m = 0; m < P.g.n; ++m) {
+    fl.xi_off[m] = P.xi_off[m];
+    fl.xi_ld[m] = P.xi_ld[m];
+    fl.rows[m] = ip.rows[m];
+    fl.rowpos[m] = ip.rowpos[m];
+  }
+  return fl;
+}
+
+// intersection copies of a sample slot, refreshed when its blocks changed
+static int refresh_xi(rtcur_engine* e, int slot) {
+  if (!e->P.fiber_mask || e->xi_valid[slot]) return RT_OK;
+  const int st = fiber_xi_extract(make_fl(e, slot), e->st);
+  if (st < 0) return fail(RT_ERR_CUDA, std::string("k_xi_extract: ") + cudaGetErrorString((cudaError_t)(-st)));
+  LAUNCH_CHECK();
+  e->xi_valid[slot] = true;
   return RT_OK;
 }
 
@@ -935,15 +1001,18 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   prof_begin(e, phase);
   const i64 smb = bp_smem_bytes(P.bp);
   const bool hs = st_s != nullptr, he = st_e != nullptr;
+  // the fiber blocks of the threshold / error passes go to the TMA fiber pass; exports stay here
+  const bool split = P.fiber_mask && !(s_out || c_out || l_out) && (with_M || sums);
+  const TileMap& tmk = split ? P.tm_core : P.tm;
 #define BP_LAUNCH(HS, HE, WM, EXP)                                                                        \
-  (P.rb == 4    ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 4, false>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
+  (P.rb == 4    ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 4, false>, tmk.first[P.g.nblk], smb, e->st, P.g, tmk,  \
                             ip, a, P.bp)                                                                          \
-   : P.rb == 8  ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 8, false>, P.tm.first[P.g.nblk], smb, e->st, P.g, P.tm,  \
+   : P.rb == 8  ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 8, false>, tmk.first[P.g.nblk], smb, e->st, P.g, tmk,  \
                             ip, a, P.bp)                                                                          \
-   : P.rb == 16 ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 16, false>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
-                            P.tm, ip, a, P.bp)                                                                    \
-                : launch_bp(k_block_pass<HS, HE, WM, EXP, false, 32, false>, P.tm.first[P.g.nblk], smb, e->st, P.g,      \
-                            P.tm, ip, a, P.bp))
+   : P.rb == 16 ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 16, false>, tmk.first[P.g.nblk], smb, e->st, P.g,      \
+                            tmk, ip, a, P.bp)                                                                    \
+                : launch_bp(k_block_pass<HS, HE, WM, EXP, false, 32, false>, tmk.first[P.g.nblk], smb, e->st, P.g,      \
+                            tmk, ip, a, P.bp))
   int lst;
   if (s_out || c_out || l_out) {
     if (hs && he) lst = BP_LAUNCH(true, true, false, true);
@@ -959,7 +1028,21 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   }
 #undef BP_LAUNCH
   if (lst) return lst;
-  LAUNCH_CHECK();
+  if (split) {
+    FiberLaunch fl = make_fl(e, e->act_slot());
+    fl.st_s = st_s;
+    fl.st_e = st_e;
+    fl.zeta = zeta;
+    fl.zetap = a.zetap;
+    for (int m = 0; m < P.g.n; ++m) fl.M[m] = a.M[m];
+    fl.partial = a.partial;
+    fl.sums = a.sums;
+    fl.counter = a.counter;
+    fl.nonfinite = a.nonfinite;
+    const int fst = fiber_pass_launch(fl, e->st);
+    if (fst < 0) return fail(RT_ERR_CUDA, std::string("k_fiber_pass: ") + cudaGetErrorString((cudaError_t)(-fst)));
+    LAUNCH_CHECK();
+  }
   prof_end(e, phase);
   return RT_OK;
 }
@@ -1268,6 +1351,7 @@ static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool r
   // RTCUR-R: the sample moved, re-evaluate the previous iterate on it
   // (reference solver.py:330-331, _eval_blocks(lcur, idx) on the new draw)
   if (reeval && (st = run_wcols(e, e->state(e->cur)))) return st;
+  if ((st = refresh_xi(e, e->act_slot()))) return st;
   if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false, PH_THRESH))) return st;
   if ((st = run_svd(e, st_s))) return st;
   if ((st = run_factors(e, st_s, zeta, newslot))) return st;
@@ -1282,6 +1366,10 @@ static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool r
 // phases timed inside the iteration body (a graph's event nodes depend only on these)
 static const unsigned kIterPhases = (1u << PH_THRESH) | (1u << PH_GRAM) | (1u << PH_EIG) | (1u << PH_SVDPOST) |
                                     (1u << PH_APASS) | (1u << PH_GPASS) | (1u << PH_WCOLS) | (1u << PH_ERROR);
+
+static inline bool fiber_refresh_pending(const rtcur_engine* e) {
+  return e->P.fiber_mask && !e->xi_valid[e->act_slot()];
+}
 
 extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first) {
   if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
@@ -1304,6 +1392,7 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   if (e->use_graphs) {
     const unsigned long long key = (unsigned long long)(e->cur + 1) | ((unsigned long long)newslot << 2) |
                                    ((unsigned long long)e->act_slot() << 4) | ((unsigned long long)reeval << 5) |
+                                   ((unsigned long long)fiber_refresh_pending(e) << 6) |
                                    ((unsigned long long)(e->prof_on ? (e->prof_mask & kIterPhases) : 0u) << 8);
     auto it = e->graphs->find(key);
     if (it == e->graphs->end()) {
