@@ -194,15 +194,14 @@ __device__ bool eig_cholqr(double* X, int s, int r, double* C, double* rinv, dou
   }
   __syncthreads();
   if (!eig_chol_warp(C, r, rinv, 1e-28 * C[0], scal)) return false;
-  // rows: y L^T = x  (forward substitution, reciprocal pivots)
+  // rows: y L^T = x  (forward substitution, reciprocal pivots), in place column by
+  // column: entries k < j of the thread's row are already the solved ones
   for (int i = tid; i < s; i += blockDim.x) {
-    double xr[RT_MAX_RANK];
     for (int j = 0; j < r; ++j) {
       double v = X[j * s + i];
-      for (int k = 0; k < j; ++k) v = fma(-xr[k], C[j + k * r], v);
-      xr[j] = v * rinv[j];
+      for (int k = 0; k < j; ++k) v = fma(-X[k * s + i], C[j + k * r], v);
+      X[j * s + i] = v * rinv[j];
     }
-    for (int j = 0; j < r; ++j) X[j * s + i] = xr[j];
   }
   __syncthreads();
   return true;
@@ -210,8 +209,9 @@ __device__ bool eig_cholqr(double* X, int s, int r, double* C, double* rinv, dou
 
 __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, double* X, double* Y, double* H,
                              double* C, double* Rm, double* red, double* red2, double* scal, const double* warmA,
-                             const int* rows, i64 d, int max_steps) {
+                             const int* rows, i64 d, int max_steps, long long* tmk) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+#define TMK(j) if (tmk && tid == 0 && step == 1) tmk[j] = clock64();
   double* rinv = Rm;   // r reciprocal pivots
   // trace and squared Frobenius norm of K, and the warm start
   double t = 0.0, f2 = 0.0;
@@ -249,6 +249,7 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
     if (!eig_cholqr(X, s, r, C, rinv, scal)) return false;
   const int nch = (r + 3) >> 2;   // 4-column chunks
   for (int step = 0; step < max_steps; ++step) {
+    TMK(2)
     // Y = K X: item (row i, 4-column chunk), each K element read once per chunk
     for (int it = tid; it < s * nch; it += blockDim.x) {
       const int ch = it / s, i = it - ch * s;
@@ -292,6 +293,7 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
       if (h3) y0[3 * s] = a3;
     }
     __syncthreads();
+    TMK(3)
     // H = X^T Y (symmetrised)
     const int np = r * (r + 1) / 2;
     for (int q = wid; q < np; q += nw) {
@@ -342,6 +344,7 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
       if (hopeless) return false;
     }
     __syncthreads();
+    TMK(4)
     if (tid == 0) scal[12 + (step & 1)] = res;
     if (tid == 0) scal[14] = (double)(step + 1);
     double trH = 0.0, hf2 = 0.0;
@@ -368,18 +371,20 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
       if (eig_chol_warp(Hs, r, rinv, 0.0, scal)) return true;
     }
     if (step + 1 == max_steps) break;
+    TMK(5)
     // X <- orth(Y)
     for (int e = tid; e < s * r; e += blockDim.x) X[e] = Y[e];
     __syncthreads();
     for (int rep = 0; rep < 2; ++rep)
       if (!eig_cholqr(X, s, r, C, rinv, scal)) return false;
+    TMK(6)
   }
   return false;
 }
 
 extern __shared__ double eig_smem[];
 
-__global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
+__global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   const int mi = blockIdx.x;
   if (mi >= ea.n) return;
   const int s = ea.s[mi], r = ea.r[mi], nb = ea.nb[mi];
@@ -433,12 +438,12 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(EigArgs ea) {
   // ---------------------------------------------------------------- 0. warm-started subspace iteration
   if (ea.warmA[mi] != nullptr) {
     const bool ok = eig_subspace(A, full, ld, s, r, E, Ysub, Hs, Cs, Rs, red, red2, scal, ea.warmA[mi],
-                                 ea.warm_rows[mi], ea.warm_d[mi], ea.max_sub_steps);
+                                 ea.warm_rows[mi], ea.warm_d[mi], ea.max_sub_steps, tm);
     if (ok) {
       if (tid == 0 && ea.fast_used) ea.fast_used[mi] = (int)scal[14];   // subspace steps taken (>= 1)
       for (int e = tid; e < s * r; e += blockDim.x) ea.E[mi][e] = E[e];
       for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = 0.0;
-      if (tm && tid == 0) tm[2] = tm[3] = tm[4] = tm[5] = clock64();
+      if (tm && tid == 0) tm[7] = clock64();
       return;
     }
   }

@@ -1,4 +1,6 @@
-"""Diagnostic: which eigensolver path (warm subspace vs full) each mode takes per iteration."""
+"""Diagnostic: which eigensolver path (warm subspace vs full) each mode takes per iteration, with the
+clock64 marks of k_eig (full path: load, tridiagonalise, multisection, inverse iteration, back-transform;
+warm path: load, setup + step 0, then step 1 split into K X, H + residual, certification, orthonormalisation)."""
 import ctypes, sys
 import numpy as np
 import torch
@@ -43,7 +45,7 @@ for k in range(1, 40):
     marks = np.frombuffer(buf, dtype=np.int64)
     m8 = marks[:8 * 8].reshape(8, 8)[:n]
     fast = marks[8 * 8:8 * 8 + n]
-    span = [[round(int(r[j + 1] - r[j]) / clk, 1) for j in range(5)] for r in m8]
+    span = [[round(int(r[j + 1] - r[j]) / clk, 2) if r[j+1] > 0 and r[j] > 0 else 0 for j in range(7)] for r in m8]
     print(f"it {k:2d} err {err:.3e} fast {[int(f) for f in fast]} eig_us {span}")
     if err <= cfg.eps:
         break
