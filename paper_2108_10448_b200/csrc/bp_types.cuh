@@ -82,6 +82,7 @@ __host__ __device__ inline long long ap_slot(const Geom& g, const TileMap& tm, i
   const long long N = tm.first[tm.nblk] - tm.first[1];
   long long base = 0;
   for (int bb = 1; bb < b; ++bb) {
+    if (tm.first[bb + 1] == tm.first[bb]) continue;   // no tiles (block taken by the fiber pass)
     const long long c0 = ap_cta_of(tm.first[bb] - tm.first[1], N, G);
     const long long c1 = ap_cta_of(tm.first[bb + 1] - 1 - tm.first[1], N, G);
     base += (c1 - c0 + 1) * g.blk[bb].P * g.blk[bb].r;

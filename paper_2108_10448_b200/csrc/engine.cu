@@ -110,6 +110,7 @@ struct Plan {
   unsigned fiber_mask;   // blocks handled by the TMA fiber pass (k_fiber.cuh)
   i64 xi_off[RT_MAX_MODES], xi_ld[RT_MAX_MODES];   // intersection copies (elements) inside o_xi
   i64 o_xi;
+  i64 o_fapart, fapart_cap;   // fiber-pass A-pass partials
   int dtype;
   int esize;
   int rmax, rb;
@@ -462,16 +463,33 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_absmax = take(8);
   {
     // A-pass partials: one P_b x r_b slot per (fiber block, CTA that touches it)
-    const i64 last = ap_slot(P.g, P.tm, P.ap_grid, P.g.nblk - 1,
-                             ap_cta_of(P.tm.first[P.g.nblk] - 1 - P.tm.first[1], P.tm.first[P.g.nblk] - P.tm.first[1],
-                                       P.ap_grid));
-    P.o_apart2 = take((last + P.g.blk[P.g.nblk - 1].P * P.g.blk[P.g.nblk - 1].r) * 8);
+    // (for the full pass map and for the map without the fiber pass's blocks)
+    auto slots = [&](const TileMap& tmx) {
+      const i64 N = tmx.first[P.g.nblk] - tmx.first[1];
+      i64 tot = 0;
+      for (int b = 1; b < P.g.nblk; ++b) {
+        if (N <= 0 || tmx.first[b + 1] == tmx.first[b]) continue;
+        const i64 c0 = ap_cta_of(tmx.first[b] - tmx.first[1], N, P.ap_grid);
+        const i64 c1 = ap_cta_of(tmx.first[b + 1] - 1 - tmx.first[1], N, P.ap_grid);
+        tot += (c1 - c0 + 1) * P.g.blk[b].P * P.g.blk[b].r;
+      }
+      return tot;
+    };
+    P.o_apart2 = take(std::max<i64>(1, std::max(slots(P.tm), slots(P.tm_core))) * 8);
   }
   P.o_gt0 = take(P.g_tmp * 8);
   P.o_gt1 = take(P.g_tmp * 8);
   P.o_wt0 = take(P.w_tmp * 8);
   P.o_wt1 = take(P.w_tmp * 8);
   P.o_bpart = take((i64)BP_GRID * g.nblk * 2 * 8 + 64);
+  {
+    // fiber-pass A pass: one d_k x r_k slot per (fiber block, CTA touching it) -- at most 148 + n slots
+    i64 mx = 1;
+    // (column offsets per CTA x rows <= max(d_k, 352 threads x 4 rows))
+    for (int m = 0; m < n; ++m) mx = std::max<i64>(mx, std::max<i64>(dims[m], 1408) * ranks[m]);
+    P.fapart_cap = P.fiber_mask ? (148 + n) * mx : 1;
+    P.o_fapart = take(P.fapart_cap * 8);
+  }
   P.o_sums = take(2 * g.nblk * 8);
   P.o_fpart = take(148 * 8 * 2 * 8);
   P.o_dbg = take(8 * RT_MAX_MODES * 8);
@@ -1041,7 +1059,7 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
     fl.nonfinite = a.nonfinite;
     const int fst = fiber_pass_launch(fl, e->st);
     if (fst < 0) return fail(RT_ERR_CUDA, std::string("k_fiber_pass: ") + cudaGetErrorString((cudaError_t)(-fst)));
-    LAUNCH_CHECK();
+    rtcur_launch_counter_add((unsigned long long)fst);
   }
   prof_end(e, phase);
   return RT_OK;
@@ -1233,7 +1251,12 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   IndexPtrs ip = make_ip(e);
   double* sto = e->state(dst);
   prof_begin(e, PH_APASS);
-  {
+  // A_k = C_k V_k S_k^+: the fiber pass for its blocks (all of them in the usual case),
+  // the block-pass A pass when some fiber block is outside its envelope
+  unsigned all_fibers = 0;
+  for (int b = 1; b < g.nblk; ++b) all_fibers |= 1u << b;
+  if ((P.fiber_mask & all_fibers) != all_fibers) {
+    const TileMap& tma = P.tm_core;   // the fiber blocks the fiber pass does not take (plus the core, unused)
     // A_k = C_k V_k S_k^+ on the block-pass tiles (fiber blocks), then the fixed-order reduction
     PassArgs pa;
     memset(&pa, 0, sizeof(pa));
@@ -1251,9 +1274,9 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     pa.nonfinite = e->at<int>(P.o_nonfinite);
     const i64 smb = bp_smem_bytes(P.bp_ap);
 #define AP_LAUNCH(RB)                                                                                  \
-  (st_s ? launch_ap(k_block_pass<true, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, P.tm, ip, pa, \
+  (st_s ? launch_ap(k_block_pass<true, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, tma, ip, pa, \
                     P.bp_ap)                                                                             \
-        : launch_ap(k_block_pass<false, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, P.tm, ip, pa, \
+        : launch_ap(k_block_pass<false, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, tma, ip, pa, \
                     P.bp_ap))
     int lst;
     switch (P.rb) {
@@ -1266,8 +1289,26 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     if (lst) return lst;
     i64 maxpr = 1;
     for (int b = 1; b < g.nblk; ++b) maxpr = std::max<i64>(maxpr, g.blk[b].P * g.blk[b].r);
-    k_areduce_bp<<<dim3((unsigned)std::min<i64>(cdiv(maxpr, 256), 1024), g.nblk - 1), 256, 0, e->st>>>(g, P.tm, pa, sto);
+    k_areduce_bp<<<dim3((unsigned)std::min<i64>(cdiv(maxpr, 256), 1024), g.nblk - 1), 256, 0, e->st>>>(g, tma, pa, sto);
     LAUNCH_CHECK();
+  }
+  if (P.fiber_mask) {
+    FiberLaunch fl = make_fl(e, e->act_slot());
+    fl.st_s = st_s;
+    fl.zeta = zeta;
+    fl.zetap = e->zetap_cur;
+    fl.ap = 1;
+    for (int m = 0; m < n; ++m) {
+      fl.Vr[m] = e->at<double>(P.o_V[m]);
+      fl.siginv[m] = e->at<double>(P.o_siginv[m]);
+    }
+    fl.apart = e->at<double>(P.o_fapart);
+    fl.apart_cap = P.fapart_cap;
+    fl.a_out = sto;
+    fl.nonfinite = e->at<int>(P.o_nonfinite);
+    const int fst = fiber_pass_launch(fl, e->st);
+    if (fst < 0) return fail(RT_ERR_CUDA, std::string("k_fiber_pass (A): ") + cudaGetErrorString((cudaError_t)(-fst)));
+    rtcur_launch_counter_add((unsigned long long)fst);
   }
   prof_end(e, PH_APASS);
   prof_begin(e, PH_GPASS);

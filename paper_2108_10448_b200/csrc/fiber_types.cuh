@@ -22,6 +22,13 @@ struct FiberLaunch {
   i64 xi_off[RT_MAX_MODES];   // element offset of mode k's copy (16-byte aligned)
   i64 xi_ld[RT_MAX_MODES];    // its column stride: |I_k| rounded up to 16 bytes
   const int* rows[RT_MAX_MODES];   // I_k (0-based)
+  // A pass (ap != 0): A_k = C_k V_k Sigma_k^+ into a_out (a state), partials in apart
+  int ap;
+  const double* Vr[RT_MAX_MODES];
+  const double* siginv[RT_MAX_MODES];
+  double* apart;
+  i64 apart_cap;                   // doubles available at apart
+  double* a_out;
 };
 
 // Blocks (bit b = block b) the fiber pass handles for this geometry: fiber
@@ -29,9 +36,9 @@ struct FiberLaunch {
 // rank is <= 16.  The rest (always the core) stay on k_block_pass.
 unsigned fiber_pass_blocks(const Geom& g, int dtype);
 
-// Threshold pass (st_e == null: M written, no sums) or error pass (st_e set:
-// sums of the handled blocks) over the handled fiber blocks.  Returns 0 or a
-// negative cudaError_t.
+// Threshold pass (st_e == null: M written, no sums), error pass (st_e set: sums
+// of the handled blocks) or A pass (ap set) over the handled fiber blocks.  Returns the
+// number of kernels launched or a negative cudaError_t.
 int fiber_pass_launch(const FiberLaunch& L, cudaStream_t st);
 
 // Refresh the intersection copies from the compact fiber blocks (after every

@@ -185,7 +185,7 @@ __global__ void k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeo
 // A-pass partials.  One thread per output (consecutive outputs, consecutive partials).
 __global__ void __launch_bounds__(256) k_areduce_bp(Geom g, TileMap tm, PassArgs a, double* __restrict__ st_out) {
   const int b = blockIdx.y + 1;
-  if (b >= g.nblk) return;
+  if (b >= g.nblk || tm.first[b + 1] == tm.first[b]) return;   // (no tiles: the fiber pass writes A_k)
   const BlockDesc& bd = g.blk[b];
   const i64 N = tm.first[tm.nblk] - tm.first[1];
   const i64 G = a.ap_grid;

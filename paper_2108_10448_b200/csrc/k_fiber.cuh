@@ -47,6 +47,8 @@ struct FiberBlk {
   int nbands;
   int H, nchB, cpr, CB;
   int b, mode, r, mrows;
+  i64 pbase;    // A pass: first partial slot of the block (doubles)
+  int c0;       // A pass: first CTA whose tile range touches the block
 };
 
 struct FiberArgs {
@@ -67,6 +69,12 @@ struct FiberArgs {
   int x_region;   // bytes of x per stage
   int w_region;   // bytes of W rows per stage and state
   i64 ntiles;
+  // A pass: A_k = C_k V_k Sigma_k^+ (fiber_cur.py:267, fib @ pinv) -- the clean fiber
+  // entries times the staged V rows, per-(CTA, block) partial rows, reduced in CTA order
+  const double* Vr[RT_MAX_MODES];       // |J_k| x r row-major
+  const double* siginv[RT_MAX_MODES];
+  double* apart;
+  double* a_out;                        // state receiving A_k (d_k x r column-major at a_off)
   FiberBlk fb[RT_MAX_MODES];
 };
 
@@ -101,12 +109,18 @@ __device__ __forceinline__ double fb_cons_sum(double v, double* red, int ncons) 
   return t;
 }
 
-template <typename T, int R, bool EX, bool HS, bool HE>
+// ns_reg: doubles of per-row register state per rank (A rows of the states, A-pass accumulators)
+template <bool HS, bool HE, bool AP>
+__host__ __device__ constexpr int fb_nsreg() {
+  return ((HS ? 1 : 0) + (HE ? 1 : 0) + (AP ? 1 : 0)) > 0 ? (HS ? 1 : 0) + (HE ? 1 : 0) + (AP ? 1 : 0) : 1;
+}
+
+template <typename T, int R, bool EX, bool HS, bool HE, bool AP>
 __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a) {
-  constexpr int NS = (HS ? 1 : 0) + (HE ? 1 : 0);
-  constexpr int V = fb_vec<T>(R, NS > 0 ? NS : 1);
-  constexpr bool WM = !HE;     // threshold pass: intersections
-  constexpr bool SUMS = HE;    // error pass: sums
+  constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);   // staged row sets per column: W_s, W_e or V
+  constexpr int V = fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
+  constexpr bool WM = !HE && !AP;   // threshold pass: intersections
+  constexpr bool SUMS = HE;         // error pass: sums
   typedef FbVec<T, V> VT;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ double red[FB_MAX_CONS / 32 + 1];
@@ -167,6 +181,8 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
                             wbytes, &full[s]);
         if (HE) tma_load_1d(dst + a.x_region + slot * a.w_region, reinterpret_cast<const char*>(a.st_e) + wsrc,
                             wbytes, &full[s]);
+        if (AP) tma_load_1d(dst + a.x_region + slot * a.w_region,
+                            reinterpret_cast<const char*>(a.Vr[B.mode] + c0 * B.r), wbytes, &full[s]);
         if (hb == B.P)   // whole fibers: the group's columns are one contiguous range
           tma_load_1d(dst, xb + (B.off + c0 * B.P) * (i64)sizeof(T), (unsigned)(nc * B.P * (i64)sizeof(T)), &full[s]);
       }
@@ -186,8 +202,21 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
   } else {
     // ---------------- consumers
     const double zeta = a.zetap ? __ldg(a.zetap) : a.zeta;
-    double as[V][R], ae[V][R];
+    double as[V][R], ae[V][R], ar[V][R];
     int pos[V];
+    // A pass: the thread's rows [row, row + V) accumulate over its columns of the
+    // band; flushed to its (block, CTA, column offset) slot at the band's end
+    double* ap_dst = nullptr;
+    int ap_f = -1, ap_r = R;
+    auto ap_flush = [&]() {
+      if (!AP || ap_dst == nullptr) return;
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+          if (EX || q < ap_r) ap_dst[v * ap_r + q] = ar[v][q];
+      ap_dst = nullptr;
+    };
     double e2 = 0.0, x2 = 0.0, nfchk = 0.0;
     int cur_f = -1, cur_band = -1;
     int chunk = 0, coff = 0, H = 0, cpr = 1, mrows = 0, r = R;
@@ -220,8 +249,20 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
       const int nc = (int)min((i64)B.CB, B.Q - c0);
       const bool act = coff < cpr && chunk * V < hb;
       const int row = r0 + chunk * V;
+      if ((int)cband != cur_band || cf != ap_f) {
+        ap_flush();
+      }
       if ((int)cband != cur_band) {
         cur_band = (int)cband;
+        if (AP && act) {
+          ap_f = cf;
+          ap_r = r;
+          ap_dst = a.apart + B.pbase + ((i64)(blockIdx.x - B.c0) * cpr + coff) * B.P * r + (i64)row * r;
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+#pragma unroll
+            for (int q = 0; q < R; ++q) ar[v][q] = 0.0;
+        }
         if (act) {
 #pragma unroll
           for (int v = 0; v < V; ++v) {
@@ -245,7 +286,7 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
         const unsigned char* sb = ring + s * stage_bytes;
         const T* xs = reinterpret_cast<const T*>(sb) + chunk * V;
         const double* wss = reinterpret_cast<const double*>(sb + a.x_region);
-        const double* wes = reinterpret_cast<const double*>(sb + a.x_region + (HS ? a.w_region : 0));
+        const double* wes = reinterpret_cast<const double*>(sb + a.x_region + (HS ? a.w_region : 0));   // W_e or V
         double* Mc = WM ? a.M[B.mode] + (c0 + coff) * (i64)mrows : nullptr;
         const i64 mstep = (i64)cpr * mrows;
 #pragma unroll 1
@@ -255,7 +296,7 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
 #pragma unroll
           for (int q = 0; q < R; ++q) {
             ws[q] = (HS && (EX || q < r)) ? wss[jj * r + q] : 0.0;
-            we[q] = (HE && (EX || q < r)) ? wes[jj * r + q] : 0.0;
+            we[q] = ((HE || AP) && (EX || q < r)) ? wes[jj * r + q] : 0.0;
           }
 #pragma unroll
           for (int v = 0; v < V; ++v) {
@@ -279,6 +320,12 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
               e2 = fma(rr, rr, e2);
               x2 = fma(x, x, x2);
             }
+            if (AP) {
+              const double c = x - sv;
+#pragma unroll
+              for (int q = 0; q < R; ++q)
+                if (EX || q < r) ar[v][q] = fma(c, we[q], ar[v][q]);
+            }
           }
           if (WM) Mc += mstep;
         }
@@ -290,6 +337,7 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
         ph ^= 1u;
       }
     }
+    ap_flush();
     bad = !(nfchk == 0.0);
     if (SUMS && cur_f >= 0) {
       const double se = fb_cons_sum(e2, red, ncons), sx = fb_cons_sum(x2, red2, ncons);
@@ -341,10 +389,34 @@ struct FbIn {
   int Pv, b, mode, r, mrows;
 };
 
-template <typename T, int R, bool EX, bool HS, bool HE>
-static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, cudaStream_t st) {
-  constexpr int NS = (HS ? 1 : 0) + (HE ? 1 : 0);
-  constexpr int V = fb_vec<T>(R, NS > 0 ? NS : 1);
+// A_k[p, q] = siginv_q * sum over the CTAs whose tiles cover p's band (and their
+// column offsets) of the A-pass partial rows: a warp per output, lanes over the
+// terms, fixed-order shuffle tree (deterministic).
+static __global__ void __launch_bounds__(256) k_fiber_areduce(FiberArgs a, int G) {
+  const int f = blockIdx.y;
+  if (f >= a.nfb) return;
+  const FiberBlk& B = a.fb[f];
+  const int r = B.r, lane = threadIdx.x & 31;
+  const i64 nout = B.P * r;
+  const i64 wstride = (i64)gridDim.x * (blockDim.x >> 5);
+  for (i64 o = blockIdx.x * (i64)(blockDim.x >> 5) + (threadIdx.x >> 5); o < nout; o += wstride) {
+    const i64 p = o / r;
+    const int q = (int)(o - p * r);
+    const i64 t_lo = B.tfirst + (p / B.H) * B.ncg, t_hi = t_lo + B.ncg - 1;
+    const i64 c_lo = ap_cta_of(t_lo, a.ntiles, G), c_hi = ap_cta_of(t_hi, a.ntiles, G);
+    const i64 nterm = (c_hi - c_lo + 1) * B.cpr;
+    const double* base = a.apart + B.pbase + (c_lo - B.c0) * B.cpr * B.P * r + o;
+    double sum = 0.0;
+    for (i64 k = lane; k < nterm; k += 32) sum += base[k * B.P * r];   // slot (c, offset) = c_lo * cpr + k
+    sum = warp_sum(sum);
+    if (lane == 0) a.a_out[B.a_off + p + (i64)q * B.dA] = sum * a.siginv[B.mode][q];
+  }
+}
+
+template <typename T, int R, bool EX, bool HS, bool HE, bool AP>
+static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, cudaStream_t st) {
+  constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);
+  constexpr int V = fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
   const int E = (int)sizeof(T);
   const int VA = 16 / E;   // bulk-copy segments are 16-byte multiples
   // per-block bands / thread mapping
@@ -401,20 +473,41 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, cudaStream_t st
   if (fa.nst < 2) return -(int)cudaErrorInvalidConfiguration;
   const int smem = 2 * FB_MAX_STAGES * 8 + (int)(fa.nst * stage);
   const int grid = (int)std::max<i64>(1, std::min<i64>(148, t));
-  auto K = k_fiber_pass<T, R, EX, HS, HE>;
+  i64 maxpr = 1;
+  if (AP) {   // partial slots: one P x r slot per (block, CTA touching it)
+    i64 pb = 0;
+    for (int f = 0; f < nin; ++f) {
+      FiberBlk& B = fa.fb[f];
+      const i64 c0 = ap_cta_of(B.tfirst, t, grid), c1 = ap_cta_of(B.tfirst + (i64)B.nbands * B.ncg - 1, t, grid);
+      B.c0 = (int)c0;
+      B.pbase = pb;
+      pb += (c1 - c0 + 1) * B.cpr * B.P * B.r;
+      maxpr = std::max<i64>(maxpr, B.P * B.r);
+    }
+    if (pb > apart_cap) return -(int)cudaErrorInvalidValue;
+  }
+  auto K = k_fiber_pass<T, R, EX, HS, HE, AP>;
   cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return -(int)e;
   K<<<grid, ncons + 32, smem, st>>>(fa);
   e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : -(int)e;
+  if (e != cudaSuccess) return -(int)e;
+  if (AP) {
+    k_fiber_areduce<<<dim3((unsigned)std::min<i64>((maxpr + 7) / 8, 1024), nin), 256, 0, st>>>(fa, grid);
+    e = cudaGetLastError();
+  }
+  return e == cudaSuccess ? (AP ? 2 : 1) : -(int)e;   // kernels launched
 }
 
 template <typename T, int R, bool EX>
-static int fb_launch_states(FiberArgs& fa, const FbIn* in, int nin, bool hs, bool he, cudaStream_t st) {
-  if (hs && he) return fb_launch_one<T, R, EX, true, true>(fa, in, nin, st);
-  if (hs) return fb_launch_one<T, R, EX, true, false>(fa, in, nin, st);
-  if (he) return fb_launch_one<T, R, EX, false, true>(fa, in, nin, st);
-  return fb_launch_one<T, R, EX, false, false>(fa, in, nin, st);
+static int fb_launch_states(FiberArgs& fa, const FbIn* in, int nin, bool hs, bool he, bool ap, i64 cap,
+                            cudaStream_t st) {
+  if (ap) return hs ? fb_launch_one<T, R, EX, true, false, true>(fa, in, nin, cap, st)
+                    : fb_launch_one<T, R, EX, false, false, true>(fa, in, nin, cap, st);
+  if (hs && he) return fb_launch_one<T, R, EX, true, true, false>(fa, in, nin, cap, st);
+  if (hs) return fb_launch_one<T, R, EX, true, false, false>(fa, in, nin, cap, st);
+  if (he) return fb_launch_one<T, R, EX, false, true, false>(fa, in, nin, cap, st);
+  return fb_launch_one<T, R, EX, false, false, false>(fa, in, nin, cap, st);
 }
 
 template <typename T>
@@ -433,12 +526,18 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
   fa.sums = L.sums;
   fa.counter = L.counter;
   fa.nonfinite = L.nonfinite;
-  const bool hs = L.st_s != nullptr, he = L.st_e != nullptr;
-  // threshold pass: the intersection copies X(I_k, J_k) (only those rows feed M_k);
+  const bool hs = L.st_s != nullptr, he = L.st_e != nullptr, ap = L.ap != 0;
+  for (int m = 0; m < RT_MAX_MODES; ++m) {
+    fa.Vr[m] = L.Vr[m];
+    fa.siginv[m] = L.siginv[m];
+  }
+  fa.apart = L.apart;
+  fa.a_out = L.a_out;
+  // A pass and error pass: the whole fiber blocks; threshold pass: the intersection copies X(I_k, J_k) (only those rows feed M_k);
   // error pass: the whole fiber blocks
   FbIn in[RT_MAX_MODES];
   int nin = 0, rmax = 1, rmin = 64;
-  fa.xb = he ? L.xb : L.xi;
+  fa.xb = (he || ap) ? L.xb : L.xi;
   fa.nblk = L.g.nblk;
   for (int b = 1; b < L.g.nblk; ++b) {
     if (!(mask >> b & 1)) continue;
@@ -453,7 +552,7 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
     I.mode = m;
     I.r = bd.r;
     I.mrows = (int)L.g.nrows[m];
-    if (he) {
+    if (he || ap) {
       I.off = bd.off;
       I.P = bd.P;
       I.Pv = (int)bd.P;
@@ -467,21 +566,40 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
     rmax = std::max(rmax, bd.r);
     rmin = std::min(rmin, bd.r);
   }
-  if (rmin == rmax) {   // uniform rank: exact unrolled dot products
-    switch (rmax) {
-#define FB_EXACT(k) \
-  case k:           \
-    return fb_launch_states<T, k, true>(fa, in, nin, hs, he, st);
+  (void)rmin;
+  (void)rmax;
+  // one launch per distinct rank (exact unrolled dot products; buckets for the rest)
+  bool done[RT_MAX_MODES] = {};
+  int nl = 0;
+  for (int f = 0; f < nin; ++f) {
+    if (done[f]) continue;
+    FbIn grp[RT_MAX_MODES];
+    int ng = 0;
+    const int rk = in[f].r;
+    for (int h = f; h < nin; ++h)
+      if (!done[h] && in[h].r == rk) {
+        grp[ng++] = in[h];
+        done[h] = true;
+      }
+    FiberArgs fg = fa;
+    int st_ = 0;
+    switch (rk) {
+#define FB_EXACT(k)                                                                           \
+  case k:                                                                                     \
+    st_ = fb_launch_states<T, k, true>(fg, grp, ng, hs, he, ap, L.apart_cap, st);             \
+    break;
       FB_EXACT(1) FB_EXACT(2) FB_EXACT(3) FB_EXACT(4) FB_EXACT(5) FB_EXACT(6) FB_EXACT(8) FB_EXACT(10)
       FB_EXACT(16)
 #undef FB_EXACT
       default:
+        st_ = rk <= 8 ? fb_launch_states<T, 8, false>(fg, grp, ng, hs, he, ap, L.apart_cap, st)
+                      : fb_launch_states<T, 16, false>(fg, grp, ng, hs, he, ap, L.apart_cap, st);
         break;
     }
+    if (st_ < 0) return st_;
+    nl += st_;
   }
-  if (rmax <= 4) return fb_launch_states<T, 4, false>(fa, in, nin, hs, he, st);
-  if (rmax <= 8) return fb_launch_states<T, 8, false>(fa, in, nin, hs, he, st);
-  return fb_launch_states<T, 16, false>(fa, in, nin, hs, he, st);
+  return nl;
 }
 
 // Intersection copies for the threshold pass: xi_k[i + q * ld_k] = x_k(I_k[i], q)
