@@ -193,8 +193,8 @@ def test_native_code_ran():
 
 @pytest.mark.gpu
 def test_graph_captured_iterations_match():
-    """RTCUR_GRAPHS=1 (per-iteration CUDA graphs, zeta from device memory) gives the
-    same iterates as the stream-launched path (R and F, several slot rotations)."""
+    """Per-iteration CUDA graphs (the default; zeta from device memory) give the same
+    iterates as the stream-launched path (RTCUR_GRAPHS=0), R and F, several slot rotations."""
     import os
     import subprocess
     import sys
@@ -213,7 +213,7 @@ for case in ("bern_R", "d20_F", "n4_R"):
 '''
     outs = []
     here = os.path.dirname(os.path.abspath(__file__))
-    for env in ({}, {"RTCUR_GRAPHS": "1"}):
+    for env in ({"RTCUR_GRAPHS": "0"}, {"RTCUR_GRAPHS": "1"}):
         e = dict(os.environ, **env)
         e["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, e.get("PYTHONPATH", "")])
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, cwd=here)
