@@ -935,12 +935,50 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   const int slot = e->stg >= 0 ? e->stg : e->act_slot();
   IndexPtrs ip = make_ip_slot(e, slot);
   prof_begin(e, PH_GATHER);
+  const bool whole = e->lo == 0 && e->hi == P.g.dim[0];
   ModeCopies mc;
-  for (int m = 0; m < RT_MAX_MODES; ++m) mc.p[m] = (e->lo == 0 && e->hi == P.g.dim[0]) ? e->mcopy[m] : nullptr;
-  k_gather<<<(unsigned)P.tm.first[P.g.nblk], 256, 0, e->st>>>(P.g, P.tm, ip, e->X, P.dtype, e->lo, e->hi,
-                                                              e->xb(slot), mc);
-  LAUNCH_CHECK();
-  e->xi_valid[slot] = false;
+  for (int m = 0; m < RT_MAX_MODES; ++m) mc.p[m] = whole ? e->mcopy[m] : nullptr;
+  // contiguous fibers (mode 1 of an unsharded X, modes with a mode-k copy): warp-per-column
+  // copies that also fill the intersection copies; the rest through the tile gather
+  FastGather fg;
+  memset(&fg, 0, sizeof(fg));
+  TileMap tg = P.tm;
+  {
+    i64 t = 0;
+    for (int b = 0; b < P.g.nblk; ++b) {
+      const BlockDesc& bd = P.g.blk[b];
+      const bool fast = whole && (bd.is_core || bd.mode == 0 || mc.p[bd.mode] != nullptr);
+      const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
+      tg.first[b] = t;
+      if (fast) {
+        fg.blk[fg.nb] = b;
+        fg.colbase[fg.nb + 1] = fg.colbase[fg.nb] + bd.Q;
+        ++fg.nb;
+        fg.src[bd.mode] = (bd.is_core || bd.mode == 0) ? e->X : mc.p[bd.mode];
+        if (P.fiber_mask >> b & 1) fg.ximask |= 1u << b;
+      } else {
+        t += nt;
+      }
+    }
+    tg.first[P.g.nblk] = t;
+  }
+  fg.xi = e->ws + P.o_xi + e->sd(slot);
+  for (int m = 0; m < P.g.n; ++m) {
+    fg.xi_off[m] = P.xi_off[m];
+    fg.xi_ld[m] = P.xi_ld[m];
+  }
+  if (tg.first[P.g.nblk] > 0) {
+    k_gather<<<(unsigned)tg.first[P.g.nblk], 256, 0, e->st>>>(P.g, tg, ip, e->X, P.dtype, e->lo, e->hi, e->xb(slot), mc);
+    LAUNCH_CHECK();
+  }
+  if (fg.nb > 0) {
+    const unsigned grid = (unsigned)std::min<i64>(cdiv(fg.colbase[fg.nb], 8), 148 * 16);
+    if (P.dtype == 0) k_gather_fibers<double><<<grid, 256, 0, e->st>>>(P.g, ip, fg, e->xb(slot));
+    else k_gather_fibers<float><<<grid, 256, 0, e->st>>>(P.g, ip, fg, e->xb(slot));
+    LAUNCH_CHECK();
+  }
+  // the intersection copies are complete when every fiber-pass block was copied here
+  e->xi_valid[slot] = (P.fiber_mask & ~fg.ximask) == 0;
   if (int st = refresh_xi(e, slot)) return st;
   prof_end(e, PH_GATHER);
   return RT_OK;

@@ -150,6 +150,73 @@ __global__ void __launch_bounds__(256) k_gather(Geom g, TileMap tm, IndexPtrs ip
   }
 }
 
+// Contiguous fiber columns (mode 1 of an unsharded X, or a mode-k-fastest copy):
+// one warp per column, 16-byte vector copy into the compact block, plus the
+// column's intersection rows X(I_k, q) into the fiber pass's copy (k_fiber.cuh).
+// Core columns (unsharded X): the warp picks the rows I_1 out of the column's
+// mode-1 fiber (one index load per entry, no per-entry division).
+struct FastGather {
+  const void* src[RT_MAX_MODES];   // mode 0: X (unsharded); k >= 1: the mode-k copy
+  void* xi;
+  i64 xi_off[RT_MAX_MODES], xi_ld[RT_MAX_MODES];
+  unsigned ximask;                 // blocks whose intersection copy is written
+  int nb;                          // blocks copied here
+  int blk[RT_MAX_BLOCKS];
+  i64 colbase[RT_MAX_BLOCKS + 1];  // prefix sums of their column counts
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather_fibers(Geom g, IndexPtrs ip, FastGather fg, void* __restrict__ xb) {
+  constexpr int VE = 16 / (int)sizeof(T);
+  const int lane = threadIdx.x & 31;
+  const i64 total = fg.colbase[fg.nb];
+  for (i64 wc = blockIdx.x * (i64)(blockDim.x >> 5) + (threadIdx.x >> 5); wc < total;
+       wc += (i64)gridDim.x * (blockDim.x >> 5)) {
+    int f = 0;
+    while (f + 1 < fg.nb && wc >= fg.colbase[f + 1]) ++f;
+    const int b = fg.blk[f];
+    const i64 q = wc - fg.colbase[f];
+    const BlockDesc& bd = g.blk[b];
+    const int k = bd.mode;
+    const i64 P = bd.P;
+    T* d = reinterpret_cast<T*>(xb) + bd.off + q * P;
+    if (bd.is_core) {   // core column: rows I_1 of the mode-1 fiber X(:, i_2..i_n)
+      const T* s = reinterpret_cast<const T*>(fg.src[0]) + g.dim[0] * ip.colR[0][q];
+      const int* rows = ip.rows[0];
+      for (i64 i = lane; i < P; i += 32) d[i] = __ldg(s + __ldg(rows + i));
+      continue;
+    }
+    const T* s = reinterpret_cast<const T*>(fg.src[k]) + P * (k == 0 ? ip.colR[b][q] : ip.cols[k][q]);
+    if (((reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(d)) & 15) == 0 && P % VE == 0) {
+      const float4* __restrict__ s4 = reinterpret_cast<const float4*>(s);
+      float4* __restrict__ d4 = reinterpret_cast<float4*>(d);
+      const i64 n4 = P / VE;
+      // chunks of 8 vectors per lane: all loads in flight before the stores
+      for (i64 base = 0; base < n4; base += 256) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const i64 i = base + u * 32 + lane;
+          if (i < n4) v[u] = __ldg(s4 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const i64 i = base + u * 32 + lane;
+          if (i < n4) d4[i] = v[u];
+        }
+      }
+    } else {
+      for (i64 i = lane; i < P; i += 32) d[i] = __ldg(s + i);
+    }
+    if (fg.ximask >> b & 1) {
+      const i64 ld = fg.xi_ld[k], nr = g.nrows[k];
+      T* xo = reinterpret_cast<T*>(fg.xi) + fg.xi_off[k] + q * ld;
+      const int* rows = ip.rows[k];
+      for (i64 i = lane; i < ld; i += 32) xo[i] = i < nr ? __ldg(s + __ldg(rows + i)) : (T)0;
+    }
+  }
+}
+
 // out = X with mode k moved first: view X as (A, d_k, B) (A = prod_{m<k} d_m),
 // out[i + d_k (a + A b)] = X[a + A (i + d_k b)] -- 32 x 32 shared-memory tiles,
 // both sides coalesced.
