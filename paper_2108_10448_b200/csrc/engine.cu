@@ -107,6 +107,7 @@ struct Plan {
   TileMap tm;
   TileMap tm_gp;   // G pass: the core block's tiles (lanes over columns when possible)
   TileMap tm_core; // threshold/error passes on k_block_pass: the blocks the fiber pass does not take
+  TileMap tm_thr;  // threshold pass on k_block_pass: only fiber blocks (the core yields nothing there)
   unsigned fiber_mask;   // blocks handled by the TMA fiber pass (k_fiber.cuh)
   i64 xi_off[RT_MAX_MODES], xi_ld[RT_MAX_MODES];   // intersection copies (elements) inside o_xi
   i64 o_xi;
@@ -336,6 +337,17 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
       if (!(P.fiber_mask >> b & 1)) t += nt;
     }
     tc.first[g.nblk] = t;
+    // threshold pass: M_k comes from fiber blocks only; the core's clean values are
+    // recomputed by the G pass, so k_block_pass needs no core tiles there
+    TileMap& tt = P.tm_thr;
+    tt = P.tm;
+    t = 0;
+    for (int b = 0; b < g.nblk; ++b) {
+      const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
+      tt.first[b] = t;
+      if (b > 0 && !(P.fiber_mask >> b & 1)) t += nt;
+    }
+    tt.first[g.nblk] = t;
   }
 
   P.col_off[0] = 0;
@@ -1063,7 +1075,8 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   const bool hs = st_s != nullptr, he = st_e != nullptr;
   // the fiber blocks of the threshold / error passes go to the TMA fiber pass; exports stay here
   const bool split = P.fiber_mask && !(s_out || c_out || l_out) && (with_M || sums);
-  const TileMap& tmk = split ? P.tm_core : P.tm;
+  const bool thr_only = with_M && !sums && !(s_out || c_out || l_out);
+  const TileMap& tmk = thr_only ? P.tm_thr : split ? P.tm_core : P.tm;
 #define BP_LAUNCH(HS, HE, WM, EXP)                                                                        \
   (P.rb == 4    ? launch_bp(k_block_pass<HS, HE, WM, EXP, false, 4, false>, tmk.first[P.g.nblk], smb, e->st, P.g, tmk,  \
                             ip, a, P.bp)                                                                          \
@@ -1073,8 +1086,10 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
                             tmk, ip, a, P.bp)                                                                    \
                 : launch_bp(k_block_pass<HS, HE, WM, EXP, false, 32, false>, tmk.first[P.g.nblk], smb, e->st, P.g,      \
                             tmk, ip, a, P.bp))
-  int lst;
-  if (s_out || c_out || l_out) {
+  int lst = 0;
+  if (tmk.first[P.g.nblk] == 0) {
+    // nothing left for k_block_pass (threshold pass with every fiber block on the fiber pass)
+  } else if (s_out || c_out || l_out) {
     if (hs && he) lst = BP_LAUNCH(true, true, false, true);
     else if (hs) lst = BP_LAUNCH(true, false, false, true);
     else if (he) lst = BP_LAUNCH(false, true, false, true);
