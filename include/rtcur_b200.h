@@ -140,6 +140,8 @@ int rtcur_engine_profile(rtcur_engine* e, int on);
  * (default: all).  Timing only the phase a measurement needs keeps the event
  * overhead (two event records per timed phase launch) out of the other phases. */
 int rtcur_engine_profile_phases(rtcur_engine* e, uint32_t mask);
+/* per-iteration CUDA graphs on (default, unless RTCUR_GRAPHS=0) or off for this engine */
+int rtcur_engine_set_graphs(rtcur_engine* e, int on);
 int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* counts, int nphase, int reset);
 
 /* ---- TNSR v1 tensor files (reference tensorfile.py:1-115), streamed disk <-> HBM ----

@@ -1661,6 +1661,13 @@ extern "C" int rtcur_engine_debug_marks(rtcur_engine* e, int64_t* out, int n) {
   return RT_OK;
 }
 
+extern "C" int rtcur_engine_set_graphs(rtcur_engine* e, int on) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  if (e->pending) return fail(RT_ERR_VALUE, "iteration in flight");
+  e->use_graphs = on != 0;
+  return RT_OK;
+}
+
 extern "C" int rtcur_engine_profile_phases(rtcur_engine* e, uint32_t mask) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
   CK(cudaStreamSynchronize(e->st));

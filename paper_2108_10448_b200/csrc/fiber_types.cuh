@@ -33,7 +33,8 @@ struct FiberLaunch {
 
 // Blocks (bit b = block b) the fiber pass handles for this geometry: fiber
 // blocks whose columns are 16-byte aligned in the compact buffer and whose
-// rank is <= 16.  The rest (always the core) stay on k_block_pass.
+// rank is <= 16, and (bit 0, error pass only) the core when |I_1| <= 352.
+// The rest stay on k_block_pass.
 unsigned fiber_pass_blocks(const Geom& g, int dtype);
 
 // Threshold pass (st_e == null: M written, no sums), error pass (st_e set: sums

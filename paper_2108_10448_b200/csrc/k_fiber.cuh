@@ -115,10 +115,12 @@ __host__ __device__ constexpr int fb_nsreg() {
   return ((HS ? 1 : 0) + (HE ? 1 : 0) + (AP ? 1 : 0)) > 0 ? (HS ? 1 : 0) + (HE ? 1 : 0) + (AP ? 1 : 0) : 1;
 }
 
-template <typename T, int R, bool EX, bool HS, bool HE, bool AP>
+// SC: scalar rows (V = 1) for blocks whose columns are not 16-byte multiples (the
+// core, |I_1| rows): whole-column tiles whose starts stay 16-byte aligned.
+template <typename T, int R, bool EX, bool HS, bool HE, bool AP, bool SC>
 __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a) {
   constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);   // staged row sets per column: W_s, W_e or V
-  constexpr int V = fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
+  constexpr int V = SC ? 1 : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
   constexpr bool WM = !HE && !AP;   // threshold pass: intersections
   constexpr bool SUMS = HE;         // error pass: sums
   typedef FbVec<T, V> VT;
@@ -175,7 +177,8 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
       const unsigned wbytes = (unsigned)((nc * B.r * 8 + 15) & ~15LL);
       const i64 wsrc = (B.w_off + c0 * B.r) * 8;
       if (lane == 0) {
-        mbar_expect_tx(&full[s], (unsigned)(hb * nc * (i64)sizeof(T)) + NS * wbytes);
+        const unsigned xbytes = (unsigned)((hb * nc * (i64)sizeof(T) + 15) & ~15LL);   // (SC: rounded up)
+        mbar_expect_tx(&full[s], xbytes + NS * wbytes);
         int slot = 0;
         if (HS) tma_load_1d(dst + a.x_region + (slot++) * a.w_region, reinterpret_cast<const char*>(a.st_s) + wsrc,
                             wbytes, &full[s]);
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
         if (AP) tma_load_1d(dst + a.x_region + slot * a.w_region,
                             reinterpret_cast<const char*>(a.Vr[B.mode] + c0 * B.r), wbytes, &full[s]);
         if (hb == B.P)   // whole fibers: the group's columns are one contiguous range
-          tma_load_1d(dst, xb + (B.off + c0 * B.P) * (i64)sizeof(T), (unsigned)(nc * B.P * (i64)sizeof(T)), &full[s]);
+          tma_load_1d(dst, xb + (B.off + c0 * B.P) * (i64)sizeof(T), xbytes, &full[s]);
       }
       if (hb != B.P) {
         __syncwarp();
@@ -267,11 +270,10 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             const int rr = row + v;
-            int arow = rr;
-            if (WM) {   // intersection copy: padded rows past |I_k| are computed (finite) but not stored
-              pos[v] = rr < B.Pv ? rr : -1;
-              arow = __ldg(B.amap + (rr < B.Pv ? rr : B.Pv - 1));
-            }
+            // row map (intersection copy: I_k; core: I_1); padded rows past Pv are
+            // computed (finite) but never stored
+            const int arow = B.amap ? __ldg(B.amap + (rr < B.Pv ? rr : B.Pv - 1)) : rr;
+            if (WM) pos[v] = rr < B.Pv ? rr : -1;
 #pragma unroll
             for (int q = 0; q < R; ++q) {
               const bool on = EX || q < r;
@@ -379,7 +381,9 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
 inline bool fb_block_ok(const Geom& g, int b, int dtype) {
   const int E = dtype == 0 ? 8 : 4;
   const BlockDesc& bd = g.blk[b];
-  return !bd.is_core && bd.r <= FB_MAX_R && (bd.P * E) % 16 == 0 && (bd.off * E) % 16 == 0 && bd.Q > 0;
+  if (bd.r > FB_MAX_R || (bd.off * E) % 16 != 0 || bd.Q <= 0) return false;
+  if (bd.is_core) return bd.P <= FB_MAX_CONS;   // error pass only: one band of scalar rows
+  return (bd.P * E) % 16 == 0;
 }
 
 // one handled block as the pass sees it (the fiber block, or its intersection copy)
@@ -387,6 +391,7 @@ struct FbIn {
   i64 off, P, Q, w_off, a_off, dA;
   const int* amap;
   int Pv, b, mode, r, mrows;
+  bool sc;   // columns not 16-byte multiples: scalar rows
 };
 
 // A_k[p, q] = siginv_q * sum over the CTAs whose tiles cover p's band (and their
@@ -413,12 +418,12 @@ static __global__ void __launch_bounds__(256) k_fiber_areduce(FiberArgs a, int G
   }
 }
 
-template <typename T, int R, bool EX, bool HS, bool HE, bool AP>
+template <typename T, int R, bool EX, bool HS, bool HE, bool AP, bool SC>
 static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, cudaStream_t st) {
   constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);
-  constexpr int V = fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
+  constexpr int V = SC ? 1 : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
   const int E = (int)sizeof(T);
-  const int VA = 16 / E;   // bulk-copy segments are 16-byte multiples
+  const int VA = SC ? 1 : 16 / E;   // bulk-copy segments are 16-byte multiples (SC: one band)
   // per-block bands / thread mapping
   int maxch = 1;
   i64 H[RT_MAX_MODES];
@@ -448,7 +453,16 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
     B.H = (int)H[f];
     B.nchB = nch[f];
     B.cpr = std::max(1, ncons / nch[f]);
-    const i64 unit = B.cpr % 2 ? 2 * B.cpr : B.cpr;   // multiple of cpr, even (16-byte aligned W rows)
+    i64 unit = B.cpr % 2 ? 2 * B.cpr : B.cpr;   // multiple of cpr, even (16-byte aligned W rows)
+    if (SC) {   // and every tile's x start 16-byte aligned
+      const i64 cb = I.P * E;
+      i64 gcd = 16, x = cb % 16;
+      while (x) { const i64 t2 = gcd % x; gcd = x; x = t2; }
+      const i64 au = 16 / gcd;
+      i64 a = unit, b2 = au;
+      while (b2) { const i64 t2 = a % b2; a = b2; b2 = t2; }
+      unit = unit / a * au;
+    }
     const i64 colb = H[f] * E + (i64)NS * I.r * 8;
     i64 CB = std::max<i64>(1, FB_STAGE_BYTES / colb) / unit * unit;
     if (CB == 0) CB = unit;
@@ -462,7 +476,7 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
     B.mode = I.mode;
     B.r = I.r;
     B.mrows = I.mrows;
-    xreg = std::max<i64>(xreg, CB * H[f] * E);
+    xreg = std::max<i64>(xreg, (CB * H[f] * E + 15) & ~15LL);
     wreg = std::max<i64>(wreg, (CB * I.r * 8 + 15) & ~15LL);
   }
   fa.ntiles = t;
@@ -486,7 +500,7 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
     }
     if (pb > apart_cap) return -(int)cudaErrorInvalidValue;
   }
-  auto K = k_fiber_pass<T, R, EX, HS, HE, AP>;
+  auto K = k_fiber_pass<T, R, EX, HS, HE, AP, SC>;
   cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return -(int)e;
   K<<<grid, ncons + 32, smem, st>>>(fa);
@@ -502,12 +516,17 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
 template <typename T, int R, bool EX>
 static int fb_launch_states(FiberArgs& fa, const FbIn* in, int nin, bool hs, bool he, bool ap, i64 cap,
                             cudaStream_t st) {
-  if (ap) return hs ? fb_launch_one<T, R, EX, true, false, true>(fa, in, nin, cap, st)
-                    : fb_launch_one<T, R, EX, false, false, true>(fa, in, nin, cap, st);
-  if (hs && he) return fb_launch_one<T, R, EX, true, true, false>(fa, in, nin, cap, st);
-  if (hs) return fb_launch_one<T, R, EX, true, false, false>(fa, in, nin, cap, st);
-  if (he) return fb_launch_one<T, R, EX, false, true, false>(fa, in, nin, cap, st);
-  return fb_launch_one<T, R, EX, false, false, false>(fa, in, nin, cap, st);
+  if (in[0].sc) {   // scalar rows: the error pass over the core only
+    if (!he || ap) return -(int)cudaErrorInvalidValue;
+    return hs ? fb_launch_one<T, R, EX, true, true, false, true>(fa, in, nin, cap, st)
+              : fb_launch_one<T, R, EX, false, true, false, true>(fa, in, nin, cap, st);
+  }
+  if (ap) return hs ? fb_launch_one<T, R, EX, true, false, true, false>(fa, in, nin, cap, st)
+                    : fb_launch_one<T, R, EX, false, false, true, false>(fa, in, nin, cap, st);
+  if (hs && he) return fb_launch_one<T, R, EX, true, true, false, false>(fa, in, nin, cap, st);
+  if (hs) return fb_launch_one<T, R, EX, true, false, false, false>(fa, in, nin, cap, st);
+  if (he) return fb_launch_one<T, R, EX, false, true, false, false>(fa, in, nin, cap, st);
+  return fb_launch_one<T, R, EX, false, false, false, false>(fa, in, nin, cap, st);
 }
 
 template <typename T>
@@ -539,11 +558,13 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
   int nin = 0, rmax = 1, rmin = 64;
   fa.xb = (he || ap) ? L.xb : L.xi;
   fa.nblk = L.g.nblk;
-  for (int b = 1; b < L.g.nblk; ++b) {
+  const int E = (int)sizeof(T);
+  for (int b = he ? 0 : 1; b < L.g.nblk; ++b) {   // the core only in the error pass
     if (!(mask >> b & 1)) continue;
     const BlockDesc& bd = L.g.blk[b];
     const int m = bd.mode;
     FbIn& I = in[nin++];
+    I.sc = (bd.P * E) % 16 != 0;
     I.Q = bd.Q;
     I.w_off = bd.w_off;
     I.a_off = L.g.a_off[m];
@@ -556,7 +577,7 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
       I.off = bd.off;
       I.P = bd.P;
       I.Pv = (int)bd.P;
-      I.amap = nullptr;
+      I.amap = bd.is_core ? L.rows[0] : nullptr;   // core rows are I_1
     } else {
       I.off = L.xi_off[m];
       I.P = L.xi_ld[m];
@@ -576,8 +597,9 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
     FbIn grp[RT_MAX_MODES];
     int ng = 0;
     const int rk = in[f].r;
+    const bool sc = in[f].sc;
     for (int h = f; h < nin; ++h)
-      if (!done[h] && in[h].r == rk) {
+      if (!done[h] && in[h].r == rk && in[h].sc == sc) {
         grp[ng++] = in[h];
         done[h] = true;
       }

@@ -17,6 +17,9 @@ unsigned fiber_pass_blocks(const Geom& g, int dtype) {
   unsigned mask = 0;
   for (int b = 1; b < g.nblk; ++b)
     if (fb_block_ok(g, b, dtype)) mask |= 1u << b;
+  // the core (bit 0) joins the error pass only
+  const char* ec = getenv("RTCUR_FIBER_CORE");
+  if (!(ec && ec[0] == '0') && fb_block_ok(g, 0, dtype)) mask |= 1u;
   return mask;
 }
 

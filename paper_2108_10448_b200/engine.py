@@ -43,6 +43,10 @@ def acquire_engine(shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=
             eng = None
     if eng is None:
         eng = Engine(shape, ranks, row_sizes, col_sizes, dtype, slab=slab, device=dev)
+        # per-iteration CUDA graphs only for solves issued on the device's default stream
+        # (concurrent solves on worker streams, sweeps.py, launch directly)
+        if torch.cuda.current_stream(dev) != torch.cuda.default_stream(dev):
+            nat.check(eng.lib.rtcur_engine_set_graphs(eng.handle, 0))
     eng._pool_key = key
     return eng
 
