@@ -125,11 +125,11 @@ def _algorithmic_bytes(bc, rows, cols):
     n_blk = n_core + n_fib
     inter = sum(r * c for r, c in zip(rows, cols))
     return {
-        "gather": 2 * E * n_blk,            # read the sampled X entries, write the compact blocks
-        "threshold": E * n_blk + 8 * inter,  # read blocks, write the fp64 intersections
-        "error": E * n_blk,                  # read blocks
-        "apass": E * n_fib,                  # read fiber blocks
-        "gpass": E * n_core,                 # read core block
+        "gather": 2 * E * n_blk + E * inter,  # read the sampled X entries, write the blocks + X(I_k, J_k) copies
+        "threshold": (E + 8) * inter,         # read the X(I_k, J_k) copies, write the fp64 intersections M_k
+        "error": E * n_blk,                   # read blocks
+        "apass": E * n_fib,                   # read fiber blocks
+        "gpass": E * n_core,                  # read core block
     }, n_blk
 
 
@@ -396,8 +396,9 @@ def run_b200(args):
     # ---------------- roofline of the dominant HBM-bound kernel (events from the timed region)
     per_launch_ms = dom_ms / max(dom_n, 1)
     achieved = alg[dom] / (per_launch_ms / 1e3) / 1e9
-    kname = {"threshold": "k_block_pass (threshold)", "error": "k_block_pass (error)", "gather": "k_gather",
-             "apass": "k_apass", "gpass": "k_gpass"}[dom]
+    kname = {"threshold": "k_fiber_pass (threshold over X(I_k, J_k))", "error": "k_fiber_pass (error: core + fibers)",
+             "gather": "k_gather_fibers + k_gather", "apass": "k_fiber_pass (A pass) + k_fiber_areduce",
+             "gpass": "k_block_pass (G pass)"}[dom]
     traffic = _ncu_traffic(args.config, dom)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic.get("bytes_per_launch") if traffic else None,

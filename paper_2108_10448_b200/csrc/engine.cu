@@ -495,11 +495,11 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_wt1 = take(P.w_tmp * 8);
   P.o_bpart = take((i64)BP_GRID * g.nblk * 2 * 8 + 64);
   {
-    // fiber-pass A pass: one d_k x r_k slot per (fiber block, CTA touching it) -- at most 148 + n slots
+    // fiber-pass A pass: one d_k x r_k slot per (fiber block, CTA touching it) -- at most 296 + n slots
     i64 mx = 1;
     // (column offsets per CTA x rows <= max(d_k, 352 threads x 4 rows))
     for (int m = 0; m < n; ++m) mx = std::max<i64>(mx, std::max<i64>(dims[m], 1408) * ranks[m]);
-    P.fapart_cap = P.fiber_mask ? (148 + n) * mx : 1;
+    P.fapart_cap = P.fiber_mask ? (148 * 2 + n) * mx : 1;   // (up to two CTAs per SM, k_fiber.cuh)
     P.o_fapart = take(P.fapart_cap * 8);
   }
   P.o_sums = take(2 * g.nblk * 8);

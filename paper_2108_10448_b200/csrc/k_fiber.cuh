@@ -30,7 +30,8 @@
 
 #define FB_MAX_CONS 352   // + the producer warp: 12 warps, so up to 168 registers per thread
 #define FB_STAGE_BYTES (32 * 1024)
-#define FB_SMEM_BUDGET (200 * 1024)
+#define FB_SMEM_BUDGET (100 * 1024)   // two CTAs per SM
+#define FB_MAX_CTAS_PER_SM 2
 #define FB_MAX_STAGES 8
 #define FB_MAX_R 16
 
@@ -118,7 +119,7 @@ __host__ __device__ constexpr int fb_nsreg() {
 // SC: scalar rows (V = 1) for blocks whose columns are not 16-byte multiples (the
 // core, |I_1| rows): whole-column tiles whose starts stay 16-byte aligned.
 template <typename T, int R, bool EX, bool HS, bool HE, bool AP, bool SC>
-__global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a) {
+__global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a) {   // (grid: up to 2 CTAs per SM)
   constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);   // staged row sets per column: W_s, W_e or V
   constexpr int V = SC ? 1 : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
   constexpr bool WM = !HE && !AP;   // threshold pass: intersections
@@ -483,10 +484,22 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
   fa.x_region = (int)((xreg + 127) & ~127LL);
   fa.w_region = (int)((wreg + 127) & ~127LL);
   const i64 stage = fa.x_region + (i64)NS * fa.w_region;
-  fa.nst = (int)std::min<i64>(FB_MAX_STAGES, FB_SMEM_BUDGET / stage);
-  if (fa.nst < 2) return -(int)cudaErrorInvalidConfiguration;
+  // shared-memory ring per CTA: the budget decides how many CTAs share an SM
+  // (RTCUR_FB_SMEM_KB overrides; default two CTAs per SM)
+  i64 budget = FB_SMEM_BUDGET;
+  if (const char* env = getenv("RTCUR_FB_SMEM_KB")) budget = std::max<i64>(16, atoll(env)) * 1024;
+  fa.nst = (int)std::min<i64>(FB_MAX_STAGES, budget / stage);
+  if (fa.nst < 2) fa.nst = 2;
   const int smem = 2 * FB_MAX_STAGES * 8 + (int)(fa.nst * stage);
-  const int grid = (int)std::max<i64>(1, std::min<i64>(148, t));
+  if (smem > 227 * 1024) return -(int)cudaErrorInvalidConfiguration;
+  auto K = k_fiber_pass<T, R, EX, HS, HE, AP, SC>;
+  cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return -(int)e;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K, ncons + 32, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  per_sm = std::min(per_sm, FB_MAX_CTAS_PER_SM);
+  const int grid = (int)std::max<i64>(1, std::min<i64>(148LL * per_sm, t));
   i64 maxpr = 1;
   if (AP) {   // partial slots: one P x r slot per (block, CTA touching it)
     i64 pb = 0;
@@ -500,9 +513,6 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
     }
     if (pb > apart_cap) return -(int)cudaErrorInvalidValue;
   }
-  auto K = k_fiber_pass<T, R, EX, HS, HE, AP, SC>;
-  cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return -(int)e;
   K<<<grid, ncons + 32, smem, st>>>(fa);
   e = cudaGetLastError();
   if (e != cudaSuccess) return -(int)e;
