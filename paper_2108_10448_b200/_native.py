@@ -46,6 +46,23 @@ class NativeUnavailable(RuntimeError):
     pass
 
 
+def _keep_large_host_blocks():
+    """Results are returned as fresh host arrays (tens to hundreds of MB).  glibc
+    serves blocks above its mmap threshold (<= 32 MB) with fresh mappings, so every
+    solve's export page-faults its destination pages again (measured: 4 -> 31 ms for
+    config 1's 64 MB of blocks).  Keep such blocks on the heap so freed result
+    memory is reused without faults.  RTCUR_NO_MALLOPT=1 leaves malloc alone."""
+    if os.environ.get("RTCUR_NO_MALLOPT") == "1":
+        return
+    try:
+        libc = ctypes.CDLL("libc.so.6")
+        M_TRIM_THRESHOLD, M_MMAP_THRESHOLD = -1, -3
+        libc.mallopt(M_MMAP_THRESHOLD, 1 << 30)
+        libc.mallopt(M_TRIM_THRESHOLD, 1 << 31 - 1)
+    except (OSError, AttributeError):
+        pass
+
+
 def load(path: str = LIB_PATH):
     """Load the sm_100a library (no fallback: raises if absent)."""
     global _lib
@@ -56,6 +73,7 @@ def load(path: str = LIB_PATH):
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(the B200 path has no CPU fallback)")
     lib = ctypes.CDLL(path)
+    _keep_large_host_blocks()
     lib.rtcur_last_error.restype = ctypes.c_char_p
     lib.rtcur_version.restype = ctypes.c_char_p
     lib.rtcur_launch_count.restype = ctypes.c_ulonglong
