@@ -296,10 +296,32 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
         for (int jj = coff; jj < nc; jj += cpr) {
           const VT xv = *reinterpret_cast<const VT*>(xs + jj * H);
           double ws[R], we[R];
+          if (EX && R % 2 == 0) {   // exact even rank: the column's rows are 16-byte aligned
+            const double2* ws2 = reinterpret_cast<const double2*>(wss + jj * R);
+            const double2* we2 = reinterpret_cast<const double2*>(wes + jj * R);
 #pragma unroll
-          for (int q = 0; q < R; ++q) {
-            ws[q] = (HS && (EX || q < r)) ? wss[jj * r + q] : 0.0;
-            we[q] = ((HE || AP) && (EX || q < r)) ? wes[jj * r + q] : 0.0;
+            for (int q = 0; q < R / 2; ++q) {
+              if (HS) {
+                const double2 t = ws2[q];
+                ws[2 * q] = t.x;
+                ws[2 * q + 1] = t.y;
+              } else {
+                ws[2 * q] = ws[2 * q + 1] = 0.0;
+              }
+              if (HE || AP) {
+                const double2 t = we2[q];
+                we[2 * q] = t.x;
+                we[2 * q + 1] = t.y;
+              } else {
+                we[2 * q] = we[2 * q + 1] = 0.0;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              ws[q] = (HS && (EX || q < r)) ? wss[jj * r + q] : 0.0;
+              we[q] = ((HE || AP) && (EX || q < r)) ? wes[jj * r + q] : 0.0;
+            }
           }
 #pragma unroll
           for (int v = 0; v < V; ++v) {
