@@ -88,6 +88,10 @@ int rtcur_engine_destroy(rtcur_engine* e);
 int rtcur_engine_bind(rtcur_engine* e, const void* x_dev);
 /* max|X| over the bound slab (K0); synchronous, result on the host */
 int rtcur_engine_absmax(rtcur_engine* e, double* out);
+/* the same scan split in two: _begin enqueues it on the engine's stream, _end waits
+ * and returns max|X| (the host can draw the first sample in between) */
+int rtcur_engine_absmax_begin(rtcur_engine* e);
+int rtcur_engine_absmax_end(rtcur_engine* e, double* out);
 /* Optional copies of X with mode k fastest (rtcur_transpose_mode layout; copies[0]
  * and NULL entries unused): the gather then reads mode-k fibers as contiguous runs
  * instead of stride-prod_{m<k} d_m elements.  Ignored on sharded (slab) engines. */

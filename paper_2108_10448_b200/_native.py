@@ -25,7 +25,7 @@ EXPORTED = (
     "rtcur_engine_absmax", "rtcur_engine_set_sample", "rtcur_engine_gather", "rtcur_engine_xblocks_offset", "rtcur_engine_iterate",
     "rtcur_engine_iterate_async", "rtcur_engine_iterate_wait",
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
-    "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_set_graphs", "rtcur_engine_profile_read",
+    "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_set_graphs", "rtcur_engine_absmax_begin", "rtcur_engine_absmax_end", "rtcur_engine_profile_read",
     "rtcur_append_distinct", "rtcur_generate_tucker", "rtcur_tnsr_read_header", "rtcur_tnsr_load", "rtcur_tnsr_store",
     "rtcur_scatter_outliers", "rtcur_abs_sum", "rtcur_ap_threshold", "rtcur_ap_residual", "rtcur_abs_max", "rtcur_engine_bind_mode_copies",
     "rtcur_transpose_mode",
@@ -102,6 +102,8 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_profile.argtypes = [c_vp, ctypes.c_int]
     lib.rtcur_engine_profile_phases.argtypes = [c_vp, ctypes.c_uint32]
     lib.rtcur_engine_set_graphs.argtypes = [c_vp, ctypes.c_int]
+    lib.rtcur_engine_absmax_begin.argtypes = [c_vp]
+    lib.rtcur_engine_absmax_end.argtypes = [c_vp, c_dp]
     lib.rtcur_engine_profile_read.argtypes = [c_vp, c_dp, c_i64p, ctypes.c_int, ctypes.c_int]
     lib.rtcur_append_distinct.argtypes = [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64]
     lib.rtcur_append_distinct.restype = c_i64

@@ -563,6 +563,8 @@ struct rtcur_engine {
   GraphEntry* cap_entry;
   const double* zetap_cur;         // device zeta while an iteration body is enqueued/captured
   bool xi_valid[2];                // the sample slot's intersection copies match its blocks
+  cudaEvent_t absmax_ev;           // rtcur_engine_absmax_begin's D2H done
+  bool absmax_pending;
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
   i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
@@ -766,6 +768,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   // written by the gather and must not carry garbage into rank all-reduces
   for (int s = 0; s < 2; ++s) CK(cudaMemsetAsync(e->xb(s), 0, e->P.g.nblk_total * e->P.esize + 64, e->st));
   for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&e->idx_ev[s], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->absmax_ev, cudaEventDisableTiming));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -785,6 +788,7 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   if (e->h_pinned) cudaFreeHost(e->h_pinned);
   if (e->h_idx) cudaFreeHost(e->h_idx);
   if (e->done) cudaEventDestroy(e->done);
+  if (e->absmax_ev) cudaEventDestroy(e->absmax_ev);
   for (int s = 0; s < 2; ++s)
     if (e->idx_ev[s]) cudaEventDestroy(e->idx_ev[s]);
   if (e->prof_pending) {
@@ -844,7 +848,10 @@ extern "C" int rtcur_transpose_mode(const void* x, int dtype, int n, const int64
   return RT_OK;
 }
 
-extern "C" int rtcur_engine_absmax(rtcur_engine* e, double* out) {
+// zeta_0 = max|X| in two halves: _begin enqueues the scan and its 8-byte D2H
+// (pinned slot 240), _end waits for it -- the host draws the first sample in
+// between.  rtcur_engine_absmax = begin + end.
+extern "C" int rtcur_engine_absmax_begin(rtcur_engine* e) {
   if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
   const Plan& P = e->P;
   i64 nloc = e->hi - e->lo;
@@ -858,15 +865,28 @@ extern "C" int rtcur_engine_absmax(rtcur_engine* e, double* out) {
   else k_absmax<float><<<grid, 256, 0, e->st>>>((const float*)e->X, nloc, d);
   LAUNCH_CHECK();
   prof_end(e, PH_ABSMAX);
-  CK(cudaMemcpyAsync(e->h_pinned, d, 8, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaStreamSynchronize(e->st));
+  CK(cudaMemcpyAsync(e->h_pinned + 240, d, 8, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaEventRecord(e->absmax_ev, e->st));
+  e->absmax_pending = true;
+  return RT_OK;
+}
+
+extern "C" int rtcur_engine_absmax_end(rtcur_engine* e, double* out) {
+  if (!e || !e->absmax_pending) return fail(RT_ERR_VALUE, "no abs-max scan in flight");
+  CK(cudaEventSynchronize(e->absmax_ev));
+  e->absmax_pending = false;
   prof_flush(e);
   unsigned long long bits;
-  memcpy(&bits, e->h_pinned, 8);
+  memcpy(&bits, e->h_pinned + 240, 8);
   double v;
   memcpy(&v, &bits, 8);
   *out = v;
   return RT_OK;
+}
+
+extern "C" int rtcur_engine_absmax(rtcur_engine* e, double* out) {
+  if (int st = rtcur_engine_absmax_begin(e)) return st;
+  return rtcur_engine_absmax_end(e, out);
 }
 
 extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols) {

@@ -195,6 +195,15 @@ class Engine:
         nat.check(self.lib.rtcur_engine_absmax(self.handle, ctypes.byref(out)))
         return float(out.value)
 
+    def absmax_begin(self):
+        """Enqueue the max|X| scan (absmax_end returns it)."""
+        nat.check(self.lib.rtcur_engine_absmax_begin(self.handle))
+
+    def absmax_end(self) -> float:
+        out = ctypes.c_double()
+        nat.check(self.lib.rtcur_engine_absmax_end(self.handle, ctypes.byref(out)))
+        return float(out.value)
+
     def set_sample(self, idx):
         rows = [np.ascontiguousarray(r, dtype=np.int64) for r in idx.rows]
         cols = [np.ascontiguousarray(c, dtype=np.int64) for c in idx.cols]

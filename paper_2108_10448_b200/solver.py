@@ -21,6 +21,7 @@ fallback: without the library or a CUDA device the call raises.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass
 from typing import Protocol, Sequence
@@ -392,11 +393,8 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> Sol
     rng = np.random.default_rng(cfg.seed)
     row_sizes, col_sizes = cfg.resolve_sample_sizes(shape)
 
-    t0 = time.perf_counter()
-    idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
-    timings["sample"] += time.perf_counter() - t0
     for m, (r, rs, cs) in enumerate(zip(cfg.ranks, row_sizes, col_sizes), start=1):
-        if r > rs or r > cs:   # fiber_cur.py:257-261
+        if r > rs or r > cs:   # fiber_cur.py:257-261 (raised before any work, as there)
             raise ValueError(f"mode {m}: rank {r} exceeds sample sizes (|rows|={rs}, |cols|={cs})")
 
     eng = acquire_engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype, slab=src.slab)
@@ -406,12 +404,24 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> Sol
     copies = _mode_copy_plan(shape, col_sizes, cfg, src)
     if copies:
         eng.bind_mode_copies(src.dev.flat, copies)
+    # the device scans max|X| (and builds the mode copies) while the host draws the
+    # first sample (the generator is consumed by sampling only, solver.py:293-316)
+    early_zeta = (cfg.zeta0 is None and src.dev is not None and src.group is None
+                  and os.environ.get("RTCUR_EARLY_ZETA", "1") != "0")
+    if early_zeta:
+        eng.absmax_begin()
+    t0 = time.perf_counter()
+    idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+    timings["sample"] += time.perf_counter() - t0
     t0 = time.perf_counter()
     eng.set_sample(idx)
     src.load_blocks(eng, idx)
     timings["gather"] += time.perf_counter() - t0
 
-    zeta = float(cfg.zeta0) if cfg.zeta0 is not None else src.inf_norm(eng)
+    if cfg.zeta0 is not None:
+        zeta = float(cfg.zeta0)
+    else:
+        zeta = eng.absmax_end() if early_zeta else src.inf_norm(eng)
     t_loop = time.perf_counter()
     history, flags = [], []
     trace = [] if record_trace else None
