@@ -640,7 +640,10 @@ static int set_smem_limits_once() {
   } while (0)
   SMEM_ATTR(k_eig);
   SMEM_ATTR(k_wcols<4>); SMEM_ATTR(k_wcols<8>); SMEM_ATTR(k_wcols<16>); SMEM_ATTR(k_wcols<32>);
-  SMEM_ATTR(k_wcols_warp<4>); SMEM_ATTR(k_wcols_warp<8>); SMEM_ATTR(k_wcols_warp<16>); SMEM_ATTR(k_wcols_warp<32>);
+  SMEM_ATTR((k_wcols_warp<4, 32>)); SMEM_ATTR((k_wcols_warp<8, 32>)); SMEM_ATTR((k_wcols_warp<16, 32>));
+  SMEM_ATTR((k_wcols_warp<32, 32>));
+  SMEM_ATTR((k_wcols_warp<4, 8>)); SMEM_ATTR((k_wcols_warp<8, 8>)); SMEM_ATTR((k_wcols_warp<16, 8>));
+  SMEM_ATTR((k_wcols_warp<32, 8>));
   SMEM_ATTR(k_zproj<4>); SMEM_ATTR(k_zproj<8>); SMEM_ATTR(k_zproj<16>); SMEM_ATTR(k_zproj<32>);
 #define BP_ATTRS(RB)                                                                                     \
   SMEM_ATTR((k_block_pass<true, true, false, true, false, RB, false>));                                  \
@@ -1305,11 +1308,30 @@ static int run_wcols(rtcur_engine* e, double* sto) {
     ncmax = std::max(ncmax, nc);
     rsmax = std::max(rsmax, rs);
   }
-  const int rows_cap = (int)(cdiv(rsmax, 32) * 32);
-  const i64 wsm = (g.gsize + (ncmax * 4 + ncmax * std::max(1, g.n - 1) + 7) / 8 + 1 + (i64)WC_WARPS * rows_cap) * 8;
-  if (wsm <= 200 * 1024 && ncmax >= 48) {   // few combinations: a thread per column is cheaper
-    const dim3 grid((unsigned)std::min<i64>(cdiv(qf, WC_WARPS * 2), 148 * 4), g.nblk);
-    DISPATCH_R(P.rb, k_wcols_warp, grid, 32 * WC_WARPS, (int)wsm, e->st, g, ip, sto, chain ? 1 : 0, rows_cap);
+  // lanes per column: a warp for many combinations, 8 lanes (4 columns per warp) for a few
+  const int gs = ncmax >= 48 ? 32 : 8;
+  const int ngrp = 32 * WC_WARPS / gs;
+  const int rows_cap = (int)(cdiv(rsmax, gs) * gs);
+  const i64 wsm = (g.gsize + (ncmax * 4 + ncmax * std::max(1, g.n - 1) + 7) / 8 + 1 + (i64)ngrp * rows_cap) * 8;
+  if (wsm <= 200 * 1024 && ncmax >= 8) {   // very few combinations: a thread per column is cheaper
+    const dim3 grid((unsigned)std::min<i64>(cdiv(qf, ngrp * 2), 148 * 4), g.nblk);
+#define WCW(RB, GS) k_wcols_warp<RB, GS><<<grid, 32 * WC_WARPS, (int)wsm, e->st>>>(g, ip, sto, chain ? 1 : 0, rows_cap)
+    if (gs == 32) {
+      switch (P.rb) {
+        case 4: WCW(4, 32); break;
+        case 8: WCW(8, 32); break;
+        case 16: WCW(16, 32); break;
+        default: WCW(32, 32); break;
+      }
+    } else {
+      switch (P.rb) {
+        case 4: WCW(4, 8); break;
+        case 8: WCW(8, 8); break;
+        case 16: WCW(16, 8); break;
+        default: WCW(32, 8); break;
+      }
+    }
+#undef WCW
   } else {
     const int rpt = wcols_rows_per_thread(g);
     DISPATCH_R(P.rb, k_wcols, dim3((unsigned)cdiv(qf, 128), g.nblk), 128, wcols_smem(g), e->st, g, ip, sto, 0,

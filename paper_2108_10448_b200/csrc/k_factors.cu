@@ -104,16 +104,19 @@ __global__ void __launch_bounds__(256) k_modeprod_fwd(const double* __restrict__
 // of the column staged per warp, and a fixed-order butterfly sum of the r_t
 // partials.  Dynamic shared memory: G | goff[ncombo] (int) | cidx[ncombo][n-1]
 // (uchar) | per warp 32 * ceil(sum r_other / 32) row values.
+// GS lanes per column (32: one warp; 8: four columns per warp for geometries with
+// few combinations, e.g. 25 at n = 3, r = 5).
 #define WC_WARPS 8
-template <int R>
+template <int R, int GS>
 __global__ void __launch_bounds__(32 * WC_WARPS) k_wcols_warp(Geom g, IndexPtrs ip, double* __restrict__ st,
                                                              int skip_core, int rows_cap) {
+  constexpr int NG = 32 * WC_WARPS / GS;   // column groups per CTA
   extern __shared__ double wsm[];
   const int b = blockIdx.y;
   if (b >= g.nblk || (skip_core && g.blk[b].is_core)) return;
   const BlockDesc& bd = g.blk[b];
   const i64 Q = bd.Q;
-  if ((i64)blockIdx.x * WC_WARPS >= Q) return;
+  if ((i64)blockIdx.x * NG >= Q) return;
   const int tgt = bd.mode, rt = g.rank[tgt];
   const i64 gst = g.gstride[tgt];
   int no = 0, ncombo = 1, rsum = 0;
@@ -143,9 +146,10 @@ __global__ void __launch_bounds__(32 * WC_WARPS) k_wcols_warp(Geom g, IndexPtrs 
     goff[c] = off;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x % GS, w = threadIdx.x / GS;
+  const unsigned gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << ((threadIdx.x & 31) & ~(GS - 1)));
   double* rb = rows + (size_t)w * rows_cap;
-  for (i64 q = (i64)blockIdx.x * WC_WARPS + w; q < Q; q += (i64)gridDim.x * WC_WARPS) {
+  for (i64 q = (i64)blockIdx.x * NG + w; q < Q; q += (i64)gridDim.x * NG) {
     // the other modes' A rows of this column
     {
       i64 t = q, j = bd.is_core ? 0 : ip.cols[tgt][q];
@@ -161,14 +165,14 @@ __global__ void __launch_bounds__(32 * WC_WARPS) k_wcols_warp(Geom g, IndexPtrs 
           im = j % g.dim[m];
           j /= g.dim[m];
         }
-        for (int bm = lane; bm < g.rank[m]; bm += 32) rb[ro[k] + bm] = st[g.a_off[m] + im + (i64)bm * g.dim[m]];
+        for (int bm = lane; bm < g.rank[m]; bm += GS) rb[ro[k] + bm] = st[g.a_off[m] + im + (i64)bm * g.dim[m]];
       }
     }
-    __syncwarp();
+    __syncwarp(gmask);
     double acc[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) acc[i] = 0.0;
-    for (int c = lane; c < ncombo; c += 32) {
+    for (int c = lane; c < ncombo; c += GS) {
       double coef = 1.0;
       for (int k = no - 1; k >= 0; --k) coef *= rb[ro[k] + cidx[(size_t)c * no + k]];
       const double* gq = G + goff[c];
@@ -180,11 +184,13 @@ __global__ void __launch_bounds__(32 * WC_WARPS) k_wcols_warp(Geom g, IndexPtrs 
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       if (i < rt) {
-        const double v = warp_sum(acc[i]);
+        double v = acc[i];
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);   // fixed order
         if (lane == 0) out[i] = v;
       }
     }
-    __syncwarp();
+    __syncwarp(gmask);
   }
 }
 
@@ -305,10 +311,14 @@ template __global__ void k_gpass<8>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<16>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_gpass<32>(Geom, IndexPtrs, GPassArgs);
 template __global__ void k_wcols<4>(Geom, IndexPtrs, double*, int, double*, int, int);
-template __global__ void k_wcols_warp<4>(Geom, IndexPtrs, double*, int, int);
-template __global__ void k_wcols_warp<8>(Geom, IndexPtrs, double*, int, int);
-template __global__ void k_wcols_warp<16>(Geom, IndexPtrs, double*, int, int);
-template __global__ void k_wcols_warp<32>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<4, 32>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<8, 32>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<16, 32>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<32, 32>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<4, 8>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<8, 8>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<16, 8>(Geom, IndexPtrs, double*, int, int);
+template __global__ void k_wcols_warp<32, 8>(Geom, IndexPtrs, double*, int, int);
 template __global__ void k_wcols<8>(Geom, IndexPtrs, double*, int, double*, int, int);
 template __global__ void k_wcols<16>(Geom, IndexPtrs, double*, int, double*, int, int);
 template __global__ void k_wcols<32>(Geom, IndexPtrs, double*, int, double*, int, int);
