@@ -982,7 +982,13 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
     i64 t = 0;
     for (int b = 0; b < P.g.nblk; ++b) {
       const BlockDesc& bd = P.g.blk[b];
-      const bool fast = whole && (bd.is_core || bd.mode == 0 || mc.p[bd.mode] != nullptr);
+      // large cores: k_gather_core (CW columns per warp); small ones ride along in k_gather_fibers
+      const bool core_fast = whole && bd.is_core && bd.P <= 256 && bd.Q >= 100000;
+      const bool fast = whole && !core_fast && (bd.is_core || bd.mode == 0 || mc.p[bd.mode] != nullptr);
+      if (core_fast) {
+        tg.first[b] = t;
+        continue;
+      }
       const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
       tg.first[b] = t;
       if (fast) {
@@ -1006,6 +1012,14 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
     k_gather<<<(unsigned)tg.first[P.g.nblk], 256, 0, e->st>>>(P.g, tg, ip, e->X, P.dtype, e->lo, e->hi, e->xb(slot), mc);
     LAUNCH_CHECK();
   }
+  if (whole && P.g.blk[0].P <= 256 && P.g.blk[0].Q >= 100000) {
+    const i64 nw = cdiv(P.g.blk[0].Q, GC_CW);
+    const unsigned grid = (unsigned)std::min<i64>(cdiv(nw, 8), 148 * 8);
+    const size_t sm = (size_t)P.g.blk[0].P * 4;
+    if (P.dtype == 0) k_gather_core<double><<<grid, 256, sm, e->st>>>(P.g, ip, e->X, e->xb(slot));
+    else k_gather_core<float><<<grid, 256, sm, e->st>>>(P.g, ip, e->X, e->xb(slot));
+    LAUNCH_CHECK();
+  }
   if (fg.nb > 0) {
     const unsigned grid = (unsigned)std::min<i64>(cdiv(fg.colbase[fg.nb], 8), 148 * 16);
     if (P.dtype == 0) k_gather_fibers<double><<<grid, 256, 0, e->st>>>(P.g, ip, fg, e->xb(slot));
@@ -1013,7 +1027,7 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
     LAUNCH_CHECK();
   }
   // the intersection copies are complete when every fiber-pass block was copied here
-  e->xi_valid[slot] = (P.fiber_mask & ~fg.ximask) == 0;
+  e->xi_valid[slot] = ((P.fiber_mask & ~1u) & ~fg.ximask) == 0;   // (bit 0: the core, no copy)
   if (int st = refresh_xi(e, slot)) return st;
   prof_end(e, PH_GATHER);
   return RT_OK;

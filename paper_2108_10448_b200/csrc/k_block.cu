@@ -217,6 +217,53 @@ __global__ void __launch_bounds__(256) k_gather_fibers(Geom g, IndexPtrs ip, Fas
   }
 }
 
+// Core block of an unsharded X: column q is X(I_1, i_2(q), .., i_n(q)), the rows
+// I_1 of one mode-1 fiber.  I_1 is staged in shared memory once per CTA; a warp
+// takes CW consecutive columns at a time and issues all their loads before the
+// stores (the fiber's sectors are shared by the ~|I_1|/d_1 of it that is sampled).
+#define GC_CW 4
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather_core(Geom g, IndexPtrs ip, const void* __restrict__ X,
+                                                     void* __restrict__ xb) {
+  extern __shared__ int rows_s[];
+  const BlockDesc& bd = g.blk[0];
+  const int P = (int)bd.P;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) rows_s[i] = ip.rows[0][i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const i64 Q = bd.Q, d1 = g.dim[0];
+  const T* Xt = reinterpret_cast<const T*>(X);
+  T* out = reinterpret_cast<T*>(xb) + bd.off;
+  const i64* colR = ip.colR[0];
+  constexpr int MAXR = 8;   // rows per lane held in flight per column (P <= 256 here)
+  for (i64 q0 = (blockIdx.x * (i64)(blockDim.x >> 5) + (threadIdx.x >> 5)) * GC_CW; q0 < Q;
+       q0 += (i64)gridDim.x * (blockDim.x >> 5) * GC_CW) {
+    T v[GC_CW][MAXR];
+#pragma unroll
+    for (int c = 0; c < GC_CW; ++c) {
+      const i64 q = q0 + c;
+      if (q >= Q) break;
+      const T* s = Xt + d1 * __ldg(colR + q);
+#pragma unroll
+      for (int u = 0; u < MAXR; ++u) {
+        const int p = lane + 32 * u;
+        if (p < P) v[c][u] = __ldg(s + rows_s[p]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < GC_CW; ++c) {
+      const i64 q = q0 + c;
+      if (q >= Q) break;
+      T* d = out + q * P;
+#pragma unroll
+      for (int u = 0; u < MAXR; ++u) {
+        const int p = lane + 32 * u;
+        if (p < P) d[p] = v[c][u];
+      }
+    }
+  }
+}
+
 // out = X with mode k moved first: view X as (A, d_k, B) (A = prod_{m<k} d_m),
 // out[i + d_k (a + A b)] = X[a + A (i + d_k b)] -- 32 x 32 shared-memory tiles,
 // both sides coalesced.
