@@ -365,10 +365,16 @@ def run_b200(args):
     x_buf = torch.empty_like(x_dev.flat)
     e2e_iters, d2h = 0, 0
     e2e_steps = max(1, args.steps if args.config <= 1 else min(args.steps, 2))
+    # untimed warm-up of the host-buffer path: the exports' pinned staging buffer and
+    # the result arrays' first touch are one-time costs (~0.2 s at config 1)
+    res = None
+    x_buf.copy_(pinned, non_blocking=True)
+    res = solve(DeviceTensor(x_buf, x_dev.shape))
+    _ = (res.sparse.core, res.sparse.fibers, res.cur.core, res.cur.fibers, res.cur.intersections, res.cur.factors)
+    del _
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = None
     for _ in range(e2e_steps):
         x_buf.copy_(pinned, non_blocking=True)
         res = None   # the previous result returns its engine to the pool
