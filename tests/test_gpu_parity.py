@@ -220,3 +220,47 @@ for case in ("bern_R", "d20_F", "n4_R"):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout)
     assert outs[0] == outs[1] and outs[0].count("\n") == 3
+
+
+@pytest.mark.parametrize("env", [{"RTCUR_FIBER_PASS": "0"}, {"RTCUR_FIBER_CORE": "0"}, {"RTCUR_EARLY_ZETA": "0"},
+                                 {"RTCUR_K3_GENERIC": "1"}],
+                         ids=["block-pass-only", "core-on-block-pass", "late-zeta0", "generic-k3"])
+def test_engine_variants_agree(env):
+    """The device-path variants (TMA fiber pass vs the block pass for every block,
+    the core on either, zeta_0 scanned before or after the first draw, TMA vs
+    generic K3) solve the golden cases identically: same iteration counts and
+    sparse support; the error histories and the full-output residual to 1e-9
+    relative (the A pass and the sums group their fixed-order additions
+    differently, ~1e-16 of L, amplified by 1/e ~ 1e5 in the relative residuals)."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+from conftest import load_golden, golden_cfg_kwargs
+from paper_2108_10448_b200 import SolverConfig, rtcur, full_output
+from paper_2108_10448_b200.tensor import DenseTensor
+for case in ("bern_R", "d20_F", "n4_R", "tall_F"):
+    g = load_golden(f"solve_{case}.npz")
+    shape = tuple(int(v) for v in g["shape"])
+    res = rtcur(DenseTensor(g["x"], shape), SolverConfig(**golden_cfg_kwargs(g)))
+    _, _, rel = full_output(res)
+    supp = int(np.count_nonzero(res.sparse.core)) + sum(int(np.count_nonzero(f)) for f in res.sparse.fibers)
+    print(case, res.iterations, supp, repr(rel), repr(list(res.error_history)))
+'''
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for e_ in ({}, env):
+        e = dict(os.environ, **e_)
+        e["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, e.get("PYTHONPATH", "")])
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, cwd=here)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append([ln.split(" ", 4) for ln in r.stdout.strip().splitlines()])
+    assert len(outs[0]) == len(outs[1]) == 4
+    for a, b in zip(*outs):
+        assert a[:3] == b[:3], (a[:3], b[:3])   # case, iterations, support size
+        assert float(a[3]) == pytest.approx(float(b[3]), rel=1e-9, abs=1e-300)
+        np.testing.assert_allclose(eval(a[4]), eval(b[4]), rtol=1e-9, atol=0)
