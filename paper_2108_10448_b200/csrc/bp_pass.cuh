@@ -108,11 +108,8 @@ __device__ __forceinline__ void bp_cols(const BPTile& T, double& e2, double& x2,
     }
     const int pb = rr * rlen, pe = min(P, pb + rlen);
     const int qoff = (valid ? ql : 0) * P;
-#pragma unroll 1
-    for (int p = pb; p < pe; ++p) {
-      const double x = bp_xt<DT>(T.x, qoff + p);
-      const double ls = HS ? bp_dot_sm<R, EX>(T.Asm + p * ap, ws, r) : 0.0;
-      const double le = HE ? bp_dot_sm<R, EX>(T.Aem + p * ap, we, r) : 0.0;
+    // one row's entry: threshold/error/exports, then the G-pass accumulation
+    auto row_step = [&](int p, double x, double ls, double le) {
       const int pos = WM ? T.rmap[p] : -1;
       double c = 0.0;
       if (valid) c = bp_entry<HS, HE, WM, EXP>(T, x, ls, le, pos, ql, p, e2, x2, bad);
@@ -125,6 +122,25 @@ __device__ __forceinline__ void bp_cols(const BPTile& T, double& e2, double& x2,
           if (kk + 1 < R && (EX || kk + 1 < r)) acc[kk + 1] = fma(u2.y, c, acc[kk + 1]);
         }
       }
+    };
+    // two rows per step: their dot products are independent chains; the entries
+    // are then applied in row order, so every sum is bit-identical to the row loop
+    int p = pb;
+#pragma unroll 1
+    for (; p + 1 < pe; p += 2) {
+      const double x0 = bp_xt<DT>(T.x, qoff + p), x1 = bp_xt<DT>(T.x, qoff + p + 1);
+      const double ls0 = HS ? bp_dot_sm<R, EX>(T.Asm + p * ap, ws, r) : 0.0;
+      const double ls1 = HS ? bp_dot_sm<R, EX>(T.Asm + (p + 1) * ap, ws, r) : 0.0;
+      const double le0 = HE ? bp_dot_sm<R, EX>(T.Aem + p * ap, we, r) : 0.0;
+      const double le1 = HE ? bp_dot_sm<R, EX>(T.Aem + (p + 1) * ap, we, r) : 0.0;
+      row_step(p, x0, ls0, le0);
+      row_step(p + 1, x1, ls1, le1);
+    }
+    if (p < pe) {
+      const double x = bp_xt<DT>(T.x, qoff + p);
+      const double ls = HS ? bp_dot_sm<R, EX>(T.Asm + p * ap, ws, r) : 0.0;
+      const double le = HE ? bp_dot_sm<R, EX>(T.Aem + p * ap, we, r) : 0.0;
+      row_step(p, x, ls, le);
     }
     if (GP) {
       if (nrr == 1) {
