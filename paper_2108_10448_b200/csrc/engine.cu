@@ -760,10 +760,10 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   cudaError_t ce = cudaMallocHost(&e->h_pinned, 4096);
   if (ce != cudaSuccess) { delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   e->h_flags = reinterpret_cast<int*>(e->h_pinned + 256);
-  i64 idx_len = 0;
-  for (int m = 0; m < n; ++m) idx_len += row_sizes[m] + col_sizes[m];
-  e->h_idx_len = idx_len;
-  ce = cudaMallocHost(&e->h_idx, 2 * (idx_len * 8 + 64));
+  // per sample slot: the byte span of the device index range (rows + cols with the carve's padding)
+  const i64 idx_span = e->P.o_cols[n - 1] + col_sizes[n - 1] * 8 - e->P.o_rows[0];
+  e->h_idx_len = (idx_span + 7) / 8;
+  ce = cudaMallocHost(&e->h_idx, 2 * (e->h_idx_len * 8 + 64));
   if (ce != cudaSuccess) { cudaFreeHost(e->h_pinned); delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   // counters + col offsets
   CK(cudaMemsetAsync(e->ws + e->P.o_counters, 0, 64 * 4, e->st));
@@ -905,44 +905,36 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
   i64* h_idx = e->h_idx + (size_t)slot * (e->h_idx_len + 8);
   const i64 sdl = e->sd(slot);
   // validate (fiber_cur.py:67-83) and stage 0-based copies in pinned memory
-  i64 o = 0;
-  std::vector<i64> offs(2 * g.n);
+  // the staging mirrors the slot's device layout (rows_0..rows_n-1, cols_0..cols_n-1
+  // as carved by make_plan): one H2D copy of the whole index range
+  char* hb = reinterpret_cast<char*>(h_idx);
   for (int m = 0; m < g.n; ++m) {
-    offs[m] = o;
-    int* dst = reinterpret_cast<int*>(h_idx + o);
+    int* dst = reinterpret_cast<int*>(hb + (P.o_rows[m] - P.o_rows[0]));
     for (i64 i = 0; i < g.nrows[m]; ++i) {
       const int64_t v = rows[m][i];
       if (v < 1 || v > g.dim[m]) return fail(RT_ERR_INDEX, "mode " + std::to_string(m + 1) + ": row index outside [1, d]");
       if (i > 0 && v <= rows[m][i - 1]) return fail(RT_ERR_VALUE, "row sets must be sorted and unique");
       dst[i] = (int)(v - 1);
     }
-    o += cdiv(g.nrows[m], 2);
   }
   for (int m = 0; m < g.n; ++m) {
-    offs[g.n + m] = o;
+    i64* dst = reinterpret_cast<i64*>(hb + (P.o_cols[m] - P.o_rows[0]));
     const i64 rest = total / g.dim[m];
     for (i64 i = 0; i < g.ncols[m]; ++i) {
       const int64_t v = cols[m][i];
       if (v < 1 || v > rest) return fail(RT_ERR_INDEX, "mode " + std::to_string(m + 1) + ": fiber column outside range");
       if (i > 0 && v <= cols[m][i - 1]) return fail(RT_ERR_VALUE, "column sets must be sorted and unique");
-      h_idx[o + i] = v - 1;
+      dst[i] = v - 1;
     }
-    o += g.ncols[m];
   }
-  for (int m = 0; m < g.n; ++m) {
-    CK(cudaMemcpyAsync(e->ws + P.o_rows[m] + sdl, h_idx + offs[m], g.nrows[m] * 4, cudaMemcpyHostToDevice, e->st));
-    CK(cudaMemcpyAsync(e->ws + P.o_cols[m] + sdl, h_idx + offs[g.n + m], g.ncols[m] * 8, cudaMemcpyHostToDevice,
-                       e->st));
-  }
+  const i64 span = P.o_cols[g.n - 1] + g.ncols[g.n - 1] * 8 - P.o_rows[0];
+  CK(cudaMemcpyAsync(e->ws + P.o_rows[0] + sdl, hb, span, cudaMemcpyHostToDevice, e->st));
   CK(cudaEventRecord(e->idx_ev[slot], e->st));
   IndexPtrs ip = make_ip_slot(e, slot);
   prof_begin(e, PH_PREP);
-  dim3 gr((unsigned)std::min<i64>(cdiv(P.dmax, 256), 1024), g.n);
-  k_rowpos<<<gr, 256, 0, e->st>>>(g, ip, e->at<int>(P.o_rowpos + sdl));
-  LAUNCH_CHECK();
-  dim3 gc((unsigned)std::min<i64>(cdiv(P.qmax, 256), 4096), g.nblk);
-  k_colprep<<<gc, 256, 0, e->st>>>(g, ip, e->at<i64>(P.o_colR + sdl), e->at<int>(P.o_coli1 + sdl),
-                                   e->at<i64>(P.o_coloff));
+  dim3 gp((unsigned)std::min<i64>(cdiv(std::max(P.dmax, P.qmax), 256), 4096), g.n + g.nblk);
+  k_prep<<<gp, 256, 0, e->st>>>(g, ip, e->at<int>(P.o_rowpos + sdl), e->at<i64>(P.o_colR + sdl),
+                                e->at<int>(P.o_coli1 + sdl), e->at<i64>(P.o_coloff));
   LAUNCH_CHECK();
   prof_end(e, PH_PREP);
   e->sampled = true;

@@ -14,15 +14,14 @@
 // ------------------------------------------------------------------ index prep
 
 // rowpos_k[p] = position of p in the sorted row set I_k, or -1.
-__global__ void k_rowpos(Geom g, IndexPtrs ip, int* __restrict__ rowpos_base) {
-  const int k = blockIdx.y;
-  if (k >= g.n) return;
+__device__ __forceinline__ void rowpos_mode(const Geom& g, const IndexPtrs& ip, int* __restrict__ rowpos_base, int k,
+                                            i64 t0, i64 tstride) {
   i64 base = 0;
   for (int m = 0; m < k; ++m) base += g.dim[m];
   int* out = rowpos_base + base;
   const int* rows = ip.rows[k];
   const int nr = (int)g.nrows[k];
-  for (i64 p = blockIdx.x * (i64)blockDim.x + threadIdx.x; p < g.dim[k]; p += (i64)gridDim.x * blockDim.x) {
+  for (i64 p = t0; p < g.dim[k]; p += tstride) {
     int lo = 0, hi = nr - 1, pos = -1;
     while (lo <= hi) {
       int mid = (lo + hi) >> 1;
@@ -34,18 +33,23 @@ __global__ void k_rowpos(Geom g, IndexPtrs ip, int* __restrict__ rowpos_base) {
   }
 }
 
+__global__ void k_rowpos(Geom g, IndexPtrs ip, int* __restrict__ rowpos_base) {
+  const int k = blockIdx.y;
+  if (k >= g.n) return;
+  rowpos_mode(g, ip, rowpos_base, k, blockIdx.x * (i64)blockDim.x + threadIdx.x, (i64)gridDim.x * blockDim.x);
+}
+
 // Per block column: the "rest" offset R over modes >= 2 and, for fiber blocks
 // of modes >= 2, the fixed mode-1 index.  Mirrors tensor.py:250-283
 // (decode_fiber_columns / fiber_base_offsets: other modes ascending, first
 // other mode fastest) and, for the core, the np.ix_ ordering of tensor.py:239.
-__global__ void k_colprep(Geom g, IndexPtrs ip, i64* __restrict__ colR_base, int* __restrict__ coli1_base,
-                          const i64* __restrict__ col_off) {
-  const int b = blockIdx.y;
-  if (b >= g.nblk) return;
+__device__ __forceinline__ void colprep_block(const Geom& g, const IndexPtrs& ip, i64* __restrict__ colR_base,
+                                              int* __restrict__ coli1_base, const i64* __restrict__ col_off, int b,
+                                              i64 t0, i64 tstride) {
   const BlockDesc bd = g.blk[b];
   i64* colR = colR_base + col_off[b];
   int* coli1 = coli1_base + col_off[b];
-  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < bd.Q; q += (i64)gridDim.x * blockDim.x) {
+  for (i64 q = t0; q < bd.Q; q += tstride) {
     i64 R = 0;
     int i1 = -1;
     if (bd.is_core) {
@@ -68,6 +72,24 @@ __global__ void k_colprep(Geom g, IndexPtrs ip, i64* __restrict__ colR_base, int
     colR[q] = R;
     coli1[q] = i1;
   }
+}
+
+__global__ void k_colprep(Geom g, IndexPtrs ip, i64* __restrict__ colR_base, int* __restrict__ coli1_base,
+                          const i64* __restrict__ col_off) {
+  const int b = blockIdx.y;
+  if (b >= g.nblk) return;
+  colprep_block(g, ip, colR_base, coli1_base, col_off, b, blockIdx.x * (i64)blockDim.x + threadIdx.x,
+                (i64)gridDim.x * blockDim.x);
+}
+
+// Both index preparations in one launch: grid rows y < n are k_rowpos's modes,
+// the rest k_colprep's blocks.
+__global__ void k_prep(Geom g, IndexPtrs ip, int* __restrict__ rowpos_base, i64* __restrict__ colR_base,
+                       int* __restrict__ coli1_base, const i64* __restrict__ col_off) {
+  const int y = blockIdx.y;
+  const i64 t0 = blockIdx.x * (i64)blockDim.x + threadIdx.x, ts = (i64)gridDim.x * blockDim.x;
+  if (y < g.n) rowpos_mode(g, ip, rowpos_base, y, t0, ts);
+  else if (y - g.n < g.nblk) colprep_block(g, ip, colR_base, coli1_base, col_off, y - g.n, t0, ts);
 }
 
 // ------------------------------------------------------------------ gather (sharded)
