@@ -112,6 +112,7 @@ struct Plan {
   i64 xi_off[RT_MAX_MODES], xi_ld[RT_MAX_MODES];   // intersection copies (elements) inside o_xi
   i64 o_xi;
   i64 o_fapart, fapart_cap;   // fiber-pass A-pass partials
+  i64 res_bytes;              // sums | flags | non-finite flag (contiguous from o_sums)
   int dtype;
   int esize;
   int rmax, rb;
@@ -469,8 +470,15 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     P.o_perm[m] = take(ranks[m] * 4);
     P.o_degen[m] = take((ranks[m] + 1) * 4);
   }
-  P.o_flags = take(n * 4);
-  P.o_nonfinite = take(4);
+  // the iteration's results in one contiguous range (one D2H per iteration):
+  // sums (2 nblk doubles) | flags (n ints, padded to 8 bytes) | non-finite flag
+  {
+    const i64 res0 = take(2 * g.nblk * 8 + ((n * 4 + 7) & ~7LL) + 8);
+    P.o_sums = res0;
+    P.o_flags = res0 + 2 * g.nblk * 8;
+    P.o_nonfinite = P.o_flags + ((n * 4 + 7) & ~7LL);
+    P.res_bytes = 2 * g.nblk * 8 + ((n * 4 + 7) & ~7LL) + 4;
+  }
   P.o_counters = take(64 * 4);
   P.o_absmax = take(8);
   {
@@ -502,7 +510,6 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     P.fapart_cap = P.fiber_mask ? (148 * 2 + n) * mx : 1;   // (up to two CTAs per SM, k_fiber.cuh)
     P.o_fapart = take(P.fapart_cap * 8);
   }
-  P.o_sums = take(2 * g.nblk * 8);
   P.o_fpart = take(148 * 8 * 2 * 8);
   P.o_dbg = take(8 * RT_MAX_MODES * 8);
   P.o_fast = take(RT_MAX_MODES * 4);
@@ -1503,9 +1510,8 @@ static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool r
   if ((st = run_factors(e, st_s, zeta, newslot))) return st;
   if ((st = run_block_pass(e, st_s, e->state(newslot), zeta, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
     return st;
-  CK(cudaMemcpyAsync(e->h_pinned, e->ws + P.o_sums, 2 * P.g.nblk * 8, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaMemcpyAsync(e->h_flags, e->ws + P.o_flags, n * 4, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaMemcpyAsync(e->h_flags + 16, e->ws + P.o_nonfinite, 4, cudaMemcpyDeviceToHost, e->st));
+  (void)n;
+  CK(cudaMemcpyAsync(e->h_pinned, e->ws + P.o_sums, P.res_bytes, cudaMemcpyDeviceToHost, e->st));
   return RT_OK;
 }
 
@@ -1596,9 +1602,13 @@ extern "C" int rtcur_engine_iterate_wait(rtcur_engine* e, double* sums, int* fla
   e->pending = false;
   CK(cudaEventSynchronize(e->done));
   prof_flush(e);
-  if (e->h_flags[16]) return fail(RT_ERR_VALUE, "truncated_svd input contains non-finite entries");
-  if (sums) memcpy(sums, e->h_pinned, 2 * e->P.g.nblk * 8);
-  if (flags) memcpy(flags, e->h_flags, e->P.g.n * 4);
+  const Plan& P = e->P;
+  const char* hr = reinterpret_cast<const char*>(e->h_pinned);
+  int nonfinite;
+  memcpy(&nonfinite, hr + (P.o_nonfinite - P.o_sums), 4);
+  if (nonfinite) return fail(RT_ERR_VALUE, "truncated_svd input contains non-finite entries");
+  if (sums) memcpy(sums, hr, 2 * P.g.nblk * 8);
+  if (flags) memcpy(flags, hr + (P.o_flags - P.o_sums), P.g.n * 4);
   return RT_OK;
 }
 
