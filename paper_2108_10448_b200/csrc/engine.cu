@@ -667,7 +667,7 @@ static int set_smem_limits_once() {
   SMEM_ATTR((k_block_pass<false, false, false, false, false, RB, true>))
   BP_ATTRS(4); BP_ATTRS(8); BP_ATTRS(16); BP_ATTRS(32);
 #undef BP_ATTRS
-  SMEM_ATTR(k_hgram<1>); SMEM_ATTR(k_hgram<2>);
+  SMEM_ATTR(k_hgram<1>); SMEM_ATTR(k_hgram<2>); SMEM_ATTR(k_hgram<3>);
 #undef SMEM_ATTR
   // L2 fetch granularity for the sampled gathers (element-sized loads scattered
   // over X): RTCUR_L2_FETCH=<32|64|128> bytes; unset leaves the device default
@@ -1251,12 +1251,10 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   const int zsm = (int)(P.smax * (P.rmax + ZP_T) * 8);
   DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(P.lmax, ZP_T), n), 32 * P.rb, zsm, e->st, sa);
   LAUNCH_CHECK();
-  const int hsm = (int)((HG_CH * P.rmax + 512) * 8);
-  // H = Z^T Z -> (last CTA) Rayleigh-Ritz rotation + short-side vectors
-  k_hgram<1><<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
-  LAUNCH_CHECK();
-  // Z <- Z Q, H' = Z^T Z -> (last CTA) sigma, order, cutoff, flags, T
-  k_hgram<2><<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
+  const int hsm = (int)((std::max<i64>(HG_CH * P.rmax + 512, 6 * P.rmax * P.rmax + 3 * P.rmax + 8)) * 8);
+  // H = Z^T Z -> (last CTA) Rayleigh-Ritz rotation, short-side vectors, then sigma,
+  // order, cutoff, flags and T' from H' = Q^T H Q
+  k_hgram<3><<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
   LAUNCH_CHECK();
   // long side Z T -> (last CTA) short-side permutation + completion
   DISPATCH_R(P.rb, k_long, dim3(gz, n), 256, 0, e->st, sa, hcnt + 8);
@@ -2069,10 +2067,8 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   const unsigned gz = (unsigned)cdiv(l, 256);
   DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(l, ZP_T), 1), 32 * P.rb, zs, st, sa);
   LAUNCH_CHECK();
-  const int hsm = (int)((HG_CH * r + 512) * 8);
-  k_hgram<1><<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
-  LAUNCH_CHECK();
-  k_hgram<2><<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
+  const int hsm = (int)((std::max<i64>(HG_CH * r + 512, 6 * (i64)r * r + 3 * r + 8)) * 8);
+  k_hgram<3><<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
   LAUNCH_CHECK();
   DISPATCH_R(P.rb, k_long, dim3(gz, 1), 256, 0, st, sa, hcnt + 8);
   LAUNCH_CHECK();

@@ -128,8 +128,11 @@ __global__ void __launch_bounds__(256) k_zrot(SvdArgs sa) {
 //       Rayleigh-Ritz rotation (svd_fin1_warp) and writes the short-side vectors.
 // PH 2: each CTA first rotates its Z rows by Q (Z <- Z Q, written back), H' = Z^T Z;
 //       the last CTA runs svd_fin2_warp (sigma, order, cutoff, flags, T).
+// PH 3: PH 1 and then the fin2 step on H' = Q^T H Q with T' = Q T (one launch; the
+//       long side is Z T' from the unrotated Z).
 __device__ void svd_fin1_warp(const SvdArgs& sa, int k);
 __device__ void svd_fin2_warp(const SvdArgs& sa, int k);
+__device__ void svd_fin2_ritz_warp(const SvdArgs& sa, int k, double* scr);
 __device__ void svd_short_vecs_cta(const SvdArgs& sa, int k, int t0, int stride);
 template <int PH>
 __global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counters) {
@@ -203,11 +206,15 @@ __global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counter
   if (tid == 0) counters[k] = 0u;
   __threadfence();
   __syncthreads();
-  if (PH == 1) {
+  if (PH == 1 || PH == 3) {
     if (tid < 32) svd_fin1_warp(sa, k);
     __threadfence();
     __syncthreads();
     svd_short_vecs_cta(sa, k, tid, blockDim.x);
+    if (PH == 3) {
+      __syncthreads();   // (the short-side vectors have read Q)
+      if (tid < 32) svd_fin2_ritz_warp(sa, k, hz);   // hz (the staged Z chunk) is free now
+    }
   } else {
     if (tid < 32) svd_fin2_warp(sa, k);
   }
@@ -330,14 +337,16 @@ __global__ void k_short_vecs(SvdArgs sa) {
 
 // sigma from ||z_a||, stable descending order, truncated-pinv reciprocals,
 // Cholesky orthonormalisation T (Z T orthonormal) over non-degenerate columns.
-__device__ void svd_fin2_warp(const SvdArgs& sa, int k) {
-  __shared__ double h[RT_MAX_RANK * RT_MAX_RANK];
-  __shared__ double R[RT_MAX_RANK * RT_MAX_RANK];
-  __shared__ double T[RT_MAX_RANK * RT_MAX_RANK];
-  __shared__ double X[RT_MAX_RANK * RT_MAX_RANK];
-  __shared__ double sg[RT_MAX_RANK];
-  __shared__ int ord[RT_MAX_RANK], dg[RT_MAX_RANK];
+// scratch: 4 r^2 + r doubles and 2 r ints (shared memory)
+__device__ void svd_fin2_warp_s(const SvdArgs& sa, int k, double* scratch) {
   const int r = sa.r[k], lane = threadIdx.x & 31;
+  double* h = scratch;
+  double* R = h + r * r;
+  double* T = R + r * r;
+  double* X = T + r * r;
+  double* sg = X + r * r;
+  int* ord = reinterpret_cast<int*>(sg + r);
+  int* dg = ord + r;
   for (int i = lane; i < r * r; i += 32) {
     h[i] = sa.H[k][i];
     R[i] = 0.0;
@@ -416,8 +425,57 @@ __device__ void svd_fin2_warp(const SvdArgs& sa, int k) {
   if (lane == 0) sa.degen[k][r] = anyd;
 }
 
+__device__ void svd_fin2_warp(const SvdArgs& sa, int k) {
+  __shared__ double scr[4 * RT_MAX_RANK * RT_MAX_RANK + 2 * RT_MAX_RANK];
+  svd_fin2_warp_s(sa, k, scr);
+}
+
 __global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
   if ((int)blockIdx.x < sa.n) svd_fin2_warp(sa, blockIdx.x);
+}
+
+// PH 3 tail: the fin2 step on H' = Q^T H Q (Q the Rayleigh-Ritz rotation, in
+// r x r arithmetic instead of a second pass over the rotated Z), then T' = Q T so
+// that the long side is Z T' straight from the unrotated projections.  `scr`:
+// shared scratch of 6 r^2 + r doubles + 2 r ints.
+__device__ void svd_fin2_ritz_warp(const SvdArgs& sa, int k, double* scr) {
+  const int r = sa.r[k], lane = threadIdx.x & 31;
+  double* q = scr;              // Q (r x r, column-major)
+  double* hq = q + r * r;       // H Q
+  double* f2 = hq + r * r;      // fin2 scratch (4 r^2 + r doubles, 2 r ints)
+  const double* H = sa.H[k];
+  for (int e = lane; e < r * r; e += 32) q[e] = sa.Q[k][e];
+  __syncwarp();
+  for (int e = lane; e < r * r; e += 32) {   // (H Q)[i, j]
+    const int i = e % r, j = e / r;
+    double v = 0.0;
+    for (int p = 0; p < r; ++p) v = fma(H[i + p * r], q[p + j * r], v);
+    hq[e] = v;
+  }
+  __syncwarp();
+  for (int e = lane; e < r * r; e += 32) {   // H' = Q^T (H Q), symmetrised
+    const int i = e % r, j = e / r;
+    if (i > j) continue;
+    double v = 0.0, w = 0.0;
+    for (int p = 0; p < r; ++p) {
+      v = fma(q[p + i * r], hq[p + j * r], v);
+      w = fma(q[p + j * r], hq[p + i * r], w);
+    }
+    const double hv = 0.5 * (v + w);
+    sa.H[k][i + j * r] = hv;
+    sa.H[k][j + i * r] = hv;
+  }
+  __syncwarp();
+  svd_fin2_warp_s(sa, k, f2);   // sa.Q <- T
+  __syncwarp();
+  for (int e = lane; e < r * r; e += 32) {   // T' = Q T into hq, then out
+    const int i = e % r, j = e / r;
+    double v = 0.0;
+    for (int p = 0; p < r; ++p) v = fma(q[i + p * r], sa.Q[k][p + j * r], v);
+    hq[e] = v;
+  }
+  __syncwarp();
+  for (int e = lane; e < r * r; e += 32) sa.Q[k][e] = hq[e];
 }
 
 // long-side vectors: out[t, a] = sum_b Z[t, b] T[b, a]; short side permuted in place later
