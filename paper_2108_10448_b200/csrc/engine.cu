@@ -1208,7 +1208,12 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   ga.maxpairs = P.gram_maxpairs;
   ga.cl = P.gram_cl;
   prof_begin(e, PH_GRAM);
-  k_gram_tiles<<<dim3(P.gram_maxpairs, P.gram_maxchunks, n), 256, 0, e->st>>>(ga);
+  {
+    // fp64 tensor cores (DMMA) unless RTCUR_GRAM_DMMA=0
+    static const bool dmma = [] { const char* v = getenv("RTCUR_GRAM_DMMA"); return !(v && v[0] == '0'); }();
+    if (dmma) k_gram_tiles_dmma<<<dim3(P.gram_maxpairs, P.gram_maxchunks, n), 128, 0, e->st>>>(ga);
+    else k_gram_tiles<<<dim3(P.gram_maxpairs, P.gram_maxchunks, n), 256, 0, e->st>>>(ga);
+  }
   LAUNCH_CHECK();
   {
     const i64 npk = P.smax * (P.smax + 1) / 2;

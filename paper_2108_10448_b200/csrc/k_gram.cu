@@ -116,6 +116,96 @@ __global__ void __launch_bounds__(256) k_gram_tiles(GramArgs ga) {
     for (int j = 0; j < 4; ++j) out[(ty * 4 + i) * GRAM_T + tx + 16 * j] = acc[i][j];
 }
 
+// The same 64 x 64 split-K tiles on the fp64 tensor cores: mma.sync m8n8k4 f64
+// (DMMA).  4 warps as 2 x 2, each a 32 x 32 sub-tile = 4 x 4 mma tiles (32 fp64
+// accumulators per thread); per k-step of 4: 4 A and 4 B fragments (one double per
+// lane each) feed 16 DMMAs.  Fragment layout (PTX m8n8k4 .f64, row.col):
+//   A[g][t], B[t][g], C[g][2t + {0,1}], g = lane / 4, t = lane % 4.
+// Shared rows padded to 68 doubles (the 4 k-rows of a fragment load hit distinct
+// banks).  Partials go to the same layout as k_gram_tiles (k_gram_reduce sums them).
+#define GRAM_LDS 68
+__global__ void __launch_bounds__(128) k_gram_tiles_dmma(GramArgs ga) {
+  const int k = blockIdx.z;
+  if (k >= ga.n) return;
+  const int s = ga.s[k];
+  const i64 l = ga.l[k];
+  const int nt = (s + GRAM_T - 1) / GRAM_T;
+  const int npairs = nt * (nt + 1) / 2;
+  const int pair = blockIdx.x;
+  if (pair >= npairs) return;
+  const i64 t0 = (i64)blockIdx.y * ga.cl;
+  if (t0 >= l) return;
+  const i64 t1 = min(l, t0 + ga.cl);
+  int I, J;
+  pair_decode(pair, I, J);
+  __shared__ __align__(16) double As[2][GRAM_KS][GRAM_LDS];
+  __shared__ __align__(16) double Bs[2][GRAM_KS][GRAM_LDS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wr = (w >> 1) * 32, wc = (w & 1) * 32;   // warp sub-tile origin
+  const int g = lane >> 2, tq = lane & 3;
+  double c[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  constexpr int PER = GRAM_T * GRAM_KS / 128;   // elements per thread per operand
+  double pa[PER], pb[PER];
+  auto fetch = [&](i64 tt) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * 128;
+      const int r = idx % GRAM_T, kk = idx / GRAM_T;
+      const i64 t = tt + kk;
+      const int a = I * GRAM_T + r, b = J * GRAM_T + r;
+      pa[u] = (a < s && t < t1) ? gram_B(ga, k, a, t) : 0.0;
+      pb[u] = (b < s && t < t1) ? gram_B(ga, k, b, t) : 0.0;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = threadIdx.x + u * 128;
+      const int r = idx % GRAM_T, kk = idx / GRAM_T;
+      As[buf][kk][r] = pa[u];
+      Bs[buf][kk][r] = pb[u];
+    }
+  };
+  fetch(t0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (i64 tt = t0; tt < t1; tt += GRAM_KS) {
+    const bool more = tt + GRAM_KS < t1;
+    if (more) fetch(tt + GRAM_KS);
+#pragma unroll
+    for (int ks = 0; ks < GRAM_KS; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][ks + tq][wr + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks + tq][wc + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(c[i][j][0]), "+d"(c[i][j][1])
+                       : "d"(af[i]), "d"(bf[j]));
+    }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  double* out = ga.part + (((i64)k * ga.maxchunks + blockIdx.y) * ga.maxpairs + pair) * (GRAM_T * GRAM_T);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double2* o = reinterpret_cast<double2*>(out + (wr + i * 8 + g) * GRAM_T + wc + j * 8 + 2 * tq);
+      *o = make_double2(c[i][j][0], c[i][j][1]);
+    }
+}
+
 // Sum the split-K partials (warp per output, fixed butterfly order) into packed lower K.
 __global__ void __launch_bounds__(256) k_gram_reduce(GramArgs ga) {
   const int k = blockIdx.y;
