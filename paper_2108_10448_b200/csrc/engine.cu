@@ -109,6 +109,8 @@ struct Plan {
   TileMap tm_core; // threshold/error passes on k_block_pass: the blocks the fiber pass does not take
   TileMap tm_thr;  // threshold pass on k_block_pass: only fiber blocks (the core yields nothing there)
   unsigned fiber_mask;   // blocks handled by the TMA fiber pass (k_fiber.cuh)
+  unsigned fb_thr, fb_ap, fb_err;   // per pass (RTCUR_FB_PASSES bits 1/2/4 switch passes off for A/B runs)
+  TileMap tm_ap;   // A pass on k_block_pass: the fiber blocks the fiber pass does not take
   i64 xi_off[RT_MAX_MODES], xi_ld[RT_MAX_MODES];   // intersection copies (elements) inside o_xi
   i64 o_xi;
   i64 o_fapart, fapart_cap;   // fiber-pass A-pass partials
@@ -329,15 +331,31 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   // fiber blocks on the TMA fiber pass; k_block_pass keeps the core (and any block outside its envelope)
   P.fiber_mask = fiber_pass_blocks(g, dtype);
   {
+    const char* fp = getenv("RTCUR_FB_PASSES");
+    const int bits = fp ? atoi(fp) : 7;
+    P.fb_thr = (bits & 1) ? P.fiber_mask & ~1u : 0u;
+    P.fb_ap = (bits & 2) ? P.fiber_mask & ~1u : 0u;
+    P.fb_err = (bits & 4) ? P.fiber_mask : 0u;
+  }
+  {
     TileMap& tc = P.tm_core;
     tc = P.tm;
     i64 t = 0;
     for (int b = 0; b < g.nblk; ++b) {
       const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
       tc.first[b] = t;
-      if (!(P.fiber_mask >> b & 1)) t += nt;
+      if (!(P.fb_err >> b & 1)) t += nt;
     }
     tc.first[g.nblk] = t;
+    TileMap& ta = P.tm_ap;
+    ta = P.tm;
+    t = 0;
+    for (int b = 0; b < g.nblk; ++b) {
+      const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
+      ta.first[b] = t;
+      if (!(P.fb_ap >> b & 1)) t += nt;
+    }
+    ta.first[g.nblk] = t;
     // threshold pass: M_k comes from fiber blocks only; the core's clean values are
     // recomputed by the G pass, so k_block_pass needs no core tiles there
     TileMap& tt = P.tm_thr;
@@ -346,7 +364,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     for (int b = 0; b < g.nblk; ++b) {
       const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
       tt.first[b] = t;
-      if (b > 0 && !(P.fiber_mask >> b & 1)) t += nt;
+      if (b > 0 && !(P.fb_thr >> b & 1)) t += nt;
     }
     tt.first[g.nblk] = t;
   }
@@ -489,13 +507,14 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
       i64 tot = 0;
       for (int b = 1; b < P.g.nblk; ++b) {
         if (N <= 0 || tmx.first[b + 1] == tmx.first[b]) continue;
-        const i64 c0 = ap_cta_of(tmx.first[b] - tmx.first[1], N, P.ap_grid);
-        const i64 c1 = ap_cta_of(tmx.first[b + 1] - 1 - tmx.first[1], N, P.ap_grid);
+        const i64 G = std::max<i64>(1, std::min<i64>(P.ap_grid, N));   // (run_factors' grid)
+        const i64 c0 = ap_cta_of(tmx.first[b] - tmx.first[1], N, G);
+        const i64 c1 = ap_cta_of(tmx.first[b + 1] - 1 - tmx.first[1], N, G);
         tot += (c1 - c0 + 1) * P.g.blk[b].P * P.g.blk[b].r;
       }
       return tot;
     };
-    P.o_apart2 = take(std::max<i64>(1, std::max(slots(P.tm), slots(P.tm_core))) * 8);
+    P.o_apart2 = take(std::max<i64>(1, std::max(slots(P.tm), slots(P.tm_ap))) * 8);
   }
   P.o_gt0 = take(P.g_tmp * 8);
   P.o_gt1 = take(P.g_tmp * 8);
@@ -1110,7 +1129,7 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   const i64 smb = bp_smem_bytes(P.bp);
   const bool hs = st_s != nullptr, he = st_e != nullptr;
   // the fiber blocks of the threshold / error passes go to the TMA fiber pass; exports stay here
-  const bool split = P.fiber_mask && !(s_out || c_out || l_out) && (with_M || sums);
+  const bool split = !(s_out || c_out || l_out) && ((with_M && !sums && P.fb_thr) || (sums && P.fb_err));
   const bool thr_only = with_M && !sums && !(s_out || c_out || l_out);
   const TileMap& tmk = thr_only ? P.tm_thr : split ? P.tm_core : P.tm;
 #define BP_LAUNCH(HS, HE, WM, EXP)                                                                        \
@@ -1141,6 +1160,7 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   if (lst) return lst;
   if (split) {
     FiberLaunch fl = make_fl(e, e->act_slot());
+    fl.mask = sums ? P.fb_err : P.fb_thr;
     fl.st_s = st_s;
     fl.st_e = st_e;
     fl.zeta = zeta;
@@ -1370,8 +1390,8 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   // the block-pass A pass when some fiber block is outside its envelope
   unsigned all_fibers = 0;
   for (int b = 1; b < g.nblk; ++b) all_fibers |= 1u << b;
-  if ((P.fiber_mask & all_fibers) != all_fibers) {
-    const TileMap& tma = P.tm_core;   // the fiber blocks the fiber pass does not take (plus the core, unused)
+  if ((P.fb_ap & all_fibers) != all_fibers) {
+    const TileMap& tma = P.tm_ap;   // the fiber blocks the fiber pass does not take
     // A_k = C_k V_k S_k^+ on the block-pass tiles (fiber blocks), then the fixed-order reduction
     PassArgs pa;
     memset(&pa, 0, sizeof(pa));
@@ -1385,13 +1405,16 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
       pa.siginv[m] = e->at<double>(P.o_siginv[m]);
     }
     pa.apart = e->at<double>(P.o_apart2);
-    pa.ap_grid = P.ap_grid;
+    // never more CTAs than the map's fiber tiles: a CTA with an empty tile range would
+    // leave its partial slot unwritten while the reduction reads it
+    const int apg = (int)std::max<i64>(1, std::min<i64>(P.ap_grid, tma.first[g.nblk] - tma.first[1]));
+    pa.ap_grid = apg;
     pa.nonfinite = e->at<int>(P.o_nonfinite);
     const i64 smb = bp_smem_bytes(P.bp_ap);
 #define AP_LAUNCH(RB)                                                                                  \
-  (st_s ? launch_ap(k_block_pass<true, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, tma, ip, pa, \
+  (st_s ? launch_ap(k_block_pass<true, false, false, false, false, RB, true>, apg, P.ap_threads, smb, e->st, g, tma, ip, pa, \
                     P.bp_ap)                                                                             \
-        : launch_ap(k_block_pass<false, false, false, false, false, RB, true>, P.ap_grid, P.ap_threads, smb, e->st, g, tma, ip, pa, \
+        : launch_ap(k_block_pass<false, false, false, false, false, RB, true>, apg, P.ap_threads, smb, e->st, g, tma, ip, pa, \
                     P.bp_ap))
     int lst;
     switch (P.rb) {
@@ -1407,8 +1430,9 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     k_areduce_bp<<<dim3((unsigned)std::min<i64>(cdiv(maxpr, 256), 1024), g.nblk - 1), 256, 0, e->st>>>(g, tma, pa, sto);
     LAUNCH_CHECK();
   }
-  if (P.fiber_mask) {
+  if (P.fb_ap) {
     FiberLaunch fl = make_fl(e, e->act_slot());
+    fl.mask = P.fb_ap;
     fl.st_s = st_s;
     fl.zeta = zeta;
     fl.zetap = e->zetap_cur;

@@ -29,6 +29,7 @@ struct FiberLaunch {
   double* apart;
   i64 apart_cap;                   // doubles available at apart
   double* a_out;
+  unsigned mask;                   // blocks to process (0: every block fiber_pass_blocks takes)
 };
 
 // Blocks (bit b = block b) the fiber pass handles for this geometry: fiber

@@ -24,7 +24,7 @@ unsigned fiber_pass_blocks(const Geom& g, int dtype) {
 }
 
 int fiber_pass_launch(const FiberLaunch& L, cudaStream_t st) {
-  const unsigned mask = fiber_pass_blocks(L.g, L.dtype);
+  const unsigned mask = L.mask ? L.mask : fiber_pass_blocks(L.g, L.dtype);
   if (!mask) return 0;
   return L.dtype == 0 ? fb_launch_t<double>(L, mask, st) : fiber_pass_launch_f32(L, mask, st);
 }

@@ -264,3 +264,23 @@ for case in ("bern_R", "d20_F", "n4_R", "tall_F"):
         assert a[:3] == b[:3], (a[:3], b[:3])   # case, iterations, support size
         assert float(a[3]) == pytest.approx(float(b[3]), rel=1e-9, abs=1e-300)
         np.testing.assert_allclose(eval(a[4]), eval(b[4]), rtol=1e-9, atol=0)
+
+
+def test_solve_on_recycled_device_memory():
+    """Regression for reads of never-written workspace: fill the caching allocator's
+    memory with junk first, then solve a fresh geometry whose blocks split between the
+    fiber pass and the block pass (a mode-3 fiber block with 4-byte-misaligned columns)
+    and compare with the fp64 oracle (iterations, error history, support)."""
+    junk = torch.full((96 * 1024 * 1024,), 12345.678, dtype=torch.float64, device="cuda")
+    del junk
+    shape, ranks = (44, 36, 30), (3, 2, 3)
+    xf, _, _ = make_gaussian_tucker(shape, ranks, 0.2, 10.0, seed=23, dtype=np.float32)
+    rows, cols = baseline_sample_sizes(shape, ranks)
+    kw = dict(eps=1e-5, variant="F", max_iters=100, seed=5, row_sample_sizes=rows, col_sample_sizes=cols)
+    res = rtcur(DeviceTensor(torch.from_numpy(xf).cuda(), shape), SolverConfig(ranks=ranks, **kw))
+    ref = orc.solve(xf.astype(np.float64), shape, ranks, **kw)
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    np.testing.assert_allclose(res.error_history, ref.error_history, atol=1e-10, rtol=0)
+    assert np.array_equal(_flat(res.sparse.core) != 0, _flat(ref.s_core) != 0)
+    for m in range(3):
+        assert np.array_equal(res.sparse.fibers[m] != 0, ref.s_fibers[m] != 0)

@@ -1,0 +1,18 @@
+"""Poisoned-allocator A-pass check: factors after one iteration, saved for comparison
+between RTCUR_FB_PASSES settings (argv[1]: output .npy prefix)."""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+from paper_2108_10448_b200 import DeviceTensor, SolverConfig, rtcur
+from paper_2108_10448_b200.synth import baseline_sample_sizes, make_gaussian_tucker
+
+junk = torch.full((64 * 1024 * 1024,), 12345.678, dtype=torch.float64, device="cuda")
+del junk
+shape, ranks = (40, 36, 30), (3, 3, 3)
+xf, _, _ = make_gaussian_tucker(shape, ranks, 0.2, 10.0, seed=21, dtype=np.float32)
+rows, cols = baseline_sample_sizes(shape, ranks)
+kw = dict(eps=1e-5, variant="F", max_iters=1, seed=4, row_sample_sizes=rows, col_sample_sizes=cols)
+res = rtcur(DeviceTensor(torch.from_numpy(xf).cuda(), shape), SolverConfig(ranks=ranks, **kw))
+for m in range(3):
+    np.save(f"gpurun_out/{sys.argv[1]}_f{m}.npy", np.asarray(res.cur.factors[m]))
