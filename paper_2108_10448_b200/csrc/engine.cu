@@ -1257,6 +1257,10 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   }
   ea.tmark = e->at<long long>(P.o_dbg);
   ea.max_sub_steps = 24;
+  {
+    static const int msw = [] { const char* v = getenv("RTCUR_EIG_MS_WARPS"); return v ? std::max(1, atoi(v)) : 1; }();
+    ea.ms_warps = msw;
+  }
   ea.fast_used = e->at<int>(P.o_fast);
   IndexPtrs ipw = make_ip(e);
   for (int m = 0; m < n; ++m) {

@@ -44,6 +44,7 @@ struct EigArgs {
   const int* warm_rows[RT_MAX_MODES];  // current row set I_k (0-based)
   i64 warm_d[RT_MAX_MODES];
   int max_sub_steps;
+  int ms_warps;                        // multisection: max warps per eigenvalue (shifts = 64 x warps)
   int* fast_used;                      // per mode: 1 if the fast path certified the subspace
 };
 
@@ -719,7 +720,9 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
     double* bhi = red2;                 // 2 x 16 warp brackets (hi)
     for (int j0 = 0; j0 < r; j0 += nw) {
       const int rr = min(nw, r - j0);
-      const int ng = nw / rr;
+      // the counts are fp64-pipe bound on this one SM: more shifts per round cost more
+      // than the rounds they save beyond ~one warp per eigenvalue
+      const int ng = max(1, min(nw / rr, ea.ms_warps));
       const int j = j0 + wid / ng, g = wid % ng;
       const bool act = wid < rr * ng;
       const double nsh = (double)(ng * 64 + 1);
