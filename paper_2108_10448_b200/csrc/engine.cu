@@ -1349,7 +1349,10 @@ static int run_wcols(rtcur_engine* e, double* sto) {
     rsmax = std::max(rsmax, rs);
   }
   // lanes per column: a warp for many combinations, 8 lanes (4 columns per warp) for a few
-  const int gs = ncmax >= 48 ? 32 : 8;
+  static const int gs_env = [] { const char* v = getenv("RTCUR_WC_GS"); return v ? atoi(v) : 0; }();
+  // (8 lanes also when each column has many outputs: the per-output shuffle trees
+  // dominate; measured: configs 2/3 wcols -21/-27 %, config 4 (r = 4) better on 32)
+  const int gs = (gs_env == 8 || gs_env == 32) ? gs_env : ((ncmax >= 48 && P.rb < 8) ? 32 : 8);
   const int ngrp = 32 * WC_WARPS / gs;
   const int rows_cap = (int)(cdiv(rsmax, gs) * gs);
   const i64 wsm = (g.gsize + (ncmax * 4 + ncmax * std::max(1, g.n - 1) + 7) / 8 + 1 + (i64)ngrp * rows_cap) * 8;
