@@ -223,12 +223,13 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
       f2 = fma(v, v, f2);
     }
   } else {
-    for (int e = tid; e < s * (s + 1) / 2; e += blockDim.x) {
-      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      while (i * (i + 1) / 2 > e) --i;
-      const double v = A[e];
-      f2 = fma(v, v * (e - i * (i + 1) / 2 == i ? 1.0 : 2.0), f2);
+    // packed rows by warps, lanes across the row (off-diagonal entries count twice)
+    for (int i = wid; i < s; i += nw) {
+      const double* row = A + pk(i, 0);
+      for (int j = lane; j <= i; j += 32) {
+        const double v = row[j];
+        f2 = fma(v, v * (j == i ? 1.0 : 2.0), f2);
+      }
     }
   }
   t = warp_sum(t);

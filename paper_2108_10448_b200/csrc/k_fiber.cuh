@@ -487,7 +487,11 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
       unit = unit / a * au;
     }
     const i64 colb = H[f] * E + (i64)NS * I.r * 8;
-    i64 CB = std::max<i64>(1, FB_STAGE_BYTES / colb) / unit * unit;
+    static const i64 stage_bytes = [] {
+      const char* v = getenv("RTCUR_FB_STAGE_KB");
+      return v ? std::max<i64>(1, atoll(v)) * 1024 : (i64)FB_STAGE_BYTES;
+    }();
+    i64 CB = std::max<i64>(1, stage_bytes / colb) / unit * unit;
     if (CB == 0) CB = unit;
     B.CB = (int)CB;
     const i64 nbands = (I.P + H[f] - 1) / H[f];
