@@ -396,6 +396,24 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     const i64 want = std::max<i64>(1, cdiv(waves * 148, pairs_tot));
     P.gram_cl = (int)std::max<i64>(std::min<i64>(mincl, cdiv(lm, GRAM_KS) * GRAM_KS),
                                    cdiv(cdiv(lm, want), GRAM_KS) * GRAM_KS);
+    if (!gw && !gm) {
+      // wave-quantised choice: the DMMA tile kernel runs 3 CTAs per SM (168
+      // registers x 128 threads, 34.8 KB static shared memory); minimise
+      // ceil(CTAs / (3 x 148)) x (chunk length + a fixed per-CTA cost of ~32
+      // columns) over chunk lengths in k-steps (a 2.03-wave grid costs 3 waves)
+      const i64 slots = 3 * 148, c0 = 32;
+      i64 best = -1, bcl = P.gram_cl;
+      for (i64 cl = GRAM_KS; cl <= cdiv(lm, GRAM_KS) * GRAM_KS; cl += GRAM_KS) {
+        i64 ctas = 0;
+        for (int m = 0; m < n; ++m) {
+          const i64 nt = cdiv(P.s[m], GRAM_T);
+          ctas += nt * (nt + 1) / 2 * cdiv(P.l[m], cl);
+        }
+        const i64 cost = cdiv(ctas, slots) * (cl + c0);
+        if (best < 0 || cost <= best) { best = cost; bcl = cl; }   // ties: longer chunks, fewer partials
+      }
+      P.gram_cl = (int)bcl;
+    }
   }
   for (int m = 0; m < n; ++m) {
     const int nt = (int)cdiv(P.s[m], GRAM_T);
