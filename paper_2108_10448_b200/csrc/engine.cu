@@ -1295,7 +1295,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   SvdArgs sa = make_svd_args(e);
   unsigned int* hcnt = e->at<unsigned int>(P.o_counters) + 16;
   const unsigned gz = (unsigned)cdiv(P.lmax, 256);
-  const int zsm = (int)(P.smax * (P.rmax + ZP_T) * 8);
+  const int zsm = (int)(P.smax * (P.rmax + ZP_LD) * 8);
   DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(P.lmax, ZP_T), n), 32 * P.rb, zsm, e->st, sa);
   LAUNCH_CHECK();
   const int hsm = (int)((std::max<i64>(HG_CH * P.rmax + 512, 6 * P.rmax * P.rmax + 3 * P.rmax + 8)) * 8);
@@ -2085,7 +2085,7 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
     int st2 = set_smem_limits_once();
     if (st2) return st2;
   }
-  const int zs = (int)(s * (r + ZP_T) * 8);
+  const int zs = (int)(s * (r + ZP_LD) * 8);
   GramArgs ga;
   memset(&ga, 0, sizeof(ga));
   ga.n = 1;

@@ -51,6 +51,7 @@ __device__ __forceinline__ double svd_B(const SvdArgs& sa, int k, i64 c, i64 t) 
 // s x ZP_T slab of B and E (s x r) are staged in shared memory; thread
 // (tl, a) = (tid % ZP_T, tid / ZP_T) reduces over c.
 #define ZP_T 32
+#define ZP_LD (ZP_T + 1)   // padded slab row: the wide-case transpose store is conflict-free
 template <int R>
 __global__ void __launch_bounds__(32 * R) k_zproj(SvdArgs sa) {
   extern __shared__ double es[];
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(32 * R) k_zproj(SvdArgs sa) {
   const i64 t0 = (i64)blockIdx.x * ZP_T;
   if (t0 >= l) return;
   const int nt = (int)min((i64)ZP_T, l - t0);
-  double* bs = es + s * r;   // s x ZP_T
+  double* bs = es + s * r;   // s x ZP_LD
   for (int i = threadIdx.x; i < s * r; i += blockDim.x) es[i] = sa.E[k][i];
   const double* M = sa.M[k];
   const i64 mr = sa.mrows[k];
@@ -69,13 +70,13 @@ __global__ void __launch_bounds__(32 * R) k_zproj(SvdArgs sa) {
     // B[c, t] = M[t + c*m]: t contiguous
     for (int i = threadIdx.x; i < s * ZP_T; i += blockDim.x) {
       const int tl = i % ZP_T, c = i / ZP_T;
-      bs[c * ZP_T + tl] = tl < nt ? M[t0 + tl + (i64)c * mr] : 0.0;
+      bs[c * ZP_LD + tl] = tl < nt ? M[t0 + tl + (i64)c * mr] : 0.0;
     }
   } else {
     // B[c, t] = M[c + t*m]: c contiguous
     for (int i = threadIdx.x; i < s * ZP_T; i += blockDim.x) {
       const int c = i % s, tl = i / s;
-      bs[c * ZP_T + tl] = tl < nt ? M[c + (t0 + tl) * mr] : 0.0;
+      bs[c * ZP_LD + tl] = tl < nt ? M[c + (t0 + tl) * mr] : 0.0;
     }
   }
   __syncthreads();
@@ -85,10 +86,10 @@ __global__ void __launch_bounds__(32 * R) k_zproj(SvdArgs sa) {
   double z0 = 0.0, z1 = 0.0;
   int c = 0;
   for (; c + 1 < s; c += 2) {
-    z0 = fma(ea[c], bs[c * ZP_T + tl], z0);
-    z1 = fma(ea[c + 1], bs[(c + 1) * ZP_T + tl], z1);
+    z0 = fma(ea[c], bs[c * ZP_LD + tl], z0);
+    z1 = fma(ea[c + 1], bs[(c + 1) * ZP_LD + tl], z1);
   }
-  if (c < s) z0 = fma(ea[c], bs[c * ZP_T + tl], z0);
+  if (c < s) z0 = fma(ea[c], bs[c * ZP_LD + tl], z0);
   sa.Z[k][(t0 + tl) * r + a] = z0 + z1;
 }
 
