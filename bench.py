@@ -133,6 +133,25 @@ def _algorithmic_bytes(bc, rows, cols):
     }, n_blk
 
 
+FP64_PEAK_TFMA = 18.5   # measured fp64 FMA-pipe rate (DFMA and DMMA share it): profiles/r01_fp64_pipes.txt
+
+
+def _fp64_fmas(bc, rows, cols):
+    """Per-launch fp64 FMAs of the fiber-pass phases (the reconstruction L = A_k(I,:) W_k(:, j)
+    is r_k FMAs per entry and state): error = 2 r_k + 2 per block entry (previous and new
+    iterate, two sums; the core rides with mode 1), A pass = 2 r_k per fiber entry (previous
+    iterate + the C V accumulation), threshold = r_k per intersection entry."""
+    n_core = int(np.prod(rows))
+    fib = [d * c for d, c in zip(bc.shape, cols)]
+    inter = [r * c for r, c in zip(rows, cols)]
+    rk = list(bc.ranks)
+    return {
+        "error": n_core * (2 * rk[0] + 2) + sum(f * (2 * r + 2) for f, r in zip(fib, rk)),
+        "apass": sum(f * 2 * r for f, r in zip(fib, rk)),
+        "threshold": sum(i * r for i, r in zip(inter, rk)),
+    }
+
+
 def run_reference(args):
     world, rank, _ = _dist()
     if rank != 0:
@@ -412,6 +431,12 @@ def run_b200(args):
             "alg_bytes_per_launch": alg[dom], "launch_us": 1e3 * per_launch_ms, "launches_timed": dom_n,
             "peak_source": peak_src,
             "share_of_device_time": phases[dom]["share"] if dom in phases else None}
+    fmas = _fp64_fmas(bc, rows, cols)
+    if dom in fmas:   # the same launch against the fp64 pipe (the fiber passes sit near the ridge)
+        tf = fmas[dom] / (per_launch_ms / 1e3) / 1e12
+        roof["fp64"] = {"achieved": tf, "peak": FP64_PEAK_TFMA, "unit": "TFMA/s", "frac": tf / FP64_PEAK_TFMA,
+                        "fma_per_launch": fmas[dom],
+                        "peak_source": "measured: tools/fp64_pipes.cu (profiles/r01_fp64_pipes.txt)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
