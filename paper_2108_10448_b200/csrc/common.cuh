@@ -10,6 +10,26 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Raise a kernel's dynamic shared-memory limit to the device's opt-in maximum
+// (minus its static shared memory), once per kernel.  Per-launch
+// cudaFuncSetAttribute calls with the launch's own size race between host
+// threads launching the same kernel with different sizes (a second thread can
+// lower the limit between the first thread's set and launch: "invalid argument").
+template <auto Kernel>   // one static per kernel (not per signature)
+inline cudaError_t raise_dyn_smem_once() {
+  static const cudaError_t err = [] {
+    int dev = 0, optin = 227 * 1024;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, Kernel);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    return e;
+  }();
+  return err;
+}
+
 #define RT_MAX_MODES 8
 #define RT_MAX_BLOCKS (RT_MAX_MODES + 1)
 #define RT_MAX_RANK 32

@@ -519,7 +519,7 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
   const int smem = 2 * FB_MAX_STAGES * 8 + (int)(fa.nst * stage);
   if (smem > 227 * 1024) return -(int)cudaErrorInvalidConfiguration;
   auto K = k_fiber_pass<T, R, EX, HS, HE, AP, SC>;
-  cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = raise_dyn_smem_once<k_fiber_pass<T, R, EX, HS, HE, AP, SC>>();
   if (e != cudaSuccess) return -(int)e;
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K, ncons + 32, smem) != cudaSuccess || per_sm < 1)

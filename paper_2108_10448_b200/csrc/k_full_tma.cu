@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(FT_MAX_CONSUMERS + 32, 1) k_full_tma(FullTmaAr
 template <typename T, int R, int V>
 static int launch_one(const FullTmaArgs& ta, int grid, int threads, int smem, cudaStream_t st) {
   auto F = k_full_tma<T, R, V>;
-  cudaError_t e = cudaFuncSetAttribute(F, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = raise_dyn_smem_once<k_full_tma<T, R, V>>();
   if (e != cudaSuccess) return -(int)e;
   F<<<grid, threads, smem, st>>>(ta);
   e = cudaGetLastError();
