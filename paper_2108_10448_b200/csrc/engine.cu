@@ -1298,7 +1298,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   const int zsm = (int)(P.smax * (P.rmax + ZP_LD) * 8);
   DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(P.lmax, ZP_T), n), 32 * P.rb, zsm, e->st, sa);
   LAUNCH_CHECK();
-  const int hsm = (int)((std::max<i64>(HG_CH * P.rmax + 512, 6 * P.rmax * P.rmax + 3 * P.rmax + 8)) * 8);
+  const int hsm = (int)((std::max<i64>(HG_CH * P.rmax + 512, 7 * P.rmax * P.rmax + 3 * P.rmax + 8)) * 8);
   // H = Z^T Z -> (last CTA) Rayleigh-Ritz rotation, short-side vectors, then sigma,
   // order, cutoff, flags and T' from H' = Q^T H Q
   k_hgram<3><<<dim3(P.h_maxchunks, n), 512, hsm, e->st>>>(sa, hcnt);
@@ -2121,7 +2121,7 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   const unsigned gz = (unsigned)cdiv(l, 256);
   DISPATCH_R(P.rb, k_zproj, dim3((unsigned)cdiv(l, ZP_T), 1), 32 * P.rb, zs, st, sa);
   LAUNCH_CHECK();
-  const int hsm = (int)((std::max<i64>(HG_CH * r + 512, 6 * (i64)r * r + 3 * r + 8)) * 8);
+  const int hsm = (int)((std::max<i64>(HG_CH * r + 512, 7 * (i64)r * r + 3 * r + 8)) * 8);
   k_hgram<3><<<dim3(P.h_maxchunks, 1), 512, hsm, st>>>(sa, hcnt);
   LAUNCH_CHECK();
   DISPATCH_R(P.rb, k_long, dim3(gz, 1), 256, 0, st, sa, hcnt + 8);

@@ -339,7 +339,36 @@ __global__ void k_short_vecs(SvdArgs sa) {
 // sigma from ||z_a||, stable descending order, truncated-pinv reciprocals,
 // Cholesky orthonormalisation T (Z T orthonormal) over non-degenerate columns.
 // scratch: 4 r^2 + r doubles and 2 r ints (shared memory)
-__device__ void svd_fin2_warp_s(const SvdArgs& sa, int k, double* scratch) {
+// Stable descending order of v[0..r) by one warp: lane i's rank is the number of
+// entries greater than v[i] plus the equal ones before it (the insertion sort's
+// order); any NaN falls back to lane 0's insertion sort.
+__device__ __forceinline__ void warp_order_desc(const double* v, int r, int* ord) {
+  const int lane = threadIdx.x & 31;
+  const bool nan = lane < r && isnan(v[lane]);
+  if (__any_sync(0xffffffffu, nan)) {
+    if (lane == 0) {
+      for (int i = 0; i < r; ++i) ord[i] = i;
+      for (int i = 1; i < r; ++i) {
+        const int t = ord[i];
+        int j = i - 1;
+        while (j >= 0 && v[ord[j]] < v[t]) { ord[j + 1] = ord[j]; --j; }
+        ord[j + 1] = t;
+      }
+    }
+  } else if (lane < r) {
+    const double x = v[lane];
+    int rank = 0;
+    for (int j = 0; j < r; ++j) rank += (v[j] > x) || (v[j] == x && j < lane);
+    ord[rank] = lane;
+  }
+  __syncwarp();
+}
+
+// hsrc: H (r x r) in shared memory, or null to read sa.H.  The normalised
+// Cholesky runs right-looking with lanes over columns: every entry sees the same
+// subtractions in the same order (and the same divisions) as the column-by-column
+// form, so the factor is bit-identical to it.  T is left in scratch + 2 r^2.
+__device__ void svd_fin2_warp_s(const SvdArgs& sa, int k, double* scratch, const double* hsrc) {
   const int r = sa.r[k], lane = threadIdx.x & 31;
   double* h = scratch;
   double* R = h + r * r;
@@ -348,24 +377,16 @@ __device__ void svd_fin2_warp_s(const SvdArgs& sa, int k, double* scratch) {
   double* sg = X + r * r;
   int* ord = reinterpret_cast<int*>(sg + r);
   int* dg = ord + r;
+  const double* H = hsrc ? hsrc : sa.H[k];
   for (int i = lane; i < r * r; i += 32) {
-    h[i] = sa.H[k][i];
+    h[i] = H[i];
     R[i] = 0.0;
     T[i] = 0.0;
   }
   __syncwarp();
   if (lane < r) sg[lane] = sqrt(fmax(h[lane + lane * r], 0.0));
   __syncwarp();
-  if (lane == 0) {
-    for (int i = 0; i < r; ++i) ord[i] = i;
-    for (int i = 1; i < r; ++i) {
-      const int t = ord[i];
-      int j = i - 1;
-      while (j >= 0 && sg[ord[j]] < sg[t]) { ord[j + 1] = ord[j]; --j; }
-      ord[j + 1] = t;
-    }
-  }
-  __syncwarp();
+  warp_order_desc(sg, r, ord);
   const double s1 = sg[ord[0]];
   const double mx = (double)(sa.mrows[k] > sa.pcols[k] ? sa.mrows[k] : sa.pcols[k]);
   const double tau = mx * s1 * 1e-12;   // linalg.py:54
@@ -381,30 +402,38 @@ __device__ void svd_fin2_warp_s(const SvdArgs& sa, int k, double* scratch) {
     sa.flags[k] = (s1 <= 0.0 || sg[ord[r - 1]] <= 1e-8 * s1) ? 1 : 0;
   }
   __syncwarp();
-  // Cholesky of C = D^-1 P^T H P D^-1 on non-degenerate columns (column by column;
-  // lanes own rows i of column j)
-  for (int j = 0; j < r; ++j) {
-    if (dg[j]) continue;
-    const int oj = ord[j];
-    for (int i = 0; i <= j; ++i) {
-      if (dg[i]) continue;
-      if (lane == 0) {
-        const int oi = ord[i];
-        double c = h[oi + oj * r] / (sg[oi] * sg[oj]);
-        for (int p = 0; p < i; ++p) c -= R[p + i * r] * R[p + j * r];
-        if (i == j) {
-          if (c <= 1e-6) dg[j] = 1;   // numerically dependent: complete instead
-          else R[j + j * r] = sqrt(c);
-        } else {
-          R[i + j * r] = c / R[i + i * r];
-        }
-      }
-      __syncwarp();
-      if (dg[j]) break;
+  // Cholesky of C = D^-1 P^T H P D^-1 on the non-degenerate columns; X holds the
+  // working upper triangle (lane j owns column j)
+  if (lane < r) {
+    const int oj = ord[lane];
+    for (int i = 0; i <= lane; ++i) {
+      const int oi = ord[i];
+      X[i + lane * r] = h[oi + oj * r] / (sg[oi] * sg[oj]);
     }
   }
   __syncwarp();
+  for (int p = 0; p < r; ++p) {
+    if (dg[p]) continue;   // (warp-uniform) row p of R stays zero
+    const double c = X[p + p * r];
+    if (c <= 1e-6) {   // numerically dependent: complete instead
+      __syncwarp();
+      if (lane == 0) dg[p] = 1;
+      __syncwarp();
+      continue;
+    }
+    const double d = sqrt(c);
+    if (lane == p) R[p + p * r] = d;
+    if (lane > p && lane < r) R[p + lane * r] = X[p + lane * r] / d;
+    __syncwarp();
+    if (lane > p && lane < r) {
+      const double rj = R[p + lane * r];
+      for (int i = p + 1; i <= lane; ++i) X[i + lane * r] -= R[p + i * r] * rj;
+    }
+    __syncwarp();
+  }
   // T = P D^-1 R^-1: lane j solves R x = e_j (upper triangular) for column j
+  // (into column j of X: the working triangle is no longer needed)
+  __syncwarp();
   if (lane < r && !dg[lane]) {
     const int j = lane;
     double* x = X + j * r;
@@ -425,10 +454,9 @@ __device__ void svd_fin2_warp_s(const SvdArgs& sa, int k, double* scratch) {
   if (lane < r) sa.degen[k][lane] = dg[lane];
   if (lane == 0) sa.degen[k][r] = anyd;
 }
-
 __device__ void svd_fin2_warp(const SvdArgs& sa, int k) {
   __shared__ double scr[4 * RT_MAX_RANK * RT_MAX_RANK + 2 * RT_MAX_RANK];
-  svd_fin2_warp_s(sa, k, scr);
+  svd_fin2_warp_s(sa, k, scr, nullptr);
 }
 
 __global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
@@ -443,40 +471,48 @@ __device__ void svd_fin2_ritz_warp(const SvdArgs& sa, int k, double* scr) {
   const int r = sa.r[k], lane = threadIdx.x & 31;
   double* q = scr;              // Q (r x r, column-major)
   double* hq = q + r * r;       // H Q
-  double* f2 = hq + r * r;      // fin2 scratch (4 r^2 + r doubles, 2 r ints)
-  const double* H = sa.H[k];
-  for (int e = lane; e < r * r; e += 32) q[e] = sa.Q[k][e];
+  double* hs = hq + r * r;      // H, then H'
+  double* f2 = hs + r * r;      // fin2 scratch (4 r^2 + r doubles, 2 r ints)
+  for (int e = lane; e < r * r; e += 32) {
+    q[e] = sa.Q[k][e];
+    hs[e] = sa.H[k][e];
+  }
   __syncwarp();
   for (int e = lane; e < r * r; e += 32) {   // (H Q)[i, j]
     const int i = e % r, j = e / r;
     double v = 0.0;
-    for (int p = 0; p < r; ++p) v = fma(H[i + p * r], q[p + j * r], v);
+    for (int p = 0; p < r; ++p) v = fma(hs[i + p * r], q[p + j * r], v);
     hq[e] = v;
   }
   __syncwarp();
-  for (int e = lane; e < r * r; e += 32) {   // H' = Q^T (H Q), symmetrised
+  double hv[(RT_MAX_RANK * RT_MAX_RANK + 31) / 32];
+  int nh = 0;
+  for (int e = lane; e < r * r; e += 32, ++nh) {   // H' = Q^T (H Q), symmetrised
     const int i = e % r, j = e / r;
-    if (i > j) continue;
+    const int a = min(i, j), b = max(i, j);
     double v = 0.0, w = 0.0;
     for (int p = 0; p < r; ++p) {
-      v = fma(q[p + i * r], hq[p + j * r], v);
-      w = fma(q[p + j * r], hq[p + i * r], w);
+      v = fma(q[p + a * r], hq[p + b * r], v);
+      w = fma(q[p + b * r], hq[p + a * r], w);
     }
-    const double hv = 0.5 * (v + w);
-    sa.H[k][i + j * r] = hv;
-    sa.H[k][j + i * r] = hv;
+    hv[nh] = 0.5 * (v + w);
   }
   __syncwarp();
-  svd_fin2_warp_s(sa, k, f2);   // sa.Q <- T
+  nh = 0;
+  for (int e = lane; e < r * r; e += 32, ++nh) {
+    hs[e] = hv[nh];
+    sa.H[k][e] = hv[nh];
+  }
   __syncwarp();
-  for (int e = lane; e < r * r; e += 32) {   // T' = Q T into hq, then out
+  svd_fin2_warp_s(sa, k, f2, hs);   // sa.Q <- T (also left at f2 + 2 r^2)
+  const double* T = f2 + 2 * r * r;
+  __syncwarp();
+  for (int e = lane; e < r * r; e += 32) {   // T' = Q T, out
     const int i = e % r, j = e / r;
     double v = 0.0;
-    for (int p = 0; p < r; ++p) v = fma(q[i + p * r], sa.Q[k][p + j * r], v);
-    hq[e] = v;
+    for (int p = 0; p < r; ++p) v = fma(q[i + p * r], T[p + j * r], v);
+    sa.Q[k][e] = v;
   }
-  __syncwarp();
-  for (int e = lane; e < r * r; e += 32) sa.Q[k][e] = hq[e];
 }
 
 // long-side vectors: out[t, a] = sum_b Z[t, b] T[b, a]; short side permuted in place later
