@@ -272,29 +272,40 @@ __device__ void svd_fin1_warp(const SvdArgs& sa, int k) {
         rs[lane] = sn;
       }
       __syncwarp();
-      // columns p, q of h and of q (every pair at once; lanes over (row, pair))
+      // two-sided update in one pass: lane task = the 2x2 block (rows of pair u,
+      // columns of pair w), column rotation first, then the row rotation -- the
+      // same expressions in the same order as a column pass followed by a row pass
+      for (int e = lane; e < half * half; e += 32) {
+        const int u = e % half, w = e / half;
+        const int pu = pp[u], qu = pq[u], pw = pp[w], qw = pq[w];
+        const bool ru = qu < r, rw = qw < r;
+        const double cu = rc[u], su = rs[u], cw = rc[w], sw = rs[w];
+        double b00 = h[pu + pw * r], b01 = rw ? h[pu + qw * r] : 0.0;
+        double b10 = ru ? h[qu + pw * r] : 0.0, b11 = (ru && rw) ? h[qu + qw * r] : 0.0;
+        if (rw) {   // columns pw, qw
+          const double t00 = cw * b00 - sw * b01, t01 = sw * b00 + cw * b01;
+          const double t10 = cw * b10 - sw * b11, t11 = sw * b10 + cw * b11;
+          b00 = t00; b01 = t01; b10 = t10; b11 = t11;
+        }
+        if (ru) {   // rows pu, qu
+          const double t00 = cu * b00 - su * b10, t10 = su * b00 + cu * b10;
+          const double t01 = cu * b01 - su * b11, t11 = su * b01 + cu * b11;
+          b00 = t00; b01 = t01; b10 = t10; b11 = t11;
+        }
+        h[pu + pw * r] = b00;
+        if (rw) h[pu + qw * r] = b01;
+        if (ru) h[qu + pw * r] = b10;
+        if (ru && rw) h[qu + qw * r] = b11;
+      }
+      // columns p, q of the accumulated rotation (lanes over (row, pair))
       for (int e = lane; e < r * half; e += 32) {
         const int row = e % r, pr = e / r;
         const int p = pp[pr], qq = pq[pr];
         if (qq >= r) continue;
         const double c = rc[pr], sn = rs[pr];
-        const double hp = h[row + p * r], hq = h[row + qq * r];
-        h[row + p * r] = c * hp - sn * hq;
-        h[row + qq * r] = sn * hp + c * hq;
         const double qp = q[row + p * r], qv = q[row + qq * r];
         q[row + p * r] = c * qp - sn * qv;
         q[row + qq * r] = sn * qp + c * qv;
-      }
-      __syncwarp();
-      // rows p, q of h
-      for (int e = lane; e < r * half; e += 32) {
-        const int col = e % r, pr = e / r;
-        const int p = pp[pr], qq = pq[pr];
-        if (qq >= r) continue;
-        const double c = rc[pr], sn = rs[pr];
-        const double hp = h[p + col * r], hq = h[qq + col * r];
-        h[p + col * r] = c * hp - sn * hq;
-        h[qq + col * r] = sn * hp + c * hq;
       }
       __syncwarp();
     }
