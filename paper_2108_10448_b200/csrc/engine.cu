@@ -121,6 +121,7 @@ struct Plan {
   i64 s[RT_MAX_MODES], l[RT_MAX_MODES];
   int tall[RT_MAX_MODES];
   int nb[RT_MAX_MODES];
+  bool lug[RT_MAX_MODES];   // inverse-iteration LU in global scratch (o_lug)
   i64 col_off[RT_MAX_BLOCKS + 1];
   int gram_maxchunks, gram_maxpairs, gram_cl;
   i64 dmax, lmax, smax, qmax;
@@ -136,7 +137,7 @@ struct Plan {
   i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
   i64 o_zeta;       // device copy of the iteration's threshold (graph-captured iterations read it)
   i64 samp_delta;   // bytes from sample slot 0 (index sets, maps, compact blocks) to slot 1
-  i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES],
+  i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES], o_lug[RT_MAX_MODES],
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
       o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_gt0, o_gt1, o_bpart, o_sums,
@@ -494,6 +495,12 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     const i64 s = P.s[m];
     P.o_K[m] = take(s * (s + 1) / 2 * 8);
     P.o_E[m] = take(s * ranks[m] * 8);
+    {
+      // RTCUR_EIG_LU_GLOBAL=1 forces the global-scratch LU (tests), =0 disables it
+      static const int lug_env = [] { const char* v = getenv("RTCUR_EIG_LU_GLOBAL"); return v ? atoi(v) : -1; }();
+      P.lug[m] = lug_env == 1 || (lug_env != 0 && P.nb[m] < ranks[m]);
+      P.o_lug[m] = take(P.lug[m] ? s * ranks[m] * 4 * 8 + s * ranks[m] : 8);
+    }
     P.o_lam[m] = take(ranks[m] * 8);
     P.o_Z[m] = take(P.l[m] * ranks[m] * 8);
     P.o_hpart[m] = take((i64)cdiv(P.l[m], HG_CH) * ranks[m] * (ranks[m] + 1) / 2 * 8);
@@ -1270,6 +1277,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ea.E[m] = e->at<double>(P.o_E[m]);
     ea.lam[m] = e->at<double>(P.o_lam[m]);
     ea.nb[m] = P.nb[m];
+    ea.lug[m] = P.lug[m] ? e->at<double>(P.o_lug[m]) : nullptr;
     ea.full[m] = eig_pick_full((int)P.s[m], P.g.rank[m]);
     esm = std::max(esm, eig_smem_bytes(P, m));
   }

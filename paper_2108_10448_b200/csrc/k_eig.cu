@@ -46,6 +46,10 @@ struct EigArgs {
   int max_sub_steps;
   int ms_warps;                        // multisection: max warps per eigenvalue (shifts = 64 x warps)
   int* fast_used;                      // per mode: 1 if the fast path certified the subspace
+  // inverse-iteration LU factors in global scratch (r x 4s doubles, then r x s
+  // pivot bytes), or null: in shared memory, nb at a time.  Used when fewer than
+  // r factorisations fit next to K (s = 213 packed: 2), so all r run at once.
+  double* lug[RT_MAX_MODES];
 };
 
 __host__ __device__ inline int eig_ld(int s) { return s | 1; }
@@ -777,13 +781,16 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   // ---------------------------------------------------------------- 3. block inverse iteration
   const double tiny = DBL_EPSILON * tn;
   const double pertol = 10.0 * DBL_EPSILON * tn;
-  for (int j0 = 0; j0 < r; j0 += nb) {
-    const int jn = min(nb, r - j0);
-    double* u0 = lu + (size_t)4 * s * tid;
+  double* const lug = ea.lug[mi];
+  const int nbe = lug ? r : nb;
+  for (int j0 = 0; j0 < r; j0 += nbe) {
+    const int jn = min(nbe, r - j0);
+    double* u0 = lug ? lug + (size_t)4 * s * tid : lu + (size_t)4 * s * tid;
     double* u1 = u0 + s;
     double* u2 = u1 + s;
     double* lm = u2 + s;
-    unsigned char* pv = piv + (size_t)s * tid;
+    unsigned char* pv = lug ? reinterpret_cast<unsigned char*>(lug + (size_t)4 * s * r) + (size_t)s * tid
+                            : piv + (size_t)s * tid;
     if (tid < jn) {
       const int j = j0 + tid;
       double mu = lam[j];
