@@ -376,6 +376,18 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
       __syncthreads();
       if (eig_chol_warp(Hs, r, rinv, 0.0, scal)) return true;
     }
+    // Long attempt, nearly converged, bound settled (within 1e-3 of the previous
+    // step's): once lambda_min(H) <= min_i H_ii lies below 0.95 ub no later step
+    // can certify (the Frobenius bound is too loose for this spectrum) -> full
+    // solver now rather than at max_steps.
+    const double ub_prev = scal[15];
+    __syncthreads();   // (every thread has read scal[15])
+    if (tid == 0) scal[15] = ub;
+    if (step >= 5 && res <= 1e-8 * trK && fabs(ub - ub_prev) <= 1e-3 * ub) {
+      double hmin = H[0];
+      for (int c = 1; c < r; ++c) hmin = fmin(hmin, H[c + c * r]);
+      if (hmin < 0.95 * ub) return false;
+    }
     if (step + 1 == max_steps) break;
     TMK(5)
     // X <- orth(Y)
