@@ -124,8 +124,9 @@ class TruncSvd:
         return (self.v * inv) @ self.u.T
 
 
-def truncated_svd(m: np.ndarray, r: int) -> TruncSvd:
-    """linalg.py:59-74."""
+def truncated_svd(m: np.ndarray, r: int, spectrum: list | None = None) -> TruncSvd:
+    """linalg.py:59-74.  ``spectrum`` (optional list) receives the full singular
+    values (parity tooling logs the sigma_r / sigma_{r+1} gap from them)."""
     m = np.asarray(m, dtype=np.float64)
     if m.ndim != 2 or m.size == 0:
         raise ValueError(f"truncated_svd needs a nonempty matrix, got shape {m.shape}")
@@ -135,6 +136,8 @@ def truncated_svd(m: np.ndarray, r: int) -> TruncSvd:
     if not 1 <= r <= q:
         raise ValueError(f"rank {r} outside [1, {q}] for shape {m.shape}")
     u, s, vt = dense_svd(m)
+    if spectrum is not None:
+        spectrum.append(s.copy())
     return TruncSvd(u=u[:, :r].copy(), singular_values=s[:r].copy(), v=vt[:r].T.copy())
 
 
@@ -260,19 +263,20 @@ class OracleCur:
     intersections: tuple
     indices: Sample
     factors: tuple
+    spectra: tuple = ()   # full singular values of each intersection (diagnostics only)
 
 
 def assemble(core: np.ndarray, fibers, idx: Sample, ranks) -> OracleCur:
     """fiber_cur.py:229-274."""
-    inters, factors = [], []
+    inters, factors, spectra = [], [], []
     for rows, rk, fib in zip(idx.rows, ranks, fibers):
         if rk > rows.size or rk > fib.shape[1]:
             raise ValueError(f"rank {rk} exceeds sample sizes")
-        inter = truncated_svd(fib[rows - 1, :], rk)
+        inter = truncated_svd(fib[rows - 1, :], rk, spectra)
         inters.append(inter)
         factors.append(fib @ inter.pinv())
     return OracleCur(core=core, fibers=tuple(fibers), intersections=tuple(inters),
-                     indices=idx, factors=tuple(factors))
+                     indices=idx, factors=tuple(factors), spectra=tuple(spectra))
 
 
 def eval_subtensor(cur: OracleCur, rows) -> np.ndarray:
@@ -283,8 +287,10 @@ def eval_subtensor(cur: OracleCur, rows) -> np.ndarray:
     return out
 
 
-def eval_fibers(cur: OracleCur, k: int, cols) -> np.ndarray:
-    """fiber_cur.py:297-326 (einsum over the |I_1|x...x|I_n| core, as the reference)."""
+def eval_fibers_einsum(cur: OracleCur, k: int, cols) -> np.ndarray:
+    """fiber_cur.py:297-326 verbatim in structure: one ``np.einsum`` over the
+    |I_1|x...x|I_n| core and the other modes' factor rows, then ``factor_k @``.
+    This is the reference's hot spot; the CPU baseline ("port") times it."""
     shape = tuple(f.shape[0] for f in cur.fibers)
     n = len(shape)
     cols = np.asarray(cols, dtype=np.int64).reshape(-1)
@@ -302,10 +308,61 @@ def eval_fibers(cur: OracleCur, k: int, cols) -> np.ndarray:
     return cur.factors[k - 1] @ small
 
 
-def eval_blocks(cur: OracleCur, idx: Sample):
+def eval_fibers_blas(cur: OracleCur, k: int, cols, chunk_bytes: int = 1 << 28) -> np.ndarray:
+    """The same contraction as ``eval_fibers_einsum`` (fiber_cur.py:318-326:
+    small[:, j] = sum over the other modes' core indices of core * prod_m
+    factor_m[i_m(j), :]), associated explicitly: one BLAS GEMM against the
+    first other mode's factor rows, then one batched dot per remaining mode,
+    columns in chunks of ``chunk_bytes`` of intermediate.  Same sum, different
+    association: agrees with the einsum to ~1e-15 relative
+    (tests/test_oracle_golden.py::test_eval_fibers_blas_matches_einsum) and is
+    15-40x faster, which is what makes full-size oracle solves at BASELINE
+    configs 1-4 feasible for the parity runs."""
+    shape = tuple(f.shape[0] for f in cur.fibers)
+    n = len(shape)
+    cols = np.asarray(cols, dtype=np.int64).reshape(-1)
+    parts = decode_fiber_columns(shape, k, cols)
+    core = cur.core
+    other = [m for m in range(1, n + 1) if m != k]
+    if not other:
+        small = np.repeat(core.reshape(-1, 1), cols.size, axis=1)
+        return cur.factors[k - 1] @ small
+    J = cols.size
+    small = np.empty((core.shape[k - 1], J))
+    m1 = other[0]
+    per_col = 8 * (core.size // core.shape[m1 - 1])
+    step = max(1, min(J, chunk_bytes // max(per_col, 1))) if J else 1
+    for j0 in range(0, J, step):
+        j1 = min(J, j0 + step)
+        rows1 = cur.factors[m1 - 1][parts[0][j0:j1] - 1, :]          # (jc, |I_m1|)
+        t = np.tensordot(rows1, core, axes=([1], [m1 - 1]))          # (jc, modes != m1 ascending)
+        axes = [m for m in range(1, n + 1) if m != m1]               # t axis i+1 <-> mode axes[i]
+        for m, r in zip(other[1:], parts[1:]):
+            rows = cur.factors[m - 1][r[j0:j1] - 1, :]                # (jc, |I_m|)
+            t = np.moveaxis(t, axes.index(m) + 1, -1)
+            lead = t.shape[:-1]
+            t = np.matmul(t.reshape(lead[0], -1, t.shape[-1]), rows[:, :, None]).reshape(lead)
+            axes.remove(m)
+        small[:, j0:j1] = t.T
+    return cur.factors[k - 1] @ small
+
+
+# which evaluation the oracle's solve uses: "blas" (parity runs, default) or
+# "einsum" (the CPU baseline that costs what the reference costs)
+EVAL_MODE = os.environ.get("RTCUR_ORACLE_EVAL", "blas")
+
+
+def eval_fibers(cur: OracleCur, k: int, cols, mode: str | None = None) -> np.ndarray:
+    """fiber_cur.py:297-326."""
+    if (mode or EVAL_MODE) == "einsum":
+        return eval_fibers_einsum(cur, k, cols)
+    return eval_fibers_blas(cur, k, cols)
+
+
+def eval_blocks(cur: OracleCur, idx: Sample, mode: str | None = None):
     """solver.py:242-249."""
     core = eval_subtensor(cur, idx.rows)
-    fibers = [eval_fibers(cur, k, c) for k, c in enumerate(idx.cols, start=1)]
+    fibers = [eval_fibers(cur, k, c, mode) for k, c in enumerate(idx.cols, start=1)]
     return core, fibers
 
 
@@ -370,20 +427,25 @@ def inf_norm(flat: np.ndarray) -> float:
     return best
 
 
-def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, upsilon=3.0,
-          variant="F", max_iters=500, seed=None, row_sample_sizes=None, col_sample_sizes=None,
-          record_trace=False, iteration_budget_s: float | None = None) -> OracleResult:
-    """solver.py:260-389 restated.  x_flat is the mode-1-fastest float64 buffer.
+def iter_solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, upsilon=3.0,
+               variant="F", max_iters=500, seed=None, row_sample_sizes=None, col_sample_sizes=None,
+               iteration_budget_s: float | None = None, eval_mode: str | None = None, stats: dict | None = None):
+    """solver.py:260-389 restated as a generator: yields one dict per iteration
+    (iteration, zeta, indices, x/s/l blocks, error, flags, cur).  ``stats``
+    (optional dict) receives timings / iter_times / converged as they happen.
+    x_flat is the mode-1-fastest float64 buffer.
 
     iteration_budget_s (CPU-baseline use only) stops after the first iteration
-    that pushes the elapsed loop time past the budget; the result is then
-    marked not converged and the caller reports per-iteration throughput.
-    """
+    that pushes the elapsed loop time past the budget."""
     shape = tuple(int(d) for d in shape)
     x_flat = np.ascontiguousarray(x_flat, dtype=np.float64).reshape(-1)
     arr = x_flat.reshape(shape, order="F")
     variant = variant.upper()
-    timings = {k: 0.0 for k in ("sample", "gather", "eval_lowrank", "threshold", "build", "error", "total")}
+    st = stats if stats is not None else {}
+    timings = st.setdefault("timings", {k: 0.0 for k in ("sample", "gather", "eval_lowrank", "threshold",
+                                                           "build", "error", "total")})
+    iter_times = st.setdefault("iter_times", [])
+    st["converged"] = False
     t_start = time.perf_counter()
     rng = np.random.default_rng(seed)
     rows, cols = sample_sizes(shape, ranks, upsilon)
@@ -408,10 +470,6 @@ def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, 
 
     lcur = None
     lblocks = None
-    history, flags, trace, iter_times = [], [], [], []
-    converged = False
-    s_core = np.zeros_like(x_core)
-    s_fibers = [np.zeros_like(f) for f in x_fibers]
     for k in range(1, max_iters + 1):
         t_iter = time.perf_counter()
         if variant == "R" and k >= 2:
@@ -428,9 +486,10 @@ def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, 
             l_core = np.zeros_like(x_core)
             l_fibers = [np.zeros_like(f) for f in x_fibers]
         elif lblocks is None:
-            l_core, l_fibers = eval_blocks(lcur, idx)
+            l_core, l_fibers = eval_blocks(lcur, idx, eval_mode)
         else:
             l_core, l_fibers = lblocks
+        prev_l = (l_core, l_fibers)
         timings["eval_lowrank"] += time.perf_counter() - t0
         t0 = time.perf_counter()
         s_core = hard_threshold(x_core - l_core, zeta)
@@ -440,32 +499,51 @@ def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, 
         clean_core = np.asfortranarray(x_core - s_core)
         clean_fibers = tuple(xf - sf for xf, sf in zip(x_fibers, s_fibers))
         lcur = assemble(clean_core, clean_fibers, idx, ranks)
-        flags.append(deficiency_flags(lcur))
+        fl = deficiency_flags(lcur)
         timings["build"] += time.perf_counter() - t0
         t0 = time.perf_counter()
-        l_core, l_fibers = eval_blocks(lcur, idx)
+        l_core, l_fibers = eval_blocks(lcur, idx, eval_mode)
         lblocks = (l_core, l_fibers)
         e_core = x_core - l_core - s_core
         e_fibers = [xf - lf - sf for xf, lf, sf in zip(x_fibers, l_fibers, s_fibers)]
         err = sampled_relative_error(e_core, e_fibers, x_core, x_fibers)
         timings["error"] += time.perf_counter() - t0
-        history.append(err)
         iter_times.append(time.perf_counter() - t_iter)
-        if record_trace:
-            trace.append({"iteration": k, "zeta": zeta, "indices": idx, "s_core": s_core,
-                          "s_fibers": tuple(s_fibers), "l_core": l_core,
-                          "l_fibers": tuple(l_fibers), "error": err})
-        if err <= eps:
-            converged = True
+        done = err <= eps
+        st["converged"] = bool(done)
+        timings["total"] = time.perf_counter() - t_start
+        timings["loop"] = time.perf_counter() - t_loop
+        yield {"iteration": k, "zeta": zeta, "indices": idx, "x_core": x_core, "x_fibers": tuple(x_fibers),
+               "s_core": s_core, "s_fibers": tuple(s_fibers), "l_core": l_core, "l_fibers": tuple(l_fibers),
+               "l_prev": prev_l, "error": err, "flags": fl, "cur": lcur}
+        if done:
             break
         if iteration_budget_s is not None and time.perf_counter() - t_loop > iteration_budget_s:
             break
-    timings["total"] = time.perf_counter() - t_start
-    timings["loop"] = time.perf_counter() - t_loop
-    return OracleResult(cur=lcur, s_core=s_core, s_fibers=tuple(s_fibers), indices=idx,
-                        error_history=tuple(history), iterations=len(history), converged=converged,
-                        diagnostics=tuple(flags), zeta_final=zeta, timings=timings, trace=trace,
-                        iter_times=iter_times)
+
+
+def solve(x_flat: np.ndarray, shape, ranks, *, eps=1e-5, zeta0=None, gamma=0.7, upsilon=3.0,
+          variant="F", max_iters=500, seed=None, row_sample_sizes=None, col_sample_sizes=None,
+          record_trace=False, iteration_budget_s: float | None = None,
+          eval_mode: str | None = None) -> OracleResult:
+    """solver.py:260-389 restated (collects ``iter_solve``)."""
+    stats: dict = {}
+    history, flags, trace = [], [], []
+    last = None
+    for it in iter_solve(x_flat, shape, ranks, eps=eps, zeta0=zeta0, gamma=gamma, upsilon=upsilon,
+                         variant=variant, max_iters=max_iters, seed=seed, row_sample_sizes=row_sample_sizes,
+                         col_sample_sizes=col_sample_sizes, iteration_budget_s=iteration_budget_s,
+                         eval_mode=eval_mode, stats=stats):
+        history.append(it["error"])
+        flags.append(it["flags"])
+        if record_trace:
+            trace.append({k: it[k] for k in ("iteration", "zeta", "indices", "s_core", "s_fibers", "l_core",
+                                             "l_fibers", "error")})
+        last = it
+    return OracleResult(cur=last["cur"], s_core=last["s_core"], s_fibers=last["s_fibers"],
+                        indices=last["indices"], error_history=tuple(history), iterations=len(history),
+                        converged=stats["converged"], diagnostics=tuple(flags), zeta_final=last["zeta"],
+                        timings=stats["timings"], trace=trace, iter_times=stats["iter_times"])
 
 
 def full_output(x_flat: np.ndarray, shape, cur: OracleCur, zeta_final: float):

@@ -7,27 +7,34 @@
 // the storage dtype of X, so fp32 tensors are processed with fp64 arithmetic
 // (the reference is fp64-only, tensor.py:8).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 // Raise a kernel's dynamic shared-memory limit to the device's opt-in maximum
-// (minus its static shared memory), once per kernel.  Per-launch
-// cudaFuncSetAttribute calls with the launch's own size race between host
-// threads launching the same kernel with different sizes (a second thread can
-// lower the limit between the first thread's set and launch: "invalid argument").
-template <auto Kernel>   // one static per kernel (not per signature)
+// (minus its static shared memory), once per kernel and device (function
+// attributes are per device context).  Per-launch cudaFuncSetAttribute calls
+// with the launch's own size race between host threads launching the same
+// kernel with different sizes (a second thread can lower the limit between the
+// first thread's set and launch: "invalid argument").
+#define RT_MAX_DEVICES 64
+template <auto Kernel>   // one table per kernel (not per signature)
 inline cudaError_t raise_dyn_smem_once() {
-  static const cudaError_t err = [] {
-    int dev = 0, optin = 227 * 1024;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa;
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, Kernel);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
-    return e;
-  }();
-  return err;
+  static std::atomic<int> state[RT_MAX_DEVICES];   // 0 unset, 1 + cudaError_t once done
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= RT_MAX_DEVICES) return cudaErrorInvalidDevice;
+  const int st = state[dev].load(std::memory_order_acquire);
+  if (st) return (cudaError_t)(st - 1);
+  int optin = 227 * 1024;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, Kernel);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  state[dev].store(1 + (int)e, std::memory_order_release);   // idempotent: racing setters write the same limit
+  return e;
 }
 
 #define RT_MAX_MODES 8

@@ -676,10 +676,12 @@ static void prof_flush(rtcur_engine* e) {
 }
 
 static int set_smem_limits_once() {
-  static std::atomic<int> done{0};
-  if (done.load()) return RT_OK;
+  // function attributes are per device context: once per device
+  static std::atomic<int> done[RT_MAX_DEVICES];
   int dev = 0, optin = 227 * 1024;
   CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= RT_MAX_DEVICES) return fail(RT_ERR_VALUE, "device ordinal out of range");
+  if (done[dev].load()) return RT_OK;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   // per kernel: opt-in maximum minus its static shared memory
 #define SMEM_ATTR(F)                                                                          \
@@ -719,7 +721,7 @@ static int set_smem_limits_once() {
     const int b = atoi(gf);
     if (b == 32 || b == 64 || b == 128) CK(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)b));
   }
-  done.store(1);
+  done[dev].store(1);
   return RT_OK;
 }
 

@@ -87,7 +87,7 @@ bool parallel_io(int fd, char* buf, size_t len, off_t off, bool write) {
   return all;
 }
 
-std::string dims_str(const std::vector<i64>& d) {
+std::string dims_str(const std::vector<unsigned long long>& d) {
   std::string s = "(";
   for (size_t i = 0; i < d.size(); ++i) {
     s += std::to_string(d[i]);
@@ -95,6 +95,39 @@ std::string dims_str(const std::vector<i64>& d) {
     else if (i + 1 < d.size()) s += ", ";
   }
   return s + ")";
+}
+
+// exact decimal of 8 * prod(d) (Python int semantics, as the reference's
+// "require {expected}" text): base-1e9 limbs, any number of u64 factors
+std::string payload_bytes_str(const std::vector<unsigned long long>& d) {
+  std::vector<unsigned long long> limbs{8};   // little-endian base 1e9
+  const unsigned long long B = 1000000000ULL;
+  for (unsigned long long f : d) {
+    const unsigned long long parts[3] = {f % B, (f / B) % B, f / B / B};   // f = p0 + p1 B + p2 B^2
+    std::vector<unsigned long long> acc(limbs.size() + 4, 0);
+    for (int q = 0; q < 3; ++q) {
+      unsigned __int128 carry = 0;
+      size_t i = 0;
+      for (; i < limbs.size(); ++i) {
+        unsigned __int128 t = (unsigned __int128)limbs[i] * parts[q] + acc[i + q] + carry;
+        acc[i + q] = (unsigned long long)(t % B);
+        carry = t / B;
+      }
+      for (size_t k = i + q; carry; ++k) {
+        unsigned __int128 t = acc[k] + carry;
+        acc[k] = (unsigned long long)(t % B);
+        carry = t / B;
+      }
+    }
+    while (acc.size() > 1 && acc.back() == 0) acc.pop_back();
+    limbs.swap(acc);
+  }
+  std::string out = std::to_string(limbs.back());
+  for (size_t i = limbs.size() - 1; i-- > 0;) {
+    std::string part = std::to_string(limbs[i]);
+    out += std::string(9 - part.size(), '0') + part;
+  }
+  return out;
 }
 
 // tensorfile._parse_header (+ the payload-size check of read_tensor when check_payload)
@@ -140,36 +173,37 @@ int parse_header(const char* path, int* version, std::vector<i64>& dims, i64* pa
                                    " extents need bytes 8.." + std::to_string(dims_end - 1));
   std::vector<unsigned char> raw((size_t)8 * n);
   if (!pread_all(f.fd, raw.data(), raw.size(), 8)) return fail(RT_ERR_IO, P + ": read failed");
-  dims.assign(n, 0);
+  std::vector<unsigned long long> ud(n, 0);
   for (int m = 0; m < n; ++m) {
     unsigned long long v = 0;
     for (int b = 7; b >= 0; --b) v = (v << 8) | raw[(size_t)8 * m + b];
-    dims[m] = (i64)v;
+    ud[m] = v;
     if (v == 0)
       return fail(RT_ERR_FORMAT, P + ": extent 0 for mode " + std::to_string(m + 1) + " at byte " +
                                      std::to_string(8 + 8 * m));
   }
   if (check_payload) {
-    // prod(dims) * 8 in unsigned 128-bit-safe arithmetic (dims up to 2^64 each)
+    // 8 * prod(dims) == payload bytes, overflow-safe: test each factor against the
+    // remaining headroom before multiplying (count <= 2^100, so count * d cannot wrap)
+    const unsigned __int128 cap = (unsigned __int128)1 << 100;
     unsigned __int128 count = 1;
     bool big = false;
-    for (int m = 0; m < n; ++m) {
-      count *= (unsigned long long)dims[m];
-      if (count > ((unsigned __int128)1 << 100)) big = true;
+    for (int m = 0; m < n && !big; ++m) {
+      if (count > cap / ud[m]) big = true;
+      else count *= ud[m];
     }
-    const unsigned __int128 expected = count * 8;
     const i64 actual = size - dims_end;
-    if (big || expected != (unsigned __int128)actual) {
-      std::string es;
-      if (big) es = "(more than 2^100)";
-      else {
-        unsigned __int128 v = expected;
-        if (v == 0) es = "0";
-        while (v > 0) { es.insert(es.begin(), (char)('0' + (int)(v % 10))); v /= 10; }
-      }
+    if (big || count * 8 != (unsigned __int128)actual)
       return fail(RT_ERR_FORMAT, P + ": payload at byte " + std::to_string(dims_end) + " holds " +
-                                     std::to_string(actual) + " bytes, dims " + dims_str(dims) + " require " + es);
-    }
+                                     std::to_string(actual) + " bytes, dims " + dims_str(ud) + " require " +
+                                     payload_bytes_str(ud));
+  }
+  dims.assign(n, 0);
+  for (int m = 0; m < n; ++m) {
+    if (ud[m] >= (1ULL << 63))   // not representable as an int64 extent (the payload check rejects it first)
+      return fail(RT_ERR_FORMAT, P + ": extent " + std::to_string(ud[m]) + " for mode " + std::to_string(m + 1) +
+                                     " at byte " + std::to_string(8 + 8 * m) + " exceeds 2^63 - 1");
+    dims[m] = (i64)ud[m];
   }
   *version = ver;
   *payload_off = dims_end;

@@ -43,6 +43,19 @@ RANK_DEFICIENCY_RTOL = 1e-8  # solver.py:64 (applied on device, k_svd_fin2)
 PROFILE = False
 PROFILE_PHASES = None  # phase names timed while PROFILE (None: all)
 
+# The reference times its phases with perf_counter around synchronous numpy
+# calls (solver.py:282-356).  Here the iteration is one asynchronous device
+# step, so host clocks cannot split it: with PHASE_TIMINGS (env
+# RTCUR_PHASE_TIMINGS=1) every device phase is bracketed by CUDA events on the
+# solve's stream and timings["gather" | "eval_lowrank" | "threshold" | "build" |
+# "error"] hold device seconds (timings["timing_source"] = "device-events").
+# Off (default, no event nodes in the per-iteration graphs): "build" holds the
+# host-observed iteration time, the other per-phase keys 0.0
+# (timings["timing_source"] = "host").
+PHASE_TIMINGS = os.environ.get("RTCUR_PHASE_TIMINGS", "0") == "1"
+_REF_PHASES = {"gather": ("prep", "gather"), "eval_lowrank": ("wcols",), "threshold": ("threshold",),
+               "build": ("gram", "eig", "svdpost", "apass", "gpass"), "error": ("error",)}
+
 
 @dataclass(frozen=True)
 class SolverConfig:
@@ -96,10 +109,13 @@ class SparseEstimate:
 
     core / fibers are copied from HBM on first access."""
 
-    def __init__(self, loader, indices: SampleIndices):
+    def __init__(self, loader, indices: SampleIndices, owner=None):
         self._loader = loader
         self._cache = None
         self.indices = indices
+        # the FiberCur whose device state the loader reads: holding it keeps the
+        # engine out of the pool (a later solve cannot overwrite these blocks)
+        self._owner = owner
 
     def _load(self):
         if self._cache is None:
@@ -160,6 +176,72 @@ class DenseTensorAccessor:
         if self._dev is None:
             self._dev = DeviceTensor.from_host(self._t)
         return self._dev
+
+    def core_block(self, rows) -> np.ndarray:
+        """X(I_1, ..., I_n) for 1-based sorted index sets (solver.py:170-171 ->
+        tensor.py:235-240), gathered on the device as strided mode-1 fibers."""
+        import torch
+
+        shape = self.shape
+        rows = [np.asarray(r, dtype=np.int64).reshape(-1) for r in rows]
+        if len(rows) != len(shape):
+            raise ValueError(f"{len(rows)} index sets for a {len(shape)}-mode tensor")
+        for m, (r, d) in enumerate(zip(rows, shape), start=1):
+            if r.size and (r.min() < 1 or r.max() > d):
+                raise IndexError(f"index outside [1, {d}] for mode {m}")
+        # the core block's mode-1 columns are the mode-1 fibers at (I_2, .., I_n),
+        # restricted to the rows I_1: gather whole fibers, then pick the rows
+        others = rows[1:]
+        if others:
+            grids = np.meshgrid(*others, indexing="ij")
+            combo = np.zeros(grids[0].shape, dtype=np.int64)
+            acc = 1
+            for g, d in zip(grids, shape[1:]):
+                combo += (g - 1) * acc
+                acc *= d
+            cols = combo.reshape(-1, order="F") + 1   # mode 2 fastest (fiber column order)
+        else:
+            cols = np.ones(1, dtype=np.int64)
+        fib = self._gather(1, cols)                                         # d_1 x prod |I_m|
+        out = fib[rows[0] - 1, :]
+        return np.asfortranarray(out.reshape(tuple(r.size for r in rows), order="F"))
+
+    def fiber_block(self, k: int, cols) -> np.ndarray:
+        """C_k = X_(k)(:, J) for 1-based columns (solver.py:173-179), gathered by
+        the device kernel behind the reference's ``gather_columns`` plug."""
+        return self._gather(k, cols)
+
+    def _gather(self, k: int, cols) -> np.ndarray:
+        import torch
+
+        from .tensor import fiber_base_offsets, mode_stride
+
+        shape = self.shape
+        if not 1 <= k <= len(shape):
+            raise ValueError(f"mode {k} outside [1, {len(shape)}]")
+        bases = fiber_base_offsets(shape, k, np.asarray(cols, dtype=np.int64).reshape(-1))
+        dev = self.device_tensor()
+        b = torch.from_numpy(np.ascontiguousarray(bases)).to(dev.flat.device)
+        length = shape[k - 1]
+        out = torch.empty(length * b.numel(), dtype=torch.float64, device=dev.flat.device)
+        lib = nat.load()
+        nat.check(lib.rtcur_gather_columns(dev.flat.data_ptr(), 0, dev.flat.numel(), b.data_ptr(), b.numel(),
+                                           mode_stride(shape, k), length, out.data_ptr(),
+                                           torch.cuda.current_stream().cuda_stream))
+        return out.cpu().numpy().reshape((length, b.numel()), order="F")
+
+    def inf_norm(self) -> float:
+        """max |x| (solver.py:182-190) by the device abs-max kernel."""
+        import ctypes
+
+        import torch
+
+        dev = self.device_tensor()
+        scratch = torch.empty(1300, dtype=torch.float64, device=dev.flat.device)
+        out = ctypes.c_double()
+        nat.check(nat.load().rtcur_abs_max(dev.flat.data_ptr(), 0, dev.flat.numel(), scratch.data_ptr(),
+                                           ctypes.byref(out), torch.cuda.current_stream().cuda_stream))
+        return float(out.value)
 
 
 def hard_threshold(values, zeta: float):
@@ -345,7 +427,7 @@ def _make_result(eng: Engine, src: _Source, idx, cfg, history, flags, timings, z
     import weakref
 
     weakref.finalize(cur, release_engine, eng)   # back to the pool once the result is gone
-    sparse = SparseEstimate(load_sparse, idx)
+    sparse = SparseEstimate(load_sparse, idx, owner=cur)
     return SolveResult(cur=cur, sparse=sparse, error_history=tuple(history), iterations=len(history),
                        converged=converged, diagnostics=tuple(flags), timings=timings, zeta_final=zeta,
                        config=cfg, trace=tuple(trace) if trace is not None else None)
@@ -372,14 +454,31 @@ def _mode_copy_plan(shape, col_sizes, cfg, src):
     cost clearly more DRAM traffic than writing and reading the copy once."""
     if cfg.variant != "R" or src.dev is None or src.group is not None or len(shape) < 2:
         return ()
+    import torch
+
     E = src.dev.flat.element_size()
     N = int(np.prod(shape, dtype=np.int64))
     gathers = min(int(cfg.max_iters), 25) + 1
-    return tuple(k for k in range(1, len(shape))
-                 if gathers * shape[k] * col_sizes[k] * (_STRIDED_BYTES - E) > 1.5 * 2 * N * E)
+    want = [k for k in range(1, len(shape))
+            if gathers * shape[k] * col_sizes[k] * (_STRIDED_BYTES - E) > 1.5 * 2 * N * E]
+    if not want:
+        return ()
+    # each copy is another N*E bytes of HBM: keep only what fits with headroom
+    # (1 GiB + 10 % of the device) next to everything already allocated
+    free, total = torch.cuda.mem_get_info(src.dev.flat.device)
+    room = free - (1 << 30) - total // 10
+    keep = []
+    for k in want:
+        if room >= N * E:
+            keep.append(k)
+            room -= N * E
+    return tuple(keep)
 
 
-def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
+def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_iteration=None) -> SolveResult:
+    """The solve loop.  ``on_iteration(k, eng, idx, zeta, err, flags)`` (optional,
+    parity tooling) runs after every iteration, while the engine still holds
+    that iteration's state (``eng.export_blocks`` / ``eng.export_cur``)."""
     import torch
 
     shape = src.shape
@@ -398,88 +497,103 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False) -> Sol
             raise ValueError(f"mode {m}: rank {r} exceeds sample sizes (|rows|={rs}, |cols|={cs})")
 
     eng = acquire_engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype, slab=src.slab)
+    phase_events = PHASE_TIMINGS and not PROFILE
     if PROFILE:
         eng.profile(True, PROFILE_PHASES)
+    elif phase_events:
+        eng.profile(True, None)
+        eng.profile_read(reset=True)
     src.attach(eng)
     copies = _mode_copy_plan(shape, col_sizes, cfg, src)
     if copies:
         eng.bind_mode_copies(src.dev.flat, copies)
-    # the device scans max|X| (and builds the mode copies) while the host draws the
-    # first sample (the generator is consumed by sampling only, solver.py:293-316)
-    early_zeta = (cfg.zeta0 is None and src.dev is not None and src.group is None
-                  and os.environ.get("RTCUR_EARLY_ZETA", "1") != "0")
-    if early_zeta:
-        eng.absmax_begin()
-    t0 = time.perf_counter()
-    idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
-    timings["sample"] += time.perf_counter() - t0
-    t0 = time.perf_counter()
-    eng.set_sample(idx)
-    src.load_blocks(eng, idx)
-    timings["gather"] += time.perf_counter() - t0
-
-    if cfg.zeta0 is not None:
-        zeta = float(cfg.zeta0)
-    else:
-        zeta = eng.absmax_end() if early_zeta else src.inf_norm(eng)
-    t_loop = time.perf_counter()
-    history, flags = [], []
-    trace = [] if record_trace else None
-    converged = False
-    # RTCUR-R draws the next sample while the GPU runs the current iteration:
-    # the generator is consumed by sampling only, so drawing ahead leaves every
-    # index set identical to the reference's (solver.py:315-317).
-    next_idx = None
-    # device-resident local tensors: the next sample's upload and gather go into the
-    # engine's inactive sample slot right behind the running iteration (no host gap)
-    prefetch = src.dev is not None and src.group is None
-    staged = False
-    for k in range(1, cfg.max_iters + 1):
-        if cfg.variant == "R" and k >= 2:
-            t0 = time.perf_counter()
-            idx = next_idx if next_idx is not None else draw_sample_indices(shape, row_sizes, col_sizes, rng)
-            next_idx = None
-            timings["sample"] += time.perf_counter() - t0
-            if not staged:
-                t0 = time.perf_counter()
-                eng.set_sample(idx)
-                src.load_blocks(eng, idx)
-                timings["gather"] += time.perf_counter() - t0
-            staged = False
-        zeta *= cfg.gamma
+    try:
+        # the device scans max|X| (and builds the mode copies) while the host draws the
+        # first sample (the generator is consumed by sampling only, solver.py:293-316)
+        early_zeta = (cfg.zeta0 is None and src.dev is not None and src.group is None
+                      and os.environ.get("RTCUR_EARLY_ZETA", "1") != "0")
+        if early_zeta:
+            eng.absmax_begin()
         t0 = time.perf_counter()
-        eng.iterate_async(zeta, first=(k == 1))
-        if cfg.variant == "R" and k < cfg.max_iters:
-            t1 = time.perf_counter()
-            next_idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
-            timings["sample"] += time.perf_counter() - t1
-            if prefetch:
+        idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+        timings["sample"] += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        eng.set_sample(idx)
+        src.load_blocks(eng, idx)
+        timings["gather"] += time.perf_counter() - t0
+
+        if cfg.zeta0 is not None:
+            zeta = float(cfg.zeta0)
+        else:
+            zeta = eng.absmax_end() if early_zeta else src.inf_norm(eng)
+        t_loop = time.perf_counter()
+        history, flags = [], []
+        trace = [] if record_trace else None
+        converged = False
+        # RTCUR-R draws the next sample while the GPU runs the current iteration:
+        # the generator is consumed by sampling only, so drawing ahead leaves every
+        # index set identical to the reference's (solver.py:315-317).
+        next_idx = None
+        # device-resident local tensors: the next sample's upload and gather go into the
+        # engine's inactive sample slot right behind the running iteration (no host gap)
+        prefetch = src.dev is not None and src.group is None
+        staged = False
+        for k in range(1, cfg.max_iters + 1):
+            if cfg.variant == "R" and k >= 2:
+                t0 = time.perf_counter()
+                idx = next_idx if next_idx is not None else draw_sample_indices(shape, row_sizes, col_sizes, rng)
+                next_idx = None
+                timings["sample"] += time.perf_counter() - t0
+                if not staged:
+                    t0 = time.perf_counter()
+                    eng.set_sample(idx)
+                    src.load_blocks(eng, idx)
+                    timings["gather"] += time.perf_counter() - t0
+                staged = False
+            zeta *= cfg.gamma
+            t0 = time.perf_counter()
+            eng.iterate_async(zeta, first=(k == 1))
+            if cfg.variant == "R" and k < cfg.max_iters:
                 t1 = time.perf_counter()
-                eng.set_sample(next_idx)
-                src.load_blocks(eng, next_idx)
-                staged = True
-                timings["gather"] += time.perf_counter() - t1
-        e2, x2, fl = eng.iterate_wait()
-        timings["build"] += time.perf_counter() - t0
-        err = _error_from_sums(e2, x2)
-        history.append(err)
-        flags.append(fl)
-        if record_trace:
-            s_dev, _, l_dev = eng.export_blocks(True, False, True)
-            s_core, s_fib = eng.split_blocks(s_dev.cpu().numpy())
-            l_core, l_fib = eng.split_blocks(l_dev.cpu().numpy())
-            trace.append({"iteration": k, "zeta": zeta, "indices": idx, "s_core": s_core, "s_fibers": s_fib,
-                          "l_core": l_core, "l_fibers": l_fib, "error": err})
-        if err <= cfg.eps:
-            converged = True
-            break
-    if copies:
-        eng.bind_mode_copies(None, ())   # the loop is done; exports do not gather
+                next_idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+                timings["sample"] += time.perf_counter() - t1
+                if prefetch:
+                    t1 = time.perf_counter()
+                    eng.set_sample(next_idx)
+                    src.load_blocks(eng, next_idx)
+                    staged = True
+                    timings["gather"] += time.perf_counter() - t1
+            e2, x2, fl = eng.iterate_wait()
+            timings["build"] += time.perf_counter() - t0
+            err = _error_from_sums(e2, x2)
+            history.append(err)
+            flags.append(fl)
+            if record_trace:
+                s_dev, _, l_dev = eng.export_blocks(True, False, True)
+                s_core, s_fib = eng.split_blocks(s_dev.cpu().numpy())
+                l_core, l_fib = eng.split_blocks(l_dev.cpu().numpy())
+                trace.append({"iteration": k, "zeta": zeta, "indices": idx, "s_core": s_core, "s_fibers": s_fib,
+                              "l_core": l_core, "l_fibers": l_fib, "error": err})
+            if on_iteration is not None:
+                on_iteration(k, eng, idx, zeta, err, fl)
+            if err <= cfg.eps:
+                converged = True
+                break
+    finally:
+        if copies:
+            eng.bind_mode_copies(None, ())   # the loop is done (or failed); exports do not gather
     timings["loop"] = time.perf_counter() - t_loop
     timings["total"] = time.perf_counter() - t_start
-    if PROFILE:
+    timings["timing_source"] = "host"
+    if PROFILE or phase_events:
         ph = eng.profile_read(reset=True)
-        timings["device_ms"] = {k: v[0] for k, v in ph.items()}
-        timings["device_launches"] = {k: v[1] for k, v in ph.items()}
+        if PROFILE:
+            timings["device_ms"] = {k: v[0] for k, v in ph.items()}
+            timings["device_launches"] = {k: v[1] for k, v in ph.items()}
+        if PROFILE_PHASES is None:   # every phase timed: the reference's keys from device events
+            timings["host_loop"] = timings["build"]
+            for key, names in _REF_PHASES.items():
+                timings[key] = 1e-3 * sum(ph[nm][0] for nm in names)
+            timings["timing_source"] = "device-events"
         eng.profile(False)
     return _make_result(eng, src, idx, cfg, history, flags, timings, zeta, converged, trace)

@@ -15,6 +15,8 @@ from __future__ import annotations
 
 from typing import Iterable, Sequence
 
+import math
+
 import numpy as np
 
 __all__ = ["DenseTensor", "DeviceTensor", "mode_stride", "decode_fiber_columns", "fiber_base_offsets", "as_shape"]
@@ -51,7 +53,7 @@ class DenseTensor:
     def __init__(self, data: Iterable[float], shape: Sequence[int]):
         shape = as_shape(shape)
         flat = np.asarray(data, dtype=np.float64).reshape(-1)
-        total = int(np.prod(shape, dtype=np.int64))
+        total = math.prod(shape)
         if flat.size != total:
             raise ValueError(f"data length {flat.size} does not match shape {shape} (expected {total})")
         arr = np.array(flat, dtype=np.float64, copy=True).reshape(shape, order="F")
@@ -129,7 +131,7 @@ class DeviceTensor:
         flat = flat.reshape(-1)
         if not flat.is_contiguous():
             raise ValueError("DeviceTensor storage must be contiguous")
-        if flat.numel() != int(np.prod(shape, dtype=np.int64)):
+        if flat.numel() != math.prod(shape):
             raise ValueError(f"{flat.numel()} elements do not match shape {shape}")
         self.flat = flat
         self.shape = shape
@@ -190,7 +192,7 @@ def decode_fiber_columns(shape: Sequence[int], k: int, cols: np.ndarray) -> tupl
         raise ValueError(f"mode {k} out of range for {len(shape)}-mode tensor")
     cols = np.asarray(cols, dtype=np.int64).reshape(-1)
     others = [d for j, d in enumerate(shape, start=1) if j != k]
-    total = int(np.prod(others, dtype=np.int64)) if others else 1
+    total = math.prod(others)
     if cols.size and (cols.min() < 1 or cols.max() > total):
         raise IndexError(f"column index outside [1, {total}] for mode {k} of {shape}")
     rem = cols - 1

@@ -18,6 +18,7 @@ offending byte offset exactly as the reference does (tensorfile.py:50-115).
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import struct
 
@@ -62,7 +63,7 @@ def read_header(path) -> tuple[int, tuple[int, ...]]:
 def read_tensor(path) -> DenseTensor:
     """Host DenseTensor (tensorfile.py:94-115): validated header, exact payload size."""
     _, dims, off = _header(path, True)
-    count = int(np.prod(dims, dtype=np.int64))
+    count = math.prod(dims)
     with open(path, "rb") as f:
         f.seek(off)
         flat = np.fromfile(f, dtype="<f8", count=count)
@@ -100,7 +101,7 @@ def read_tensor_device(path, dtype=None, slab=None, stream=None) -> DeviceTensor
         raise ValueError(f"slab {slab} outside mode 1 of extent {dims[0]}")
     shape = (hi - lo,) + tuple(dims[1:])
     dev = torch.device("cuda", torch.cuda.current_device())
-    out = torch.empty(int(np.prod(shape, dtype=np.int64)), dtype=dtype, device=dev)
+    out = torch.empty(math.prod(shape), dtype=dtype, device=dev)
     st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
     nat.check(nat.load().rtcur_tnsr_load(os.fsencode(os.fspath(path)), int(lo), int(hi),
                                          0 if dtype == torch.float64 else 1, out.data_ptr(), st))

@@ -284,3 +284,69 @@ def test_solve_on_recycled_device_memory():
     assert np.array_equal(_flat(res.sparse.core) != 0, _flat(ref.s_core) != 0)
     for m in range(3):
         assert np.array_equal(res.sparse.fibers[m] != 0, ref.s_fibers[m] != 0)
+
+
+def test_sparse_estimate_outlives_its_result():
+    """res.sparse must keep its own blocks after the SolveResult is dropped and a
+    same-geometry solve reuses the pooled engine (reference SparseEstimate holds
+    arrays, solver.py:121-127)."""
+    import gc
+
+    shape, ranks = (24, 20, 16), (2, 2, 2)
+    rows, cols = baseline_sample_sizes(shape, ranks)
+    kw = dict(ranks=ranks, eps=1e-5, variant="F", max_iters=60, row_sample_sizes=rows, col_sample_sizes=cols)
+    xa, _, _ = make_gaussian_tucker(shape, ranks, 0.15, 10.0, seed=5)
+    xb, _, _ = make_gaussian_tucker(shape, ranks, 0.25, 10.0, seed=6)
+    want = orc.solve(xa, shape, ranks, **{k: v for k, v in kw.items() if k != "ranks"}, seed=3)
+    res = rtcur(DenseTensor(xa, shape), SolverConfig(seed=3, **kw))
+    sp = res.sparse
+    del res
+    gc.collect()
+    other = rtcur(DenseTensor(xb, shape), SolverConfig(seed=4, **kw))
+    np.testing.assert_allclose(_flat(sp.core), _flat(want.s_core), atol=1e-10)
+    for m in range(3):
+        np.testing.assert_allclose(sp.fibers[m], want.s_fibers[m], atol=1e-10)
+    assert other.iterations >= 1
+
+
+def test_dense_accessor_methods_match_oracle():
+    """DenseTensorAccessor.core_block / fiber_block / inf_norm (solver.py:162-192)."""
+    from paper_2108_10448_b200 import DenseTensorAccessor
+
+    shape = (7, 5, 6, 4)
+    rng = np.random.default_rng(9)
+    xf = rng.standard_normal(int(np.prod(shape)))
+    acc = DenseTensorAccessor(DenseTensor(xf, shape))
+    arr = xf.reshape(shape, order="F")
+    rows = tuple(np.sort(rng.choice(d, s, replace=False)) + 1 for d, s in zip(shape, (3, 2, 4, 1)))
+    np.testing.assert_array_equal(acc.core_block(rows), orc.core_block(arr, rows))
+    for k in range(1, 5):
+        tot = int(np.prod(shape)) // shape[k - 1]
+        cols = np.sort(rng.choice(tot, 9, replace=False)) + 1
+        np.testing.assert_array_equal(acc.fiber_block(k, cols), orc.gather_fibers(xf, shape, k, cols))
+    assert acc.inf_norm() == float(np.max(np.abs(xf)))
+    with pytest.raises(IndexError):
+        acc.core_block((np.array([8]), np.array([1]), np.array([1]), np.array([1])))
+
+
+def test_phase_timings_from_device_events():
+    from paper_2108_10448_b200 import solver as solver_mod
+
+    shape, ranks = (30, 24, 20), (2, 2, 2)
+    rows, cols = baseline_sample_sizes(shape, ranks)
+    xf, _, _ = make_gaussian_tucker(shape, ranks, 0.15, 10.0, seed=8)
+    cfg = SolverConfig(ranks=ranks, eps=1e-5, variant="R", max_iters=40, seed=2, row_sample_sizes=rows,
+                       col_sample_sizes=cols)
+    base = rtcur(DenseTensor(xf, shape), cfg)
+    assert base.timings["timing_source"] == "host"
+    solver_mod.PHASE_TIMINGS = True
+    try:
+        res = rtcur(DenseTensor(xf, shape), cfg)
+    finally:
+        solver_mod.PHASE_TIMINGS = False
+    t = res.timings
+    assert t["timing_source"] == "device-events"
+    assert set(t) >= {"sample", "gather", "eval_lowrank", "threshold", "build", "error", "total"}
+    for key in ("gather", "eval_lowrank", "threshold", "build", "error"):
+        assert t[key] > 0.0, key
+    assert res.error_history == base.error_history

@@ -154,3 +154,100 @@ def test_oracle_cfg0_matches_reference_summary():
         assert np.array_equal(np.packbits(s != 0), g[f"s_fib{m}_bits"])
         np.testing.assert_allclose(s[g[f"s_fib{m}_pos"]], g[f"s_fib{m}_val"], atol=1e-10)
         np.testing.assert_allclose(res.cur.intersections[m].singular_values, g[f"sv{m}"], rtol=1e-10)
+
+
+def test_eval_fibers_blas_matches_einsum():
+    """The BLAS-associated fiber evaluation the parity runs use equals the
+    reference-shaped einsum (fiber_cur.py:318-326) to rounding, for 1-4 modes
+    and column chunking."""
+    rng = np.random.default_rng(11)
+    for shape, isz in [((9,), (4,)), ((12, 7), (5, 3)), ((30, 20, 10), (6, 5, 4)),
+                       ((11, 9, 7, 5), (4, 3, 5, 2))]:
+        n = len(shape)
+        core = np.asfortranarray(rng.standard_normal(isz))
+        facs = tuple(rng.standard_normal((d, i)) for d, i in zip(shape, isz))
+        cur = orc.OracleCur(core=core, fibers=tuple(np.zeros((d, 1)) for d in shape), intersections=(),
+                            indices=None, factors=facs)
+        for k in range(1, n + 1):
+            tot = int(np.prod(shape)) // shape[k - 1]
+            cols = np.sort(rng.choice(tot, min(tot, 23), replace=False)) + 1
+            a = orc.eval_fibers_einsum(cur, k, cols)
+            for chunk in (1 << 28, 64):
+                b = orc.eval_fibers_blas(cur, k, cols, chunk_bytes=chunk)
+                np.testing.assert_allclose(b, a, rtol=0, atol=1e-13 * max(1.0, np.abs(a).max()))
+
+
+def test_oracle_einsum_and_blas_solves_agree():
+    g = load_golden("solve_d10_R.npz")
+    shape = tuple(int(d) for d in g["shape"])
+    kw = golden_cfg_kwargs(g)
+    ranks = kw.pop("ranks")
+    a = orc.solve(g["x"], shape, ranks, eval_mode="einsum", **kw)
+    b = orc.solve(g["x"], shape, ranks, eval_mode="blas", **kw)
+    assert a.iterations == b.iterations
+    np.testing.assert_allclose(a.error_history, b.error_history, atol=1e-13, rtol=0)
+    np.testing.assert_array_equal(a.s_core != 0, b.s_core != 0)
+
+
+def test_iter_solve_yields_reference_loop_state():
+    """iter_solve's per-iteration state: zeta = gamma^k zeta0, S = HT(X - L_prev),
+    error recomputed from the yielded blocks (solver.py:324-355)."""
+    g = load_golden("solve_d10_F.npz")
+    shape = tuple(int(d) for d in g["shape"])
+    kw = golden_cfg_kwargs(g)
+    ranks = kw.pop("ranks")
+    zeta0 = orc.inf_norm(np.asarray(g["x"], dtype=np.float64)) if kw["zeta0"] is None else kw["zeta0"]
+    for it in orc.iter_solve(g["x"], shape, ranks, **kw):
+        k = it["iteration"]
+        assert it["zeta"] == pytest.approx(kw["gamma"] ** k * zeta0, rel=1e-14)
+        np.testing.assert_array_equal(it["s_core"], orc.hard_threshold(it["x_core"] - it["l_prev"][0], it["zeta"]))
+        e_core = it["x_core"] - it["l_core"] - it["s_core"]
+        e_f = [x - lf - s for x, lf, s in zip(it["x_fibers"], it["l_fibers"], it["s_fibers"])]
+        assert orc.sampled_relative_error(e_core, e_f, it["x_core"], it["x_fibers"]) == it["error"]
+        assert len(it["cur"].spectra) == len(shape)
+        for m, inter in enumerate(it["cur"].intersections):
+            np.testing.assert_array_equal(it["cur"].spectra[m][:ranks[m]], inter.singular_values)
+
+
+def test_oracle_cfg1_matches_reference_summary():
+    """BASELINE config 1 (400^3, RTCUR-R, fp64, the bench headline) solved by the
+    oracle vs the REAL reference's run of the same instance
+    (tests/golden/make_cfg1_golden.py): every iteration's index sets and S
+    support per block (SHA-256), error (1e-10), S and L at fixed positions
+    (1e-10); final singular values and the low-rank estimate at 2000 positions."""
+    import hashlib
+
+    from paper_2108_10448_b200.synth import baseline_sample_sizes, make_config
+
+    def sha(a):
+        return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), dtype=np.uint8)
+
+    g = load_golden("cfg1_summary.npz")
+    xf, _, _, bc = make_config(1)
+    rows, cols = baseline_sample_sizes(bc.shape, bc.ranks)
+    n = len(bc.shape)
+    last = None
+    k = 0
+    for it in orc.iter_solve(xf, bc.shape, bc.ranks, eps=bc.eps, variant=bc.variant, max_iters=100,
+                             seed=bc.seed_solver, row_sample_sizes=rows, col_sample_sizes=cols):
+        t = it["iteration"] - 1
+        idx = it["indices"]
+        assert np.array_equal(sha(np.concatenate([np.asarray(a, dtype=np.int64) for a in
+                                                  list(idx.rows) + list(idx.cols)])), g[f"t{t}_idx_sha"])
+        assert it["error"] == pytest.approx(float(g["error_history"][t]), abs=1e-10)
+        assert it["zeta"] == pytest.approx(float(g[f"t{t}_zeta"]), rel=1e-15)
+        sb = [it["s_core"].reshape(-1, order="F")] + [f.reshape(-1, order="F") for f in it["s_fibers"]]
+        lb = [it["l_core"].reshape(-1, order="F")] + [f.reshape(-1, order="F") for f in it["l_fibers"]]
+        for b in range(n + 1):
+            assert np.array_equal(sha(np.packbits(sb[b] != 0.0)), g[f"t{t}_b{b}_supp_sha"]), (t, b)
+            np.testing.assert_allclose(sb[b][g[f"pos{b}"]], g[f"t{t}_b{b}_s"], atol=1e-10, rtol=0)
+            np.testing.assert_allclose(lb[b][g[f"pos{b}"]], g[f"t{t}_b{b}_l"], atol=1e-10, rtol=0)
+        last = it
+        k += 1
+    assert k == int(g["iterations"])
+    assert np.array_equal(np.packbits(last["s_core"].reshape(-1, order="F") != 0), g["s_core_bits"])
+    for m in range(n):
+        sv = last["cur"].intersections[m].singular_values
+        np.testing.assert_allclose(sv, g[f"sv{m}"], rtol=1e-10)
+    low = orc.reconstruct_full(last["cur"]).reshape(-1, order="F")
+    np.testing.assert_allclose(low[g["L_pos"]], g["L_val"], atol=1e-10 * float(np.max(np.abs(g["L_val"]))))

@@ -97,3 +97,19 @@ def test_round_trip_property(tmp_path):
         back = read_tensor(p)
         assert back.shape == shape
         assert np.array_equal(back.data, t.data)
+
+
+@pytest.mark.parametrize("dims", [(2 ** 32,) * 4, (2 ** 63 - 1, 3), (2 ** 64 - 1,), (2 ** 40, 2 ** 40, 2 ** 40)])
+def test_huge_extents_rejected_like_reference(tmp_path, dims):
+    """A header whose extents overflow 64/128-bit products must fail the payload
+    check with the reference's exact text (Python-int product,
+    tensorfile.py:94-108), never wrap to a small size."""
+    p = tmp_path / "huge.tnsr"
+    p.write_bytes(MAGIC + struct.pack("<HH", FORMAT_VERSION, len(dims)) + struct.pack(f"<{len(dims)}Q", *dims))
+    count = 1
+    for d in dims:
+        count *= d
+    with pytest.raises(TensorFormatError) as exc:
+        read_tensor(p)
+    assert str(exc.value) == (f"{p}: payload at byte {8 + 8 * len(dims)} holds 0 bytes, dims {tuple(dims)} "
+                              f"require {count * 8}")
