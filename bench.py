@@ -13,13 +13,19 @@ iterations / device time), ``ms_per_step`` = seconds-to-tolerance.  X is
 copies X from pinned host memory to HBM, solves, and materialises the full
 SolveResult on the host (sparse blocks, FiberCur pieces).
 
-``--impl reference`` times the CPU port of the reference loop (oracle/, the
-reference itself is Python and cannot be installed as a GPU-box baseline) on
-the host cores: one step = one steady-state RTCUR-R iteration of the same
-config.
+``parity``: the timed solve against the real reference's solve of the same
+instance (tests/golden/cfg1_summary.npz).  ``per_config``: configs 0, 2, 3, 4
+measured the same way (3 solves each) with their phase HBM fractions.
 
-Multi-GPU (torchrun, N>1): config 1 does not shard (BASELINE runs it on one
-GPU), so N ranks run N independent replicas ("scaling": "weak").
+``--impl reference`` times the REAL reference package (oracle/_ref, built by
+oracle/build_ref.sh from /root/reference/pkg with its Cython backend) through
+its public rtcur() API on the host cores: one step = one RTCUR iteration
+(steady-state iterations W+1..W+K of the same config's solve); it falls back to
+the oracle port only when oracle/_ref is missing.
+
+Multi-GPU (torchrun, N>1): config 4 by default, sharded in mode-1 slabs
+(``"scaling": "strong"``, all-gather of the owned sampled entries); an
+explicit ``--config 0|1|3`` runs N independent replicas (``"weak"``).
 """
 
 from __future__ import annotations
@@ -152,38 +158,97 @@ def _fp64_fmas(bc, rows, cols):
     }
 
 
+def _default_config(args, world: int) -> int:
+    """config 1 (BASELINE's single-GPU headline) at N=1; config 4 (mode-1 slabs,
+    BASELINE's sharded R config) under torchrun."""
+    if args.config is not None:
+        return int(args.config)
+    return 1 if world == 1 else 4
+
+
+def _host_problem(config: int):
+    """(bc, rows, cols, x64 flat F-order) -- configs 0-1 from the host generator,
+    2-4 from the device generator copied back (exact fp32 -> fp64)."""
+    from paper_2108_10448_b200.synth import CONFIGS, baseline_sample_sizes, make_config
+
+    bc = CONFIGS[config]
+    rows, cols = baseline_sample_sizes(bc.shape, bc.ranks)
+    if config <= 1 or bc.kind == "video":
+        xf, _, _, bc = make_config(config)
+        return bc, rows, cols, xf.astype(np.float64)
+    import torch
+
+    from paper_2108_10448_b200.synth import make_config_device
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    x_dev, bc = make_config_device(config)
+    x64 = x_dev.flat.cpu().numpy().astype(np.float64)
+    del x_dev
+    torch.cuda.empty_cache()
+    return bc, rows, cols, x64
+
+
+def _reference_sample(bc, rows, cols, x64, warmup: int, steps: int):
+    """Time the REAL reference (oracle/_ref: rtcur with its compiled Cython backend,
+    driven through its public rtcur()/TensorAccessor API) on iterations
+    warmup+1 .. warmup+steps of this config's solve.  Falls back to the oracle
+    port (kind "port", its einsum evaluation = the reference's cost) when
+    oracle/_ref was not built."""
+    from oracle import ref_runner
+
+    kw = dict(eps=bc.eps, variant=bc.variant, max_iters=warmup + steps, seed=bc.seed_solver,
+              row_sample_sizes=rows, col_sample_sizes=cols)
+    if ref_runner.available():
+        res, info = ref_runner.run(x64, bc.shape, bc.ranks, **kw)
+        its = info["iter_times"]
+        kind = "reference"
+        what = ("the reference package itself (oracle/_ref, built from /root/reference/pkg by oracle/build_ref.sh; "
+                "RTCUR_BACKEND=compiled), rtcur.rtcur() through its TensorAccessor API")
+        extra = {"error_history": info["error_history"], "iterations": res.iterations,
+                 "s_core_support_sha256": info["s_core_support_sha256"], "backend": info["backend"],
+                 "setup_s": info["setup_s"], "wall_s": info["wall_s"]}
+    else:
+        from oracle import rtcur_oracle as orc
+
+        orc.build_oracle_lib()
+        r = orc.solve(x64, bc.shape, bc.ranks, eval_mode="einsum", **kw)
+        its = list(r.iter_times)
+        kind = "port"
+        what = "the oracle port (oracle/rtcur_oracle.py, einsum evaluation as the reference) -- oracle/_ref missing"
+        extra = {"error_history": list(r.error_history), "iterations": r.iterations, "wall_s": sum(its)}
+    timed = [t for t in its[warmup:warmup + steps] if t is not None]
+    if len(timed) < steps:   # converged early / untimed first iteration: the trailing timed iterations
+        timed = [t for t in its if t is not None][-steps:]
+    value = len(timed) / sum(timed)
+    first = len(its) - len(timed) + 1 if len(timed) < steps else warmup + 1
+    sample = (f"RTCUR-{bc.variant} iterations {first}..{first + len(timed) - 1} of config {bc.index} "
+              f"({'x'.join(map(str, bc.shape))}) on the host: {what}; numpy/OpenBLAS on all host threads, einsum "
+              f"and the Cython kernels single-threaded as in the reference")
+    return {"value": value, "unit": "iters/s", "cores": os.cpu_count(), "kind": kind, "sample": sample,
+            "ms_per_iteration": 1e3 * sum(timed) / len(timed), "iterations_timed": len(timed)}, extra
+
+
 def run_reference(args):
     world, rank, _ = _dist()
-    if rank != 0:
+    if rank != 0:   # the CPU reference runs once per box (rank 0)
         return 0
-    from oracle import rtcur_oracle as orc
-
-    orc.build_oracle_lib()
-    xf, _, bc, rows, cols = _make_problem(args.config)
-    x64 = xf.astype(np.float64)
-    n_iters = args.warmup + args.steps
+    config = _default_config(args, world)
+    bc, rows, cols, x64 = _host_problem(config)
     t0 = time.perf_counter()
-    res = orc.solve(x64, bc.shape, bc.ranks, eps=bc.eps, variant=bc.variant, max_iters=n_iters, seed=bc.seed_solver,
-                    row_sample_sizes=rows, col_sample_sizes=cols)
+    cpu, extra = _reference_sample(bc, rows, cols, x64, args.warmup, args.steps)
     wall = time.perf_counter() - t0
-    its = res.iter_times
-    timed = its[args.warmup:args.warmup + args.steps]
-    if len(timed) < args.steps:   # converged early: time the trailing iterations available
-        timed = its[-args.steps:]
-    value = len(timed) / sum(timed)
-    cores = os.cpu_count()
     line = {
-        "metric": METRIC, "value": value, "unit": "iters/s", "impl": "reference", "n_gpus": world,
-        "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * sum(timed) / len(timed),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": bc.dtype,
+        "metric": METRIC, "value": cpu["value"], "unit": "iters/s", "impl": "reference", "n_gpus": world,
+        "steps": cpu["iterations_timed"], "warmup": args.warmup, "ms_per_step": cpu["ms_per_iteration"],
+        "higher_is_better": True, "scaling": "strong" if (world > 1 and _sharded(config)) else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, paper_2108_10448_b200.synth)",
-        "config": _config_dict(bc, rows, cols, world),
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port",
-                         "sample": f"RTCUR-{bc.variant} iterations {args.warmup + 1}..{args.warmup + len(timed)} of "
-                                   f"config {bc.index} on the host (numpy/OpenBLAS all cores; einsum and SVD "
-                                   f"single-threaded as in the reference)"},
-        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": wall,
+        "config": _config_dict(bc, rows, cols, 1),
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_run": extra, "wall_s": wall,
+        "step_note": "one step = one RTCUR iteration of the reference's solve (a full GPU-arm step is a whole "
+                     "solve; iters/s is the common unit)",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -199,17 +264,35 @@ def _config_dict(bc, rows, cols, world, shard=False):
                             f"replicas x{world}" if world > 1 else "single GPU")}
 
 
-def _cpu_baseline(bc, rows, cols, xf, budget_iters=2):
-    from oracle import rtcur_oracle as orc
+def _cpu_baseline(bc, rows, cols, x64):
+    """Reported CPU baseline for the b200 arm's line: the real reference on
+    iterations 2..3 of the same solve (a bounded sample, ~30 s on the box)."""
+    cpu, _ = _reference_sample(bc, rows, cols, x64, 1, 2)
+    return cpu
 
-    orc.build_oracle_lib()
-    res = orc.solve(xf.astype(np.float64), bc.shape, bc.ranks, eps=bc.eps, variant=bc.variant,
-                    max_iters=budget_iters, seed=bc.seed_solver, row_sample_sizes=rows, col_sample_sizes=cols)
-    t = res.iter_times[-1]
-    return {"value": 1.0 / t, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"iteration {len(res.iter_times)} (steady state, both _eval_blocks) of a config-{bc.index} "
-                      f"RTCUR-{bc.variant} solve by the oracle port on the host; setup (sample+gather) "
-                      f"{res.timings['gather'] + res.timings['sample']:.2f}s excluded"}
+
+def _parity_block(config: int, res):
+    """The timed solve against the REAL reference's solve of the same instance
+    (tests/golden/cfg1_summary.npz, tests/golden/make_cfg1_golden.py): error
+    history (1e-10 abs), iteration count, final S support of the core block
+    (bit-exact) and singular values (1e-10 rel).  Config 1 only."""
+    p = os.path.join(ROOT, "tests", "golden", f"cfg{config}_summary.npz")
+    if not os.path.exists(p):
+        return None
+    g = np.load(p)
+    eh = np.asarray(res.error_history)
+    ref_eh = np.asarray(g["error_history"])
+    same_len = eh.size == ref_eh.size
+    err_diff = float(np.max(np.abs(eh - ref_eh))) if same_len else None
+    core = np.asarray(res.sparse.core).reshape(-1, order="F")
+    supp = bool(np.array_equal(np.packbits(core != 0), g["s_core_bits"]))
+    sv = max(float(np.max(np.abs(res.cur.intersections[m].singular_values - g[f"sv{m}"]) / g[f"sv{m}"][0]))
+             for m in range(len(res.cur.indices.rows)))
+    ok = bool(same_len and err_diff <= 1e-10 and supp and sv <= 1e-10 and res.converged == bool(g["converged"]))
+    return {"vs": "the real reference's solve of this instance (tests/golden/cfg1_summary.npz)", "ok": ok,
+            "iterations": [int(res.iterations), int(g["iterations"])], "error_history_max_abs_diff": err_diff,
+            "s_core_support_equal": supp, "sigma_max_rel_diff": sv,
+            "full_record": "profiles/r02_parity_config*.json (tools/parity_configs.py, per-iteration lockstep)"}
 
 
 def _ncu_traffic(config: int, phase: str):
@@ -265,6 +348,76 @@ def _sharded(config: int) -> bool:
     return config in (2, 4)
 
 
+def _per_config(configs, local: int, peak: float, steps: int = 3):
+    """Compact single-GPU measurements of the other BASELINE configs: iters/s and
+    seconds-to-tolerance over `steps` device-resident solves (CUDA events, one
+    warm-up solve), the HBM fraction of every sampled-block phase from one
+    profiled solve (events around each phase), K3 / K0 fractions, clocks."""
+    import torch
+
+    from paper_2108_10448_b200 import DeviceTensor, SolverConfig, rtcur
+    from paper_2108_10448_b200 import solver as solver_mod
+    from paper_2108_10448_b200.synth import CONFIGS, baseline_sample_sizes, make_config_device
+
+    out = {}
+    clocks = ClockSampler(local)
+    clocks.start()
+    for c in configs:
+        bc = CONFIGS[c]
+        rows, cols = baseline_sample_sizes(bc.shape, bc.ranks)
+        if c <= 1:
+            xf, _, bc, rows, cols = _make_problem(c)
+            x_dev = DeviceTensor(torch.from_numpy(xf).cuda(), bc.shape)
+        else:
+            x_dev, _ = make_config_device(c)
+        cfg = SolverConfig(ranks=bc.ranks, eps=bc.eps, gamma=0.7, variant=bc.variant, max_iters=100,
+                           seed=bc.seed_solver, row_sample_sizes=rows, col_sample_sizes=cols)
+        solver_mod.PROFILE, solver_mod.PROFILE_PHASES = True, None
+        res = rtcur(x_dev, cfg)   # warm (engine) + the profiled breakdown pass
+        res = None
+        res = rtcur(x_dev, cfg)
+        solver_mod.PROFILE = False
+        dm, dn = res.timings["device_ms"], res.timings["device_launches"]
+        total_dev = sum(dm.values())
+        alg, _ = _algorithmic_bytes(bc, rows, cols)
+        fr = {}
+        for ph, b in alg.items():
+            if dn.get(ph):
+                us = 1e3 * dm[ph] / dn[ph]
+                fr[ph] = {"frac": b / (us * 1e-6) / 1e9 / peak, "launch_us": us, "alg_bytes_per_launch": b,
+                          "share": dm[ph] / total_dev}
+        shares = {k: round(v / total_dev, 4) for k, v in sorted(dm.items(), key=lambda kv: -kv[1]) if dn.get(k)}
+        phases = {"absmax": {"ms_per_step": dm["absmax"], "launches_per_step": dn["absmax"]}} if dn.get("absmax") \
+            else {}
+        full = _full_tensor_rooflines(res, x_dev, bc, phases, peak, 1)
+        res = None
+        res = rtcur(x_dev, cfg)   # untimed: per-iteration graphs without profiling events
+        res = None
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters, conv = 0, True
+        ev0.record()
+        for _ in range(steps):
+            res = None
+            res = rtcur(x_dev, cfg)
+            iters += res.iterations
+            conv &= res.converged
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        out[str(c)] = {"workload": _config_dict(bc, rows, cols, 1)["workload"], "iters_per_s": iters / (ms / 1e3),
+                       "ms_per_solve": ms / steps, "iterations_per_solve": iters / steps, "converged": bool(conv),
+                       "hbm_phases": fr, "device_time_shares": shares,
+                       "k3_full_frac": full["k3_full"]["frac"], "k0_absmax_frac": full.get("k0_absmax", {}).get("frac")}
+        res = None
+        del x_dev
+        torch.cuda.empty_cache()
+    out["clocks"] = clocks.stop()
+    out["note"] = (f"{steps} timed device-resident solves per config after one warm-up; phase fractions from one "
+                   "profiled solve; alg bytes per DESIGN.md §3")
+    return out
+
+
 def run_b200(args):
     import torch
 
@@ -282,18 +435,19 @@ def run_b200(args):
     from paper_2108_10448_b200.dist import rtcur_sharded
     from paper_2108_10448_b200.synth import CONFIGS, baseline_sample_sizes, make_config_device, slab_bounds
 
-    bc = CONFIGS[args.config]
+    config = _default_config(args, world)
+    bc = CONFIGS[config]
     rows, cols = baseline_sample_sizes(bc.shape, bc.ranks)
     dt = torch.float64 if bc.dtype == "f64" else torch.float32
-    shard = _sharded(args.config) and world > 1
+    shard = _sharded(config) and world > 1
     slab = slab_bounds(bc.shape[0], world, rank) if shard else None
     xf = None
-    if args.config <= 1:
-        xf, _, bc, rows, cols = _make_problem(args.config)
+    if config <= 1:
+        xf, _, bc, rows, cols = _make_problem(config)
         host = torch.from_numpy(xf).to(dt)
         x_dev = DeviceTensor(host.cuda(), bc.shape)
     else:
-        x_dev, _ = make_config_device(args.config, slab=slab, group=group if shard else None)
+        x_dev, _ = make_config_device(config, slab=slab, group=group if shard else None)
         host = None
     cfg = SolverConfig(ranks=bc.ranks, eps=bc.eps, gamma=0.7, variant=bc.variant, max_iters=100,
                        seed=bc.seed_solver + (0 if shard else 1000 * rank), row_sample_sizes=rows,
@@ -375,6 +529,7 @@ def run_b200(args):
     # K3 / K0 rooflines on the timed solve's iterate (before the e2e loop, so that loop
     # recycles the warmed-up engines instead of building a new one)
     full_roof = _full_tensor_rooflines(res_dev, x_dev, bc, phases, peak, args.steps)
+    parity = _parity_block(config, res_dev) if not shard else None
     del res_dev, res
 
     # ---------------- e2e through the public API with host buffers
@@ -383,7 +538,7 @@ def run_b200(args):
     pinned = host.pin_memory()
     x_buf = torch.empty_like(x_dev.flat)
     e2e_iters, d2h = 0, 0
-    e2e_steps = max(1, args.steps if args.config <= 1 else min(args.steps, 2))
+    e2e_steps = max(1, args.steps if config <= 1 else min(args.steps, 2))
     # untimed warm-up of the host-buffer path: the exports' pinned staging buffer and
     # the result arrays' first touch are one-time costs (~0.2 s at config 1)
     res = None
@@ -424,7 +579,7 @@ def run_b200(args):
     kname = {"threshold": "k_fiber_pass (threshold over X(I_k, J_k))", "error": "k_fiber_pass (error: core + fibers)",
              "gather": "k_gather_fibers + k_gather", "apass": "k_fiber_pass (A pass) + k_fiber_areduce",
              "gpass": "k_block_pass (G pass)"}[dom]
-    traffic = _ncu_traffic(args.config, dom)
+    traffic = _ncu_traffic(config, dom)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic.get("bytes_per_launch") if traffic else None,
             "traffic_source": traffic.get("source") if traffic else None,
@@ -438,14 +593,20 @@ def run_b200(args):
                         "fma_per_launch": fmas[dom],
                         "peak_source": "measured: tools/fp64_pipes.cu (profiles/r01_fp64_pipes.txt)"}
 
+    # the other BASELINE configs (same device, after the headline measurement)
+    per_config = None
+    if world == 1 and not args.no_per_config:
+        del x_buf, pinned
+        per_config = _per_config([c for c in (0, 2, 3, 4) if c != config], local, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if xf is not None:
-            cpu = _cpu_baseline(bc, rows, cols, xf)
+            cpu = _cpu_baseline(bc, rows, cols, xf.astype(np.float64))
         else:
-            cpu = {"value": None, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"not run for config {bc.index}: one CPU iteration of the port takes minutes "
-                             "(SURVEY §6: ~12 min/iter config 2, ~91 s config 3, ~6.5 s config 4)"}
+            cpu = {"value": None, "unit": "iters/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"not run for config {bc.index} in the b200 arm (one reference iteration takes "
+                             "seconds to minutes here; SURVEY §6); bench.py --impl reference times it"}
 
     if rank == 0:
         line = {
@@ -461,7 +622,7 @@ def run_b200(args):
             "roofline": roof, "full_tensor_rooflines": full_roof, "phases": phases,
             "phases_note": f"per-phase CUDA-event times from a separate profiled pass of {bd_steps} solve(s); "
                            "the timed region carries events on the dominant phase only",
-            "clocks": clk, "cpu_baseline": cpu,
+            "clocks": clk, "cpu_baseline": cpu, "parity": parity, "per_config": per_config,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -475,8 +636,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE config (default: 1 at N=1, 4 sharded in mode-1 slabs under torchrun)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

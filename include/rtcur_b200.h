@@ -103,6 +103,19 @@ int rtcur_transpose_mode(const void* x, int dtype, int n, const int64_t* dims, i
 int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols);
 /* gather this rank's owned sampled entries into the compact x blocks (others 0) */
 int rtcur_engine_gather(rtcur_engine* e);
+/* Mode-1 slab sharding (replaces the reference's in-process
+ * _gather_blocks, solver.py:234-239, regathered per RTCUR-R iteration at
+ * solver.py:315-322).  bounds: world + 1 slab boundaries of mode 1 (0-based,
+ * bounds[rank], bounds[rank+1] = this engine's [lo, hi)).  After set_sample +
+ * gather: shard_plan returns each rank's packed entry count (host, world
+ * entries); shard_pack writes this rank's owned entries (dtype of X) to send;
+ * after an all-gather of the padded segments (recv = world x stride entries),
+ * shard_unpack writes every rank's entries into the replicated compact blocks,
+ * bit-identical to an unsharded gather. */
+int rtcur_engine_set_shards(rtcur_engine* e, int world, int rank, const int64_t* bounds);
+int rtcur_engine_shard_plan(rtcur_engine* e, int64_t* counts);
+int rtcur_engine_shard_pack(rtcur_engine* e, void* send);
+int rtcur_engine_shard_unpack(rtcur_engine* e, const void* recv, int64_t stride);
 /* Sample slots: set_sample + gather fill the inactive slot (so they may be enqueued
  * while the previous iteration still runs on the stream); the next iterate_async
  * makes it active.  Workspace byte offset of the compact blocks the next gather

@@ -28,7 +28,8 @@ EXPORTED = (
     "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_set_graphs", "rtcur_engine_absmax_begin", "rtcur_engine_absmax_end", "rtcur_engine_profile_read",
     "rtcur_append_distinct", "rtcur_generate_tucker", "rtcur_tnsr_read_header", "rtcur_tnsr_load", "rtcur_tnsr_store",
     "rtcur_scatter_outliers", "rtcur_abs_sum", "rtcur_ap_threshold", "rtcur_ap_residual", "rtcur_abs_max", "rtcur_engine_bind_mode_copies",
-    "rtcur_transpose_mode",
+    "rtcur_transpose_mode", "rtcur_engine_set_shards", "rtcur_engine_shard_plan", "rtcur_engine_shard_pack",
+    "rtcur_engine_shard_unpack",
 )
 PHASES = ("absmax", "prep", "gather", "threshold", "gram", "eig", "svdpost", "apass", "gpass", "wcols", "error",
           "export", "full")
@@ -89,6 +90,10 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_absmax.argtypes = [c_vp, c_dp]
     lib.rtcur_engine_set_sample.argtypes = [c_vp, ctypes.POINTER(c_i64p), ctypes.POINTER(c_i64p)]
     lib.rtcur_engine_gather.argtypes = [c_vp]
+    lib.rtcur_engine_set_shards.argtypes = [c_vp, ctypes.c_int, ctypes.c_int, c_i64p]
+    lib.rtcur_engine_shard_plan.argtypes = [c_vp, c_i64p]
+    lib.rtcur_engine_shard_pack.argtypes = [c_vp, c_vp]
+    lib.rtcur_engine_shard_unpack.argtypes = [c_vp, c_vp, c_i64]
     lib.rtcur_engine_xblocks_offset.argtypes = [c_vp, c_i64p]
     lib.rtcur_engine_iterate.argtypes = [c_vp, ctypes.c_double, ctypes.c_int, c_dp, c_i32p]
     lib.rtcur_engine_iterate_async.argtypes = [c_vp, ctypes.c_double, ctypes.c_int]

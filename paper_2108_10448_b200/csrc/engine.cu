@@ -576,6 +576,8 @@ struct GraphEntry {
   std::vector<ProfPair> prof;      // event-record nodes of the profiled phases
 };
 
+struct ShardState;   // shard_xchg.cu
+
 struct rtcur_engine {
   Plan P;
   char* ws;
@@ -616,6 +618,7 @@ struct rtcur_engine {
   bool xi_valid[2];                // the sample slot's intersection copies match its blocks
   cudaEvent_t absmax_ev;           // rtcur_engine_absmax_begin's D2H done
   bool absmax_pending;
+  ShardState* shard;               // mode-1 slab exchange plan (rtcur_engine_set_shards), or null
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
   i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
@@ -674,6 +677,8 @@ static void prof_flush(rtcur_engine* e) {
   }
   e->prof_pending->swap(keep);
 }
+
+#include "shard_xchg.cu"   // after prof_begin/prof_end, fail()/CK/LAUNCH_CHECK
 
 static int set_smem_limits_once() {
   // function attributes are per device context: once per device
@@ -841,6 +846,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
 extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   if (!e) return RT_OK;
   cudaStreamSynchronize(e->st);
+  shard_free(e);
   if (e->h_pinned) cudaFreeHost(e->h_pinned);
   if (e->h_idx) cudaFreeHost(e->h_idx);
   if (e->done) cudaEventDestroy(e->done);

@@ -215,6 +215,24 @@ class Engine:
     def gather(self):
         nat.check(self.lib.rtcur_engine_gather(self.handle))
 
+    # ------------------------------------------------------------ mode-1 slab exchange (csrc/shard_xchg.cu)
+    def set_shards(self, world: int, rank: int, bounds):
+        b = nat.i64_array([int(v) for v in bounds])
+        nat.check(self.lib.rtcur_engine_set_shards(self.handle, int(world), int(rank), b))
+        self.world = int(world)
+
+    def shard_plan(self):
+        """Packed entry count of every rank for the staged sample."""
+        counts = (ctypes.c_int64 * self.world)()
+        nat.check(self.lib.rtcur_engine_shard_plan(self.handle, counts))
+        return [int(c) for c in counts]
+
+    def shard_pack(self, send):
+        nat.check(self.lib.rtcur_engine_shard_pack(self.handle, ctypes.c_void_p(send.data_ptr())))
+
+    def shard_unpack(self, recv, stride: int):
+        nat.check(self.lib.rtcur_engine_shard_unpack(self.handle, ctypes.c_void_p(recv.data_ptr()), int(stride)))
+
     def iterate(self, zeta: float, first: bool):
         sums = (ctypes.c_double * (2 * (self.n + 1)))()
         flags = (ctypes.c_int32 * self.n)()

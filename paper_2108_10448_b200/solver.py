@@ -308,10 +308,14 @@ class _Source:
     by the fused K1 gather) or a generic host TensorAccessor (blocks uploaded).
 
     Sharded (``slab``/``group`` given): the device tensor is this rank's mode-1
-    slab of a ``global_shape`` tensor; the gather fills only the entries the
-    rank owns and a sum all-reduce of the compact blocks completes them (each
-    sampled entry has exactly one owner, so the sum is exact); zeta_0 is a max
-    all-reduce of the slab abs-maxima."""
+    slab of a ``global_shape`` tensor.  Every sampled entry has exactly one
+    owner (the rank whose slab holds its mode-1 index): the gather fills the
+    owned entries, ``shard_pack`` packs them, one all-gather of the packed
+    segments (padded to the largest) moves each entry once, and ``shard_unpack``
+    writes all of them into the replicated compact blocks -- bit-identical to
+    an unsharded gather, so the replicated CUR build, error and stop rule run
+    identically on every rank.  zeta_0 is a max all-reduce of the slab
+    abs-maxima (csrc/shard_xchg.cu)."""
 
     def __init__(self, x, slab=None, group=None, global_shape=None):
         import torch
@@ -350,27 +354,42 @@ class _Source:
     def attach(self, eng: Engine):
         if self.dev is not None:
             eng.bind(self.dev.flat)
+        if self.group is not None:
+            import torch
+
+            from . import dist as shard
+
+            world = shard.group_size(self.group)
+            lo_hi = shard.all_gather_host(torch.tensor(list(self.slab), dtype=torch.int64), self.group, eng.device)
+            bounds = [0]
+            for p in range(world):
+                lo, hi = (int(v) for v in lo_hi[2 * p:2 * p + 2])
+                if lo != bounds[-1]:
+                    raise ValueError(f"mode-1 slabs are not contiguous in rank order (rank {p} starts at {lo})")
+                bounds.append(hi)
+            if bounds[-1] != self.shape[0]:
+                raise ValueError(f"mode-1 slabs cover [0, {bounds[-1]}) of {self.shape[0]}")
+            eng.set_shards(world, shard.group_rank(self.group), bounds)
+
+    def reduce_max(self, v: float, device) -> float:
+        if self.group is None:
+            return v
+        from . import dist as shard
+
+        return shard.all_reduce_max(v, self.group, device)
 
     def inf_norm(self, eng: Engine) -> float:
         if self.dev is not None:
-            v = eng.absmax()
-            if self.group is not None:
-                import torch
-                import torch.distributed as dist
-
-                t = torch.tensor([v], dtype=torch.float64, device=eng.device)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
-                v = float(t.item())
-            return v
+            return self.reduce_max(eng.absmax(), eng.device)
         return float(self.accessor.inf_norm())
 
     def load_blocks(self, eng: Engine, idx: SampleIndices):
         if self.dev is not None:
             eng.gather()
             if self.group is not None:
-                import torch.distributed as dist
+                from . import dist as shard
 
-                dist.all_reduce(eng.xblocks(), op=dist.ReduceOp.SUM, group=self.group)
+                shard.exchange_blocks(eng, self.group)
             return
         import torch
 
@@ -510,7 +529,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
     try:
         # the device scans max|X| (and builds the mode copies) while the host draws the
         # first sample (the generator is consumed by sampling only, solver.py:293-316)
-        early_zeta = (cfg.zeta0 is None and src.dev is not None and src.group is None
+        early_zeta = (cfg.zeta0 is None and src.dev is not None
                       and os.environ.get("RTCUR_EARLY_ZETA", "1") != "0")
         if early_zeta:
             eng.absmax_begin()
@@ -525,7 +544,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
         if cfg.zeta0 is not None:
             zeta = float(cfg.zeta0)
         else:
-            zeta = eng.absmax_end() if early_zeta else src.inf_norm(eng)
+            zeta = src.reduce_max(eng.absmax_end(), eng.device) if early_zeta else src.inf_norm(eng)
         t_loop = time.perf_counter()
         history, flags = [], []
         trace = [] if record_trace else None
@@ -536,7 +555,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
         next_idx = None
         # device-resident local tensors: the next sample's upload and gather go into the
         # engine's inactive sample slot right behind the running iteration (no host gap)
-        prefetch = src.dev is not None and src.group is None
+        prefetch = src.dev is not None
         staged = False
         for k in range(1, cfg.max_iters + 1):
             if cfg.variant == "R" and k >= 2:
