@@ -619,6 +619,15 @@ struct rtcur_engine {
   cudaEvent_t absmax_ev;           // rtcur_engine_absmax_begin's D2H done
   bool absmax_pending;
   ShardState* shard;               // mode-1 slab exchange plan (rtcur_engine_set_shards), or null
+  // RTCUR-R prefetch: a sample staged while an iteration is in flight (set_sample +
+  // gather) runs on a side stream, concurrently with that iteration (its eigensolver
+  // occupies a few SMs); the side stream first waits for pre_ev (everything enqueued
+  // before the running iteration: the last readers of the slot being refilled) and
+  // the next iteration waits for side_ev.  RTCUR_SIDE_PREFETCH=0 keeps it in order.
+  bool use_side;
+  bool staging_on_side;
+  cudaStream_t side;
+  cudaEvent_t pre_ev, side_ev;
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
   i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
@@ -830,6 +839,13 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   for (int s = 0; s < 2; ++s) CK(cudaMemsetAsync(e->xb(s), 0, e->P.g.nblk_total * e->P.esize + 64, e->st));
   for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&e->idx_ev[s], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->absmax_ev, cudaEventDisableTiming));
+  {
+    const char* sv = getenv("RTCUR_SIDE_PREFETCH");
+    e->use_side = !(sv && sv[0] == '0');
+  }
+  CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e->pre_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->side_ev, cudaEventDisableTiming));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -872,6 +888,9 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
     delete e->graphs;
   }
   if (e->cap_st) cudaStreamDestroy(e->cap_st);
+  if (e->side) cudaStreamSynchronize(e->side), cudaStreamDestroy(e->side);
+  if (e->pre_ev) cudaEventDestroy(e->pre_ev);
+  if (e->side_ev) cudaEventDestroy(e->side_ev);
   if (e->prof_pool) {
     for (auto ev : *e->prof_pool) cudaEventDestroy(ev);
     delete e->prof_pool;
@@ -951,8 +970,28 @@ extern "C" int rtcur_engine_absmax(rtcur_engine* e, double* out) {
   return rtcur_engine_absmax_end(e, out);
 }
 
+// Issue the staging work of a prefetched sample on the side stream (see use_side)
+struct SideScope {
+  rtcur_engine* e;
+  cudaStream_t saved;
+  explicit SideScope(rtcur_engine* en) : e(en), saved(en->st) {
+    if (e->staging_on_side) e->st = e->side;
+  }
+  ~SideScope() {
+    if (e->staging_on_side) {
+      cudaEventRecord(e->side_ev, e->side);
+      e->st = saved;
+    }
+  }
+};
+
 extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
+  if (e->pending && e->use_side && !e->shard && !e->staging_on_side && e->use_graphs) {
+    e->staging_on_side = true;
+    CK(cudaStreamWaitEvent(e->side, e->pre_ev, 0));
+  }
+  SideScope side_scope(e);
   const Plan& P = e->P;
   const Geom& g = P.g;
   const i64 total = [&] { i64 t = 1; for (int m = 0; m < g.n; ++m) t *= g.dim[m]; return t; }();
@@ -1017,6 +1056,7 @@ static int refresh_xi(rtcur_engine* e, int slot);
 extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
   if (!e->sampled) return fail(RT_ERR_VALUE, "no sample set");
+  SideScope side_scope(e);
   const Plan& P = e->P;
   const int slot = e->stg >= 0 ? e->stg : e->act_slot();
   IndexPtrs ip = make_ip_slot(e, slot);
@@ -1595,11 +1635,18 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
   if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
   if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
+  if (e->staging_on_side) {   // the prefetched sample's staging must be complete
+    CK(cudaStreamWaitEvent(e->st, e->side_ev, 0));
+    e->staging_on_side = false;
+  }
   if (e->stg >= 0) {   // the staged sample (set_sample + gather) becomes the active one
     e->act = e->stg;
     e->stg = -1;
     e->sample_epoch++;
   }
+  // everything before this iteration (the previous iteration, exports) is what a
+  // prefetch into the other sample slot must wait for
+  CK(cudaEventRecord(e->pre_ev, e->st));
   if (first) e->cur = e->prev = -1;
   const double* st_s = (e->cur >= 0) ? e->state(e->cur) : nullptr;
   int newslot = 0;
