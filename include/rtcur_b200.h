@@ -211,6 +211,17 @@ int rtcur_ap_residual(const double* X, const double* L, const double* S, int64_t
  * order; returns the new length (-1 if a value is out of range). */
 int64_t rtcur_append_distinct(int64_t* out, int64_t nout, const int64_t* batch, int64_t nb, unsigned char* seen,
                               int64_t population);
+/* The whole iid branch of the reference's without-replacement draw
+ * (fiber_cur.py:197-208: batches of need + need//2 + 16 integers(0, population),
+ * first occurrences in order, sort(out[:k]) + 1), drawing from a numpy bit
+ * generator through its C interface (Generator.bit_generator.ctypes: state
+ * address + next_uint32) with numpy's bounded-integer algorithm, so the stream
+ * consumed is the one rng.integers would consume.  2 <= population <= 2^32 - 1,
+ * 1 <= k < population; seen: (population + 63) / 64 zeroed words (membership
+ * bitmap, left zeroed); out: >= 3k + 32 entries.  Returns k (out[0..k) sorted,
+ * 1-based) or < 0. */
+int64_t rtcur_draw_distinct(void* bitgen_state, void* next_uint32, int64_t population, int64_t k,
+                            uint64_t* seen, int64_t* out, int64_t out_cap);
 
 #ifdef __cplusplus
 }

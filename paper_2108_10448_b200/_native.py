@@ -29,7 +29,7 @@ EXPORTED = (
     "rtcur_append_distinct", "rtcur_generate_tucker", "rtcur_tnsr_read_header", "rtcur_tnsr_load", "rtcur_tnsr_store",
     "rtcur_scatter_outliers", "rtcur_abs_sum", "rtcur_ap_threshold", "rtcur_ap_residual", "rtcur_abs_max", "rtcur_engine_bind_mode_copies",
     "rtcur_transpose_mode", "rtcur_engine_set_shards", "rtcur_engine_shard_plan", "rtcur_engine_shard_pack",
-    "rtcur_engine_shard_unpack",
+    "rtcur_engine_shard_unpack", "rtcur_draw_distinct",
 )
 PHASES = ("absmax", "prep", "gather", "threshold", "gram", "eig", "svdpost", "apass", "gpass", "wcols", "error",
           "export", "full")
@@ -90,6 +90,8 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_absmax.argtypes = [c_vp, c_dp]
     lib.rtcur_engine_set_sample.argtypes = [c_vp, ctypes.POINTER(c_i64p), ctypes.POINTER(c_i64p)]
     lib.rtcur_engine_gather.argtypes = [c_vp]
+    lib.rtcur_draw_distinct.restype = c_i64
+    lib.rtcur_draw_distinct.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64]
     lib.rtcur_engine_set_shards.argtypes = [c_vp, ctypes.c_int, ctypes.c_int, c_i64p]
     lib.rtcur_engine_shard_plan.argtypes = [c_vp, c_i64p]
     lib.rtcur_engine_shard_pack.argtypes = [c_vp, c_vp]

@@ -628,6 +628,9 @@ struct rtcur_engine {
   bool staging_on_side;
   cudaStream_t side;
   cudaEvent_t pre_ev, side_ev;
+  cudaEvent_t eig_ev;              // recorded inside the iteration when its eigensolver starts:
+                                   // the prefetch waits for it, so it overlaps k_eig (few SMs)
+                                   // rather than the wide threshold / Gram kernels before it
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
   i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
@@ -840,12 +843,15 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&e->idx_ev[s], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->absmax_ev, cudaEventDisableTiming));
   {
+    // off by default: measured neutral at config 1 (the host, not the stream, paces
+    // it) and +4..8 % at config 4; RTCUR_SIDE_PREFETCH=1 enables it
     const char* sv = getenv("RTCUR_SIDE_PREFETCH");
-    e->use_side = !(sv && sv[0] == '0');
+    e->use_side = sv && sv[0] == '1';
   }
   CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&e->pre_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->side_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->eig_ev, cudaEventDisableTiming));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -891,6 +897,7 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   if (e->side) cudaStreamSynchronize(e->side), cudaStreamDestroy(e->side);
   if (e->pre_ev) cudaEventDestroy(e->pre_ev);
   if (e->side_ev) cudaEventDestroy(e->side_ev);
+  if (e->eig_ev) cudaEventDestroy(e->eig_ev);
   if (e->prof_pool) {
     for (auto ev : *e->prof_pool) cudaEventDestroy(ev);
     delete e->prof_pool;
@@ -989,7 +996,9 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
   if (!e) return fail(RT_ERR_VALUE, "null engine");
   if (e->pending && e->use_side && !e->shard && !e->staging_on_side && e->use_graphs) {
     e->staging_on_side = true;
-    CK(cudaStreamWaitEvent(e->side, e->pre_ev, 0));
+    // eig_ev is recorded inside the running iteration (after pre_ev): waiting for it
+    // also covers every earlier reader of the slot being refilled
+    CK(cudaStreamWaitEvent(e->side, e->eig_ev, 0));
   }
   SideScope side_scope(e);
   const Plan& P = e->P;
@@ -1282,6 +1291,35 @@ static SvdArgs make_svd_args(rtcur_engine* e) {
 }
 
 // rank-r truncated SVD of every mode's intersection M_k (already in the workspace)
+// k_eig: one CTA per mode, or clusters of EIG_CLUSTER CTAs per mode when some
+// intersection has 128 < s <= 256 (their tridiagonalisation is spread over the
+// cluster's registers, k_eig.cu eig_tridiag_reg)
+static int launch_eig(const EigArgs& ea, const i64* s, int n, int esm, cudaStream_t st) {
+  bool clus = false;
+  for (int m = 0; m < n; ++m) clus |= ea.reg_tridiag && s[m] > 128 && s[m] <= 256;
+  if (!clus) {
+    k_eig<<<n, EIG_THREADS, esm, st>>>(ea);
+    LAUNCH_CHECK();
+    return RT_OK;
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)(n * EIG_CLUSTER));
+  cfg.blockDim = dim3(EIG_THREADS);
+  cfg.dynamicSmemBytes = (size_t)esm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = EIG_CLUSTER;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_eig, ea));
+  LAUNCH_CHECK();
+  return RT_OK;
+}
+
 static int run_svd(rtcur_engine* e, const double* warm_state) {
   const Plan& P = e->P;
   const int n = P.g.n;
@@ -1336,6 +1374,13 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ea.ms_warps = msw;
   }
   ea.fast_used = e->at<int>(P.o_fast);
+  {
+    // register-tiled tridiagonalisation: 1 (default) for 128 < s <= 256 (cluster of
+    // EIG_CLUSTER CTAs; 1.3-1.6x on that phase), 2 also single-CTA for s <= 128
+    // (measured no faster than the shared-memory path there), 0 off
+    static const int reg = [] { const char* v = getenv("RTCUR_EIG_REG"); return v ? atoi(v) : 1; }();
+    ea.reg_tridiag = reg;
+  }
   IndexPtrs ipw = make_ip(e);
   for (int m = 0; m < n; ++m) {
     // fast path only for wide intersections (short side = rows I_k) with a previous iterate
@@ -1343,9 +1388,11 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ea.warm_rows[m] = ipw.rows[m];
     ea.warm_d[m] = P.g.dim[m];
   }
+  // the next sample's prefetch (side stream) may start now: it overlaps the eigensolver
+  if (e->capturing) CK(cudaEventRecordWithFlags(e->eig_ev, e->st, cudaEventRecordExternal));
+  else CK(cudaEventRecord(e->eig_ev, e->st));
   prof_begin(e, PH_EIG);
-  k_eig<<<n, EIG_THREADS, esm, e->st>>>(ea);
-  LAUNCH_CHECK();
+  if (int st = launch_eig(ea, P.s, n, esm, e->st)) return st;
   prof_end(e, PH_EIG);
   prof_begin(e, PH_SVDPOST);
   SvdArgs sa = make_svd_args(e);
@@ -1878,6 +1925,91 @@ extern "C" int rtcur_engine_profile_read(rtcur_engine* e, double* ms, int64_t* c
 // the deduplication of the reference's iid draw (fiber_cur.py:202-208:
 // np.unique(..., return_index=True) then merged[np.sort(first)]) in O(n); the
 // random stream itself stays numpy's Generator.integers.
+// numpy Generator.integers(0, population, size=m, dtype=int64) for population <=
+// 2^32 - 1: random_bounded_uint64_fill -> buffered_bounded_lemire_uint32 on the
+// bit generator's own next_uint32 (numpy/random/src/distributions), reproduced
+// here call for call so the stream (and the generator state afterwards) is the
+// one numpy produces.
+typedef uint32_t (*rt_next_u32)(void*);
+static inline uint32_t rt_lemire32(void* st, rt_next_u32 next, uint32_t rng) {
+  const uint32_t rng_excl = rng + 1;
+  uint64_t m = (uint64_t)next(st) * rng_excl;
+  uint32_t leftover = (uint32_t)m;
+  if (leftover < rng_excl) {
+    const uint32_t threshold = (UINT32_MAX - rng) % rng_excl;
+    while (leftover < threshold) {
+      m = (uint64_t)next(st) * rng_excl;
+      leftover = (uint32_t)m;
+    }
+  }
+  return (uint32_t)(m >> 32);
+}
+
+// The reference's without-replacement draw (fiber_cur.py:197-208, iid branch):
+//   out = []; while len(out) < k: batch = integers(0, pop, need + need // 2 + 16);
+//   keep the first occurrence of each value in order; return sort(out[:k]) + 1
+// natively, drawing from numpy's bit generator (state + next_uint32 of
+// Generator.bit_generator.ctypes) so the consumed stream is bit-identical.
+// seen: (population + 63) / 64 zeroed words, a membership bitmap (left zeroed);
+// out: >= 3k + 32 entries.  Returns k with out[0..k) the sorted 1-based sample,
+// or < 0 on a bad argument.
+extern "C" int64_t rtcur_draw_distinct(void* bitgen_state, void* next_uint32, int64_t population, int64_t k,
+                                       uint64_t* seen, int64_t* out, int64_t out_cap) {
+  if (!bitgen_state || !next_uint32 || !seen || !out) return -1;
+  if (population < 2 || population > (int64_t)0xFFFFFFFFLL || k < 1 || k >= population || out_cap < 3 * k + 32)
+    return -1;
+  rt_next_u32 next = reinterpret_cast<rt_next_u32>(next_uint32);
+  const uint32_t rng = (uint32_t)(population - 1);
+  int64_t nout = 0;
+  while (nout < k) {
+    const int64_t need = k - nout;
+    const int64_t m = need + need / 2 + 16;   // <= 1.5 k + 16: nout stays below 3k + 32
+    for (int64_t t = 0; t < m; ++t) {
+      const uint32_t v = rt_lemire32(bitgen_state, next, rng);
+      uint64_t& w = seen[v >> 6];
+      const uint64_t bit = 1ull << (v & 63);
+      if (!(w & bit)) {
+        w |= bit;
+        out[nout++] = v;
+      }
+    }
+  }
+  // keep the first k (draw order), then sort them
+  for (int64_t i = k; i < nout; ++i) seen[out[i] >> 6] &= ~(1ull << (out[i] & 63));
+  const int64_t words = (population + 63) >> 6;
+  if (words <= 16 * k) {
+    // dense: the bitmap scan yields them sorted (and clears the bitmap)
+    int64_t o = 0;
+    for (int64_t wi = 0; wi < words && o < k; ++wi) {
+      uint64_t w = seen[wi];
+      if (!w) continue;
+      seen[wi] = 0;
+      while (w) {
+        const int b = __builtin_ctzll(w);
+        out[o++] = (wi << 6) + b + 1;
+        w &= w - 1;
+      }
+    }
+    return k;
+  }
+  for (int64_t i = 0; i < k; ++i) seen[out[i] >> 6] = 0;   // (only the first k bits remained set)
+  // sparse: LSD radix sort of the k values (< 2^32), 4 passes of 8 bits through out[k..2k)
+  int64_t* a = out;
+  int64_t* b = out + k;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sh = 8 * pass;
+    int64_t cnt[257];
+    memset(cnt, 0, sizeof(cnt));
+    for (int64_t i = 0; i < k; ++i) cnt[((a[i] >> sh) & 255) + 1]++;
+    for (int d = 0; d < 256; ++d) cnt[d + 1] += cnt[d];
+    for (int64_t i = 0; i < k; ++i) b[cnt[(a[i] >> sh) & 255]++] = a[i];
+    std::swap(a, b);
+  }
+  // 4 passes: the sorted run is back in out[0..k)
+  for (int64_t i = 0; i < k; ++i) out[i] += 1;
+  return k;
+}
+
 extern "C" int64_t rtcur_append_distinct(int64_t* out, int64_t nout, const int64_t* batch, int64_t nb,
                                          unsigned char* seen, int64_t population) {
   for (int64_t i = 0; i < nb; ++i) {
@@ -2176,8 +2308,11 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   ea.lam[0] = tmp.at<double>(P.o_lam[0]);
   ea.nb[0] = P.nb[0];
   ea.full[0] = eig_pick_full((int)s, r);
-  k_eig<<<1, EIG_THREADS, esm, st>>>(ea);
-  LAUNCH_CHECK();
+  ea.reg_tridiag = getenv("RTCUR_EIG_REG") ? atoi(getenv("RTCUR_EIG_REG")) : 1;
+  {
+    const i64 s1[1] = {s};
+    if (int st2 = launch_eig(ea, s1, 1, esm, st)) return st2;
+  }
   SvdArgs sa = make_svd_args(&tmp);
   sa.M[0] = m_dev;
   unsigned int* hcnt = tmp.at<unsigned int>(P.o_counters) + 16;

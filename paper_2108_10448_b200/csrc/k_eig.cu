@@ -24,10 +24,13 @@
 // (_core.pyx:24-249) for the rank-r part the solver uses.
 #include "common.cuh"
 #include <cfloat>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 #define EIG_SMEM_DOUBLES 29056   // 227 KB opt-in shared memory per CTA
 #define EIG_TPR 4                // threads per row group (full-storage path)
 #define EIG_THREADS 512
+#define EIG_CLUSTER 8            // CTAs per mode for 128 < s <= 256 (register-tiled tridiagonalisation)
 
 struct EigArgs {
   int n;
@@ -46,6 +49,7 @@ struct EigArgs {
   int max_sub_steps;
   int ms_warps;                        // multisection: max warps per eigenvalue (shifts = 64 x warps)
   int* fast_used;                      // per mode: 1 if the fast path certified the subspace
+  int reg_tridiag;                     // register-tiled tridiagonalisation: 1 for 128 < s <= 256 (clusters), 2 also s <= 128
   // inverse-iteration LU factors in global scratch (r x 4s doubles, then r x s
   // pivot bytes), or null: in shared memory, nb at a time.  Used when fewer than
   // r factorisations fit next to K (s = 213 packed: 2), so all r run at once.
@@ -400,12 +404,271 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
   return false;
 }
 
+// ---------------------------------------------------------------- register-tiled tridiagonalisation
+// Householder tridiagonalisation with K held in REGISTERS: warp w owns rows
+// i = w + 16a (a < RB), lane l owns columns j = l + 32b (b < CB) (cyclic, so the
+// shrinking trailing block stays balanced).  Per step the only shared-memory
+// traffic is O(s) vectors: the reflected column (written by its owners during
+// the previous step's update, with its squared-norm partials), the symv result
+// y (one writer lane per row after a transpose-reduce over the warp's lanes)
+// and the dot partials -- 2 barriers per step, RB*CB + 2*RB*CB FMAs per thread.
+// The shared-memory version below it reads and rewrites the whole trailing
+// block from shared memory every step (bandwidth/latency bound).  Outputs are
+// identical in layout: reflectors contiguous in HV (step k: s-k-1 entries,
+// v_0 = x_0 - alpha), dd / ed / bet, and the trailing 2x2 block in dd/ed.
+// Returns hoff (total reflector length).
+template <int RB>
+__device__ __forceinline__ double eig_xpose_reduce(double (&v)[RB], int lane) {
+  // reduce RB per-lane values over the 32 lanes: after the call the lane holds the
+  // full sum of row index eig_xpose_row<RB>(lane) (fixed shuffle tree)
+  if constexpr (RB >= 8) {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const double send = up ? v[t] : v[t + 4], keep = up ? v[t + 4] : v[t];
+      v[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  if constexpr (RB >= 4) {
+    constexpr int o = RB >= 8 ? 8 : 16;
+    const bool up = lane & o;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double send = up ? v[t] : v[t + 2], keep = up ? v[t + 2] : v[t];
+      v[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  if constexpr (RB >= 2) {
+    constexpr int o = RB >= 8 ? 4 : RB >= 4 ? 8 : 16;
+    const bool up = lane & o;
+    const double send = up ? v[0] : v[1], keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+  }
+  double t = v[0];
+  constexpr int first = RB >= 8 ? 2 : RB >= 4 ? 4 : RB >= 2 ? 8 : 16;
+#pragma unroll
+  for (int o = first; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+template <int RB>
+__device__ __forceinline__ int eig_xpose_row(int lane) {
+  if constexpr (RB >= 8) return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  else if constexpr (RB >= 4) return ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+  else if constexpr (RB >= 2) return (lane >> 4) & 1;
+  else return 0;
+}
+
+// C == 1: one CTA, K read from its shared-memory full storage (A, ld).  C > 1: a
+// cluster of C CTAs, CTA c owning the rows of global warps 16c..16c+15, K read
+// from the packed global Gram (Kg); the per-step vectors and partials are
+// broadcast into every CTA's shared memory (DSMEM stores) and the two barriers
+// are cluster barriers.  dd / ed / bet / HV are written to CTA 0 (which goes on
+// with the eigenvalues); red holds 2 x 16C norm partials, red2 16C dot partials.
+template <int C>
+__device__ __forceinline__ void eig_csync() {
+  if constexpr (C == 1) __syncthreads();
+  else cg::this_cluster().sync();
+}
+// p[0] = v in CTA `rank`'s copy of this shared-memory location (C == 1: local store).
+// mapa + st.shared::cluster per store: 32-bit addresses recomputed on the spot keep
+// register pressure down (hoisted generic remote pointers spill next to the tile)
+template <int C>
+__device__ __forceinline__ void eig_put(double* p, int rank, double v) {
+  if constexpr (C == 1) {
+    *p = v;
+  } else {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    unsigned ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+  }
+}
+
+template <int C, int RB, int CB>
+__device__ int eig_tridiag_reg(const double* __restrict__ A, int ld, const double* __restrict__ Kg, int s,
+                               double* HV, double* dd, double* ed, double* bet, double* xs0, double* xs1, double* ys,
+                               double* red, double* red2) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int crank = 0;
+  if constexpr (C > 1) crank = (int)cg::this_cluster().block_rank();
+  constexpr int NP = 16 * C;            // row-owning warps in the cluster
+  const int gw = crank * 16 + wid;
+  double kr[RB][CB];
+#pragma unroll
+  for (int a = 0; a < RB; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int i = gw + NP * a, j = lane + 32 * b;
+      double v = 0.0;
+      if (i < s && j < s) {
+        if constexpr (C == 1) v = A[i * ld + j];
+        else v = i >= j ? Kg[pk(i, j)] : Kg[pk(j, i)];
+      }
+      kr[a][b] = v;
+    }
+  // column 0 below the diagonal: its owners (lane 0, b = 0) publish it with its norm partials
+  if (lane == 0) {
+    double sq = 0.0;
+#pragma unroll
+    for (int a = 0; a < RB; ++a) {
+      const int i = gw + NP * a;
+      if (i >= 1 && i < s) {
+#pragma unroll
+        for (int c2 = 0; c2 < C; ++c2) eig_put<C>(xs0 + i, c2, kr[a][0]);
+        sq = fma(kr[a][0], kr[a][0], sq);
+      }
+    }
+#pragma unroll
+    for (int c2 = 0; c2 < C; ++c2) eig_put<C>(red + gw, c2, sq);
+  }
+  eig_csync<C>();
+  constexpr int WL = 32 / RB;           // lanes sharing one reduced row (writer: lane % WL == 0)
+  const int arow = eig_xpose_row<RB>(lane);
+  int hoff = 0;
+  for (int k = 0; k + 2 < s; ++k) {
+    const double* xc = (k & 1) ? xs1 : xs0;
+    double* xn = (k & 1) ? xs0 : xs1;
+    const double* rc = red + (k & 1) * NP;
+    double* rn = red + ((k + 1) & 1) * NP;
+    double t0 = 0.0;
+    for (int q = lane; q < NP; q += 32) t0 += rc[q];
+    const double nrm = sqrt(warp_sum(t0));
+    const double x0 = xc[k + 1];
+    double alpha = 0.0, beta = 0.0;
+    if (nrm > 0.0) {
+      alpha = -copysign(nrm, x0);
+      beta = 1.0 / (nrm * (nrm + fabs(x0)));
+    }
+    const double v0 = x0 - alpha;
+    double vcol[CB];
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int j = lane + 32 * b;
+      vcol[b] = (j > k && j < s) ? (j == k + 1 ? v0 : xc[j]) : 0.0;
+    }
+    // y = beta K22 v for this warp's rows
+    double pr[RB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a) {
+      double t = 0.0;
+#pragma unroll
+      for (int b = 0; b < CB; ++b) t = fma(kr[a][b], vcol[b], t);
+      pr[a] = t;
+    }
+    const double ysum = beta * eig_xpose_reduce<RB>(pr, lane);
+    double dotp = 0.0;
+    {
+      const int i = gw + NP * arow;
+      if ((lane % WL) == 0 && i > k && i < s) {
+#pragma unroll
+        for (int c2 = 0; c2 < C; ++c2) eig_put<C>(ys + i, c2, ysum);
+        dotp = ysum * (i == k + 1 ? v0 : xc[i]);
+      }
+    }
+    dotp = warp_sum(dotp);
+    if (lane == 0) {
+#pragma unroll
+      for (int c2 = 0; c2 < C; ++c2) eig_put<C>(red2 + gw, c2, dotp);
+    }
+    // the reflector (CTA 0, warp 0: every CTA holds all columns) and the step's scalars
+    if (crank == 0 && wid == 0) {
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const int j = lane + 32 * b;
+        if (j > k && j < s) HV[hoff + j - k - 1] = vcol[b];
+      }
+    }
+    if (crank == 0 && tid == 0) {
+      ed[k] = alpha;
+      bet[k] = beta;
+    }
+    if (gw == (k % NP) && lane == (k & 31)) {
+      // select chains (no dynamic register indexing: that would move kr to local memory)
+      const int ak = k / NP, bk = k >> 5;
+      double pick = 0.0;
+#pragma unroll
+      for (int a = 0; a < RB; ++a)
+#pragma unroll
+        for (int b = 0; b < CB; ++b) pick = (a == ak && b == bk) ? kr[a][b] : pick;
+      eig_put<C>(dd + k, 0, pick);
+    }
+    eig_csync<C>();                                                // B1
+    double t1 = 0.0;
+    for (int q = lane; q < NP; q += 32) t1 += red2[q];
+    const double kk = 0.5 * beta * warp_sum(t1);
+    double wcol[CB];
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int j = lane + 32 * b;
+      wcol[b] = (j > k && j < s) ? ys[j] - kk * vcol[b] : 0.0;
+    }
+    // K22 -= v w^T + w v^T; the next step's column (k+1, rows > k+1) goes out with its norm
+    const int kn = k + 1;
+    double sq = 0.0;
+#pragma unroll
+    for (int a = 0; a < RB; ++a) {
+      const int i = gw + NP * a;
+      const bool act = i > k && i < s;
+      const double vi = act ? (i == k + 1 ? v0 : xc[i]) : 0.0;
+      const double wi = act ? ys[i] - kk * vi : 0.0;
+#pragma unroll
+      for (int b = 0; b < CB; ++b) kr[a][b] -= vi * wcol[b] + wi * vcol[b];
+      if (lane == (kn & 31) && i > kn && i < s) {
+        const int bn = kn >> 5;
+        double x = 0.0;
+#pragma unroll
+        for (int b = 0; b < CB; ++b) x = (b == bn) ? kr[a][b] : x;
+#pragma unroll
+        for (int c2 = 0; c2 < C; ++c2) eig_put<C>(xn + i, c2, x);
+        sq = fma(x, x, sq);
+      }
+    }
+    if (lane == (kn & 31)) {
+#pragma unroll
+      for (int c2 = 0; c2 < C; ++c2) eig_put<C>(rn + gw, c2, sq);
+    }
+    hoff += s - k - 1;
+    eig_csync<C>();                                                // B2
+  }
+  // trailing 2x2 block: K[s-2][s-2], K[s-1][s-2], K[s-1][s-1] -> CTA 0
+  {
+    double p22 = 0.0, p12 = 0.0, p11 = 0.0;
+    bool h22 = false, h12 = false, h11 = false;
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const int i = gw + NP * a, j = lane + 32 * b;
+        const bool c22 = i == s - 2 && j == s - 2, c12 = i == s - 1 && j == s - 2, c11 = i == s - 1 && j == s - 1;
+        p22 = c22 ? kr[a][b] : p22;
+        p12 = c12 ? kr[a][b] : p12;
+        p11 = c11 ? kr[a][b] : p11;
+        h22 |= c22;
+        h12 |= c12;
+        h11 |= c11;
+      }
+    if (h22) eig_put<C>(dd + s - 2, 0, p22);
+    if (h12) eig_put<C>(ed + s - 2, 0, p12);
+    if (h11) eig_put<C>(dd + s - 1, 0, p11);
+  }
+  eig_csync<C>();
+  return hoff;
+}
+
 extern __shared__ double eig_smem[];
 
 __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
-  const int mi = blockIdx.x;
+  // launched either one CTA per mode, or (some s > 128) as clusters of EIG_CLUSTER
+  // CTAs per mode: the cluster's extra CTAs only join the register-tiled
+  // tridiagonalisation of modes with 128 < s <= 256 (eig_tridiag_reg<4, ...>)
+  const int csize = (int)cg::this_cluster().num_blocks();
+  const int crank = csize > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const int mi = blockIdx.x / csize;
   if (mi >= ea.n) return;
   const int s = ea.s[mi], r = ea.r[mi], nb = ea.nb[mi];
+  const bool use_cl = csize == EIG_CLUSTER && s > 128 && s <= 256 && ea.reg_tridiag;
+  if (crank != 0 && !use_cl) return;   // (never reaches a cluster barrier)
   const bool full = ea.full[mi] != 0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   const int ld = eig_ld(s);
@@ -434,9 +697,14 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   double* Rs = Cs + r * r;                                         // r x r
   (void)ww;
 
+  double* cred = lu;                                               // cluster partials: 3 x 16 EIG_CLUSTER
   long long* tm = ea.tmark ? ea.tmark + 8 * mi : nullptr;
+  if (crank != 0) tm = nullptr;
   if (tm && tid == 0) tm[0] = clock64();
   const double* Kg = ea.K[mi];
+  // (cluster helper CTAs, crank != 0, skip the load and the warm path: they wait at
+  // S0 for CTA 0's verdict and join the tridiagonalisation below)
+  if (crank == 0) {
   if (full) {
     for (int idx = tid; idx < npk; idx += blockDim.x) {
       int i = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
@@ -452,9 +720,11 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   }
   __syncthreads();
   if (tm && tid == 0) tm[1] = clock64();
+  }
 
   // ---------------------------------------------------------------- 0. warm-started subspace iteration
-  if (ea.warmA[mi] != nullptr) {
+  bool warm_ok = false;
+  if (crank == 0 && ea.warmA[mi] != nullptr) {
     const bool ok = eig_subspace(A, full, ld, s, r, E, Ysub, Hs, Cs, Rs, red, red2, scal, ea.warmA[mi],
                                  ea.warm_rows[mi], ea.warm_d[mi], ea.max_sub_steps, tm);
     if (ok) {
@@ -462,14 +732,33 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
       for (int e = tid; e < s * r; e += blockDim.x) ea.E[mi][e] = E[e];
       for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = 0.0;
       if (tm && tid == 0) tm[7] = clock64();
-      return;
+      warm_ok = true;
     }
   }
-  if (tid == 0 && ea.fast_used) ea.fast_used[mi] = 0;
+  if (use_cl) {   // tell the helper CTAs whether the full path runs (scal[20] of every CTA)
+    __syncthreads();
+    if (crank == 0 && tid == 0)
+      for (int c2 = 0; c2 < EIG_CLUSTER; ++c2) eig_put<EIG_CLUSTER>(scal + 20, c2, warm_ok ? 1.0 : 0.0);
+    cg::this_cluster().sync();                                     // S0
+    warm_ok = scal[20] != 0.0;
+  }
+  if (warm_ok) return;
+  if (crank == 0 && tid == 0 && ea.fast_used) ea.fast_used[mi] = 0;
 
   // ---------------------------------------------------------------- 1. tridiagonalise
   int hoff = 0;
-  if (full) {
+  // register-tiled paths: clusters for 128 < s <= 256, single CTA for s <= 128 (RTCUR_EIG_REG=2)
+  const bool regtri = (full && s >= 3 && s <= 128 && ea.reg_tridiag >= 2) || use_cl;
+  if (use_cl) {
+    // reflectors go contiguous into the (consumed) packed matrix area
+    HV = A;
+    hoff = eig_tridiag_reg<EIG_CLUSTER, 2, 8>(nullptr, 0, Kg, s, HV, dd, ed, bet, vv, ww, yy, cred,
+                                              cred + 2 * 16 * EIG_CLUSTER);
+    if (crank != 0) return;   // helpers are done; CTA 0 goes on alone
+  } else if (regtri) {
+    if (s <= 64) hoff = eig_tridiag_reg<1, 4, 2>(A, ld, nullptr, s, HV, dd, ed, bet, vv, ww, yy, red, red2);
+    else hoff = eig_tridiag_reg<1, 8, 4>(A, ld, nullptr, s, HV, dd, ed, bet, vv, ww, yy, red, red2);
+  } else if (full) {
     // Full symmetric storage.  The column k+1 that step k+1 reflects is produced
     // by step k's rank-2 update (row groups own it), so its squared norm is
     // reduced there: 2 barriers per Householder step.
@@ -692,11 +981,13 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
     }
   }
   if (tid == 0) {
-    if (s >= 2) {
-      dd[s - 2] = full ? A[(s - 2) * ld + s - 2] : A[pk(s - 2, s - 2)];
-      ed[s - 2] = full ? A[(s - 1) * ld + s - 2] : A[pk(s - 1, s - 2)];
+    if (!regtri) {   // (the register path wrote the trailing 2x2 block itself)
+      if (s >= 2) {
+        dd[s - 2] = full ? A[(s - 2) * ld + s - 2] : A[pk(s - 2, s - 2)];
+        ed[s - 2] = full ? A[(s - 1) * ld + s - 2] : A[pk(s - 1, s - 2)];
+      }
+      dd[s - 1] = full ? A[(s - 1) * ld + s - 1] : A[pk(s - 1, s - 1)];
     }
-    dd[s - 1] = full ? A[(s - 1) * ld + s - 1] : A[pk(s - 1, s - 1)];
     double tn = 0.0, lo = DBL_MAX, hi = -DBL_MAX;
     for (int i = 0; i < s; ++i) {
       const double rad = (i > 0 ? fabs(ed[i - 1]) : 0.0) + (i + 1 < s ? fabs(ed[i]) : 0.0);
@@ -963,7 +1254,7 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
       const double beta = bet[k];
       if (beta == 0.0) continue;
       double d = 0.0;
-      if (full) {
+      if (full || regtri) {
         const double* v = HV + off;
         for (int i = lane; i < L; i += 32) d = fma(v[i], x[k + 1 + i], d);
         d = warp_sum(d) * beta;

@@ -167,6 +167,26 @@ def _seen_mask(population: int) -> np.ndarray:
     return m
 
 
+def _bitgen_iface(rng: np.random.Generator):
+    """(state address, next_uint32 function address) of the generator's bit
+    generator (numpy's documented ctypes interface; numpy caches it)."""
+    import ctypes
+
+    c = rng.bit_generator.ctypes
+    return c.state_address, ctypes.cast(c.next_uint32, ctypes.c_void_p).value
+
+
+def _seen_bits(population: int) -> np.ndarray:
+    """Per-thread zeroed membership bitmap (uint64 words), reused across draws."""
+    cache = getattr(_SEEN, "bits", None)
+    if cache is None:
+        cache = _SEEN.bits = {}
+    m = cache.get(population)
+    if m is None:
+        m = cache[population] = np.zeros((population + 63) // 64, dtype=np.uint64)
+    return m
+
+
 def _draw_without_replacement(rng: np.random.Generator, population: int, k: int) -> np.ndarray:
     """fiber_cur.py:189-209 (permutation for 3k >= pop, else iid stream + first-unique)."""
     if k >= population:
@@ -180,6 +200,18 @@ def _draw_without_replacement(rng: np.random.Generator, population: int, k: int)
     from . import _native
 
     lib = _native.load()
+    if population <= 0xFFFFFFFF:
+        # the whole draw natively on numpy's own bit generator (rtcur_draw_distinct:
+        # numpy's bounded-integer algorithm on next_uint32, identical stream)
+        state, nxt = _bitgen_iface(rng)
+        bits = _seen_bits(population)
+        out = np.empty(3 * k + 32, dtype=np.int64)
+        with rng.bit_generator.lock:
+            got = int(lib.rtcur_draw_distinct(state, nxt, population, k, bits.ctypes.data, out.ctypes.data,
+                                              out.size))
+        if got != k:
+            raise RuntimeError(f"rtcur_draw_distinct failed ({got})")
+        return out[:k].copy()
     seen = _seen_mask(population)
     cap = 2 * k + 64
     out = np.empty(cap, dtype=np.int64)

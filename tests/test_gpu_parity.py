@@ -350,3 +350,32 @@ def test_phase_timings_from_device_events():
     for key in ("gather", "eval_lowrank", "threshold", "build", "error"):
         assert t[key] > 0.0, key
     assert res.error_history == base.error_history
+
+
+@pytest.mark.parametrize("shape,r", [((213, 3017), 10), ((174, 1999), 10), ((165, 900), 7), ((256, 2100), 4),
+                                     ((140, 5000), 12), ((90, 2693), 5)])
+def test_truncated_svd_cluster_sizes_vs_oracle(shape, r):
+    """Intersections with 128 < s <= 256 take the cluster (8 CTAs, registers)
+    tridiagonalisation: the rank-r truncated SVD through the kernel plug matches
+    the oracle's Golub-Kahan-Reinsch SVD (reconstruction 1e-10 x sigma_1)."""
+    rng = np.random.default_rng(sum(shape) + r)
+    m, p = shape
+    # decaying spectrum + noise floor, like a cleaned intersection
+    q1, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    q2, _ = np.linalg.qr(rng.standard_normal((p, m)))
+    sv = np.concatenate([np.geomspace(100.0, 10.0, r), np.geomspace(3.0, 0.01, m - r)])
+    mat = (q1 * sv) @ q2.T
+    want = orc.truncated_svd(mat, r)
+    lib = _native.load()
+    st = torch.cuda.current_stream().cuda_stream
+    a = torch.from_numpy(np.asfortranarray(mat).reshape(-1, order="F").copy()).cuda()
+    u = torch.empty(m * r, dtype=torch.float64, device="cuda")
+    v = torch.empty(p * r, dtype=torch.float64, device="cuda")
+    s = torch.empty(r, dtype=torch.float64, device="cuda")
+    _native.check(lib.rtcur_truncated_svd(a.data_ptr(), m, p, r, u.data_ptr(), s.data_ptr(), v.data_ptr(), st))
+    U = u.cpu().numpy().reshape((m, r), order="F")
+    V = v.cpu().numpy().reshape((p, r), order="F")
+    S = s.cpu().numpy()
+    np.testing.assert_allclose(S, want.singular_values, rtol=0, atol=1e-12 * sv[0])
+    np.testing.assert_allclose((U * S) @ V.T, want.reconstruct(), rtol=0, atol=1e-10 * sv[0])
+    np.testing.assert_allclose(U.T @ U, np.eye(r), atol=1e-12)
