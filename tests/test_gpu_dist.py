@@ -92,6 +92,7 @@ def test_sharded_solve_single_rank_matches_plain():
         assert np.array_equal(a.sparse.core, b.sparse.core)
         _, _, rel = full_output_sharded(b)
         assert rel < 1e-3
+    dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
