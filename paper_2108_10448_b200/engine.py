@@ -260,40 +260,28 @@ class Engine:
         nat.check(self.lib.rtcur_engine_export_blocks(self.handle, *ptr))
         return outs
 
-    def to_host(self, dev_tensors, chunk_bytes: int = 8 << 20):
-        """Copy fp64 device vectors into fresh host numpy arrays: D2H in chunks
-        through two pinned staging buffers kept by the engine (full PCIe rate),
-        each chunk's multi-threaded host copy into memory the caller owns
-        overlapping the next chunk's D2H."""
+    def to_host(self, dev_tensors):
+        """Copy fp64 device vectors into fresh host numpy arrays: D2H through a
+        pinned staging buffer kept by the engine (full PCIe rate), then a
+        multi-threaded host copy into memory the caller owns."""
         import torch
 
-        outs = [np.empty(int(t.numel()), dtype=np.float64) for t in dev_tensors]
-        per = max(1, chunk_bytes // 8)
-        st = getattr(self, "_pin_stage2", None)
-        if st is None:
-            st = self._pin_stage2 = (torch.empty(per, dtype=torch.float64, pin_memory=True),
-                                     torch.empty(per, dtype=torch.float64, pin_memory=True))
-            self._pin_ev = (torch.cuda.Event(), torch.cuda.Event())
-        stream = torch.cuda.current_stream(self.device)
-        jobs = []   # (tensor index, start, length)
-        for ti, t in enumerate(dev_tensors):
-            n = int(t.numel())
-            for a in range(0, n, per):
-                jobs.append((ti, a, min(per, n - a)))
-        pending = None
-        for ji, (ti, a, ln) in enumerate(jobs):
-            slot = ji & 1
-            st[slot][:ln].copy_(dev_tensors[ti].reshape(-1)[a:a + ln], non_blocking=True)
-            self._pin_ev[slot].record(stream)
-            if pending is not None:   # host copy of the previous chunk while this one transfers
-                pti, pa, pln, pslot = pending
-                self._pin_ev[pslot].synchronize()
-                _parallel_copy(outs[pti][pa:pa + pln], st[pslot].numpy()[:pln])
-            pending = (ti, a, ln, slot)
-        if pending is not None:
-            pti, pa, pln, pslot = pending
-            self._pin_ev[pslot].synchronize()
-            _parallel_copy(outs[pti][pa:pa + pln], st[pslot].numpy()[:pln])
+        total = sum(int(t.numel()) for t in dev_tensors)
+        st = getattr(self, "_pin_stage", None)
+        if st is None or st.numel() < total:
+            st = self._pin_stage = torch.empty(total, dtype=torch.float64, pin_memory=True)
+        o = 0
+        for t in dev_tensors:
+            st[o:o + t.numel()].copy_(t, non_blocking=True)
+            o += t.numel()
+        torch.cuda.current_stream(self.device).synchronize()
+        stage = st.numpy()
+        outs, o = [], 0
+        for t in dev_tensors:
+            a = np.empty(int(t.numel()), dtype=np.float64)
+            _parallel_copy(a, stage[o:o + a.size])
+            outs.append(a)
+            o += a.size
         return outs
 
     def export_cur(self):

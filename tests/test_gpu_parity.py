@@ -352,7 +352,7 @@ def test_phase_timings_from_device_events():
     assert res.error_history == base.error_history
 
 
-@pytest.mark.parametrize("shape,r", [((213, 3017), 10), ((174, 1999), 10), ((165, 900), 7), ((235, 2100), 4),
+@pytest.mark.parametrize("shape,r", [((213, 3017), 10), ((174, 1999), 10), ((165, 900), 7), ((220, 2100), 4),
                                      ((140, 5000), 12), ((90, 2693), 5)])
 def test_truncated_svd_cluster_sizes_vs_oracle(shape, r):
     """Intersections with 128 < s <= 256 take the cluster (8 CTAs, registers)
