@@ -30,6 +30,7 @@
 #include "k_factors.cu"
 #include "k_full.cu"
 #include "fiber_types.cuh"
+#include "core_types.cuh"
 #include "../../include/rtcur_b200.h"
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -110,6 +111,8 @@ struct Plan {
   TileMap tm_thr;  // threshold pass on k_block_pass: only fiber blocks (the core yields nothing there)
   unsigned fiber_mask;   // blocks handled by the TMA fiber pass (k_fiber.cuh)
   unsigned fb_thr, fb_ap, fb_err;   // per pass (RTCUR_FB_PASSES bits 1/2/4 switch passes off for A/B runs)
+  bool core_k;                      // the core's G pass and error pass on k_core_pass (short columns)
+  i64 o_cpart;                      // its per-CTA error partials
   TileMap tm_ap;   // A pass on k_block_pass: the fiber blocks the fiber pass does not take
   i64 xi_off[RT_MAX_MODES], xi_ld[RT_MAX_MODES];   // intersection copies (elements) inside o_xi
   i64 o_xi;
@@ -337,6 +340,12 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     P.fb_thr = (bits & 1) ? P.fiber_mask & ~1u : 0u;
     P.fb_ap = (bits & 2) ? P.fiber_mask & ~1u : 0u;
     P.fb_err = (bits & 4) ? P.fiber_mask : 0u;
+    // short core columns: the core's G pass and error share on k_core_pass -- opt-in
+    // (RTCUR_CORE_PASS=1): measured +2 % at config 4, -3 % at config 0 against the
+    // block pass / fiber pass, so the default keeps those
+    const char* cpv = getenv("RTCUR_CORE_PASS");
+    P.core_k = (cpv && cpv[0] == '1') && core_pass_fits((int)g.blk[0].P, g.rank[0], dtype) && g.blk[0].Q >= 64;
+    if (P.core_k) P.fb_err &= ~1u;
   }
   {
     TileMap& tc = P.tm_core;
@@ -345,7 +354,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     for (int b = 0; b < g.nblk; ++b) {
       const i64 nt = P.tm.first[b + 1] - P.tm.first[b];
       tc.first[b] = t;
-      if (!(P.fb_err >> b & 1)) t += nt;
+      if (!(P.fb_err >> b & 1) && !(b == 0 && P.core_k)) t += nt;
     }
     tc.first[g.nblk] = t;
     TileMap& ta = P.tm_ap;
@@ -546,6 +555,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_wt0 = take(P.w_tmp * 8);
   P.o_wt1 = take(P.w_tmp * 8);
   P.o_bpart = take((i64)BP_GRID * g.nblk * 2 * 8 + 64);
+  P.o_cpart = take(2 * 148 * 8 * 8 + 64);
   {
     // fiber-pass A pass: one d_k x r_k slot per (fiber block, CTA touching it) -- at most 296 + n slots
     i64 mx = 1;
@@ -1184,6 +1194,26 @@ static int refresh_xi(rtcur_engine* e, int slot) {
   return RT_OK;
 }
 
+static CoreLaunch make_cl(rtcur_engine* e, const double* st_s, double zeta, const double* zetap) {
+  const Plan& P = e->P;
+  const Geom& g = P.g;
+  CoreLaunch cl;
+  memset(&cl, 0, sizeof(cl));
+  cl.x = e->xb(e->act_slot()) + g.blk[0].off * P.esize;
+  cl.dtype = P.dtype;
+  cl.P = (int)g.blk[0].P;
+  cl.Q = g.blk[0].Q;
+  cl.r = g.rank[0];
+  cl.rows0 = make_ip(e).rows[0];
+  cl.dA = g.dim[0];
+  cl.a_off = g.a_off[0];
+  cl.w_off = g.blk[0].w_off;
+  cl.st_s = st_s;
+  cl.zeta = zeta;
+  cl.zetap = zetap;
+  return cl;
+}
+
 static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_e, double zeta, bool with_M,
                           double* s_out, double* c_out, double* l_out, bool sums, int phase) {
   const Plan& P = e->P;
@@ -1211,7 +1241,7 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   const i64 smb = bp_smem_bytes(P.bp);
   const bool hs = st_s != nullptr, he = st_e != nullptr;
   // the fiber blocks of the threshold / error passes go to the TMA fiber pass; exports stay here
-  const bool split = !(s_out || c_out || l_out) && ((with_M && !sums && P.fb_thr) || (sums && P.fb_err));
+  const bool split = !(s_out || c_out || l_out) && ((with_M && !sums && P.fb_thr) || (sums && (P.fb_err || P.core_k)));
   const bool thr_only = with_M && !sums && !(s_out || c_out || l_out);
   const TileMap& tmk = thr_only ? P.tm_thr : split ? P.tm_core : P.tm;
 #define BP_LAUNCH(HS, HE, WM, EXP)                                                                        \
@@ -1240,7 +1270,19 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   }
 #undef BP_LAUNCH
   if (lst) return lst;
-  if (split) {
+  if (split && sums && P.core_k) {
+    // the core's share of the error pass (sums of block 0)
+    CoreLaunch cl = make_cl(e, st_s, zeta, a.zetap);
+    cl.mode = 1;
+    cl.st_e = st_e;
+    cl.partial = e->at<double>(P.o_cpart);
+    cl.sums = a.sums;
+    cl.counter = e->at<unsigned int>(P.o_counters) + 48;
+    const int cst = core_pass_launch(cl, e->st);
+    if (cst < 0) return fail(RT_ERR_CUDA, std::string("k_core_pass (error): ") + cudaGetErrorString((cudaError_t)(-cst)));
+    rtcur_launch_counter_add(1);
+  }
+  if (split && (sums ? P.fb_err : P.fb_thr)) {
     FiberLaunch fl = make_fl(e, e->act_slot());
     fl.mask = sums ? P.fb_err : P.fb_thr;
     fl.st_s = st_s;
@@ -1606,7 +1648,15 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     pa.nonfinite = e->at<int>(P.o_nonfinite);
     const BPGeom& G = P.bp_gp;
     const i64 smb = bp_smem_bytes(G);
-    if (P.tm_gp.cols[0]) {
+    if (P.core_k) {
+      CoreLaunch cl = make_cl(e, st_s, zeta, e->zetap_cur);
+      cl.mode = 0;
+      cl.U = gp.U[0];
+      cl.t1 = gp.t1;
+      const int cst = core_pass_launch(cl, e->st);
+      if (cst < 0) return fail(RT_ERR_CUDA, std::string("k_core_pass (G): ") + cudaGetErrorString((cudaError_t)(-cst)));
+      rtcur_launch_counter_add(1);
+    } else if (P.tm_gp.cols[0]) {
       int lst;
 #define GP_LAUNCH(RB)                                                                                      \
   (st_s ? launch_bp(k_block_pass<true, false, false, false, true, RB, false>, P.tm_gp.first[1], smb, e->st, g, P.tm_gp, \

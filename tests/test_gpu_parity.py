@@ -223,8 +223,10 @@ for case in ("bern_R", "d20_F", "n4_R"):
 
 
 @pytest.mark.parametrize("env", [{"RTCUR_FIBER_PASS": "0"}, {"RTCUR_FIBER_CORE": "0"}, {"RTCUR_EARLY_ZETA": "0"},
-                                 {"RTCUR_K3_GENERIC": "1"}],
-                         ids=["block-pass-only", "core-on-block-pass", "late-zeta0", "generic-k3"])
+                                 {"RTCUR_K3_GENERIC": "1"}, {"RTCUR_CORE_PASS": "1"}, {"RTCUR_EIG_REG": "0"},
+                                 {"RTCUR_EIG_REG": "2"}, {"RTCUR_SIDE_PREFETCH": "1"}],
+                         ids=["block-pass-only", "core-on-block-pass", "late-zeta0", "generic-k3", "core-pass",
+                              "eig-smem-tridiag", "eig-reg-tridiag", "side-prefetch"])
 def test_engine_variants_agree(env):
     """The device-path variants (TMA fiber pass vs the block pass for every block,
     the core on either, zeta_0 scanned before or after the first draw, TMA vs
