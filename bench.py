@@ -423,12 +423,21 @@ def run_b200(args):
 
     world, rank, local = _dist()
     group = None
+    # NCCL over NVLink; RTCUR_BENCH_BACKEND=gloo exercises the N > 1 code path with
+    # all ranks on however many devices exist (validation on a one-GPU box)
+    backend = os.environ.get("RTCUR_BENCH_BACKEND", "nccl")
+    device = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(device)
+    local = device
+    red_dev = "cuda" if backend == "nccl" else "cpu"
     from paper_2108_10448_b200 import DeviceTensor, SolverConfig, rtcur
     from paper_2108_10448_b200 import _native
     from paper_2108_10448_b200 import solver as solver_mod
@@ -517,8 +526,8 @@ def run_b200(args):
     clk = clocks.stop()
     solver_mod.PROFILE, solver_mod.PROFILE_PHASES = False, None
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    it = torch.tensor([iters], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
+    it = torch.tensor([iters], dtype=torch.float64, device=red_dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         if not shard:   # replicas: every rank's iterations count; sharded: one solve spans all ranks
@@ -565,8 +574,8 @@ def run_b200(args):
                + sum(f.nbytes for f in facs) + 8 * res.iterations)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    ie = torch.tensor([e2e_iters], dtype=torch.float64, device="cuda")
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
+    ie = torch.tensor([e2e_iters], dtype=torch.float64, device=red_dev)
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         if not shard:

@@ -1410,7 +1410,9 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     esm = std::max(esm, eig_smem_bytes(P, m));
   }
   ea.tmark = e->at<long long>(P.o_dbg);
-  ea.max_sub_steps = 24;
+  // certified attempts take <= 15 steps at configs 0-4 (tools/eig_paths.py); a
+  // failing one is capped near the full path's cost
+  ea.max_sub_steps = 16;
   {
     static const int msw = [] { const char* v = getenv("RTCUR_EIG_MS_WARPS"); return v ? std::max(1, atoi(v)) : 1; }();
     ea.ms_warps = msw;

@@ -391,13 +391,7 @@ __device__ bool eig_subspace(const double* A, bool full, int ld, int s, int r, d
       double hmin = H[0];
       for (int c = 1; c < r; ++c) hmin = fmin(hmin, H[c + c * r]);
       if (hmin < 0.95 * ub) return false;
-      // the residual cannot fall much below ~1e-16 tr K (rounding), so certification
-      // needs lambda_min(H) - ub > ~1e12 * 1e-16 tr K: when even min_i H_ii (an upper
-      // bound of lambda_min(H)) misses that margin, no later step can certify
-      if (hmin - ub <= 1e-4 * trK) return false;
     }
-    // converged to rounding level without certifying: further steps cannot help
-    if (res <= 1e-14 * trK) return false;
     if (step + 1 == max_steps) break;
     TMK(5)
     // X <- orth(Y)

@@ -194,6 +194,8 @@ def make_gaussian_tucker_device(shape, ranks, alpha, c, seed, dtype=None, slab=N
         if group is not None:
             import torch.distributed as dist
 
+            if dist.get_backend(group) != "nccl":   # gloo groups reduce host tensors
+                tot = tot.cpu()
             dist.all_reduce(tot, group=group)
         mu = float(tot.item()) / float(np.prod(shape, dtype=np.float64))
     X = torch.empty((hi - lo) * ncols, dtype=dtype, device=dev)
