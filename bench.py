@@ -386,6 +386,10 @@ def _per_config(configs, local: int, peak: float, steps: int = 3):
                 us = 1e3 * dm[ph] / dn[ph]
                 fr[ph] = {"frac": b / (us * 1e-6) / 1e9 / peak, "launch_us": us, "alg_bytes_per_launch": b,
                           "share": dm[ph] / total_dev}
+                tr = _ncu_traffic(c, ph)
+                if tr:
+                    fr[ph]["traffic"] = tr["bytes_per_launch"]
+                    fr[ph]["traffic_frac"] = tr["bytes_per_launch"] / (us * 1e-6) / 1e9 / peak
         shares = {k: round(v / total_dev, 4) for k, v in sorted(dm.items(), key=lambda kv: -kv[1]) if dn.get(k)}
         phases = {"absmax": {"ms_per_step": dm["absmax"], "launches_per_step": dn["absmax"]}} if dn.get("absmax") \
             else {}
@@ -595,6 +599,9 @@ def run_b200(args):
             "alg_bytes_per_launch": alg[dom], "launch_us": 1e3 * per_launch_ms, "launches_timed": dom_n,
             "peak_source": peak_src,
             "share_of_device_time": phases[dom]["share"] if dom in phases else None}
+    if roof["traffic"]:   # the DRAM bytes ncu counted for this phase, over the same launch time
+        roof["traffic_achieved"] = roof["traffic"] / (per_launch_ms / 1e3) / 1e9
+        roof["traffic_frac"] = roof["traffic_achieved"] / peak
     fmas = _fp64_fmas(bc, rows, cols)
     if dom in fmas:   # the same launch against the fp64 pipe (the fiber passes sit near the ridge)
         tf = fmas[dom] / (per_launch_ms / 1e3) / 1e12

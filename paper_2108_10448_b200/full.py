@@ -34,7 +34,8 @@ def full_output(res, x=None, want_L: bool = True, want_S: bool = True):
         dev = x if isinstance(x, DeviceTensor) else DeviceTensor.from_host(x)
         eng.bind(dev.flat)
     L, S, e2, x2 = eng.full_output(res.zeta_final, want_L=want_L, want_S=want_S)
-    shape = eng.shape
+    lo, hi = eng.slab   # a sharded engine reconstructs its mode-1 slab (residual of the slab only;
+    shape = (hi - lo,) + tuple(eng.shape[1:])   # dist.full_output_sharded all-reduces the global one)
     rel = float(np.sqrt(e2) / np.sqrt(x2)) if x2 > 0 else (0.0 if e2 == 0 else float("inf"))
     return (DeviceTensor(L, shape) if L is not None else None,
             DeviceTensor(S, shape) if S is not None else None, rel)
