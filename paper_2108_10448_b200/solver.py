@@ -494,6 +494,64 @@ def _mode_copy_plan(shape, col_sizes, cfg, src):
     return tuple(keep)
 
 
+class _AheadSampler:
+    """RTCUR-R index draws on a background thread, in stream order.
+
+    The solve consumes the generator only through these draws (solver.py:293-317:
+    the first sample, then one per iteration), so a thread that keeps drawing the
+    next samples into a short queue hands the loop exactly the sets the
+    reference draws, in the same order.  The draw itself runs in native code
+    without the GIL (rtcur_draw_distinct), so it overlaps the loop's own host
+    work (staging, launches, the stop check) instead of adding to it: at config 1
+    the host loop was ~60 % draw and paced the device.  Draws past the last
+    iteration are discarded (the generator is local to the solve)."""
+
+    def __init__(self, shape, row_sizes, col_sizes, rng, depth: int = 3):
+        import queue
+        import threading
+
+        self._args = (shape, row_sizes, col_sizes, rng)
+        self._q = queue.Queue(maxsize=depth)
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, name="rtcur-sampler", daemon=True)
+        self._t.start()
+
+    def _run(self):
+        import queue
+
+        shape, row_sizes, col_sizes, rng = self._args
+        while not self._stop.is_set():
+            try:
+                item = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+            except BaseException as exc:   # surfaced by next()
+                item = exc
+            while not self._stop.is_set():
+                try:
+                    self._q.put(item, timeout=0.05)
+                    break
+                except queue.Full:
+                    continue
+            if isinstance(item, BaseException):
+                return
+
+    def next(self):
+        item = self._q.get()
+        if isinstance(item, BaseException):
+            raise item
+        return item
+
+    def close(self):
+        import queue
+
+        self._stop.set()
+        try:
+            while True:
+                self._q.get_nowait()
+        except queue.Empty:
+            pass
+        self._t.join()
+
+
 def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_iteration=None) -> SolveResult:
     """The solve loop.  ``on_iteration(k, eng, idx, zeta, err, flags)`` (optional,
     parity tooling) runs after every iteration, while the engine still holds
@@ -526,6 +584,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
     copies = _mode_copy_plan(shape, col_sizes, cfg, src)
     if copies:
         eng.bind_mode_copies(src.dev.flat, copies)
+    sampler = None
     try:
         # the device scans max|X| (and builds the mode copies) while the host draws the
         # first sample (the generator is consumed by sampling only, solver.py:293-316)
@@ -533,8 +592,13 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                       and os.environ.get("RTCUR_EARLY_ZETA", "1") != "0")
         if early_zeta:
             eng.absmax_begin()
+        # RTCUR-R: every draw (the first one included) from the background sampler
+        sampler = (_AheadSampler(shape, row_sizes, col_sizes, rng)
+                   if cfg.variant == "R" and cfg.max_iters > 1 and os.environ.get("RTCUR_AHEAD_SAMPLER", "1") != "0"
+                   else None)
+        draw = sampler.next if sampler is not None else (lambda: draw_sample_indices(shape, row_sizes, col_sizes, rng))
         t0 = time.perf_counter()
-        idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+        idx = draw()
         timings["sample"] += time.perf_counter() - t0
         t0 = time.perf_counter()
         eng.set_sample(idx)
@@ -560,7 +624,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
         for k in range(1, cfg.max_iters + 1):
             if cfg.variant == "R" and k >= 2:
                 t0 = time.perf_counter()
-                idx = next_idx if next_idx is not None else draw_sample_indices(shape, row_sizes, col_sizes, rng)
+                idx = next_idx if next_idx is not None else draw()
                 next_idx = None
                 timings["sample"] += time.perf_counter() - t0
                 if not staged:
@@ -574,7 +638,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
             eng.iterate_async(zeta, first=(k == 1))
             if cfg.variant == "R" and k < cfg.max_iters:
                 t1 = time.perf_counter()
-                next_idx = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+                next_idx = draw()
                 timings["sample"] += time.perf_counter() - t1
                 if prefetch:
                     t1 = time.perf_counter()
@@ -599,6 +663,8 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                 converged = True
                 break
     finally:
+        if sampler is not None:
+            sampler.close()
         if copies:
             eng.bind_mode_copies(None, ())   # the loop is done (or failed); exports do not gather
     timings["loop"] = time.perf_counter() - t_loop
