@@ -1409,6 +1409,18 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ea.full[m] = eig_pick_full((int)P.s[m], P.g.rank[m]);
     esm = std::max(esm, eig_smem_bytes(P, m));
   }
+  // Lanczos full path: the Krylov basis goes after the mode's base layout
+  {
+    static const bool lz = [] { const char* v = getenv("RTCUR_EIG_LANCZOS"); return !(v && v[0] == '0'); }();
+    for (int m = 0; m < n; ++m) {
+      const int sm = (int)P.s[m], rm = P.g.rank[m];
+      const long long base = eig_smem_doubles(sm, rm, P.nb[m], ea.full[m], eig_fast_ok(P, m));
+      const int mcap = lz ? eig_lz_mcap(sm, rm, base, ea.full[m]) : 0;
+      ea.lz_mcap[m] = mcap;
+      ea.lz_off[m] = (int)base;
+      if (mcap) esm = std::max(esm, (int)((base + (long long)sm * (mcap + 1) + mcap + 1 + 8) * 8));
+    }
+  }
   ea.tmark = e->at<long long>(P.o_dbg);
   // certified attempts take <= 15 steps at configs 0-4 (tools/eig_paths.py); a
   // failing one is capped near the full path's cost

@@ -50,6 +50,10 @@ struct EigArgs {
   int ms_warps;                        // multisection: max warps per eigenvalue (shifts = 64 x warps)
   int* fast_used;                      // per mode: 1 if the fast path certified the subspace
   int reg_tridiag;                     // register-tiled tridiagonalisation: 1 for 128 < s <= 256 (clusters), 2 also s <= 128
+  // Lanczos full path (s <= 128, full storage): Krylov basis capacity (0: off) and
+  // its shared-memory offset (doubles from the start of the dynamic smem)
+  int lz_mcap[RT_MAX_MODES];
+  int lz_off[RT_MAX_MODES];
   // inverse-iteration LU factors in global scratch (r x 4s doubles, then r x s
   // pivot bytes), or null: in shared memory, nb at a time.  Used when fewer than
   // r factorisations fit next to K (s = 213 packed: 2), so all r run at once.
@@ -69,6 +73,18 @@ __host__ __device__ inline long long eig_smem_doubles(int s, int r, int nb, int 
   const long long amat = full ? (long long)s * eig_ld(s) + (long long)s * (s - 1) / 2 : (long long)s * (s + 1) / 2;
   const long long need = (long long)s * r + 3LL * r * r, tail = eig_tail_doubles(s, nb);
   return amat + (long long)s * r + 2LL * r + 96 + tail + (sub && need > tail ? need - tail : 0);
+}
+
+// Lanczos basis capacity for the full path (0: not used): full storage, 16 <= s <=
+// 128, basis columns up to 64 and within the 227 KB next to the base layout
+#define EIG_LZ_MMAX 64
+__host__ __device__ inline int eig_lz_mcap(int s, int r, long long base_doubles, int full) {
+  if (!full || s < 16 || s > 128) return 0;
+  const long long avail = EIG_SMEM_DOUBLES - base_doubles - 8;
+  long long m = avail / (s + 1) - 1;
+  m = m < EIG_LZ_MMAX ? m : EIG_LZ_MMAX;
+  m = m < s - 1 ? m : s - 1;
+  return m >= (3 * r > 12 ? 3 * r : 12) ? (int)m : 0;
 }
 
 __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // i >= j
@@ -658,6 +674,267 @@ __device__ int eig_tridiag_reg(const double* __restrict__ A, int ld, const doubl
 
 extern __shared__ double eig_smem[];
 
+// The r largest eigenpairs of the symmetric tridiagonal T (dd: diagonal, ed:
+// off-diagonal, size s) into E (s x r, column-major, stride s): multisection on
+// Sturm counts of the tn-normalised T, then block inverse iteration with cluster
+// re-orthogonalisation and a final CGS2 (see the header).  Used on the
+// Householder tridiagonal (s = |I_k|) and on the Lanczos tridiagonal T_m.
+// scal[1], scal[2]: Gershgorin bounds of T; tn > 0 its norm bound.
+__device__ void eig_tri_vectors(const EigArgs& ea, int mi, int s, int r, int nb, double tn, const double* dd,
+                                const double* ed, double* dn, double* e2n, double* lam, int* clus, double* red,
+                                double* red2, const double* scal, double* lu, unsigned char* piv, double* E,
+                                long long* tm) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  // ---------------------------------------------------------------- 2. multisection (normalised T)
+  const double itn = 1.0 / tn;
+  const int s4 = 1 + ((s - 1 + 3) / 4) * 4;   // padded length of the Sturm arrays
+  for (int i = tid; i < s4; i += blockDim.x) {
+    dn[i] = i < s ? dd[i] * itn : 1e30;
+    const double en = (i + 1 < s) ? ed[i] * itn : 0.0;
+    e2n[i] = en * en;
+  }
+  __syncthreads();
+  {
+    // ng warps per eigenvalue test ng*32 shifts per round; brackets combined in
+    // shared memory (double-buffered by round parity: one barrier per round)
+    const double pad = 4.0 * DBL_EPSILON * s;
+    double* blo = red;                  // 2 x 16 warp brackets (lo); red/red2 are free here
+    double* bhi = red2;                 // 2 x 16 warp brackets (hi)
+    for (int j0 = 0; j0 < r; j0 += nw) {
+      const int rr = min(nw, r - j0);
+      // the counts are fp64-pipe bound on this one SM: more shifts per round cost more
+      // than the rounds they save beyond ~one warp per eigenvalue
+      const int ng = max(1, min(nw / rr, ea.ms_warps));
+      const int j = j0 + wid / ng, g = wid % ng;
+      const bool act = wid < rr * ng;
+      const double nsh = (double)(ng * 64 + 1);
+      const int rounds = (int)ceil(log(16.0 / DBL_EPSILON) / log(nsh)) + 1;
+      double lo = scal[1] * itn - pad, hi = scal[2] * itn + pad;
+      for (int round = 0; round < rounds; ++round) {
+        double nlo = -DBL_MAX, nhi = DBL_MAX;
+        if (act && hi > lo) {
+          const int target = s - 1 - j;   // ascending index of the j-th largest
+          const double xa = lo + (hi - lo) * (double)(g * 64 + 2 * lane + 1) / nsh;
+          const double xb = lo + (hi - lo) * (double)(g * 64 + 2 * lane + 2) / nsh;
+          int ca, cb;
+          sturm_count2(dn, e2n, s4, xa, xb, ca, cb);
+          if (ca <= target) nlo = xa;
+          if (cb <= target) nlo = xb;
+          if (cb >= target + 1) nhi = xb;
+          if (ca >= target + 1) nhi = xa;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          nlo = fmax(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
+          nhi = fmin(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+        }
+        double* bl = blo + (round & 1) * 16;
+        double* bh = bhi + (round & 1) * 16;
+        if (lane == 0) { bl[wid] = nlo; bh[wid] = nhi; }
+        __syncthreads();
+        if (act) {
+          for (int q = 0; q < ng; ++q) {
+            const int w2 = (wid / ng) * ng + q;
+            if (bl[w2] != -DBL_MAX) lo = fmax(lo, bl[w2]);
+            if (bh[w2] != DBL_MAX) hi = fmin(hi, bh[w2]);
+          }
+          if (lo > hi) lo = hi = 0.5 * (lo + hi);
+        }
+      }
+      if (act && g == 0 && lane == 0) lam[j] = 0.5 * (lo + hi) * tn;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // clusters (descending order): j joins j-1 when the gap is below ORTOL * ||T||
+    clus[0] = 0;
+    for (int j = 1; j < r; ++j) clus[j] = (lam[j - 1] - lam[j] < 1e-3 * tn) ? clus[j - 1] : j;
+  }
+  for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = lam[j];
+  __syncthreads();
+  if (tm && tid == 0) tm[3] = clock64();
+
+  // ---------------------------------------------------------------- 3. block inverse iteration
+  const double tiny = DBL_EPSILON * tn;
+  const double pertol = 10.0 * DBL_EPSILON * tn;
+  double* const lug = ea.lug[mi];
+  const int nbe = lug ? r : nb;
+  for (int j0 = 0; j0 < r; j0 += nbe) {
+    const int jn = min(nbe, r - j0);
+    double* u0 = lug ? lug + (size_t)4 * s * tid : lu + (size_t)4 * s * tid;
+    double* u1 = u0 + s;
+    double* u2 = u1 + s;
+    double* lm = u2 + s;
+    unsigned char* pv = lug ? reinterpret_cast<unsigned char*>(lug + (size_t)4 * s * r) + (size_t)s * tid
+                            : piv + (size_t)s * tid;
+    if (tid < jn) {
+      const int j = j0 + tid;
+      double mu = lam[j];
+      // separate (nearly) equal shifts so every factorisation is distinct
+      for (int i = 0; i < j; ++i)
+        if (fabs(lam[i] - mu) < pertol * (j - i)) mu = lam[i] - pertol * (j - i);
+      double ca = dd[0] - mu, cb = (s > 1) ? ed[0] : 0.0;
+      for (int i = 0; i + 1 < s; ++i) {
+        const double na = dd[i + 1] - mu;
+        const double nbv = (i + 2 < s) ? ed[i + 1] : 0.0;
+        const double c = ed[i];
+        if (fabs(ca) >= fabs(c)) {
+          if (fabs(ca) < tiny) ca = copysign(tiny, ca);
+          const double inv = 1.0 / ca;
+          const double l = c * inv;
+          u0[i] = inv;
+          u1[i] = cb;
+          u2[i] = 0.0;
+          pv[i] = 0;
+          lm[i] = l;
+          ca = na - l * cb;
+          cb = nbv;
+        } else {
+          const double inv = 1.0 / c;
+          const double l = ca * inv;
+          u0[i] = inv;
+          u1[i] = na;
+          u2[i] = nbv;
+          pv[i] = 1;
+          lm[i] = l;
+          ca = cb - l * na;
+          cb = -l * nbv;
+        }
+      }
+      if (fabs(ca) < tiny) ca = copysign(tiny, ca);
+      u0[s - 1] = 1.0 / ca;
+      u1[s - 1] = 0.0;
+      u2[s - 1] = 0.0;
+      if (s >= 2) u2[s - 2] = 0.0;
+      double* x = E + j * s;
+      for (int i = 0; i < s; ++i) x[i] = hash_unit(((unsigned long long)j << 32) ^ (unsigned long long)i);
+    }
+    __syncthreads();
+    bool any_cluster = false;
+    for (int j = j0; j < j0 + jn; ++j) any_cluster |= (clus[j] != j);
+    for (int it = 0; it < 3; ++it) {
+      if (tid < jn) {
+        double* __restrict__ x = E + (j0 + tid) * s;
+        double bi = x[0];
+        double bn = s > 1 ? x[1] : 0.0;
+        double l_i = lm[0];
+        bool p_i = s > 1 ? pv[0] : 0;
+        for (int i = 0; i + 1 < s; ++i) {
+          // prefetch the next step's operands before the dependent update
+          const double bnn = (i + 2 < s) ? x[i + 2] : 0.0;
+          const double lnx = (i + 2 < s) ? lm[i + 1] : 0.0;
+          const bool pnx = (i + 2 < s) ? pv[i + 1] : 0;
+          double b_lo = bi, b_hi = bn;
+          if (p_i) { b_lo = bn; b_hi = bi; }
+          x[i] = b_lo;
+          bi = fma(-l_i, b_lo, b_hi);
+          bn = bnn;
+          l_i = lnx;
+          p_i = pnx;
+        }
+        x[s - 1] = bi;
+        double xn1 = 0.0, xn2 = 0.0, mx = 0.0;
+        double xi = x[s - 1], a1 = u1[s - 1], a2 = u2[s - 1], a0 = u0[s - 1];
+        for (int i = s - 1; i >= 0; --i) {
+          const double xp = i > 0 ? x[i - 1] : 0.0;
+          const double b1 = i > 0 ? u1[i - 1] : 0.0, b2 = i > 0 ? u2[i - 1] : 0.0, b0 = i > 0 ? u0[i - 1] : 0.0;
+          double v = (xi - a1 * xn1 - a2 * xn2) * a0;
+          v = isfinite(v) ? v : 0.0;
+          x[i] = v;
+          mx = fmax(mx, fabs(v));
+          xn2 = xn1;
+          xn1 = v;
+          xi = xp; a1 = b1; a2 = b2; a0 = b0;
+        }
+        const double inv = mx > 0.0 ? 1.0 / mx : 0.0;
+        for (int i = 0; i < s; ++i) x[i] *= inv;
+      }
+      __syncthreads();
+      if (!any_cluster) continue;
+      // orthogonalise each clustered vector against the earlier members of its cluster
+      for (int j = j0; j < j0 + jn; ++j) {
+        const int c0 = clus[j];
+        if (c0 == j) continue;
+        double* xj = E + j * s;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int i = c0 + wid; i < j; i += nw) {
+            const double* xi = E + i * s;
+            double d = 0.0;
+            for (int t = lane; t < s; t += 32) d = fma(xi[t], xj[t], d);
+            d = warp_sum(d);
+            if (lane == 0) red[i - c0] = d;
+          }
+          __syncthreads();
+          for (int t = tid; t < s; t += blockDim.x) {
+            double v = xj[t];
+            for (int i = c0; i < j; ++i) v = fma(-red[i - c0], E[t + i * s], v);
+            xj[t] = v;
+          }
+          __syncthreads();
+        }
+        double nn = 0.0;
+        for (int t = tid; t < s; t += blockDim.x) nn = fma(xj[t], xj[t], nn);
+        nn = warp_sum(nn);
+        if (lane == 0) red2[wid] = nn;
+        __syncthreads();
+        nn = warp_sum_of(red2, nw);
+        const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+        for (int t = tid; t < s; t += blockDim.x) xj[t] = nn > 0.0 ? xj[t] * inv : (t == j % s ? 1.0 : 0.0);
+        __syncthreads();
+      }
+    }
+  }
+  // final CGS2 over all r vectors (warp w owns vector j; dots against the finished ones)
+  for (int j = 0; j < r; ++j) {
+    double* xj = E + j * s;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (j > 0) {
+        for (int i = wid; i < j; i += nw) {
+          const double* xi = E + i * s;
+          double d = 0.0;
+          for (int t = lane; t < s; t += 32) d = fma(xi[t], xj[t], d);
+          d = warp_sum(d);
+          if (lane == 0) red[i] = d;
+        }
+        __syncthreads();
+        for (int t = tid; t < s; t += blockDim.x) {
+          double v = xj[t];
+          for (int i = 0; i < j; ++i) v = fma(-red[i], E[t + i * s], v);
+          xj[t] = v;
+        }
+      }
+      double nn = 0.0;
+      for (int t = tid; t < s; t += blockDim.x) nn = fma(xj[t], xj[t], nn);
+      nn = warp_sum(nn);
+      __syncthreads();
+      if (lane == 0) red2[wid] = nn;
+      __syncthreads();
+      nn = warp_sum_of(red2, nw);
+      const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+      for (int t = tid; t < s; t += blockDim.x) xj[t] = nn > 0.0 ? xj[t] * inv : (t == j % s ? 1.0 : 0.0);
+      __syncthreads();
+    }
+  }
+  if (tm && tid == 0) tm[4] = clock64();
+
+}
+
+// Gershgorin bounds of the tridiagonal (dd, ed) of size n into scal[0..2]:
+// tn = max row sum, lo, hi (thread 0)
+__device__ __forceinline__ void eig_tri_bounds(const double* dd, const double* ed, int n, double* scal) {
+  double tn = 0.0, lo = DBL_MAX, hi = -DBL_MAX;
+  for (int i = 0; i < n; ++i) {
+    const double rad = (i > 0 ? fabs(ed[i - 1]) : 0.0) + (i + 1 < n ? fabs(ed[i]) : 0.0);
+    tn = fmax(tn, fabs(dd[i]) + rad);
+    lo = fmin(lo, dd[i] - rad);
+    hi = fmax(hi, dd[i] + rad);
+  }
+  scal[0] = tn;
+  scal[1] = lo;
+  scal[2] = hi;
+}
+
 __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   // launched either one CTA per mode, or (some s > 128) as clusters of EIG_CLUSTER
   // CTAs per mode: the cluster's extra CTAs only join the register-tiled
@@ -744,6 +1021,128 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   }
   if (warm_ok) return;
   if (crank == 0 && tid == 0 && ea.fast_used) ea.fast_used[mi] = 0;
+
+  // ---------------------------------------------------------------- 0b. Lanczos (full path, s <= 128)
+  // Lanczos with full (CGS2) reorthogonalisation from a fixed pseudo-random start
+  // builds T_m = V_m^T K V_m; every 8 steps the r largest eigenpairs of T_m
+  // (eig_tri_vectors: the same multisection + inverse iteration as the
+  // Householder path, on the small T_m) give Ritz pairs with residuals
+  // ||K V y - theta V y|| = beta_m |y_m|; once all r are below 1e-14 ||T_m|| the
+  // Ritz vectors V_m Y are the eigenbasis (the Rayleigh-Ritz step of k_svdpost
+  // then fixes the basis inside their span, as for the other paths).  The
+  // Householder path needs s - 2 dependent steps; the top-r Ritz pairs of a
+  // well separated spectrum converge in far fewer.  Not converged within the
+  // basis capacity (or breakdown below r): the Householder path below (K is
+  // untouched).
+  if (crank == 0 && ea.lz_mcap[mi] > 0) {
+    const int mcap = ea.lz_mcap[mi];
+    double* V = eig_smem + ea.lz_off[mi];        // s x (mcap + 1), column k at V + k s
+    double* hv = V + (size_t)s * (mcap + 1);     // mcap + 1 projection coefficients
+    double* al = dd;                             // T_m diagonal
+    double* be = ed;                             // T_m off-diagonal; be[m-1] = the residual norm
+    double kn2 = 0.0;                            // ||K||_F^2 (breakdown scale)
+    for (int e = tid; e < s * s; e += blockDim.x) {
+      const double v = A[(e / s) * ld + (e % s)];
+      kn2 = fma(v, v, kn2);
+    }
+    double v0 = 0.0;
+    for (int i = tid; i < s; i += blockDim.x) {
+      const double h = hash_unit(0x5DEECE66DULL ^ ((unsigned long long)i * 0x9E3779B9ULL));
+      V[i] = h;
+      v0 = fma(h, h, v0);
+    }
+    kn2 = warp_sum(kn2);
+    v0 = warp_sum(v0);
+    if (lane == 0) {
+      red[wid] = kn2;
+      red2[wid] = v0;
+    }
+    __syncthreads();
+    const double knorm = sqrt(warp_sum_of(red, nw));
+    const double vinv = 1.0 / sqrt(warp_sum_of(red2, nw));
+    __syncthreads();
+    for (int i = tid; i < s; i += blockDim.x) V[i] *= vinv;
+    __syncthreads();
+    int m = 0;
+    bool conv = false;
+    const int first_chk = max(16, 3 * r);
+    for (int j = 0; j < mcap && !conv; ++j) {
+      const double* vj = V + (size_t)j * s;
+      double* w = V + (size_t)(j + 1) * s;
+      // w = K v_j: rows by groups of EIG_TPR threads (512 / 4 = 128 >= s rows)
+      {
+        const int i = tid / EIG_TPR, sub = tid & (EIG_TPR - 1);
+        double acc = 0.0;
+        if (i < s) {
+          const double* row = A + i * ld;
+          for (int c = sub; c < s; c += EIG_TPR) acc = fma(row[c], vj[c], acc);
+        }
+#pragma unroll
+        for (int o = EIG_TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (i < s && sub == 0) w[i] = acc;
+      }
+      __syncthreads();
+      // CGS2 against v_0..v_j; alpha_j = v_j^T K v_j from the two passes
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int k = wid; k <= j; k += nw) {
+          const double* vk = V + (size_t)k * s;
+          double d = 0.0;
+          for (int t = lane; t < s; t += 32) d = fma(vk[t], w[t], d);
+          d = warp_sum(d);
+          if (lane == 0) hv[k] = d;
+        }
+        __syncthreads();
+        if (tid == 0) al[j] = pass == 0 ? hv[j] : al[j] + hv[j];
+        for (int t = tid; t < s; t += blockDim.x) {
+          double v = w[t];
+          for (int k = 0; k <= j; ++k) v = fma(-hv[k], V[(size_t)k * s + t], v);
+          w[t] = v;
+        }
+        __syncthreads();
+      }
+      double nn = 0.0;
+      for (int t = tid; t < s; t += blockDim.x) nn = fma(w[t], w[t], nn);
+      nn = warp_sum(nn);
+      if (lane == 0) red[wid] = nn;
+      __syncthreads();
+      const double b = sqrt(warp_sum_of(red, nw));
+      m = j + 1;
+      const bool brk = !(b > 1e-13 * knorm);   // invariant subspace: T_m is exact
+      if (tid == 0) be[j] = brk ? 0.0 : b;
+      if (!brk) {
+        const double bi = 1.0 / b;
+        for (int t = tid; t < s; t += blockDim.x) w[t] *= bi;
+      }
+      __syncthreads();
+      if (brk && m < r) break;   // fewer than r directions: the Householder path
+      if (brk || m == mcap || (m >= first_chk && (m - first_chk) % 8 == 0)) {
+        if (tid == 0) eig_tri_bounds(al, be, m, scal);
+        __syncthreads();
+        const double tn = scal[0];
+        if (tn > 0.0) {
+          eig_tri_vectors(ea, mi, m, r, nb, tn, al, be, dn, e2n, lam, clus, red, red2, scal, lu, piv, E, nullptr);
+          double rmax = 0.0;
+          for (int c = 0; c < r; ++c) rmax = fmax(rmax, fabs(be[m - 1] * E[(size_t)c * m + m - 1]));
+          conv = rmax <= 1e-14 * tn;   // (block-uniform: every thread reads the same values)
+        }
+        __syncthreads();
+      }
+    }
+    if (conv) {
+      // Ritz vectors V_m Y (s x r) straight to the output
+      double* Eo = ea.E[mi];
+      for (int e = tid; e < s * r; e += blockDim.x) {
+        const int i = e % s, c = e / s;
+        double acc = 0.0;
+        for (int k = 0; k < m; ++k) acc = fma(V[(size_t)k * s + i], E[(size_t)c * m + k], acc);
+        Eo[e] = acc;
+      }
+      if (tid == 0 && ea.fast_used) ea.fast_used[mi] = -m;   // (diagnostic: Lanczos steps, negated)
+      if (tm && tid == 0) tm[6] = clock64();
+      return;
+    }
+    __syncthreads();
+  }
 
   // ---------------------------------------------------------------- 1. tridiagonalise
   int hoff = 0;
@@ -988,16 +1387,7 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
       }
       dd[s - 1] = full ? A[(s - 1) * ld + s - 1] : A[pk(s - 1, s - 1)];
     }
-    double tn = 0.0, lo = DBL_MAX, hi = -DBL_MAX;
-    for (int i = 0; i < s; ++i) {
-      const double rad = (i > 0 ? fabs(ed[i - 1]) : 0.0) + (i + 1 < s ? fabs(ed[i]) : 0.0);
-      tn = fmax(tn, fabs(dd[i]) + rad);
-      lo = fmin(lo, dd[i] - rad);
-      hi = fmax(hi, dd[i] + rad);
-    }
-    scal[0] = tn;
-    scal[1] = lo;
-    scal[2] = hi;
+    eig_tri_bounds(dd, ed, s, scal);
   }
   __syncthreads();
   if (tm && tid == 0) tm[2] = clock64();
@@ -1011,238 +1401,7 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
     return;
   }
 
-  // ---------------------------------------------------------------- 2. multisection (normalised T)
-  const double itn = 1.0 / tn;
-  const int s4 = 1 + ((s - 1 + 3) / 4) * 4;   // padded length of the Sturm arrays
-  for (int i = tid; i < s4; i += blockDim.x) {
-    dn[i] = i < s ? dd[i] * itn : 1e30;
-    const double en = (i + 1 < s) ? ed[i] * itn : 0.0;
-    e2n[i] = en * en;
-  }
-  __syncthreads();
-  {
-    // ng warps per eigenvalue test ng*32 shifts per round; brackets combined in
-    // shared memory (double-buffered by round parity: one barrier per round)
-    const double pad = 4.0 * DBL_EPSILON * s;
-    double* blo = red;                  // 2 x 16 warp brackets (lo); red/red2 are free here
-    double* bhi = red2;                 // 2 x 16 warp brackets (hi)
-    for (int j0 = 0; j0 < r; j0 += nw) {
-      const int rr = min(nw, r - j0);
-      // the counts are fp64-pipe bound on this one SM: more shifts per round cost more
-      // than the rounds they save beyond ~one warp per eigenvalue
-      const int ng = max(1, min(nw / rr, ea.ms_warps));
-      const int j = j0 + wid / ng, g = wid % ng;
-      const bool act = wid < rr * ng;
-      const double nsh = (double)(ng * 64 + 1);
-      const int rounds = (int)ceil(log(16.0 / DBL_EPSILON) / log(nsh)) + 1;
-      double lo = scal[1] * itn - pad, hi = scal[2] * itn + pad;
-      for (int round = 0; round < rounds; ++round) {
-        double nlo = -DBL_MAX, nhi = DBL_MAX;
-        if (act && hi > lo) {
-          const int target = s - 1 - j;   // ascending index of the j-th largest
-          const double xa = lo + (hi - lo) * (double)(g * 64 + 2 * lane + 1) / nsh;
-          const double xb = lo + (hi - lo) * (double)(g * 64 + 2 * lane + 2) / nsh;
-          int ca, cb;
-          sturm_count2(dn, e2n, s4, xa, xb, ca, cb);
-          if (ca <= target) nlo = xa;
-          if (cb <= target) nlo = xb;
-          if (cb >= target + 1) nhi = xb;
-          if (ca >= target + 1) nhi = xa;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          nlo = fmax(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
-          nhi = fmin(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
-        }
-        double* bl = blo + (round & 1) * 16;
-        double* bh = bhi + (round & 1) * 16;
-        if (lane == 0) { bl[wid] = nlo; bh[wid] = nhi; }
-        __syncthreads();
-        if (act) {
-          for (int q = 0; q < ng; ++q) {
-            const int w2 = (wid / ng) * ng + q;
-            if (bl[w2] != -DBL_MAX) lo = fmax(lo, bl[w2]);
-            if (bh[w2] != DBL_MAX) hi = fmin(hi, bh[w2]);
-          }
-          if (lo > hi) lo = hi = 0.5 * (lo + hi);
-        }
-      }
-      if (act && g == 0 && lane == 0) lam[j] = 0.5 * (lo + hi) * tn;
-      __syncthreads();
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // clusters (descending order): j joins j-1 when the gap is below ORTOL * ||T||
-    clus[0] = 0;
-    for (int j = 1; j < r; ++j) clus[j] = (lam[j - 1] - lam[j] < 1e-3 * tn) ? clus[j - 1] : j;
-  }
-  for (int j = tid; j < r; j += blockDim.x) ea.lam[mi][j] = lam[j];
-  __syncthreads();
-  if (tm && tid == 0) tm[3] = clock64();
-
-  // ---------------------------------------------------------------- 3. block inverse iteration
-  const double tiny = DBL_EPSILON * tn;
-  const double pertol = 10.0 * DBL_EPSILON * tn;
-  double* const lug = ea.lug[mi];
-  const int nbe = lug ? r : nb;
-  for (int j0 = 0; j0 < r; j0 += nbe) {
-    const int jn = min(nbe, r - j0);
-    double* u0 = lug ? lug + (size_t)4 * s * tid : lu + (size_t)4 * s * tid;
-    double* u1 = u0 + s;
-    double* u2 = u1 + s;
-    double* lm = u2 + s;
-    unsigned char* pv = lug ? reinterpret_cast<unsigned char*>(lug + (size_t)4 * s * r) + (size_t)s * tid
-                            : piv + (size_t)s * tid;
-    if (tid < jn) {
-      const int j = j0 + tid;
-      double mu = lam[j];
-      // separate (nearly) equal shifts so every factorisation is distinct
-      for (int i = 0; i < j; ++i)
-        if (fabs(lam[i] - mu) < pertol * (j - i)) mu = lam[i] - pertol * (j - i);
-      double ca = dd[0] - mu, cb = (s > 1) ? ed[0] : 0.0;
-      for (int i = 0; i + 1 < s; ++i) {
-        const double na = dd[i + 1] - mu;
-        const double nbv = (i + 2 < s) ? ed[i + 1] : 0.0;
-        const double c = ed[i];
-        if (fabs(ca) >= fabs(c)) {
-          if (fabs(ca) < tiny) ca = copysign(tiny, ca);
-          const double inv = 1.0 / ca;
-          const double l = c * inv;
-          u0[i] = inv;
-          u1[i] = cb;
-          u2[i] = 0.0;
-          pv[i] = 0;
-          lm[i] = l;
-          ca = na - l * cb;
-          cb = nbv;
-        } else {
-          const double inv = 1.0 / c;
-          const double l = ca * inv;
-          u0[i] = inv;
-          u1[i] = na;
-          u2[i] = nbv;
-          pv[i] = 1;
-          lm[i] = l;
-          ca = cb - l * na;
-          cb = -l * nbv;
-        }
-      }
-      if (fabs(ca) < tiny) ca = copysign(tiny, ca);
-      u0[s - 1] = 1.0 / ca;
-      u1[s - 1] = 0.0;
-      u2[s - 1] = 0.0;
-      if (s >= 2) u2[s - 2] = 0.0;
-      double* x = E + j * s;
-      for (int i = 0; i < s; ++i) x[i] = hash_unit(((unsigned long long)j << 32) ^ (unsigned long long)i);
-    }
-    __syncthreads();
-    bool any_cluster = false;
-    for (int j = j0; j < j0 + jn; ++j) any_cluster |= (clus[j] != j);
-    for (int it = 0; it < 3; ++it) {
-      if (tid < jn) {
-        double* __restrict__ x = E + (j0 + tid) * s;
-        double bi = x[0];
-        double bn = s > 1 ? x[1] : 0.0;
-        double l_i = lm[0];
-        bool p_i = s > 1 ? pv[0] : 0;
-        for (int i = 0; i + 1 < s; ++i) {
-          // prefetch the next step's operands before the dependent update
-          const double bnn = (i + 2 < s) ? x[i + 2] : 0.0;
-          const double lnx = (i + 2 < s) ? lm[i + 1] : 0.0;
-          const bool pnx = (i + 2 < s) ? pv[i + 1] : 0;
-          double b_lo = bi, b_hi = bn;
-          if (p_i) { b_lo = bn; b_hi = bi; }
-          x[i] = b_lo;
-          bi = fma(-l_i, b_lo, b_hi);
-          bn = bnn;
-          l_i = lnx;
-          p_i = pnx;
-        }
-        x[s - 1] = bi;
-        double xn1 = 0.0, xn2 = 0.0, mx = 0.0;
-        double xi = x[s - 1], a1 = u1[s - 1], a2 = u2[s - 1], a0 = u0[s - 1];
-        for (int i = s - 1; i >= 0; --i) {
-          const double xp = i > 0 ? x[i - 1] : 0.0;
-          const double b1 = i > 0 ? u1[i - 1] : 0.0, b2 = i > 0 ? u2[i - 1] : 0.0, b0 = i > 0 ? u0[i - 1] : 0.0;
-          double v = (xi - a1 * xn1 - a2 * xn2) * a0;
-          v = isfinite(v) ? v : 0.0;
-          x[i] = v;
-          mx = fmax(mx, fabs(v));
-          xn2 = xn1;
-          xn1 = v;
-          xi = xp; a1 = b1; a2 = b2; a0 = b0;
-        }
-        const double inv = mx > 0.0 ? 1.0 / mx : 0.0;
-        for (int i = 0; i < s; ++i) x[i] *= inv;
-      }
-      __syncthreads();
-      if (!any_cluster) continue;
-      // orthogonalise each clustered vector against the earlier members of its cluster
-      for (int j = j0; j < j0 + jn; ++j) {
-        const int c0 = clus[j];
-        if (c0 == j) continue;
-        double* xj = E + j * s;
-        for (int pass = 0; pass < 2; ++pass) {
-          for (int i = c0 + wid; i < j; i += nw) {
-            const double* xi = E + i * s;
-            double d = 0.0;
-            for (int t = lane; t < s; t += 32) d = fma(xi[t], xj[t], d);
-            d = warp_sum(d);
-            if (lane == 0) red[i - c0] = d;
-          }
-          __syncthreads();
-          for (int t = tid; t < s; t += blockDim.x) {
-            double v = xj[t];
-            for (int i = c0; i < j; ++i) v = fma(-red[i - c0], E[t + i * s], v);
-            xj[t] = v;
-          }
-          __syncthreads();
-        }
-        double nn = 0.0;
-        for (int t = tid; t < s; t += blockDim.x) nn = fma(xj[t], xj[t], nn);
-        nn = warp_sum(nn);
-        if (lane == 0) red2[wid] = nn;
-        __syncthreads();
-        nn = warp_sum_of(red2, nw);
-        const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-        for (int t = tid; t < s; t += blockDim.x) xj[t] = nn > 0.0 ? xj[t] * inv : (t == j % s ? 1.0 : 0.0);
-        __syncthreads();
-      }
-    }
-  }
-  // final CGS2 over all r vectors (warp w owns vector j; dots against the finished ones)
-  for (int j = 0; j < r; ++j) {
-    double* xj = E + j * s;
-    for (int pass = 0; pass < 2; ++pass) {
-      if (j > 0) {
-        for (int i = wid; i < j; i += nw) {
-          const double* xi = E + i * s;
-          double d = 0.0;
-          for (int t = lane; t < s; t += 32) d = fma(xi[t], xj[t], d);
-          d = warp_sum(d);
-          if (lane == 0) red[i] = d;
-        }
-        __syncthreads();
-        for (int t = tid; t < s; t += blockDim.x) {
-          double v = xj[t];
-          for (int i = 0; i < j; ++i) v = fma(-red[i], E[t + i * s], v);
-          xj[t] = v;
-        }
-      }
-      double nn = 0.0;
-      for (int t = tid; t < s; t += blockDim.x) nn = fma(xj[t], xj[t], nn);
-      nn = warp_sum(nn);
-      __syncthreads();
-      if (lane == 0) red2[wid] = nn;
-      __syncthreads();
-      nn = warp_sum_of(red2, nw);
-      const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-      for (int t = tid; t < s; t += blockDim.x) xj[t] = nn > 0.0 ? xj[t] * inv : (t == j % s ? 1.0 : 0.0);
-      __syncthreads();
-    }
-  }
-  if (tm && tid == 0) tm[4] = clock64();
+  eig_tri_vectors(ea, mi, s, r, nb, tn, dd, ed, dn, e2n, lam, clus, red, red2, scal, lu, piv, E, tm);
 
   // ---------------------------------------------------------------- 4. back-transform
   for (int j = wid; j < r; j += nw) {
