@@ -75,11 +75,13 @@ __host__ __device__ inline long long eig_smem_doubles(int s, int r, int nb, int 
   return amat + (long long)s * r + 2LL * r + 96 + tail + (sub && need > tail ? need - tail : 0);
 }
 
-// Lanczos basis capacity for the full path (0: not used): full storage, 16 <= s <=
-// 128, basis columns up to 64 and within the 227 KB next to the base layout
+// Lanczos basis capacity for the full path (0: not used): full storage, 64 <= s <=
+// 128 (below 64 the Householder path's s - 2 steps are no more than the ~24 Lanczos
+// steps plus Ritz checks: measured 1.63 vs 1.70 ms per solve at s = 42), basis
+// columns up to 64 and within the 227 KB next to the base layout
 #define EIG_LZ_MMAX 64
 __host__ __device__ inline int eig_lz_mcap(int s, int r, long long base_doubles, int full) {
-  if (!full || s < 16 || s > 128) return 0;
+  if (!full || s < 64 || s > 128) return 0;
   const long long avail = EIG_SMEM_DOUBLES - base_doubles - 8;
   long long m = avail / (s + 1) - 1;
   m = m < EIG_LZ_MMAX ? m : EIG_LZ_MMAX;

@@ -79,10 +79,14 @@ def _parallel_copy(dst, src, parts=8):
 _COPY_POOL = None
 
 
+CREATED = [0]   # engines constructed in this process (diagnostics: pooled solves construct none)
+
+
 class Engine:
     def __init__(self, shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=None):
         import torch
 
+        CREATED[0] += 1
         self.lib = nat.load()
         if not torch.cuda.is_available():
             raise RuntimeError("rtcur_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")

@@ -53,6 +53,8 @@ PROFILE_PHASES = None  # phase names timed while PROFILE (None: all)
 # host-observed iteration time, the other per-phase keys 0.0
 # (timings["timing_source"] = "host").
 PHASE_TIMINGS = os.environ.get("RTCUR_PHASE_TIMINGS", "0") == "1"
+# diagnostics: a list receives (event, iteration, perf_counter) host timestamps of the loop
+_TIMELINE = None
 _REF_PHASES = {"gather": ("prep", "gather"), "eval_lowrank": ("wcols",), "threshold": ("threshold",),
                "build": ("gram", "eig", "svdpost", "apass", "gpass"), "error": ("error",)}
 
@@ -573,7 +575,11 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
         if r > rs or r > cs:   # fiber_cur.py:257-261 (raised before any work, as there)
             raise ValueError(f"mode {m}: rank {r} exceeds sample sizes (|rows|={rs}, |cols|={cs})")
 
+    if _TIMELINE is not None:
+        _TIMELINE.append(("enter", 0, time.perf_counter()))
     eng = acquire_engine(shape, cfg.ranks, row_sizes, col_sizes, src.torch_dtype, slab=src.slab)
+    if _TIMELINE is not None:
+        _TIMELINE.append(("engine", 0, time.perf_counter()))
     phase_events = PHASE_TIMINGS and not PROFILE
     if PROFILE:
         eng.profile(True, PROFILE_PHASES)
@@ -584,6 +590,8 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
     copies = _mode_copy_plan(shape, col_sizes, cfg, src)
     if copies:
         eng.bind_mode_copies(src.dev.flat, copies)
+    if _TIMELINE is not None:
+        _TIMELINE.append(("copies", 0, time.perf_counter()))
     sampler = None
     try:
         # the device scans max|X| (and builds the mode copies) while the host draws the
@@ -600,15 +608,21 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
         t0 = time.perf_counter()
         idx = draw()
         timings["sample"] += time.perf_counter() - t0
+        if _TIMELINE is not None:
+            _TIMELINE.append(("first_draw", 0, time.perf_counter()))
         t0 = time.perf_counter()
         eng.set_sample(idx)
         src.load_blocks(eng, idx)
         timings["gather"] += time.perf_counter() - t0
 
+        if _TIMELINE is not None:
+            _TIMELINE.append(("staged0", 0, time.perf_counter()))
         if cfg.zeta0 is not None:
             zeta = float(cfg.zeta0)
         else:
             zeta = src.reduce_max(eng.absmax_end(), eng.device) if early_zeta else src.inf_norm(eng)
+        if _TIMELINE is not None:
+            _TIMELINE.append(("zeta0", 0, time.perf_counter()))
         t_loop = time.perf_counter()
         history, flags = [], []
         trace = [] if record_trace else None
@@ -635,6 +649,8 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                 staged = False
             zeta *= cfg.gamma
             t0 = time.perf_counter()
+            if _TIMELINE is not None:
+                _TIMELINE.append(("async", k, t0))
             eng.iterate_async(zeta, first=(k == 1))
             if cfg.variant == "R" and k < cfg.max_iters:
                 t1 = time.perf_counter()
@@ -646,8 +662,12 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                     src.load_blocks(eng, next_idx)
                     staged = True
                     timings["gather"] += time.perf_counter() - t1
+            if _TIMELINE is not None:
+                _TIMELINE.append(("staged", k, time.perf_counter()))
             e2, x2, fl = eng.iterate_wait()
             timings["build"] += time.perf_counter() - t0
+            if _TIMELINE is not None:
+                _TIMELINE.append(("waited", k, time.perf_counter()))
             err = _error_from_sums(e2, x2)
             history.append(err)
             flags.append(fl)

@@ -46,6 +46,7 @@ for k in range(1, 40):
     m8 = marks[:8 * 8].reshape(8, 8)[:n]
     fast = marks[8 * 8:8 * 8 + n]
     span = [[round(int(r[j + 1] - r[j]) / clk, 2) if r[j+1] > 0 and r[j] > 0 else 0 for j in range(7)] for r in m8]
+    # fast: > 0 warm-path steps, < 0 Lanczos steps (full path without Householder), 0 Householder
     print(f"it {k:2d} err {err:.3e} fast {[int(f) for f in fast]} eig_us {span}")
     if err <= cfg.eps:
         break
