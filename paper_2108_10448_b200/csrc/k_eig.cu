@@ -81,9 +81,10 @@ __host__ __device__ inline long long eig_smem_doubles(int s, int r, int nb, int 
 // columns up to 64 and within the 227 KB next to the base layout
 #define EIG_LZ_MMAX 64
 __host__ __device__ inline int eig_lz_mcap(int s, int r, long long base_doubles, int full) {
-  if (!full || s < 64 || s > 128) return 0;
-  const long long avail = EIG_SMEM_DOUBLES - base_doubles - 8;
-  long long m = avail / (s + 1) - 1;
+  if (s < 64 || s > 256 || (full && s > 128)) return 0;
+  // full storage: after the base layout; packed: over the shared-memory copy of K
+  const long long avail = full ? EIG_SMEM_DOUBLES - base_doubles - 8 : (long long)s * (s + 1) / 2;
+  long long m = full ? avail / (s + 1) - 1 : avail / s - 1;
   m = m < EIG_LZ_MMAX ? m : EIG_LZ_MMAX;
   m = m < s - 1 ? m : s - 1;
   return m >= (3 * r > 12 ? 3 * r : 12) ? (int)m : 0;
@@ -1014,17 +1015,7 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
       warm_ok = true;
     }
   }
-  if (use_cl) {   // tell the helper CTAs whether the full path runs (scal[20] of every CTA)
-    __syncthreads();
-    if (crank == 0 && tid == 0)
-      for (int c2 = 0; c2 < EIG_CLUSTER; ++c2) eig_put<EIG_CLUSTER>(scal + 20, c2, warm_ok ? 1.0 : 0.0);
-    cg::this_cluster().sync();                                     // S0
-    warm_ok = scal[20] != 0.0;
-  }
-  if (warm_ok) return;
-  if (crank == 0 && tid == 0 && ea.fast_used) ea.fast_used[mi] = 0;
-
-  // ---------------------------------------------------------------- 0b. Lanczos (full path, s <= 128)
+  // ---------------------------------------------------------------- 0b. Lanczos (full path, 64 <= s <= 256)
   // Lanczos with full (CGS2) reorthogonalisation from a fixed pseudo-random start
   // builds T_m = V_m^T K V_m; every 8 steps the r largest eigenpairs of T_m
   // (eig_tri_vectors: the same multisection + inverse iteration as the
@@ -1033,20 +1024,34 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   // Ritz vectors V_m Y are the eigenbasis (the Rayleigh-Ritz step of k_svdpost
   // then fixes the basis inside their span, as for the other paths).  The
   // Householder path needs s - 2 dependent steps; the top-r Ritz pairs of a
-  // well separated spectrum converge in far fewer.  Not converged within the
-  // basis capacity (or breakdown below r): the Householder path below (K is
-  // untouched).
-  if (crank == 0 && ea.lz_mcap[mi] > 0) {
+  // well separated spectrum converge in far fewer.  Full storage (s <= 128): K
+  // stays in shared memory, the basis goes after the base layout.  Packed storage
+  // (s > 128): the matvec reads the packed Gram from global memory (L2) and the
+  // basis overwrites the shared-memory copy of K (the warm path is done with it).
+  // Not converged within the basis capacity (or breakdown below r): the
+  // Householder path below (K reloaded into shared memory when it was
+  // overwritten).
+  bool lz_done = false;
+  if (!warm_ok && crank == 0 && ea.lz_mcap[mi] > 0) {
     const int mcap = ea.lz_mcap[mi];
-    double* V = eig_smem + ea.lz_off[mi];        // s x (mcap + 1), column k at V + k s
-    double* hv = V + (size_t)s * (mcap + 1);     // mcap + 1 projection coefficients
+    double* V = full ? eig_smem + ea.lz_off[mi] : A;   // s x (mcap + 1), column k at V + k s
+    double* hv = full ? V + (size_t)s * (mcap + 1) : yy;   // mcap + 1 projection coefficients
     double* al = dd;                             // T_m diagonal
     double* be = ed;                             // T_m off-diagonal; be[m-1] = the residual norm
     double kn2 = 0.0;                            // ||K||_F^2 (breakdown scale)
-    for (int e = tid; e < s * s; e += blockDim.x) {
-      const double v = A[(e / s) * ld + (e % s)];
-      kn2 = fma(v, v, kn2);
+    if (full) {
+      for (int e = tid; e < s * s; e += blockDim.x) {
+        const double v = A[(e / s) * ld + (e % s)];
+        kn2 = fma(v, v, kn2);
+      }
+    } else {
+      for (int i = wid; i < s; i += nw)
+        for (int c = lane; c <= i; c += 32) {
+          const double v = Kg[pk(i, c)];
+          kn2 = fma(v, v * (c == i ? 1.0 : 2.0), kn2);
+        }
     }
+    __syncthreads();   // (packed: every thread is done reading K before the basis overwrites it)
     double v0 = 0.0;
     for (int i = tid; i < s; i += blockDim.x) {
       const double h = hash_unit(0x5DEECE66DULL ^ ((unsigned long long)i * 0x9E3779B9ULL));
@@ -1071,13 +1076,20 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
     for (int j = 0; j < mcap && !conv; ++j) {
       const double* vj = V + (size_t)j * s;
       double* w = V + (size_t)(j + 1) * s;
-      // w = K v_j: rows by groups of EIG_TPR threads (512 / 4 = 128 >= s rows)
-      {
-        const int i = tid / EIG_TPR, sub = tid & (EIG_TPR - 1);
+      // w = K v_j: rows by groups of EIG_TPR threads (128 groups; packed: K from L2)
+      for (int ib = 0; ib < s; ib += (int)blockDim.x / EIG_TPR) {
+        const int i = ib + tid / EIG_TPR, sub = tid & (EIG_TPR - 1);
         double acc = 0.0;
         if (i < s) {
-          const double* row = A + i * ld;
-          for (int c = sub; c < s; c += EIG_TPR) acc = fma(row[c], vj[c], acc);
+          if (full) {
+            const double* row = A + i * ld;
+            for (int c = sub; c < s; c += EIG_TPR) acc = fma(row[c], vj[c], acc);
+          } else {
+            const double* row = Kg + pk(i, 0);
+            for (int c = sub; c <= i; c += EIG_TPR) acc = fma(__ldg(row + c), vj[c], acc);
+            int c = i + 1 + ((sub - (i + 1)) & (EIG_TPR - 1));
+            for (; c < s; c += EIG_TPR) acc = fma(__ldg(Kg + pk(c, i)), vj[c], acc);
+          }
         }
 #pragma unroll
         for (int o = EIG_TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1141,10 +1153,24 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
       }
       if (tid == 0 && ea.fast_used) ea.fast_used[mi] = -m;   // (diagnostic: Lanczos steps, negated)
       if (tm && tid == 0) tm[6] = clock64();
-      return;
+      lz_done = true;
+    } else if (!full) {
+      __syncthreads();   // the basis overwrote the packed K: reload it for the Householder path
+      for (int i = tid; i < npk; i += blockDim.x) A[i] = Kg[i];
     }
     __syncthreads();
   }
+
+  warm_ok |= lz_done;
+  if (use_cl) {   // tell the helper CTAs whether the full path runs (scal[20] of every CTA)
+    __syncthreads();
+    if (crank == 0 && tid == 0)
+      for (int c2 = 0; c2 < EIG_CLUSTER; ++c2) eig_put<EIG_CLUSTER>(scal + 20, c2, warm_ok ? 1.0 : 0.0);
+    cg::this_cluster().sync();                                     // S0
+    warm_ok = scal[20] != 0.0;
+  }
+  if (warm_ok) return;   // (warm path or Lanczos)
+  if (crank == 0 && tid == 0 && ea.fast_used) ea.fast_used[mi] = 0;
 
   // ---------------------------------------------------------------- 1. tridiagonalise
   int hoff = 0;
