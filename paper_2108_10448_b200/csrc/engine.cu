@@ -1418,7 +1418,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
       const int mcap = lz ? eig_lz_mcap(sm, rm, base, ea.full[m]) : 0;
       ea.lz_mcap[m] = mcap;
       ea.lz_off[m] = (int)base;
-      if (mcap && ea.full[m]) esm = std::max(esm, (int)((base + (long long)sm * (mcap + 1) + mcap + 1 + 8) * 8));
+      if (mcap && ea.full[m]) esm = std::max(esm, (int)((base + (long long)sm * (mcap + 1) + 2 * (mcap + 1) + 8) * 8));
     }
   }
   ea.tmark = e->at<long long>(P.o_dbg);

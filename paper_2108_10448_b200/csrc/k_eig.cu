@@ -84,7 +84,7 @@ __host__ __device__ inline int eig_lz_mcap(int s, int r, long long base_doubles,
   if (s < 64 || s > 256 || (full && s > 128)) return 0;
   // full storage: after the base layout; packed: over the shared-memory copy of K
   const long long avail = full ? EIG_SMEM_DOUBLES - base_doubles - 8 : (long long)s * (s + 1) / 2;
-  long long m = full ? avail / (s + 1) - 1 : avail / s - 1;
+  long long m = full ? avail / (s + 2) - 1 : avail / s - 1;   // full: basis + 2 coefficient vectors
   m = m < EIG_LZ_MMAX ? m : EIG_LZ_MMAX;
   m = m < s - 1 ? m : s - 1;
   return m >= (3 * r > 12 ? 3 * r : 12) ? (int)m : 0;
@@ -1033,9 +1033,10 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
   // overwritten).
   bool lz_done = false;
   if (!warm_ok && crank == 0 && ea.lz_mcap[mi] > 0) {
+    if (tm && tid == 0) tm[2] = clock64();
     const int mcap = ea.lz_mcap[mi];
     double* V = full ? eig_smem + ea.lz_off[mi] : A;   // s x (mcap + 1), column k at V + k s
-    double* hv = full ? V + (size_t)s * (mcap + 1) : yy;   // mcap + 1 projection coefficients
+    double* hv = full ? V + (size_t)s * (mcap + 1) : yy;   // 2 (mcap + 1) projection coefficients (yy, ww adjacent)
     double* al = dd;                             // T_m diagonal
     double* be = ed;                             // T_m off-diagonal; be[m-1] = the residual norm
     double kn2 = 0.0;                            // ||K||_F^2 (breakdown scale)
@@ -1083,7 +1084,14 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
         if (i < s) {
           if (full) {
             const double* row = A + i * ld;
-            for (int c = sub; c < s; c += EIG_TPR) acc = fma(row[c], vj[c], acc);
+            double acc1 = 0.0;
+            int c = sub;
+            for (; c + EIG_TPR < s; c += 2 * EIG_TPR) {
+              acc = fma(row[c], vj[c], acc);
+              acc1 = fma(row[c + EIG_TPR], vj[c + EIG_TPR], acc1);
+            }
+            if (c < s) acc = fma(row[c], vj[c], acc);
+            acc += acc1;
           } else {
             const double* row = Kg + pk(i, 0);
             for (int c = sub; c <= i; c += EIG_TPR) acc = fma(__ldg(row + c), vj[c], acc);
@@ -1096,38 +1104,75 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
         if (i < s && sub == 0) w[i] = acc;
       }
       __syncthreads();
-      // CGS2 against v_0..v_j; alpha_j = v_j^T K v_j from the two passes
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int k = wid; k <= j; k += nw) {
-          const double* vk = V + (size_t)k * s;
-          double d = 0.0;
-          for (int t = lane; t < s; t += 32) d = fma(vk[t], w[t], d);
-          d = warp_sum(d);
-          if (lane == 0) hv[k] = d;
-        }
-        __syncthreads();
-        if (tid == 0) al[j] = pass == 0 ? hv[j] : al[j] + hv[j];
+      // CGS2 against v_0..v_j; alpha_j = v_j^T K v_j from the two passes.  The
+      // second pass also reduces ||w1||^2, so beta^2 = ||w1||^2 - ||h2||^2 (V
+      // orthonormal) and the second update and the normalisation share one sweep;
+      // under heavy cancellation (beta^2 < 0.01 ||w1||^2) beta is recomputed from
+      // the updated vector instead.
+      for (int k = wid; k <= j; k += nw) {
+        const double* vk = V + (size_t)k * s;
+        double d = 0.0;
+        for (int t = lane; t < s; t += 32) d = fma(vk[t], w[t], d);
+        d = warp_sum(d);
+        if (lane == 0) hv[k] = d;
+      }
+      __syncthreads();
+      if (tid == 0) al[j] = hv[j];
+      for (int t = tid; t < s; t += blockDim.x) {
+        double v = w[t];
+        for (int k = 0; k <= j; ++k) v = fma(-hv[k], V[(size_t)k * s + t], v);
+        w[t] = v;
+      }
+      __syncthreads();
+      double* h2 = hv + (mcap + 1);   // (second-pass coefficients; hv has 2 (mcap + 1) doubles)
+      for (int k = wid; k <= j; k += nw) {
+        const double* vk = V + (size_t)k * s;
+        double d = 0.0;
+        for (int t = lane; t < s; t += 32) d = fma(vk[t], w[t], d);
+        d = warp_sum(d);
+        if (lane == 0) h2[k] = d;
+      }
+      {
+        double nn = 0.0;
+        for (int t = tid; t < s; t += blockDim.x) nn = fma(w[t], w[t], nn);
+        nn = warp_sum(nn);
+        if (lane == 0) red2[wid] = nn;
+      }
+      __syncthreads();
+      if (tid == 0) al[j] += h2[j];
+      const double n1 = warp_sum_of(red2, nw);
+      double hh = 0.0;
+      for (int k = 0; k <= j; ++k) hh = fma(h2[k], h2[k], hh);
+      double b;
+      if (n1 - hh >= 0.01 * n1) {
+        b = sqrt(n1 - hh);
+        const double bi = b > 0.0 ? 1.0 / b : 0.0;
         for (int t = tid; t < s; t += blockDim.x) {
           double v = w[t];
-          for (int k = 0; k <= j; ++k) v = fma(-hv[k], V[(size_t)k * s + t], v);
+          for (int k = 0; k <= j; ++k) v = fma(-h2[k], V[(size_t)k * s + t], v);
+          w[t] = v * bi;
+        }
+        __syncthreads();
+      } else {
+        for (int t = tid; t < s; t += blockDim.x) {
+          double v = w[t];
+          for (int k = 0; k <= j; ++k) v = fma(-h2[k], V[(size_t)k * s + t], v);
           w[t] = v;
         }
         __syncthreads();
+        double nn = 0.0;
+        for (int t = tid; t < s; t += blockDim.x) nn = fma(w[t], w[t], nn);
+        nn = warp_sum(nn);
+        if (lane == 0) red[wid] = nn;
+        __syncthreads();
+        b = sqrt(warp_sum_of(red, nw));
+        const double bi = b > 0.0 ? 1.0 / b : 0.0;
+        for (int t = tid; t < s; t += blockDim.x) w[t] *= bi;
+        __syncthreads();
       }
-      double nn = 0.0;
-      for (int t = tid; t < s; t += blockDim.x) nn = fma(w[t], w[t], nn);
-      nn = warp_sum(nn);
-      if (lane == 0) red[wid] = nn;
-      __syncthreads();
-      const double b = sqrt(warp_sum_of(red, nw));
       m = j + 1;
       const bool brk = !(b > 1e-13 * knorm);   // invariant subspace: T_m is exact
       if (tid == 0) be[j] = brk ? 0.0 : b;
-      if (!brk) {
-        const double bi = 1.0 / b;
-        for (int t = tid; t < s; t += blockDim.x) w[t] *= bi;
-      }
-      __syncthreads();
       if (brk && m < r) break;   // fewer than r directions: the Householder path
       if (brk || m == mcap || (m >= first_chk && (m - first_chk) % 8 == 0)) {
         if (tid == 0) eig_tri_bounds(al, be, m, scal);
@@ -1152,7 +1197,7 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
         Eo[e] = acc;
       }
       if (tid == 0 && ea.fast_used) ea.fast_used[mi] = -m;   // (diagnostic: Lanczos steps, negated)
-      if (tm && tid == 0) tm[6] = clock64();
+      if (tm && tid == 0) tm[3] = clock64();   // (eig_paths: span 2 = the Lanczos solve)
       lz_done = true;
     } else if (!full) {
       __syncthreads();   // the basis overwrote the packed K: reload it for the Householder path
