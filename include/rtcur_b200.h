@@ -129,6 +129,20 @@ int rtcur_engine_iterate(rtcur_engine* e, double zeta, int first, double* sums, 
  * then wait for it (lets the host draw the next RTCUR-R sample while the GPU works) */
 int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first);
 int rtcur_engine_iterate_wait(rtcur_engine* e, double* sums, int* flags);
+/* Speculative pipelining of the stop rule (solver.py:357-358, `if err <= cfg.eps: break`).
+ * With a tolerance set (rtcur_engine_set_eps) every iteration ends with a device-side
+ * evaluation of the reference's stop test on its own sums; rtcur_engine_last_stop
+ * returns it for the iteration waited for last.  When rtcur_engine_can_speculate is 1,
+ * iterate_async may be called ONCE more while an iteration is still in flight: the
+ * second iteration is enqueued right behind the first, so the stream never idles over
+ * the host's round trip; every kernel of an iteration tests the stop flag first, so
+ * the second one runs nothing if the first met the stop rule.  iterate_wait always waits for the oldest
+ * iteration in flight; after a stop, rtcur_engine_iterate_cancel drops the speculative
+ * one and the engine's exportable iterate is again the one that stopped. */
+int rtcur_engine_set_eps(rtcur_engine* e, double eps);
+int rtcur_engine_can_speculate(rtcur_engine* e);
+int rtcur_engine_last_stop(rtcur_engine* e);
+int rtcur_engine_iterate_cancel(rtcur_engine* e);
 
 /* Export (device outputs, caller-allocated, fp64), for the iterate of the last
  * rtcur_engine_iterate call:

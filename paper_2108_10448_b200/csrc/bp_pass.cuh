@@ -370,6 +370,7 @@ __device__ __forceinline__ void bp_tile_r(const BPTile& T, bool cols, double& e2
 // assignment is static).  GP: the G pass over the core block's tiles only.
 template <bool HS, bool HE, bool WM, bool EXP, bool GP, int RB, bool AP>
 __global__ void __launch_bounds__(AP ? 512 : 256, AP ? 1 : BP_MIN_CTAS) k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeom G) {
+  if (rt_stopped(g.stop)) return;
   extern __shared__ __align__(128) unsigned char bp_smem[];
   __shared__ unsigned long long bars[4];
   __shared__ double red[16];

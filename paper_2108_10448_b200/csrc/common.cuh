@@ -83,7 +83,16 @@ struct Geom {
   i64 state_doubles;             // size of one state (G + A + W)
   BlockDesc blk[RT_MAX_BLOCKS];
   i64 nblk_total;                // sum of P*Q
+  const int* stop;               // iteration launches: the engine's stop flag (kernels of an
+                                 // iteration enqueued behind one that met the stop rule return at
+                                 // once); null for every other launch
 };
+
+// An iteration's kernels start with this test: all threads read the same word, so the
+// whole grid leaves before any barrier / mbarrier is touched.
+__device__ __forceinline__ bool rt_stopped(const int* stop) {
+  return stop != nullptr && *reinterpret_cast<const volatile int*>(stop) != 0;
+}
 
 // Pointers to the per-mode index data on the device.
 struct IndexPtrs {

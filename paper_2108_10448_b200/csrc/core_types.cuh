@@ -24,6 +24,7 @@ struct CoreLaunch {
   double* partial;         // error pass: [cta][2]
   double* sums;            // error pass: sums[0] = sum (x - L - S)^2, sums[1] = sum x^2 of the core
   unsigned int* counter;   // error pass: last-CTA ticket
+  const int* stop;         // the engine's stop flag (iteration launches), or null
   int nbuf;                // x runs per warp (set by the launcher): 1, or 2 (double-buffered)
 };
 

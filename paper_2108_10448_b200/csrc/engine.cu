@@ -497,7 +497,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.samp_delta = o - samp0;
   take(P.samp_delta - 8);   // slot 1 (aligned like slot 0)
   P.o_state = take(3 * g.state_doubles * 8);
-  P.o_zeta = take(8);
+  P.o_zeta = take(32);   // zeta | eps | stop flag
   for (int m = 0; m < n; ++m) P.o_M[m] = take(row_sizes[m] * col_sizes[m] * 8);
   P.o_gpart = take((i64)n * P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
   for (int m = 0; m < n; ++m) {
@@ -529,7 +529,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     P.o_sums = res0;
     P.o_flags = res0 + 2 * g.nblk * 8;
     P.o_nonfinite = P.o_flags + ((n * 4 + 7) & ~7LL);
-    P.res_bytes = 2 * g.nblk * 8 + ((n * 4 + 7) & ~7LL) + 4;
+    P.res_bytes = 2 * g.nblk * 8 + ((n * 4 + 7) & ~7LL) + 8;   // (+ the stop flag's copy)
   }
   P.o_counters = take(64 * 4);
   P.o_absmax = take(8);
@@ -580,10 +580,20 @@ struct ProfPair {
   cudaEvent_t b, e;
   bool owned;   // from the engine's event pool (returned at flush); graph-owned events are reused
 };
+// An iteration is captured as a short list of graph segments.  A segment ends where
+// the stream needs an event between graphs: the begin / end of a profiled phase, or
+// the point where the eigensolver starts (eig_ev: the side-stream prefetch of the next
+// sample waits for it).  (Gating the segments with conditional IF nodes on the stop
+// flag was measured at ~50 us per iteration on B200 -- more than the host round trip
+// it hides -- so the kernels test the flag themselves, Geom::stop / rt_stopped.)
+enum { CUT_NONE = 0, CUT_PROF_BEGIN, CUT_PROF_END, CUT_EIG };
+struct GraphSeg {
+  cudaGraphExec_t exec = nullptr;   // null: nothing was captured before the cut
+  int cut = CUT_NONE, ph = 0;       // event to record after the segment
+};
 struct GraphEntry {
-  cudaGraphExec_t exec = nullptr;
+  std::vector<GraphSeg> segs;
   unsigned long long nkernels = 0;   // kernel launches captured (counted at every replay)
-  std::vector<ProfPair> prof;      // event-record nodes of the profiled phases
 };
 
 struct ShardState;   // shard_xchg.cu
@@ -599,9 +609,19 @@ struct rtcur_engine {
   int act, stg;     // sample slots: active (iterations, exports) and staged (next set_sample/gather), -1: none
   int sample_epoch; // bumped whenever a staged sample becomes active
   int w_epoch[3];   // sample epoch each slot's W (column weights) was built for
-  bool pending;     // an iterate_async awaits its iterate_wait
+  int npending;     // iterate_async calls awaiting their iterate_wait (2: one speculative)
   bool use_fast;    // allow the warm-started subspace-iteration eigensolver
-  cudaEvent_t done; // recorded after the iteration's result copies
+  cudaEvent_t done[2];   // recorded after the iteration's result copies (by launch parity)
+  int par;          // parity of the next launch: pinned zeta / result slot, done event
+  int pend_par[2];  // parities of the launches in flight, oldest first
+  int last_stop;    // stop flag the device computed for the iteration waited for last
+  double eps;       // stop tolerance of the device-side stop rule (<= 0: never stops)
+  // speculation (rtcur_engine_iterate_async while one iteration is in flight): the
+  // bookkeeping before the speculative launch, restored by rtcur_engine_iterate_cancel
+  bool spec_ok;     // speculative launches allowed (RTCUR_SPEC=0 disables them)
+  struct Snap { int cur, prev, act, stg, sample_epoch, w_epoch[3]; double zeta_last; bool xi_valid[2]; } snap;
+  bool snap_valid;
+  size_t snap_prof;  // prof_pending entries before the speculative launch
   int prev;         // ring slot of the one before (-1: none, i.e. latest is iteration 1)
   double zeta_last;
   bool sampled;
@@ -624,6 +644,7 @@ struct rtcur_engine {
   cudaStream_t cap_st;             // private stream the iteration is captured on
   std::map<unsigned long long, GraphEntry>* graphs;
   GraphEntry* cap_entry;
+  int cap_err;                     // first error inside a capture cut (prof_begin/prof_end are void)
   const double* zetap_cur;         // device zeta while an iteration body is enqueued/captured
   bool xi_valid[2];                // the sample slot's intersection copies match its blocks
   cudaEvent_t absmax_ev;           // rtcur_engine_absmax_begin's D2H done
@@ -658,24 +679,79 @@ static cudaEvent_t prof_event(rtcur_engine* e) {
   cudaEventCreate(&ev);
   return ev;
 }
+// ---- graph segments (see GraphSeg)
+// the device control words: [zeta (double) | eps (double) | stop (int)] at o_zeta
+static inline int* stop_flag(const rtcur_engine* e) { return e->at<int>(e->P.o_zeta + 16); }
+
+static cudaError_t seg_begin(rtcur_engine* e) {
+  return cudaStreamBeginCapture(e->cap_st, cudaStreamCaptureModeThreadLocal);
+}
+
+// close the segment being captured: instantiate it (unless empty) and note the event
+// the stream records after it
+static cudaError_t seg_end(rtcur_engine* e, int cut, int ph) {
+  cudaGraph_t cap = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(e->cap_st, &cap);
+  GraphSeg sg;
+  sg.cut = cut;
+  sg.ph = ph;
+  if (ce == cudaSuccess && cap) {
+    size_t nn = 0;
+    ce = cudaGraphGetNodes(cap, nullptr, &nn);
+    if (ce == cudaSuccess && nn > 0) ce = cudaGraphInstantiate(&sg.exec, cap, 0);
+  }
+  if (cap) cudaGraphDestroy(cap);
+  if (ce == cudaSuccess) e->cap_entry->segs.push_back(sg);
+  return ce;
+}
+
+static void cap_cut(rtcur_engine* e, int cut, int ph) {
+  if (e->cap_err != (int)cudaSuccess) return;
+  cudaError_t ce = seg_end(e, cut, ph);
+  if (ce == cudaSuccess) ce = seg_begin(e);
+  e->cap_err = (int)ce;
+}
+
 static void prof_begin(rtcur_engine* e, int ph) {
   if (!e->prof_on || !((e->prof_mask >> ph) & 1u)) return;
+  if (e->capturing) {   // the event goes between two graph segments
+    cap_cut(e, CUT_PROF_BEGIN, ph);
+    return;
+  }
   cudaEvent_t ev = prof_event(e);
-  if (e->capturing) cudaEventRecordWithFlags(ev, e->st, cudaEventRecordExternal);
-  else cudaEventRecord(ev, e->st);
+  cudaEventRecord(ev, e->st);
   e->prof_open[ph] = ev;
 }
 static void prof_end(rtcur_engine* e, int ph) {
-  if (!e->prof_on || !e->prof_open[ph]) return;
-  cudaEvent_t ev = prof_event(e);
+  if (!e->prof_on) return;
   if (e->capturing) {
-    cudaEventRecordWithFlags(ev, e->st, cudaEventRecordExternal);
-    e->cap_entry->prof.push_back({ph, e->prof_open[ph], ev, false});
-  } else {
-    cudaEventRecord(ev, e->st);
-    e->prof_pending->push_back({ph, e->prof_open[ph], ev, true});
+    if ((e->prof_mask >> ph) & 1u) cap_cut(e, CUT_PROF_END, ph);
+    return;
   }
+  if (!e->prof_open[ph]) return;
+  cudaEvent_t ev = prof_event(e);
+  cudaEventRecord(ev, e->st);
+  e->prof_pending->push_back({ph, e->prof_open[ph], ev, true});
   e->prof_open[ph] = nullptr;
+}
+// replay a captured iteration: its segments with the events between them
+static int launch_entry(rtcur_engine* e, GraphEntry& ge) {
+  for (auto& sg : ge.segs) {
+    if (sg.exec) CK(cudaGraphLaunch(sg.exec, e->st));
+    if (sg.cut == CUT_PROF_BEGIN) {
+      cudaEvent_t ev = prof_event(e);
+      CK(cudaEventRecord(ev, e->st));
+      e->prof_open[sg.ph] = ev;
+    } else if (sg.cut == CUT_PROF_END && e->prof_open[sg.ph]) {
+      cudaEvent_t ev = prof_event(e);
+      CK(cudaEventRecord(ev, e->st));
+      e->prof_pending->push_back({sg.ph, e->prof_open[sg.ph], ev, true});
+      e->prof_open[sg.ph] = nullptr;
+    } else if (sg.cut == CUT_EIG) {
+      CK(cudaEventRecord(e->eig_ev, e->st));
+    }
+  }
+  return RT_OK;
 }
 // after a stream synchronisation: fold the completed intervals into the totals;
 // intervals still in flight (work enqueued behind the synchronisation point, e.g.
@@ -818,9 +894,14 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->prof_mask = ~0u;
   e->use_fast = getenv("RTCUR_NO_FAST_EIG") == nullptr;
   e->prof_pool = new std::vector<cudaEvent_t>();
-  if (cudaEventCreateWithFlags(&e->done, cudaEventDisableTiming) != cudaSuccess) {
+  if (cudaEventCreateWithFlags(&e->done[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->done[1], cudaEventDisableTiming) != cudaSuccess) {
     delete e;
     return fail(RT_ERR_CUDA, "cudaEventCreate");
+  }
+  {
+    const char* sv = getenv("RTCUR_SPEC");
+    e->spec_ok = !(sv && sv[0] == '0');
   }
   e->prof_pending = new std::vector<ProfPair>();
   e->graphs = new std::map<unsigned long long, GraphEntry>();
@@ -853,10 +934,10 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&e->idx_ev[s], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->absmax_ev, cudaEventDisableTiming));
   {
-    // off by default: measured neutral at config 1 (the host, not the stream, paces
-    // it) and +4..8 % at config 4; RTCUR_SIDE_PREFETCH=1 enables it
+    // on by default (with the speculative pipeline: config 1 +5 %, config 4 +12 %,
+    // DESIGN.md §6); RTCUR_SIDE_PREFETCH=0 keeps the staging in stream order
     const char* sv = getenv("RTCUR_SIDE_PREFETCH");
-    e->use_side = sv && sv[0] == '1';
+    e->use_side = !(sv && sv[0] == '0');
   }
   CK(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&e->pre_ev, cudaEventDisableTiming));
@@ -881,7 +962,8 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   shard_free(e);
   if (e->h_pinned) cudaFreeHost(e->h_pinned);
   if (e->h_idx) cudaFreeHost(e->h_idx);
-  if (e->done) cudaEventDestroy(e->done);
+  for (int s = 0; s < 2; ++s)
+    if (e->done[s]) cudaEventDestroy(e->done[s]);
   if (e->absmax_ev) cudaEventDestroy(e->absmax_ev);
   for (int s = 0; s < 2; ++s)
     if (e->idx_ev[s]) cudaEventDestroy(e->idx_ev[s]);
@@ -894,13 +976,9 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
     delete e->prof_pending;
   }
   if (e->graphs) {
-    for (auto& kv : *e->graphs) {
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-      for (auto& p : kv.second.prof) {
-        cudaEventDestroy(p.b);
-        cudaEventDestroy(p.e);
-      }
-    }
+    for (auto& kv : *e->graphs)
+      for (auto& sg : kv.second.segs)
+        if (sg.exec) cudaGraphExecDestroy(sg.exec);
     delete e->graphs;
   }
   if (e->cap_st) cudaStreamDestroy(e->cap_st);
@@ -1004,7 +1082,7 @@ struct SideScope {
 
 extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* rows, const int64_t* const* cols) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
-  if (e->pending && e->use_side && !e->shard && !e->staging_on_side && e->use_graphs) {
+  if (e->npending > 0 && e->use_side && !e->shard && !e->staging_on_side && e->use_graphs) {
     e->staging_on_side = true;
     // eig_ev is recorded inside the running iteration (after pre_ev): waiting for it
     // also covers every earlier reader of the slot being refilled
@@ -1199,6 +1277,7 @@ static CoreLaunch make_cl(rtcur_engine* e, const double* st_s, double zeta, cons
   const Geom& g = P.g;
   CoreLaunch cl;
   memset(&cl, 0, sizeof(cl));
+  cl.stop = g.stop;
   cl.x = e->xb(e->act_slot()) + g.blk[0].off * P.esize;
   cl.dtype = P.dtype;
   cl.P = (int)g.blk[0].P;
@@ -1306,6 +1385,7 @@ static SvdArgs make_svd_args(rtcur_engine* e) {
   const Plan& P = e->P;
   SvdArgs sa;
   memset(&sa, 0, sizeof(sa));
+  sa.stop = P.g.stop;
   sa.n = P.g.n;
   for (int m = 0; m < P.g.n; ++m) {
     sa.s[m] = (int)P.s[m];
@@ -1367,6 +1447,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   const int n = P.g.n;
   GramArgs ga;
   memset(&ga, 0, sizeof(ga));
+  ga.stop = P.g.stop;
   ga.n = n;
   for (int m = 0; m < n; ++m) {
     ga.s[m] = (int)P.s[m];
@@ -1396,6 +1477,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
   prof_end(e, PH_GRAM);
   EigArgs ea;
   memset(&ea, 0, sizeof(ea));
+  ea.stop = P.g.stop;
   ea.n = n;
   int esm = 0;
   for (int m = 0; m < n; ++m) {
@@ -1445,8 +1527,11 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ea.warm_d[m] = P.g.dim[m];
   }
   // the next sample's prefetch (side stream) may start now: it overlaps the eigensolver
-  if (e->capturing) CK(cudaEventRecordWithFlags(e->eig_ev, e->st, cudaEventRecordExternal));
-  else CK(cudaEventRecord(e->eig_ev, e->st));
+  if (e->capturing) {
+    if (e->use_side) cap_cut(e, CUT_EIG, 0);
+  } else {
+    CK(cudaEventRecord(e->eig_ev, e->st));
+  }
   prof_begin(e, PH_EIG);
   if (int st = launch_eig(ea, P.s, n, esm, e->st)) return st;
   prof_end(e, PH_EIG);
@@ -1489,7 +1574,7 @@ static int run_wchain(rtcur_engine* e, const double* sto, const int* const* rows
     double* out = (m == n - 1) ? dst : (in == t0 ? t1 : t0);
     const i64 total = rho * Pm[m] * beta;
     k_modeprod_fwd<<<(unsigned)std::min<i64>(cdiv(total, 256), 148 * 16), 256, 0, e->st>>>(
-        in, out, sto + g.a_off[m], rows ? rows[m] : nullptr, g.dim[m], rho, Pm[m], g.rank[m], beta);
+        in, out, sto + g.a_off[m], rows ? rows[m] : nullptr, g.dim[m], rho, Pm[m], g.rank[m], beta, g.stop);
     LAUNCH_CHECK();
     rho *= Pm[m];
     in = out;
@@ -1700,7 +1785,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
       double* out = (m == n - 1) ? sto : (in == t0 ? t1 : t0);
       const i64 total = rho * g.rank[m] * beta;
       k_modeprod<<<(unsigned)std::min<i64>(cdiv(total * 32, 256), 4096), 256, 0, e->st>>>(
-          in, out, e->at<double>(P.o_U[m]), rho, (int)g.nrows[m], g.rank[m], beta);
+          in, out, e->at<double>(P.o_U[m]), rho, (int)g.nrows[m], g.rank[m], beta, g.stop);
       LAUNCH_CHECK();
       rho *= g.rank[m];
       in = out;
@@ -1711,13 +1796,34 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   return run_wcols(e, sto);   // (w_epoch of the new slot is set by the caller)
 }
 
-// The launch sequence of one iteration (captured into a CUDA graph per launch
+// Device-side stop rule: the sampled relative error from the per-block sums, in the
+// host's own operation order (solver._error_from_sums: sum of block norms over sum of
+// block norms, IEEE sqrt / divide), against eps.  Sets the engine's stop flag -- the kernels
+// of an iteration enqueued behind this one then return at once -- and its copy in the
+// result range the host reads.
+static __global__ void k_stop_check(const double* sums, int nblk, const double* ctl, int* stop, int* stop_copy) {
+  if (threadIdx.x != 0 || *reinterpret_cast<volatile int*>(stop)) return;   // (a cancelled iteration keeps the flag)
+  double num = 0.0, den = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    num += sqrt(sums[2 * b]);
+    den += sqrt(sums[2 * b + 1]);
+  }
+  const double err = den == 0.0 ? (num == 0.0 ? 0.0 : __longlong_as_double(0x7ff0000000000000LL)) : num / den;
+  const double eps = ctl[1];
+  const int s = (eps > 0.0 && err <= eps) ? 1 : 0;
+  *stop = s;
+  *stop_copy = s;
+}
+
+#define RES_SLOT 96   // doubles between the two result slots in h_pinned (zeta/eps slots at 200 + 4 par)
+
+// The launch sequence of one iteration (captured into CUDA graph segments per launch
 // shape).  Pure stream work: host-side bookkeeping stays in the caller.
-static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool reeval) {
+static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool reeval, int par) {
   const Plan& P = e->P;
   const int n = P.g.n;
   const double zeta = e->zeta_last;   // (kernels read the device copy when zetap_cur is set)
-  CK(cudaMemcpyAsync(e->ws + P.o_zeta, e->h_pinned + 200, 8, cudaMemcpyHostToDevice, e->st));
+  CK(cudaMemcpyAsync(e->ws + P.o_zeta, e->h_pinned + 200 + 4 * par, 16, cudaMemcpyHostToDevice, e->st));
   CK(cudaMemsetAsync(e->ws + P.o_nonfinite, 0, 4, e->st));
   int st;
   // RTCUR-R: the sample moved, re-evaluate the previous iterate on it
@@ -1730,11 +1836,14 @@ static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool r
   if ((st = run_block_pass(e, st_s, e->state(newslot), zeta, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
     return st;
   (void)n;
-  CK(cudaMemcpyAsync(e->h_pinned, e->ws + P.o_sums, P.res_bytes, cudaMemcpyDeviceToHost, e->st));
+  k_stop_check<<<1, 32, 0, e->st>>>(e->at<double>(P.o_sums), P.g.nblk, e->at<double>(P.o_zeta), stop_flag(e),
+                                    e->at<int>(P.o_nonfinite + 4));
+  LAUNCH_CHECK();
+  CK(cudaMemcpyAsync(e->h_pinned + par * RES_SLOT, e->ws + P.o_sums, P.res_bytes, cudaMemcpyDeviceToHost, e->st));
   return RT_OK;
 }
 
-// phases timed inside the iteration body (a graph's event nodes depend only on these)
+// phases timed inside the iteration body (they cut its graph into segments)
 static const unsigned kIterPhases = (1u << PH_THRESH) | (1u << PH_GRAM) | (1u << PH_EIG) | (1u << PH_SVDPOST) |
                                     (1u << PH_APASS) | (1u << PH_GPASS) | (1u << PH_WCOLS) | (1u << PH_ERROR);
 
@@ -1742,10 +1851,66 @@ static inline bool fiber_refresh_pending(const rtcur_engine* e) {
   return e->P.fiber_mask && !e->xi_valid[e->act_slot()];
 }
 
+// capture one iteration into `ge`
+static int capture_iteration(rtcur_engine* e, GraphEntry& ge, const double* st_s, int newslot, bool reeval, int par) {
+  e->cap_entry = &ge;
+  e->cap_err = (int)cudaSuccess;
+  cudaStream_t saved = e->st;
+  e->st = e->cap_st;
+  e->capturing = true;
+  const unsigned long long l0 = rtcur_launch_counter_add(0);
+  int st = RT_OK;
+  cudaError_t ce = seg_begin(e);
+  if (ce == cudaSuccess) {
+    st = iterate_body(e, st_s, newslot, reeval, par);
+    ge.nkernels = rtcur_launch_counter_add(0) - l0;
+    g_launches.fetch_sub(ge.nkernels);   // capturing executes nothing
+    ce = seg_end(e, CUT_NONE, 0);
+    if (ce == cudaSuccess) ce = (cudaError_t)e->cap_err;
+  }
+  e->capturing = false;
+  e->st = saved;
+  e->cap_entry = nullptr;
+  if (ce != cudaSuccess || st != RT_OK) {
+    cudaGraph_t junk = nullptr;
+    cudaStreamEndCapture(e->cap_st, &junk);   // leave no capture open
+    if (junk) cudaGraphDestroy(junk);
+    cudaGetLastError();
+    for (auto& sg : ge.segs)
+      if (sg.exec) cudaGraphExecDestroy(sg.exec);
+    ge.segs.clear();
+    if (st) return st;
+    return fail(RT_ERR_CUDA, std::string("iteration capture: ") + cudaGetErrorString(ce));
+  }
+  return RT_OK;
+}
+
+// (a sharded solve exchanges blocks between iterations from the host: one at a time)
+static inline bool can_speculate(const rtcur_engine* e) { return e->spec_ok && !e->shard; }
+
+extern "C" int rtcur_engine_can_speculate(rtcur_engine* e) { return e && can_speculate(e) ? 1 : 0; }
+
+extern "C" int rtcur_engine_set_eps(rtcur_engine* e, double eps) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  e->eps = eps;
+  return RT_OK;
+}
+
 extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first) {
   if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
-  if (e->pending) return fail(RT_ERR_VALUE, "previous iteration not waited for");
+  if (e->npending >= 2) return fail(RT_ERR_VALUE, "two iterations already in flight");
+  const bool spec = e->npending == 1;
+  if (spec && (first || !can_speculate(e))) return fail(RT_ERR_VALUE, "previous iteration not waited for");
   if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
+  if (spec) {   // what rtcur_engine_iterate_cancel restores
+    auto& sn = e->snap;
+    sn.cur = e->cur; sn.prev = e->prev; sn.act = e->act; sn.stg = e->stg; sn.sample_epoch = e->sample_epoch;
+    for (int i = 0; i < 3; ++i) sn.w_epoch[i] = e->w_epoch[i];
+    sn.zeta_last = e->zeta_last;
+    sn.xi_valid[0] = e->xi_valid[0]; sn.xi_valid[1] = e->xi_valid[1];
+    e->snap_valid = true;
+    e->snap_prof = e->prof_pending->size();
+  }
   if (e->staging_on_side) {   // the prefetched sample's staging must be complete
     CK(cudaStreamWaitEvent(e->st, e->side_ev, 0));
     e->staging_on_side = false;
@@ -1758,83 +1923,113 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   // everything before this iteration (the previous iteration, exports) is what a
   // prefetch into the other sample slot must wait for
   CK(cudaEventRecord(e->pre_ev, e->st));
-  if (first) e->cur = e->prev = -1;
+  if (first) {
+    e->cur = e->prev = -1;
+    CK(cudaMemsetAsync(stop_flag(e), 0, 4, e->st));   // a new solve: the previous one's stop flag
+  }
   const double* st_s = (e->cur >= 0) ? e->state(e->cur) : nullptr;
   int newslot = 0;
   while (newslot == e->cur || newslot == e->prev) ++newslot;
   const bool reeval = e->cur >= 0 && e->w_epoch[e->cur] != e->sample_epoch;
+  const int par = e->par;
   e->zeta_last = zeta;
-  e->h_pinned[200] = zeta;   // read by the iteration's first (memcpy) node
+  e->h_pinned[200 + 4 * par] = zeta;   // read by the iteration's first (memcpy) node
+  e->h_pinned[200 + 4 * par + 1] = e->eps;
   e->zetap_cur = e->at<double>(e->P.o_zeta);
   int st = RT_OK;
+  // the iteration's kernels test the stop flag (Geom::stop is copied into every launch)
+  e->P.g.stop = stop_flag(e);
   if (e->use_graphs) {
     const unsigned long long key = (unsigned long long)(e->cur + 1) | ((unsigned long long)newslot << 2) |
                                    ((unsigned long long)e->act_slot() << 4) | ((unsigned long long)reeval << 5) |
                                    ((unsigned long long)fiber_refresh_pending(e) << 6) |
-                                   ((unsigned long long)(e->prof_on ? (e->prof_mask & kIterPhases) : 0u) << 8);
+                                   ((unsigned long long)par << 7) |
+                                   ((unsigned long long)(e->prof_on ? (e->prof_mask & kIterPhases) : 0u) << 8) |
+                                   ((unsigned long long)e->use_side << 41);
     auto it = e->graphs->find(key);
     if (it == e->graphs->end()) {
       GraphEntry ge;
-      e->cap_entry = &ge;
-      cudaStream_t saved = e->st;
-      e->st = e->cap_st;
-      e->capturing = true;
-      const unsigned long long l0 = rtcur_launch_counter_add(0);
-      cudaError_t ce = cudaStreamBeginCapture(e->cap_st, cudaStreamCaptureModeThreadLocal);
-      if (ce == cudaSuccess) st = iterate_body(e, st_s, newslot, reeval);
-      ge.nkernels = rtcur_launch_counter_add(0) - l0;
-      g_launches.fetch_sub(ge.nkernels);   // capturing executes nothing
-      cudaGraph_t graph = nullptr;
-      const cudaError_t ce2 = cudaStreamEndCapture(e->cap_st, &graph);
-      e->capturing = false;
-      e->st = saved;
-      e->cap_entry = nullptr;
-      if (ce != cudaSuccess || ce2 != cudaSuccess || st != RT_OK) {
-        if (graph) cudaGraphDestroy(graph);
+      st = capture_iteration(e, ge, st_s, newslot, reeval, par);
+      if (st != RT_OK) {
         e->zetap_cur = nullptr;
-        if (st) return st;
-        return fail(RT_ERR_CUDA, std::string("iteration capture: ") + cudaGetErrorString(ce != cudaSuccess ? ce : ce2));
-      }
-      ce = cudaGraphInstantiate(&ge.exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ce != cudaSuccess) {
-        e->zetap_cur = nullptr;
-        return fail(RT_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ce));
+        e->P.g.stop = nullptr;
+        return st;
       }
       it = e->graphs->emplace(key, std::move(ge)).first;
     }
-    CK(cudaGraphLaunch(it->second.exec, e->st));
-    rtcur_launch_counter_add(it->second.nkernels);   // the graph's kernels run now
-    for (auto& p : it->second.prof) e->prof_pending->push_back(p);
-  } else {
-    st = iterate_body(e, st_s, newslot, reeval);
+    st = launch_entry(e, it->second);
     if (st) {
       e->zetap_cur = nullptr;
+      e->P.g.stop = nullptr;
+      return st;
+    }
+    rtcur_launch_counter_add(it->second.nkernels);   // the graph's kernels run now
+  } else {
+    st = iterate_body(e, st_s, newslot, reeval, par);
+    if (st) {
+      e->zetap_cur = nullptr;
+      e->P.g.stop = nullptr;
       return st;
     }
   }
   e->zetap_cur = nullptr;
-  CK(cudaEventRecord(e->done, e->st));
+  e->P.g.stop = nullptr;
+  CK(cudaEventRecord(e->done[par], e->st));
   if (reeval) e->w_epoch[e->cur] = e->sample_epoch;
   e->w_epoch[newslot] = e->sample_epoch;
   e->prev = e->cur;
   e->cur = newslot;
-  e->pending = true;
+  e->pend_par[e->npending++] = par;
+  e->par ^= 1;
   return RT_OK;
 }
 
 extern "C" int rtcur_engine_iterate_wait(rtcur_engine* e, double* sums, int* flags) {
-  if (!e || !e->pending) return fail(RT_ERR_VALUE, "no iteration in flight");
-  e->pending = false;
-  CK(cudaEventSynchronize(e->done));
+  if (!e || e->npending < 1) return fail(RT_ERR_VALUE, "no iteration in flight");
+  const int par = e->pend_par[0];
+  e->pend_par[0] = e->pend_par[1];
+  e->npending--;
+  CK(cudaEventSynchronize(e->done[par]));
   prof_flush(e);
   const Plan& P = e->P;
-  const char* hr = reinterpret_cast<const char*>(e->h_pinned);
+  const char* hr = reinterpret_cast<const char*>(e->h_pinned + par * RES_SLOT);
   int nonfinite;
   memcpy(&nonfinite, hr + (P.o_nonfinite - P.o_sums), 4);
+  memcpy(&e->last_stop, hr + (P.o_nonfinite + 4 - P.o_sums), 4);
   if (nonfinite) return fail(RT_ERR_VALUE, "truncated_svd input contains non-finite entries");
   if (sums) memcpy(sums, hr, 2 * P.g.nblk * 8);
   if (flags) memcpy(flags, hr + (P.o_flags - P.o_sums), P.g.n * 4);
+  return RT_OK;
+}
+
+// 1 when the device-side stop rule fired for the iteration waited for last (its
+// sampled relative error <= eps): a speculative iteration enqueued behind it ran nothing.
+extern "C" int rtcur_engine_last_stop(rtcur_engine* e) { return e ? e->last_stop : 0; }
+
+// Forget the speculative iteration (enqueued while its predecessor was in flight, after
+// that predecessor met the stop rule: its kernels returned at once): the engine's
+// bookkeeping returns to the predecessor, which stays the exportable iterate.
+extern "C" int rtcur_engine_iterate_cancel(rtcur_engine* e) {
+  if (!e || e->npending != 1 || !e->snap_valid) return fail(RT_ERR_VALUE, "no speculative iteration to cancel");
+  const auto& sn = e->snap;
+  e->cur = sn.cur; e->prev = sn.prev; e->act = sn.act; e->stg = sn.stg; e->sample_epoch = sn.sample_epoch;
+  for (int i = 0; i < 3; ++i) e->w_epoch[i] = sn.w_epoch[i];
+  e->zeta_last = sn.zeta_last;
+  e->xi_valid[0] = sn.xi_valid[0]; e->xi_valid[1] = sn.xi_valid[1];
+  e->snap_valid = false;
+  e->npending = 0;
+  // its profiled phases measured empty segments: drop them
+  while (e->prof_pending->size() > e->snap_prof) {
+    ProfPair p = e->prof_pending->back();
+    e->prof_pending->pop_back();
+    e->prof_pool->push_back(p.b);
+    e->prof_pool->push_back(p.e);
+  }
+  for (int ph = 0; ph < RT_NPHASE; ++ph)
+    if (e->prof_open[ph]) {
+      e->prof_pool->push_back(e->prof_open[ph]);
+      e->prof_open[ph] = nullptr;
+    }
   return RT_OK;
 }
 
@@ -1947,7 +2142,7 @@ extern "C" int rtcur_engine_debug_marks(rtcur_engine* e, int64_t* out, int n) {
 
 extern "C" int rtcur_engine_set_graphs(rtcur_engine* e, int on) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
-  if (e->pending) return fail(RT_ERR_VALUE, "iteration in flight");
+  if (e->npending) return fail(RT_ERR_VALUE, "iteration in flight");
   e->use_graphs = on != 0;
   return RT_OK;
 }

@@ -320,6 +320,7 @@ __global__ void k_block_pass(Geom g, TileMap tm, IndexPtrs ip, PassArgs a, BPGeo
 // A_k[p, a] = siginv_a * sum over the CTAs that touched block k+1 (CTA order) of the
 // A-pass partials.  One thread per output (consecutive outputs, consecutive partials).
 __global__ void __launch_bounds__(256) k_areduce_bp(Geom g, TileMap tm, PassArgs a, double* __restrict__ st_out) {
+  if (rt_stopped(g.stop)) return;
   const int b = blockIdx.y + 1;
   if (b >= g.nblk || tm.first[b + 1] == tm.first[b]) return;   // (no tiles: the fiber pass writes A_k)
   const BlockDesc& bd = g.blk[b];

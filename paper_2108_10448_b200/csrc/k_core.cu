@@ -45,6 +45,7 @@ __host__ __device__ inline size_t cp_fixed_bytes(int P, int R) {
 
 template <typename T, int R, bool HS, int MODE>
 __global__ void __launch_bounds__(CP_MAX_WARPS * 32, 3) k_core_pass(CoreLaunch c) {
+  if (rt_stopped(c.stop)) return;
   extern __shared__ __align__(16) unsigned char csm[];
   const int P = c.P, r = c.r;
   double* As = reinterpret_cast<double*>(csm);   // P x R: A_1^s rows (threshold state)

@@ -33,6 +33,7 @@ namespace cg = cooperative_groups;
 #define EIG_CLUSTER 8            // CTAs per mode for 128 < s <= 256 (register-tiled tridiagonalisation)
 
 struct EigArgs {
+  const int* stop;   // the engine's stop flag (iteration launches), or null
   int n;
   int s[RT_MAX_MODES];
   int r[RT_MAX_MODES];
@@ -939,6 +940,7 @@ __device__ __forceinline__ void eig_tri_bounds(const double* dd, const double* e
 }
 
 __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
+  if (rt_stopped(ea.stop)) return;   // (every CTA of every cluster: no cluster barrier is pending)
   // launched either one CTA per mode, or (some s > 128) as clusters of EIG_CLUSTER
   // CTAs per mode: the cluster's extra CTAs only join the register-tiled
   // tridiagonalisation of modes with 128 < s <= 256 (eig_tridiag_reg<4, ...>)

@@ -29,6 +29,7 @@ struct GPassArgs {
 // first contraction of the clean core with U~_1^T (warp per core column)
 template <int R>
 __global__ void __launch_bounds__(256) k_gpass(Geom g, IndexPtrs ip, GPassArgs a) {
+  if (rt_stopped(g.stop)) return;
   const BlockDesc bd = g.blk[0];
   const int r = bd.r;
   const int lane = threadIdx.x & 31;
@@ -59,7 +60,9 @@ __global__ void __launch_bounds__(256) k_gpass(Geom g, IndexPtrs ip, GPassArgs a
 // out = in x_m U_m^T on the small partially-contracted core:
 // in dims (r_1..r_{m-1}, |I_m|, |I_{m+1}|..), out dims (r_1..r_m, |I_{m+1}|..)
 __global__ void __launch_bounds__(256) k_modeprod(const double* __restrict__ in, double* __restrict__ out,
-                                                   const double* __restrict__ U, i64 rho, int Im, int rm, i64 beta_n) {
+                                                   const double* __restrict__ U, i64 rho, int Im, int rm, i64 beta_n,
+                                                   const int* __restrict__ stop) {
+  if (rt_stopped(stop)) return;
   const i64 total = rho * rm * beta_n;
   const int lane = threadIdx.x & 31;
   for (i64 e = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < total; e += ((i64)gridDim.x * blockDim.x) >> 5) {
@@ -82,7 +85,9 @@ __global__ void __launch_bounds__(256) k_modeprod(const double* __restrict__ in,
 // prod r per column).
 __global__ void __launch_bounds__(256) k_modeprod_fwd(const double* __restrict__ in, double* __restrict__ out,
                                                        const double* __restrict__ A, const int* __restrict__ rows,
-                                                       i64 d, i64 rho, i64 Pm, int rm, i64 beta_n) {
+                                                       i64 d, i64 rho, i64 Pm, int rm, i64 beta_n,
+                                                       const int* __restrict__ stop) {
+  if (rt_stopped(stop)) return;
   const i64 total = rho * Pm * beta_n;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
     const i64 alpha = e % rho;
@@ -110,6 +115,7 @@ __global__ void __launch_bounds__(256) k_modeprod_fwd(const double* __restrict__
 template <int R, int GS>
 __global__ void __launch_bounds__(32 * WC_WARPS) k_wcols_warp(Geom g, IndexPtrs ip, double* __restrict__ st,
                                                              int skip_core, int rows_cap) {
+  if (rt_stopped(g.stop)) return;
   constexpr int NG = 32 * WC_WARPS / GS;   // column groups per CTA
   extern __shared__ double wsm[];
   const int b = blockIdx.y;
@@ -203,6 +209,7 @@ __global__ void __launch_bounds__(32 * WC_WARPS) k_wcols_warp(Geom g, IndexPtrs 
 template <int R>
 __global__ void __launch_bounds__(128) k_wcols(Geom g, IndexPtrs ip, double* __restrict__ st, int full,
                                               double* __restrict__ wfull, int rows_per_thread, int skip_core) {
+  if (rt_stopped(g.stop)) return;
   extern __shared__ double gsm[];
   const int b = blockIdx.y;
   i64 Q;

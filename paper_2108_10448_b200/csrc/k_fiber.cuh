@@ -53,6 +53,7 @@ struct FiberBlk {
 };
 
 struct FiberArgs {
+  const int* stop;   // the engine's stop flag (iteration launches), or null
   const void* xb;
   const double* st_s;
   const double* st_e;
@@ -120,6 +121,7 @@ __host__ __device__ constexpr int fb_nsreg() {
 // core, |I_1| rows): whole-column tiles whose starts stay 16-byte aligned.
 template <typename T, int R, bool EX, bool HS, bool HE, bool AP, bool SC>
 __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a) {   // (grid: up to 2 CTAs per SM)
+  if (rt_stopped(a.stop)) return;
   constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);   // staged row sets per column: W_s, W_e or V
   constexpr int V = SC ? 1 : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
   constexpr bool WM = !HE && !AP;   // threshold pass: intersections
@@ -421,6 +423,7 @@ struct FbIn {
 // column offsets) of the A-pass partial rows: a warp per output, lanes over the
 // terms, fixed-order shuffle tree (deterministic).
 static __global__ void __launch_bounds__(256) k_fiber_areduce(FiberArgs a, int G) {
+  if (rt_stopped(a.stop)) return;
   const int f = blockIdx.y;
   if (f >= a.nfb) return;
   const FiberBlk& B = a.fb[f];
@@ -569,6 +572,7 @@ template <typename T>
 static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
   FiberArgs fa;
   memset(&fa, 0, sizeof(fa));
+  fa.stop = L.g.stop;
   fa.st_s = L.st_s;
   fa.st_e = L.st_e;
   fa.zeta = L.zeta;
@@ -664,6 +668,7 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
 // from the compact fiber block (rows past |I_k| zero).  One CTA row per (mode, column chunk).
 template <typename T>
 __global__ void __launch_bounds__(256) k_xi_extract(FiberLaunch L, unsigned mask) {
+  if (rt_stopped(L.g.stop)) return;
   const int b = blockIdx.y + 1;
   if (b >= L.g.nblk || !(mask >> b & 1)) return;
   const BlockDesc& bd = L.g.blk[b];

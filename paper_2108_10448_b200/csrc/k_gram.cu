@@ -15,6 +15,7 @@
 
 
 struct GramArgs {
+  const int* stop;   // the engine's stop flag (iteration launches), or null
   int n;
   int s[RT_MAX_MODES];
   i64 l[RT_MAX_MODES];
@@ -41,6 +42,7 @@ __device__ __forceinline__ void pair_decode(int pair, int& I, int& J) {
 }
 
 __global__ void __launch_bounds__(256) k_gram_tiles(GramArgs ga) {
+  if (rt_stopped(ga.stop)) return;
   const int k = blockIdx.z;
   if (k >= ga.n) return;
   const int s = ga.s[k];
@@ -125,6 +127,7 @@ __global__ void __launch_bounds__(256) k_gram_tiles(GramArgs ga) {
 // banks).  Partials go to the same layout as k_gram_tiles (k_gram_reduce sums them).
 #define GRAM_LDS 68
 __global__ void __launch_bounds__(128) k_gram_tiles_dmma(GramArgs ga) {
+  if (rt_stopped(ga.stop)) return;
   const int k = blockIdx.z;
   if (k >= ga.n) return;
   const int s = ga.s[k];
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(128) k_gram_tiles_dmma(GramArgs ga) {
 
 // Sum the split-K partials (warp per output, fixed butterfly order) into packed lower K.
 __global__ void __launch_bounds__(256) k_gram_reduce(GramArgs ga) {
+  if (rt_stopped(ga.stop)) return;
   const int k = blockIdx.y;
   if (k >= ga.n) return;
   const int s = ga.s[k];

@@ -18,6 +18,7 @@
 #include <cfloat>
 
 struct SvdArgs {
+  const int* stop;   // the engine's stop flag (iteration launches), or null
   int n;
   int s[RT_MAX_MODES];
   i64 l[RT_MAX_MODES];
@@ -54,6 +55,7 @@ __device__ __forceinline__ double svd_B(const SvdArgs& sa, int k, i64 c, i64 t) 
 #define ZP_LD (ZP_T + 1)   // padded slab row: the wide-case transpose store is conflict-free
 template <int R>
 __global__ void __launch_bounds__(32 * R) k_zproj(SvdArgs sa) {
+  if (rt_stopped(sa.stop)) return;
   extern __shared__ double es[];
   const int k = blockIdx.y;
   if (k >= sa.n) return;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(32 * R) k_zproj(SvdArgs sa) {
 // Z <- Z Q (in place, per long-side row)
 template <int R>
 __global__ void __launch_bounds__(256) k_zrot(SvdArgs sa) {
+  if (rt_stopped(sa.stop)) return;
   __shared__ double qs[RT_MAX_RANK * RT_MAX_RANK];
   const int k = blockIdx.y;
   if (k >= sa.n) return;
@@ -137,6 +140,7 @@ __device__ void svd_fin2_ritz_warp(const SvdArgs& sa, int k, double* scr);
 __device__ void svd_short_vecs_cta(const SvdArgs& sa, int k, int t0, int stride);
 template <int PH>
 __global__ void __launch_bounds__(512) k_hgram(SvdArgs sa, unsigned int* counters) {
+  if (rt_stopped(sa.stop)) return;
   extern __shared__ double hz[];   // HG_CH * r + blockDim
   __shared__ bool am_last;
   __shared__ double qs[RT_MAX_RANK * RT_MAX_RANK];
@@ -327,6 +331,7 @@ __device__ void svd_fin1_warp(const SvdArgs& sa, int k) {
 }
 
 __global__ void __launch_bounds__(32) k_svd_fin1(SvdArgs sa) {
+  if (rt_stopped(sa.stop)) return;
   if ((int)blockIdx.x < sa.n) svd_fin1_warp(sa, blockIdx.x);
 }
 
@@ -342,6 +347,7 @@ __device__ void svd_short_vecs_cta(const SvdArgs& sa, int k, int t0, int stride)
   }
 }
 __global__ void k_short_vecs(SvdArgs sa) {
+  if (rt_stopped(sa.stop)) return;
   const int k = blockIdx.y;
   if (k >= sa.n) return;
   svd_short_vecs_cta(sa, k, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
@@ -471,6 +477,7 @@ __device__ void svd_fin2_warp(const SvdArgs& sa, int k) {
 }
 
 __global__ void __launch_bounds__(32) k_svd_fin2(SvdArgs sa) {
+  if (rt_stopped(sa.stop)) return;
   if ((int)blockIdx.x < sa.n) svd_fin2_warp(sa, blockIdx.x);
 }
 
@@ -532,6 +539,7 @@ __device__ void svd_complete_cta(const SvdArgs& sa, int k);
 // degenerate columns (svd_complete_cta)
 template <int R>
 __global__ void __launch_bounds__(256) k_long(SvdArgs sa, unsigned int* counters) {
+  if (rt_stopped(sa.stop)) return;
   __shared__ double ts[RT_MAX_RANK * RT_MAX_RANK];
   __shared__ bool am_last;
   const int k = blockIdx.y;
@@ -627,5 +635,6 @@ __device__ void svd_complete_cta(const SvdArgs& sa, int k) {
 }
 
 __global__ void __launch_bounds__(256) k_complete(SvdArgs sa) {
+  if (rt_stopped(sa.stop)) return;
   if ((int)blockIdx.x < sa.n) svd_complete_cta(sa, blockIdx.x);
 }

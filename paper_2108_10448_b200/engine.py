@@ -8,6 +8,7 @@ CUDA stream.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -77,6 +78,9 @@ def _parallel_copy(dst, src, parts=8):
 
 
 _COPY_POOL = None
+
+# SolveResult arrays as views of the page-locked D2H target (no second host copy)
+PINNED_RESULTS = os.environ.get("RTCUR_PINNED_RESULTS", "1") != "0"
 
 
 CREATED = [0]   # engines constructed in this process (diagnostics: pooled solves construct none)
@@ -254,6 +258,22 @@ class Engine:
         s = np.frombuffer(sums, dtype=np.float64).copy()
         return s[0::2], s[1::2], tuple(bool(f) for f in flags)
 
+    def set_eps(self, eps: float):
+        """Tolerance of the device-side stop rule (0: it never fires)."""
+        nat.check(self.lib.rtcur_engine_set_eps(self.handle, float(eps)))
+
+    def can_speculate(self) -> bool:
+        """A second iterate_async may be enqueued behind the one in flight."""
+        return bool(self.lib.rtcur_engine_can_speculate(self.handle))
+
+    def last_stop(self) -> bool:
+        """The device's stop decision for the iteration waited for last."""
+        return bool(self.lib.rtcur_engine_last_stop(self.handle))
+
+    def iterate_cancel(self):
+        """Drop the speculative iteration (its predecessor met the stop rule)."""
+        nat.check(self.lib.rtcur_engine_iterate_cancel(self.handle))
+
     def export_blocks(self, want_s=True, want_clean=True, want_l=False):
         """Device fp64 tensors (N_blk) of S, X - S and L_new on the compact blocks."""
         import torch
@@ -265,12 +285,30 @@ class Engine:
         return outs
 
     def to_host(self, dev_tensors):
-        """Copy fp64 device vectors into fresh host numpy arrays: D2H through a
-        pinned staging buffer kept by the engine (full PCIe rate), then a
-        multi-threaded host copy into memory the caller owns."""
+        """Copy fp64 device vectors into host numpy arrays the caller owns.
+
+        Default: the arrays ARE the D2H target -- one page-locked block per call
+        (torch's caching host allocator recycles it once the arrays are gone, so
+        a steady stream of solves allocates nothing), filled at full PCIe rate
+        and handed out as numpy views that keep it alive.  No second host copy.
+        ``RTCUR_PINNED_RESULTS=0``: D2H into a staging buffer kept by the engine,
+        then a multi-threaded copy into ordinary (pageable) arrays."""
         import torch
 
         total = sum(int(t.numel()) for t in dev_tensors)
+        if PINNED_RESULTS:
+            st = torch.empty(max(total, 1), dtype=torch.float64, pin_memory=True)
+            o = 0
+            for t in dev_tensors:
+                st[o:o + t.numel()].copy_(t, non_blocking=True)
+                o += t.numel()
+            torch.cuda.current_stream(self.device).synchronize()
+            stage = st.numpy()   # keeps ``st`` (and so the pinned block) alive through .base
+            outs, o = [], 0
+            for t in dev_tensors:
+                outs.append(stage[o:o + int(t.numel())])
+                o += int(t.numel())
+            return outs
         st = getattr(self, "_pin_stage", None)
         if st is None or st.numel() < total:
             st = self._pin_stage = torch.empty(total, dtype=torch.float64, pin_memory=True)

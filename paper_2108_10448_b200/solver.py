@@ -454,6 +454,10 @@ def _make_result(eng: Engine, src: _Source, idx, cfg, history, flags, timings, z
                        config=cfg, trace=tuple(trace) if trace is not None else None)
 
 
+# enqueue iteration k + 1 behind k before k's stop check (RTCUR_SPECULATE=0: one at a time)
+SPECULATE = os.environ.get("RTCUR_SPECULATE", "1") != "0"
+
+
 def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
     """Separate a sampled observation into low-multilinear-rank + sparse
     (solver.py:260-389) on the GPU.
@@ -467,6 +471,29 @@ def rtcur(x, cfg: SolverConfig, record_trace: bool = False) -> SolveResult:
 # DRAM bytes a strided fiber element costs the gather (8-byte reads one per
 # 32-byte sector, >= 64-byte DRAM fetches; ~120 B measured by ncu on config 1)
 _STRIDED_BYTES = 100
+
+
+_HBM_SEEN: dict = {}
+
+
+def _free_hbm(device):
+    """(free, total) bytes of HBM as this process can use them: the driver's figure
+    (cudaMemGetInfo, refreshed at most every few seconds -- it takes a driver-wide lock
+    and was seen stalling a solve's setup for milliseconds while monitoring tools poll
+    the GPU) corrected by what torch's caching allocator has reserved since."""
+    import torch
+
+    key = str(device)
+    now = time.monotonic()
+    seen = _HBM_SEEN.get(key)
+    reserved = torch.cuda.memory_reserved(device)
+    if seen is None or now - seen[0] > 5.0:
+        free, total = torch.cuda.mem_get_info(device)
+        # memory held outside torch's allocator (other processes, contexts, the engine's own cudaMallocs)
+        seen = _HBM_SEEN[key] = (now, total - free - reserved, total)
+    _, other, total = seen
+    cached = reserved - torch.cuda.memory_allocated(device)   # reusable without a cudaMalloc
+    return total - other - reserved + cached, total
 
 
 def _mode_copy_plan(shape, col_sizes, cfg, src):
@@ -486,7 +513,7 @@ def _mode_copy_plan(shape, col_sizes, cfg, src):
         return ()
     # each copy is another N*E bytes of HBM: keep only what fits with headroom
     # (1 GiB + 10 % of the device) next to everything already allocated
-    free, total = torch.cuda.mem_get_info(src.dev.flat.device)
+    free, total = _free_hbm(src.dev.flat.device)
     room = free - (1 << 30) - total // 10
     keep = []
     for k in want:
@@ -630,47 +657,53 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
         # RTCUR-R draws the next sample while the GPU runs the current iteration:
         # the generator is consumed by sampling only, so drawing ahead leaves every
         # index set identical to the reference's (solver.py:315-317).
-        next_idx = None
         # device-resident local tensors: the next sample's upload and gather go into the
         # engine's inactive sample slot right behind the running iteration (no host gap)
         prefetch = src.dev is not None
-        staged = False
-        for k in range(1, cfg.max_iters + 1):
-            if cfg.variant == "R" and k >= 2:
-                t0 = time.perf_counter()
-                idx = next_idx if next_idx is not None else draw()
-                next_idx = None
-                timings["sample"] += time.perf_counter() - t0
-                if not staged:
-                    t0 = time.perf_counter()
-                    eng.set_sample(idx)
-                    src.load_blocks(eng, idx)
-                    timings["gather"] += time.perf_counter() - t0
-                staged = False
-            zeta *= cfg.gamma
-            t0 = time.perf_counter()
-            if _TIMELINE is not None:
-                _TIMELINE.append(("async", k, t0))
-            eng.iterate_async(zeta, first=(k == 1))
-            if cfg.variant == "R" and k < cfg.max_iters:
+        # Speculation: iteration k + 1 is enqueued while k is still running, so the stream
+        # never idles over the host's stop check (solver.py:357-358); the device evaluates
+        # the same test at the end of k and k + 1's kernels return at once when it
+        # holds.  Needs the engine's state untouched between iterations: not with a
+        # trace / iteration callback, a host accessor or a sharded exchange.
+        eng.set_eps(cfg.eps)
+        spec = (SPECULATE and src.dev is not None and src.group is None and not record_trace
+                and on_iteration is None and eng.can_speculate())
+        resample = cfg.variant == "R"
+        k = 1
+        zeta *= cfg.gamma
+        t0 = time.perf_counter()
+        if _TIMELINE is not None:
+            _TIMELINE.append(("async", k, t0))
+        eng.iterate_async(zeta, first=True)
+        while True:
+            # iteration k is in flight with sample `idx` at threshold `zeta`
+            nxt, staged, ahead = None, False, False
+            if resample and k < cfg.max_iters:
                 t1 = time.perf_counter()
-                next_idx = draw()
+                nxt = draw()
                 timings["sample"] += time.perf_counter() - t1
                 if prefetch:
                     t1 = time.perf_counter()
-                    eng.set_sample(next_idx)
-                    src.load_blocks(eng, next_idx)
+                    eng.set_sample(nxt)
+                    src.load_blocks(eng, nxt)
                     staged = True
                     timings["gather"] += time.perf_counter() - t1
+            if spec and k < cfg.max_iters and (staged or not resample):
+                eng.iterate_async(zeta * cfg.gamma, first=False)
+                ahead = True
             if _TIMELINE is not None:
                 _TIMELINE.append(("staged", k, time.perf_counter()))
             e2, x2, fl = eng.iterate_wait()
             timings["build"] += time.perf_counter() - t0
+            t0 = time.perf_counter()
             if _TIMELINE is not None:
-                _TIMELINE.append(("waited", k, time.perf_counter()))
+                _TIMELINE.append(("waited", k, t0))
             err = _error_from_sums(e2, x2)
             history.append(err)
             flags.append(fl)
+            stop = err <= cfg.eps
+            if ahead and stop != eng.last_stop():
+                raise RuntimeError(f"device stop rule disagrees with the host at iteration {k} (err {err!r})")
             if record_trace:
                 s_dev, _, l_dev = eng.export_blocks(True, False, True)
                 s_core, s_fib = eng.split_blocks(s_dev.cpu().numpy())
@@ -679,9 +712,26 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                               "l_core": l_core, "l_fibers": l_fib, "error": err})
             if on_iteration is not None:
                 on_iteration(k, eng, idx, zeta, err, fl)
-            if err <= cfg.eps:
+            if stop:
                 converged = True
+                if ahead:
+                    eng.iterate_cancel()   # k + 1 ran nothing: k stays the engine's iterate
                 break
+            if k >= cfg.max_iters:
+                break
+            k += 1
+            zeta *= cfg.gamma
+            if resample:
+                idx = nxt
+            if not ahead:
+                if resample and not staged:
+                    t1 = time.perf_counter()
+                    eng.set_sample(idx)
+                    src.load_blocks(eng, idx)
+                    timings["gather"] += time.perf_counter() - t1
+                if _TIMELINE is not None:
+                    _TIMELINE.append(("async", k, time.perf_counter()))
+                eng.iterate_async(zeta, first=False)
     finally:
         if sampler is not None:
             sampler.close()
