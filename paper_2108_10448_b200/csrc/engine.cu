@@ -578,7 +578,8 @@ enum { PH_ABSMAX = 0, PH_PREP, PH_GATHER, PH_THRESH, PH_GRAM, PH_EIG, PH_SVDPOST
 struct ProfPair {
   int ph;
   cudaEvent_t b, e;
-  bool owned;   // from the engine's event pool (returned at flush); graph-owned events are reused
+  bool owned;   // from the engine's event pool (returned at flush)
+  unsigned seq; // iteration launch it belongs to (0: outside an iteration)
 };
 // An iteration is captured as a short list of graph segments.  A segment ends where
 // the stream needs an event between graphs: the begin / end of a profiled phase, or
@@ -621,7 +622,7 @@ struct rtcur_engine {
   bool spec_ok;     // speculative launches allowed (RTCUR_SPEC=0 disables them)
   struct Snap { int cur, prev, act, stg, sample_epoch, w_epoch[3]; double zeta_last; bool xi_valid[2]; } snap;
   bool snap_valid;
-  size_t snap_prof;  // prof_pending entries before the speculative launch
+  unsigned launch_seq, cur_seq, snap_seq;   // iteration launches so far; the one being enqueued; the speculative one
   int prev;         // ring slot of the one before (-1: none, i.e. latest is iteration 1)
   double zeta_last;
   bool sampled;
@@ -731,7 +732,7 @@ static void prof_end(rtcur_engine* e, int ph) {
   if (!e->prof_open[ph]) return;
   cudaEvent_t ev = prof_event(e);
   cudaEventRecord(ev, e->st);
-  e->prof_pending->push_back({ph, e->prof_open[ph], ev, true});
+  e->prof_pending->push_back({ph, e->prof_open[ph], ev, true, e->cur_seq});
   e->prof_open[ph] = nullptr;
 }
 // replay a captured iteration: its segments with the events between them
@@ -745,7 +746,7 @@ static int launch_entry(rtcur_engine* e, GraphEntry& ge) {
     } else if (sg.cut == CUT_PROF_END && e->prof_open[sg.ph]) {
       cudaEvent_t ev = prof_event(e);
       CK(cudaEventRecord(ev, e->st));
-      e->prof_pending->push_back({sg.ph, e->prof_open[sg.ph], ev, true});
+      e->prof_pending->push_back({sg.ph, e->prof_open[sg.ph], ev, true, e->cur_seq});
       e->prof_open[sg.ph] = nullptr;
     } else if (sg.cut == CUT_EIG) {
       CK(cudaEventRecord(e->eig_ev, e->st));
@@ -1909,8 +1910,9 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
     sn.zeta_last = e->zeta_last;
     sn.xi_valid[0] = e->xi_valid[0]; sn.xi_valid[1] = e->xi_valid[1];
     e->snap_valid = true;
-    e->snap_prof = e->prof_pending->size();
+    e->snap_seq = e->launch_seq + 1;
   }
+  e->cur_seq = ++e->launch_seq;
   if (e->staging_on_side) {   // the prefetched sample's staging must be complete
     CK(cudaStreamWaitEvent(e->st, e->side_ev, 0));
     e->staging_on_side = false;
@@ -1974,6 +1976,7 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   }
   e->zetap_cur = nullptr;
   e->P.g.stop = nullptr;
+  e->cur_seq = 0;
   CK(cudaEventRecord(e->done[par], e->st));
   if (reeval) e->w_epoch[e->cur] = e->sample_epoch;
   e->w_epoch[newslot] = e->sample_epoch;
@@ -2019,11 +2022,17 @@ extern "C" int rtcur_engine_iterate_cancel(rtcur_engine* e) {
   e->snap_valid = false;
   e->npending = 0;
   // its profiled phases measured empty segments: drop them
-  while (e->prof_pending->size() > e->snap_prof) {
-    ProfPair p = e->prof_pending->back();
-    e->prof_pending->pop_back();
-    e->prof_pool->push_back(p.b);
-    e->prof_pool->push_back(p.e);
+  {
+    std::vector<ProfPair> keep;
+    for (auto& p : *e->prof_pending) {
+      if (p.seq != e->snap_seq) {
+        keep.push_back(p);
+        continue;
+      }
+      e->prof_pool->push_back(p.b);
+      e->prof_pool->push_back(p.e);
+    }
+    e->prof_pending->swap(keep);
   }
   for (int ph = 0; ph < RT_NPHASE; ++ph)
     if (e->prof_open[ph]) {

@@ -222,11 +222,49 @@ for case in ("bern_R", "d20_F", "n4_R"):
     assert outs[0] == outs[1] and outs[0].count("\n") == 3
 
 
+@pytest.mark.parametrize("case", ["bern_R", "d20_F", "n4_R", "nonconv", "zero", "n1"])
+def test_speculative_pipeline_matches_one_at_a_time(case):
+    """The speculative loop (iteration k + 1 enqueued behind k, cancelled on the device
+    when k meets the stop rule, solver.py:357-358) returns what the one-at-a-time loop
+    returns: iterates, index sets, exported blocks, factors -- also when the solve stops
+    at max_iters (no iteration enqueued past it) and when the next solve reuses the
+    pooled engine after a cancel."""
+    from paper_2108_10448_b200 import solver as S
+
+    g = load_golden(f"solve_{case}.npz")
+    shape = tuple(int(d) for d in g["shape"])
+    kw = golden_cfg_kwargs(g)
+    x = DeviceTensor.from_host(DenseTensor(g["x"], shape))
+    full_iters = int(g["iterations"])
+    for max_iters in (kw["max_iters"], 1, 2, max(1, full_iters - 1)):
+        cfg = SolverConfig(**dict(kw, max_iters=max_iters))
+        got = {}
+        for spec in (False, True, True):   # (twice: the pooled engine right after a cancel)
+            S.SPECULATE = spec
+            try:
+                res = rtcur(x, cfg)
+                got[spec] = (res.iterations, res.converged, tuple(res.error_history), res.zeta_final,
+                             [np.array(r) for r in res.sparse.indices.rows], [np.array(c) for c in res.sparse.indices.cols],
+                             _flat(res.sparse.core).copy(), [np.array(f) for f in res.sparse.fibers],
+                             _flat(res.cur.core.data).copy(), [np.array(t.singular_values) for t in res.cur.intersections],
+                             [np.array(f) for f in res.cur.factors], tuple(res.diagnostics))
+            finally:
+                S.SPECULATE = True
+            del res
+        a, b = got[False], got[True]
+        assert a[:4] == b[:4] and a[11] == b[11], (max_iters, a[:2], b[:2])
+        for i in (4, 5, 7, 9, 10):
+            assert len(a[i]) == len(b[i])
+            for u, v in zip(a[i], b[i]):
+                assert np.array_equal(u, v), (max_iters, i)
+        assert np.array_equal(a[6], b[6]) and np.array_equal(a[8], b[8])
+
+
 @pytest.mark.parametrize("env", [{"RTCUR_FIBER_PASS": "0"}, {"RTCUR_FIBER_CORE": "0"}, {"RTCUR_EARLY_ZETA": "0"},
                                  {"RTCUR_K3_GENERIC": "1"}, {"RTCUR_CORE_PASS": "1"}, {"RTCUR_EIG_REG": "0"},
-                                 {"RTCUR_EIG_REG": "2"}, {"RTCUR_SIDE_PREFETCH": "1"}],
+                                 {"RTCUR_EIG_REG": "2"}, {"RTCUR_SIDE_PREFETCH": "0"}],
                          ids=["block-pass-only", "core-on-block-pass", "late-zeta0", "generic-k3", "core-pass",
-                              "eig-smem-tridiag", "eig-reg-tridiag", "side-prefetch"])
+                              "eig-smem-tridiag", "eig-reg-tridiag", "in-order-prefetch"])
 def test_engine_variants_agree(env):
     """The device-path variants (TMA fiber pass vs the block pass for every block,
     the core on either, zeta_0 scanned before or after the first draw, TMA vs
