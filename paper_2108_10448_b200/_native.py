@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librtcur_b200.so")
+# (RTCUR_LIB: another build of the same library, for A/B runs of compile-time variants)
+LIB_PATH = os.environ.get("RTCUR_LIB") or os.path.join(_HERE, "_lib", "librtcur_b200.so")
 
 (RTCUR_OK, RTCUR_E_VALUE, RTCUR_E_INDEX, RTCUR_E_ARITH, RTCUR_E_CUDA, RTCUR_E_UNSUPPORTED, RTCUR_E_FORMAT,
  RTCUR_E_NOTFOUND, RTCUR_E_IO) = range(9)

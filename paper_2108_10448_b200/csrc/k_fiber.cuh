@@ -34,6 +34,9 @@
 #define FB_MAX_CTAS_PER_SM 2
 #define FB_MAX_STAGES 8
 #define FB_MAX_R 16
+#ifndef FB_COL_UNROLL
+#define FB_COL_UNROLL 1   // columns in flight per consumer thread (A/B: make EXTRA=-DFB_COL_UNROLL=2)
+#endif
 
 struct FiberBlk {
   i64 off;      // element offset of the block in its buffer
@@ -294,7 +297,8 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
         const double* wes = reinterpret_cast<const double*>(sb + a.x_region + (HS ? a.w_region : 0));   // W_e or V
         double* Mc = WM ? a.M[B.mode] + (c0 + coff) * (i64)mrows : nullptr;
         const i64 mstep = (i64)cpr * mrows;
-#pragma unroll 1
+        constexpr int CU = FB_COL_UNROLL;
+#pragma unroll CU
         for (int jj = coff; jj < nc; jj += cpr) {
           const VT xv = *reinterpret_cast<const VT*>(xs + jj * H);
           double ws[R], we[R];
@@ -384,18 +388,38 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
   __syncthreads();
   if (!am_last) return;
   __threadfence();
-  for (int f = 0; f < a.nfb; ++f) {   // per-block sums over CTAs in CTA order (deterministic)
-    const int b = a.fb[f].b;
-    double se = 0.0, sx = 0.0;
+  // per-block sums over the CTAs' partials, every (block, sum) at once: thread t adds
+  // the partials of CTAs t, t + blockDim, ... (all loads in flight together), a fixed
+  // shuffle tree per warp, then the warps in order -- the operation order of one
+  // block_sum per value (deterministic), without its serial per-value round trips
+  {
+    constexpr int NVAL = 2 * RT_MAX_MODES;
+    __shared__ double redf[NVAL][FB_MAX_CONS / 32 + 1];
+    double acc[NVAL];
+#pragma unroll
+    for (int v = 0; v < NVAL; ++v) acc[v] = 0.0;
     for (int c = tid; c < (int)gridDim.x; c += blockDim.x) {
-      se += ((volatile double*)a.partial)[((i64)c * a.nblk + b) * 2];
-      sx += ((volatile double*)a.partial)[((i64)c * a.nblk + b) * 2 + 1];
+      const volatile double* pc = reinterpret_cast<const volatile double*>(a.partial) + (i64)c * a.nblk * 2;
+#pragma unroll
+      for (int f = 0; f < RT_MAX_MODES; ++f)
+        if (f < a.nfb) {
+          const int b = a.fb[f].b;
+          acc[2 * f] += pc[2 * b];
+          acc[2 * f + 1] += pc[2 * b + 1];
+        }
     }
-    se = block_sum(se, red);
-    sx = block_sum(sx, red);
-    if (tid == 0) {
-      a.sums[2 * b] = se;
-      a.sums[2 * b + 1] = sx;
+    const int wid = tid >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int v = 0; v < NVAL; ++v)
+      if (v < 2 * a.nfb) {   // (block-uniform)
+        const double s = warp_sum(acc[v]);
+        if (lane == 0) redf[v][wid] = s;
+      }
+    __syncthreads();
+    if (tid < 2 * a.nfb) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += redf[tid][w];
+      a.sums[2 * a.fb[tid >> 1].b + (tid & 1)] = t;
     }
   }
   if (tid == 0) *a.counter = 0u;
