@@ -1620,7 +1620,9 @@ static int run_wcols(rtcur_engine* e, double* sto) {
   const int rows_cap = (int)(cdiv(rsmax, gs) * gs);
   const i64 wsm = (g.gsize + (ncmax * 4 + ncmax * std::max(1, g.n - 1) + 7) / 8 + 1 + (i64)ngrp * rows_cap) * 8;
   if (wsm <= 200 * 1024 && ncmax >= 8) {   // very few combinations: a thread per column is cheaper
-    const dim3 grid((unsigned)std::min<i64>(cdiv(qf, ngrp * 2), 148 * 4), g.nblk);
+    // columns per lane group and pass (RTCUR_WC_CPG; 1: +0.4..1.8 % over 2 at configs 0-4)
+    static const int cpg = [] { const char* v = getenv("RTCUR_WC_CPG"); return v ? std::max(1, atoi(v)) : 1; }();
+    const dim3 grid((unsigned)std::min<i64>(cdiv(qf, ngrp * cpg), 148 * 4 * (cpg == 1 ? 2 : 1)), g.nblk);
 #define WCW(RB, GS) k_wcols_warp<RB, GS><<<grid, 32 * WC_WARPS, (int)wsm, e->st>>>(g, ip, sto, chain ? 1 : 0, rows_cap)
     if (gs == 32) {
       switch (P.rb) {

@@ -97,6 +97,13 @@ __host__ __device__ constexpr int fb_vec(int r, int ns) {
          : (int)(4 / sizeof(T)) >= 1 ? (int)(4 / sizeof(T)) : 1;
 }
 
+// scalar-row blocks (SC): rows per thread, loaded one element at a time (the columns
+// are not vector-aligned) -- as many as keep the A rows within 48 doubles, so the
+// column's W rows and the loop overhead are shared by up to four entries
+__host__ __device__ constexpr int fb_sc_vec(int r, int ns) {
+  return 4 * r * ns <= 48 ? 4 : 2 * r * ns <= 48 ? 2 : 1;
+}
+
 __device__ __forceinline__ void fb_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -120,13 +127,13 @@ __host__ __device__ constexpr int fb_nsreg() {
   return ((HS ? 1 : 0) + (HE ? 1 : 0) + (AP ? 1 : 0)) > 0 ? (HS ? 1 : 0) + (HE ? 1 : 0) + (AP ? 1 : 0) : 1;
 }
 
-// SC: scalar rows (V = 1) for blocks whose columns are not 16-byte multiples (the
+// SC: scalar rows (fb_sc_vec per thread) for blocks whose columns are not 16-byte multiples (the
 // core, |I_1| rows): whole-column tiles whose starts stay 16-byte aligned.
 template <typename T, int R, bool EX, bool HS, bool HE, bool AP, bool SC>
 __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a) {   // (grid: up to 2 CTAs per SM)
   if (rt_stopped(a.stop)) return;
   constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);   // staged row sets per column: W_s, W_e or V
-  constexpr int V = SC ? 1 : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
+  constexpr int V = SC ? fb_sc_vec(R, fb_nsreg<HS, HE, AP>()) : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
   constexpr bool WM = !HE && !AP;   // threshold pass: intersections
   constexpr bool SUMS = HE;         // error pass: sums
   typedef FbVec<T, V> VT;
@@ -280,9 +287,10 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
             // computed (finite) but never stored
             const int arow = B.amap ? __ldg(B.amap + (rr < B.Pv ? rr : B.Pv - 1)) : rr;
             if (WM) pos[v] = rr < B.Pv ? rr : -1;
+            const bool live = !SC || rr < r0 + hb;   // (SC: rows past the column read x = 0 with zero A rows)
 #pragma unroll
             for (int q = 0; q < R; ++q) {
-              const bool on = EX || q < r;
+              const bool on = (EX || q < r) && live;
               as[v][q] = (HS && on) ? __ldg(a.st_s + B.a_off + arow + (i64)q * B.dA) : 0.0;
               ae[v][q] = (HE && on) ? __ldg(a.st_e + B.a_off + arow + (i64)q * B.dA) : 0.0;
             }
@@ -300,7 +308,13 @@ __global__ void __launch_bounds__(FB_MAX_CONS + 32, 1) k_fiber_pass(FiberArgs a)
         constexpr int CU = FB_COL_UNROLL;
 #pragma unroll CU
         for (int jj = coff; jj < nc; jj += cpr) {
-          const VT xv = *reinterpret_cast<const VT*>(xs + jj * H);
+          VT xv;
+          if (SC) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) xv.v[v] = chunk * V + v < hb ? xs[jj * H + v] : (T)0;
+          } else {
+            xv = *reinterpret_cast<const VT*>(xs + jj * H);
+          }
           double ws[R], we[R];
           if (EX && R % 2 == 0) {   // exact even rank: the column's rows are 16-byte aligned
             const double2* ws2 = reinterpret_cast<const double2*>(wss + jj * R);
@@ -471,7 +485,7 @@ static __global__ void __launch_bounds__(256) k_fiber_areduce(FiberArgs a, int G
 template <typename T, int R, bool EX, bool HS, bool HE, bool AP, bool SC>
 static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, cudaStream_t st) {
   constexpr int NS = (HS ? 1 : 0) + ((HE || AP) ? 1 : 0);
-  constexpr int V = SC ? 1 : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
+  constexpr int V = SC ? fb_sc_vec(R, fb_nsreg<HS, HE, AP>()) : fb_vec<T>(R, fb_nsreg<HS, HE, AP>());
   const int E = (int)sizeof(T);
   const int VA = SC ? 1 : 16 / E;   // bulk-copy segments are 16-byte multiples (SC: one band)
   // per-block bands / thread mapping
