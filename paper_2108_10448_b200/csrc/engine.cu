@@ -103,6 +103,8 @@ static int rbucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32; 
     }                                                                                \
   } while (0)
 
+#define RT_STATE_SLOTS 6   // iterate ring: latest, its threshold state, a shadow, the speculative pair + 1
+
 struct Plan {
   Geom g;
   TileMap tm;
@@ -144,7 +146,8 @@ struct Plan {
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
       o_degen[RT_MAX_MODES], o_flags, o_nonfinite, o_counters, o_absmax, o_gt0, o_gt1, o_bpart, o_sums,
-      o_fpart, o_dbg, o_fast, o_wt0, o_wt1;
+      o_fpart, o_dbg, o_fast, o_wt0, o_wt1, o_wt0s, o_wt1s;
+  i64 res_stride;             // bytes between the two (launch-parity) copies of the result range
   i64 total;
 };
 
@@ -496,8 +499,8 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   }
   P.samp_delta = o - samp0;
   take(P.samp_delta - 8);   // slot 1 (aligned like slot 0)
-  P.o_state = take(3 * g.state_doubles * 8);
-  P.o_zeta = take(32);   // zeta | eps | stop flag
+  P.o_state = take((i64)RT_STATE_SLOTS * g.state_doubles * 8);
+  P.o_zeta = take(64);   // per launch parity p, at +32 p: zeta | eps; the stop flag at +16
   for (int m = 0; m < n; ++m) P.o_M[m] = take(row_sizes[m] * col_sizes[m] * 8);
   P.o_gpart = take((i64)n * P.gram_maxchunks * P.gram_maxpairs * GRAM_T * GRAM_T * 8);
   for (int m = 0; m < n; ++m) {
@@ -525,7 +528,9 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   // the iteration's results in one contiguous range (one D2H per iteration):
   // sums (2 nblk doubles) | flags (n ints, padded to 8 bytes) | non-finite flag
   {
-    const i64 res0 = take(2 * g.nblk * 8 + ((n * 4 + 7) & ~7LL) + 8);
+    P.res_stride = align256(2 * g.nblk * 8 + ((n * 4 + 7) & ~7LL) + 8);
+    const i64 res0 = take(2 * P.res_stride);   // one copy per launch parity (an iteration's error
+                                               // pass may run under the next iteration's eigensolver)
     P.o_sums = res0;
     P.o_flags = res0 + 2 * g.nblk * 8;
     P.o_nonfinite = P.o_flags + ((n * 4 + 7) & ~7LL);
@@ -554,6 +559,8 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   P.o_gt1 = take(P.g_tmp * 8);
   P.o_wt0 = take(P.w_tmp * 8);
   P.o_wt1 = take(P.w_tmp * 8);
+  P.o_wt0s = take(P.w_tmp * 8);   // the side stream's W chain (shadow state, concurrent with the iteration's)
+  P.o_wt1s = take(P.w_tmp * 8);
   P.o_bpart = take((i64)BP_GRID * g.nblk * 2 * 8 + 64);
   P.o_cpart = take(2 * 148 * 8 * 8 + 64);
   {
@@ -587,14 +594,19 @@ struct ProfPair {
 // sample waits for it).  (Gating the segments with conditional IF nodes on the stop
 // flag was measured at ~50 us per iteration on B200 -- more than the host round trip
 // it hides -- so the kernels test the flag themselves, Geom::stop / rt_stopped.)
-enum { CUT_NONE = 0, CUT_PROF_BEGIN, CUT_PROF_END, CUT_EIG };
+enum { CUT_NONE = 0, CUT_PROF_BEGIN, CUT_PROF_END,
+       CUT_EIG,     // the eigensolver starts: record eig_ev, enqueue the previous iteration's tail under it
+       CUT_JOIN,    // the eigensolver is enqueued: wait for that tail (its stop flag) before the SVD post
+       CUT_STATE }; // G and A of the new iterate are complete: record st_ev (the shadow's W waits for it)
 struct GraphSeg {
   cudaGraphExec_t exec = nullptr;   // null: nothing was captured before the cut
   int cut = CUT_NONE, ph = 0;       // event to record after the segment
 };
 struct GraphEntry {
-  std::vector<GraphSeg> segs;
-  unsigned long long nkernels = 0;   // kernel launches captured (counted at every replay)
+  std::vector<GraphSeg> segs;        // threshold ... column weights of the new iterate
+  std::vector<GraphSeg> tail;        // error pass, stop rule, result copy
+  unsigned long long nkernels = 0;   // kernel launches captured in segs (counted at every replay)
+  unsigned long long nk_tail = 0;    // ... in tail
 };
 
 struct ShardState;   // shard_xchg.cu
@@ -609,7 +621,29 @@ struct rtcur_engine {
   int cur;          // ring slot of the latest iterate (-1: none)
   int act, stg;     // sample slots: active (iterations, exports) and staged (next set_sample/gather), -1: none
   int sample_epoch; // bumped whenever a staged sample becomes active
-  int w_epoch[3];   // sample epoch each slot's W (column weights) was built for
+  int w_epoch[RT_STATE_SLOTS];   // sample epoch each slot's W (column weights) was built for
+  // RTCUR-R shadow: slot `shadow` holds a copy of state `shadow_of` (G, A) whose W was
+  // evaluated on the sample staged for epoch `shadow_epoch` (side stream, under the running
+  // iteration): the next iteration thresholds against it instead of re-evaluating in place,
+  // so the running iterate stays intact for its error pass and for the exports
+  int shadow, shadow_of, shadow_epoch;
+  int alloc_rr;     // ring cursor of the state-slot allocator
+  int cur_par;      // parity of the launch being enqueued / captured (result range, control words)
+  bool wt_alt;      // W-chain scratch: the side stream's pair
+  // The tail of an iteration (error pass, stop rule, result copy) does not feed the next
+  // iteration's threshold / Gram / eigensolver: it is held back and enqueued on `tail`
+  // under the NEXT iteration's eigensolver (3-4 CTAs on an otherwise idle GPU); that
+  // iteration joins it before its SVD post, the first kernel that must see the stop flag.
+  cudaStream_t tail;
+  struct TailRef { struct GraphEntry* ge; int par; unsigned seq; bool valid; } tail_pending;
+  cudaEvent_t st_ev;      // the running iteration's G and A are complete (the shadow's W waits for it)
+  unsigned st_ev_seq;     // launch that recorded st_ev last
+  cudaEvent_t main_ev;    // the running iteration's main part is enqueued up to here
+  bool r_mode;            // samples are re-staged between iterations (RTCUR-R): cut the graph at CUT_STATE
+  unsigned cur_of_seq;    // launch that produced the latest iterate
+  cudaEvent_t tl_base;    // diagnostics: recorded at a solve's first iteration (RTCUR_PROF_TIMELINE)
+  bool join_needed;       // the iteration being launched must wait for join_ev before its SVD post
+  cudaEvent_t join_ev;
   int npending;     // iterate_async calls awaiting their iterate_wait (2: one speculative)
   bool use_fast;    // allow the warm-started subspace-iteration eigensolver
   cudaEvent_t done[2];   // recorded after the iteration's result copies (by launch parity)
@@ -620,7 +654,11 @@ struct rtcur_engine {
   // speculation (rtcur_engine_iterate_async while one iteration is in flight): the
   // bookkeeping before the speculative launch, restored by rtcur_engine_iterate_cancel
   bool spec_ok;     // speculative launches allowed (RTCUR_SPEC=0 disables them)
-  struct Snap { int cur, prev, act, stg, sample_epoch, w_epoch[3]; double zeta_last; bool xi_valid[2]; } snap;
+  struct Snap {
+    int cur, prev, act, stg, sample_epoch, w_epoch[RT_STATE_SLOTS], shadow, shadow_of, shadow_epoch, alloc_rr;
+    double zeta_last;
+    bool xi_valid[2];
+  } snap;
   bool snap_valid;
   unsigned launch_seq, cur_seq, snap_seq;   // iteration launches so far; the one being enqueued; the speculative one
   int prev;         // ring slot of the one before (-1: none, i.e. latest is iteration 1)
@@ -645,6 +683,7 @@ struct rtcur_engine {
   cudaStream_t cap_st;             // private stream the iteration is captured on
   std::map<unsigned long long, GraphEntry>* graphs;
   GraphEntry* cap_entry;
+  std::vector<GraphSeg>* cap_segs; // the list the capture appends to (cap_entry->segs or ->tail)
   int cap_err;                     // first error inside a capture cut (prof_begin/prof_end are void)
   const double* zetap_cur;         // device zeta while an iteration body is enqueued/captured
   bool xi_valid[2];                // the sample slot's intersection copies match its blocks
@@ -665,6 +704,7 @@ struct rtcur_engine {
                                    // rather than the wide threshold / Gram kernels before it
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
+  i64 roff() const { return (i64)cur_par * P.res_stride; }   // this launch's copy of the result range
   i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
   int act_slot() const { return act >= 0 ? act : 0; }
   char* xb(int slot) const { return ws + P.o_xb + sd(slot); }
@@ -702,7 +742,7 @@ static cudaError_t seg_end(rtcur_engine* e, int cut, int ph) {
     if (ce == cudaSuccess && nn > 0) ce = cudaGraphInstantiate(&sg.exec, cap, 0);
   }
   if (cap) cudaGraphDestroy(cap);
-  if (ce == cudaSuccess) e->cap_entry->segs.push_back(sg);
+  if (ce == cudaSuccess) e->cap_segs->push_back(sg);
   return ce;
 }
 
@@ -735,21 +775,64 @@ static void prof_end(rtcur_engine* e, int ph) {
   e->prof_pending->push_back({ph, e->prof_open[ph], ev, true, e->cur_seq});
   e->prof_open[ph] = nullptr;
 }
-// replay a captured iteration: its segments with the events between them
-static int launch_entry(rtcur_engine* e, GraphEntry& ge) {
-  for (auto& sg : ge.segs) {
-    if (sg.exec) CK(cudaGraphLaunch(sg.exec, e->st));
+// the tail of iteration `t` (error pass, stop rule, result copy) on `st`, then its done event
+static int launch_tail(rtcur_engine* e, const rtcur_engine::TailRef& t, cudaStream_t st) {
+  for (auto& sg : t.ge->tail) {
+    if (sg.exec) CK(cudaGraphLaunch(sg.exec, st));
     if (sg.cut == CUT_PROF_BEGIN) {
       cudaEvent_t ev = prof_event(e);
-      CK(cudaEventRecord(ev, e->st));
+      CK(cudaEventRecord(ev, st));
       e->prof_open[sg.ph] = ev;
     } else if (sg.cut == CUT_PROF_END && e->prof_open[sg.ph]) {
       cudaEvent_t ev = prof_event(e);
-      CK(cudaEventRecord(ev, e->st));
+      CK(cudaEventRecord(ev, st));
+      e->prof_pending->push_back({sg.ph, e->prof_open[sg.ph], ev, true, t.seq});
+      e->prof_open[sg.ph] = nullptr;
+    }
+  }
+  rtcur_launch_counter_add(t.ge->nk_tail);
+  CK(cudaEventRecord(e->done[t.par], st));
+  return RT_OK;
+}
+
+// a held-back tail goes out in stream order (nothing will run over it)
+static int flush_tail(rtcur_engine* e) {
+  if (!e->tail_pending.valid) return RT_OK;
+  const rtcur_engine::TailRef t = e->tail_pending;
+  e->tail_pending.valid = false;
+  return launch_tail(e, t, e->st);
+}
+
+// replay a captured iteration's main part: its segments with the events between them
+static int launch_entry(rtcur_engine* e, GraphEntry& ge) {
+  cudaStream_t cs = e->st;
+  for (auto& sg : ge.segs) {
+    if (sg.exec) CK(cudaGraphLaunch(sg.exec, cs));
+    if (sg.cut == CUT_PROF_BEGIN) {
+      cudaEvent_t ev = prof_event(e);
+      CK(cudaEventRecord(ev, cs));
+      e->prof_open[sg.ph] = ev;
+    } else if (sg.cut == CUT_PROF_END && e->prof_open[sg.ph]) {
+      cudaEvent_t ev = prof_event(e);
+      CK(cudaEventRecord(ev, cs));
       e->prof_pending->push_back({sg.ph, e->prof_open[sg.ph], ev, true, e->cur_seq});
       e->prof_open[sg.ph] = nullptr;
     } else if (sg.cut == CUT_EIG) {
       CK(cudaEventRecord(e->eig_ev, e->st));
+      if (e->tail_pending.valid) {   // the previous iteration's tail runs under this eigensolver
+        const rtcur_engine::TailRef t = e->tail_pending;
+        e->tail_pending.valid = false;
+        CK(cudaStreamWaitEvent(e->tail, e->eig_ev, 0));
+        if (int st = launch_tail(e, t, e->tail)) return st;
+        e->join_needed = true;
+        e->join_ev = e->done[t.par];
+      }
+    } else if (sg.cut == CUT_JOIN) {
+      if (e->join_needed) CK(cudaStreamWaitEvent(e->st, e->join_ev, 0));
+      e->join_needed = false;
+    } else if (sg.cut == CUT_STATE) {
+      CK(cudaEventRecord(e->st_ev, e->st));
+      e->st_ev_seq = e->cur_seq;
     }
   }
   return RT_OK;
@@ -768,6 +851,12 @@ static void prof_flush(rtcur_engine* e) {
     if (cudaEventElapsedTime(&ms, p.b, p.e) == cudaSuccess) {
       e->prof_ms[p.ph] += ms;
       e->prof_cnt[p.ph] += 1;
+      // diagnostics (RTCUR_PROF_TIMELINE=1): where each profiled interval sits, relative to
+      // the solve's first iteration, on whichever stream ran it
+      static const bool tl = getenv("RTCUR_PROF_TIMELINE") != nullptr;
+      float t0 = 0.f;
+      if (tl && e->tl_base && cudaEventElapsedTime(&t0, e->tl_base, p.b) == cudaSuccess)
+        fprintf(stderr, "TL seq %u phase %d start_us %.1f dur_us %.1f\n", p.seq, p.ph, 1e3f * t0, 1e3f * ms);
     }
     if (p.owned) {
       e->prof_pool->push_back(p.b);
@@ -888,7 +977,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->st = (cudaStream_t)stream;
   e->lo = slab_lo;
   e->hi = slab_hi;
-  e->cur = e->prev = -1;
+  e->cur = e->prev = e->shadow = -1;
   e->act = e->stg = -1;
   for (int m = 0; m < RT_MAX_MODES; ++m) e->mcopy[m] = nullptr;
   e->idx_ev[0] = e->idx_ev[1] = nullptr;
@@ -944,6 +1033,10 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   CK(cudaEventCreateWithFlags(&e->pre_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->side_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->eig_ev, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&e->tail, cudaStreamNonBlocking));
+
+  CK(cudaEventCreateWithFlags(&e->st_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->main_ev, cudaEventDisableTiming));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -978,8 +1071,9 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   }
   if (e->graphs) {
     for (auto& kv : *e->graphs)
-      for (auto& sg : kv.second.segs)
-        if (sg.exec) cudaGraphExecDestroy(sg.exec);
+      for (auto* v : {&kv.second.segs, &kv.second.tail})
+        for (auto& sg : *v)
+          if (sg.exec) cudaGraphExecDestroy(sg.exec);
     delete e->graphs;
   }
   if (e->cap_st) cudaStreamDestroy(e->cap_st);
@@ -987,6 +1081,9 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   if (e->pre_ev) cudaEventDestroy(e->pre_ev);
   if (e->side_ev) cudaEventDestroy(e->side_ev);
   if (e->eig_ev) cudaEventDestroy(e->eig_ev);
+  if (e->tail) cudaStreamSynchronize(e->tail), cudaStreamDestroy(e->tail);
+  if (e->st_ev) cudaEventDestroy(e->st_ev);
+  if (e->main_ev) cudaEventDestroy(e->main_ev);
   if (e->prof_pool) {
     for (auto ev : *e->prof_pool) cudaEventDestroy(ev);
     delete e->prof_pool;
@@ -1089,6 +1186,7 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
     // also covers every earlier reader of the slot being refilled
     CK(cudaStreamWaitEvent(e->side, e->eig_ev, 0));
   }
+  if (e->npending > 0 || e->cur >= 0) e->r_mode = true;   // a sample staged between iterations: RTCUR-R
   SideScope side_scope(e);
   const Plan& P = e->P;
   const Geom& g = P.g;
@@ -1150,6 +1248,32 @@ extern "C" int rtcur_engine_xblocks_offset(rtcur_engine* e, int64_t* offset) {
 }
 
 static int refresh_xi(rtcur_engine* e, int slot);
+static int run_wcols(rtcur_engine* e, double* sto, int sample_slot);
+static int alloc_slot(rtcur_engine* e);
+
+// Shadow of the running iteration for the sample just staged on the side stream: a copy of
+// its G and A (complete at st_ev, else at the end of its main part) with W evaluated on
+// that sample.  The next iteration thresholds against it (reference solver.py:330-331,
+// _eval_blocks(lcur, idx) on the new draw) without touching the running iterate's own W,
+// which its error pass and the exports still read -- and the evaluation leaves the
+// iteration's critical path.
+static int make_shadow(rtcur_engine* e, int sample_slot) {
+  const Plan& P = e->P;
+  e->shadow = -1;
+  const int sh = alloc_slot(e);
+  if (sh < 0) return RT_OK;   // (no free slot: the next iteration re-evaluates in place)
+  CK(cudaStreamWaitEvent(e->st, e->st_ev_seq == e->cur_of_seq ? e->st_ev : e->main_ev, 0));
+  CK(cudaMemcpyAsync(e->state(sh), e->state(e->cur), (size_t)P.g.blk[0].w_off * 8, cudaMemcpyDeviceToDevice, e->st));
+  e->wt_alt = true;
+  const int st = run_wcols(e, e->state(sh), sample_slot);
+  e->wt_alt = false;
+  if (st) return st;
+  e->shadow = sh;
+  e->shadow_of = e->cur;
+  e->shadow_epoch = e->sample_epoch + 1;
+  e->w_epoch[sh] = e->sample_epoch + 1;
+  return RT_OK;
+}
 
 extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
@@ -1219,6 +1343,10 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   e->xi_valid[slot] = ((P.fiber_mask & ~1u) & ~fg.ximask) == 0;   // (bit 0: the core, no copy)
   if (int st = refresh_xi(e, slot)) return st;
   prof_end(e, PH_GATHER);
+  // staged on the side stream behind a running iteration: evaluate that iterate on this sample too
+  static const bool shadow_on = [] { const char* v = getenv("RTCUR_SHADOW"); return !(v && v[0] == '0'); }();
+  if (shadow_on && e->staging_on_side && e->npending > 0 && e->cur >= 0 && e->stg == slot && e->use_graphs)
+    if (int st = make_shadow(e, slot)) return st;
   return RT_OK;
 }
 
@@ -1313,10 +1441,10 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
   a.l_out = l_out;
   if (sums) {
     a.partial = e->at<double>(P.o_bpart);
-    a.sums = e->at<double>(P.o_sums);
+    a.sums = e->at<double>(P.o_sums + e->roff());
     a.counter = e->at<unsigned int>(P.o_counters);
   }
-  a.nonfinite = e->at<int>(P.o_nonfinite);
+  a.nonfinite = e->at<int>(P.o_nonfinite + e->roff());
   prof_begin(e, phase);
   const i64 smb = bp_smem_bytes(P.bp);
   const bool hs = st_s != nullptr, he = st_e != nullptr;
@@ -1408,7 +1536,7 @@ static SvdArgs make_svd_args(rtcur_engine* e) {
     sa.perm[m] = e->at<int>(P.o_perm[m]);
     sa.degen[m] = e->at<int>(P.o_degen[m]);
   }
-  sa.flags = e->at<int>(P.o_flags);
+  sa.flags = e->at<int>(P.o_flags + e->roff());
   sa.hchunk = P.hchunk;
   return sa;
 }
@@ -1528,14 +1656,14 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ea.warm_d[m] = P.g.dim[m];
   }
   // the next sample's prefetch (side stream) may start now: it overlaps the eigensolver
-  if (e->capturing) {
-    if (e->use_side) cap_cut(e, CUT_EIG, 0);
-  } else {
-    CK(cudaEventRecord(e->eig_ev, e->st));
-  }
+  if (e->capturing) cap_cut(e, CUT_EIG, 0);
+  else CK(cudaEventRecord(e->eig_ev, e->st));
   prof_begin(e, PH_EIG);
   if (int st = launch_eig(ea, P.s, n, esm, e->st)) return st;
   prof_end(e, PH_EIG);
+  // the previous iteration's tail (enqueued under this eigensolver) sets the stop flag:
+  // everything from here on must see it
+  if (e->capturing) cap_cut(e, CUT_JOIN, 0);
   prof_begin(e, PH_SVDPOST);
   SvdArgs sa = make_svd_args(e);
   unsigned int* hcnt = e->at<unsigned int>(P.o_counters) + 16;
@@ -1565,8 +1693,8 @@ static int run_wchain(rtcur_engine* e, const double* sto, const int* const* rows
     CK(cudaMemcpyAsync(dst, sto, g.gsize * 8, cudaMemcpyDeviceToDevice, e->st));
     return RT_OK;
   }
-  double* t0 = e->at<double>(P.o_wt0);
-  double* t1 = e->at<double>(P.o_wt1);
+  double* t0 = e->at<double>(e->wt_alt ? P.o_wt0s : P.o_wt0);
+  double* t1 = e->at<double>(e->wt_alt ? P.o_wt1s : P.o_wt1);
   const double* in = sto;   // G
   i64 rho = g.rank[0];
   for (int m = 1; m < n; ++m) {
@@ -1585,10 +1713,10 @@ static int run_wchain(rtcur_engine* e, const double* sto, const int* const* rows
 
 // W_b of every block column for state `sto`: the core by the separable chain,
 // the fiber blocks (arbitrary multi-indices) by k_wcols
-static int run_wcols(rtcur_engine* e, double* sto) {
+static int run_wcols(rtcur_engine* e, double* sto, int sample_slot) {
   const Plan& P = e->P;
   const Geom& g = P.g;
-  IndexPtrs ip = make_ip(e);
+  IndexPtrs ip = make_ip_slot(e, sample_slot);
   prof_begin(e, PH_WCOLS);
   // large cores: separable chain (r_m FMAs per output); small ones stay in the
   // single k_wcols launch (launch overhead dominates there)
@@ -1681,7 +1809,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     // leave its partial slot unwritten while the reduction reads it
     const int apg = (int)std::max<i64>(1, std::min<i64>(P.ap_grid, tma.first[g.nblk] - tma.first[1]));
     pa.ap_grid = apg;
-    pa.nonfinite = e->at<int>(P.o_nonfinite);
+    pa.nonfinite = e->at<int>(P.o_nonfinite + e->roff());
     const i64 smb = bp_smem_bytes(P.bp_ap);
 #define AP_LAUNCH(RB)                                                                                  \
   (st_s ? launch_ap(k_block_pass<true, false, false, false, false, RB, true>, apg, P.ap_threads, smb, e->st, g, tma, ip, pa, \
@@ -1716,7 +1844,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     fl.apart = e->at<double>(P.o_fapart);
     fl.apart_cap = P.fapart_cap;
     fl.a_out = sto;
-    fl.nonfinite = e->at<int>(P.o_nonfinite);
+    fl.nonfinite = e->at<int>(P.o_nonfinite + e->roff());
     const int fst = fiber_pass_launch(fl, e->st);
     if (fst < 0) return fail(RT_ERR_CUDA, std::string("k_fiber_pass (A): ") + cudaGetErrorString((cudaError_t)(-fst)));
     rtcur_launch_counter_add((unsigned long long)fst);
@@ -1747,7 +1875,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     pa.zetap = e->zetap_cur;
     pa.U = gp.U[0];
     pa.t1 = gp.t1;
-    pa.nonfinite = e->at<int>(P.o_nonfinite);
+    pa.nonfinite = e->at<int>(P.o_nonfinite + e->roff());
     const BPGeom& G = P.bp_gp;
     const i64 smb = bp_smem_bytes(G);
     if (P.core_k) {
@@ -1795,8 +1923,15 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     }
   }
   prof_end(e, PH_GPASS);
+  // G and A of the new iterate are complete: the side stream may evaluate it on the next sample
+  if (e->capturing) {
+    if (e->r_mode) cap_cut(e, CUT_STATE, 0);
+  } else {
+    CK(cudaEventRecord(e->st_ev, e->st));
+    e->st_ev_seq = e->cur_seq;
+  }
   // W for every block column
-  return run_wcols(e, sto);   // (w_epoch of the new slot is set by the caller)
+  return run_wcols(e, sto, e->act_slot());   // (w_epoch of the new slot is set by the caller)
 }
 
 // Device-side stop rule: the sampled relative error from the per-block sums, in the
@@ -1820,29 +1955,35 @@ static __global__ void k_stop_check(const double* sums, int nblk, const double* 
 
 #define RES_SLOT 96   // doubles between the two result slots in h_pinned (zeta/eps slots at 200 + 4 par)
 
-// The launch sequence of one iteration (captured into CUDA graph segments per launch
-// shape).  Pure stream work: host-side bookkeeping stays in the caller.
-static int iterate_body(rtcur_engine* e, const double* st_s, int newslot, bool reeval, int par) {
+// The launch sequence of one iteration, in two parts (each captured into CUDA graph
+// segments per launch shape).  Pure stream work: host-side bookkeeping stays in the caller.
+// Main part: everything the NEXT iteration's threshold depends on.
+static int iterate_main(rtcur_engine* e, const double* st_s, int newslot, bool reeval, int par) {
   const Plan& P = e->P;
-  const int n = P.g.n;
   const double zeta = e->zeta_last;   // (kernels read the device copy when zetap_cur is set)
-  CK(cudaMemcpyAsync(e->ws + P.o_zeta, e->h_pinned + 200 + 4 * par, 16, cudaMemcpyHostToDevice, e->st));
-  CK(cudaMemsetAsync(e->ws + P.o_nonfinite, 0, 4, e->st));
+  CK(cudaMemcpyAsync(e->ws + P.o_zeta + 32 * par, e->h_pinned + 200 + 4 * par, 16, cudaMemcpyHostToDevice, e->st));
+  CK(cudaMemsetAsync(e->ws + P.o_nonfinite + e->roff(), 0, 4, e->st));
   int st;
-  // RTCUR-R: the sample moved, re-evaluate the previous iterate on it
-  // (reference solver.py:330-331, _eval_blocks(lcur, idx) on the new draw)
-  if (reeval && (st = run_wcols(e, e->state(e->cur)))) return st;
+  // RTCUR-R without a shadow state: the sample moved, re-evaluate the previous iterate on
+  // it in place (reference solver.py:330-331, _eval_blocks(lcur, idx) on the new draw)
+  if (reeval && (st = run_wcols(e, e->state(e->cur), e->act_slot()))) return st;
   if ((st = refresh_xi(e, e->act_slot()))) return st;
   if ((st = run_block_pass(e, st_s, nullptr, zeta, true, nullptr, nullptr, nullptr, false, PH_THRESH))) return st;
   if ((st = run_svd(e, st_s))) return st;
-  if ((st = run_factors(e, st_s, zeta, newslot))) return st;
-  if ((st = run_block_pass(e, st_s, e->state(newslot), zeta, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
+  return run_factors(e, st_s, zeta, newslot);
+}
+
+// Tail: the sampled error of the new iterate, the stop rule, the result copy.
+static int iterate_tail(rtcur_engine* e, const double* st_s, int newslot, int par) {
+  const Plan& P = e->P;
+  int st;
+  if ((st = run_block_pass(e, st_s, e->state(newslot), e->zeta_last, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
     return st;
-  (void)n;
-  k_stop_check<<<1, 32, 0, e->st>>>(e->at<double>(P.o_sums), P.g.nblk, e->at<double>(P.o_zeta), stop_flag(e),
-                                    e->at<int>(P.o_nonfinite + 4));
+  k_stop_check<<<1, 32, 0, e->st>>>(e->at<double>(P.o_sums + e->roff()), P.g.nblk, e->at<double>(P.o_zeta + 32 * par),
+                                    stop_flag(e), e->at<int>(P.o_nonfinite + 4 + e->roff()));
   LAUNCH_CHECK();
-  CK(cudaMemcpyAsync(e->h_pinned + par * RES_SLOT, e->ws + P.o_sums, P.res_bytes, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaMemcpyAsync(e->h_pinned + par * RES_SLOT, e->ws + P.o_sums + e->roff(), P.res_bytes, cudaMemcpyDeviceToHost,
+                     e->st));
   return RT_OK;
 }
 
@@ -1854,34 +1995,41 @@ static inline bool fiber_refresh_pending(const rtcur_engine* e) {
   return e->P.fiber_mask && !e->xi_valid[e->act_slot()];
 }
 
-// capture one iteration into `ge`
+// capture one iteration into `ge`: the main part's segments, then the tail's
 static int capture_iteration(rtcur_engine* e, GraphEntry& ge, const double* st_s, int newslot, bool reeval, int par) {
   e->cap_entry = &ge;
   e->cap_err = (int)cudaSuccess;
   cudaStream_t saved = e->st;
   e->st = e->cap_st;
   e->capturing = true;
-  const unsigned long long l0 = rtcur_launch_counter_add(0);
   int st = RT_OK;
-  cudaError_t ce = seg_begin(e);
-  if (ce == cudaSuccess) {
-    st = iterate_body(e, st_s, newslot, reeval, par);
-    ge.nkernels = rtcur_launch_counter_add(0) - l0;
-    g_launches.fetch_sub(ge.nkernels);   // capturing executes nothing
+  cudaError_t ce = cudaSuccess;
+  for (int part = 0; part < 2 && st == RT_OK && ce == cudaSuccess; ++part) {
+    e->cap_segs = part == 0 ? &ge.segs : &ge.tail;
+    const unsigned long long l0 = rtcur_launch_counter_add(0);
+    ce = seg_begin(e);
+    if (ce != cudaSuccess) break;
+    st = part == 0 ? iterate_main(e, st_s, newslot, reeval, par) : iterate_tail(e, st_s, newslot, par);
+    const unsigned long long nk = rtcur_launch_counter_add(0) - l0;
+    g_launches.fetch_sub(nk);   // capturing executes nothing
+    (part == 0 ? ge.nkernels : ge.nk_tail) = nk;
     ce = seg_end(e, CUT_NONE, 0);
     if (ce == cudaSuccess) ce = (cudaError_t)e->cap_err;
   }
   e->capturing = false;
   e->st = saved;
   e->cap_entry = nullptr;
+  e->cap_segs = nullptr;
   if (ce != cudaSuccess || st != RT_OK) {
     cudaGraph_t junk = nullptr;
     cudaStreamEndCapture(e->cap_st, &junk);   // leave no capture open
     if (junk) cudaGraphDestroy(junk);
     cudaGetLastError();
-    for (auto& sg : ge.segs)
-      if (sg.exec) cudaGraphExecDestroy(sg.exec);
-    ge.segs.clear();
+    for (auto* v : {&ge.segs, &ge.tail}) {
+      for (auto& sg : *v)
+        if (sg.exec) cudaGraphExecDestroy(sg.exec);
+      v->clear();
+    }
     if (st) return st;
     return fail(RT_ERR_CUDA, std::string("iteration capture: ") + cudaGetErrorString(ce));
   }
@@ -1899,21 +2047,39 @@ extern "C" int rtcur_engine_set_eps(rtcur_engine* e, double eps) {
   return RT_OK;
 }
 
+// a state slot nothing still reads: not the latest iterate, its threshold state, the
+// shadow, nor (while a speculative iteration may be cancelled) what the iteration before
+// it would fall back to
+static int alloc_slot(rtcur_engine* e) {
+  for (int t = 0; t < RT_STATE_SLOTS; ++t) {
+    const int s = (e->alloc_rr + t) % RT_STATE_SLOTS;
+    if (s == e->cur || s == e->prev || s == e->shadow) continue;
+    if (e->snap_valid && (s == e->snap.cur || s == e->snap.prev || s == e->snap.shadow)) continue;
+    e->alloc_rr = (s + 1) % RT_STATE_SLOTS;
+    return s;
+  }
+  return -1;
+}
+
+static void take_snapshot(rtcur_engine* e) {
+  auto& sn = e->snap;
+  sn.cur = e->cur; sn.prev = e->prev; sn.act = e->act; sn.stg = e->stg; sn.sample_epoch = e->sample_epoch;
+  for (int i = 0; i < RT_STATE_SLOTS; ++i) sn.w_epoch[i] = e->w_epoch[i];
+  sn.shadow = e->shadow; sn.shadow_of = e->shadow_of; sn.shadow_epoch = e->shadow_epoch; sn.alloc_rr = e->alloc_rr;
+  sn.zeta_last = e->zeta_last;
+  sn.xi_valid[0] = e->xi_valid[0]; sn.xi_valid[1] = e->xi_valid[1];
+  e->snap_valid = true;
+  e->snap_seq = e->launch_seq + 1;
+}
+
 extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int first) {
   if (!e || !e->sampled) return fail(RT_ERR_VALUE, "engine has no sample");
   if (e->npending >= 2) return fail(RT_ERR_VALUE, "two iterations already in flight");
   const bool spec = e->npending == 1;
   if (spec && (first || !can_speculate(e))) return fail(RT_ERR_VALUE, "previous iteration not waited for");
   if (!(zeta >= 0.0)) return fail(RT_ERR_VALUE, "threshold must be nonnegative");
-  if (spec) {   // what rtcur_engine_iterate_cancel restores
-    auto& sn = e->snap;
-    sn.cur = e->cur; sn.prev = e->prev; sn.act = e->act; sn.stg = e->stg; sn.sample_epoch = e->sample_epoch;
-    for (int i = 0; i < 3; ++i) sn.w_epoch[i] = e->w_epoch[i];
-    sn.zeta_last = e->zeta_last;
-    sn.xi_valid[0] = e->xi_valid[0]; sn.xi_valid[1] = e->xi_valid[1];
-    e->snap_valid = true;
-    e->snap_seq = e->launch_seq + 1;
-  }
+  if (spec) take_snapshot(e);   // what rtcur_engine_iterate_cancel restores
+  else e->snap_valid = false;
   e->cur_seq = ++e->launch_seq;
   if (e->staging_on_side) {   // the prefetched sample's staging must be complete
     CK(cudaStreamWaitEvent(e->st, e->side_ev, 0));
@@ -1928,62 +2094,94 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   // prefetch into the other sample slot must wait for
   CK(cudaEventRecord(e->pre_ev, e->st));
   if (first) {
-    e->cur = e->prev = -1;
+    if (int st = flush_tail(e)) return st;   // (a previous solve's)
+    e->cur = e->prev = e->shadow = -1;
+    e->r_mode = false;
+    e->join_needed = false;
+    if (e->prof_on && getenv("RTCUR_PROF_TIMELINE")) {
+      if (!e->tl_base) cudaEventCreate(&e->tl_base);
+      CK(cudaEventRecord(e->tl_base, e->st));
+    }
     CK(cudaMemsetAsync(stop_flag(e), 0, 4, e->st));   // a new solve: the previous one's stop flag
   }
-  const double* st_s = (e->cur >= 0) ? e->state(e->cur) : nullptr;
-  int newslot = 0;
-  while (newslot == e->cur || newslot == e->prev) ++newslot;
-  const bool reeval = e->cur >= 0 && e->w_epoch[e->cur] != e->sample_epoch;
+  // the threshold state: the shadow (a copy of the latest iterate evaluated on the sample
+  // that just became active) when the side stream prepared one, else the latest iterate
+  // itself, re-evaluated in place when the sample moved
+  const bool use_shadow = e->cur >= 0 && e->shadow >= 0 && e->shadow_of == e->cur && e->shadow_epoch == e->sample_epoch;
+  const int st_slot = e->cur < 0 ? -1 : (use_shadow ? e->shadow : e->cur);
+  const double* st_s = st_slot >= 0 ? e->state(st_slot) : nullptr;
+  const bool reeval = st_slot >= 0 && !use_shadow && e->w_epoch[e->cur] != e->sample_epoch;
+  // an in-place re-evaluation overwrites the W the previous iteration's error pass reads,
+  // and without graphs nothing is deferred: that tail goes first, in stream order
+  if (reeval || !e->use_graphs)
+    if (int st = flush_tail(e)) return st;
+  if (use_shadow) e->shadow = -1;   // consumed: it is this iteration's threshold state from here on
+  const int keep_prev = e->prev;
+  e->prev = st_slot;                // (so the allocator keeps it)
+  const int newslot = alloc_slot(e);
+  e->prev = keep_prev;
+  if (newslot < 0) return fail(RT_ERR_VALUE, "no free iterate slot");
   const int par = e->par;
+  e->cur_par = par;
   e->zeta_last = zeta;
   e->h_pinned[200 + 4 * par] = zeta;   // read by the iteration's first (memcpy) node
   e->h_pinned[200 + 4 * par + 1] = e->eps;
-  e->zetap_cur = e->at<double>(e->P.o_zeta);
-  int st = RT_OK;
+  e->zetap_cur = e->at<double>(e->P.o_zeta + 32 * par);
   // the iteration's kernels test the stop flag (Geom::stop is copied into every launch)
   e->P.g.stop = stop_flag(e);
+  int st = RT_OK;
+  auto leave = [&](int code) {
+    e->zetap_cur = nullptr;
+    e->P.g.stop = nullptr;
+    e->cur_seq = 0;
+    return code;
+  };
   if (e->use_graphs) {
-    const unsigned long long key = (unsigned long long)(e->cur + 1) | ((unsigned long long)newslot << 2) |
-                                   ((unsigned long long)e->act_slot() << 4) | ((unsigned long long)reeval << 5) |
-                                   ((unsigned long long)fiber_refresh_pending(e) << 6) |
-                                   ((unsigned long long)par << 7) |
-                                   ((unsigned long long)(e->prof_on ? (e->prof_mask & kIterPhases) : 0u) << 8) |
-                                   ((unsigned long long)e->use_side << 41);
+    const unsigned long long key = (unsigned long long)(e->cur + 1) | ((unsigned long long)(st_slot + 1) << 3) |
+                                   ((unsigned long long)newslot << 6) | ((unsigned long long)e->act_slot() << 9) |
+                                   ((unsigned long long)reeval << 10) |
+                                   ((unsigned long long)fiber_refresh_pending(e) << 11) |
+                                   ((unsigned long long)par << 12) | ((unsigned long long)e->r_mode << 13) |
+                                   ((unsigned long long)(e->prof_on ? (e->prof_mask & kIterPhases) : 0u) << 16);
     auto it = e->graphs->find(key);
     if (it == e->graphs->end()) {
       GraphEntry ge;
       st = capture_iteration(e, ge, st_s, newslot, reeval, par);
-      if (st != RT_OK) {
-        e->zetap_cur = nullptr;
-        e->P.g.stop = nullptr;
-        return st;
-      }
+      if (st != RT_OK) return leave(st);
       it = e->graphs->emplace(key, std::move(ge)).first;
     }
     st = launch_entry(e, it->second);
-    if (st) {
-      e->zetap_cur = nullptr;
-      e->P.g.stop = nullptr;
-      return st;
-    }
+    if (st) return leave(st);
     rtcur_launch_counter_add(it->second.nkernels);   // the graph's kernels run now
+    // the tail is held back: the next iteration enqueues it under its eigensolver, or
+    // iterate_wait sends it out in stream order
+    if (int fst = flush_tail(e)) return leave(fst);   // (one not taken at CUT_EIG: cannot happen, kept for safety)
+    e->tail_pending.ge = &it->second;
+    e->tail_pending.par = par;
+    e->tail_pending.seq = e->cur_seq;
+    e->tail_pending.valid = true;
+    // Policy (RTCUR_TAIL_DEFER=0|1 overrides): always for RTCUR-F; for RTCUR-R only while the
+    // sampled blocks are small -- there the next sample's gather already runs under the
+    // eigensolver, and at config 4 (87 MB of blocks, a 116 us gather against a 72 us
+    // eigensolver) adding the error pass to it stalled the join (13.9 vs 12.7 ms per solve)
+    static const int defer_env = [] { const char* v = getenv("RTCUR_TAIL_DEFER"); return v ? atoi(v) : -1; }();
+    const bool defer = defer_env >= 0 ? defer_env != 0
+                                      : (!e->r_mode || e->P.g.nblk_total * e->P.esize <= ((i64)48 << 20));
+    if (!defer)
+      if (int fst = flush_tail(e)) return leave(fst);
   } else {
-    st = iterate_body(e, st_s, newslot, reeval, par);
-    if (st) {
-      e->zetap_cur = nullptr;
-      e->P.g.stop = nullptr;
-      return st;
-    }
+    st = iterate_main(e, st_s, newslot, reeval, par);
+    if (st == RT_OK) st = iterate_tail(e, st_s, newslot, par);
+    if (st) return leave(st);
+    CK(cudaEventRecord(e->done[par], e->st));
   }
-  e->zetap_cur = nullptr;
-  e->P.g.stop = nullptr;
-  e->cur_seq = 0;
-  CK(cudaEventRecord(e->done[par], e->st));
+  leave(RT_OK);
+  CK(cudaEventRecord(e->main_ev, e->st));
   if (reeval) e->w_epoch[e->cur] = e->sample_epoch;
   e->w_epoch[newslot] = e->sample_epoch;
-  e->prev = e->cur;
+  e->prev = st_slot;
   e->cur = newslot;
+  e->cur_of_seq = e->launch_seq;
   e->pend_par[e->npending++] = par;
   e->par ^= 1;
   return RT_OK;
@@ -1992,6 +2190,9 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
 extern "C" int rtcur_engine_iterate_wait(rtcur_engine* e, double* sums, int* flags) {
   if (!e || e->npending < 1) return fail(RT_ERR_VALUE, "no iteration in flight");
   const int par = e->pend_par[0];
+  // its tail is still held back when no iteration was enqueued behind it
+  if (e->npending == 1 && e->tail_pending.valid && e->tail_pending.par == par)
+    if (int st = flush_tail(e)) return st;
   e->pend_par[0] = e->pend_par[1];
   e->npending--;
   CK(cudaEventSynchronize(e->done[par]));
@@ -2018,11 +2219,13 @@ extern "C" int rtcur_engine_iterate_cancel(rtcur_engine* e) {
   if (!e || e->npending != 1 || !e->snap_valid) return fail(RT_ERR_VALUE, "no speculative iteration to cancel");
   const auto& sn = e->snap;
   e->cur = sn.cur; e->prev = sn.prev; e->act = sn.act; e->stg = sn.stg; e->sample_epoch = sn.sample_epoch;
-  for (int i = 0; i < 3; ++i) e->w_epoch[i] = sn.w_epoch[i];
+  for (int i = 0; i < RT_STATE_SLOTS; ++i) e->w_epoch[i] = sn.w_epoch[i];
+  e->shadow = sn.shadow; e->shadow_of = sn.shadow_of; e->shadow_epoch = sn.shadow_epoch; e->alloc_rr = sn.alloc_rr;
   e->zeta_last = sn.zeta_last;
   e->xi_valid[0] = sn.xi_valid[0]; e->xi_valid[1] = sn.xi_valid[1];
   e->snap_valid = false;
   e->npending = 0;
+  e->tail_pending.valid = false;   // its tail is never enqueued
   // its profiled phases measured empty segments: drop them
   {
     std::vector<ProfPair> keep;

@@ -86,6 +86,19 @@ PINNED_RESULTS = os.environ.get("RTCUR_PINNED_RESULTS", "1") != "0"
 CREATED = [0]   # engines constructed in this process (diagnostics: pooled solves construct none)
 
 
+def marshal_sample(idx):
+    """The C-ABI view of a SampleIndices: per-mode int64 pointer arrays (and the arrays
+    they point into).  The RTCUR-R sampler thread builds it right after the draw, so the
+    solve loop's set_sample is the native call alone (the marshalling was ~30 us of an
+    ~80 us call on the loop's critical host path)."""
+    n = len(idx.rows)
+    rows = [np.ascontiguousarray(r, dtype=np.int64) for r in idx.rows]
+    cols = [np.ascontiguousarray(c, dtype=np.int64) for c in idx.cols]
+    rp = (nat.c_i64p * n)(*[r.ctypes.data_as(nat.c_i64p) for r in rows])
+    cp = (nat.c_i64p * n)(*[c.ctypes.data_as(nat.c_i64p) for c in cols])
+    return rp, cp, (rows, cols)
+
+
 class Engine:
     def __init__(self, shape, ranks, row_sizes, col_sizes, dtype, slab=None, device=None):
         import torch
@@ -212,13 +225,12 @@ class Engine:
         nat.check(self.lib.rtcur_engine_absmax_end(self.handle, ctypes.byref(out)))
         return float(out.value)
 
-    def set_sample(self, idx):
-        rows = [np.ascontiguousarray(r, dtype=np.int64) for r in idx.rows]
-        cols = [np.ascontiguousarray(c, dtype=np.int64) for c in idx.cols]
-        rp = (nat.c_i64p * self.n)(*[r.ctypes.data_as(nat.c_i64p) for r in rows])
-        cp = (nat.c_i64p * self.n)(*[c.ctypes.data_as(nat.c_i64p) for c in cols])
+    def set_sample(self, idx, view=None):
+        """Upload a sample's index sets; ``view``: its marshal_sample() result when the
+        caller prepared it ahead of time (the RTCUR-R sampler thread does)."""
+        rp, cp, keep = view if view is not None else marshal_sample(idx)
         nat.check(self.lib.rtcur_engine_set_sample(self.handle, rp, cp))
-        self._keep = (rows, cols)
+        self._keep = keep
 
     def gather(self):
         nat.check(self.lib.rtcur_engine_gather(self.handle))

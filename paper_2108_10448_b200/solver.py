@@ -29,6 +29,7 @@ from typing import Protocol, Sequence
 import numpy as np
 
 from . import _native as nat
+from .engine import marshal_sample  # noqa: E402
 from .engine import Engine, acquire_engine, release_engine
 from .fiber_cur import FiberCur, SampleIndices, TruncatedSvd, draw_sample_indices, sample_sizes
 from .tensor import DenseTensor, DeviceTensor, as_shape
@@ -540,6 +541,7 @@ class _AheadSampler:
         import threading
 
         self._args = (shape, row_sizes, col_sizes, rng)
+        self.views = {}   # id(sample) -> its marshalled view, taken by the loop's set_sample
         self._q = queue.Queue(maxsize=depth)
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, name="rtcur-sampler", daemon=True)
@@ -552,6 +554,7 @@ class _AheadSampler:
         while not self._stop.is_set():
             try:
                 item = draw_sample_indices(shape, row_sizes, col_sizes, rng)
+                self.views[id(item)] = marshal_sample(item)   # the C-ABI view, off the loop's thread
             except BaseException as exc:   # surfaced by next()
                 item = exc
             while not self._stop.is_set():
@@ -632,13 +635,14 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                    if cfg.variant == "R" and cfg.max_iters > 1 and os.environ.get("RTCUR_AHEAD_SAMPLER", "1") != "0"
                    else None)
         draw = sampler.next if sampler is not None else (lambda: draw_sample_indices(shape, row_sizes, col_sizes, rng))
+        views = sampler.views if sampler is not None else {}
         t0 = time.perf_counter()
         idx = draw()
         timings["sample"] += time.perf_counter() - t0
         if _TIMELINE is not None:
             _TIMELINE.append(("first_draw", 0, time.perf_counter()))
         t0 = time.perf_counter()
-        eng.set_sample(idx)
+        eng.set_sample(idx, views.pop(id(idx), None))
         src.load_blocks(eng, idx)
         timings["gather"] += time.perf_counter() - t0
 
@@ -684,7 +688,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                 timings["sample"] += time.perf_counter() - t1
                 if prefetch:
                     t1 = time.perf_counter()
-                    eng.set_sample(nxt)
+                    eng.set_sample(nxt, views.pop(id(nxt), None))
                     src.load_blocks(eng, nxt)
                     staged = True
                     timings["gather"] += time.perf_counter() - t1
@@ -726,7 +730,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
             if not ahead:
                 if resample and not staged:
                     t1 = time.perf_counter()
-                    eng.set_sample(idx)
+                    eng.set_sample(idx, views.pop(id(idx), None))
                     src.load_blocks(eng, idx)
                     timings["gather"] += time.perf_counter() - t1
                 if _TIMELINE is not None:
