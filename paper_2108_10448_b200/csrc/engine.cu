@@ -103,6 +103,7 @@ static int rbucket(int r) { return r <= 4 ? 4 : r <= 8 ? 8 : r <= 16 ? 16 : 32; 
     }                                                                                \
   } while (0)
 
+#define RT_SAMPLE_SLOTS 3  // sample ring: the running iteration's, the next one's (staged), the one being staged
 #define RT_STATE_SLOTS 6   // iterate ring: latest, its threshold state, a shadow, the speculative pair + 1
 
 struct Plan {
@@ -498,7 +499,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
     P.o_xi = take(P.fiber_mask ? xo * P.esize + 64 : 8);
   }
   P.samp_delta = o - samp0;
-  take(P.samp_delta - 8);   // slot 1 (aligned like slot 0)
+  for (int s = 1; s < RT_SAMPLE_SLOTS; ++s) take(P.samp_delta - 8);   // slots 1.. (aligned like slot 0)
   P.o_state = take((i64)RT_STATE_SLOTS * g.state_doubles * 8);
   P.o_zeta = take(64);   // per launch parity p, at +32 p: zeta | eps; the stop flag at +16
   for (int m = 0; m < n; ++m) P.o_M[m] = take(row_sizes[m] * col_sizes[m] * 8);
@@ -657,7 +658,7 @@ struct rtcur_engine {
   struct Snap {
     int cur, prev, act, stg, sample_epoch, w_epoch[RT_STATE_SLOTS], shadow, shadow_of, shadow_epoch, alloc_rr;
     double zeta_last;
-    bool xi_valid[2];
+    bool xi_valid[RT_SAMPLE_SLOTS];
   } snap;
   bool snap_valid;
   unsigned launch_seq, cur_seq, snap_seq;   // iteration launches so far; the one being enqueued; the speculative one
@@ -668,7 +669,7 @@ struct rtcur_engine {
   int* h_flags;
   i64* h_idx;        // pinned staging for index upload (one half per sample slot)
   i64 h_idx_len;
-  cudaEvent_t idx_ev[2];   // H2D of each slot's index staging done
+  cudaEvent_t idx_ev[RT_SAMPLE_SLOTS];   // H2D of each slot's index staging done
   // optional per-phase CUDA-event timing (rtcur_engine_profile)
   bool prof_on;
   unsigned prof_mask;  // phases timed while prof_on
@@ -686,7 +687,7 @@ struct rtcur_engine {
   std::vector<GraphSeg>* cap_segs; // the list the capture appends to (cap_entry->segs or ->tail)
   int cap_err;                     // first error inside a capture cut (prof_begin/prof_end are void)
   const double* zetap_cur;         // device zeta while an iteration body is enqueued/captured
-  bool xi_valid[2];                // the sample slot's intersection copies match its blocks
+  bool xi_valid[RT_SAMPLE_SLOTS];  // the sample slot's intersection copies match its blocks
   cudaEvent_t absmax_ev;           // rtcur_engine_absmax_begin's D2H done
   bool absmax_pending;
   ShardState* shard;               // mode-1 slab exchange plan (rtcur_engine_set_shards), or null
@@ -705,7 +706,7 @@ struct rtcur_engine {
   template <typename T> T* at(i64 off) const { return reinterpret_cast<T*>(ws + off); }
   double* state(int slot) const { return at<double>(P.o_state) + (i64)slot * P.g.state_doubles; }
   i64 roff() const { return (i64)cur_par * P.res_stride; }   // this launch's copy of the result range
-  i64 sd(int slot) const { return slot > 0 ? P.samp_delta : 0; }   // byte shift of a sample slot
+  i64 sd(int slot) const { return (i64)slot * P.samp_delta; }   // byte shift of a sample slot
   int act_slot() const { return act >= 0 ? act : 0; }
   char* xb(int slot) const { return ws + P.o_xb + sd(slot); }
 };
@@ -980,7 +981,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   e->cur = e->prev = e->shadow = -1;
   e->act = e->stg = -1;
   for (int m = 0; m < RT_MAX_MODES; ++m) e->mcopy[m] = nullptr;
-  e->idx_ev[0] = e->idx_ev[1] = nullptr;
+  for (int s = 0; s < RT_SAMPLE_SLOTS; ++s) e->idx_ev[s] = nullptr;
   e->prof_mask = ~0u;
   e->use_fast = getenv("RTCUR_NO_FAST_EIG") == nullptr;
   e->prof_pool = new std::vector<cudaEvent_t>();
@@ -1014,14 +1015,14 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   // per sample slot: the byte span of the device index range (rows + cols with the carve's padding)
   const i64 idx_span = e->P.o_cols[n - 1] + col_sizes[n - 1] * 8 - e->P.o_rows[0];
   e->h_idx_len = (idx_span + 7) / 8;
-  ce = cudaMallocHost(&e->h_idx, 2 * (e->h_idx_len * 8 + 64));
+  ce = cudaMallocHost(&e->h_idx, RT_SAMPLE_SLOTS * (e->h_idx_len * 8 + 64));
   if (ce != cudaSuccess) { cudaFreeHost(e->h_pinned); delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   // counters + col offsets
   CK(cudaMemsetAsync(e->ws + e->P.o_counters, 0, 64 * 4, e->st));
   // zero the compact blocks once: the alignment pads between blocks are never
   // written by the gather and must not carry garbage into rank all-reduces
-  for (int s = 0; s < 2; ++s) CK(cudaMemsetAsync(e->xb(s), 0, e->P.g.nblk_total * e->P.esize + 64, e->st));
-  for (int s = 0; s < 2; ++s) CK(cudaEventCreateWithFlags(&e->idx_ev[s], cudaEventDisableTiming));
+  for (int s = 0; s < RT_SAMPLE_SLOTS; ++s) CK(cudaMemsetAsync(e->xb(s), 0, e->P.g.nblk_total * e->P.esize + 64, e->st));
+  for (int s = 0; s < RT_SAMPLE_SLOTS; ++s) CK(cudaEventCreateWithFlags(&e->idx_ev[s], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->absmax_ev, cudaEventDisableTiming));
   {
     // on by default (with the speculative pipeline: config 1 +5 %, config 4 +12 %,
@@ -1059,7 +1060,7 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   for (int s = 0; s < 2; ++s)
     if (e->done[s]) cudaEventDestroy(e->done[s]);
   if (e->absmax_ev) cudaEventDestroy(e->absmax_ev);
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < RT_SAMPLE_SLOTS; ++s)
     if (e->idx_ev[s]) cudaEventDestroy(e->idx_ev[s]);
   if (e->prof_pending) {
     for (auto& p : *e->prof_pending)
@@ -1194,7 +1195,13 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
   // the next sample goes to the inactive slot (stream-ordered after the running
   // iteration, which keeps reading the active one); its pinned index staging is
   // free once that slot's previous upload has completed
-  const int slot = e->stg >= 0 ? e->stg : (e->act < 0 ? 0 : (e->act ^ 1));
+  // the slot: the staged one again, else one that is neither the active sample nor (while a
+  // speculative iteration may be cancelled) the sample the solve would fall back to
+  int slot = e->stg;
+  if (slot < 0) {
+    slot = 0;
+    while (slot == e->act || (e->snap_valid && slot == e->snap.act)) ++slot;
+  }
   CK(cudaEventSynchronize(e->idx_ev[slot]));
   i64* h_idx = e->h_idx + (size_t)slot * (e->h_idx_len + 8);
   const i64 sdl = e->sd(slot);
@@ -2067,7 +2074,7 @@ static void take_snapshot(rtcur_engine* e) {
   for (int i = 0; i < RT_STATE_SLOTS; ++i) sn.w_epoch[i] = e->w_epoch[i];
   sn.shadow = e->shadow; sn.shadow_of = e->shadow_of; sn.shadow_epoch = e->shadow_epoch; sn.alloc_rr = e->alloc_rr;
   sn.zeta_last = e->zeta_last;
-  sn.xi_valid[0] = e->xi_valid[0]; sn.xi_valid[1] = e->xi_valid[1];
+  for (int s = 0; s < RT_SAMPLE_SLOTS; ++s) sn.xi_valid[s] = e->xi_valid[s];
   e->snap_valid = true;
   e->snap_seq = e->launch_seq + 1;
 }
@@ -2138,7 +2145,7 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   };
   if (e->use_graphs) {
     const unsigned long long key = (unsigned long long)(e->cur + 1) | ((unsigned long long)(st_slot + 1) << 3) |
-                                   ((unsigned long long)newslot << 6) | ((unsigned long long)e->act_slot() << 9) |
+                                   ((unsigned long long)newslot << 6) | ((unsigned long long)e->act_slot() << 14) |
                                    ((unsigned long long)reeval << 10) |
                                    ((unsigned long long)fiber_refresh_pending(e) << 11) |
                                    ((unsigned long long)par << 12) | ((unsigned long long)e->r_mode << 13) |
@@ -2222,7 +2229,7 @@ extern "C" int rtcur_engine_iterate_cancel(rtcur_engine* e) {
   for (int i = 0; i < RT_STATE_SLOTS; ++i) e->w_epoch[i] = sn.w_epoch[i];
   e->shadow = sn.shadow; e->shadow_of = sn.shadow_of; e->shadow_epoch = sn.shadow_epoch; e->alloc_rr = sn.alloc_rr;
   e->zeta_last = sn.zeta_last;
-  e->xi_valid[0] = sn.xi_valid[0]; e->xi_valid[1] = sn.xi_valid[1];
+  for (int s = 0; s < RT_SAMPLE_SLOTS; ++s) e->xi_valid[s] = sn.xi_valid[s];
   e->snap_valid = false;
   e->npending = 0;
   e->tail_pending.valid = false;   // its tail is never enqueued

@@ -673,28 +673,47 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
         spec = (SPECULATE and src.dev is not None and src.group is None and not record_trace
                 and on_iteration is None and eng.can_speculate())
         resample = cfg.variant == "R"
+
+        def stage(sample):
+            # upload + gather into a free sample slot of the engine (on its side stream when an
+            # iteration is in flight: under that iteration's eigensolver)
+            t1 = time.perf_counter()
+            eng.set_sample(sample, views.pop(id(sample), None))
+            src.load_blocks(eng, sample)
+            timings["gather"] += time.perf_counter() - t1
+
+        def draw_next():
+            t1 = time.perf_counter()
+            smp = draw()
+            timings["sample"] += time.perf_counter() - t1
+            return smp
+
         k = 1
         zeta *= cfg.gamma
         t0 = time.perf_counter()
         if _TIMELINE is not None:
             _TIMELINE.append(("async", k, t0))
         eng.iterate_async(zeta, first=True)
+        nxt, nxt_staged = None, False   # RTCUR-R: the sample of iteration k + 1, once drawn / staged
         while True:
             # iteration k is in flight with sample `idx` at threshold `zeta`
-            nxt, staged, ahead = None, False, False
-            if resample and k < cfg.max_iters:
-                t1 = time.perf_counter()
-                nxt = draw()
-                timings["sample"] += time.perf_counter() - t1
+            ahead, launched = False, None
+            more = k < cfg.max_iters
+            if resample and more and nxt is None:
+                nxt = draw_next()
                 if prefetch:
-                    t1 = time.perf_counter()
-                    eng.set_sample(nxt, views.pop(id(nxt), None))
-                    src.load_blocks(eng, nxt)
-                    staged = True
-                    timings["gather"] += time.perf_counter() - t1
-            if spec and k < cfg.max_iters and (staged or not resample):
+                    stage(nxt)
+                    nxt_staged = True
+            if spec and more and (nxt_staged or not resample):
                 eng.iterate_async(zeta * cfg.gamma, first=False)
-                ahead = True
+                ahead, launched = True, nxt
+                nxt, nxt_staged = None, False
+                # the sample after next goes to the third slot while k and k + 1 run, so the
+                # host's staging work is off the path between k's result and k + 2's launch
+                if resample and k + 1 < cfg.max_iters:
+                    nxt = draw_next()
+                    stage(nxt)
+                    nxt_staged = True
             if _TIMELINE is not None:
                 _TIMELINE.append(("staged", k, time.perf_counter()))
             e2, x2, fl = eng.iterate_wait()
@@ -725,14 +744,15 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
                 break
             k += 1
             zeta *= cfg.gamma
-            if resample:
-                idx = nxt
-            if not ahead:
-                if resample and not staged:
-                    t1 = time.perf_counter()
-                    eng.set_sample(idx, views.pop(id(idx), None))
-                    src.load_blocks(eng, idx)
-                    timings["gather"] += time.perf_counter() - t1
+            if ahead:
+                if resample:
+                    idx = launched
+            else:
+                if resample:
+                    idx = nxt
+                    if not nxt_staged:
+                        stage(idx)
+                    nxt, nxt_staged = None, False
                 if _TIMELINE is not None:
                     _TIMELINE.append(("async", k, time.perf_counter()))
                 eng.iterate_async(zeta, first=False)
