@@ -139,6 +139,9 @@ int rtcur_engine_iterate_wait(rtcur_engine* e, double* sums, int* flags);
  * the second one runs nothing if the first met the stop rule.  iterate_wait always waits for the oldest
  * iteration in flight; after a stop, rtcur_engine_iterate_cancel drops the speculative
  * one and the engine's exportable iterate is again the one that stopped. */
+/* start of a solve on a reused engine: the iterate / sample / parity rings restart, so the
+ * solve replays the CUDA graphs an earlier solve of this geometry captured */
+int rtcur_engine_reset(rtcur_engine* e);
 int rtcur_engine_set_eps(rtcur_engine* e, double eps);
 int rtcur_engine_can_speculate(rtcur_engine* e);
 int rtcur_engine_last_stop(rtcur_engine* e);

@@ -24,7 +24,7 @@ EXPORTED = (
     "rtcur_last_error", "rtcur_version", "rtcur_launch_count", "rtcur_gather_columns", "rtcur_hard_threshold",
     "rtcur_truncated_svd", "rtcur_engine_plan", "rtcur_engine_create", "rtcur_engine_destroy", "rtcur_engine_bind",
     "rtcur_engine_absmax", "rtcur_engine_set_sample", "rtcur_engine_gather", "rtcur_engine_xblocks_offset", "rtcur_engine_iterate",
-    "rtcur_engine_iterate_async", "rtcur_engine_iterate_wait", "rtcur_engine_set_eps", "rtcur_engine_can_speculate",
+    "rtcur_engine_iterate_async", "rtcur_engine_iterate_wait", "rtcur_engine_set_eps", "rtcur_engine_reset", "rtcur_engine_can_speculate",
     "rtcur_engine_last_stop", "rtcur_engine_iterate_cancel",
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
     "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_set_graphs", "rtcur_engine_absmax_begin", "rtcur_engine_absmax_end", "rtcur_engine_profile_read",
@@ -103,6 +103,7 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_iterate_async.argtypes = [c_vp, ctypes.c_double, ctypes.c_int]
     lib.rtcur_engine_iterate_wait.argtypes = [c_vp, c_dp, c_i32p]
     lib.rtcur_engine_set_eps.argtypes = [c_vp, ctypes.c_double]
+    lib.rtcur_engine_reset.argtypes = [c_vp]
     lib.rtcur_engine_can_speculate.argtypes = [c_vp]
     lib.rtcur_engine_last_stop.argtypes = [c_vp]
     lib.rtcur_engine_iterate_cancel.argtypes = [c_vp]

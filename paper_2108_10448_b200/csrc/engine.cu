@@ -1093,6 +1093,34 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   return RT_OK;
 }
 
+// Start of a solve on a (pooled) engine: every ring -- iterate slots, sample slots, launch
+// parity -- restarts from zero, so each solve walks the same sequence of launch shapes and
+// replays the graphs the first solve of this geometry captured (a solve that started where
+// the previous one left off kept meeting new slot combinations: tens of milliseconds of
+// capture + instantiation each, for many solves).
+extern "C" int rtcur_engine_reset(rtcur_engine* e) {
+  if (!e) return fail(RT_ERR_VALUE, "null engine");
+  if (e->npending) return fail(RT_ERR_VALUE, "iteration in flight");
+  if (int st = flush_tail(e)) return st;
+  e->cur = e->prev = e->shadow = -1;
+  e->act = e->stg = -1;
+  e->alloc_rr = 0;
+  e->par = 0;
+  e->cur_par = 0;
+  e->snap_valid = false;
+  e->r_mode = false;
+  e->join_needed = false;
+  e->sampled = false;
+  e->sample_epoch = 0;
+  for (int i = 0; i < RT_STATE_SLOTS; ++i) e->w_epoch[i] = -1;
+  for (int s = 0; s < RT_SAMPLE_SLOTS; ++s) e->xi_valid[s] = false;
+  if (e->staging_on_side) {   // (a staged sample the previous solve never used)
+    CK(cudaStreamWaitEvent(e->st, e->side_ev, 0));
+    e->staging_on_side = false;
+  }
+  return RT_OK;
+}
+
 extern "C" int rtcur_engine_bind(rtcur_engine* e, const void* x_dev) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
   e->X = x_dev;   // NULL unbinds (K3 then reconstructs L only)
@@ -1638,6 +1666,10 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
       ea.lz_off[m] = (int)base;
       if (mcap && ea.full[m]) esm = std::max(esm, (int)((base + (long long)sm * (mcap + 1) + 2 * (mcap + 1) + 8) * 8));
     }
+  }
+  {
+    static const int lzs = [] { const char* v = getenv("RTCUR_LZ_STRIDE"); return v ? std::max(1, atoi(v)) : 8; }();
+    ea.lz_stride = lzs;
   }
   ea.tmark = e->at<long long>(P.o_dbg);
   // certified attempts take <= 15 steps at configs 0-4 (tools/eig_paths.py); a
@@ -2788,6 +2820,7 @@ extern "C" int rtcur_truncated_svd(const double* m_dev, int64_t m, int64_t p, in
   ea.lam[0] = tmp.at<double>(P.o_lam[0]);
   ea.nb[0] = P.nb[0];
   ea.full[0] = eig_pick_full((int)s, r);
+  ea.lz_stride = 8;   // (no Lanczos capacity is planned here: lz_mcap = 0)
   ea.reg_tridiag = getenv("RTCUR_EIG_REG") ? atoi(getenv("RTCUR_EIG_REG")) : 1;
   {
     const i64 s1[1] = {s};

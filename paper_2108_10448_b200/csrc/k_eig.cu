@@ -44,6 +44,7 @@ struct EigArgs {
   int full[RT_MAX_MODES];          // 1: full-storage tridiagonalisation
   long long* tmark;                // optional: per-matrix clock64 marks at phase boundaries (8 each)
   // warm start for the subspace-iteration fast path (null: full solver only)
+  int lz_stride;                       // Lanczos: Ritz extraction every lz_stride steps from max(16, 3r)
   const double* warmA[RT_MAX_MODES];   // previous iterate's A_k (d_k x r_k, column-major)
   const int* warm_rows[RT_MAX_MODES];  // current row set I_k (0-based)
   i64 warm_d[RT_MAX_MODES];
@@ -1176,7 +1177,7 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
       const bool brk = !(b > 1e-13 * knorm);   // invariant subspace: T_m is exact
       if (tid == 0) be[j] = brk ? 0.0 : b;
       if (brk && m < r) break;   // fewer than r directions: the Householder path
-      if (brk || m == mcap || (m >= first_chk && (m - first_chk) % 8 == 0)) {
+      if (brk || m == mcap || (m >= first_chk && (m - first_chk) % ea.lz_stride == 0)) {
         if (tid == 0) eig_tri_bounds(al, be, m, scal);
         __syncthreads();
         const double tn = scal[0];

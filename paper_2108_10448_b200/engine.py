@@ -270,6 +270,10 @@ class Engine:
         s = np.frombuffer(sums, dtype=np.float64).copy()
         return s[0::2], s[1::2], tuple(bool(f) for f in flags)
 
+    def reset(self):
+        """Start of a solve: restart the engine's slot rings (same graphs every solve)."""
+        nat.check(self.lib.rtcur_engine_reset(self.handle))
+
     def set_eps(self, eps: float):
         """Tolerance of the device-side stop rule (0: it never fires)."""
         nat.check(self.lib.rtcur_engine_set_eps(self.handle, float(eps)))

@@ -616,6 +616,7 @@ def _solve(src: "_Source", cfg: SolverConfig, record_trace: bool = False, on_ite
     elif phase_events:
         eng.profile(True, None)
         eng.profile_read(reset=True)
+    eng.reset()
     src.attach(eng)
     copies = _mode_copy_plan(shape, col_sizes, cfg, src)
     if copies:
