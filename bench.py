@@ -523,18 +523,25 @@ def run_b200(args):
     total_dev = sum(phase_ms.values())
     hbm_phases = {k: v for k, v in phase_ms.items() if k in alg and phase_n.get(k)}
     # The roofline goes to the HBM-bound pass with the most device time ON THE ITERATION'S
-    # STREAM.  An RTCUR-R solve stages its next sample (prep + gather) on a side stream under
-    # the eigensolver, so its events time it while it shares the GPU: it is listed in
-    # k1_rooflines but does not carry the headline.  The error pass (the one pass over every
-    # sampled block, core + fibers) keeps it when it is within 15 % of the largest.
-    on_path = {k: v for k, v in hbm_phases.items() if not (bc.variant == "R" and k == "gather")} or hbm_phases
+    # STREAM (its critical path).  An RTCUR-R solve stages its next sample (prep + gather) on a
+    # side stream under the eigensolver, so its events time it while it shares the GPU: it is
+    # listed in k1_rooflines (concurrent_with_iteration) but does not carry the headline.
+    # Likewise the error pass when the engine holds an iteration's tail back and runs it under
+    # the next iteration's eigensolver (always for RTCUR-F, for RTCUR-R while
+    # the sampled blocks are <= 48 MB; one process per GPU only -- a sharded solve runs its
+    # iterations one at a time).
+    tail_deferred = (not shard) and os.environ.get("RTCUR_SPECULATE", "1") != "0" and (
+        os.environ["RTCUR_TAIL_DEFER"] != "0" if "RTCUR_TAIL_DEFER" in os.environ
+        else (bc.variant != "R" or n_blk * (8 if bc.dtype == "f64" else 4) <= (48 << 20)))
+    off_path = {"gather"} if bc.variant == "R" else set()
+    if tail_deferred:
+        off_path.add("error")
+    on_path = {k: v for k, v in hbm_phases.items() if k not in off_path} or hbm_phases
     dom = max(on_path, key=on_path.get)
-    if "error" in on_path and on_path["error"] >= 0.85 * on_path[dom]:
-        dom = "error"
     k1_roof = {k: {"alg_bytes_per_launch": alg[k], "launch_us": 1e3 * v / phase_n[k],
                    "frac": alg[k] / (v / phase_n[k] / 1e3) / 1e9 / peak,
                    "launches_per_step": phase_n[k] / bd_steps,
-                   "concurrent_with_iteration": bool(bc.variant == "R" and k == "gather")}
+                   "concurrent_with_iteration": k in off_path}
                for k, v in hbm_phases.items()}
     for k, v in k1_roof.items():   # DRAM bytes ncu counted for the phase's kernels (committed capture)
         tr = _ncu_traffic(config, k)

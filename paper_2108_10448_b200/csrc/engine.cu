@@ -1969,8 +1969,11 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     CK(cudaEventRecord(e->st_ev, e->st));
     e->st_ev_seq = e->cur_seq;
   }
-  // W for every block column
-  return run_wcols(e, sto, e->act_slot());   // (w_epoch of the new slot is set by the caller)
+  // W for every block column (w_epoch of the new slot is set by the caller).  RTCUR-R: the
+  // next iteration evaluates this iterate on ITS sample (shadow or in place), so W on the
+  // current sample feeds only the error pass and the exports: it opens the tail instead
+  if (e->r_mode) return RT_OK;
+  return run_wcols(e, sto, e->act_slot());
 }
 
 // Device-side stop rule: the sampled relative error from the per-block sums, in the
@@ -2016,6 +2019,7 @@ static int iterate_main(rtcur_engine* e, const double* st_s, int newslot, bool r
 static int iterate_tail(rtcur_engine* e, const double* st_s, int newslot, int par) {
   const Plan& P = e->P;
   int st;
+  if (e->r_mode && (st = run_wcols(e, e->state(newslot), e->act_slot()))) return st;   // (see run_factors)
   if ((st = run_block_pass(e, st_s, e->state(newslot), e->zeta_last, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
     return st;
   k_stop_check<<<1, 32, 0, e->st>>>(e->at<double>(P.o_sums + e->roff()), P.g.nblk, e->at<double>(P.o_zeta + 32 * par),
@@ -2150,9 +2154,11 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
   const int st_slot = e->cur < 0 ? -1 : (use_shadow ? e->shadow : e->cur);
   const double* st_s = st_slot >= 0 ? e->state(st_slot) : nullptr;
   const bool reeval = st_slot >= 0 && !use_shadow && e->w_epoch[e->cur] != e->sample_epoch;
-  // an in-place re-evaluation overwrites the W the previous iteration's error pass reads,
-  // and without graphs nothing is deferred: that tail goes first, in stream order
-  if (reeval || !e->use_graphs)
+  // an in-place re-evaluation overwrites the W the previous iteration's error pass reads;
+  // in RTCUR-R mode that tail also produces the W this iteration would read when it does
+  // not have a shadow; and without graphs nothing is deferred: the tail goes first, in
+  // stream order
+  if (reeval || !e->use_graphs || (e->r_mode && !use_shadow))
     if (int st = flush_tail(e)) return st;
   if (use_shadow) e->shadow = -1;   // consumed: it is this iteration's threshold state from here on
   const int keep_prev = e->prev;
