@@ -96,6 +96,10 @@ int rtcur_engine_absmax_end(rtcur_engine* e, double* out);
  * and NULL entries unused): the gather then reads mode-k fibers as contiguous runs
  * instead of stride-prod_{m<k} d_m elements.  Ignored on sharded (slab) engines. */
 int rtcur_engine_bind_mode_copies(rtcur_engine* e, const void* const* copies);
+/* the same, built by the engine: the mode-k-fastest copy of the bound tensor into `out`
+ * (caller-allocated, size of X) on the engine's side stream; the solve's first gather and
+ * iteration do not wait for it */
+int rtcur_engine_build_mode_copy(rtcur_engine* e, int k, void* out);
 /* out = X with mode k moved to the front (then the other modes in order), i.e. for X
  * viewed as (A, d_k, B), out[i + d_k (a + A b)] = X[a + A (i + d_k b)]; dtype 0/1. */
 int rtcur_transpose_mode(const void* x, int dtype, int n, const int64_t* dims, int k, void* out, void* stream);

@@ -29,7 +29,7 @@ EXPORTED = (
     "rtcur_engine_export_blocks", "rtcur_engine_export_cur", "rtcur_engine_full_output",
     "rtcur_engine_full_scratch_bytes", "rtcur_engine_profile", "rtcur_engine_profile_phases", "rtcur_engine_set_graphs", "rtcur_engine_absmax_begin", "rtcur_engine_absmax_end", "rtcur_engine_profile_read",
     "rtcur_append_distinct", "rtcur_generate_tucker", "rtcur_tnsr_read_header", "rtcur_tnsr_load", "rtcur_tnsr_store",
-    "rtcur_scatter_outliers", "rtcur_abs_sum", "rtcur_ap_threshold", "rtcur_ap_residual", "rtcur_abs_max", "rtcur_engine_bind_mode_copies",
+    "rtcur_scatter_outliers", "rtcur_abs_sum", "rtcur_ap_threshold", "rtcur_ap_residual", "rtcur_abs_max", "rtcur_engine_bind_mode_copies", "rtcur_engine_build_mode_copy",
     "rtcur_transpose_mode", "rtcur_engine_set_shards", "rtcur_engine_shard_plan", "rtcur_engine_shard_pack",
     "rtcur_engine_shard_unpack", "rtcur_draw_distinct",
 )
@@ -104,6 +104,7 @@ def load(path: str = LIB_PATH):
     lib.rtcur_engine_iterate_wait.argtypes = [c_vp, c_dp, c_i32p]
     lib.rtcur_engine_set_eps.argtypes = [c_vp, ctypes.c_double]
     lib.rtcur_engine_reset.argtypes = [c_vp]
+    lib.rtcur_engine_build_mode_copy.argtypes = [c_vp, ctypes.c_int, c_vp]
     lib.rtcur_engine_can_speculate.argtypes = [c_vp]
     lib.rtcur_engine_last_stop.argtypes = [c_vp]
     lib.rtcur_engine_iterate_cancel.argtypes = [c_vp]

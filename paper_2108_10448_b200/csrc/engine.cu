@@ -606,6 +606,7 @@ struct GraphSeg {
 struct GraphEntry {
   std::vector<GraphSeg> segs;        // threshold ... column weights of the new iterate
   std::vector<GraphSeg> tail;        // error pass, stop rule, result copy
+  std::vector<ProfPair> prof, prof_tail;   // event-record nodes of the profiled phases (graph-owned events)
   unsigned long long nkernels = 0;   // kernel launches captured in segs (counted at every replay)
   unsigned long long nk_tail = 0;    // ... in tail
 };
@@ -640,6 +641,8 @@ struct rtcur_engine {
   cudaEvent_t st_ev;      // the running iteration's G and A are complete (the shadow's W waits for it)
   unsigned st_ev_seq;     // launch that recorded st_ev last
   cudaEvent_t main_ev;    // the running iteration's main part is enqueued up to here
+  bool mcopy_fresh;       // mode copies being built on the side stream (mcopy_ev), not yet ordered with st
+  cudaEvent_t mcopy_ev;
   bool r_mode;            // samples are re-staged between iterations (RTCUR-R): cut the graph at CUT_STATE
   unsigned cur_of_seq;    // launch that produced the latest iterate
   cudaEvent_t tl_base;    // diagnostics: recorded at a solve's first iteration (RTCUR_PROF_TIMELINE)
@@ -756,8 +759,11 @@ static void cap_cut(rtcur_engine* e, int cut, int ph) {
 
 static void prof_begin(rtcur_engine* e, int ph) {
   if (!e->prof_on || !((e->prof_mask >> ph) & 1u)) return;
-  if (e->capturing) {   // the event goes between two graph segments
-    cap_cut(e, CUT_PROF_BEGIN, ph);
+  if (e->capturing) {   // an event-record node inside the segment (events owned by the graph entry)
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreate(&ev) == cudaSuccess &&
+        cudaEventRecordWithFlags(ev, e->st, cudaEventRecordExternal) == cudaSuccess)
+      e->prof_open[ph] = ev;
     return;
   }
   cudaEvent_t ev = prof_event(e);
@@ -767,7 +773,13 @@ static void prof_begin(rtcur_engine* e, int ph) {
 static void prof_end(rtcur_engine* e, int ph) {
   if (!e->prof_on) return;
   if (e->capturing) {
-    if ((e->prof_mask >> ph) & 1u) cap_cut(e, CUT_PROF_END, ph);
+    if (!e->prof_open[ph]) return;
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreate(&ev) == cudaSuccess &&
+        cudaEventRecordWithFlags(ev, e->st, cudaEventRecordExternal) == cudaSuccess)
+      (e->cap_segs == &e->cap_entry->tail ? e->cap_entry->prof_tail : e->cap_entry->prof)
+          .push_back({ph, e->prof_open[ph], ev, false, 0u});
+    e->prof_open[ph] = nullptr;
     return;
   }
   if (!e->prof_open[ph]) return;
@@ -790,6 +802,10 @@ static int launch_tail(rtcur_engine* e, const rtcur_engine::TailRef& t, cudaStre
       e->prof_pending->push_back({sg.ph, e->prof_open[sg.ph], ev, true, t.seq});
       e->prof_open[sg.ph] = nullptr;
     }
+  }
+  for (auto p : t.ge->prof_tail) {
+    p.seq = t.seq;
+    e->prof_pending->push_back(p);
   }
   rtcur_launch_counter_add(t.ge->nk_tail);
   CK(cudaEventRecord(e->done[t.par], st));
@@ -835,6 +851,10 @@ static int launch_entry(rtcur_engine* e, GraphEntry& ge) {
       CK(cudaEventRecord(e->st_ev, e->st));
       e->st_ev_seq = e->cur_seq;
     }
+  }
+  for (auto p : ge.prof) {
+    p.seq = e->cur_seq;
+    e->prof_pending->push_back(p);
   }
   return RT_OK;
 }
@@ -1038,6 +1058,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
 
   CK(cudaEventCreateWithFlags(&e->st_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->main_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->mcopy_ev, cudaEventDisableTiming));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -1071,10 +1092,16 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
     delete e->prof_pending;
   }
   if (e->graphs) {
-    for (auto& kv : *e->graphs)
+    for (auto& kv : *e->graphs) {
       for (auto* v : {&kv.second.segs, &kv.second.tail})
         for (auto& sg : *v)
           if (sg.exec) cudaGraphExecDestroy(sg.exec);
+      for (auto* v : {&kv.second.prof, &kv.second.prof_tail})
+        for (auto& p : *v) {
+          cudaEventDestroy(p.b);
+          cudaEventDestroy(p.e);
+        }
+    }
     delete e->graphs;
   }
   if (e->cap_st) cudaStreamDestroy(e->cap_st);
@@ -1085,6 +1112,7 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   if (e->tail) cudaStreamSynchronize(e->tail), cudaStreamDestroy(e->tail);
   if (e->st_ev) cudaEventDestroy(e->st_ev);
   if (e->main_ev) cudaEventDestroy(e->main_ev);
+  if (e->mcopy_ev) cudaEventDestroy(e->mcopy_ev);
   if (e->prof_pool) {
     for (auto ev : *e->prof_pool) cudaEventDestroy(ev);
     delete e->prof_pool;
@@ -1129,7 +1157,38 @@ extern "C" int rtcur_engine_bind(rtcur_engine* e, const void* x_dev) {
 
 extern "C" int rtcur_engine_bind_mode_copies(rtcur_engine* e, const void* const* copies) {
   if (!e) return fail(RT_ERR_VALUE, "null engine");
+  if (e->mcopy_fresh) {   // copies still being built on the side stream: whatever reuses their
+    CK(cudaStreamWaitEvent(e->st, e->mcopy_ev, 0));   // memory on this stream comes after
+    e->mcopy_fresh = false;
+  }
   for (int m = 0; m < RT_MAX_MODES; ++m) e->mcopy[m] = (copies && m < e->P.g.n && m > 0) ? copies[m] : nullptr;
+  return RT_OK;
+}
+
+extern "C" int rtcur_transpose_mode(const void* x, int dtype, int n, const int64_t* dims, int k, void* out,
+                                    void* stream);
+
+// Build the mode-k-fastest copy of the bound tensor into `out` on the engine's side stream
+// and let the gathers that follow it there read mode-k fibers contiguously.  The solve's
+// first gather and iteration do not wait for it (that gather reads strided fibers once):
+// the copies (2 x 233 us at config 1) leave the solve's start-up path.
+extern "C" int rtcur_engine_build_mode_copy(rtcur_engine* e, int k, void* out) {
+  if (!e || !e->X) return fail(RT_ERR_VALUE, "no tensor bound");
+  if (k < 1 || k >= e->P.g.n || !out) return fail(RT_ERR_VALUE, "bad mode copy");
+  if (!(e->lo == 0 && e->hi == e->P.g.dim[0])) return fail(RT_ERR_VALUE, "mode copies need the whole tensor");
+  cudaStream_t st = e->use_side ? e->side : e->st;
+  if (st != e->st) {
+    CK(cudaEventRecord(e->pre_ev, e->st));        // X is complete on the solve's stream
+    CK(cudaStreamWaitEvent(st, e->pre_ev, 0));
+  }
+  int64_t dims[RT_MAX_MODES];
+  for (int m = 0; m < e->P.g.n; ++m) dims[m] = e->P.g.dim[m];
+  if (int rc = rtcur_transpose_mode(e->X, e->P.dtype, e->P.g.n, dims, k, out, st)) return rc;
+  e->mcopy[k] = out;
+  if (st != e->st) {
+    CK(cudaEventRecord(e->mcopy_ev, st));
+    e->mcopy_fresh = true;
+  }
   return RT_OK;
 }
 
@@ -1319,8 +1378,20 @@ extern "C" int rtcur_engine_gather(rtcur_engine* e) {
   IndexPtrs ip = make_ip_slot(e, slot);
   prof_begin(e, PH_GATHER);
   const bool whole = e->lo == 0 && e->hi == P.g.dim[0];
+  // mode copies still being built on the side stream: a gather staged there comes after them
+  // in stream order; on the solve's own stream the first gather of a solve reads strided
+  // fibers instead of waiting, a later one waits once
+  bool copies_ok = true;
+  if (e->mcopy_fresh && !e->staging_on_side) {
+    if (e->cur < 0 && e->npending == 0) {
+      copies_ok = false;
+    } else {
+      CK(cudaStreamWaitEvent(e->st, e->mcopy_ev, 0));
+      e->mcopy_fresh = false;
+    }
+  }
   ModeCopies mc;
-  for (int m = 0; m < RT_MAX_MODES; ++m) mc.p[m] = whole ? e->mcopy[m] : nullptr;
+  for (int m = 0; m < RT_MAX_MODES; ++m) mc.p[m] = (whole && copies_ok) ? e->mcopy[m] : nullptr;
   // contiguous fibers (mode 1 of an unsharded X, modes with a mode-k copy): warp-per-column
   // copies that also fill the intersection copies; the rest through the tile gather
   FastGather fg;
@@ -2279,6 +2350,7 @@ extern "C" int rtcur_engine_iterate_cancel(rtcur_engine* e) {
         keep.push_back(p);
         continue;
       }
+      if (!p.owned) continue;
       e->prof_pool->push_back(p.b);
       e->prof_pool->push_back(p.e);
     }

@@ -184,19 +184,18 @@ class Engine:
         let the gather read their fibers contiguously; ``modes`` empty: drop them."""
         import torch
 
+        if not modes:
+            # (the engine orders anything that reuses the copies' memory after their build)
+            nat.check(self.lib.rtcur_engine_bind_mode_copies(self.handle, (ctypes.c_void_p * self.n)()))
+            self._mode_copies = {}
+            return
+        # built on the engine's side stream: the first gather and iteration of the solve do
+        # not wait for them (rtcur_engine_build_mode_copy)
         self._mode_copies = {}
-        if modes:
-            dims = nat.i64_array(self.shape)
-            dt = 0 if flat.dtype == torch.float64 else 1
-            for k in modes:
-                out = torch.empty_like(flat)
-                nat.check(self.lib.rtcur_transpose_mode(ctypes.c_void_p(flat.data_ptr()), dt, self.n, dims, int(k),
-                                                        ctypes.c_void_p(out.data_ptr()),
-                                                        ctypes.c_void_p(self.stream.cuda_stream)))
-                self._mode_copies[int(k)] = out
-        ptrs = (ctypes.c_void_p * self.n)(*[ctypes.c_void_p(self._mode_copies[k].data_ptr())
-                                            if k in self._mode_copies else None for k in range(self.n)])
-        nat.check(self.lib.rtcur_engine_bind_mode_copies(self.handle, ptrs))
+        for k in modes:
+            out = torch.empty_like(flat)
+            nat.check(self.lib.rtcur_engine_build_mode_copy(self.handle, int(k), ctypes.c_void_p(out.data_ptr())))
+            self._mode_copies[int(k)] = out
 
     def bind(self, flat):
         """flat: contiguous CUDA tensor holding this rank's mode-1 slab."""
