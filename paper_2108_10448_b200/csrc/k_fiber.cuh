@@ -465,20 +465,28 @@ static __global__ void __launch_bounds__(256) k_fiber_areduce(FiberArgs a, int G
   const int f = blockIdx.y;
   if (f >= a.nfb) return;
   const FiberBlk& B = a.fb[f];
-  const int r = B.r, lane = threadIdx.x & 31;
+  // a warp takes 8 consecutive outputs x 4 slices of the terms: lanes 8 s + j read output
+  // o0 + j of slot s, s + 4, ... -- 64 contiguous bytes per slot (whole sectors), four
+  // partial sums per output combined by a fixed two-step shuffle tree (deterministic)
+  const int r = B.r, lane = threadIdx.x & 31, oj = lane & 7, sl = lane >> 3;
   const i64 nout = B.P * r;
-  const i64 wstride = (i64)gridDim.x * (blockDim.x >> 5);
-  for (i64 o = blockIdx.x * (i64)(blockDim.x >> 5) + (threadIdx.x >> 5); o < nout; o += wstride) {
-    const i64 p = o / r;
-    const int q = (int)(o - p * r);
-    const i64 t_lo = B.tfirst + (p / B.H) * B.ncg, t_hi = t_lo + B.ncg - 1;
-    const i64 c_lo = ap_cta_of(t_lo, a.ntiles, G), c_hi = ap_cta_of(t_hi, a.ntiles, G);
-    const i64 nterm = (c_hi - c_lo + 1) * B.cpr;
-    const double* base = a.apart + B.pbase + (c_lo - B.c0) * B.cpr * B.P * r + o;
+  const i64 wstride = (i64)gridDim.x * (blockDim.x >> 5) * 8;
+  for (i64 o0 = (blockIdx.x * (i64)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; o0 < nout; o0 += wstride) {
+    const i64 o = o0 + oj;
+    const bool on = o < nout;
+    const i64 p = on ? o / r : 0;
+    const int q = on ? (int)(o - p * r) : 0;
     double sum = 0.0;
-    for (i64 k = lane; k < nterm; k += 32) sum += base[k * B.P * r];   // slot (c, offset) = c_lo * cpr + k
-    sum = warp_sum(sum);
-    if (lane == 0) a.a_out[B.a_off + p + (i64)q * B.dA] = sum * a.siginv[B.mode][q];
+    if (on) {
+      const i64 t_lo = B.tfirst + (p / B.H) * B.ncg, t_hi = t_lo + B.ncg - 1;
+      const i64 c_lo = ap_cta_of(t_lo, a.ntiles, G), c_hi = ap_cta_of(t_hi, a.ntiles, G);
+      const i64 nterm = (c_hi - c_lo + 1) * B.cpr;
+      const double* base = a.apart + B.pbase + (c_lo - B.c0) * B.cpr * B.P * r + o;
+      for (i64 k = sl; k < nterm; k += 4) sum += base[k * B.P * r];   // slot (c, offset) = c_lo * cpr + k
+    }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 8);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+    if (on && sl == 0) a.a_out[B.a_off + p + (i64)q * B.dA] = sum * a.siginv[B.mode][q];
   }
 }
 
@@ -584,7 +592,7 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
   e = cudaGetLastError();
   if (e != cudaSuccess) return -(int)e;
   if (AP) {
-    k_fiber_areduce<<<dim3((unsigned)std::min<i64>((maxpr + 7) / 8, 1024), nin), 256, 0, st>>>(fa, grid);
+    k_fiber_areduce<<<dim3((unsigned)std::min<i64>((maxpr + 63) / 64, 1024), nin), 256, 0, st>>>(fa, grid);
     e = cudaGetLastError();
   }
   return e == cudaSuccess ? (AP ? 2 : 1) : -(int)e;   // kernels launched
