@@ -638,6 +638,8 @@ struct rtcur_engine {
   // iteration joins it before its SVD post, the first kernel that must see the stop flag.
   cudaStream_t tail;
   struct TailRef { struct GraphEntry* ge; int par; unsigned seq; bool valid; } tail_pending;
+  int tail_reserve;       // SMs the held-back tail's error pass leaves to the eigensolver it runs beside
+  cudaEvent_t svd_ev;     // recorded when an iteration's SVD post starts (after its eigensolver and the join)
   cudaEvent_t st_ev;      // the running iteration's G and A are complete (the shadow's W waits for it)
   unsigned st_ev_seq;     // launch that recorded st_ev last
   cudaEvent_t main_ev;    // the running iteration's main part is enqueued up to here
@@ -849,6 +851,7 @@ static int launch_entry(rtcur_engine* e, GraphEntry& ge) {
     } else if (sg.cut == CUT_JOIN) {
       if (e->join_needed) CK(cudaStreamWaitEvent(e->st, e->join_ev, 0));
       e->join_needed = false;
+      CK(cudaEventRecord(e->svd_ev, e->st));   // the SVD post starts (see rtcur_engine_set_sample)
     } else if (sg.cut == CUT_STATE) {
       CK(cudaEventRecord(e->st_ev, e->st));
       e->st_ev_seq = e->cur_seq;
@@ -1061,6 +1064,7 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
   CK(cudaEventCreateWithFlags(&e->st_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->main_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->mcopy_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->svd_ev, cudaEventDisableTiming));
   CK(cudaMemcpyAsync(e->ws + e->P.o_coloff, e->P.col_off, sizeof(i64) * (RT_MAX_BLOCKS + 1), cudaMemcpyHostToDevice, e->st));
   CK(cudaStreamSynchronize(e->st));
   // opt-in shared memory: kernel attributes are process-global, so raise every
@@ -1116,6 +1120,7 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
   if (e->st_ev) cudaEventDestroy(e->st_ev);
   if (e->main_ev) cudaEventDestroy(e->main_ev);
   if (e->mcopy_ev) cudaEventDestroy(e->mcopy_ev);
+  if (e->svd_ev) cudaEventDestroy(e->svd_ev);
   if (e->prof_pool) {
     for (auto ev : *e->prof_pool) cudaEventDestroy(ev);
     delete e->prof_pool;
@@ -1254,6 +1259,20 @@ extern "C" int rtcur_engine_absmax(rtcur_engine* e, double* out) {
   return rtcur_engine_absmax_end(e, out);
 }
 
+// Is an iteration's tail held back and run under the next eigensolver?  (RTCUR_TAIL_DEFER=0|1
+// overrides.)  Always for RTCUR-F; for RTCUR-R only while the sampled blocks are small --
+// there the next sample's gather already runs under the eigensolver, and at config 4 (87 MB
+// of blocks, a 116 us gather against a 72 us eigensolver) adding the error pass to it
+// stalled the join (13.9 vs 12.7 ms per solve).
+static bool tail_deferred_r(const rtcur_engine* e) {   // (for an RTCUR-R solve)
+  static const int defer_env = [] { const char* v = getenv("RTCUR_TAIL_DEFER"); return v ? atoi(v) : -1; }();
+  return defer_env >= 0 ? defer_env != 0 : e->P.g.nblk_total * e->P.esize <= ((i64)48 << 20);
+}
+static bool tail_deferred(const rtcur_engine* e) {
+  static const int defer_env = [] { const char* v = getenv("RTCUR_TAIL_DEFER"); return v ? atoi(v) : -1; }();
+  return !e->r_mode ? defer_env != 0 : tail_deferred_r(e);
+}
+
 // Issue the staging work of a prefetched sample on the side stream (see use_side)
 struct SideScope {
   rtcur_engine* e;
@@ -1274,8 +1293,13 @@ extern "C" int rtcur_engine_set_sample(rtcur_engine* e, const int64_t* const* ro
   if (e->npending > 0 && e->use_side && !e->shard && !e->staging_on_side && e->use_graphs) {
     e->staging_on_side = true;
     // eig_ev is recorded inside the running iteration (after pre_ev): waiting for it
-    // also covers every earlier reader of the slot being refilled
-    CK(cudaStreamWaitEvent(e->side, e->eig_ev, 0));
+    // also covers every earlier reader of the slot being refilled.  With a held-back tail
+    // the eigensolver's window already takes the previous iteration's error pass (config 1:
+    // 44 us of tail against a 49 us warm eigensolver; adding the 27 us of staging stalled
+    // the join by ~20 us): the staging then starts with the SVD post, whose Rayleigh-Ritz
+    // tail runs on one CTA per mode
+    static const bool late = [] { const char* v = getenv("RTCUR_STAGE_LATE"); return !(v && v[0] == '0'); }();
+    CK(cudaStreamWaitEvent(e->side, (late && e->npending > 0 && tail_deferred_r(e)) ? e->svd_ev : e->eig_ev, 0));
   }
   if (e->npending > 0 || e->cur >= 0) e->r_mode = true;   // a sample staged between iterations: RTCUR-R
   SideScope side_scope(e);
@@ -1607,6 +1631,7 @@ static int run_block_pass(rtcur_engine* e, const double* st_s, const double* st_
     fl.zeta = zeta;
     fl.zetap = a.zetap;
     for (int m = 0; m < P.g.n; ++m) fl.M[m] = a.M[m];
+    fl.reserve_sms = sums ? e->tail_reserve : 0;
     fl.partial = a.partial;
     fl.sums = a.sums;
     fl.counter = a.counter;
@@ -2093,6 +2118,14 @@ static int iterate_main(rtcur_engine* e, const double* st_s, int newslot, bool r
 static int iterate_tail(rtcur_engine* e, const double* st_s, int newslot, int par) {
   const Plan& P = e->P;
   int st;
+  // a held-back tail runs beside the next eigensolver: one CTA per mode, or a cluster of
+  // EIG_CLUSTER per mode when some short side exceeds 128 (see launch_eig)
+  e->tail_reserve = 0;
+  if (e->capturing && tail_deferred(e)) {
+    bool clus = false;
+    for (int m = 0; m < P.g.n; ++m) clus |= P.s[m] > 128 && P.s[m] <= 256;
+    e->tail_reserve = P.g.n * (clus ? EIG_CLUSTER : 1);
+  }
   if (e->r_mode && (st = run_wcols(e, e->state(newslot), e->act_slot()))) return st;   // (see run_factors)
   if ((st = run_block_pass(e, st_s, e->state(newslot), e->zeta_last, false, nullptr, nullptr, nullptr, true, PH_ERROR)))
     return st;
@@ -2101,6 +2134,7 @@ static int iterate_tail(rtcur_engine* e, const double* st_s, int newslot, int pa
   LAUNCH_CHECK();
   CK(cudaMemcpyAsync(e->h_pinned + par * RES_SLOT, e->ws + P.o_sums + e->roff(), P.res_bytes, cudaMemcpyDeviceToHost,
                      e->st));
+  e->tail_reserve = 0;
   return RT_OK;
 }
 
@@ -2279,13 +2313,7 @@ extern "C" int rtcur_engine_iterate_async(rtcur_engine* e, double zeta, int firs
     e->tail_pending.par = par;
     e->tail_pending.seq = e->cur_seq;
     e->tail_pending.valid = true;
-    // Policy (RTCUR_TAIL_DEFER=0|1 overrides): always for RTCUR-F; for RTCUR-R only while the
-    // sampled blocks are small -- there the next sample's gather already runs under the
-    // eigensolver, and at config 4 (87 MB of blocks, a 116 us gather against a 72 us
-    // eigensolver) adding the error pass to it stalled the join (13.9 vs 12.7 ms per solve)
-    static const int defer_env = [] { const char* v = getenv("RTCUR_TAIL_DEFER"); return v ? atoi(v) : -1; }();
-    const bool defer = defer_env >= 0 ? defer_env != 0
-                                      : (!e->r_mode || e->P.g.nblk_total * e->P.esize <= ((i64)48 << 20));
+    const bool defer = tail_deferred(e);
     if (!defer)
       if (int fst = flush_tail(e)) return leave(fst);
   } else {

@@ -30,6 +30,8 @@ struct FiberLaunch {
   i64 apart_cap;                   // doubles available at apart
   double* a_out;
   unsigned mask;                   // blocks to process (0: every block fiber_pass_blocks takes)
+  int reserve_sms;                 // SMs to leave to a kernel this pass runs beside (the eigensolver's CTAs):
+                                   // the grid is sized for the rest, so no CTA waits for a second wave
 };
 
 // Blocks (bit b = block b) the fiber pass handles for this geometry: fiber

@@ -71,6 +71,7 @@ struct FiberArgs {
   int nfb;        // handled blocks
   int nblk;       // all blocks (partial stride)
   int nst;
+  int reserve_sms;   // (host: grid sizing)
   int x_region;   // bytes of x per stage
   int w_region;   // bytes of W rows per stage and state
   i64 ntiles;
@@ -574,7 +575,7 @@ static int fb_launch_one(FiberArgs& fa, const FbIn* in, int nin, i64 apart_cap, 
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K, ncons + 32, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   per_sm = std::min(per_sm, FB_MAX_CTAS_PER_SM);
-  const int grid = (int)std::max<i64>(1, std::min<i64>(148LL * per_sm, t));
+  const int grid = (int)std::max<i64>(1, std::min<i64>((i64)std::max(1, 148 - fa.reserve_sms) * per_sm, t));
   i64 maxpr = 1;
   if (AP) {   // partial slots: one P x r slot per (block, CTA touching it)
     i64 pb = 0;
@@ -619,6 +620,7 @@ static int fb_launch_t(const FiberLaunch& L, unsigned mask, cudaStream_t st) {
   FiberArgs fa;
   memset(&fa, 0, sizeof(fa));
   fa.stop = L.g.stop;
+  fa.reserve_sms = L.reserve_sms;
   fa.st_s = L.st_s;
   fa.st_e = L.st_e;
   fa.zeta = L.zeta;
