@@ -143,6 +143,7 @@ struct Plan {
   i64 o_rows[RT_MAX_MODES], o_cols[RT_MAX_MODES], o_rowpos, o_colR, o_coli1, o_coloff;
   i64 o_zeta;       // device copy of the iteration's threshold (graph-captured iterations read it)
   i64 samp_delta;   // bytes from sample slot 0 (index sets, maps, compact blocks) to slot 1
+  i64 o_Kfull[RT_MAX_MODES];
   i64 o_xb, o_state, o_M[RT_MAX_MODES], o_gpart, o_K[RT_MAX_MODES], o_hv[RT_MAX_MODES], o_E[RT_MAX_MODES], o_lug[RT_MAX_MODES],
       o_lam[RT_MAX_MODES], o_Z[RT_MAX_MODES], o_hpart[RT_MAX_MODES], o_H[RT_MAX_MODES], o_Q[RT_MAX_MODES],
       o_U[RT_MAX_MODES], o_V[RT_MAX_MODES], o_sig[RT_MAX_MODES], o_siginv[RT_MAX_MODES], o_perm[RT_MAX_MODES],
@@ -507,6 +508,7 @@ static int make_plan(Plan& P, int n, const int64_t* dims, const int32_t* ranks, 
   for (int m = 0; m < n; ++m) {
     const i64 s = P.s[m];
     P.o_K[m] = take(s * (s + 1) / 2 * 8);
+    P.o_Kfull[m] = take(s > 128 ? s * s * 8 : 8);   // mirrored copy for the packed-storage Lanczos matvec
     P.o_E[m] = take(s * ranks[m] * 8);
     {
       // RTCUR_EIG_LU_GLOBAL=1 forces the global-scratch LU (tests), =0 disables it
@@ -1708,6 +1710,7 @@ static int launch_eig(const EigArgs& ea, const i64* s, int n, int esm, cudaStrea
 static int run_svd(rtcur_engine* e, const double* warm_state) {
   const Plan& P = e->P;
   const int n = P.g.n;
+  static const bool kfull_on = [] { const char* v = getenv("RTCUR_EIG_KFULL"); return !(v && v[0] == '0'); }();
   GramArgs ga;
   memset(&ga, 0, sizeof(ga));
   ga.stop = P.g.stop;
@@ -1719,6 +1722,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ga.mrows[m] = P.g.nrows[m];
     ga.M[m] = e->at<double>(P.o_M[m]);
     ga.K[m] = e->at<double>(P.o_K[m]);
+    ga.Kfull[m] = (kfull_on && P.s[m] > 128) ? e->at<double>(P.o_Kfull[m]) : nullptr;
   }
   ga.part = e->at<double>(P.o_gpart);
   ga.maxchunks = P.gram_maxchunks;
@@ -1747,6 +1751,7 @@ static int run_svd(rtcur_engine* e, const double* warm_state) {
     ea.s[m] = (int)P.s[m];
     ea.r[m] = P.g.rank[m];
     ea.K[m] = e->at<double>(P.o_K[m]);
+    ea.Kfull[m] = ga.Kfull[m];
     ea.E[m] = e->at<double>(P.o_E[m]);
     ea.lam[m] = e->at<double>(P.o_lam[m]);
     ea.nb[m] = P.nb[m];

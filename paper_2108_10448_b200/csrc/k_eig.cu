@@ -45,6 +45,7 @@ struct EigArgs {
   long long* tmark;                // optional: per-matrix clock64 marks at phase boundaries (8 each)
   // warm start for the subspace-iteration fast path (null: full solver only)
   int lz_stride;                       // Lanczos: Ritz extraction every lz_stride steps from max(16, 3r)
+  const double* Kfull[RT_MAX_MODES];   // packed storage: the mirrored s x s Gram in global memory (Lanczos matvec), or null
   const double* warmA[RT_MAX_MODES];   // previous iterate's A_k (d_k x r_k, column-major)
   const int* warm_rows[RT_MAX_MODES];  // current row set I_k (0-based)
   i64 warm_d[RT_MAX_MODES];
@@ -1094,6 +1095,18 @@ __global__ void __launch_bounds__(EIG_THREADS, 1) k_eig(EigArgs ea) {
               acc1 = fma(row[c + EIG_TPR], vj[c + EIG_TPR], acc1);
             }
             if (c < s) acc = fma(row[c], vj[c], acc);
+            acc += acc1;
+          } else if (ea.Kfull[mi]) {
+            // row i of the mirrored copy: contiguous (the packed column part is a
+            // strided walk, one sector per element)
+            const double* row = ea.Kfull[mi] + (size_t)i * s;
+            double acc1 = 0.0;
+            int c = sub;
+            for (; c + EIG_TPR < s; c += 2 * EIG_TPR) {
+              acc = fma(__ldg(row + c), vj[c], acc);
+              acc1 = fma(__ldg(row + c + EIG_TPR), vj[c + EIG_TPR], acc1);
+            }
+            if (c < s) acc = fma(__ldg(row + c), vj[c], acc);
             acc += acc1;
           } else {
             const double* row = Kg + pk(i, 0);

@@ -24,6 +24,7 @@ struct GramArgs {
   const double* M[RT_MAX_MODES];
   double* part;                     // [n][maxchunks][maxpairs][T*T]
   double* K[RT_MAX_MODES];          // packed lower s(s+1)/2
+  double* Kfull[RT_MAX_MODES];      // optional mirrored s x s copy (row-major), or null
   int maxchunks, maxpairs;
   int cl;                           // long-side chunk per CTA (split-K), multiple of GRAM_KS
 };
@@ -231,6 +232,12 @@ __global__ void __launch_bounds__(256) k_gram_reduce(GramArgs ga) {
     double acc = 0.0;
     for (int c = lane; c < nchunks; c += 32) acc += p[(i64)c * ga.maxpairs * (GRAM_T * GRAM_T)];
     acc = warp_sum(acc);
-    if (lane == 0) ga.K[k][idx] = acc;
+    if (lane == 0) {
+      ga.K[k][idx] = acc;
+      if (ga.Kfull[k]) {   // the mirrored s x s copy (row-contiguous matvecs of the Lanczos path)
+        ga.Kfull[k][(i64)i * s + j] = acc;
+        ga.Kfull[k][(i64)j * s + i] = acc;
+      }
+    }
   }
 }
