@@ -262,13 +262,18 @@ def test_speculative_pipeline_matches_one_at_a_time(case):
 
 @pytest.mark.parametrize("env", [{"RTCUR_FIBER_PASS": "0"}, {"RTCUR_FIBER_CORE": "0"}, {"RTCUR_EARLY_ZETA": "0"},
                                  {"RTCUR_K3_GENERIC": "1"}, {"RTCUR_CORE_PASS": "1"}, {"RTCUR_EIG_REG": "0"},
-                                 {"RTCUR_EIG_REG": "2"}, {"RTCUR_SIDE_PREFETCH": "0"}],
+                                 {"RTCUR_EIG_REG": "2"}, {"RTCUR_SIDE_PREFETCH": "0"}, {"RTCUR_SPECULATE": "0"},
+                                 {"RTCUR_TAIL_DEFER": "0"}, {"RTCUR_TAIL_DEFER": "1"}, {"RTCUR_SHADOW": "0"},
+                                 {"RTCUR_STAGE_LATE": "0"}, {"RTCUR_EIG_KFULL": "0"}, {"RTCUR_GRAPHS": "0"}],
                          ids=["block-pass-only", "core-on-block-pass", "late-zeta0", "generic-k3", "core-pass",
-                              "eig-smem-tridiag", "eig-reg-tridiag", "in-order-prefetch"])
+                              "eig-smem-tridiag", "eig-reg-tridiag", "in-order-prefetch", "one-at-a-time",
+                              "tail-in-order", "tail-held-back", "no-shadow", "stage-under-eig", "packed-lanczos-matvec",
+                              "no-graphs"])
 def test_engine_variants_agree(env):
     """The device-path variants (TMA fiber pass vs the block pass for every block,
     the core on either, zeta_0 scanned before or after the first draw, TMA vs
-    generic K3) solve the golden cases identically: same iteration counts and
+    generic K3, and the pipeline's switches: speculation, held-back tail, shadow
+    iterate, staging point, graphs) solve the golden cases identically: same iteration counts and
     sparse support; the error histories and the full-output residual to 1e-9
     relative (the A pass and the sums group their fixed-order additions
     differently, ~1e-16 of L, amplified by 1/e ~ 1e5 in the relative residuals)."""
