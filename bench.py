@@ -283,7 +283,7 @@ def _config_dict(bc, rows, cols, world, shard=False):
             "shape": list(bc.shape), "ranks": list(bc.ranks), "variant": bc.variant, "row_samples": list(rows),
             "col_samples": list(cols), "l2": "inputs larger than L2 (X = %.0f MB > 126 MB)" % (
                 np.prod(bc.shape) * (8 if bc.dtype == "f64" else 4) / 1e6),
-            "parallelism": (f"mode-1 slabs x{world} (NCCL all-reduce of the sampled blocks)" if shard else
+            "parallelism": (f"mode-1 slabs x{world} (one all-gather of the owned sampled entries per sample)" if shard else
                             f"replicas x{world}" if world > 1 else "single GPU")}
 
 
