@@ -691,6 +691,8 @@ struct rtcur_engine {
   bool use_graphs;
   bool capturing;
   cudaStream_t cap_st;             // private stream the iteration is captured on
+  cudaStream_t cap_st2;            // second capture stream: a parallel branch inside the iteration's graph
+  cudaEvent_t fork_ev, join2_ev;   // its fork / join (captured as graph edges)
   std::map<unsigned long long, GraphEntry>* graphs;
   GraphEntry* cap_entry;
   std::vector<GraphSeg>* cap_segs; // the list the capture appends to (cap_entry->segs or ->tail)
@@ -1036,6 +1038,12 @@ extern "C" int rtcur_engine_create(rtcur_engine** out, int n, const int64_t* dim
     delete e;
     return fail(RT_ERR_CUDA, "cudaStreamCreate");
   }
+  if (cudaStreamCreateWithFlags(&e->cap_st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->join2_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete e;
+    return fail(RT_ERR_CUDA, "cudaStreamCreate");
+  }
   cudaError_t ce = cudaMallocHost(&e->h_pinned, 4096);
   if (ce != cudaSuccess) { delete e; return fail(RT_ERR_CUDA, "cudaMallocHost"); }
   e->h_flags = reinterpret_cast<int*>(e->h_pinned + 256);
@@ -1114,6 +1122,9 @@ extern "C" int rtcur_engine_destroy(rtcur_engine* e) {
     delete e->graphs;
   }
   if (e->cap_st) cudaStreamDestroy(e->cap_st);
+  if (e->cap_st2) cudaStreamDestroy(e->cap_st2);
+  if (e->fork_ev) cudaEventDestroy(e->fork_ev);
+  if (e->join2_ev) cudaEventDestroy(e->join2_ev);
   if (e->side) cudaStreamSynchronize(e->side), cudaStreamDestroy(e->side);
   if (e->pre_ev) cudaEventDestroy(e->pre_ev);
   if (e->side_ev) cudaEventDestroy(e->side_ev);
@@ -1928,6 +1939,17 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
   const int n = g.n;
   IndexPtrs ip = make_ip(e);
   double* sto = e->state(dst);
+  // The A pass (fiber blocks -> A_k) and the G pass (core -> G) are independent: in a
+  // captured iteration they are two branches of the graph (fork here, join before the
+  // column weights), so their launch ramps and reduction tails overlap
+  // (RTCUR_AG_FORK=0: one after the other).
+  static const bool ag_fork = [] { const char* v = getenv("RTCUR_AG_FORK"); return !(v && v[0] == '0'); }();
+  const bool forked = ag_fork && e->capturing && e->cap_st2 != nullptr;
+  cudaStream_t st_main = e->st;
+  if (forked) {
+    CK(cudaEventRecord(e->fork_ev, st_main));
+    CK(cudaStreamWaitEvent(e->cap_st2, e->fork_ev, 0));
+  }
   prof_begin(e, PH_APASS);
   // A_k = C_k V_k S_k^+: the fiber pass for its blocks (all of them in the usual case),
   // the block-pass A pass when some fiber block is outside its envelope
@@ -1993,6 +2015,7 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     rtcur_launch_counter_add((unsigned long long)fst);
   }
   prof_end(e, PH_APASS);
+  if (forked) e->st = e->cap_st2;   // the G pass's branch
   prof_begin(e, PH_GPASS);
   // G = clean_core x_1 U_1^T x_2 ... x_n U_n^T
   GPassArgs gp;
@@ -2066,6 +2089,11 @@ static int run_factors(rtcur_engine* e, const double* st_s, double zeta, int dst
     }
   }
   prof_end(e, PH_GPASS);
+  if (forked) {   // join
+    CK(cudaEventRecord(e->join2_ev, e->cap_st2));
+    e->st = st_main;
+    CK(cudaStreamWaitEvent(st_main, e->join2_ev, 0));
+  }
   // G and A of the new iterate are complete: the side stream may evaluate it on the next sample
   if (e->capturing) {
     if (e->r_mode) cap_cut(e, CUT_STATE, 0);
