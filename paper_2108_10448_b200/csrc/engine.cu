@@ -1875,11 +1875,22 @@ static int run_wcols(rtcur_engine* e, double* sto, int sample_slot) {
   // large cores: separable chain (r_m FMAs per output); small ones stay in the
   // single k_wcols launch (launch overhead dominates there)
   const bool chain = g.n >= 2 && g.blk[0].Q * (g.gsize / g.rank[0]) > (i64)2000000;
+  // the core's chain and the fiber blocks' kernel are independent: two branches of the graph
+  // in a captured iteration (RTCUR_W_FORK=0: in order)
+  static const bool w_fork = [] { const char* v = getenv("RTCUR_W_FORK"); return !(v && v[0] == '0'); }();
+  const bool forked = chain && w_fork && e->capturing && e->cap_st2 != nullptr && e->st != e->cap_st2;
+  cudaStream_t st_main = e->st;
   if (chain) {
     const int* rows[RT_MAX_MODES];
     i64 Pm[RT_MAX_MODES];
     for (int m = 0; m < g.n; ++m) { rows[m] = ip.rows[m]; Pm[m] = g.nrows[m]; }
+    if (forked) {
+      CK(cudaEventRecord(e->fork_ev, st_main));
+      CK(cudaStreamWaitEvent(e->cap_st2, e->fork_ev, 0));
+      e->st = e->cap_st2;
+    }
     int st = run_wchain(e, sto, rows, Pm, sto + g.blk[0].w_off);
+    e->st = st_main;
     if (st) return st;
   }
   i64 qf = 1;
@@ -1928,6 +1939,10 @@ static int run_wcols(rtcur_engine* e, double* sto, int sample_slot) {
                (double*)nullptr, rpt, chain ? 1 : 0);
   }
   LAUNCH_CHECK();
+  if (forked) {   // join the core chain's branch
+    CK(cudaEventRecord(e->join2_ev, e->cap_st2));
+    CK(cudaStreamWaitEvent(st_main, e->join2_ev, 0));
+  }
   prof_end(e, PH_WCOLS);
   return RT_OK;
 }
