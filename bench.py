@@ -177,6 +177,7 @@ def _fp64_fmas(bc, rows, cols):
     return {
         "error": n_core * (2 * rk[0] + 2) + sum(f * (2 * r + 2) for f, r in zip(fib, rk)),
         "apass": sum(f * 2 * r for f, r in zip(fib, rk)),
+        "factors": sum(f * 2 * r for f, r in zip(fib, rk)) + n_core * 2 * rk[0],
         "threshold": sum(i * r for i, r in zip(inter, rk)),
     }
 
@@ -425,6 +426,17 @@ def _per_config(configs, local: int, peak: float, steps: int = 3):
                 if tr:
                     fr[ph]["traffic"] = tr["bytes_per_launch"]
                     fr[ph]["traffic_frac"] = tr["bytes_per_launch"] / (us * 1e-6) / 1e9 / peak
+        if "apass" in fr and "gpass" in fr and os.environ.get("RTCUR_AG_FORK", "1") != "0":
+            # parallel branches of the iteration's graph: one phase, both passes' bytes over
+            # the longer interval (see run_b200)
+            a_, g_ = fr.pop("apass"), fr.pop("gpass")
+            us = max(a_["launch_us"], g_["launch_us"])
+            b = a_["alg_bytes_per_launch"] + g_["alg_bytes_per_launch"]
+            fr["factors"] = {"frac": b / (us * 1e-6) / 1e9 / peak, "launch_us": us, "alg_bytes_per_launch": b,
+                             "share": max(a_["share"], g_["share"]), "phases": ["apass", "gpass"]}
+            if "traffic" in a_ and "traffic" in g_:
+                fr["factors"]["traffic"] = a_["traffic"] + g_["traffic"]
+                fr["factors"]["traffic_frac"] = fr["factors"]["traffic"] / (us * 1e-6) / 1e9 / peak
         shares = {k: round(v / total_dev, 4) for k, v in sorted(dm.items(), key=lambda kv: -kv[1]) if dn.get(k)}
         phases = {"absmax": {"ms_per_step": dm["absmax"], "launches_per_step": dn["absmax"]}} if dn.get("absmax") \
             else {}
@@ -534,6 +546,17 @@ def run_b200(args):
     torch.cuda.synchronize()
     total_dev = sum(phase_ms.values())
     hbm_phases = {k: v for k, v in phase_ms.items() if k in alg and phase_n.get(k)}
+    # The A pass (+ reduce) and the G pass (+ mode products) are two parallel branches of the
+    # iteration's graph: their event intervals start at the same fork and
+    # overlap, so they are one phase here -- "factors": both passes' bytes over the longer of
+    # the two intervals.
+    merged = {}
+    if (os.environ.get("RTCUR_AG_FORK", "1") != "0" and os.environ.get("RTCUR_GRAPHS", "1") != "0"
+            and "apass" in hbm_phases and "gpass" in hbm_phases):
+        merged["factors"] = ("apass", "gpass")
+        alg["factors"] = alg["apass"] + alg["gpass"]
+        phase_n["factors"] = max(phase_n["apass"], phase_n["gpass"])
+        hbm_phases["factors"] = max(hbm_phases.pop("apass"), hbm_phases.pop("gpass"))
     # The roofline goes to the HBM-bound pass with the most device time ON THE ITERATION'S
     # STREAM (its critical path).  An RTCUR-R solve stages its next sample (prep + gather) on a
     # side stream under the eigensolver, so its events time it while it shares the GPU: it is
@@ -557,6 +580,10 @@ def run_b200(args):
                for k, v in hbm_phases.items()}
     for k, v in k1_roof.items():   # DRAM bytes ncu counted for the phase's kernels (committed capture)
         tr = _ncu_traffic(config, k)
+        if k in merged:
+            parts = [_ncu_traffic(config, m) for m in merged[k]]
+            tr = {"bytes_per_launch": sum(p_["bytes_per_launch"] for p_ in parts)} if all(parts) else None
+            v["phases"] = list(merged[k])
         if tr:
             v["traffic"] = tr["bytes_per_launch"]
             v["traffic_frac"] = tr["bytes_per_launch"] / (v["launch_us"] * 1e-6) / 1e9 / peak
@@ -565,7 +592,7 @@ def run_b200(args):
               for k, v in sorted(phase_ms.items(), key=lambda kv: -kv[1]) if phase_n.get(k)}
 
     # ---------------- device-resident timed region (only the dominant HBM phase carries CUDA events)
-    solver_mod.PROFILE_PHASES = (dom,)
+    solver_mod.PROFILE_PHASES = merged.get(dom, (dom,))
     res = None
     clocks.wait_ready()
     solve(x_dev)   # untimed: the engine's per-iteration CUDA graphs for this profiling setting exist now
@@ -587,8 +614,8 @@ def run_b200(args):
         iters += res.iterations
         conv &= res.converged
         if solver_mod.PROFILE:
-            dom_ms += res.timings["device_ms"][dom]
-            dom_n += res.timings["device_launches"][dom]
+            dom_ms += max(res.timings["device_ms"][m] for m in merged.get(dom, (dom,)))
+            dom_n += max(res.timings["device_launches"][m] for m in merged.get(dom, (dom,)))
     ev1.record()
     res_dev = res
     torch.cuda.synchronize()
@@ -659,14 +686,20 @@ def run_b200(args):
     achieved = alg[dom] / (per_launch_ms / 1e3) / 1e9
     kname = {"threshold": "k_fiber_pass (threshold over X(I_k, J_k))", "error": "k_fiber_pass (error: core + fibers)",
              "gather": "k_gather_fibers + k_gather", "apass": "k_fiber_pass (A pass) + k_fiber_areduce",
+             "factors": "k_fiber_pass (A pass) + k_fiber_areduce || k_block_pass (G pass) + k_modeprod (parallel branches)",
              "gpass": "k_block_pass (G pass)"}[dom]
     traffic = _ncu_traffic(config, dom)
+    if dom in merged:
+        parts = [_ncu_traffic(config, m) for m in merged[dom]]
+        traffic = ({"bytes_per_launch": sum(p_["bytes_per_launch"] for p_ in parts),
+                    "source": "; ".join(p_["source"] for p_ in parts)} if all(parts) else None)
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic.get("bytes_per_launch") if traffic else None,
             "traffic_source": traffic.get("source") if traffic else None,
             "alg_bytes_per_launch": alg[dom], "launch_us": 1e3 * per_launch_ms, "launches_timed": dom_n,
             "peak_source": peak_src,
-            "share_of_device_time": phases[dom]["share"] if dom in phases else None}
+            "share_of_device_time": (max(phases[m]["share"] for m in merged[dom] if m in phases) if dom in merged
+                                     else phases[dom]["share"] if dom in phases else None)}
     if roof["traffic"]:   # the DRAM bytes ncu counted for this phase, over the same launch time
         roof["traffic_achieved"] = roof["traffic"] / (per_launch_ms / 1e3) / 1e9
         roof["traffic_frac"] = roof["traffic_achieved"] / peak
